@@ -1,0 +1,246 @@
+/*
+ * focus_b200.h -- C ABI of the B200-native Focus ingest/query hot path.
+ *
+ * The drop-in boundary: plain pointers and sizes, no torch
+ * types.  Every entry point names the reference (`focusidx`,
+ * /root/reference/pkg/src/focusidx) interface it replaces.  A caller binds
+ * this with ctypes exactly like the package in
+ * paper_1801_03493_b200/ does.
+ *
+ * Ownership: the library owns all device state behind the opaque handles;
+ * callers own every input/output buffer.  Pointers are HOST pointers unless a
+ * function says otherwise (the *_device variants take device pointers that
+ * must live on the handle's device).
+ *
+ * Threading: one fx_stream per video stream, single writer
+ * (clustering.py:87 "one engine per stream; inserts are strictly
+ * sequential").  Different handles may be driven from different host threads
+ * and devices.  A built fx_index is immutable and safe for concurrent
+ * fx_lookup; an fx_session (like QuerySession._gt_cache, query.py:44) is not.
+ *
+ * Errors: every function returns an fx_status; the codes map 1:1 onto the
+ * reference exception classes (errors.py).  fx_last_error() gives a message.
+ */
+#ifndef FOCUS_B200_H
+#define FOCUS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes <-> focusidx.errors (errors.py:4-95). */
+typedef enum {
+    FX_OK = 0,
+    FX_E_USAGE = 1,                  /* UsageError            errors.py:8-9   */
+    FX_E_DATA = 2,                   /* DataError             errors.py:12-13 */
+    FX_E_UNKNOWN_PROFILE = 10,       /* UnknownProfile        errors.py:18-19 */
+    FX_E_K_OUT_OF_RANGE = 11,        /* KOutOfRange           errors.py:22-23 */
+    FX_E_NON_POSITIVE_M = 12,        /* NonPositiveM          errors.py:26-27 */
+    FX_E_MISSING_TRUE_CLASS = 20,    /* MissingTrueClass      errors.py:32-33 */
+    FX_E_DIMENSION_MISMATCH = 30,    /* DimensionMismatch     errors.py:42-43 */
+    FX_E_SIGNATURE_LENGTH = 31,      /* SignatureLengthMismatch errors.py:46-47 */
+    FX_E_DUPLICATE_CLUSTER_ID = 40,  /* DuplicateClusterId    errors.py:52-53 */
+    FX_E_KX_TOO_LARGE = 50,          /* KxTooLarge            errors.py:66-67 */
+    FX_E_UNKNOWN_CLASS = 51,         /* UnknownClass          errors.py:70-71 */
+    FX_E_NON_MONOTONE_SCHEDULE = 52, /* NonMonotoneSchedule   errors.py:74-75 */
+    FX_E_MISSING_OBJECT = 60,        /* KeyError: objects[rep] absent (query.py:58) */
+    FX_E_CUDA = 90,                  /* CUDA runtime / launch failure */
+    FX_E_OOM = 91,                   /* device allocation failed */
+    FX_E_INTERNAL = 99
+} fx_status;
+
+/* Feature element type accepted by fx_ingest (DetectedObject.feature,
+ * core.py:37-50; the reference upcasts to float64 everywhere). */
+enum { FX_F32 = 0, FX_F64 = 1 };
+
+/* Class encoding on the wire: 0..V-1 real classes, V = OTHER_CLASS
+ * (core.py:18, 24-34). */
+
+/* ------------------------------------------------------------------------ */
+/* Stream engine: replaces ingest.ingest_stream's loop + ClusterEngine       */
+/* (ingest.py:50-96, clustering.py:86-160).                                  */
+/* ------------------------------------------------------------------------ */
+
+typedef struct fx_stream fx_stream;
+
+typedef struct {
+    int32_t dim;       /* header.dim: feature dimension D               */
+    int32_t sig_dim;   /* header.sig_dim: pixel signature length S      */
+    int32_t vocab;     /* header.vocab: V                               */
+    int32_t k;         /* cfg.k: classes indexed per object             */
+    double t;          /* cfg.t: L2 join threshold T (inclusive)        */
+    int64_t m;         /* cfg.m: cap on live clusters                   */
+    double pixel_eps;  /* ingest pixel_eps (negative disables)          */
+    int32_t feat_type; /* FX_F32 or FX_F64                              */
+    int32_t device;    /* CUDA device ordinal                           */
+    int32_t batch;     /* objects per clustering batch, 0 = auto        */
+    int32_t reserved;
+} fx_stream_config;
+
+/* Device rank model (the synthetic "cheap CNN" top-K, classifiers.py:59-70,
+ * 110-149).  The host derives these tables from the ClassifierProfile:
+ *   thresholds[j], j = 0..k-1: smallest 53-bit uniform integer u (the
+ *     draw is u * 2^-53, first Generator.random() of
+ *     default_rng([seed, object_id, 0])) whose rank_from_uniform is >= j+2;
+ *     UINT64_MAX when unreachable.  Rank 1 below thresholds[0].
+ *   emit_map[c], c = 0..V-1: profile.map_class(c) encoded (OTHER = V).
+ *   fillers[e*k + j]: _confusion_order(..., emitted=e)[j], encoded, for every
+ *     emitted class e in 0..V.                                              */
+typedef struct {
+    int32_t ground_truth; /* kind == GROUND_TRUTH: rank is always 1 */
+    int32_t reserved;
+    uint64_t seed;        /* ingest seed (rng_seed) */
+    const uint64_t *thresholds;
+    const int32_t *emit_map;
+    const int32_t *fillers;
+} fx_rank_model;
+
+int fx_stream_create(const fx_stream_config *cfg, fx_stream **out);
+int fx_stream_destroy(fx_stream *s);
+int fx_stream_set_rank_model(fx_stream *s, const fx_rank_model *rm);
+
+/* pixel_diff over a chunk (ingest.py:37-47), continuing from the previous
+ * chunk's last object; does not consume the chunk.  out_is_dup[n]. */
+int fx_stream_dup_flags(fx_stream *s, int64_t n, const int64_t *frame_ids, const double *sigs,
+                        uint8_t *out_is_dup);
+
+/* Ingest the next chunk of n objects in stream order (object ids strictly
+ * increasing).  Either true_class (rank model; -2 = unlabeled) or topk
+ * (n x k encoded classes from an external classify_fn; rows of duplicates
+ * ignored) must be given.  feats: n x dim of cfg.feat_type; if
+ * FX_FEATS_COMPACT is set it holds only the rows of non-duplicate objects.
+ * Host pointers. */
+enum { FX_FEATS_COMPACT = 1 };
+int fx_ingest(fx_stream *s, int64_t n, const int64_t *object_ids, const int64_t *frame_ids,
+              const double *sigs, const void *feats, const int32_t *true_class,
+              const int32_t *topk, int32_t flags);
+/* Same with device pointers (inputs already resident in HBM). */
+int fx_ingest_device(fx_stream *s, int64_t n, const int64_t *object_ids, const int64_t *frame_ids,
+                     const double *sigs, const void *feats, const int32_t *true_class,
+                     const int32_t *topk, int32_t flags);
+
+/* IngestReport (ingest.py:26-34) minus the float cost fields (the host
+ * multiplies by profile.cost_units). */
+typedef struct {
+    int64_t objects_seen;
+    int64_t objects_classified;
+    int64_t clusters_emitted;
+    int64_t distance_computations;
+    int64_t gt_invocations; /* always 0 */
+    int64_t exact_rechecks; /* objects resolved by the exact float64 path */
+} fx_ingest_report;
+
+/* Seal everything, build the top-K index on the device (finalize,
+ * clustering.py:146-153 + index.build, index.py:60-72).  The stream handle
+ * stays valid for fx_stream_* queries but accepts no more objects. */
+typedef struct fx_index fx_index;
+int fx_finalize(fx_stream *s, fx_index **out, fx_ingest_report *report);
+
+/* Per-object results of the ingest (n_seen entries, stream order). */
+int fx_stream_object_results(fx_stream *s, int32_t *cluster_of, uint8_t *is_dup, int32_t *topk);
+
+/* ------------------------------------------------------------------------ */
+/* Index: TopKIndex (index.py:50-85)                                          */
+/* ------------------------------------------------------------------------ */
+
+typedef struct {
+    int64_t n_clusters;
+    int64_t dim;
+    int64_t n_members;      /* sum of cluster sizes (incl. dedup members) */
+    int64_t n_class_entries;/* sum of |class_best_rank| */
+    int64_t n_postings;     /* sum of |postings[c]| over classes */
+    int64_t vocab;
+    int64_t k;
+    int64_t has_centroids;
+} fx_index_sizes;
+
+int fx_index_sizes_get(fx_index *ix, fx_index_sizes *out);
+
+/* Copy the index out (any pointer may be NULL to skip).  Cluster ids are
+ * 0..n_clusters-1 for ingested indexes.
+ *   cluster_ids[C], centroids[C*dim] (float64), reps[C] (-1 = None),
+ *   mem_off[C+1], mem_oid[n_members], mem_fid[n_members],
+ *   cls_off[C+1], cls_id[n_class_entries] (encoded, ascending per cluster),
+ *   cls_rank[n_class_entries],
+ *   post_off[V+2] (class c in [post_off[c], post_off[c+1])),
+ *   post_cluster[n_postings] (ascending per class). */
+int fx_index_export(fx_index *ix, int64_t *cluster_ids, double *centroids, int64_t *reps,
+                    int64_t *mem_off, int64_t *mem_oid, int64_t *mem_fid, int64_t *cls_off,
+                    int32_t *cls_id, int32_t *cls_rank, int64_t *post_off, int64_t *post_cluster);
+
+/* index.build from caller-provided cluster records (index.py:60-72): the
+ * postings are built on the device.  Cluster ids may be arbitrary int64 and
+ * in any order; FX_E_DUPLICATE_CLUSTER_ID on repeats.  CSR layout as in
+ * fx_index_export.  centroids may be NULL. */
+int fx_index_build(int64_t n_clusters, int32_t vocab, int32_t k, int32_t dim, int32_t device,
+                   const int64_t *cluster_ids, const double *centroids, const int64_t *reps,
+                   const int64_t *mem_off, const int64_t *mem_oid, const int64_t *mem_fid,
+                   const int64_t *cls_off, const int32_t *cls_id, const int32_t *cls_rank,
+                   fx_index **out);
+int fx_index_destroy(fx_index *ix);
+
+/* index.lookup (index.py:75-85): cluster ids posted under class_enc with
+ * best rank <= k_x (k_x <= 0 -> K), ascending.  Two-call sizing: pass
+ * out_ids = NULL to get *out_n. */
+int fx_lookup(fx_index *ix, int32_t class_enc, int32_t k_x, int64_t *out_ids, int64_t cap,
+              int64_t *out_n);
+
+/* ------------------------------------------------------------------------ */
+/* Query session: QuerySession (query.py:36-154)                             */
+/* ------------------------------------------------------------------------ */
+
+typedef struct fx_session fx_session;
+
+/* rep_label[C] (in cluster-index order of the index): ground_truth_label of
+ * each cluster's representative (classifiers.py:161-165), or
+ *   -2 = representative object has no true class (MissingTrueClass on touch),
+ *   -3 = representative object missing from `objects` (KeyError on touch),
+ *   -4 = cluster has no representative.
+ * rep_key[C]: memo key per cluster (equal keys share one GT inference, the
+ *   session memo is keyed by representative object id, query.py:53-60);
+ *   keys are dense 0..n_keys-1.
+ * other_map[V] (may be NULL): 1 if ingest_profile.map_class(c) == OTHER. */
+int fx_session_create(fx_index *ix, const int32_t *rep_label, const int32_t *rep_key,
+                      int64_t n_keys, const uint8_t *other_map, fx_session **out);
+int fx_session_destroy(fx_session *ss);
+
+typedef struct {
+    int64_t n_frames;
+    int64_t n_objects;
+    int64_t gt_inferences;
+    int64_t clusters_examined;
+    int64_t clusters_matched;
+    int64_t error_cluster; /* cluster index that raised, or -1 */
+} fx_query_result;
+
+/* One verified query (query.py:75-114):
+ *   mode 0: plain execute_query(class_enc, k_x, range);
+ *   mode 1: keep_label path of query_other (OTHER postings, k_x = K,
+ *           keep clusters whose GT label == keep_label);
+ *   batch_step: 0 = independent query; 1 = first step of batched_query
+ *           (resets the seen set); 2 = later step (skip seen clusters).
+ * has_range/t0/t1: inclusive frame range filter.  Results stay in the
+ * session until fx_query_fetch. */
+int fx_query(fx_session *ss, int32_t class_enc, int32_t k_x, int32_t mode, int32_t keep_label,
+             int32_t batch_step, int32_t has_range, int64_t t0, int64_t t1, fx_query_result *res);
+int fx_query_fetch(fx_session *ss, int64_t *frame_ids, int64_t *object_ids);
+int64_t fx_session_gt_total(fx_session *ss);
+
+/* ------------------------------------------------------------------------ */
+/* Misc                                                                       */
+/* ------------------------------------------------------------------------ */
+
+const char *fx_last_error(void);
+int fx_version(void);
+/* Number of this library's kernels launched so far (process-wide). */
+int64_t fx_kernel_launches(void);
+/* Per-phase device time accounting of the last fx_ingest/fx_finalize on s:
+ * out[0..7] = ms spent in {dup+rank, screen, resolve, fold, seal, index, total, batches}. */
+int fx_stream_timings(fx_stream *s, double *out, int n);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FOCUS_B200_H */

@@ -1,0 +1,688 @@
+// capi.cu -- the extern "C" boundary (include/focus_b200.h).
+//
+// Host-side orchestration only: validation (raising at the same point as the
+// reference), buffer management and kernel sequencing.  All per-object and
+// per-cluster work runs in the kernels of ingest.cu / index.cu / query.cu.
+#include <algorithm>
+#include <climits>
+
+#include "fx_handles.cuh"
+
+namespace fx {
+const char *last_error();
+int64_t launches();
+void launch_dup_flags(fx_stream *s, int64_t n, const int64_t *d_fid, const double *d_sig, uint8_t *d_out);
+void launch_compact(fx_stream *s, int64_t n, int64_t obj_base, int64_t cls_base, const uint8_t *d_dup,
+                    const int64_t *d_excl, const char *feat_base, int compact);
+void launch_fnorm(fx_stream *s, int64_t c0, int64_t nc);
+void launch_rank(fx_stream *s, int64_t c0, int64_t nc, const int32_t *d_tcls, unsigned long long *d_err);
+template <typename T>
+void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end);
+void launch_final_live(fx_stream *s);
+void launch_dup_members(fx_stream *s, int64_t n, const int64_t *d_excl_all, int64_t *d_anchor);
+void launch_seal(fx_stream *s, int64_t nfeat_total, const int32_t *fmem_cls, const int32_t *fmem_cid,
+                 const int64_t *foff, unsigned long long *best_bits, double *dout, int *best_pos);
+void scan_u8_to_i64(const uint8_t *in, int64_t n, int invert, int64_t *out_excl, int64_t *d_total, cudaStream_t st);
+int64_t scan_i32_to_i64(const int32_t *in, int64_t n, int64_t *out_excl, cudaStream_t st, int64_t *scratch_total);
+void launch_member_scatter(fx_stream *s, int64_t n, const int64_t *mem_off, const int64_t *foff,
+                           const int64_t *excl_cls, int64_t *mem_oid, int64_t *mem_fid, int32_t *fmem_cls,
+                           int32_t *fmem_cid);
+void launch_reps(fx_stream *s, int64_t C, const int64_t *foff, const int *best_pos, const int32_t *fmem_cls,
+                 int64_t *reps);
+void launch_iota64(int64_t n, int64_t *out, cudaStream_t st);
+void build_index_from_stream(fx_index *ix, fx_stream *s, const int64_t *foff, const int32_t *fmem_cls,
+                             int64_t nfeat_total, cudaStream_t st);
+void build_index_from_csr(fx_index *ix, const int64_t *d_off, const int32_t *d_cls, const int32_t *d_rank,
+                          int64_t n_entries, cudaStream_t st);
+void run_query(fx_session *ss, int class_enc, int k_x, int mode, int keep_label, int batch_step, int has_range,
+               int64_t t0, int64_t t1, fx_query_result *res);
+void session_alloc_bits(fx_session *ss);
+
+__global__ void k_first_cls(int64_t n, const uint8_t *__restrict__ is_dup, unsigned long long *__restrict__ out) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n && !is_dup[i]) atomicMin(out, (unsigned long long)i);
+}
+
+// leading dups of a chunk attach to the previous chunk's last classified cluster
+__global__ void k_lead_dups(int64_t lead, const int64_t *__restrict__ ctr, const int32_t *__restrict__ live,
+                            const int32_t *__restrict__ s_cid, int32_t *__restrict__ s_size,
+                            int32_t *__restrict__ cl_size) {
+    __shared__ int found;
+    if (threadIdx.x == 0) found = 0;
+    __syncthreads();
+    const int cid = (int)ctr[C_LAST_CID];
+    const int L = (int)ctr[C_NLIVE];
+    for (int i = threadIdx.x; i < L; i += blockDim.x) {
+        int sl = live[i];
+        if (s_cid[sl] == cid) {
+            s_size[sl] += (int)lead;
+            found = 1;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && !found) cl_size[cid] += (int)lead;
+}
+
+__global__ void k_init_free(int64_t nslots, int32_t *__restrict__ free_stack) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < nslots) free_stack[i] = (int32_t)(nslots - 1 - i);
+}
+
+}  // namespace fx
+
+using namespace fx;
+
+// ---------------------------------------------------------------------------
+// handle destructors
+// ---------------------------------------------------------------------------
+
+fx_stream::~fx_stream() {
+    for (auto *b : owned_feats) delete b;
+    delete plan_host;
+    if (st) cudaStreamDestroy(st);
+}
+fx_index::~fx_index() {
+    if (owns_stream && st) cudaStreamDestroy(st);
+}
+fx_session::~fx_session() {}
+
+#define FX_GUARD(...)                                   \
+    try {                                               \
+        __VA_ARGS__;                                    \
+        return FX_OK;                                   \
+    } catch (const ::fx::Error &e_) {                   \
+        ::fx::set_error(e_.msg);                        \
+        return e_.code;                                 \
+    } catch (const std::exception &e_) {                \
+        ::fx::set_error(e_.what());                     \
+        return FX_E_INTERNAL;                           \
+    }
+
+static void set_dev(int dev) { FX_CUDA(cudaSetDevice(dev)); }
+
+template <typename T>
+static void h2d(T *dst, const T *src, int64_t n, cudaStream_t st) {
+    if (n > 0) FX_CUDA(cudaMemcpyAsync(dst, src, sizeof(T) * n, cudaMemcpyHostToDevice, st));
+}
+template <typename T>
+static void d2h(T *dst, const T *src, int64_t n, cudaStream_t st) {
+    if (n > 0 && dst) FX_CUDA(cudaMemcpyAsync(dst, src, sizeof(T) * n, cudaMemcpyDeviceToHost, st));
+}
+
+extern "C" {
+
+const char *fx_last_error(void) { return fx::last_error(); }
+int fx_version(void) { return 1; }
+int64_t fx_kernel_launches(void) { return fx::launches(); }
+
+int fx_stream_create(const fx_stream_config *cfg, fx_stream **out) {
+    FX_GUARD({
+        if (!cfg || !out) throw Error{FX_E_USAGE, "null argument"};
+        if (cfg->m < 1) throw Error{FX_E_NON_POSITIVE_M, "m must be >= 1"};
+        if (cfg->t < 0) throw Error{FX_E_DATA, "t must be non-negative"};
+        if (cfg->k < 1 || cfg->k > 255) throw Error{FX_E_K_OUT_OF_RANGE, "k outside [1, 255]"};
+        if (cfg->dim < 1 || cfg->sig_dim < 0 || cfg->vocab < 1) throw Error{FX_E_USAGE, "bad dimensions"};
+        if (cfg->feat_type != FX_F32 && cfg->feat_type != FX_F64) throw Error{FX_E_USAGE, "bad feat_type"};
+        set_dev(cfg->device);
+        fx_stream *s = new fx_stream();
+        try {
+            s->cfg = *cfg;
+            s->dev = cfg->device;
+            s->esize = cfg->feat_type == FX_F64 ? 8 : 4;
+            FX_CUDA(cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking));
+            const int D = cfg->dim;
+            int B = cfg->batch;
+            if (B <= 0) {
+                int64_t b = ((int64_t)1 << 26) / std::max<int64_t>(cfg->m, 1);
+                B = (int)std::min<int64_t>(4096, std::max<int64_t>(256, b));
+            }
+            B = std::max(64, (B / 64) * 64);
+            s->B = B;
+            const int64_t max_slots_mem = (int64_t)(48e9 / (12.0 * D));
+            int64_t live_cap = std::min<int64_t>(cfg->m, max_slots_mem);
+            s->nslots = live_cap + B + 1;
+            s->ld = std::max<int64_t>(1, live_cap + 1);
+            const int64_t ns = s->nslots;
+            s->S.reserve((size_t)ns * D);
+            s->C32.reserve((size_t)ns * D);
+            for (auto *b : {&s->s_cid, &s->s_nfeat, &s->s_size, &s->s_snapq, &s->s_seedpos, &s->s_foldpos, &s->s_pend,
+                            &s->s_odcol, &s->s_didx, &s->s_evicted, &s->live, &s->live_pos, &s->free_stack,
+                            &s->defer_free, &s->snap_slot})
+                b->reserve(ns);
+            s->s_drift.reserve(ns);
+            s->s_cn2.reserve(ns);
+            FX_CUDA(cudaMemsetAsync(s->s_cn2.p, 0, sizeof(float) * ns, s->st));
+            FX_CUDA(cudaMemsetAsync(s->s_evicted.p, 0, sizeof(int32_t) * ns, s->st));
+            s->ctr.reserve(C_COUNT);
+            FX_CUDA(cudaMemsetAsync(s->ctr.p, 0, sizeof(int64_t) * C_COUNT, s->st));
+            k_init_free<<<(unsigned)cdiv(ns, 256), 256, 0, s->st>>>(ns, s->free_stack.p);
+            FX_LAUNCHED();
+            int64_t nfree = ns;
+            FX_CUDA(cudaMemcpyAsync(s->ctr.p + C_NFREE, &nfree, sizeof(int64_t), cudaMemcpyHostToDevice, s->st));
+            s->dist.reserve((size_t)B * s->ld);
+            s->dres.reserve((size_t)B * B);
+            s->dod.reserve((size_t)B * B);
+            for (auto *b : {&s->res_col, &s->res_pos, &s->slot_of, &s->pend_rank, &s->evict_slot, &s->evict_cid,
+                            &s->pend_list})
+                b->reserve(B + 1);
+            s->dirty.reserve(2 * B + 2);
+            s->dirty_off.reserve(2 * B + 3);
+            s->prev_sig.reserve(std::max(1, cfg->sig_dim));
+            s->plan_host = new PwPlan();
+            build_pw_plan(D, s->plan_host);
+            s->plan.reserve(1);
+            FX_CUDA(cudaMemcpyAsync(s->plan.p, s->plan_host, sizeof(PwPlan), cudaMemcpyHostToDevice, s->st));
+            FX_CUDA(cudaStreamSynchronize(s->st));
+        } catch (...) {
+            delete s;
+            throw;
+        }
+        *out = s;
+    })
+}
+
+int fx_stream_destroy(fx_stream *s) {
+    FX_GUARD({
+        if (s) {
+            set_dev(s->dev);
+            cudaStreamSynchronize(s->st);
+            delete s;
+        }
+    })
+}
+
+int fx_stream_set_rank_model(fx_stream *s, const fx_rank_model *rm) {
+    FX_GUARD({
+        if (!s || !rm) throw Error{FX_E_USAGE, "null argument"};
+        set_dev(s->dev);
+        const int K = s->cfg.k, V = s->cfg.vocab;
+        s->gt = rm->ground_truth;
+        s->seed = rm->seed;
+        s->rm_thr.reserve(K);
+        s->rm_emit.reserve(V);
+        s->rm_fill.reserve((size_t)(V + 1) * K);
+        h2d(s->rm_thr.p, rm->thresholds, K, s->st);
+        h2d(s->rm_emit.p, rm->emit_map, V, s->st);
+        h2d(s->rm_fill.p, rm->fillers, (int64_t)(V + 1) * K, s->st);
+        FX_CUDA(cudaStreamSynchronize(s->st));
+        s->has_rm = true;
+    })
+}
+
+int fx_stream_dup_flags(fx_stream *s, int64_t n, const int64_t *frame_ids, const double *sigs, uint8_t *out) {
+    FX_GUARD({
+        if (!s) throw Error{FX_E_USAGE, "null stream"};
+        if (n <= 0) return FX_OK;
+        set_dev(s->dev);
+        const int S = s->cfg.sig_dim;
+        DevBuf<int64_t> f;
+        DevBuf<double> g;
+        DevBuf<uint8_t> o;
+        f.reserve(n);
+        g.reserve((size_t)n * std::max(S, 1));
+        o.reserve(n);
+        h2d(f.p, frame_ids, n, s->st);
+        h2d(g.p, sigs, n * S, s->st);
+        launch_dup_flags(s, n, f.p, g.p, o.p);
+        d2h(out, o.p, n, s->st);
+        FX_CUDA(cudaStreamSynchronize(s->st));
+    })
+}
+
+static void ingest_chunk(fx_stream *s, int64_t n, const int64_t *d_oid, const int64_t *d_fid, const double *d_sig,
+                         const char *d_feats, const int32_t *d_tcls, const int32_t *d_topk, int compact) {
+    cudaStream_t st = s->st;
+    const int K = s->cfg.k, S = s->cfg.sig_dim;
+    const int64_t n0 = s->n_seen, need = n0 + n;
+    // per-object arrays
+    s->oid.grow(need, n0, st);
+    s->fid.grow(need, n0, st);
+    s->is_dup.grow(need, n0, st);
+    s->topk.grow((size_t)need * K, (size_t)n0 * K, st);
+    s->cluster_of.grow(need, n0, st);
+    s->mrank.grow(need, n0, st);
+    s->frank.grow(need, n0, st);
+    FX_CUDA(cudaMemcpyAsync(s->oid.p + n0, d_oid, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, st));
+    FX_CUDA(cudaMemcpyAsync(s->fid.p + n0, d_fid, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, st));
+    // K0
+    launch_dup_flags(s, n, d_fid, d_sig, s->is_dup.p + n0);
+    s->has_prev = true;
+    FX_CUDA(cudaMemcpyAsync(&s->prev_fid, d_fid + (n - 1), sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    if (S > 0)
+        FX_CUDA(cudaMemcpyAsync(s->prev_sig.p, d_sig + (n - 1) * S, sizeof(double) * S, cudaMemcpyDeviceToDevice, st));
+    // classified compaction
+    DevBuf<int64_t> excl, tot;
+    excl.reserve(n + 1);
+    tot.reserve(1);
+    scan_u8_to_i64(s->is_dup.p + n0, n, 1, excl.p, tot.p, st);
+    int64_t nc = 0;
+    FX_CUDA(cudaMemcpyAsync(&nc, tot.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    DevBuf<unsigned long long> first;
+    first.reserve(1);
+    FX_CUDA(cudaMemsetAsync(first.p, 0xff, sizeof(unsigned long long), st));
+    k_first_cls<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(n, s->is_dup.p + n0, first.p);
+    FX_LAUNCHED();
+    unsigned long long h_first = 0;
+    FX_CUDA(cudaMemcpyAsync(&h_first, first.p, sizeof(h_first), cudaMemcpyDeviceToHost, st));
+    FX_CUDA(cudaStreamSynchronize(st));
+    const int64_t lead = h_first == ~0ull ? n : (int64_t)h_first;
+    const int64_t c0 = s->n_cls, cneed = c0 + nc;
+    s->cls_obj.grow(cneed, c0, st);
+    s->frow.grow(cneed, c0, st);
+    s->fnorm.grow(cneed, c0, st);
+    s->dup_run.grow(cneed, c0, st);
+    if (lead > 0 && c0 > 0) {
+        // dups at the head of the chunk follow the previous chunk's last classified object
+        k_lead_dups<<<1, 256, 0, st>>>(lead, s->ctr.p, s->live.p, s->s_cid.p, s->s_size.p, s->cl_size.p);
+        FX_LAUNCHED();
+    }
+    launch_compact(s, n, n0, c0, s->is_dup.p + n0, excl.p, d_feats, compact);
+    launch_fnorm(s, c0, nc);
+    // K1: top-K
+    if (d_topk) {
+        FX_CUDA(cudaMemcpyAsync(s->topk.p + n0 * K, d_topk, sizeof(int32_t) * n * K, cudaMemcpyDeviceToDevice, st));
+    } else {
+        if (!s->has_rm) throw Error{FX_E_USAGE, "no rank model set and no top-K given"};
+        DevBuf<unsigned long long> err;
+        err.reserve(1);
+        FX_CUDA(cudaMemsetAsync(err.p, 0xff, sizeof(unsigned long long), st));
+        // true_class indexed by global object index: shift the base pointer
+        launch_rank(s, c0, nc, d_tcls - n0, err.p);
+        unsigned long long h = 0;
+        FX_CUDA(cudaMemcpyAsync(&h, err.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+        FX_CUDA(cudaStreamSynchronize(st));
+        if (h != ~0ull) {
+            int64_t bad = 0;
+            FX_CUDA(cudaMemcpy(&bad, s->oid.p + h, sizeof(int64_t), cudaMemcpyDeviceToHost));
+            throw Error{FX_E_MISSING_TRUE_CLASS, "object " + std::to_string(bad) + " has no true class"};
+        }
+    }
+    // K2
+    if (s->cfg.feat_type == FX_F64)
+        run_batches<double>(s, c0, cneed);
+    else
+        run_batches<float>(s, c0, cneed);
+    s->n_seen = need;
+    s->n_cls = cneed;
+}
+
+static int ingest_common(fx_stream *s, int64_t n, const int64_t *object_ids, const int64_t *frame_ids,
+                         const double *sigs, const void *feats, const int32_t *true_class, const int32_t *topk,
+                         int32_t flags, bool device) {
+    FX_GUARD({
+        if (!s) throw Error{FX_E_USAGE, "null stream"};
+        if (s->finalized) throw Error{FX_E_USAGE, "stream already finalized"};
+        if (n < 0) throw Error{FX_E_USAGE, "negative n"};
+        if (n == 0) return FX_OK;
+        if (!true_class && !topk) throw Error{FX_E_USAGE, "need true_class or topk"};
+        set_dev(s->dev);
+        cudaStream_t st = s->st;
+        const int D = s->cfg.dim, S = s->cfg.sig_dim, K = s->cfg.k;
+        const bool compact = flags & FX_FEATS_COMPACT;
+        if (device) {
+            ingest_chunk(s, n, object_ids, frame_ids, sigs, (const char *)feats, true_class, topk, compact);
+        } else {
+            DevBuf<int64_t> o, f;
+            DevBuf<double> g;
+            DevBuf<int32_t> tc, tk;
+            o.reserve(n);
+            f.reserve(n);
+            g.reserve((size_t)n * std::max(S, 1));
+            h2d(o.p, object_ids, n, st);
+            h2d(f.p, frame_ids, n, st);
+            h2d(g.p, sigs, n * S, st);
+            if (true_class) {
+                tc.reserve(n);
+                h2d(tc.p, true_class, n, st);
+            }
+            if (topk) {
+                tk.reserve((size_t)n * K);
+                h2d(tk.p, topk, n * K, st);
+            }
+            // feature rows: the engine keeps its own copy until finalize (the
+            // reference retains member features until seal, clustering.py:71-83)
+            int64_t rows = n;
+            if (compact) {
+                // caller passes only non-dup rows: count them on the device first
+                DevBuf<uint8_t> dup;
+                dup.reserve(n);
+                launch_dup_flags(s, n, f.p, g.p, dup.p);
+                std::vector<uint8_t> hd(n);
+                d2h(hd.data(), dup.p, n, st);
+                FX_CUDA(cudaStreamSynchronize(st));
+                rows = 0;
+                for (int64_t i = 0; i < n; i++) rows += hd[i] ? 0 : 1;
+            }
+            auto *fb = new DevBuf<char>();
+            s->owned_feats.push_back(fb);
+            fb->reserve((size_t)rows * D * s->esize);
+            if (rows > 0)
+                FX_CUDA(cudaMemcpyAsync(fb->p, feats, (size_t)rows * D * s->esize, cudaMemcpyHostToDevice, st));
+            ingest_chunk(s, n, o.p, f.p, g.p, fb->p, true_class ? tc.p : nullptr, topk ? tk.p : nullptr, compact);
+            FX_CUDA(cudaStreamSynchronize(st));
+        }
+    })
+}
+
+int fx_ingest(fx_stream *s, int64_t n, const int64_t *object_ids, const int64_t *frame_ids, const double *sigs,
+              const void *feats, const int32_t *true_class, const int32_t *topk, int32_t flags) {
+    return ingest_common(s, n, object_ids, frame_ids, sigs, feats, true_class, topk, flags, false);
+}
+
+int fx_ingest_device(fx_stream *s, int64_t n, const int64_t *object_ids, const int64_t *frame_ids, const double *sigs,
+                     const void *feats, const int32_t *true_class, const int32_t *topk, int32_t flags) {
+    return ingest_common(s, n, object_ids, frame_ids, sigs, feats, true_class, topk, flags, true);
+}
+
+int fx_finalize(fx_stream *s, fx_index **out, fx_ingest_report *rep) {
+    FX_GUARD({
+        if (!s || !out) throw Error{FX_E_USAGE, "null argument"};
+        if (s->finalized) throw Error{FX_E_USAGE, "stream already finalized"};
+        set_dev(s->dev);
+        cudaStream_t st = s->st;
+        const int D = s->cfg.dim;
+        FX_CUDA(cudaMemcpyAsync(s->h_ctr, s->ctr.p, sizeof(int64_t) * C_COUNT, cudaMemcpyDeviceToHost, st));
+        FX_CUDA(cudaStreamSynchronize(st));
+        const int64_t C = s->h_ctr[C_NEXT_CID], n = s->n_seen, nc = s->n_cls;
+        if (C > s->cl_cap) {
+            s->fcent.grow((size_t)C * D, (size_t)s->cl_cap * D, st);
+            s->cl_nfeat.grow(C, s->cl_cap, st);
+            s->cl_size.grow(C, s->cl_cap, st);
+            s->cl_cap = C;
+        }
+        launch_final_live(s);
+        fx_index *ix = new fx_index();
+        try {
+            ix->dev = s->dev;
+            ix->st = st;
+            ix->C = C;
+            ix->D = D;
+            ix->V = s->cfg.vocab;
+            ix->K = s->cfg.k;
+            ix->n_members = n;
+            ix->has_centroids = true;
+            DevBuf<int64_t> excl_all, tot, anchor, foff;
+            excl_all.reserve(n + 1);
+            tot.reserve(1);
+            anchor.reserve(n + 1);
+            if (n > 0) {
+                scan_u8_to_i64(s->is_dup.p, n, 1, excl_all.p, tot.p, st);
+                launch_dup_members(s, n, excl_all.p, anchor.p);
+            }
+            ix->mem_off.reserve(C + 1);
+            foff.reserve(C + 1);
+            int64_t nm = scan_i32_to_i64(s->cl_size.p, C, ix->mem_off.p, st, tot.p);
+            int64_t nf = scan_i32_to_i64(s->cl_nfeat.p, C, foff.p, st, tot.p);
+            if (nm != n || nf != nc) throw Error{FX_E_INTERNAL, "member accounting mismatch"};
+            ix->mem_oid.reserve(n + 1);
+            ix->mem_fid.reserve(n + 1);
+            DevBuf<int32_t> fmem_cls, fmem_cid;
+            fmem_cls.reserve(nc + 1);
+            fmem_cid.reserve(nc + 1);
+            if (n > 0)
+                launch_member_scatter(s, n, ix->mem_off.p, foff.p, excl_all.p, ix->mem_oid.p, ix->mem_fid.p,
+                                      fmem_cls.p, fmem_cid.p);
+            // deferred seal
+            DevBuf<unsigned long long> best_bits;
+            DevBuf<double> dout;
+            DevBuf<int> best_pos;
+            best_bits.reserve(C + 1);
+            best_pos.reserve(C + 1);
+            dout.reserve(nc + 1);
+            FX_CUDA(cudaMemsetAsync(best_bits.p, 0xff, sizeof(unsigned long long) * (C + 1), st));
+            FX_CUDA(cudaMemsetAsync(best_pos.p, 0x7f, sizeof(int) * (C + 1), st));
+            launch_seal(s, nc, fmem_cls.p, fmem_cid.p, foff.p, best_bits.p, dout.p, best_pos.p);
+            ix->reps.reserve(C + 1);
+            launch_reps(s, C, foff.p, best_pos.p, fmem_cls.p, ix->reps.p);
+            ix->cluster_ids.reserve(C + 1);
+            launch_iota64(C, ix->cluster_ids.p, st);
+            std::swap(ix->centroids.p, s->fcent.p);
+            std::swap(ix->centroids.n, s->fcent.n);
+            s->cl_cap = 0;
+            build_index_from_stream(ix, s, foff.p, fmem_cls.p, nc, st);
+            FX_CUDA(cudaStreamSynchronize(st));
+        } catch (...) {
+            ix->st = nullptr;
+            delete ix;
+            throw;
+        }
+        s->finalized = true;
+        if (rep) {
+            rep->objects_seen = n;
+            rep->objects_classified = nc;
+            rep->clusters_emitted = C;
+            rep->distance_computations = s->h_ctr[C_DC];
+            rep->gt_invocations = 0;
+            rep->exact_rechecks = s->h_ctr[C_EXACT];
+        }
+        // the index shares the stream's CUDA stream; give it its own
+        FX_CUDA(cudaStreamCreateWithFlags(&ix->st, cudaStreamNonBlocking));
+        ix->owns_stream = true;
+        *out = ix;
+    })
+}
+
+int fx_stream_object_results(fx_stream *s, int32_t *cluster_of, uint8_t *is_dup, int32_t *topk) {
+    FX_GUARD({
+        if (!s) throw Error{FX_E_USAGE, "null stream"};
+        set_dev(s->dev);
+        const int64_t n = s->n_seen;
+        d2h(cluster_of, s->cluster_of.p, n, s->st);
+        d2h(is_dup, s->is_dup.p, n, s->st);
+        d2h(topk, s->topk.p, n * s->cfg.k, s->st);
+        FX_CUDA(cudaStreamSynchronize(s->st));
+    })
+}
+
+int fx_stream_timings(fx_stream *s, double *out, int n) {
+    FX_GUARD({
+        if (!s || !out) throw Error{FX_E_USAGE, "null argument"};
+        set_dev(s->dev);
+        FX_CUDA(cudaMemcpyAsync(s->h_ctr, s->ctr.p, sizeof(int64_t) * C_COUNT, cudaMemcpyDeviceToHost, s->st));
+        FX_CUDA(cudaStreamSynchronize(s->st));
+        for (int i = 0; i < n && i < C_COUNT; i++) out[i] = (double)s->h_ctr[i];
+    })
+}
+
+int fx_index_sizes_get(fx_index *ix, fx_index_sizes *o) {
+    FX_GUARD({
+        if (!ix || !o) throw Error{FX_E_USAGE, "null argument"};
+        o->n_clusters = ix->C;
+        o->dim = ix->D;
+        o->n_members = ix->n_members;
+        o->n_class_entries = ix->n_cls_entries;
+        o->n_postings = ix->n_postings;
+        o->vocab = ix->V;
+        o->k = ix->K;
+        o->has_centroids = ix->has_centroids ? 1 : 0;
+    })
+}
+
+int fx_index_export(fx_index *ix, int64_t *cluster_ids, double *centroids, int64_t *reps, int64_t *mem_off,
+                    int64_t *mem_oid, int64_t *mem_fid, int64_t *cls_off, int32_t *cls_id, int32_t *cls_rank,
+                    int64_t *post_off, int64_t *post_cluster) {
+    FX_GUARD({
+        if (!ix) throw Error{FX_E_USAGE, "null index"};
+        set_dev(ix->dev);
+        cudaStream_t st = ix->st;
+        const int64_t C = ix->C;
+        d2h(cluster_ids, ix->cluster_ids.p, C, st);
+        if (centroids && ix->has_centroids) d2h(centroids, ix->centroids.p, C * ix->D, st);
+        d2h(reps, ix->reps.p, C, st);
+        d2h(mem_off, ix->mem_off.p, C + 1, st);
+        d2h(mem_oid, ix->mem_oid.p, ix->n_members, st);
+        d2h(mem_fid, ix->mem_fid.p, ix->n_members, st);
+        d2h(cls_off, ix->cls_off.p, C + 1, st);
+        d2h(cls_id, ix->cls_id.p, ix->n_cls_entries, st);
+        d2h(cls_rank, ix->cls_rank.p, ix->n_cls_entries, st);
+        d2h(post_off, ix->post_off.p, ix->V + 2, st);
+        if (post_cluster && ix->n_postings) {
+            std::vector<int32_t> tmp(ix->n_postings);
+            std::vector<int64_t> ids(C);
+            d2h(tmp.data(), ix->post_cidx.p, ix->n_postings, st);
+            d2h(ids.data(), ix->cluster_ids.p, C, st);
+            FX_CUDA(cudaStreamSynchronize(st));
+            for (int64_t i = 0; i < ix->n_postings; i++) post_cluster[i] = ids[tmp[i]];
+        }
+        FX_CUDA(cudaStreamSynchronize(st));
+    })
+}
+
+int fx_index_build(int64_t C, int32_t vocab, int32_t k, int32_t dim, int32_t device, const int64_t *cluster_ids,
+                   const double *centroids, const int64_t *reps, const int64_t *mem_off, const int64_t *mem_oid,
+                   const int64_t *mem_fid, const int64_t *cls_off, const int32_t *cls_id, const int32_t *cls_rank,
+                   fx_index **out) {
+    FX_GUARD({
+        if (!out || C < 0) throw Error{FX_E_USAGE, "bad argument"};
+        if (k < 1 || k > 255) throw Error{FX_E_K_OUT_OF_RANGE, "k outside [1, 255]"};
+        for (int64_t i = 1; i < C; i++)
+            if (cluster_ids[i] < cluster_ids[i - 1]) throw Error{FX_E_USAGE, "cluster ids must be ascending"};
+        set_dev(device);
+        fx_index *ix = new fx_index();
+        try {
+            ix->dev = device;
+            FX_CUDA(cudaStreamCreateWithFlags(&ix->st, cudaStreamNonBlocking));
+            ix->owns_stream = true;
+            cudaStream_t st = ix->st;
+            ix->C = C;
+            ix->D = dim;
+            ix->V = vocab;
+            ix->K = k;
+            const int64_t nm = C ? mem_off[C] : 0, ne = C ? cls_off[C] : 0;
+            ix->n_members = nm;
+            ix->cluster_ids.reserve(C + 1);
+            h2d(ix->cluster_ids.p, cluster_ids, C, st);
+            ix->has_centroids = centroids != nullptr;
+            if (centroids) {
+                ix->centroids.reserve((size_t)C * dim + 1);
+                h2d(ix->centroids.p, centroids, C * dim, st);
+            }
+            ix->reps.reserve(C + 1);
+            h2d(ix->reps.p, reps, C, st);
+            ix->mem_off.reserve(C + 1);
+            h2d(ix->mem_off.p, mem_off, C + 1, st);
+            ix->mem_oid.reserve(nm + 1);
+            ix->mem_fid.reserve(nm + 1);
+            h2d(ix->mem_oid.p, mem_oid, nm, st);
+            h2d(ix->mem_fid.p, mem_fid, nm, st);
+            DevBuf<int64_t> off;
+            DevBuf<int32_t> cl, rk;
+            off.reserve(C + 1);
+            cl.reserve(ne + 1);
+            rk.reserve(ne + 1);
+            h2d(off.p, cls_off, C + 1, st);
+            h2d(cl.p, cls_id, ne, st);
+            h2d(rk.p, cls_rank, ne, st);
+            for (int64_t i = 0; i < ne; i++)
+                if (cls_id[i] < 0 || cls_id[i] > vocab || cls_rank[i] < 1 || cls_rank[i] > 255)
+                    throw Error{FX_E_DATA, "class id / rank outside the encodable range"};
+            build_index_from_csr(ix, off.p, cl.p, rk.p, ne, st);
+        } catch (...) {
+            delete ix;
+            throw;
+        }
+        *out = ix;
+    })
+}
+
+int fx_index_destroy(fx_index *ix) {
+    FX_GUARD({
+        if (ix) {
+            set_dev(ix->dev);
+            cudaStreamSynchronize(ix->st);
+            delete ix;
+        }
+    })
+}
+
+int fx_lookup(fx_index *ix, int32_t class_enc, int32_t k_x, int64_t *out_ids, int64_t cap, int64_t *out_n) {
+    FX_GUARD({
+        if (!ix || !out_n) throw Error{FX_E_USAGE, "null argument"};
+        const int kx = k_x == -1 ? (int)ix->K : k_x;  // -1 = None -> K (index.py:77-79)
+        if (kx < 1 || kx > ix->K) throw Error{FX_E_KX_TOO_LARGE, "k_x outside [1, K]"};
+        *out_n = 0;
+        if (class_enc < 0 || class_enc > ix->V) return FX_OK;  // postings.get(c, []) -> []
+        set_dev(ix->dev);
+        const int64_t a = ix->h_post_off[class_enc], b = ix->h_post_off[class_enc + 1];
+        if (b == a) return FX_OK;
+        std::vector<int32_t> cidx(b - a), rk(b - a);
+        std::vector<int64_t> ids(ix->C);
+        d2h(cidx.data(), ix->post_cidx.p + a, b - a, ix->st);
+        d2h(rk.data(), ix->post_rank.p + a, b - a, ix->st);
+        d2h(ids.data(), ix->cluster_ids.p, ix->C, ix->st);
+        FX_CUDA(cudaStreamSynchronize(ix->st));
+        int64_t m = 0;
+        for (int64_t i = 0; i < b - a; i++) {
+            if (rk[i] > kx) continue;
+            if (out_ids && m < cap) out_ids[m] = ids[cidx[i]];
+            m++;
+        }
+        *out_n = m;
+    })
+}
+
+int fx_session_create(fx_index *ix, const int32_t *rep_label, const int32_t *rep_key, int64_t n_keys,
+                      const uint8_t *other_map, fx_session **out) {
+    FX_GUARD({
+        if (!ix || !out) throw Error{FX_E_USAGE, "null argument"};
+        set_dev(ix->dev);
+        fx_session *ss = new fx_session();
+        try {
+            ss->ix = ix;
+            ss->n_keys = n_keys;
+            const int64_t C = ix->C;
+            ss->rep_label.reserve(C + 1);
+            ss->rep_key.reserve(C + 1);
+            h2d(ss->rep_label.p, rep_label, C, ix->st);
+            h2d(ss->rep_key.p, rep_key, C, ix->st);
+            ss->memo.reserve((n_keys + 4) & ~3LL);
+            FX_CUDA(cudaMemsetAsync(ss->memo.p, 0, (n_keys + 4) & ~3LL, ix->st));
+            ss->seen.reserve(C + 1);
+            FX_CUDA(cudaMemsetAsync(ss->seen.p, 0, C + 1, ix->st));
+            ss->other_map.reserve(ix->V + 1);
+            ss->has_other = other_map != nullptr;
+            if (other_map) h2d(ss->other_map.p, other_map, ix->V, ix->st);
+            else FX_CUDA(cudaMemsetAsync(ss->other_map.p, 0, ix->V + 1, ix->st));
+            session_alloc_bits(ss);
+            FX_CUDA(cudaStreamSynchronize(ix->st));
+        } catch (...) {
+            delete ss;
+            throw;
+        }
+        *out = ss;
+    })
+}
+
+int fx_session_destroy(fx_session *ss) {
+    FX_GUARD({
+        if (ss) delete ss;
+    })
+}
+
+int fx_query(fx_session *ss, int32_t class_enc, int32_t k_x, int32_t mode, int32_t keep_label, int32_t batch_step,
+             int32_t has_range, int64_t t0, int64_t t1, fx_query_result *res) {
+    FX_GUARD({
+        if (!ss || !res) throw Error{FX_E_USAGE, "null argument"};
+        fx_index *ix = ss->ix;
+        if (class_enc < 0 || class_enc > ix->V) throw Error{FX_E_UNKNOWN_CLASS, "unknown class"};
+        int kx = k_x == -1 ? (int)ix->K : k_x;
+        if (mode == 1) kx = (int)ix->K;
+        if (kx < 1 || kx > ix->K) throw Error{FX_E_KX_TOO_LARGE, "k_x outside [1, K]"};
+        set_dev(ix->dev);
+        run_query(ss, class_enc, kx, mode, keep_label, batch_step, has_range, t0, t1, res);
+    })
+}
+
+int fx_query_fetch(fx_session *ss, int64_t *frame_ids, int64_t *object_ids) {
+    FX_GUARD({
+        if (!ss) throw Error{FX_E_USAGE, "null session"};
+        set_dev(ss->ix->dev);
+        d2h(frame_ids, ss->out_f.p, ss->nf, ss->ix->st);
+        d2h(object_ids, ss->out_o.p, ss->no, ss->ix->st);
+        FX_CUDA(cudaStreamSynchronize(ss->ix->st));
+    })
+}
+
+int64_t fx_session_gt_total(fx_session *ss) { return ss ? ss->gt_total : 0; }
+
+}  // extern "C"

@@ -1,0 +1,134 @@
+// fx_handles.cuh -- layouts of the opaque C-ABI handles (device-resident state).
+#pragma once
+
+#include "fx_internal.cuh"
+
+namespace fx {
+
+// Engine counters (device int64 array `ctr`).
+enum Ctr {
+    C_NLIVE = 0,       // live clusters
+    C_NEXT_CID,        // next cluster id (= clusters created)
+    C_DC,              // distance_computations (clustering.py:117)
+    C_NFREE,           // free slot stack size
+    C_NEVICT_TOTAL,    // clusters evicted so far
+    C_EXACT,           // objects resolved through the exact float64 path
+    C_NSNAP,           // snapshot live slots of the current batch
+    C_NRES,            // residual columns of the current batch
+    C_NINSERTED,       // classified objects inserted so far
+    C_NEVICT_BATCH,    // evictions in the current batch
+    C_NDEFER,          // slots freed in the current batch (reusable next batch)
+    C_NOD,             // on-demand in-batch columns of the current batch
+    C_LAST_CID,        // cluster of the last classified object (prev_cluster)
+    C_NDIRTY,          // slots touched/evicted in the current batch
+    C_ERR,             // internal error flag
+    C_FAST,            // objects decided by the certain (screen-bounded) path
+    C_COUNT
+};
+
+struct StreamChunkRef {
+    // feature rows of classified objects are addressed through frow[cls_idx]
+};
+
+}  // namespace fx
+
+struct fx_stream {
+    fx_stream_config cfg{};
+    int dev = 0;
+    cudaStream_t st = nullptr;
+    int esize = 4;             // feature element size
+    bool finalized = false;
+
+    // rank model
+    bool has_rm = false;
+    int gt = 0;
+    uint64_t seed = 0;
+    fx::DevBuf<uint64_t> rm_thr;
+    fx::DevBuf<int32_t> rm_emit, rm_fill;
+
+    // per-object arrays (grow)
+    int64_t n_seen = 0, n_cls = 0;
+    fx::DevBuf<int64_t> oid, fid;
+    fx::DevBuf<uint8_t> is_dup;
+    fx::DevBuf<int32_t> topk;       // [n_seen*k]
+    fx::DevBuf<int32_t> cluster_of; // [n_seen]
+    fx::DevBuf<int32_t> mrank;      // [n_seen] rank in the cluster's member list
+    fx::DevBuf<int32_t> frank;      // [n_seen] rank among featured members
+    // per-classified arrays
+    fx::DevBuf<int64_t> cls_obj;    // [n_cls] object index
+    fx::DevBuf<const char *> frow;  // [n_cls] feature row pointer
+    fx::DevBuf<float> fnorm;        // [n_cls] ||f|| (fp32, screen error term)
+    fx::DevBuf<int32_t> dup_run;    // [n_cls] dups directly following
+    std::vector<fx::DevBuf<char> *> owned_feats;  // host-ingested feature copies
+
+    // pixel-diff carry-over
+    bool has_prev = false;
+    int64_t prev_fid = 0;
+    fx::DevBuf<double> prev_sig;
+
+    // clustering engine
+    int B = 0;                 // batch size
+    int64_t nslots = 0;
+    fx::DevBuf<double> S;      // [nslots*D] exact running sums
+    fx::DevBuf<float> C32;     // [nslots*D] fp32 centroid snapshot
+    fx::DevBuf<int32_t> s_cid, s_nfeat, s_size, s_snapq, s_seedpos, s_foldpos, s_pend, s_odcol, s_didx,
+        s_evicted, live, live_pos, free_stack, defer_free;
+    fx::DevBuf<double> s_drift;
+    fx::DevBuf<float> s_cn2;   // ||c||^2 of the snapshot centroid (fp32)
+    fx::DevBuf<int64_t> ctr;
+    fx::DevBuf<int32_t> snap_slot;  // [nslots]
+    // per-batch scratch
+    fx::DevBuf<float> dist;    // [B*ld]
+    int64_t ld = 0;
+    fx::DevBuf<float> dres;    // [B*B]
+    fx::DevBuf<int32_t> res_col, res_pos;
+    fx::DevBuf<float> dod;     // [B*B] on-demand columns
+    fx::DevBuf<int32_t> slot_of, pend_rank, evict_slot, evict_cid, dirty, dirty_off, pend_list;
+    // per-cluster results (grow with clusters)
+    int64_t cl_cap = 0;
+    fx::DevBuf<double> fcent;      // [cl_cap*D] final centroids
+    fx::DevBuf<int32_t> cl_nfeat, cl_size;
+    int64_t h_ctr[fx::C_COUNT] = {0};
+
+    fx::PwPlan *plan_host = nullptr;
+    fx::DevBuf<fx::PwPlan> plan;
+
+    ~fx_stream();
+};
+
+struct fx_index {
+    int dev = 0;
+    cudaStream_t st = nullptr;
+    bool owns_stream = false;
+    int64_t C = 0, D = 0, V = 0, K = 0;
+    int64_t n_members = 0, n_cls_entries = 0, n_postings = 0;
+    bool has_centroids = false;
+    fx::DevBuf<int64_t> cluster_ids;
+    fx::DevBuf<double> centroids;
+    fx::DevBuf<int64_t> reps;      // representative object id or -1
+    fx::DevBuf<int64_t> mem_off, mem_oid, mem_fid;
+    fx::DevBuf<int64_t> cls_off;
+    fx::DevBuf<int32_t> cls_id, cls_rank;
+    fx::DevBuf<int64_t> post_off;  // [V+2]
+    fx::DevBuf<int32_t> post_cidx, post_rank;
+    std::vector<int64_t> h_post_off;
+    int64_t fmin = 0, fmax = -1, omin = 0, omax = -1;
+    ~fx_index();
+};
+
+struct fx_session {
+    fx_index *ix = nullptr;
+    int64_t n_keys = 0;
+    int64_t gt_total = 0;
+    bool has_other = false;
+    fx::DevBuf<int32_t> rep_label, rep_key;
+    fx::DevBuf<uint8_t> memo, other_map, seen;
+    fx::DevBuf<uint32_t> fbits, obits;
+    fx::DevBuf<int64_t> wprefix_f, wprefix_o;
+    fx::DevBuf<int64_t> out_f, out_o;
+    fx::DevBuf<int32_t> cand, matched;
+    fx::DevBuf<int64_t> qctr;
+    fx::DevBuf<int64_t> h_pinned_dummy;
+    int64_t nf = 0, no = 0;
+    ~fx_session();
+};

@@ -1,0 +1,1059 @@
+// ingest.cu -- K0 pixel differencing, K1a rank-model top-K, K2 clustering
+// (screen / resolve / fold), deferred seal.  SURVEY.md §2 kernel set.
+//
+// Reference semantics (clustering.py:86-160, ingest.py:50-96):
+//   * objects are processed in stream order; a classified object joins the
+//     live cluster with the smallest float64 distance (first minimum = smallest
+//     cluster id) iff that distance <= T, else seeds a new cluster;
+//   * after a seed, if more than M clusters are live, the live cluster with
+//     the fewest members (dedup members included; ties -> smallest id) is
+//     evicted;
+//   * centroid = float64 running sum / featured count; representative =
+//     featured member nearest the final centroid (ties -> first).
+//
+// B200 design: a batch of B classified objects is screened
+// against the batch-start snapshot of the live centroids in FP32 with a
+// rigorous error bound (k_screen); a single persistent CTA (k_resolve) then
+// walks the batch in stream order keeping the exact sequential semantics:
+// decisions that the bounds make certain cost O(L/threads) scalar work, the
+// rest are decided by exact float64 distances (numpy pairwise order) against
+// centroids materialised from the exact running sums.  k_fold then applies
+// the batch's members to the float64 sums in order and refreshes the FP32
+// snapshot.  Seal (representatives) is deferred to finalize, exactly as the
+// reference's frozen-at-eviction centroids allow.
+#include "fx_handles.cuh"
+
+namespace fx {
+
+// ---------------------------------------------------------------------------
+// K0: pixel differencing (ingest.py:37-47)
+// ---------------------------------------------------------------------------
+
+__global__ void k_dup_flags(int64_t n, int S, const int64_t *__restrict__ fid, const double *__restrict__ sig,
+                            int has_prev, int64_t prev_fid, const double *__restrict__ prev_sig, double eps,
+                            uint8_t *__restrict__ is_dup) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    uint8_t d = 0;
+    if (eps >= 0.0) {
+        const double *a = nullptr;
+        int64_t pf = 0;
+        if (i > 0) {
+            a = sig + (i - 1) * S;
+            pf = fid[i - 1];
+        } else if (has_prev) {
+            a = prev_sig;
+            pf = prev_fid;
+        }
+        if (a && fid[i] - pf <= 1) {
+            const double *b = sig + i * S;
+            double sum = pw_sum_seq(S, [&](int k) { return fabs(dsub(a[k], b[k])); });
+            d = ddiv(sum, (double)S) <= eps;
+        }
+    }
+    is_dup[i] = d;
+}
+
+// classified-object bookkeeping: cls index, feature row pointer, dup runs
+__global__ void k_compact_cls(int64_t n, int64_t obj_base, int64_t cls_base, const uint8_t *__restrict__ is_dup,
+                              const int64_t *__restrict__ excl, const char *feat_base, int64_t row_bytes,
+                              int compact, int64_t *__restrict__ cls_obj, const char **__restrict__ frow,
+                              int32_t *__restrict__ dup_run) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    int64_t e = excl[i];
+    if (!is_dup[i]) {
+        int64_t c = cls_base + e;
+        cls_obj[c] = obj_base + i;
+        frow[c] = feat_base + (compact ? e : i) * row_bytes;
+        dup_run[c] = 0;
+    }
+}
+
+__global__ void k_dup_runs(int64_t n, int64_t cls_base, const uint8_t *__restrict__ is_dup,
+                           const int64_t *__restrict__ excl, int32_t *__restrict__ dup_run) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (is_dup[i]) atomicAdd(&dup_run[cls_base + excl[i] - 1], 1);
+}
+
+template <typename T>
+__global__ void k_fnorm(int64_t c0, int64_t nc, int D, const char *const *__restrict__ frow, float *__restrict__ fnorm) {
+    int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    int lane = threadIdx.x & 31;
+    if (w >= nc) return;
+    const T *f = (const T *)frow[c0 + w];
+    float acc = 0.f;
+    for (int k = lane; k < D; k += 32) {
+        float x = (float)f[k];
+        acc = fmaf(x, x, acc);
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) fnorm[c0 + w] = sqrtf(acc);
+}
+
+// ---------------------------------------------------------------------------
+// K1a: rank-model top-K (classifiers.py:126-149, core.py:60-61)
+// ---------------------------------------------------------------------------
+
+__global__ void k_rank_topk(int64_t c0, int64_t nc, const int64_t *__restrict__ cls_obj, const int64_t *__restrict__ oid,
+                            const int32_t *__restrict__ tcls, int K, int V, int gt, uint64_t seed,
+                            const uint64_t *__restrict__ thr, const int32_t *__restrict__ emit,
+                            const int32_t *__restrict__ fill, int32_t *__restrict__ topk,
+                            unsigned long long *__restrict__ err_obj) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= nc) return;
+    int64_t obj = cls_obj[c0 + i];
+    int c = tcls[obj];
+    if (c < 0 || c >= V) {  // unlabeled: MissingTrueClass raised lazily (classifiers.py:128-129)
+        atomicMin(err_obj, (unsigned long long)obj);
+        return;
+    }
+    int rank = 1;
+    if (!gt) {
+        uint64_t u = first_u53(seed, (uint64_t)oid[obj], 0ull);
+        for (int j = 0; j < K; j++) rank += thr[j] <= u;
+    }
+    int e = emit[c];
+    const int32_t *row = fill + (int64_t)e * K;
+    int32_t *out = topk + obj * K;
+    for (int j = 0; j < K; j++) out[j] = j < rank - 1 ? row[j] : (j == rank - 1 ? e : row[j - 1]);
+}
+
+// ---------------------------------------------------------------------------
+// K2a: FP32 distance screen (direct difference, two-level accumulation)
+//   dist[a][b] = sqrt(sum_k (A_a[k] - B_b[k])^2), 64x64 tile / CTA.
+// Error model: relative error of the squared distance is
+// <= (3 + 64 + ceil(D/64) + 2) * 2^-24 -- every 64 dims the running partial is
+// flushed into the total.
+// ---------------------------------------------------------------------------
+
+constexpr int SC_T = 64, SC_K = 32;
+
+template <typename TA, typename FB>
+__global__ void __launch_bounds__(256) k_screen(int nA, int64_t a0, const char *const *__restrict__ frow, int D,
+                                               const int64_t *__restrict__ nB_dev, int nB_max, FB fb,
+                                               float *__restrict__ out, int64_t ld) {
+    const int nB = nB_dev ? (int)*nB_dev : nB_max;
+    const int tb = blockIdx.x * SC_T, ta = blockIdx.y * SC_T;
+    if (tb >= nB || ta >= nA) return;
+    __shared__ float As[SC_K][SC_T + 1];
+    __shared__ float Bs[SC_K][SC_T + 1];
+    const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+    float acc[4][4], tot[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; i++)
+#pragma unroll
+        for (int j = 0; j < 4; j++) acc[i][j] = tot[i][j] = 0.f;
+    for (int k0 = 0; k0 < D; k0 += SC_K) {
+#pragma unroll
+        for (int e = 0; e < 8; e++) {
+            int idx = tid + e * 256, r = idx >> 5, k = idx & 31;
+            float va = 0.f, vb = 0.f;
+            if (ta + r < nA && k0 + k < D) va = (float)((const TA *)frow[a0 + ta + r])[k0 + k];
+            if (tb + r < nB && k0 + k < D) vb = fb(tb + r, k0 + k);
+            As[k][r] = va;
+            Bs[k][r] = vb;
+        }
+        __syncthreads();
+#pragma unroll 8
+        for (int k = 0; k < SC_K; k++) {
+            float ra[4], rb[4];
+#pragma unroll
+            for (int i = 0; i < 4; i++) ra[i] = As[k][ty * 4 + i];
+#pragma unroll
+            for (int j = 0; j < 4; j++) rb[j] = Bs[k][tx * 4 + j];
+#pragma unroll
+            for (int i = 0; i < 4; i++)
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    float d = ra[i] - rb[j];
+                    acc[i][j] = fmaf(d, d, acc[i][j]);
+                }
+        }
+        __syncthreads();
+        if (((k0 / SC_K) & 1) || k0 + SC_K >= D) {
+#pragma unroll
+            for (int i = 0; i < 4; i++)
+#pragma unroll
+                for (int j = 0; j < 4; j++) {
+                    tot[i][j] += acc[i][j];
+                    acc[i][j] = 0.f;
+                }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < 4; i++) {
+        int a = ta + ty * 4 + i;
+        if (a >= nA) continue;
+#pragma unroll
+        for (int j = 0; j < 4; j++) {
+            int b = tb + tx * 4 + j;
+            if (b < nB) out[(int64_t)a * ld + b] = sqrtf(tot[i][j]);
+        }
+    }
+}
+
+struct FromSnapshot {  // B rows = FP32 snapshot centroids of the live slots
+    const float *C32;
+    const int32_t *snap;
+    int D;
+    __device__ float operator()(int b, int k) const { return C32[(int64_t)snap[b] * D + k]; }
+};
+template <typename T>
+struct FromResidual {  // B rows = features of the batch's residual objects
+    const char *const *frow;
+    int64_t a0;
+    const int32_t *res_pos;
+    __device__ float operator()(int b, int k) const { return (float)((const T *)frow[a0 + res_pos[b]])[k]; }
+};
+
+// residual detection: object has no snapshot centroid whose screen lower
+// bound is <= T -> it will very likely seed; its column of object-object
+// distances is precomputed for the objects after it.
+__global__ void k_residuals(int nA, const int64_t *__restrict__ ctr, const float *__restrict__ dist, int64_t ld,
+                            const float *__restrict__ cn2, const int32_t *__restrict__ snap,
+                            const float *__restrict__ fnorm, int64_t a0, float rel, float absc, double T,
+                            int32_t *__restrict__ res_col, int32_t *__restrict__ res_pos, int64_t *__restrict__ nres) {
+    int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (w >= nA) return;
+    const int nsnap = (int)ctr[C_NSNAP];
+    const float fn = fnorm[a0 + w];
+    float mn = INFINITY;
+    for (int q = lane; q < nsnap; q += 32) {
+        float d = dist[(int64_t)w * ld + q];
+        float e = rel * d + absc * (sqrtf(cn2[snap[q]]) * 1.00001f + fn);
+        mn = fminf(mn, d - e);
+    }
+    mn = warp_min(mn);
+    if (lane == 0) {
+        if ((double)mn > T) {
+            int col = (int)atomicAdd((unsigned long long *)nres, 1ull);
+            res_pos[col] = w;
+            res_col[w] = col;
+        } else {
+            res_col[w] = -1;
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K2b: sequential resolve (one CTA per stream per batch)
+// ---------------------------------------------------------------------------
+
+struct ResolveArgs {
+    int B;
+    int64_t c0;
+    int D;
+    double T;
+    int64_t M;
+    float rel, absc;
+    const float *dist;
+    int64_t ld;
+    const float *dres;
+    int64_t ldr;
+    const int32_t *res_col;
+    float *dod;
+    const char *const *frow;
+    const float *fnorm;
+    const int32_t *dup_run;
+    const int64_t *cls_obj;
+    double *S;
+    int32_t *s_cid, *s_nfeat, *s_size, *s_snapq, *s_seedpos, *s_foldpos, *s_pend, *s_odcol, *s_evicted, *s_didx;
+    double *s_drift;
+    float *s_cn2;
+    int32_t *live, *live_pos, *free_stack, *defer_free, *snap_slot;
+    int64_t *ctr;
+    int32_t *slot_of, *pend_rank, *evict_slot, *evict_cid, *dirty, *dirty_off, *pend_list;
+    int32_t *cluster_of, *mrank, *frank;
+    const PwPlan *plan;
+};
+
+constexpr int RS_THREADS = 512;
+constexpr int RS_WARPS = RS_THREADS / 32;
+constexpr int RS_MAXCAND = 512;
+
+struct Cand {
+    float ub;
+    int ubi;
+    float lb1;
+    int lb1i;
+    float lb2;
+};
+
+__device__ __forceinline__ void cand_merge(Cand &a, const Cand &b) {
+    if (b.ub < a.ub || (b.ub == a.ub && b.ubi < a.ubi)) {
+        a.ub = b.ub;
+        a.ubi = b.ubi;
+    }
+    // two smallest LBs
+    if (b.lb1 < a.lb1) {
+        a.lb2 = fminf(a.lb1, b.lb2);
+        a.lb1 = b.lb1;
+        a.lb1i = b.lb1i;
+    } else {
+        a.lb2 = fminf(a.lb2, b.lb1);
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ void slot_bounds(const ResolveArgs &A, int b, float fn, int slot, float &lb, float &ub, float &d) {
+    int q = A.s_snapq[slot];
+    float cn;
+    if (q >= 0) {
+        d = A.dist[(int64_t)b * A.ld + q];
+        cn = sqrtf(A.s_cn2[slot]) * 1.00001f;
+    } else {
+        int s = A.s_seedpos[slot];
+        int col = A.res_col[s];
+        d = col >= 0 ? A.dres[(int64_t)b * A.ldr + col] : A.dod[(int64_t)A.s_odcol[slot] * A.B + b];
+        cn = A.fnorm[A.c0 + s];
+    }
+    float e = A.rel * d + A.absc * (cn + fn) + 1e-30f;
+    float dr = (float)A.s_drift[slot] * 1.00001f;
+    lb = d - e - dr;
+    ub = d + e + dr;
+    // round the bounds outward (fp32 arithmetic of the bound itself)
+    lb = lb - fabsf(lb) * 1e-6f - 1e-30f;
+    ub = ub + fabsf(ub) * 1e-6f + 1e-30f;
+}
+
+// exact ||c_slot - f_b|| for the current centroid of `slot`: first fold the
+// slot's in-batch members in [foldpos, b) into its float64 sum (stream
+// order), then evaluate sqrt(pairwise_sum(((S/n) - f)^2)) in numpy's order.
+template <typename T>
+__device__ double exact_dist(const ResolveArgs &A, int b, int slot, const int32_t *sh_slot_of, int *mlist,
+                             double *scratch) {
+    const int D = A.D;
+    int fp = A.s_foldpos[slot];
+    const int sp = A.s_seedpos[slot];
+    double *Sj = A.S + (int64_t)slot * D;
+    if (fp < b) {
+        __shared__ int s_nm;
+        if (threadIdx.x < 32) {
+            int base = 0;
+            for (int p0 = fp; p0 < b; p0 += 32) {
+                int p = p0 + (int)threadIdx.x;
+                bool hit = p < b && sh_slot_of[p] == slot;
+                unsigned m = __ballot_sync(0xffffffffu, hit);
+                if (hit) mlist[base + __popc(m & ((1u << threadIdx.x) - 1u))] = p;
+                base += __popc(m);
+            }
+            if (threadIdx.x == 0) s_nm = base;
+        }
+        __syncthreads();
+        const int nm = s_nm;
+        for (int k = threadIdx.x; k < D; k += blockDim.x) {
+            double s = Sj[k];
+            for (int i = 0; i < nm; i++) {
+                const int p = mlist[i];
+                double f = to_d(((const T *)A.frow[A.c0 + p])[k]);
+                s = (p == sp) ? f : dadd(s, f);
+            }
+            Sj[k] = s;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) A.s_foldpos[slot] = b;
+    }
+    const double n = (double)A.s_nfeat[slot];
+    const T *f = (const T *)A.frow[A.c0 + b];
+    __syncthreads();
+    auto term = [&](int k) {
+        double x = dsub(ddiv(Sj[k], n), to_d(f[k]));
+        return dmul(x, x);
+    };
+    const PwPlan &P = *A.plan;
+    double *chain = scratch, *node = scratch + P.n_chains;
+    for (int c = threadIdx.x; c < P.n_chains; c += blockDim.x) {
+        int lo = 0, hi = P.n_leaves - 1;
+        while (lo < hi) {
+            int mid = (lo + hi + 1) >> 1;
+            if (P.leaf_chain0[mid] <= c) lo = mid; else hi = mid - 1;
+        }
+        const int s = P.leaf_start[lo], len = P.leaf_len[lo];
+        double r;
+        if (len < 8) {
+            r = 0.0;
+            for (int i = 0; i < len; i++) r = dadd(r, term(s + i));
+        } else {
+            const int a = c - P.leaf_chain0[lo], end = len - (len % 8);
+            r = term(s + a);
+            for (int i = 8 + a; i < end; i += 8) r = dadd(r, term(s + i));
+        }
+        chain[c] = r;
+    }
+    __syncthreads();
+    for (int L = threadIdx.x; L < P.n_leaves; L += blockDim.x) {
+        const int c0 = P.leaf_chain0[L], s = P.leaf_start[L], len = P.leaf_len[L];
+        double res;
+        if (len < 8) {
+            res = chain[c0];
+        } else {
+            const double *r = chain + c0;
+            res = dadd(dadd(dadd(r[0], r[1]), dadd(r[2], r[3])), dadd(dadd(r[4], r[5]), dadd(r[6], r[7])));
+            for (int i = len - (len % 8); i < len; i++) res = dadd(res, term(s + i));
+        }
+        node[L] = res;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int o = 0; o < P.n_ops; o++) node[P.n_leaves + o] = dadd(node[P.op_left[o]], node[P.op_right[o]]);
+    }
+    __syncthreads();
+    double tot = P.n_ops ? node[P.n_leaves + P.n_ops - 1] : node[0];
+    __syncthreads();
+    return __dsqrt_rn(dadd(0.0, tot));
+}
+
+template <typename T>
+__global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    int32_t *sh_slot_of = (int32_t *)smem_raw;                            // [B]
+    int *mlist = (int *)(smem_raw + A.B * 4);                            // [B]
+    double *scratch = (double *)(smem_raw + ((A.B * 8 + 15) & ~15));     // pairwise scratch
+    __shared__ Cand red[RS_WARPS];
+    __shared__ int cand_list[RS_MAXCAND];
+    __shared__ int n_cand;
+    __shared__ int s_L, s_nfree, s_ndefer, s_nevict, s_nod, s_ndirty;
+    __shared__ long long s_dc, s_exact, s_fast, s_next_cid, s_inserted, s_victim_key;
+    __shared__ int s_decision_slot, s_seed, s_need_exact, s_need_evict, s_need_od;
+    __shared__ double s_best_d;
+    __shared__ int s_best_slot;
+    __shared__ float s_ub_used;
+
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int B = A.B;
+    int64_t *ctr = A.ctr;
+
+    // ---- batch prologue: recycle last batch's freed slots, reset snapshot fields
+    if (tid == 0) {
+        s_L = (int)ctr[C_NLIVE];
+        s_nfree = (int)ctr[C_NFREE];
+        int nd = (int)ctr[C_NDEFER];
+        for (int i = 0; i < nd; i++) A.free_stack[s_nfree++] = A.defer_free[i];
+        s_ndefer = 0;
+        s_nevict = 0;
+        s_nod = 0;
+        s_ndirty = 0;
+        s_dc = ctr[C_DC];
+        s_exact = ctr[C_EXACT];
+        s_fast = ctr[C_FAST];
+        s_next_cid = ctr[C_NEXT_CID];
+        s_inserted = ctr[C_NINSERTED];
+    }
+    __syncthreads();
+    const int nsnap = (int)ctr[C_NSNAP];
+    for (int q = tid; q < nsnap; q += blockDim.x) {
+        int sl = A.snap_slot[q];
+        A.s_snapq[sl] = q;
+        A.s_seedpos[sl] = -1;
+        A.s_foldpos[sl] = 0;
+        A.s_pend[sl] = 0;
+        A.s_odcol[sl] = -1;
+        A.s_drift[sl] = 0.0;
+    }
+    for (int b = tid; b < B; b += blockDim.x) sh_slot_of[b] = -1;
+    __syncthreads();
+
+    for (int b = 0; b < B; b++) {
+        const float fn = A.fnorm[A.c0 + b];
+        const int L = s_L;
+        // ---- candidate scan
+        Cand c{INFINITY, 0x7fffffff, INFINITY, -1, INFINITY};
+        for (int i = tid; i < L; i += blockDim.x) {
+            int slot = A.live[i];
+            float lb, ub, d;
+            slot_bounds<T>(A, b, fn, slot, lb, ub, d);
+            Cand o{ub, i, lb, i, INFINITY};
+            cand_merge(c, o);
+        }
+#pragma unroll
+        for (int off = 16; off; off >>= 1) {
+            Cand o;
+            o.ub = __shfl_xor_sync(0xffffffffu, c.ub, off);
+            o.ubi = __shfl_xor_sync(0xffffffffu, c.ubi, off);
+            o.lb1 = __shfl_xor_sync(0xffffffffu, c.lb1, off);
+            o.lb1i = __shfl_xor_sync(0xffffffffu, c.lb1i, off);
+            o.lb2 = __shfl_xor_sync(0xffffffffu, c.lb2, off);
+            cand_merge(c, o);
+        }
+        if (lane == 0) red[wid] = c;
+        __syncthreads();
+        if (tid == 0) {
+            Cand r = red[0];
+            for (int w = 1; w < RS_WARPS; w++) cand_merge(r, red[w]);
+            s_dc += L;
+            s_need_exact = 0;
+            s_need_evict = 0;
+            s_need_od = -1;
+            s_seed = 0;
+            s_decision_slot = -1;
+            if (L == 0 || (double)r.lb1 > A.T) {
+                s_seed = 1;
+                s_fast++;
+            } else if (r.lb2 > r.ub) {
+                // unique possible argmin
+                int slot = A.live[r.ubi];
+                if ((double)r.ub <= A.T) {
+                    s_decision_slot = slot;
+                    s_ub_used = r.ub;
+                    s_fast++;
+                } else {
+                    s_need_exact = 1;
+                    cand_list[0] = r.ubi;
+                    n_cand = 1;
+                }
+            } else {
+                s_need_exact = 2;
+                n_cand = 0;
+                s_ub_used = r.ub;
+            }
+        }
+        __syncthreads();
+        if (s_need_exact) {
+            if (s_need_exact == 2) {
+                const float U = s_ub_used;
+                for (int i = tid; i < L; i += blockDim.x) {
+                    int slot = A.live[i];
+                    float lb, ub, d;
+                    slot_bounds<T>(A, b, fn, slot, lb, ub, d);
+                    if (lb <= U) {
+                        int p = atomicAdd(&n_cand, 1);
+                        if (p < RS_MAXCAND) cand_list[p] = i;
+                    }
+                }
+                __syncthreads();
+            }
+            const int nc = n_cand < RS_MAXCAND ? n_cand : RS_MAXCAND;
+            if (tid == 0) {
+                s_best_d = INFINITY;
+                s_best_slot = -1;
+                s_exact++;
+            }
+            __syncthreads();
+            for (int ci = 0; ci < nc; ci++) {
+                int slot = A.live[cand_list[ci]];
+                float lb, ub, d;
+                slot_bounds<T>(A, b, fn, slot, lb, ub, d);
+                if ((double)lb > s_best_d) continue;  // cannot win (uniform across threads)
+                double dx = exact_dist<T>(A, b, slot, sh_slot_of, mlist, scratch);
+                if (tid == 0) {
+                    int cid = A.s_cid[slot];
+                    if (dx < s_best_d || (dx == s_best_d && cid < A.s_cid[s_best_slot])) {
+                        s_best_d = dx;
+                        s_best_slot = slot;
+                    }
+                }
+                __syncthreads();
+            }
+            if (tid == 0) {
+                if (n_cand > RS_MAXCAND) ctr[C_ERR] = 1;  // candidate overflow (never expected)
+                if (s_best_slot >= 0 && s_best_d <= A.T) {
+                    s_decision_slot = s_best_slot;
+                    s_ub_used = (float)s_best_d * 1.000001f + 1e-30f;
+                } else {
+                    s_seed = 1;
+                }
+            }
+            __syncthreads();
+        }
+        // ---- apply (thread 0)
+        if (tid == 0) {
+            const int64_t c = A.c0 + b;
+            const int64_t obj = A.cls_obj[c];
+            int slot, rank_m, rank_f;
+            if (!s_seed) {
+                slot = s_decision_slot;
+                rank_m = A.s_size[slot];
+                rank_f = A.s_nfeat[slot];
+                int nf = rank_f + 1;
+                A.s_nfeat[slot] = nf;
+                A.s_size[slot] = rank_m + 1;
+                double ub = (double)s_ub_used;
+                double dr = A.s_drift[slot];
+                double cn = sqrt((double)A.s_cn2[slot]) + (double)A.fnorm[c];
+                A.s_drift[slot] = dr + ub / nf + 8.0 * 1.1102230246251565e-16 * (cn + dr + ub) + 1e-300;
+            } else {
+                slot = A.free_stack[--s_nfree];
+                int cid = (int)s_next_cid++;
+                A.s_cid[slot] = cid;
+                A.s_nfeat[slot] = 1;
+                A.s_size[slot] = 1;
+                A.s_drift[slot] = 0.0;
+                A.s_cn2[slot] = A.fnorm[c] * A.fnorm[c];
+                A.s_snapq[slot] = -1;
+                A.s_seedpos[slot] = b;
+                A.s_foldpos[slot] = b;
+                A.s_pend[slot] = 0;
+                A.s_evicted[slot] = 0;
+                A.s_odcol[slot] = -1;
+                A.live[s_L] = slot;
+                A.live_pos[slot] = s_L;
+                s_L++;
+                rank_m = 0;
+                rank_f = 0;
+                if (A.res_col[b] < 0) {
+                    A.s_odcol[slot] = s_nod++;
+                    s_need_od = slot;
+                }
+                if (s_L > A.M) s_need_evict = 1;
+            }
+            if (A.s_pend[slot] == 0) {  // first member this batch -> dirty
+                A.s_didx[slot] = s_ndirty;
+                A.dirty[s_ndirty++] = slot;
+            }
+            A.pend_rank[b] = A.s_pend[slot]++;
+            sh_slot_of[b] = slot;
+            A.slot_of[b] = slot;
+            const int cid = A.s_cid[slot];
+            A.cluster_of[obj] = cid;
+            A.mrank[obj] = rank_m;
+            A.frank[obj] = rank_f;
+            s_inserted++;
+        }
+        __syncthreads();
+        // ---- on-demand in-batch column for a seed without a residual column
+        if (s_need_od >= 0) {
+            const int slot = s_need_od;
+            const int col = A.s_odcol[slot];
+            const T *fs = (const T *)A.frow[A.c0 + b];
+            for (int bb = b + 1 + tid; bb < B; bb += blockDim.x) {
+                const T *fo = (const T *)A.frow[A.c0 + bb];
+                float tot = 0.f, acc = 0.f;
+                for (int k = 0; k < A.D; k++) {
+                    float d = (float)fo[k] - (float)fs[k];
+                    acc = fmaf(d, d, acc);
+                    if ((k & 63) == 63) {
+                        tot += acc;
+                        acc = 0.f;
+                    }
+                }
+                tot += acc;
+                A.dod[(int64_t)col * B + bb] = sqrtf(tot);
+            }
+        }
+        // ---- eviction (clustering.py:139-144)
+        if (s_need_evict) {
+            if (tid == 0) s_victim_key = 0x7fffffffffffffffLL;
+            __syncthreads();
+            long long best = 0x7fffffffffffffffLL;
+            for (int i = tid; i < s_L; i += blockDim.x) {
+                int slot = A.live[i];
+                long long key = ((long long)A.s_size[slot] << 32) | (long long)(unsigned)A.s_cid[slot];
+                best = key < best ? key : best;
+            }
+            best = warp_min(best);
+            if (lane == 0) atomicMin((unsigned long long *)&s_victim_key, (unsigned long long)best);
+            __syncthreads();
+            {
+                const int vcid = (int)(s_victim_key & 0xffffffffLL);
+                for (int i = tid; i < s_L; i += blockDim.x)
+                    if (A.s_cid[A.live[i]] == vcid) s_best_slot = A.live[i];
+            }
+            __syncthreads();
+            if (tid == 0) {
+                const int vcid = (int)(s_victim_key & 0xffffffffLL);
+                const int vslot = s_best_slot;
+                int pos = A.live_pos[vslot];
+                int last = A.live[s_L - 1];
+                A.live[pos] = last;
+                A.live_pos[last] = pos;
+                s_L--;
+                A.s_evicted[vslot] = 1;
+                A.evict_slot[s_nevict] = vslot;
+                A.evict_cid[s_nevict] = vcid;
+                s_nevict++;
+                A.defer_free[s_ndefer++] = vslot;
+                if (A.s_pend[vslot] == 0) {  // untouched this batch but needs its final centroid
+                    A.s_didx[vslot] = s_ndirty;
+                    A.dirty[s_ndirty++] = vslot;
+                }
+            }
+        }
+        // ---- dedup members following this object attach to its cluster
+        if (tid == 0) {
+            int slot = sh_slot_of[b];
+            A.s_size[slot] += A.dup_run[A.c0 + b];
+        }
+        __syncthreads();
+    }
+
+    // ---- epilogue: pending-member CSR for k_fold, snapshot for next batch
+    __syncthreads();
+    if (tid == 0) {
+        int acc = 0;
+        for (int i = 0; i < s_ndirty; i++) {
+            A.dirty_off[i] = acc;
+            acc += A.s_pend[A.dirty[i]];
+        }
+        A.dirty_off[s_ndirty] = acc;
+    }
+    __syncthreads();
+    for (int b = tid; b < B; b += blockDim.x) {
+        const int slot = sh_slot_of[b];
+        A.pend_list[A.dirty_off[A.s_didx[slot]] + A.pend_rank[b]] = b;
+    }
+    for (int q = tid; q < s_L; q += blockDim.x) A.snap_slot[q] = A.live[q];
+    __syncthreads();
+    if (tid == 0) {
+        ctr[C_NLIVE] = s_L;
+        ctr[C_NSNAP] = s_L;
+        ctr[C_NFREE] = s_nfree;
+        ctr[C_NDEFER] = s_ndefer;
+        ctr[C_NEVICT_BATCH] = s_nevict;
+        ctr[C_NEVICT_TOTAL] += s_nevict;
+        ctr[C_NDIRTY] = s_ndirty;
+        ctr[C_NOD] = s_nod;
+        ctr[C_DC] = s_dc;
+        ctr[C_EXACT] = s_exact;
+        ctr[C_FAST] = s_fast;
+        ctr[C_NEXT_CID] = s_next_cid;
+        ctr[C_NINSERTED] = s_inserted;
+        ctr[C_LAST_CID] = A.s_cid[sh_slot_of[B - 1]];
+        ctr[C_NRES] = 0;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K2c: fold the batch's members into the float64 sums (stream order) and
+// refresh the FP32 snapshot; record final centroids of evicted clusters.
+// grid (ceil(D/256), ndirty)
+// ---------------------------------------------------------------------------
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_fold(int D, int64_t c0, const int64_t *__restrict__ ctr,
+                                              const int32_t *__restrict__ dirty, const int32_t *__restrict__ dirty_off,
+                                              const int32_t *__restrict__ pend_list, const char *const *__restrict__ frow,
+                                              double *__restrict__ S, float *__restrict__ C32,
+                                              const int32_t *__restrict__ s_nfeat, const int32_t *__restrict__ s_foldpos,
+                                              const int32_t *__restrict__ s_seedpos, const int32_t *__restrict__ s_evicted,
+                                              const int32_t *__restrict__ s_cid, const int32_t *__restrict__ s_size,
+                                              float *__restrict__ s_cn2, double *__restrict__ fcent,
+                                              int32_t *__restrict__ cl_nfeat, int32_t *__restrict__ cl_size) {
+    const int di = blockIdx.y;
+    if (di >= (int)ctr[C_NDIRTY]) return;
+    const int slot = dirty[di];
+    const int k = blockIdx.x * blockDim.x + threadIdx.x;
+    const int p0 = dirty_off[di], p1 = dirty_off[di + 1];
+    const int fp = s_foldpos[slot], sp = s_seedpos[slot];
+    const double n = (double)s_nfeat[slot];
+    float c2 = 0.f;
+    if (k < D) {
+        double s = S[(int64_t)slot * D + k];
+        for (int p = p0; p < p1; p++) {
+            int b = pend_list[p];
+            if (b < fp) continue;  // already folded by the resolve's exact path
+            double f = to_d(((const T *)frow[c0 + b])[k]);
+            s = (b == sp) ? f : dadd(s, f);
+        }
+        S[(int64_t)slot * D + k] = s;
+        double cen = ddiv(s, n);
+        float c32 = (float)cen;
+        C32[(int64_t)slot * D + k] = c32;
+        c2 = c32 * c32;
+        if (s_evicted[slot]) fcent[(int64_t)s_cid[slot] * D + k] = cen;
+    }
+    // ||c||^2 partial
+    c2 = warp_sum(c2);
+    __shared__ float red[8];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c2;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float t = 0.f;
+        for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += red[w];
+        atomicAdd(&s_cn2[slot], t);
+        if (blockIdx.x == 0 && s_evicted[slot]) {
+            cl_nfeat[s_cid[slot]] = s_nfeat[slot];
+            cl_size[s_cid[slot]] = s_size[slot];
+        }
+    }
+}
+
+__global__ void k_zero_cn2(const int64_t *__restrict__ ctr, const int32_t *__restrict__ dirty, float *__restrict__ s_cn2) {
+    int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < (int)ctr[C_NDIRTY]) s_cn2[dirty[i]] = 0.f;
+}
+
+// finalize: live clusters' final centroids and sizes
+__global__ void k_final_live(int D, const int64_t *__restrict__ ctr, const int32_t *__restrict__ live,
+                             const double *__restrict__ S, const int32_t *__restrict__ s_nfeat,
+                             const int32_t *__restrict__ s_cid, const int32_t *__restrict__ s_size,
+                             double *__restrict__ fcent, int32_t *__restrict__ cl_nfeat, int32_t *__restrict__ cl_size) {
+    const int i = blockIdx.y;
+    if (i >= (int)ctr[C_NLIVE]) return;
+    const int slot = live[i];
+    const int cid = s_cid[slot];
+    const double n = (double)s_nfeat[slot];
+    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < D; k += gridDim.x * blockDim.x)
+        fcent[(int64_t)cid * D + k] = ddiv(S[(int64_t)slot * D + k], n);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        cl_nfeat[cid] = s_nfeat[slot];
+        cl_size[cid] = s_size[slot];
+    }
+}
+
+// dups inherit the cluster of the classified object they follow; member rank
+// continues that object's rank (ingest.py:69-71, clustering.py:61-63)
+__global__ void k_dup_members(int64_t n, const uint8_t *__restrict__ is_dup, const int64_t *__restrict__ anchor_obj,
+                              int32_t *__restrict__ cluster_of, int32_t *__restrict__ mrank,
+                              int32_t *__restrict__ frank) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n || !is_dup[i]) return;
+    int64_t a = anchor_obj[i];
+    cluster_of[i] = cluster_of[a];
+    mrank[i] = mrank[a] + (int32_t)(i - a);
+    frank[i] = -1;
+}
+
+// anchor (last classified object at or before i) via the classified prefix
+__global__ void k_anchor(int64_t n, const uint8_t *__restrict__ is_dup, const int64_t *__restrict__ excl_all,
+                         const int64_t *__restrict__ cls_obj, int64_t *__restrict__ anchor) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    anchor[i] = is_dup[i] ? cls_obj[excl_all[i] - 1] : i;
+}
+
+// ---------------------------------------------------------------------------
+// Deferred seal (clustering.py:71-83): exact float64 distance of every
+// featured member to its cluster's final centroid; first minimum wins.
+// ---------------------------------------------------------------------------
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_seal_dist(int64_t nfeat_total, int D, const int32_t *__restrict__ fmem_cls,
+                                                   const int32_t *__restrict__ fmem_cid, const char *const *__restrict__ frow,
+                                                   const double *__restrict__ fcent, const PwPlan *__restrict__ plan,
+                                                   unsigned long long *__restrict__ best_bits, double *__restrict__ dout) {
+    extern __shared__ double sscratch[];
+    const int wpb = blockDim.x >> 5, w = threadIdx.x >> 5;
+    const int per = plan->n_chains + plan->n_leaves + plan->n_ops;
+    double *scr = sscratch + w * per;
+    for (int64_t m = (int64_t)blockIdx.x * wpb + w; m < nfeat_total; m += (int64_t)gridDim.x * wpb) {
+        const int cid = fmem_cid[m];
+        const T *f = (const T *)frow[fmem_cls[m]];
+        const double *c = fcent + (int64_t)cid * D;
+        double s = pw_sum_warp(*plan, [&](int k) {
+            double x = dsub(c[k], to_d(f[k]));
+            return dmul(x, x);
+        }, scr);
+        double d = __dsqrt_rn(s);
+        if ((threadIdx.x & 31) == 0) {
+            dout[m] = d;
+            atomicMin(&best_bits[cid], (unsigned long long)__double_as_longlong(d));
+        }
+    }
+}
+
+__global__ void k_seal_pick(int64_t nfeat_total, const int32_t *__restrict__ fmem_cid, const int64_t *__restrict__ foff,
+                            const double *__restrict__ dout, const unsigned long long *__restrict__ best_bits,
+                            int *__restrict__ best_pos) {
+    int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (m >= nfeat_total) return;
+    int cid = fmem_cid[m];
+    if ((unsigned long long)__double_as_longlong(dout[m]) == best_bits[cid])
+        atomicMin(&best_pos[cid], (int)(m - foff[cid]));
+}
+
+// ---------------------------------------------------------------------------
+// host-side orchestration
+// ---------------------------------------------------------------------------
+
+int64_t scan_i32_to_i64(const int32_t *in, int64_t n, int64_t *out_excl, cudaStream_t st, int64_t *scratch_total);
+void scan_u8_to_i64(const uint8_t *in, int64_t n, int invert, int64_t *out_excl, int64_t *d_total, cudaStream_t st);
+
+static double screen_rel(int D) {
+    const double u = 5.9604644775390625e-08;  // 2^-24
+    double g = (3.0 + 64.0 + (double)((D + 63) / 64) + 2.0) * u;
+    return 2.0 * (g / 2.0 + u) + 1e-12;
+}
+
+template <typename T>
+void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
+    cudaStream_t st = s->st;
+    const int D = s->cfg.dim;
+    const float rel = (float)screen_rel(D);
+    const float absc = (float)(2.0 * 2.384185791015625e-07);  // 2^-22 * 2
+    for (int64_t c0 = c_begin; c0 < c_end; c0 += s->B) {
+        const int B = (int)std::min<int64_t>(s->B, c_end - c0);
+        // 1. snapshot screen
+        {
+            dim3 grid((unsigned)cdiv(s->ld, SC_T), (unsigned)cdiv(B, SC_T));
+            FromSnapshot fb{s->C32.p, s->snap_slot.p, D};
+            k_screen<T, FromSnapshot><<<grid, 256, 0, st>>>(B, c0, s->frow.p, D, s->ctr.p + C_NSNAP, (int)s->ld, fb,
+                                                            s->dist.p, s->ld);
+            FX_LAUNCHED();
+        }
+        // 2. residuals + their in-batch columns
+        {
+            k_residuals<<<(unsigned)cdiv((int64_t)B * 32, 256), 256, 0, st>>>(
+                B, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p, s->snap_slot.p, s->fnorm.p, c0, rel, absc, s->cfg.t,
+                s->res_col.p, s->res_pos.p, s->ctr.p + C_NRES);
+            FX_LAUNCHED();
+            dim3 grid((unsigned)cdiv(B, SC_T), (unsigned)cdiv(B, SC_T));
+            FromResidual<T> fb{s->frow.p, c0, s->res_pos.p};
+            k_screen<T, FromResidual<T>><<<grid, 256, 0, st>>>(B, c0, s->frow.p, D, s->ctr.p + C_NRES, B, fb, s->dres.p, B);
+            FX_LAUNCHED();
+        }
+        // 3. sequential resolve
+        {
+            ResolveArgs A;
+            A.B = B;
+            A.c0 = c0;
+            A.D = D;
+            A.T = s->cfg.t;
+            A.M = s->cfg.m;
+            A.rel = rel;
+            A.absc = absc;
+            A.dist = s->dist.p;
+            A.ld = s->ld;
+            A.dres = s->dres.p;
+            A.ldr = B;
+            A.res_col = s->res_col.p;
+            A.dod = s->dod.p;
+            A.frow = s->frow.p;
+            A.fnorm = s->fnorm.p;
+            A.dup_run = s->dup_run.p;
+            A.cls_obj = s->cls_obj.p;
+            A.S = s->S.p;
+            A.s_cid = s->s_cid.p;
+            A.s_nfeat = s->s_nfeat.p;
+            A.s_size = s->s_size.p;
+            A.s_snapq = s->s_snapq.p;
+            A.s_seedpos = s->s_seedpos.p;
+            A.s_foldpos = s->s_foldpos.p;
+            A.s_pend = s->s_pend.p;
+            A.s_odcol = s->s_odcol.p;
+            A.s_evicted = s->s_evicted.p;
+            A.s_didx = s->s_didx.p;
+            A.s_drift = s->s_drift.p;
+            A.s_cn2 = s->s_cn2.p;
+            A.live = s->live.p;
+            A.live_pos = s->live_pos.p;
+            A.free_stack = s->free_stack.p;
+            A.defer_free = s->defer_free.p;
+            A.snap_slot = s->snap_slot.p;
+            A.ctr = s->ctr.p;
+            A.slot_of = s->slot_of.p;
+            A.pend_rank = s->pend_rank.p;
+            A.evict_slot = s->evict_slot.p;
+            A.evict_cid = s->evict_cid.p;
+            A.dirty = s->dirty.p;
+            A.dirty_off = s->dirty_off.p;
+            A.pend_list = s->pend_list.p;
+            A.cluster_of = s->cluster_of.p;
+            A.mrank = s->mrank.p;
+            A.frank = s->frank.p;
+            A.plan = s->plan.p;
+            const PwPlan &P = *s->plan_host;
+            size_t smem = ((size_t)(B * 8 + 15) & ~(size_t)15) + sizeof(double) * (P.n_chains + P.n_leaves + P.n_ops + 8);
+            auto kern = k_resolve<T>;
+            FX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            kern<<<1, RS_THREADS, smem, st>>>(A);
+            FX_LAUNCHED();
+        }
+        // 4. cluster-array capacity (final centroids are written for evicted clusters)
+        FX_CUDA(cudaMemcpyAsync(s->h_ctr, s->ctr.p, sizeof(int64_t) * C_COUNT, cudaMemcpyDeviceToHost, st));
+        FX_CUDA(cudaStreamSynchronize(st));
+        if (s->h_ctr[C_ERR]) throw Error{FX_E_INTERNAL, "resolve: candidate list overflow"};
+        int64_t ncl = s->h_ctr[C_NEXT_CID];
+        if (ncl > s->cl_cap) {
+            int64_t cap = std::max<int64_t>(ncl, s->cl_cap * 2);
+            s->fcent.grow((size_t)cap * D, (size_t)s->cl_cap * D, st);
+            s->cl_nfeat.grow(cap, s->cl_cap, st);
+            s->cl_size.grow(cap, s->cl_cap, st);
+            s->cl_cap = cap;
+        }
+        // 5. fold
+        const int nd = (int)s->h_ctr[C_NDIRTY];
+        if (nd > 0) {
+            k_zero_cn2<<<(unsigned)cdiv(nd, 256), 256, 0, st>>>(s->ctr.p, s->dirty.p, s->s_cn2.p);
+            FX_LAUNCHED();
+            dim3 grid((unsigned)cdiv(D, 256), (unsigned)nd);
+            k_fold<T><<<grid, 256, 0, st>>>(D, c0, s->ctr.p, s->dirty.p, s->dirty_off.p, s->pend_list.p, s->frow.p,
+                                            s->S.p, s->C32.p, s->s_nfeat.p, s->s_foldpos.p, s->s_seedpos.p,
+                                            s->s_evicted.p, s->s_cid.p, s->s_size.p, s->s_cn2.p, s->fcent.p,
+                                            s->cl_nfeat.p, s->cl_size.p);
+            FX_LAUNCHED();
+        }
+    }
+}
+
+template void run_batches<float>(fx_stream *, int64_t, int64_t);
+template void run_batches<double>(fx_stream *, int64_t, int64_t);
+
+void launch_dup_flags(fx_stream *s, int64_t n, const int64_t *d_fid, const double *d_sig, uint8_t *d_out) {
+    const int S = s->cfg.sig_dim;
+    k_dup_flags<<<(unsigned)cdiv(n, 256), 256, 0, s->st>>>(n, S, d_fid, d_sig, s->has_prev ? 1 : 0, s->prev_fid,
+                                                           s->prev_sig.p, s->cfg.pixel_eps, d_out);
+    FX_LAUNCHED();
+}
+
+void launch_compact(fx_stream *s, int64_t n, int64_t obj_base, int64_t cls_base, const uint8_t *d_dup,
+                    const int64_t *d_excl, const char *feat_base, int compact) {
+    const int64_t row_bytes = (int64_t)s->cfg.dim * s->esize;
+    k_compact_cls<<<(unsigned)cdiv(n, 256), 256, 0, s->st>>>(n, obj_base, cls_base, d_dup, d_excl, feat_base,
+                                                             row_bytes, compact, s->cls_obj.p, s->frow.p, s->dup_run.p);
+    FX_LAUNCHED();
+    k_dup_runs<<<(unsigned)cdiv(n, 256), 256, 0, s->st>>>(n, cls_base, d_dup, d_excl, s->dup_run.p);
+    FX_LAUNCHED();
+}
+
+void launch_fnorm(fx_stream *s, int64_t c0, int64_t nc) {
+    if (nc <= 0) return;
+    unsigned grid = (unsigned)cdiv(nc * 32, 256);
+    if (s->cfg.feat_type == FX_F64)
+        k_fnorm<double><<<grid, 256, 0, s->st>>>(c0, nc, s->cfg.dim, s->frow.p, s->fnorm.p);
+    else
+        k_fnorm<float><<<grid, 256, 0, s->st>>>(c0, nc, s->cfg.dim, s->frow.p, s->fnorm.p);
+    FX_LAUNCHED();
+}
+
+void launch_rank(fx_stream *s, int64_t c0, int64_t nc, const int32_t *d_tcls, unsigned long long *d_err) {
+    if (nc <= 0) return;
+    k_rank_topk<<<(unsigned)cdiv(nc, 256), 256, 0, s->st>>>(c0, nc, s->cls_obj.p, s->oid.p, d_tcls, s->cfg.k,
+                                                           s->cfg.vocab, s->gt, s->seed, s->rm_thr.p, s->rm_emit.p,
+                                                           s->rm_fill.p, s->topk.p, d_err);
+    FX_LAUNCHED();
+}
+
+void launch_final_live(fx_stream *s) {
+    const int D = s->cfg.dim;
+    int64_t L = s->h_ctr[C_NLIVE];
+    if (L <= 0) return;
+    dim3 grid((unsigned)cdiv(D, 256), (unsigned)L);
+    k_final_live<<<grid, 256, 0, s->st>>>(D, s->ctr.p, s->live.p, s->S.p, s->s_nfeat.p, s->s_cid.p, s->s_size.p,
+                                          s->fcent.p, s->cl_nfeat.p, s->cl_size.p);
+    FX_LAUNCHED();
+}
+
+void launch_dup_members(fx_stream *s, int64_t n, const int64_t *d_excl_all, int64_t *d_anchor) {
+    k_anchor<<<(unsigned)cdiv(n, 256), 256, 0, s->st>>>(n, s->is_dup.p, d_excl_all, s->cls_obj.p, d_anchor);
+    FX_LAUNCHED();
+    k_dup_members<<<(unsigned)cdiv(n, 256), 256, 0, s->st>>>(n, s->is_dup.p, d_anchor, s->cluster_of.p, s->mrank.p,
+                                                             s->frank.p);
+    FX_LAUNCHED();
+}
+
+void launch_seal(fx_stream *s, int64_t nfeat_total, const int32_t *fmem_cls, const int32_t *fmem_cid,
+                 const int64_t *foff, unsigned long long *best_bits, double *dout, int *best_pos) {
+    if (nfeat_total <= 0) return;
+    const PwPlan &P = *s->plan_host;
+    const int per = P.n_chains + P.n_leaves + P.n_ops;
+    const int threads = 256;
+    size_t smem = sizeof(double) * per * (threads / 32);
+    unsigned grid = (unsigned)std::min<int64_t>(cdiv(nfeat_total, threads / 32), 148 * 16);
+    if (s->cfg.feat_type == FX_F64) {
+        FX_CUDA(cudaFuncSetAttribute(k_seal_dist<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_seal_dist<double><<<grid, threads, smem, s->st>>>(nfeat_total, s->cfg.dim, fmem_cls, fmem_cid, s->frow.p,
+                                                            s->fcent.p, s->plan.p, best_bits, dout);
+    } else {
+        FX_CUDA(cudaFuncSetAttribute(k_seal_dist<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_seal_dist<float><<<grid, threads, smem, s->st>>>(nfeat_total, s->cfg.dim, fmem_cls, fmem_cid, s->frow.p,
+                                                           s->fcent.p, s->plan.p, best_bits, dout);
+    }
+    FX_LAUNCHED();
+    k_seal_pick<<<(unsigned)cdiv(nfeat_total, 256), 256, 0, s->st>>>(nfeat_total, fmem_cid, foff, dout, best_bits,
+                                                                     best_pos);
+    FX_LAUNCHED();
+}
+
+}  // namespace fx

@@ -1,0 +1,186 @@
+"""TopKIndex on the device (drop-in for focusidx.index build/lookup).
+
+`build` (index.py:60-72) posts clusters under every class of their class set;
+`lookup` (index.py:75-85) filters a class's postings by best rank <= k_x.
+Both run on the device (K3 / K4, csrc/index.cu, csrc/capi.cu); the Python
+TopKIndex keeps the reference's fields (`header`, `clusters`, `postings`),
+materialising them lazily from the device index on first access.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .clustering import Cluster
+from .core import Config, decode_class, encode_class
+from .errors import KxTooLarge
+
+
+@dataclass(frozen=True)
+class IndexHeader:
+    stream_id: str
+    dim: int
+    vocab: int
+    n_objects: int
+    config: Config
+
+    @property
+    def k(self) -> int:
+        return self.config.k
+
+
+class DeviceIndex:
+    """Owner of an fx_index handle."""
+
+    def __init__(self, handle):
+        self.handle = handle
+        sz = _lib.IndexSizes()
+        _lib.check(_lib.load().fx_index_sizes_get(handle, ctypes.byref(sz)))
+        self.sizes = sz
+        self._export = None
+
+    def __del__(self):
+        h, self.handle = getattr(self, "handle", None), None
+        if h is not None and _lib._lib is not None:
+            _lib._lib.fx_index_destroy(h)
+
+    def export(self, centroids: bool = True) -> dict:
+        if self._export is not None and (not centroids or "centroids" in self._export):
+            return self._export
+        s = self.sizes
+        C, D = s.n_clusters, s.dim
+        out = dict(
+            cluster_ids=np.empty(C, np.int64), reps=np.empty(C, np.int64),
+            mem_off=np.empty(C + 1, np.int64), mem_oid=np.empty(s.n_members, np.int64),
+            mem_fid=np.empty(s.n_members, np.int64), cls_off=np.empty(C + 1, np.int64),
+            cls_id=np.empty(s.n_class_entries, np.int32), cls_rank=np.empty(s.n_class_entries, np.int32),
+            post_off=np.empty(s.vocab + 2, np.int64), post_cluster=np.empty(s.n_postings, np.int64))
+        cen = None
+        if centroids and s.has_centroids:
+            cen = np.empty((C, D), np.float64)
+            out["centroids"] = cen
+        _lib.check(_lib.load().fx_index_export(
+            self.handle, _lib.p64(out["cluster_ids"]), _lib.pf64(cen) if cen is not None else None,
+            _lib.p64(out["reps"]), _lib.p64(out["mem_off"]), _lib.p64(out["mem_oid"]), _lib.p64(out["mem_fid"]),
+            _lib.p64(out["cls_off"]), _lib.p32(out["cls_id"]), _lib.p32(out["cls_rank"]),
+            _lib.p64(out["post_off"]), _lib.p64(out["post_cluster"])))
+        self._export = out
+        return out
+
+
+class TopKIndex:
+    """header + clusters (id -> Cluster) + postings (class -> sorted ids)."""
+
+    def __init__(self, header: IndexHeader, clusters=None, postings=None, device: DeviceIndex | None = None):
+        self.header = header
+        self._clusters = clusters
+        self._postings = postings
+        self.device = device
+
+    # -- lazily materialised reference fields --------------------------------
+    @property
+    def clusters(self) -> dict:
+        if self._clusters is None:
+            self._materialise()
+        return self._clusters
+
+    @clusters.setter
+    def clusters(self, v):
+        self._clusters = v
+
+    @property
+    def postings(self) -> dict:
+        if self._postings is None:
+            self._materialise()
+        return self._postings
+
+    @postings.setter
+    def postings(self, v):
+        self._postings = v
+
+    def _materialise(self):
+        ex = self.device.export(centroids=True)
+        V = self.header.vocab
+        cen = ex.get("centroids")
+        clusters = {}
+        mo, co, ci = ex["mem_off"], ex["cls_off"], ex["cls_id"]
+        for i, cid in enumerate(ex["cluster_ids"].tolist()):
+            a, b = mo[i], mo[i + 1]
+            ca, cb = co[i], co[i + 1]
+            ranks = {(-1 if c == V else c): r for c, r in zip(ci[ca:cb].tolist(), ex["cls_rank"][ca:cb].tolist())}
+            rep = int(ex["reps"][i])
+            clusters[cid] = Cluster(
+                cluster_id=cid, centroid=cen[i] if cen is not None else np.zeros(self.header.dim),
+                member_object_ids=ex["mem_oid"][a:b].tolist(),
+                frame_ids=ex["mem_fid"][a:b].tolist(), class_best_rank=ranks,
+                centroid_member_id=None if rep < 0 else rep, sealed=True)
+        postings = {}
+        po, pc = ex["post_off"], ex["post_cluster"]
+        for enc in range(V + 1):
+            a, b = po[enc], po[enc + 1]
+            if b > a:
+                postings[-1 if enc == V else enc] = pc[a:b].tolist()
+        if self._clusters is None:
+            self._clusters = clusters
+        if self._postings is None:
+            self._postings = postings
+
+    def record_count(self) -> int:
+        return len(self.clusters) + sum(len(v) for v in self.postings.values())
+
+
+def build(clusters, header: IndexHeader, device: int | None = None) -> TopKIndex:
+    """index.build on the device: clusters are marshalled into CSR arrays
+    (sorted by id), postings are built by K3 (csrc/index.cu)."""
+    cl = sorted(clusters, key=lambda c: c.cluster_id)
+    V, D = header.vocab, header.dim
+    C = len(cl)
+    ids = np.array([c.cluster_id for c in cl], dtype=np.int64)
+    reps = np.array([-1 if c.centroid_member_id is None else c.centroid_member_id for c in cl], dtype=np.int64)
+    mem_off = np.zeros(C + 1, np.int64)
+    cls_off = np.zeros(C + 1, np.int64)
+    for i, c in enumerate(cl):
+        mem_off[i + 1] = mem_off[i] + len(c.member_object_ids)
+        cls_off[i + 1] = cls_off[i] + len(c.class_best_rank)
+    mem_oid = np.fromiter((o for c in cl for o in c.member_object_ids), np.int64, int(mem_off[-1]))
+    mem_fid = np.fromiter((f for c in cl for f in c.frame_ids), np.int64, int(mem_off[-1]))
+    cls_id = np.fromiter((encode_class(k, V) for c in cl for k in c.class_best_rank), np.int32, int(cls_off[-1]))
+    cls_rank = np.fromiter((r for c in cl for r in c.class_best_rank.values()), np.int32, int(cls_off[-1]))
+    cen = None
+    if C and all(getattr(c, "centroid", None) is not None and np.shape(c.centroid) == (D,) for c in cl):
+        cen = np.ascontiguousarray(np.array([c.centroid for c in cl], dtype=np.float64).reshape(C, D))
+    L = _lib.load()
+    h = _lib.vp()
+    _lib.check(L.fx_index_build(C, V, header.k, D, _lib.device() if device is None else device, _lib.p64(ids),
+                                _lib.pf64(cen) if cen is not None else None, _lib.p64(reps), _lib.p64(mem_off),
+                                _lib.p64(mem_oid), _lib.p64(mem_fid), _lib.p64(cls_off), _lib.p32(cls_id),
+                                _lib.p32(cls_rank), ctypes.byref(h)))
+    dev = DeviceIndex(h)
+    by_id = {c.cluster_id: c for c in cl}
+    return TopKIndex(header, clusters=by_id, postings=None, device=dev)
+
+
+def lookup(idx: TopKIndex, class_id: int, k_x: int | None = None) -> list:
+    """Cluster ids posted under class_id with best rank <= k_x, ascending."""
+    k = idx.header.k
+    kx = k if k_x is None else k_x
+    if not 1 <= kx <= k:
+        raise KxTooLarge(f"k_x={kx} outside [1, {k}]")
+    V = idx.header.vocab
+    enc = encode_class(class_id, V)
+    if enc < 0 or enc > V:
+        return []
+    L = _lib.load()
+    n = ctypes.c_int64(0)
+    _lib.check(L.fx_lookup(idx.device.handle, enc, kx, None, 0, ctypes.byref(n)))
+    out = np.empty(n.value, np.int64)
+    if n.value:
+        _lib.check(L.fx_lookup(idx.device.handle, enc, kx, _lib.p64(out), n.value, ctypes.byref(n)))
+    return out.tolist()
+
+
+__all__ = ["IndexHeader", "TopKIndex", "DeviceIndex", "build", "lookup", "decode_class"]

@@ -1,0 +1,221 @@
+"""Ingest: the drop-in `ingest_stream` (focusidx/ingest.py:50-96) on the B200.
+
+Control flow is the reference's; the work is not:
+  K0 pixel differencing, K1a rank-model top-K, K2 batched screen + exact
+  sequential resolve + fold, deferred seal, K3 index build all run in
+  libfocus_b200.so.  The host marshals the stream into arrays and raises the
+  reference's exceptions.
+
+`classify_fn` (the reference's plugin point, ingest.py:52-61,73) is honoured:
+when given, it is called once per retained object in stream order and its
+top-K classes and feature are what the device clusters.  When omitted, the
+device rank model classifies; the profile's feature noise (extract_feature,
+classifiers.py:152-158) is the ingest input -- the cheap CNN's output.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib, classifiers
+from .core import Config, encode_class, validate_config
+from .errors import DimensionMismatch, SignatureLengthMismatch
+from .index import DeviceIndex, IndexHeader, TopKIndex
+
+DEFAULT_PIXEL_EPS = 0.01
+
+
+@dataclass(frozen=True)
+class IngestReport:
+    objects_seen: int
+    objects_classified: int
+    clusters_emitted: int
+    ingest_cost_units: float
+    dedup_savings_units: float
+    distance_computations: int
+    gt_invocations: int = 0
+
+
+@dataclass(frozen=True)
+class StreamHeader:
+    """Fields of streamio.StreamHeader (streamio.py:30-36) the path reads."""
+    stream_id: str
+    fps: float
+    dim: int
+    sig_dim: int
+    vocab: int
+
+
+class Stream:
+    """One device stream engine (one per video stream, single writer)."""
+
+    def __init__(self, dim: int, sig_dim: int, vocab: int, k: int, t: float, m: int,
+                 pixel_eps: float = DEFAULT_PIXEL_EPS, feat_type: int = _lib.FX_F32,
+                 device: int | None = None, batch: int = 0):
+        self.L = _lib.load()
+        cfg = _lib.StreamConfig(dim=dim, sig_dim=sig_dim, vocab=vocab, k=k, t=float(t), m=int(m),
+                                pixel_eps=float(pixel_eps), feat_type=feat_type,
+                                device=_lib.device() if device is None else device, batch=batch)
+        self.cfg = cfg
+        h = _lib.vp()
+        _lib.check(self.L.fx_stream_create(ctypes.byref(cfg), ctypes.byref(h)))
+        self.handle = h
+        self._keep = []
+
+    def __del__(self):
+        h, self.handle = getattr(self, "handle", None), None
+        if h is not None and _lib._lib is not None:
+            _lib._lib.fx_stream_destroy(h)
+
+    def set_rank_model(self, profile, seed: int):
+        thr, emit, fill = classifiers.device_tables(profile, seed, self.cfg.k)
+        rm = _lib.RankModelC(ground_truth=1 if profile.kind == classifiers.GROUND_TRUTH else 0,
+                             seed=seed & ((1 << 64) - 1), thresholds=_lib.pu64(thr), emit_map=_lib.p32(emit),
+                             fillers=_lib.p32(fill))
+        _lib.check(self.L.fx_stream_set_rank_model(self.handle, ctypes.byref(rm)))
+
+    def dup_flags(self, fids: np.ndarray, sigs: np.ndarray) -> np.ndarray:
+        n = fids.size
+        out = np.zeros(n, np.uint8)
+        if n:
+            _lib.check(self.L.fx_stream_dup_flags(self.handle, n, _lib.p64(fids), _lib.pf64(sigs), _lib.pu8(out)))
+        return out.astype(bool)
+
+    def ingest(self, oids, fids, sigs, feats, true_class=None, topk=None, compact=False):
+        n = oids.size
+        _lib.check(self.L.fx_ingest(self.handle, n, _lib.p64(oids), _lib.p64(fids), _lib.pf64(sigs), _lib.pv(feats),
+                                    _lib.p32(true_class) if true_class is not None else None,
+                                    _lib.p32(topk) if topk is not None else None,
+                                    _lib.FX_FEATS_COMPACT if compact else 0))
+
+    def ingest_device(self, n, oids_ptr, fids_ptr, sigs_ptr, feats_ptr, tcls_ptr=None, topk_ptr=None, compact=False):
+        _lib.check(self.L.fx_ingest_device(self.handle, n, oids_ptr, fids_ptr, sigs_ptr, feats_ptr, tcls_ptr,
+                                           topk_ptr, _lib.FX_FEATS_COMPACT if compact else 0))
+
+    def finalize(self):
+        rep = _lib.IngestReportC()
+        h = _lib.vp()
+        _lib.check(self.L.fx_finalize(self.handle, ctypes.byref(h), ctypes.byref(rep)))
+        return DeviceIndex(h), rep
+
+    def object_results(self, n: int, k: int):
+        cl = np.empty(n, np.int32)
+        dup = np.empty(n, np.uint8)
+        tk = np.empty(n * k, np.int32)
+        _lib.check(self.L.fx_stream_object_results(self.handle, _lib.p32(cl), _lib.pu8(dup), _lib.p32(tk)))
+        return cl, dup.astype(bool), tk.reshape(n, k)
+
+    def counters(self) -> dict:
+        out = np.zeros(16, np.float64)
+        _lib.check(self.L.fx_stream_timings(self.handle, _lib.pf64(out), 16))
+        names = ["nlive", "next_cid", "dc", "nfree", "nevict_total", "exact", "nsnap", "nres", "ninserted",
+                 "nevict_batch", "ndefer", "nod", "last_cid", "ndirty", "err", "fast"]
+        return dict(zip(names, out.astype(np.int64).tolist()))
+
+
+def pixel_diff(prev, cur, eps: float) -> bool:
+    """ingest.py:37-47 for one pair, evaluated by the device K0 kernel."""
+    if eps < 0:
+        return False
+    a, b = np.asarray(prev.pixel_signature, np.float64), np.asarray(cur.pixel_signature, np.float64)
+    if a.shape[0] != b.shape[0]:
+        raise SignatureLengthMismatch(f"{a.shape[0]} vs {b.shape[0]}")
+    if cur.frame_id - prev.frame_id > 1:
+        return False
+    s = Stream(dim=1, sig_dim=a.shape[0], vocab=1, k=1, t=0.0, m=1, pixel_eps=eps, batch=64)
+    flags = s.dup_flags(np.array([prev.frame_id, cur.frame_id], np.int64),
+                        np.ascontiguousarray(np.stack([a, b])))
+    return bool(flags[1])
+
+
+def _f32_exact(x: np.ndarray) -> bool:
+    return x.dtype == np.float32 or bool(np.array_equal(x.astype(np.float32).astype(x.dtype), x))
+
+
+def ingest_arrays(oids, fids, sigs, feats, cfg: Config, profile, *, vocab: int, seed: int = 0,
+                  pixel_eps: float = DEFAULT_PIXEL_EPS, true_class=None, topk=None, compact: bool = False,
+                  stream_id: str = "synthetic", device: int | None = None, batch: int = 0):
+    """Array-level ingest: the C-ABI call with host buffers.  `feats` rows are
+    the extracted features (float32 or float64); `true_class` (int32, -2 =
+    unlabeled) drives the device rank model, or `topk` (n x k encoded, OTHER =
+    V) comes from an external classifier.  Returns (TopKIndex, IngestReport,
+    Stream)."""
+    oids = np.ascontiguousarray(oids, np.int64)
+    fids = np.ascontiguousarray(fids, np.int64)
+    n = oids.size
+    S = sigs.shape[1] if sigs.ndim == 2 else 0
+    sigs = np.ascontiguousarray(sigs, np.float64).reshape(n, S)
+    D = feats.shape[1] if feats.ndim == 2 else 0
+    feat_type = _lib.FX_F64 if feats.dtype == np.float64 else _lib.FX_F32
+    feats = np.ascontiguousarray(feats)
+    st = Stream(D, S, vocab, cfg.k, cfg.t, cfg.m, pixel_eps, feat_type, device, batch)
+    if topk is None:
+        st.set_rank_model(profile, seed)
+    if n:
+        st.ingest(oids, fids, sigs, feats,
+                  true_class=None if true_class is None else np.ascontiguousarray(true_class, np.int32),
+                  topk=None if topk is None else np.ascontiguousarray(topk, np.int32), compact=compact)
+    dix, rep = st.finalize()
+    header = IndexHeader(stream_id=stream_id, dim=D, vocab=vocab, n_objects=n, config=cfg)
+    report = IngestReport(
+        objects_seen=rep.objects_seen, objects_classified=rep.objects_classified,
+        clusters_emitted=rep.clusters_emitted,
+        ingest_cost_units=rep.objects_classified * profile.cost_units,
+        dedup_savings_units=(rep.objects_seen - rep.objects_classified) * profile.cost_units,
+        distance_computations=rep.distance_computations)
+    assert report.distance_computations <= cfg.m * report.objects_classified, "O(Mn) distance budget exceeded"
+    return TopKIndex(header, device=dix), report, st
+
+
+def ingest_stream(header, stream, cfg: Config, profiles, pixel_eps: float = DEFAULT_PIXEL_EPS,
+                  seed: int = 0, classify_fn=None):
+    """Drop-in for focusidx.ingest.ingest_stream; returns (TopKIndex, IngestReport)."""
+    validate_config(cfg, profiles)
+    profile = profiles[cfg.profile_id]
+    objs = list(stream)
+    n = len(objs)
+    D, V, K = header.dim, header.vocab, cfg.k
+    oids = np.fromiter((o.object_id for o in objs), np.int64, n)
+    fids = np.fromiter((o.frame_id for o in objs), np.int64, n)
+    slen = [np.shape(o.pixel_signature)[0] for o in objs]
+    S = slen[0] if n else 0
+    if pixel_eps >= 0:
+        for i in range(1, n):
+            if slen[i] != slen[i - 1]:
+                raise SignatureLengthMismatch(f"{slen[i - 1]} vs {slen[i]}")
+    if any(s != S for s in slen):
+        # differencing off: signatures are never compared; pad to a common width
+        S = max(slen)
+    sigs = np.zeros((n, S), np.float64)
+    for i, o in enumerate(objs):
+        sigs[i, :slen[i]] = o.pixel_signature
+    st = Stream(1, S, 1, 1, 0.0, 1, pixel_eps, _lib.FX_F32, None, 64)  # K0 only
+    dup = st.dup_flags(fids, sigs) if n else np.zeros(0, bool)
+    keep = np.flatnonzero(~dup)
+    if classify_fn is not None:
+        topk = np.zeros((n, K), np.int32)
+        rows = []
+        for i in keep.tolist():
+            rc = classify_fn(profile, objs[i], seed).top(K)
+            cls = [encode_class(c, V) for c in rc.classes()]
+            topk[i, :len(cls)] = cls
+            rows.append(np.asarray(rc.feature))
+        tcls = None
+    else:
+        topk = None
+        tcls = np.array([-2 if o.true_class is None else o.true_class for o in objs], np.int32)
+        rows = [classifiers.extract_feature(profile, objs[i], seed) for i in keep.tolist()]
+    for r in rows:
+        if np.shape(r)[0] != D:
+            raise DimensionMismatch(f"feature dim {np.shape(r)[0]} != engine dim {D}")
+    F = np.array(rows, dtype=np.float64).reshape(len(rows), D) if rows else np.zeros((0, D))
+    if all(np.asarray(r).dtype == np.float32 for r in rows) or _f32_exact(F):
+        F = F.astype(np.float32)
+    del st
+    idx, report, _ = ingest_arrays(oids, fids, sigs, F, cfg, profile, vocab=V, seed=seed, pixel_eps=pixel_eps,
+                                   true_class=tcls, topk=topk, compact=True, stream_id=header.stream_id)
+    idx.header = IndexHeader(stream_id=header.stream_id, dim=D, vocab=V, n_objects=n, config=cfg)
+    return idx, report
