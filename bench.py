@@ -1,0 +1,296 @@
+"""Benchmark: Focus ingest hot path on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+One step = ingest of one whole synthetic stream through K0 (pixel diff) +
+K1a (rank-model top-K) + K2 (screen / resolve / fold) + seal + K3 (index
+build): the C2 workload (1 stream x 1M objects, D=2048, V=1000, K=4, T=7.5,
+M=100) per GPU.  Multi-GPU: one process per GPU, each owns its own stream
+(natural stream sharding, no data-path collective) -> weak scaling; value =
+objects of all ranks / max-over-ranks device time.
+
+`value` times fx_ingest_device + fx_finalize with inputs resident in HBM
+(CUDA events on the library's stream).  `e2e` times the host-buffer C-ABI
+call (fx_ingest from pinned host memory, H2D inside, index read back).
+`cpu_baseline` runs the CPU oracle port (oracle/) on a bounded prefix of the
+same workload; `--impl reference` times that port as the reference arm.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+WORKLOAD = dict(n=1_000_000, dim=2048, vocab=1000, n_stream_classes=100, k=4, t=7.5, m=100)
+METRIC = "ingest objects/sec (top-K+cluster+index)"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region."""
+
+    def __init__(self, dev: int):
+        self.dev = dev
+        self.proc = None
+        self.path = os.path.join(REPO, "gpurun_out", f"clocks_{os.getpid()}.csv")
+
+    def __enter__(self):
+        os.makedirs(os.path.dirname(self.path), exist_ok=True)
+        try:
+            self.fh = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.dev), "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.fh, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            self.proc.wait()
+            self.fh.close()
+
+    def summary(self):
+        try:
+            rows = [l.strip().split(",") for l in open(self.path) if l.strip()]
+        except Exception:
+            return None
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows if r[0].strip().replace(".", "").isdigit()]
+        mx = max(float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if len(r) > 3 + i and "Active" in r[3 + i]
+                          and "Not" not in r[3 + i]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(rows)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_sample(n_sample: int, seed: int, threads: int):
+    """Time the CPU oracle port (reference algorithm restated in C + numpy) on
+    the first n_sample objects of the workload.  Returns objects/s."""
+    from oracle import oracle as O
+    from paper_1801_03493_b200 import synth
+    st = synth.generate(n_sample, dim=WORKLOAD["dim"], vocab=WORKLOAD["vocab"],
+                        n_stream_classes=WORKLOAD["n_stream_classes"], seed=seed, device="cpu")
+    oids, fids = st.oids.numpy(), st.fids.numpy()
+    sigs, feats, tcls = st.sigs.numpy(), st.feats.numpy(), st.true_class.numpy()
+    prof = O.default_profiles(WORKLOAD["vocab"])["cheap"]
+    O.set_threads(threads)
+    k = WORKLOAD["k"]
+    t0 = time.perf_counter()
+    dup = O.dup_flags(fids, sigs, 0.01)
+    keep = ~dup
+    topk = np.zeros((oids.size, k), np.int32)
+    topk[keep] = O.classify_topk(prof, 0, oids[keep], tcls[keep], k)
+    res = O.ingest(oids, fids, sigs, feats, topk, k, WORKLOAD["t"], WORKLOAD["m"], is_dup=dup, with_centroids=False)
+    O.build_postings(res.clusters)
+    dt = time.perf_counter() - t0
+    return n_sample / dt, dt, len(res.clusters)
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    n_sample = args.ref_sample
+    for _ in range(args.warmup):
+        cpu_sample(n_sample, 0, threads)
+    vals = []
+    for _ in range(args.steps):
+        v, dt, ncl = cpu_sample(n_sample, 0, threads)
+        vals.append(v)
+    value = float(np.mean(vals))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "objects/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": n_sample / value * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"C2 prefix: first {n_sample} objects of 1 stream (D=2048, V=1000, K=4, T=7.5, "
+                               f"M=100); CPU oracle port of the reference focusidx path", **WORKLOAD},
+        "cpu_baseline": {"value": value, "unit": "objects/s", "cores": threads, "kind": "port",
+                         "sample": f"first {n_sample} objects of the C2 stream per step"},
+        "e2e": {"value": value, "unit": "objects/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--n", type=int, default=WORKLOAD["n"])
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--cpu-sample", type=int, default=20000)
+    ap.add_argument("--ref-sample", type=int, default=20000)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--batch", type=int, default=0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_1801_03493_b200 as fx
+    from paper_1801_03493_b200 import _lib, synth
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    fx.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    W = dict(WORKLOAD, n=args.n)
+    data = synth.generate(W["n"], dim=W["dim"], vocab=W["vocab"], n_stream_classes=W["n_stream_classes"], seed=rank)
+    torch.cuda.synchronize()
+    cfg = fx.Config("cheap", k=W["k"], l_s=W["vocab"], t=W["t"], m=W["m"])
+    prof = fx.make_default_profiles(W["vocab"])["cheap"]
+    L = _lib.load()
+
+    def make_stream():
+        s = fx.ingest.Stream(W["dim"], 16, W["vocab"], W["k"], W["t"], W["m"], 0.01, _lib.FX_F32, local, args.batch)
+        s.set_rank_model(prof, 0)
+        return s
+
+    def step(s):
+        s.ingest_device(W["n"], data.oids.data_ptr(), data.fids.data_ptr(), data.sigs.data_ptr(),
+                        data.feats.data_ptr(), data.true_class.data_ptr())
+        return s.finalize()
+
+    # warm-up
+    for _ in range(args.warmup):
+        s = make_stream()
+        step(s)
+        del s
+    streams = [make_stream() for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    launches0 = L.fx_kernel_launches()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    results = []
+    with Clocks(local) as clk:
+        ev0.record(torch.cuda.ExternalStream(streams[0].cuda_stream()))
+        for s in streams:
+            results.append(step(s))
+        ev1.record(torch.cuda.ExternalStream(streams[-1].cuda_stream()))
+        torch.cuda.synchronize()
+    launches = L.fx_kernel_launches() - launches0
+    t_ms = ev0.elapsed_time(ev1)
+    if ws > 1:
+        tt = torch.tensor([t_ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        dist.barrier()
+        t_ms = float(tt.item())
+    ms_per_step = t_ms / args.steps
+    value = W["n"] * ws * args.steps / (t_ms / 1e3)
+    rep = results[-1][1]
+    phases = streams[-1].timings()
+    counters = streams[-1].counters()
+
+    # roofline of the dominant kernel (algorithmic bytes)
+    D, n_cls = W["dim"], rep.objects_classified
+    nb = max(1.0, phases["batches"])
+    algo = {
+        "screen": 4.0 * D * n_cls,                   # features streamed once
+        "resolve": 4.0 * counters["dc"],             # screen distances consumed
+        "fold": 4.0 * D * n_cls,                     # features re-read into the float64 sums
+        "seal": 4.0 * D * n_cls,                     # every featured member vs its centroid
+        "k0_k1a": 128.0 * rep.objects_seen + (12.0 + 4 * W["k"]) * n_cls,
+        "index": 12.0 * W["k"] * n_cls,
+    }
+    dom = max(algo, key=lambda k: phases.get(k, 0.0))
+    peak, peak_kind = _peaks()
+    dom_ms = phases[dom]
+    achieved = algo[dom] / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0
+    roofline = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                "launches_per_step": int(nb) if dom in ("screen", "resolve", "fold") else 1,
+                "phase_ms_per_step": {k: v for k, v in phases.items() if k != "batches"}}
+
+    # end-to-end through the host-buffer C ABI
+    e2e = None
+    if rank == 0 or True:
+        ho = data.oids.cpu().pin_memory()
+        hf = data.fids.cpu().pin_memory()
+        hs = data.sigs.cpu().pin_memory()
+        hx = data.feats.cpu().pin_memory()
+        ht = data.true_class.cpu().pin_memory()
+        h2d = sum(t.numel() * t.element_size() for t in (ho, hf, hs, hx, ht))
+        e_times = []
+        d2h = 0
+        for i in range(args.e2e_steps + 1):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            s = fx.ingest.Stream(W["dim"], 16, W["vocab"], W["k"], W["t"], W["m"], 0.01, _lib.FX_F32, local,
+                                 args.batch)
+            s.set_rank_model(prof, 0)
+            s.ingest(ho.numpy(), hf.numpy(), hs.numpy(), hx.numpy(), true_class=ht.numpy())
+            dix, r = s.finalize()
+            ex = dix.export(centroids=True)
+            d2h = sum(a.nbytes for a in ex.values())
+            t1 = time.perf_counter()
+            if i > 0:
+                e_times.append(t1 - t0)
+            del s, dix
+        e2e_v = W["n"] * ws / float(np.mean(e_times))
+        e2e = {"value": e2e_v, "unit": "objects/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "timing": "host wall clock around fx_ingest(host ptrs)+fx_finalize+index export, pinned inputs"}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        v, dt, ncl = cpu_sample(args.cpu_sample, 0, 1)
+        cpu = {"value": v, "unit": "objects/s", "cores": 1, "kind": "port",
+               "sample": f"first {args.cpu_sample} objects of the C2 stream ({dt:.1f} s, single thread)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "objects/s", "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32+f64", "data": "synthetic (device generator, reference model)",
+            "config": {"workload": "C2: 1 stream x 1M objects per GPU, D=2048, V=1000, K=4, T=7.5, M=100",
+                       "streams_per_gpu": 1, "parallelism": f"stream-sharded x{ws}",
+                       "l2": "inputs (8 GB features/stream) exceed L2; no flush", **W},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
+            "gpu_launches": int(launches),
+            "ingest": {"clusters": rep.clusters_emitted, "classified": rep.objects_classified,
+                       "distance_computations": rep.distance_computations, "exact_rechecks": rep.exact_rechecks,
+                       "fast_decisions": counters["fast"]},
+        }
+        print(json.dumps(line))
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

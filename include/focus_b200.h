@@ -236,9 +236,17 @@ const char *fx_last_error(void);
 int fx_version(void);
 /* Number of this library's kernels launched so far (process-wide). */
 int64_t fx_kernel_launches(void);
-/* Per-phase device time accounting of the last fx_ingest/fx_finalize on s:
- * out[0..7] = ms spent in {dup+rank, screen, resolve, fold, seal, index, total, batches}. */
+/* Device time (CUDA events on the stream's CUDA stream) accumulated over all
+ * fx_ingest / fx_finalize calls on s, in ms per phase:
+ * out[0] K0+K1a (dup flags, compaction, rank top-K), out[1] K2 screen,
+ * out[2] K2 resolve, out[3] K2 fold, out[4] seal, out[5] index build (K3),
+ * out[6] number of clustering batches. */
 int fx_stream_timings(fx_stream *s, double *out, int n);
+/* Engine counters: live, clusters, distance_computations, ... (see
+ * fx_handles.cuh Ctr); out[i] for i < n. */
+int fx_stream_counters(fx_stream *s, int64_t *out, int n);
+/* The cudaStream_t the stream's kernels run on (for caller-side CUDA events). */
+void *fx_stream_cuda_stream(fx_stream *s);
 
 #ifdef __cplusplus
 }

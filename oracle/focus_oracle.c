@@ -21,6 +21,9 @@
  * IEEE round-to-nearest everywhere, glibc log() exactly as CPython math.log).
  */
 #include <math.h>
+#ifdef _OPENMP
+#include <omp.h>
+#endif
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -275,9 +278,15 @@ typedef struct {
     int64_t *live; /* ascending cluster ids */
     int64_t nlive, caplive;
     int64_t distance_computations;
-    double *dbuf, *diff;
+    double *dbuf, *diff, *tdiff;
     int64_t dbuf_cap;
+    int nthreads;
 } orc_engine;
+
+static int g_threads = 1;
+/* threads used for the per-insert distance row (bench's reference arm) */
+ORC_API void orc_set_threads(int n) { g_threads = n > 0 ? n : 1; }
+ORC_API int orc_get_threads(void) { return g_threads; }
 
 ORC_API orc_engine *orc_engine_new(int dim, double t, int64_t m, const double *feats) {
     orc_engine *e = (orc_engine *)calloc(1, sizeof(orc_engine));
@@ -286,6 +295,8 @@ ORC_API orc_engine *orc_engine_new(int dim, double t, int64_t m, const double *f
     e->m = m;
     e->feats = feats;
     e->diff = (double *)malloc(sizeof(double) * (dim > 0 ? dim : 1));
+    e->nthreads = g_threads;
+    e->tdiff = (double *)malloc(sizeof(double) * (dim > 0 ? dim : 1) * (size_t)e->nthreads);
     return e;
 }
 
@@ -306,6 +317,7 @@ ORC_API void orc_engine_free(orc_engine *e) {
     free(e->live);
     free(e->dbuf);
     free(e->diff);
+    free(e->tdiff);
     free(e);
 }
 
@@ -370,8 +382,23 @@ ORC_API int64_t orc_insert(orc_engine *e, int64_t row, int64_t oid, int64_t fid,
             e->dbuf_cap = e->nlive * 2;
             e->dbuf = (double *)realloc(e->dbuf, sizeof(double) * e->dbuf_cap);
         }
-        for (int64_t j = 0; j < e->nlive; j++)
-            e->dbuf[j] = orc_dist(e, e->cl[e->live[j]].centroid, f);
+        /* distances are independent per live cluster: threads split the row
+         * (bit-identical to the serial loop; each distance is one pairwise sum) */
+        if (e->nthreads > 1 && e->nlive * (int64_t)e->dim >= 65536) {
+#pragma omp parallel for num_threads(e->nthreads) schedule(static)
+            for (int64_t j = 0; j < e->nlive; j++) {
+                double *tmp = e->tdiff + (size_t)omp_get_thread_num() * e->dim;
+                const double *c = e->cl[e->live[j]].centroid;
+                for (int k = 0; k < e->dim; k++) {
+                    double x = c[k] - f[k];
+                    tmp[k] = x * x;
+                }
+                e->dbuf[j] = sqrt(orc_pairwise_sum(tmp, e->dim));
+            }
+        } else {
+            for (int64_t j = 0; j < e->nlive; j++)
+                e->dbuf[j] = orc_dist(e, e->cl[e->live[j]].centroid, f);
+        }
         e->distance_computations += e->nlive;
         int64_t idx = 0;
         for (int64_t j = 1; j < e->nlive; j++)

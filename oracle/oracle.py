@@ -68,6 +68,8 @@ def lib():
         L.orc_ingest.restype = ctypes.c_void_p
         L.orc_ingest.argtypes = [ctypes.c_int64, ctypes.c_int, _i64p, _i64p, _f64p, _i32p,
                                  ctypes.c_int, _u8p, ctypes.c_double, ctypes.c_int64, _i64p]
+        L.orc_set_threads.restype = None
+        L.orc_set_threads.argtypes = [ctypes.c_int]
         L.orc_engine_free.restype = None
         L.orc_engine_free.argtypes = [ctypes.c_void_p]
         for name in ("orc_n_clusters", "orc_distance_computations", "orc_n_live"):
@@ -80,6 +82,11 @@ def lib():
                                          _f64p, _i32p, _i32p]
         _lib = L
     return _lib
+
+
+def set_threads(n: int) -> None:
+    """Host threads for the per-insert distance row (results are identical)."""
+    lib().orc_set_threads(int(n))
 
 
 def _p(a, t):

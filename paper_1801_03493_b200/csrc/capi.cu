@@ -76,7 +76,47 @@ using namespace fx;
 // handle destructors
 // ---------------------------------------------------------------------------
 
+void fx_stream::tstart(int phase) {
+    int idx = -1;
+    for (size_t i = 0; i < timers.size(); i++) {
+        if (timers[i].phase < 0) {
+            idx = (int)i;
+            break;
+        }
+    }
+    if (idx < 0) {
+        Timer t;
+        FX_CUDA(cudaEventCreate(&t.a));
+        FX_CUDA(cudaEventCreate(&t.b));
+        timers.push_back(t);
+        idx = (int)timers.size() - 1;
+    }
+    timers[idx].phase = phase;
+    FX_CUDA(cudaEventRecord(timers[idx].a, st));
+    open_timer = idx;
+}
+void fx_stream::tstop() {
+    if (open_timer < 0) return;
+    FX_CUDA(cudaEventRecord(timers[open_timer].b, st));
+    pending.push_back(open_timer);
+    open_timer = -1;
+}
+void fx_stream::tcollect() {
+    for (int i : pending) {
+        float ms = 0.f;
+        FX_CUDA(cudaEventSynchronize(timers[i].b));
+        FX_CUDA(cudaEventElapsedTime(&ms, timers[i].a, timers[i].b));
+        t_ms[timers[i].phase] += ms;
+        timers[i].phase = -1;
+    }
+    pending.clear();
+}
+
 fx_stream::~fx_stream() {
+    for (auto &t : timers) {
+        if (t.a) cudaEventDestroy(t.a);
+        if (t.b) cudaEventDestroy(t.b);
+    }
     for (auto *b : owned_feats) delete b;
     delete plan_host;
     if (st) cudaStreamDestroy(st);
@@ -245,6 +285,7 @@ static void ingest_chunk(fx_stream *s, int64_t n, const int64_t *d_oid, const in
     FX_CUDA(cudaMemcpyAsync(s->oid.p + n0, d_oid, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, st));
     FX_CUDA(cudaMemcpyAsync(s->fid.p + n0, d_fid, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, st));
     // K0
+    s->tstart(0);
     launch_dup_flags(s, n, d_fid, d_sig, s->is_dup.p + n0);
     s->has_prev = true;
     FX_CUDA(cudaMemcpyAsync(&s->prev_fid, d_fid + (n - 1), sizeof(int64_t), cudaMemcpyDeviceToHost, st));
@@ -264,7 +305,9 @@ static void ingest_chunk(fx_stream *s, int64_t n, const int64_t *d_oid, const in
     FX_LAUNCHED();
     unsigned long long h_first = 0;
     FX_CUDA(cudaMemcpyAsync(&h_first, first.p, sizeof(h_first), cudaMemcpyDeviceToHost, st));
+    s->tstop();
     FX_CUDA(cudaStreamSynchronize(st));
+    s->tstart(0);
     const int64_t lead = h_first == ~0ull ? n : (int64_t)h_first;
     const int64_t c0 = s->n_cls, cneed = c0 + nc;
     s->cls_obj.grow(cneed, c0, st);
@@ -281,6 +324,7 @@ static void ingest_chunk(fx_stream *s, int64_t n, const int64_t *d_oid, const in
     // K1: top-K
     if (d_topk) {
         FX_CUDA(cudaMemcpyAsync(s->topk.p + n0 * K, d_topk, sizeof(int32_t) * n * K, cudaMemcpyDeviceToDevice, st));
+        s->tstop();
     } else {
         if (!s->has_rm) throw Error{FX_E_USAGE, "no rank model set and no top-K given"};
         DevBuf<unsigned long long> err;
@@ -288,6 +332,7 @@ static void ingest_chunk(fx_stream *s, int64_t n, const int64_t *d_oid, const in
         FX_CUDA(cudaMemsetAsync(err.p, 0xff, sizeof(unsigned long long), st));
         // true_class indexed by global object index: shift the base pointer
         launch_rank(s, c0, nc, d_tcls - n0, err.p);
+        s->tstop();
         unsigned long long h = 0;
         FX_CUDA(cudaMemcpyAsync(&h, err.p, sizeof(h), cudaMemcpyDeviceToHost, st));
         FX_CUDA(cudaStreamSynchronize(st));
@@ -431,7 +476,9 @@ int fx_finalize(fx_stream *s, fx_index **out, fx_ingest_report *rep) {
             dout.reserve(nc + 1);
             FX_CUDA(cudaMemsetAsync(best_bits.p, 0xff, sizeof(unsigned long long) * (C + 1), st));
             FX_CUDA(cudaMemsetAsync(best_pos.p, 0x7f, sizeof(int) * (C + 1), st));
+            s->tstart(4);
             launch_seal(s, nc, fmem_cls.p, fmem_cid.p, foff.p, best_bits.p, dout.p, best_pos.p);
+            s->tstop();
             ix->reps.reserve(C + 1);
             launch_reps(s, C, foff.p, best_pos.p, fmem_cls.p, ix->reps.p);
             ix->cluster_ids.reserve(C + 1);
@@ -439,8 +486,11 @@ int fx_finalize(fx_stream *s, fx_index **out, fx_ingest_report *rep) {
             std::swap(ix->centroids.p, s->fcent.p);
             std::swap(ix->centroids.n, s->fcent.n);
             s->cl_cap = 0;
+            s->tstart(5);
             build_index_from_stream(ix, s, foff.p, fmem_cls.p, nc, st);
+            s->tstop();
             FX_CUDA(cudaStreamSynchronize(st));
+            s->tcollect();
         } catch (...) {
             ix->st = nullptr;
             delete ix;
@@ -478,11 +528,22 @@ int fx_stream_timings(fx_stream *s, double *out, int n) {
     FX_GUARD({
         if (!s || !out) throw Error{FX_E_USAGE, "null argument"};
         set_dev(s->dev);
-        FX_CUDA(cudaMemcpyAsync(s->h_ctr, s->ctr.p, sizeof(int64_t) * C_COUNT, cudaMemcpyDeviceToHost, s->st));
-        FX_CUDA(cudaStreamSynchronize(s->st));
-        for (int i = 0; i < n && i < C_COUNT; i++) out[i] = (double)s->h_ctr[i];
+        s->tcollect();
+        for (int i = 0; i < n && i < 8; i++) out[i] = s->t_ms[i];
     })
 }
+
+int fx_stream_counters(fx_stream *s, int64_t *out, int n) {
+    FX_GUARD({
+        if (!s || !out) throw Error{FX_E_USAGE, "null argument"};
+        set_dev(s->dev);
+        FX_CUDA(cudaMemcpyAsync(s->h_ctr, s->ctr.p, sizeof(int64_t) * C_COUNT, cudaMemcpyDeviceToHost, s->st));
+        FX_CUDA(cudaStreamSynchronize(s->st));
+        for (int i = 0; i < n && i < C_COUNT; i++) out[i] = s->h_ctr[i];
+    })
+}
+
+void *fx_stream_cuda_stream(fx_stream *s) { return s ? (void *)s->st : nullptr; }
 
 int fx_index_sizes_get(fx_index *ix, fx_index_sizes *o) {
     FX_GUARD({

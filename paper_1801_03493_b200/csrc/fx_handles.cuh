@@ -93,6 +93,19 @@ struct fx_stream {
     fx::PwPlan *plan_host = nullptr;
     fx::DevBuf<fx::PwPlan> plan;
 
+    // per-phase device timing (CUDA events, collected at sync points)
+    struct Timer {
+        cudaEvent_t a = nullptr, b = nullptr;
+        int phase = -1;
+    };
+    std::vector<Timer> timers;  // pool
+    std::vector<int> pending;   // indices into timers awaiting collection
+    int open_timer = -1;
+    double t_ms[8] = {0};
+    void tstart(int phase);
+    void tstop();
+    void tcollect();
+
     ~fx_stream();
 };
 

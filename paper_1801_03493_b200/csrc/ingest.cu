@@ -874,7 +874,9 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
     const float absc = (float)(2.0 * 2.384185791015625e-07);  // 2^-22 * 2
     for (int64_t c0 = c_begin; c0 < c_end; c0 += s->B) {
         const int B = (int)std::min<int64_t>(s->B, c_end - c0);
+        s->t_ms[6] += 1.0;
         // 1. snapshot screen
+        s->tstart(1);
         {
             dim3 grid((unsigned)cdiv(s->ld, SC_T), (unsigned)cdiv(B, SC_T));
             FromSnapshot fb{s->C32.p, s->snap_slot.p, D};
@@ -893,7 +895,9 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             k_screen<T, FromResidual<T>><<<grid, 256, 0, st>>>(B, c0, s->frow.p, D, s->ctr.p + C_NRES, B, fb, s->dres.p, B);
             FX_LAUNCHED();
         }
+        s->tstop();
         // 3. sequential resolve
+        s->tstart(2);
         {
             ResolveArgs A;
             A.B = B;
@@ -950,9 +954,11 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             kern<<<1, RS_THREADS, smem, st>>>(A);
             FX_LAUNCHED();
         }
+        s->tstop();
         // 4. cluster-array capacity (final centroids are written for evicted clusters)
         FX_CUDA(cudaMemcpyAsync(s->h_ctr, s->ctr.p, sizeof(int64_t) * C_COUNT, cudaMemcpyDeviceToHost, st));
         FX_CUDA(cudaStreamSynchronize(st));
+        s->tcollect();
         if (s->h_ctr[C_ERR]) throw Error{FX_E_INTERNAL, "resolve: candidate list overflow"};
         int64_t ncl = s->h_ctr[C_NEXT_CID];
         if (ncl > s->cl_cap) {
@@ -965,6 +971,7 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
         // 5. fold
         const int nd = (int)s->h_ctr[C_NDIRTY];
         if (nd > 0) {
+            s->tstart(3);
             k_zero_cn2<<<(unsigned)cdiv(nd, 256), 256, 0, st>>>(s->ctr.p, s->dirty.p, s->s_cn2.p);
             FX_LAUNCHED();
             dim3 grid((unsigned)cdiv(D, 256), (unsigned)nd);
@@ -973,6 +980,7 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
                                             s->s_evicted.p, s->s_cid.p, s->s_size.p, s->s_cn2.p, s->fcent.p,
                                             s->cl_nfeat.p, s->cl_size.p);
             FX_LAUNCHED();
+            s->tstop();
         }
     }
 }

@@ -108,12 +108,22 @@ class Stream:
         _lib.check(self.L.fx_stream_object_results(self.handle, _lib.p32(cl), _lib.pu8(dup), _lib.p32(tk)))
         return cl, dup.astype(bool), tk.reshape(n, k)
 
+    COUNTERS = ("nlive", "next_cid", "dc", "nfree", "nevict_total", "exact", "nsnap", "nres", "ninserted",
+                "nevict_batch", "ndefer", "nod", "last_cid", "ndirty", "err", "fast")
+    PHASES = ("k0_k1a", "screen", "resolve", "fold", "seal", "index", "batches")
+
     def counters(self) -> dict:
-        out = np.zeros(16, np.float64)
-        _lib.check(self.L.fx_stream_timings(self.handle, _lib.pf64(out), 16))
-        names = ["nlive", "next_cid", "dc", "nfree", "nevict_total", "exact", "nsnap", "nres", "ninserted",
-                 "nevict_batch", "ndefer", "nod", "last_cid", "ndirty", "err", "fast"]
-        return dict(zip(names, out.astype(np.int64).tolist()))
+        out = np.zeros(len(self.COUNTERS), np.int64)
+        _lib.check(self.L.fx_stream_counters(self.handle, _lib.p64(out), out.size))
+        return dict(zip(self.COUNTERS, out.tolist()))
+
+    def timings(self) -> dict:
+        out = np.zeros(len(self.PHASES), np.float64)
+        _lib.check(self.L.fx_stream_timings(self.handle, _lib.pf64(out), out.size))
+        return dict(zip(self.PHASES, out.tolist()))
+
+    def cuda_stream(self) -> int:
+        return int(self.L.fx_stream_cuda_stream(self.handle) or 0)
 
 
 def pixel_diff(prev, cur, eps: float) -> bool:
