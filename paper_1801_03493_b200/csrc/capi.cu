@@ -186,13 +186,14 @@ int fx_stream_create(const fx_stream_config *cfg, fx_stream **out) {
             s->S.reserve((size_t)ns * D);
             s->C32.reserve((size_t)ns * D);
             for (auto *b : {&s->s_cid, &s->s_nfeat, &s->s_size, &s->s_snapq, &s->s_seedpos, &s->s_foldpos, &s->s_pend,
-                            &s->s_odcol, &s->s_didx, &s->s_evicted, &s->live, &s->live_pos, &s->free_stack,
+                            &s->s_odcol, &s->s_didx, &s->s_grp, &s->s_evicted, &s->live, &s->live_pos, &s->free_stack,
                             &s->defer_free, &s->snap_slot})
                 b->reserve(ns);
             s->s_drift.reserve(ns);
             s->s_cn2.reserve(ns);
             FX_CUDA(cudaMemsetAsync(s->s_cn2.p, 0, sizeof(float) * ns, s->st));
             FX_CUDA(cudaMemsetAsync(s->s_evicted.p, 0, sizeof(int32_t) * ns, s->st));
+            FX_CUDA(cudaMemsetAsync(s->s_grp.p, 0xff, sizeof(int32_t) * ns, s->st));
             s->ctr.reserve(C_COUNT);
             FX_CUDA(cudaMemsetAsync(s->ctr.p, 0, sizeof(int64_t) * C_COUNT, s->st));
             k_init_free<<<(unsigned)cdiv(ns, 256), 256, 0, s->st>>>(ns, s->free_stack.p);
@@ -203,8 +204,9 @@ int fx_stream_create(const fx_stream_config *cfg, fx_stream **out) {
             s->dres.reserve((size_t)B * B);
             s->dod.reserve((size_t)B * B);
             for (auto *b : {&s->res_col, &s->res_pos, &s->slot_of, &s->pend_rank, &s->evict_slot, &s->evict_cid,
-                            &s->pend_list})
+                            &s->pend_list, &s->sum_slot})
                 b->reserve(B + 1);
+            for (auto *b : {&s->sum_d1, &s->sum_e1, &s->sum_lbr}) b->reserve(B + 1);
             s->dirty.reserve(2 * B + 2);
             s->dirty_off.reserve(2 * B + 3);
             s->prev_sig.reserve(std::max(1, cfg->sig_dim));

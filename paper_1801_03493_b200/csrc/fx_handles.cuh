@@ -71,7 +71,7 @@ struct fx_stream {
     int64_t nslots = 0;
     fx::DevBuf<double> S;      // [nslots*D] exact running sums
     fx::DevBuf<float> C32;     // [nslots*D] fp32 centroid snapshot
-    fx::DevBuf<int32_t> s_cid, s_nfeat, s_size, s_snapq, s_seedpos, s_foldpos, s_pend, s_odcol, s_didx,
+    fx::DevBuf<int32_t> s_cid, s_nfeat, s_size, s_snapq, s_seedpos, s_foldpos, s_pend, s_odcol, s_didx, s_grp,
         s_evicted, live, live_pos, free_stack, defer_free;
     fx::DevBuf<double> s_drift;
     fx::DevBuf<float> s_cn2;   // ||c||^2 of the snapshot centroid (fp32)
@@ -83,7 +83,8 @@ struct fx_stream {
     fx::DevBuf<float> dres;    // [B*B]
     fx::DevBuf<int32_t> res_col, res_pos;
     fx::DevBuf<float> dod;     // [B*B] on-demand columns
-    fx::DevBuf<int32_t> slot_of, pend_rank, evict_slot, evict_cid, dirty, dirty_off, pend_list;
+    fx::DevBuf<int32_t> slot_of, pend_rank, evict_slot, evict_cid, dirty, dirty_off, pend_list, sum_slot;
+    fx::DevBuf<float> sum_d1, sum_e1, sum_lbr;
     // per-cluster results (grow with clusters)
     int64_t cl_cap = 0;
     fx::DevBuf<double> fcent;      // [cl_cap*D] final centroids

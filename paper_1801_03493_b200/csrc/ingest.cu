@@ -267,6 +267,9 @@ struct ResolveArgs {
     int32_t *slot_of, *pend_rank, *evict_slot, *evict_cid, *dirty, *dirty_off, *pend_list;
     int32_t *cluster_of, *mrank, *frank;
     const PwPlan *plan;
+    int32_t *s_grp;
+    const int32_t *sum_slot;
+    const float *sum_d1, *sum_e1, *sum_lbr;
 };
 
 constexpr int RS_THREADS = 512;
@@ -405,24 +408,94 @@ __device__ double exact_dist(const ResolveArgs &A, int b, int slot, const int32_
     return __dsqrt_rn(dadd(0.0, tot));
 }
 
+// Per-object summary of the snapshot screen row: best snapshot slot, its
+// distance and error bound, and min over the other snapshot slots of
+// (d - e).  One warp per object.
+__global__ void k_row_summary(int nA, const int64_t *__restrict__ ctr, const float *__restrict__ dist, int64_t ld,
+                              const float *__restrict__ cn2, const int32_t *__restrict__ snap,
+                              const float *__restrict__ fnorm, int64_t a0, float rel, float absc,
+                              int32_t *__restrict__ sum_slot, float *__restrict__ sum_d1, float *__restrict__ sum_e1,
+                              float *__restrict__ sum_lbr) {
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (w >= nA) return;
+    const int nsnap = (int)ctr[C_NSNAP];
+    const float fn = fnorm[a0 + w];
+    float d1 = INFINITY, e1 = 0.f, lbr = INFINITY;
+    int q1 = -1;
+    for (int q = lane; q < nsnap; q += 32) {
+        const float d = dist[(int64_t)w * ld + q];
+        const float e = rel * d + absc * (sqrtf(cn2[snap[q]]) * 1.00001f + fn) + 1e-30f;
+        if (d < d1) {
+            if (q1 >= 0) lbr = fminf(lbr, d1 - e1);
+            d1 = d;
+            e1 = e;
+            q1 = q;
+        } else {
+            lbr = fminf(lbr, d - e);
+        }
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const float od1 = __shfl_xor_sync(0xffffffffu, d1, o), oe1 = __shfl_xor_sync(0xffffffffu, e1, o);
+        const float olbr = __shfl_xor_sync(0xffffffffu, lbr, o);
+        const int oq1 = __shfl_xor_sync(0xffffffffu, q1, o);
+        const bool take = oq1 >= 0 && (q1 < 0 || od1 < d1 || (od1 == d1 && oq1 < q1));
+        if (take) {
+            lbr = fminf(fminf(lbr, olbr), q1 >= 0 ? d1 - e1 : INFINITY);
+            d1 = od1;
+            e1 = oe1;
+            q1 = oq1;
+        } else {
+            lbr = fminf(fminf(lbr, olbr), oq1 >= 0 ? od1 - oe1 : INFINITY);
+        }
+    }
+    if (lane == 0) {
+        sum_slot[w] = q1 >= 0 ? snap[q1] : -1;
+        sum_d1[w] = d1;
+        sum_e1[w] = e1;
+        sum_lbr[w] = lbr;
+    }
+}
+
+constexpr int RS_MAXGRP = 1024;
+constexpr int RS_WIN0 = 64;
+
+__device__ __forceinline__ double drift_step(double dr, double ub, int nf, double cn) {
+    // ||c_new - c_old|| <= ub / nf in exact arithmetic (c' - c = (f - c)/n');
+    // 8 u64 (|c| + dr + ub) covers the float64 rounding of the sum and of S/n.
+    return dr + ub / nf + 8.0 * 1.1102230246251565e-16 * (cn + dr + ub) + 1e-300;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    int32_t *sh_slot_of = (int32_t *)smem_raw;                            // [B]
-    int *mlist = (int *)(smem_raw + A.B * 4);                            // [B]
-    double *scratch = (double *)(smem_raw + ((A.B * 8 + 15) & ~15));     // pairwise scratch
+    const int B = A.B;
+    double *seg_ub = (double *)smem_raw;                  // [B] UB of the hypothesis
+    int32_t *sh_slot_of = (int32_t *)(seg_ub + B);        // [B]
+    int *mlist = (int *)(sh_slot_of + B);                 // [B]
+    int32_t *seg_key = (int32_t *)(mlist + B);            // [B] hypothesis slot
+    float *seg_ub0 = (float *)(seg_key + B);              // [B] d1 + e1
+    float *seg_lbr = (float *)(seg_ub0 + B);              // [B] min over others of d - e
+    int32_t *seedlist = (int32_t *)(seg_lbr + B);         // [B] in-batch seed slots
+    double *scratch = (double *)(seedlist + B + (B & 1)); // pairwise scratch
     __shared__ Cand red[RS_WARPS];
     __shared__ int cand_list[RS_MAXCAND];
     __shared__ int n_cand;
-    __shared__ int s_L, s_nfree, s_ndefer, s_nevict, s_nod, s_ndirty;
+    __shared__ int s_L, s_nfree, s_ndefer, s_nevict, s_nod, s_ndirty, s_nseeds, s_any_evicted;
     __shared__ long long s_dc, s_exact, s_fast, s_next_cid, s_inserted, s_victim_key;
     __shared__ int s_decision_slot, s_seed, s_need_exact, s_need_evict, s_need_od;
     __shared__ double s_best_d;
     __shared__ int s_best_slot;
     __shared__ float s_ub_used;
+    __shared__ int grp_slot[RS_MAXGRP];
+    __shared__ double grp_drift[RS_MAXGRP];
+    __shared__ int s_ngrp, s_fail;
+    __shared__ double s_md1, s_md2;
+    __shared__ int s_md1_slot;
+    __shared__ double wmd1[RS_WARPS], wmd2[RS_WARPS];
+    __shared__ int wmds[RS_WARPS];
 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const int B = A.B;
     int64_t *ctr = A.ctr;
 
     // ---- batch prologue: recycle last batch's freed slots, reset snapshot fields
@@ -435,6 +508,8 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
         s_nevict = 0;
         s_nod = 0;
         s_ndirty = 0;
+        s_nseeds = 0;
+        s_any_evicted = 0;
         s_dc = ctr[C_DC];
         s_exact = ctr[C_EXACT];
         s_fast = ctr[C_FAST];
@@ -455,7 +530,215 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
     for (int b = tid; b < B; b += blockDim.x) sh_slot_of[b] = -1;
     __syncthreads();
 
-    for (int b = 0; b < B; b++) {
+    int b = 0, win = RS_WIN0;
+    while (b < B) {
+        // =================== parallel segment: speculate every object in
+        // [b, e_end) joins its nearest candidate, verify with bounds, commit
+        // the verified prefix ===================
+        const int e_end = min(B, b + win);
+        const int L = s_L;
+        if (tid == 0) {
+            s_ngrp = 0;
+            s_fail = e_end;
+        }
+        // pass A: hypothesis per object (snapshot summary + in-batch seeds)
+        for (int p = b + tid; p < e_end; p += blockDim.x) {
+            const float fn = A.fnorm[A.c0 + p];
+            int j1 = A.sum_slot[p];
+            float d1 = A.sum_d1[p], e1 = A.sum_e1[p], lbr = A.sum_lbr[p];
+            if (s_any_evicted && (j1 < 0 || A.s_evicted[j1])) {
+                j1 = -1;
+                d1 = INFINITY;
+                lbr = INFINITY;
+                for (int i = 0; i < L; i++) {
+                    const int sl = A.live[i];
+                    const int q = A.s_snapq[sl];
+                    if (q < 0) continue;
+                    const float d = A.dist[(int64_t)p * A.ld + q];
+                    const float e = A.rel * d + A.absc * (sqrtf(A.s_cn2[sl]) * 1.00001f + fn) + 1e-30f;
+                    if (d < d1) {
+                        if (j1 >= 0) lbr = fminf(lbr, d1 - e1);
+                        j1 = sl;
+                        d1 = d;
+                        e1 = e;
+                    } else {
+                        lbr = fminf(lbr, d - e);
+                    }
+                }
+            }
+            for (int k = 0; k < s_nseeds; k++) {
+                const int sl = seedlist[k];
+                if (A.s_evicted[sl]) continue;
+                const int s = A.s_seedpos[sl];
+                const int col = A.res_col[s];
+                const float d = col >= 0 ? A.dres[(int64_t)p * A.ldr + col] : A.dod[(int64_t)A.s_odcol[sl] * B + p];
+                const float e = A.rel * d + A.absc * (A.fnorm[A.c0 + s] + fn) + 1e-30f;
+                if (d < d1) {
+                    if (j1 >= 0) lbr = fminf(lbr, d1 - e1);
+                    j1 = sl;
+                    d1 = d;
+                    e1 = e;
+                } else {
+                    lbr = fminf(lbr, d - e);
+                }
+            }
+            seg_key[p] = (L > 0) ? j1 : -1;
+            seg_ub0[p] = (d1 + e1) * 1.000001f + 1e-30f;
+            seg_lbr[p] = lbr - fabsf(lbr) * 1e-6f - 1e-30f;
+        }
+        __syncthreads();
+        // pass B1: distinct hypothesis slots -> group ids
+        for (int p = b + tid; p < e_end; p += blockDim.x) {
+            const int key = seg_key[p];
+            if (key < 0) continue;
+            if (A.s_grp[key] == -1 && atomicCAS(&A.s_grp[key], -1, -2) == -1) {
+                int g = atomicAdd(&s_ngrp, 1);
+                if (g < RS_MAXGRP) grp_slot[g] = key;
+                A.s_grp[key] = g < RS_MAXGRP ? g : RS_MAXGRP;
+            }
+        }
+        __syncthreads();
+        const int ngrp = min(s_ngrp, RS_MAXGRP);
+        // pass B2: drift recurrence along every group's chain (stream order)
+        for (int g = tid; g < ngrp; g += blockDim.x) {
+            const int sl = grp_slot[g];
+            double dr = A.s_drift[sl];
+            int nf = A.s_nfeat[sl];
+            const double cn = sqrt((double)A.s_cn2[sl]);
+            for (int p = b; p < e_end; p++) {
+                if (seg_key[p] != sl) continue;
+                const double ub = (double)seg_ub0[p] + dr;
+                seg_ub[p] = ub;
+                nf++;
+                dr = drift_step(dr, ub, nf, cn + (double)A.fnorm[A.c0 + p]);
+            }
+            grp_drift[g] = dr;
+        }
+        __syncthreads();
+        // pass C: the two largest end-of-segment drifts over live slots
+        {
+            double m1 = -1.0, m2 = -1.0;
+            int m1s = -1;
+            for (int i = tid; i < L; i += blockDim.x) {
+                const int sl = A.live[i];
+                const int g = A.s_grp[sl];
+                const double d = (g >= 0 && g < RS_MAXGRP) ? grp_drift[g] : A.s_drift[sl];
+                if (d > m1) {
+                    m2 = m1;
+                    m1 = d;
+                    m1s = sl;
+                } else if (d > m2) {
+                    m2 = d;
+                }
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                const double o1 = __shfl_xor_sync(0xffffffffu, m1, o), o2 = __shfl_xor_sync(0xffffffffu, m2, o);
+                const int os = __shfl_xor_sync(0xffffffffu, m1s, o);
+                if (o1 > m1) {
+                    m2 = fmax(m1, o2);
+                    m1 = o1;
+                    m1s = os;
+                } else {
+                    m2 = fmax(m2, o1);
+                }
+            }
+            if (lane == 0) {
+                wmd1[wid] = m1;
+                wmd2[wid] = m2;
+                wmds[wid] = m1s;
+            }
+            __syncthreads();
+            if (tid == 0) {
+                double a1 = wmd1[0], a2 = wmd2[0];
+                int as = wmds[0];
+                for (int w = 1; w < RS_WARPS; w++) {
+                    if (wmd1[w] > a1) {
+                        a2 = fmax(a1, wmd2[w]);
+                        a1 = wmd1[w];
+                        as = wmds[w];
+                    } else {
+                        a2 = fmax(a2, wmd1[w]);
+                    }
+                }
+                s_md1 = a1 < 0 ? 0.0 : a1;
+                s_md2 = a2 < 0 ? 0.0 : a2;
+                s_md1_slot = as;
+                if (s_ngrp > RS_MAXGRP) s_fail = b;  // too many distinct slots: go sequential
+            }
+            __syncthreads();
+        }
+        // pass D: certainty check; first failure
+        for (int p = b + tid; p < e_end; p += blockDim.x) {
+            const int key = seg_key[p];
+            bool ok = key >= 0;
+            if (ok) {
+                const double ub = seg_ub[p];
+                const double md = (key == s_md1_slot) ? s_md2 : s_md1;
+                const double lbo = (double)seg_lbr[p] - md * 1.000001;
+                ok = ub <= A.T && lbo > ub;
+            }
+            if (!ok) atomicMin(&s_fail, p);
+        }
+        __syncthreads();
+        const int f = s_fail;
+        // pass E: commit [b, f) -- same recurrence, applied to the slot state
+        for (int g = tid; g < ngrp; g += blockDim.x) {
+            const int sl = grp_slot[g];
+            double dr = A.s_drift[sl];
+            int nf = A.s_nfeat[sl], sz = A.s_size[sl], pend = A.s_pend[sl];
+            const int pend0 = pend;
+            const int cid = A.s_cid[sl];
+            const double cn = sqrt((double)A.s_cn2[sl]);
+            for (int p = b; p < f; p++) {
+                if (seg_key[p] != sl) continue;
+                const double ub = (double)seg_ub0[p] + dr;
+                const int64_t c = A.c0 + p;
+                const int64_t obj = A.cls_obj[c];
+                A.cluster_of[obj] = cid;
+                A.mrank[obj] = sz;
+                A.frank[obj] = nf;
+                A.pend_rank[p] = pend++;
+                A.slot_of[p] = sl;
+                sh_slot_of[p] = sl;
+                nf++;
+                sz += 1 + A.dup_run[c];
+                dr = drift_step(dr, ub, nf, cn + (double)A.fnorm[c]);
+            }
+            A.s_drift[sl] = dr;
+            A.s_nfeat[sl] = nf;
+            A.s_size[sl] = sz;
+            A.s_pend[sl] = pend;
+            if (pend0 == 0 && pend > 0) {
+                const int di = atomicAdd(&s_ndirty, 1);
+                A.s_didx[sl] = di;
+                A.dirty[di] = sl;
+            }
+            A.s_grp[sl] = -1;
+        }
+        if (s_ngrp > RS_MAXGRP) {
+            __syncthreads();
+            for (int p = b + tid; p < e_end; p += blockDim.x) {
+                const int key = seg_key[p];
+                if (key >= 0 && A.s_grp[key] == RS_MAXGRP) A.s_grp[key] = -1;
+            }
+        }
+        if (tid == 0) {
+            const long long nok = f - b;
+            s_dc += (long long)L * nok;
+            s_fast += nok;
+            s_inserted += nok;
+        }
+        __syncthreads();
+        if (f >= e_end) {
+            b = e_end;
+            win = min(win * 2, B);
+            continue;
+        }
+        win = RS_WIN0;
+        b = f;
+        // =================== sequential exact step for object b ===================
+        {
         const float fn = A.fnorm[A.c0 + b];
         const int L = s_L;
         // ---- candidate scan
@@ -569,10 +852,8 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
                 int nf = rank_f + 1;
                 A.s_nfeat[slot] = nf;
                 A.s_size[slot] = rank_m + 1;
-                double ub = (double)s_ub_used;
-                double dr = A.s_drift[slot];
-                double cn = sqrt((double)A.s_cn2[slot]) + (double)A.fnorm[c];
-                A.s_drift[slot] = dr + ub / nf + 8.0 * 1.1102230246251565e-16 * (cn + dr + ub) + 1e-300;
+                A.s_drift[slot] = drift_step(A.s_drift[slot], (double)s_ub_used, nf,
+                                             sqrt((double)A.s_cn2[slot]) + (double)A.fnorm[c]);
             } else {
                 slot = A.free_stack[--s_nfree];
                 int cid = (int)s_next_cid++;
@@ -587,9 +868,11 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
                 A.s_pend[slot] = 0;
                 A.s_evicted[slot] = 0;
                 A.s_odcol[slot] = -1;
+                A.s_grp[slot] = -1;
                 A.live[s_L] = slot;
                 A.live_pos[slot] = s_L;
                 s_L++;
+                seedlist[s_nseeds++] = slot;
                 rank_m = 0;
                 rank_f = 0;
                 if (A.res_col[b] < 0) {
@@ -660,6 +943,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
                 A.live_pos[last] = pos;
                 s_L--;
                 A.s_evicted[vslot] = 1;
+                s_any_evicted = 1;
                 A.evict_slot[s_nevict] = vslot;
                 A.evict_cid[s_nevict] = vcid;
                 s_nevict++;
@@ -676,6 +960,8 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
             A.s_size[slot] += A.dup_run[A.c0 + b];
         }
         __syncthreads();
+        }
+        b = b + 1;
     }
 
     // ---- epilogue: pending-member CSR for k_fold, snapshot for next batch
@@ -689,9 +975,9 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
         A.dirty_off[s_ndirty] = acc;
     }
     __syncthreads();
-    for (int b = tid; b < B; b += blockDim.x) {
-        const int slot = sh_slot_of[b];
-        A.pend_list[A.dirty_off[A.s_didx[slot]] + A.pend_rank[b]] = b;
+    for (int bb = tid; bb < B; bb += blockDim.x) {
+        const int slot = sh_slot_of[bb];
+        A.pend_list[A.dirty_off[A.s_didx[slot]] + A.pend_rank[bb]] = bb;
     }
     for (int q = tid; q < s_L; q += blockDim.x) A.snap_slot[q] = A.live[q];
     __syncthreads();
@@ -732,20 +1018,50 @@ __global__ void __launch_bounds__(256) k_fold(int D, int64_t c0, const int64_t *
                                               int32_t *__restrict__ cl_nfeat, int32_t *__restrict__ cl_size) {
     const int di = blockIdx.y;
     if (di >= (int)ctr[C_NDIRTY]) return;
+    __shared__ const T *rows[256];
+    __shared__ unsigned char first[256];
     const int slot = dirty[di];
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     const int p0 = dirty_off[di], p1 = dirty_off[di + 1];
     const int fp = s_foldpos[slot], sp = s_seedpos[slot];
     const double n = (double)s_nfeat[slot];
     float c2 = 0.f;
-    if (k < D) {
-        double s = S[(int64_t)slot * D + k];
-        for (int p = p0; p < p1; p++) {
-            int b = pend_list[p];
-            if (b < fp) continue;  // already folded by the resolve's exact path
-            double f = to_d(((const T *)frow[c0 + b])[k]);
-            s = (b == sp) ? f : dadd(s, f);
+    double s = k < D ? S[(int64_t)slot * D + k] : 0.0;
+    for (int cs = p0; cs < p1; cs += 256) {
+        // stage the chunk's row pointers (members already folded by the
+        // resolve's exact path are skipped)
+        const int p = cs + (int)threadIdx.x;
+        const T *r = nullptr;
+        unsigned char fst = 0;
+        if (p < p1) {
+            const int b = pend_list[p];
+            if (b >= fp) {
+                r = (const T *)frow[c0 + b];
+                fst = b == sp;
+            }
         }
+        rows[threadIdx.x] = r;
+        first[threadIdx.x] = fst;
+        __syncthreads();
+        const int nch = min(256, p1 - cs);
+        if (k < D) {
+            for (int i = 0; i < nch; i += 16) {
+                double v[16];
+#pragma unroll
+                for (int j = 0; j < 16; j++) {
+                    const T *rr = (i + j < nch) ? rows[i + j] : nullptr;
+                    v[j] = rr ? to_d(rr[k]) : 0.0;
+                }
+#pragma unroll
+                for (int j = 0; j < 16; j++) {
+                    if (i + j >= nch || !rows[i + j]) continue;
+                    s = first[i + j] ? v[j] : dadd(s, v[j]);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    if (k < D) {
         S[(int64_t)slot * D + k] = s;
         double cen = ddiv(s, n);
         float c32 = (float)cen;
@@ -895,8 +1211,12 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             k_screen<T, FromResidual<T>><<<grid, 256, 0, st>>>(B, c0, s->frow.p, D, s->ctr.p + C_NRES, B, fb, s->dres.p, B);
             FX_LAUNCHED();
         }
+        k_row_summary<<<(unsigned)cdiv((int64_t)B * 32, 256), 256, 0, st>>>(
+            B, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p, s->snap_slot.p, s->fnorm.p, c0, rel, absc, s->sum_slot.p,
+            s->sum_d1.p, s->sum_e1.p, s->sum_lbr.p);
+        FX_LAUNCHED();
         s->tstop();
-        // 3. sequential resolve
+        // 3. resolve (parallel verified segments + exact sequential events)
         s->tstart(2);
         {
             ResolveArgs A;
@@ -947,8 +1267,13 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             A.mrank = s->mrank.p;
             A.frank = s->frank.p;
             A.plan = s->plan.p;
+            A.s_grp = s->s_grp.p;
+            A.sum_slot = s->sum_slot.p;
+            A.sum_d1 = s->sum_d1.p;
+            A.sum_e1 = s->sum_e1.p;
+            A.sum_lbr = s->sum_lbr.p;
             const PwPlan &P = *s->plan_host;
-            size_t smem = ((size_t)(B * 8 + 15) & ~(size_t)15) + sizeof(double) * (P.n_chains + P.n_leaves + P.n_ops + 8);
+            size_t smem = (size_t)B * (8 + 4 * 6) + 16 + sizeof(double) * (P.n_chains + P.n_leaves + P.n_ops + 8);
             auto kern = k_resolve<T>;
             FX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             kern<<<1, RS_THREADS, smem, st>>>(A);
