@@ -326,7 +326,7 @@ __device__ __forceinline__ void slot_bounds(const ResolveArgs &A, int b, float f
 // order), then evaluate sqrt(pairwise_sum(((S/n) - f)^2)) in numpy's order.
 template <typename T>
 __device__ double exact_dist(const ResolveArgs &A, int b, int slot, const int32_t *sh_slot_of, int *mlist,
-                             double *scratch) {
+                             double *scratch, int nfeat = -1) {
     const int D = A.D;
     int fp = A.s_foldpos[slot];
     const int sp = A.s_seedpos[slot];
@@ -358,7 +358,7 @@ __device__ double exact_dist(const ResolveArgs &A, int b, int slot, const int32_
         __syncthreads();
         if (threadIdx.x == 0) A.s_foldpos[slot] = b;
     }
-    const double n = (double)A.s_nfeat[slot];
+    const double n = (double)(nfeat >= 0 ? nfeat : A.s_nfeat[slot]);
     const T *f = (const T *)A.frow[A.c0 + b];
     __syncthreads();
     auto term = [&](int k) {
@@ -477,7 +477,9 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
     float *seg_ub0 = (float *)(seg_key + B);              // [B] d1 + e1
     float *seg_lbr = (float *)(seg_ub0 + B);              // [B] min over others of d - e
     int32_t *seedlist = (int32_t *)(seg_lbr + B);         // [B] in-batch seed slots
-    double *scratch = (double *)(seedlist + B + (B & 1)); // pairwise scratch
+    int32_t *seg_nf = seedlist + B;                       // [B] featured count before p
+    unsigned char *seg_flag = (unsigned char *)(seg_nf + B);  // [B]
+    double *scratch = (double *)(seg_flag + ((B + 15) & ~15));  // pairwise scratch
     __shared__ Cand red[RS_WARPS];
     __shared__ int cand_list[RS_MAXCAND];
     __shared__ int n_cand;
@@ -490,6 +492,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
     __shared__ int grp_slot[RS_MAXGRP];
     __shared__ double grp_drift[RS_MAXGRP];
     __shared__ int s_ngrp, s_fail;
+    (void)0;
     __shared__ double s_md1, s_md2;
     __shared__ int s_md1_slot;
     __shared__ double wmd1[RS_WARPS], wmd2[RS_WARPS];
@@ -599,20 +602,49 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
         }
         __syncthreads();
         const int ngrp = min(s_ngrp, RS_MAXGRP);
-        // pass B2: drift recurrence along every group's chain (stream order)
-        for (int g = tid; g < ngrp; g += blockDim.x) {
+        // pass B2: drift bound along every group's chain.  One warp per group;
+        // the recurrence d' = d (1 + 1/n) + ub0/n + slack is affine in d, so each
+        // 32-slice of the window is an inclusive warp scan of affine maps
+        // (fp32, rounded up: every grouping yields an upper bound).
+        for (int g = wid; g < ngrp; g += RS_WARPS) {
             const int sl = grp_slot[g];
-            double dr = A.s_drift[sl];
+            float dr = __double2float_ru(A.s_drift[sl]);
             int nf = A.s_nfeat[sl];
-            const double cn = sqrt((double)A.s_cn2[sl]);
-            for (int p = b; p < e_end; p++) {
-                if (seg_key[p] != sl) continue;
-                const double ub = (double)seg_ub0[p] + dr;
-                seg_ub[p] = ub;
-                nf++;
-                dr = drift_step(dr, ub, nf, cn + (double)A.fnorm[A.c0 + p]);
+            const float cn = sqrtf(A.s_cn2[sl]) * 1.00001f;
+            for (int p0 = b; p0 < e_end; p0 += 32) {
+                const int p = p0 + lane;
+                const bool match = p < e_end && seg_key[p] == sl;
+                const unsigned mask = __ballot_sync(0xffffffffu, match);
+                if (!mask) continue;
+                const int rk = __popc(mask & ((1u << lane) - 1u));
+                float a = 1.f, c = 0.f, ub0 = 0.f;
+                if (match) {
+                    const int n_after = nf + rk + 1;
+                    ub0 = seg_ub0[p];
+                    const float inv = __frcp_ru((float)n_after);
+                    a = __fadd_ru(__fadd_ru(1.f, inv), 2.5e-7f);
+                    c = __fadd_ru(__fmul_ru(ub0, inv), __fmul_ru(1e-13f, __fadd_ru(cn, ub0)) + 1e-30f);
+                    seg_nf[p] = nf + rk;
+                }
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const float ap = __shfl_up_sync(0xffffffffu, a, o), cp = __shfl_up_sync(0xffffffffu, c, o);
+                    if (lane >= o) {
+                        c = __fmaf_ru(a, cp, c);
+                        a = __fmul_ru(a, ap);
+                    }
+                }
+                float ae = __shfl_up_sync(0xffffffffu, a, 1), ce = __shfl_up_sync(0xffffffffu, c, 1);
+                if (lane == 0) {
+                    ae = 1.f;
+                    ce = 0.f;
+                }
+                if (match) seg_ub[p] = (double)__fadd_ru(ub0, __fmaf_ru(ae, dr, ce));
+                const float a31 = __shfl_sync(0xffffffffu, a, 31), c31 = __shfl_sync(0xffffffffu, c, 31);
+                dr = __fmaf_ru(a31, dr, c31);
+                nf += __popc(mask);
             }
-            grp_drift[g] = dr;
+            if (lane == 0) grp_drift[g] = (double)dr;
         }
         __syncthreads();
         // pass C: the two largest end-of-segment drifts over live slots
@@ -664,59 +696,111 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
                 s_md1 = a1 < 0 ? 0.0 : a1;
                 s_md2 = a2 < 0 ? 0.0 : a2;
                 s_md1_slot = as;
-                if (s_ngrp > RS_MAXGRP) s_fail = b;  // too many distinct slots: go sequential
             }
             __syncthreads();
         }
-        // pass D: certainty check; first failure
+        // pass D: certainty check -> 0 certain, 1 only the T test is open
+        // (confirmable by one exact distance), 2 anything else
+        const bool overflow = s_ngrp > RS_MAXGRP;
         for (int p = b + tid; p < e_end; p += blockDim.x) {
             const int key = seg_key[p];
-            bool ok = key >= 0;
-            if (ok) {
+            unsigned char fl = 2;
+            if (key >= 0 && !overflow) {
                 const double ub = seg_ub[p];
                 const double md = (key == s_md1_slot) ? s_md2 : s_md1;
                 const double lbo = (double)seg_lbr[p] - md * 1.000001;
-                ok = ub <= A.T && lbo > ub;
+                if (lbo > ub) fl = ub <= A.T ? 0 : 1;
             }
-            if (!ok) atomicMin(&s_fail, p);
+            seg_flag[p] = fl;
+            sh_slot_of[p] = key;  // tentative, for materialisation by the exact path
         }
         __syncthreads();
-        const int f = s_fail;
-        // pass E: commit [b, f) -- same recurrence, applied to the slot state
-        for (int g = tid; g < ngrp; g += blockDim.x) {
+        // confirm T-only failures in order with one exact distance each
+        int f = b;
+        while (true) {
+            if (tid == 0) s_fail = e_end;
+            __syncthreads();
+            for (int p = f + tid; p < e_end; p += blockDim.x)
+                if (seg_flag[p]) atomicMin(&s_fail, p);
+            __syncthreads();
+            f = s_fail;
+            if (f >= e_end || seg_flag[f] != 1) break;
+            const double dx = exact_dist<T>(A, f, seg_key[f], sh_slot_of, mlist, scratch, seg_nf[f]);
+            if (tid == 0) s_exact++;
+            if (dx > A.T) break;  // nearest is beyond T: the object seeds (sequential path)
+            f++;
+            __syncthreads();
+        }
+        __syncthreads();
+        for (int p = f + tid; p < e_end; p += blockDim.x) sh_slot_of[p] = -1;
+        // pass E: commit [b, f) -- same maps as pass B2, applied to the slot state
+        for (int g = wid; g < ngrp; g += RS_WARPS) {
             const int sl = grp_slot[g];
-            double dr = A.s_drift[sl];
+            float dr = __double2float_ru(A.s_drift[sl]);
             int nf = A.s_nfeat[sl], sz = A.s_size[sl], pend = A.s_pend[sl];
             const int pend0 = pend;
             const int cid = A.s_cid[sl];
-            const double cn = sqrt((double)A.s_cn2[sl]);
-            for (int p = b; p < f; p++) {
-                if (seg_key[p] != sl) continue;
-                const double ub = (double)seg_ub0[p] + dr;
-                const int64_t c = A.c0 + p;
-                const int64_t obj = A.cls_obj[c];
-                A.cluster_of[obj] = cid;
-                A.mrank[obj] = sz;
-                A.frank[obj] = nf;
-                A.pend_rank[p] = pend++;
-                A.slot_of[p] = sl;
-                sh_slot_of[p] = sl;
-                nf++;
-                sz += 1 + A.dup_run[c];
-                dr = drift_step(dr, ub, nf, cn + (double)A.fnorm[c]);
+            const float cn = sqrtf(A.s_cn2[sl]) * 1.00001f;
+            for (int p0 = b; p0 < f; p0 += 32) {
+                const int p = p0 + lane;
+                const bool match = p < f && seg_key[p] == sl;
+                const unsigned mask = __ballot_sync(0xffffffffu, match);
+                if (!mask) continue;
+                const int rk = __popc(mask & ((1u << lane) - 1u));
+                float a = 1.f, c = 0.f;
+                int w = 0;
+                int64_t cc = 0;
+                if (match) {
+                    cc = A.c0 + p;
+                    const float ub0 = seg_ub0[p];
+                    const float inv = __frcp_ru((float)(nf + rk + 1));
+                    a = __fadd_ru(__fadd_ru(1.f, inv), 2.5e-7f);
+                    c = __fadd_ru(__fmul_ru(ub0, inv), __fmul_ru(1e-13f, __fadd_ru(cn, ub0)) + 1e-30f);
+                    w = 1 + A.dup_run[cc];
+                }
+                int wsum = w;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const float ap = __shfl_up_sync(0xffffffffu, a, o), cp = __shfl_up_sync(0xffffffffu, c, o);
+                    const int wp = __shfl_up_sync(0xffffffffu, wsum, o);
+                    if (lane >= o) {
+                        c = __fmaf_ru(a, cp, c);
+                        a = __fmul_ru(a, ap);
+                        wsum += wp;
+                    }
+                }
+                if (match) {
+                    const int64_t obj = A.cls_obj[cc];
+                    A.cluster_of[obj] = cid;
+                    A.mrank[obj] = sz + wsum - w;
+                    A.frank[obj] = nf + rk;
+                    A.pend_rank[p] = pend + rk;
+                    A.slot_of[p] = sl;
+                    sh_slot_of[p] = sl;
+                }
+                const float a31 = __shfl_sync(0xffffffffu, a, 31), c31 = __shfl_sync(0xffffffffu, c, 31);
+                dr = __fmaf_ru(a31, dr, c31);
+                const int cnt = __popc(mask);
+                nf += cnt;
+                pend += cnt;
+                sz += __shfl_sync(0xffffffffu, wsum, 31);
             }
-            A.s_drift[sl] = dr;
-            A.s_nfeat[sl] = nf;
-            A.s_size[sl] = sz;
-            A.s_pend[sl] = pend;
-            if (pend0 == 0 && pend > 0) {
-                const int di = atomicAdd(&s_ndirty, 1);
-                A.s_didx[sl] = di;
-                A.dirty[di] = sl;
+            if (lane == 0) {
+                if (pend > pend0) {
+                    A.s_drift[sl] = (double)dr;
+                    A.s_nfeat[sl] = nf;
+                    A.s_size[sl] = sz;
+                    A.s_pend[sl] = pend;
+                    if (pend0 == 0) {
+                        const int di = atomicAdd(&s_ndirty, 1);
+                        A.s_didx[sl] = di;
+                        A.dirty[di] = sl;
+                    }
+                }
+                A.s_grp[sl] = -1;
             }
-            A.s_grp[sl] = -1;
         }
-        if (s_ngrp > RS_MAXGRP) {
+        if (overflow) {
             __syncthreads();
             for (int p = b + tid; p < e_end; p += blockDim.x) {
                 const int key = seg_key[p];
@@ -735,7 +819,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
             win = min(win * 2, B);
             continue;
         }
-        win = RS_WIN0;
+        win = max(RS_WIN0, win / 4);
         b = f;
         // =================== sequential exact step for object b ===================
         {
@@ -1040,22 +1124,21 @@ __global__ void __launch_bounds__(256) k_fold(int D, int64_t c0, const int64_t *
                 fst = b == sp;
             }
         }
-        rows[threadIdx.x] = r;
-        first[threadIdx.x] = fst;
+        // padded / skipped members point at a valid row and are masked (flag 2)
+        rows[threadIdx.x] = r ? r : (const T *)frow[c0];
+        first[threadIdx.x] = r ? fst : 2;
         __syncthreads();
         const int nch = min(256, p1 - cs);
         if (k < D) {
             for (int i = 0; i < nch; i += 16) {
                 double v[16];
 #pragma unroll
-                for (int j = 0; j < 16; j++) {
-                    const T *rr = (i + j < nch) ? rows[i + j] : nullptr;
-                    v[j] = rr ? to_d(rr[k]) : 0.0;
-                }
+                for (int j = 0; j < 16; j++) v[j] = to_d(__ldg(rows[(i + j) & 255] + k));
 #pragma unroll
                 for (int j = 0; j < 16; j++) {
-                    if (i + j >= nch || !rows[i + j]) continue;
-                    s = first[i + j] ? v[j] : dadd(s, v[j]);
+                    const unsigned char fl = (i + j < nch) ? first[i + j] : 2;
+                    const double add = dadd(s, v[j]);
+                    s = fl == 1 ? v[j] : (fl == 0 ? add : s);
                 }
             }
         }
@@ -1273,7 +1356,7 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             A.sum_e1 = s->sum_e1.p;
             A.sum_lbr = s->sum_lbr.p;
             const PwPlan &P = *s->plan_host;
-            size_t smem = (size_t)B * (8 + 4 * 6) + 16 + sizeof(double) * (P.n_chains + P.n_leaves + P.n_ops + 8);
+            size_t smem = (size_t)B * (8 + 4 * 7) + ((B + 15) & ~15) + 16 + sizeof(double) * (P.n_chains + P.n_leaves + P.n_ops + 8);
             auto kern = k_resolve<T>;
             FX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             kern<<<1, RS_THREADS, smem, st>>>(A);
