@@ -285,7 +285,9 @@ def main():
             "gpu_launches": int(launches),
             "ingest": {"clusters": rep.clusters_emitted, "classified": rep.objects_classified,
                        "distance_computations": rep.distance_computations, "exact_rechecks": rep.exact_rechecks,
-                       "fast_decisions": counters["fast"]},
+                       "fast_decisions": counters["fast"],
+                       "resolve_profile": {k: counters[k] for k in counters if k.startswith("cyc_")
+                                           or k in ("windows", "seq_steps")}},
         }
         print(json.dumps(line))
     if ws > 1:

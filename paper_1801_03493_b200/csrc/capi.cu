@@ -113,6 +113,9 @@ void fx_stream::tcollect() {
 }
 
 fx_stream::~fx_stream() {
+    if (h_ctr_ring) cudaFreeHost(h_ctr_ring);
+    for (auto &e : ring_ev)
+        if (e) cudaEventDestroy(e);
     for (auto &t : timers) {
         if (t.a) cudaEventDestroy(t.a);
         if (t.b) cudaEventDestroy(t.b);
@@ -194,6 +197,10 @@ int fx_stream_create(const fx_stream_config *cfg, fx_stream **out) {
             FX_CUDA(cudaMemsetAsync(s->s_cn2.p, 0, sizeof(float) * ns, s->st));
             FX_CUDA(cudaMemsetAsync(s->s_evicted.p, 0, sizeof(int32_t) * ns, s->st));
             FX_CUDA(cudaMemsetAsync(s->s_grp.p, 0xff, sizeof(int32_t) * ns, s->st));
+            FX_CUDA(cudaMallocHost(&s->h_ctr_ring, sizeof(int64_t) * 3 * C_COUNT));
+            for (int i = 0; i < 3; i++) FX_CUDA(cudaEventCreateWithFlags(&s->ring_ev[i], cudaEventDisableTiming));
+            s->prof.reserve(8);
+            FX_CUDA(cudaMemsetAsync(s->prof.p, 0, sizeof(int64_t) * 8, s->st));
             s->ctr.reserve(C_COUNT);
             FX_CUDA(cudaMemsetAsync(s->ctr.p, 0, sizeof(int64_t) * C_COUNT, s->st));
             k_init_free<<<(unsigned)cdiv(ns, 256), 256, 0, s->st>>>(ns, s->free_stack.p);
@@ -430,6 +437,7 @@ int fx_finalize(fx_stream *s, fx_index **out, fx_ingest_report *rep) {
         const int D = s->cfg.dim;
         FX_CUDA(cudaMemcpyAsync(s->h_ctr, s->ctr.p, sizeof(int64_t) * C_COUNT, cudaMemcpyDeviceToHost, st));
         FX_CUDA(cudaStreamSynchronize(st));
+        if (s->h_ctr[C_ERR]) throw Error{FX_E_INTERNAL, "resolve: candidate list overflow"};
         const int64_t C = s->h_ctr[C_NEXT_CID], n = s->n_seen, nc = s->n_cls;
         if (C > s->cl_cap) {
             s->fcent.grow((size_t)C * D, (size_t)s->cl_cap * D, st);
@@ -542,6 +550,11 @@ int fx_stream_counters(fx_stream *s, int64_t *out, int n) {
         FX_CUDA(cudaMemcpyAsync(s->h_ctr, s->ctr.p, sizeof(int64_t) * C_COUNT, cudaMemcpyDeviceToHost, s->st));
         FX_CUDA(cudaStreamSynchronize(s->st));
         for (int i = 0; i < n && i < C_COUNT; i++) out[i] = s->h_ctr[i];
+        if (n > C_COUNT) {
+            int64_t pr[8];
+            FX_CUDA(cudaMemcpy(pr, s->prof.p, sizeof(pr), cudaMemcpyDeviceToHost));
+            for (int i = C_COUNT; i < n && i < C_COUNT + 8; i++) out[i] = pr[i - C_COUNT];
+        }
     })
 }
 

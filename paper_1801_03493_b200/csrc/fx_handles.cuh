@@ -76,6 +76,7 @@ struct fx_stream {
     fx::DevBuf<double> s_drift;
     fx::DevBuf<float> s_cn2;   // ||c||^2 of the snapshot centroid (fp32)
     fx::DevBuf<int64_t> ctr;
+    fx::DevBuf<int64_t> prof;  // resolve cycle counters (diagnostics)
     fx::DevBuf<int32_t> snap_slot;  // [nslots]
     // per-batch scratch
     fx::DevBuf<float> dist;    // [B*ld]
@@ -90,6 +91,9 @@ struct fx_stream {
     fx::DevBuf<double> fcent;      // [cl_cap*D] final centroids
     fx::DevBuf<int32_t> cl_nfeat, cl_size;
     int64_t h_ctr[fx::C_COUNT] = {0};
+    int64_t *h_ctr_ring = nullptr;  // pinned [3][C_COUNT], async per-batch readback
+    cudaEvent_t ring_ev[3] = {nullptr, nullptr, nullptr};
+    int64_t batch_no = 0;
 
     fx::PwPlan *plan_host = nullptr;
     fx::DevBuf<fx::PwPlan> plan;

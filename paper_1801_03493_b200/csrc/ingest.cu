@@ -242,7 +242,7 @@ __global__ void k_residuals(int nA, const int64_t *__restrict__ ctr, const float
 // ---------------------------------------------------------------------------
 
 struct ResolveArgs {
-    int B;
+    int B, Bcap;
     int64_t c0;
     int D;
     double T;
@@ -268,6 +268,7 @@ struct ResolveArgs {
     int32_t *cluster_of, *mrank, *frank;
     const PwPlan *plan;
     int32_t *s_grp;
+    long long *prof;  // [8] cycles: A, B1B2, CD, confirm, E, seq; [6] windows, [7] seq steps
     const int32_t *sum_slot;
     const float *sum_d1, *sum_e1, *sum_lbr;
 };
@@ -470,16 +471,17 @@ template <typename T>
 __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int B = A.B;
+    const int BC = A.Bcap;  // layout by capacity (multiple of 64): every array stays aligned
     double *seg_ub = (double *)smem_raw;                  // [B] UB of the hypothesis
-    int32_t *sh_slot_of = (int32_t *)(seg_ub + B);        // [B]
-    int *mlist = (int *)(sh_slot_of + B);                 // [B]
-    int32_t *seg_key = (int32_t *)(mlist + B);            // [B] hypothesis slot
-    float *seg_ub0 = (float *)(seg_key + B);              // [B] d1 + e1
-    float *seg_lbr = (float *)(seg_ub0 + B);              // [B] min over others of d - e
-    int32_t *seedlist = (int32_t *)(seg_lbr + B);         // [B] in-batch seed slots
-    int32_t *seg_nf = seedlist + B;                       // [B] featured count before p
-    unsigned char *seg_flag = (unsigned char *)(seg_nf + B);  // [B]
-    double *scratch = (double *)(seg_flag + ((B + 15) & ~15));  // pairwise scratch
+    int32_t *sh_slot_of = (int32_t *)(seg_ub + BC);        // [B]
+    int *mlist = (int *)(sh_slot_of + BC);                 // [B]
+    int32_t *seg_key = (int32_t *)(mlist + BC);            // [B] hypothesis slot
+    float *seg_ub0 = (float *)(seg_key + BC);              // [B] d1 + e1
+    float *seg_lbr = (float *)(seg_ub0 + BC);              // [B] min over others of d - e
+    int32_t *seedlist = (int32_t *)(seg_lbr + BC);         // [B] in-batch seed slots
+    int32_t *seg_nf = seedlist + BC;                       // [B] featured count before p
+    unsigned char *seg_flag = (unsigned char *)(seg_nf + BC);  // [B]
+    double *scratch = (double *)(seg_flag + BC);  // pairwise scratch
     __shared__ Cand red[RS_WARPS];
     __shared__ int cand_list[RS_MAXCAND];
     __shared__ int n_cand;
@@ -540,9 +542,11 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
         // the verified prefix ===================
         const int e_end = min(B, b + win);
         const int L = s_L;
+        long long t0 = clock64();
         if (tid == 0) {
             s_ngrp = 0;
             s_fail = e_end;
+            A.prof[6]++;
         }
         // pass A: hypothesis per object (snapshot summary + in-batch seeds)
         for (int p = b + tid; p < e_end; p += blockDim.x) {
@@ -590,6 +594,8 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
             seg_lbr[p] = lbr - fabsf(lbr) * 1e-6f - 1e-30f;
         }
         __syncthreads();
+        long long t1 = clock64();
+        if (tid == 0) A.prof[0] += t1 - t0;
         // pass B1: distinct hypothesis slots -> group ids
         for (int p = b + tid; p < e_end; p += blockDim.x) {
             const int key = seg_key[p];
@@ -647,6 +653,8 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
             if (lane == 0) grp_drift[g] = (double)dr;
         }
         __syncthreads();
+        long long t2 = clock64();
+        if (tid == 0) A.prof[1] += t2 - t1;
         // pass C: the two largest end-of-segment drifts over live slots
         {
             double m1 = -1.0, m2 = -1.0;
@@ -715,6 +723,8 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
             sh_slot_of[p] = key;  // tentative, for materialisation by the exact path
         }
         __syncthreads();
+        long long t3 = clock64();
+        if (tid == 0) A.prof[2] += t3 - t2;
         // confirm T-only failures in order with one exact distance each
         int f = b;
         while (true) {
@@ -733,6 +743,8 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
         }
         __syncthreads();
         for (int p = f + tid; p < e_end; p += blockDim.x) sh_slot_of[p] = -1;
+        long long t4 = clock64();
+        if (tid == 0) A.prof[3] += t4 - t3;
         // pass E: commit [b, f) -- same maps as pass B2, applied to the slot state
         for (int g = wid; g < ngrp; g += RS_WARPS) {
             const int sl = grp_slot[g];
@@ -814,11 +826,13 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
             s_inserted += nok;
         }
         __syncthreads();
+        if (tid == 0) A.prof[4] += clock64() - t4;
         if (f >= e_end) {
             b = e_end;
             win = min(win * 2, B);
             continue;
         }
+        long long t5 = clock64();
         win = max(RS_WIN0, win / 4);
         b = f;
         // =================== sequential exact step for object b ===================
@@ -1045,6 +1059,10 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
         }
         __syncthreads();
         }
+        if (tid == 0) {
+            A.prof[5] += clock64() - t5;
+            A.prof[7]++;
+        }
         b = b + 1;
     }
 
@@ -1100,10 +1118,11 @@ __global__ void __launch_bounds__(256) k_fold(int D, int64_t c0, const int64_t *
                                               const int32_t *__restrict__ s_cid, const int32_t *__restrict__ s_size,
                                               float *__restrict__ s_cn2, double *__restrict__ fcent,
                                               int32_t *__restrict__ cl_nfeat, int32_t *__restrict__ cl_size) {
-    const int di = blockIdx.y;
-    if (di >= (int)ctr[C_NDIRTY]) return;
     __shared__ const T *rows[256];
     __shared__ unsigned char first[256];
+    __shared__ float red[8];
+    const int nd = (int)ctr[C_NDIRTY];
+    for (int di = blockIdx.y; di < nd; di += gridDim.y) {
     const int slot = dirty[di];
     const int k = blockIdx.x * blockDim.x + threadIdx.x;
     const int p0 = dirty_off[di], p1 = dirty_off[di + 1];
@@ -1154,7 +1173,6 @@ __global__ void __launch_bounds__(256) k_fold(int D, int64_t c0, const int64_t *
     }
     // ||c||^2 partial
     c2 = warp_sum(c2);
-    __shared__ float red[8];
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c2;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1166,9 +1184,12 @@ __global__ void __launch_bounds__(256) k_fold(int D, int64_t c0, const int64_t *
             cl_size[s_cid[slot]] = s_size[slot];
         }
     }
+    __syncthreads();
+    }
 }
 
 __global__ void k_zero_cn2(const int64_t *__restrict__ ctr, const int32_t *__restrict__ dirty, float *__restrict__ s_cn2) {
+    // (grid sized for the maximum dirty count; the device count bounds it)
     int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < (int)ctr[C_NDIRTY]) s_cn2[dirty[i]] = 0.f;
 }
@@ -1304,6 +1325,7 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
         {
             ResolveArgs A;
             A.B = B;
+            A.Bcap = s->B;
             A.c0 = c0;
             A.D = D;
             A.T = s->cfg.t;
@@ -1351,44 +1373,60 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             A.frank = s->frank.p;
             A.plan = s->plan.p;
             A.s_grp = s->s_grp.p;
+            A.prof = (long long *)s->prof.p;
             A.sum_slot = s->sum_slot.p;
             A.sum_d1 = s->sum_d1.p;
             A.sum_e1 = s->sum_e1.p;
             A.sum_lbr = s->sum_lbr.p;
             const PwPlan &P = *s->plan_host;
-            size_t smem = (size_t)B * (8 + 4 * 7) + ((B + 15) & ~15) + 16 + sizeof(double) * (P.n_chains + P.n_leaves + P.n_ops + 8);
+            size_t smem = (size_t)s->B * (8 + 4 * 7 + 1) + 16 + sizeof(double) * (P.n_chains + P.n_leaves + P.n_ops + 8);
             auto kern = k_resolve<T>;
             FX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             kern<<<1, RS_THREADS, smem, st>>>(A);
             FX_LAUNCHED();
         }
         s->tstop();
-        // 4. cluster-array capacity (final centroids are written for evicted clusters)
-        FX_CUDA(cudaMemcpyAsync(s->h_ctr, s->ctr.p, sizeof(int64_t) * C_COUNT, cudaMemcpyDeviceToHost, st));
-        FX_CUDA(cudaStreamSynchronize(st));
-        s->tcollect();
-        if (s->h_ctr[C_ERR]) throw Error{FX_E_INTERNAL, "resolve: candidate list overflow"};
-        int64_t ncl = s->h_ctr[C_NEXT_CID];
-        if (ncl > s->cl_cap) {
-            int64_t cap = std::max<int64_t>(ncl, s->cl_cap * 2);
-            s->fcent.grow((size_t)cap * D, (size_t)s->cl_cap * D, st);
-            s->cl_nfeat.grow(cap, s->cl_cap, st);
-            s->cl_size.grow(cap, s->cl_cap, st);
-            s->cl_cap = cap;
+        // 4. cluster-array capacity for final centroids of evicted clusters,
+        //    without a per-batch host sync: each batch creates <= B clusters, so
+        //    the count read back (asynchronously) two batches ago + 3B bounds it.
+        {
+            const int slot_k = (int)(s->batch_no % 3);
+            FX_CUDA(cudaMemcpyAsync(s->h_ctr_ring + slot_k * C_COUNT, s->ctr.p, sizeof(int64_t) * C_COUNT,
+                                    cudaMemcpyDeviceToHost, st));
+            FX_CUDA(cudaEventRecord(s->ring_ev[slot_k], st));
+            int64_t known = 0;
+            if (s->batch_no >= 2) {
+                const int slot_old = (int)((s->batch_no - 2) % 3);
+                FX_CUDA(cudaEventSynchronize(s->ring_ev[slot_old]));
+                known = s->h_ctr_ring[slot_old * C_COUNT + C_NEXT_CID];
+            }
+            s->batch_no++;
+            const int64_t need = known + 3 * (int64_t)s->B;
+            if (need > s->cl_cap) {
+                FX_CUDA(cudaStreamSynchronize(st));
+                int64_t cap = std::max<int64_t>(need, s->cl_cap * 2);
+                s->fcent.grow((size_t)cap * D, (size_t)s->cl_cap * D, st);
+                s->cl_nfeat.grow(cap, s->cl_cap, st);
+                s->cl_size.grow(cap, s->cl_cap, st);
+                s->cl_cap = cap;
+            }
         }
-        // 5. fold
-        const int nd = (int)s->h_ctr[C_NDIRTY];
-        if (nd > 0) {
+        // 5. fold (persistent grid over the batch's dirty slots)
+        {
             s->tstart(3);
-            k_zero_cn2<<<(unsigned)cdiv(nd, 256), 256, 0, st>>>(s->ctr.p, s->dirty.p, s->s_cn2.p);
+            k_zero_cn2<<<(unsigned)cdiv(2 * s->B + 2, 256), 256, 0, st>>>(s->ctr.p, s->dirty.p, s->s_cn2.p);
             FX_LAUNCHED();
-            dim3 grid((unsigned)cdiv(D, 256), (unsigned)nd);
+            dim3 grid((unsigned)cdiv(D, 256), (unsigned)std::min<int64_t>(2 * (int64_t)B + 1, 1024));
             k_fold<T><<<grid, 256, 0, st>>>(D, c0, s->ctr.p, s->dirty.p, s->dirty_off.p, s->pend_list.p, s->frow.p,
                                             s->S.p, s->C32.p, s->s_nfeat.p, s->s_foldpos.p, s->s_seedpos.p,
                                             s->s_evicted.p, s->s_cid.p, s->s_size.p, s->s_cn2.p, s->fcent.p,
                                             s->cl_nfeat.p, s->cl_size.p);
             FX_LAUNCHED();
             s->tstop();
+        }
+        if (s->pending.size() > 64) {
+            FX_CUDA(cudaStreamSynchronize(st));
+            s->tcollect();
         }
     }
 }

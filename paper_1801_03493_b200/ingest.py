@@ -109,7 +109,8 @@ class Stream:
         return cl, dup.astype(bool), tk.reshape(n, k)
 
     COUNTERS = ("nlive", "next_cid", "dc", "nfree", "nevict_total", "exact", "nsnap", "nres", "ninserted",
-                "nevict_batch", "ndefer", "nod", "last_cid", "ndirty", "err", "fast")
+                "nevict_batch", "ndefer", "nod", "last_cid", "ndirty", "err", "fast",
+                "cyc_passA", "cyc_passB", "cyc_passCD", "cyc_confirm", "cyc_passE", "cyc_seq", "windows", "seq_steps")
     PHASES = ("k0_k1a", "screen", "resolve", "fold", "seal", "index", "batches")
 
     def counters(self) -> dict:
