@@ -181,10 +181,18 @@ def main():
         s.set_rank_model(prof, 0)
         return s
 
+    host_split = {"ingest_call_ms": 0.0, "finalize_call_ms": 0.0}
+
     def step(s):
+        t0 = time.perf_counter()
         s.ingest_device(W["n"], data.oids.data_ptr(), data.fids.data_ptr(), data.sigs.data_ptr(),
                         data.feats.data_ptr(), data.true_class.data_ptr())
-        return s.finalize()
+        t1 = time.perf_counter()
+        out = s.finalize()
+        t2 = time.perf_counter()
+        host_split["ingest_call_ms"] += (t1 - t0) * 1e3
+        host_split["finalize_call_ms"] += (t2 - t1) * 1e3
+        return out
 
     # warm-up
     for _ in range(args.warmup):
@@ -206,6 +214,7 @@ def main():
         ev1.record(torch.cuda.ExternalStream(streams[-1].cuda_stream()))
         torch.cuda.synchronize()
     launches = L.fx_kernel_launches() - launches0
+    host_split = {k: v / args.steps for k, v in host_split.items()}
     t_ms = ev0.elapsed_time(ev1)
     if ws > 1:
         tt = torch.tensor([t_ms], device="cuda")
@@ -236,7 +245,8 @@ def main():
     roofline = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
                 "launches_per_step": int(nb) if dom in ("screen", "resolve", "fold") else 1,
-                "phase_ms_per_step": {k: v for k, v in phases.items() if k != "batches"}}
+                "phase_ms_per_step": {k: v for k, v in phases.items() if k != "batches"},
+                "host_wall_ms_per_step": host_split}
 
     # end-to-end through the host-buffer C ABI
     e2e = None

@@ -21,6 +21,8 @@
 // the batch's members to the float64 sums in order and refreshes the FP32
 // snapshot.  Seal (representatives) is deferred to finalize, exactly as the
 // reference's frozen-at-eviction centroids allow.
+#include <climits>
+
 #include "fx_handles.cuh"
 
 namespace fx {
@@ -480,8 +482,10 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
     float *seg_lbr = (float *)(seg_ub0 + BC);              // [B] min over others of d - e
     int32_t *seedlist = (int32_t *)(seg_lbr + BC);         // [B] in-batch seed slots
     int32_t *seg_nf = seedlist + BC;                       // [B] featured count before p
-    unsigned char *seg_flag = (unsigned char *)(seg_nf + BC);  // [B]
-    double *scratch = (double *)(seg_flag + BC);  // pairwise scratch
+    int32_t *glist = seg_nf + BC;                         // [B] group-ordered positions
+    short *seg_grp = (short *)(glist + BC);               // [B]
+    unsigned char *seg_flag = (unsigned char *)(seg_grp + BC);  // [B]
+    double *scratch = (double *)(seg_flag + BC);          // pairwise scratch
     __shared__ Cand red[RS_WARPS];
     __shared__ int cand_list[RS_MAXCAND];
     __shared__ int n_cand;
@@ -492,6 +496,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
     __shared__ int s_best_slot;
     __shared__ float s_ub_used;
     __shared__ int grp_slot[RS_MAXGRP];
+    __shared__ int grp_cnt[RS_MAXGRP], grp_off[RS_MAXGRP];
     __shared__ double grp_drift[RS_MAXGRP];
     __shared__ int s_ngrp, s_fail;
     (void)0;
@@ -549,6 +554,14 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
             A.prof[6]++;
         }
         // pass A: hypothesis per object (snapshot summary + in-batch seeds)
+        if (s_nseeds == 0 && !s_any_evicted) {
+            for (int p = b + tid; p < e_end; p += blockDim.x) {
+                const float d1 = A.sum_d1[p], e1 = A.sum_e1[p], lbr = A.sum_lbr[p];
+                seg_key[p] = (L > 0) ? A.sum_slot[p] : -1;
+                seg_ub0[p] = (d1 + e1) * 1.000001f + 1e-30f;
+                seg_lbr[p] = lbr - fabsf(lbr) * 1e-6f - 1e-30f;
+            }
+        } else
         for (int p = b + tid; p < e_end; p += blockDim.x) {
             const float fn = A.fnorm[A.c0 + p];
             int j1 = A.sum_slot[p];
@@ -593,6 +606,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
             seg_ub0[p] = (d1 + e1) * 1.000001f + 1e-30f;
             seg_lbr[p] = lbr - fabsf(lbr) * 1e-6f - 1e-30f;
         }
+        for (int g = tid; g < RS_MAXGRP; g += blockDim.x) grp_cnt[g] = 0;
         __syncthreads();
         long long t1 = clock64();
         if (tid == 0) A.prof[0] += t1 - t0;
@@ -608,29 +622,75 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
         }
         __syncthreads();
         const int ngrp = min(s_ngrp, RS_MAXGRP);
-        // pass B2: drift bound along every group's chain.  One warp per group;
-        // the recurrence d' = d (1 + 1/n) + ub0/n + slack is affine in d, so each
-        // 32-slice of the window is an inclusive warp scan of affine maps
-        // (fp32, rounded up: every grouping yields an upper bound).
+        const bool overflow = s_ngrp > RS_MAXGRP;
+        for (int p = b + tid; p < e_end; p += blockDim.x) {
+            const int key = seg_key[p];
+            const int g = key >= 0 ? A.s_grp[key] : -1;
+            seg_grp[p] = (short)((g >= 0 && g < RS_MAXGRP) ? g : -1);
+        }
+        __syncthreads();
+        // stable rank of every object inside its group (warp 0, 32-slices in order)
+        if (wid == 0 && !overflow) {
+            for (int p0 = b; p0 < e_end; p0 += 32) {
+                const int p = p0 + lane;
+                const int g = p < e_end ? seg_grp[p] : -1;
+                const unsigned act = __ballot_sync(0xffffffffu, g >= 0);
+                unsigned peers = 0;
+                int r = 0;
+                if (g >= 0) {
+                    peers = __match_any_sync(act, g);
+                    r = grp_cnt[g] + __popc(peers & ((1u << lane) - 1u));
+                    seg_nf[p] = r;
+                }
+                __syncwarp();
+                if (g >= 0 && (peers & ((1u << lane) - 1u)) == 0) grp_cnt[g] += __popc(peers);
+                __syncwarp();
+            }
+            // exclusive prefix over groups
+            int run = 0;
+            for (int g0 = 0; g0 < ngrp; g0 += 32) {
+                const int g = g0 + lane;
+                const int c = g < ngrp ? grp_cnt[g] : 0;
+                int x = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= o) x += y;
+                }
+                if (g < ngrp) grp_off[g] = run + x - c;
+                run += __shfl_sync(0xffffffffu, x, 31);
+            }
+        }
+        __syncthreads();
+        if (!overflow)
+            for (int p = b + tid; p < e_end; p += blockDim.x) {
+                const int g = seg_grp[p];
+                if (g >= 0) glist[grp_off[g] + seg_nf[p]] = p;
+            }
+        __syncthreads();
+        // pass B2: drift bound along every group's chain.  One warp per group
+        // over its contiguous, stream-ordered member list; the recurrence
+        // d' = d (1 + 1/n) + ub0/n + slack is affine in d, so each 32-slice is an
+        // inclusive warp scan of affine maps (fp32, rounded up: every grouping
+        // yields an upper bound).
+        if (!overflow)
         for (int g = wid; g < ngrp; g += RS_WARPS) {
             const int sl = grp_slot[g];
             float dr = __double2float_ru(A.s_drift[sl]);
-            int nf = A.s_nfeat[sl];
+            const int nf0 = A.s_nfeat[sl];
             const float cn = sqrtf(A.s_cn2[sl]) * 1.00001f;
-            for (int p0 = b; p0 < e_end; p0 += 32) {
-                const int p = p0 + lane;
-                const bool match = p < e_end && seg_key[p] == sl;
-                const unsigned mask = __ballot_sync(0xffffffffu, match);
-                if (!mask) continue;
-                const int rk = __popc(mask & ((1u << lane) - 1u));
+            const int off = grp_off[g], cnt = grp_cnt[g];
+            for (int i0 = 0; i0 < cnt; i0 += 32) {
+                const int i = i0 + lane;
+                const bool match = i < cnt;
+                const int p = match ? glist[off + i] : 0;
                 float a = 1.f, c = 0.f, ub0 = 0.f;
                 if (match) {
-                    const int n_after = nf + rk + 1;
                     ub0 = seg_ub0[p];
-                    const float inv = __frcp_ru((float)n_after);
+                    const float inv = __frcp_ru((float)(nf0 + i + 1));
                     a = __fadd_ru(__fadd_ru(1.f, inv), 2.5e-7f);
                     c = __fadd_ru(__fmul_ru(ub0, inv), __fmul_ru(1e-13f, __fadd_ru(cn, ub0)) + 1e-30f);
-                    seg_nf[p] = nf + rk;
+                    seg_nf[p] = nf0 + i;
                 }
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
@@ -648,7 +708,6 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
                 if (match) seg_ub[p] = (double)__fadd_ru(ub0, __fmaf_ru(ae, dr, ce));
                 const float a31 = __shfl_sync(0xffffffffu, a, 31), c31 = __shfl_sync(0xffffffffu, c, 31);
                 dr = __fmaf_ru(a31, dr, c31);
-                nf += __popc(mask);
             }
             if (lane == 0) grp_drift[g] = (double)dr;
         }
@@ -709,7 +768,6 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
         }
         // pass D: certainty check -> 0 certain, 1 only the T test is open
         // (confirmable by one exact distance), 2 anything else
-        const bool overflow = s_ngrp > RS_MAXGRP;
         for (int p = b + tid; p < e_end; p += blockDim.x) {
             const int key = seg_key[p];
             unsigned char fl = 2;
@@ -749,23 +807,25 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
         for (int g = wid; g < ngrp; g += RS_WARPS) {
             const int sl = grp_slot[g];
             float dr = __double2float_ru(A.s_drift[sl]);
-            int nf = A.s_nfeat[sl], sz = A.s_size[sl], pend = A.s_pend[sl];
-            const int pend0 = pend;
+            const int nf0 = A.s_nfeat[sl], pend0 = A.s_pend[sl];
+            int sz = A.s_size[sl];
             const int cid = A.s_cid[sl];
             const float cn = sqrtf(A.s_cn2[sl]) * 1.00001f;
-            for (int p0 = b; p0 < f; p0 += 32) {
-                const int p = p0 + lane;
-                const bool match = p < f && seg_key[p] == sl;
+            const int off = grp_off[g], cnt = overflow ? 0 : grp_cnt[g];
+            int ncommit = 0;
+            for (int i0 = 0; i0 < cnt; i0 += 32) {
+                const int i = i0 + lane;
+                const int p = i < cnt ? glist[off + i] : INT_MAX;
+                const bool match = p < f;
                 const unsigned mask = __ballot_sync(0xffffffffu, match);
-                if (!mask) continue;
-                const int rk = __popc(mask & ((1u << lane) - 1u));
+                if (!mask) break;
                 float a = 1.f, c = 0.f;
                 int w = 0;
                 int64_t cc = 0;
                 if (match) {
                     cc = A.c0 + p;
                     const float ub0 = seg_ub0[p];
-                    const float inv = __frcp_ru((float)(nf + rk + 1));
+                    const float inv = __frcp_ru((float)(nf0 + i + 1));
                     a = __fadd_ru(__fadd_ru(1.f, inv), 2.5e-7f);
                     c = __fadd_ru(__fmul_ru(ub0, inv), __fmul_ru(1e-13f, __fadd_ru(cn, ub0)) + 1e-30f);
                     w = 1 + A.dup_run[cc];
@@ -785,24 +845,23 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
                     const int64_t obj = A.cls_obj[cc];
                     A.cluster_of[obj] = cid;
                     A.mrank[obj] = sz + wsum - w;
-                    A.frank[obj] = nf + rk;
-                    A.pend_rank[p] = pend + rk;
+                    A.frank[obj] = nf0 + i;
+                    A.pend_rank[p] = pend0 + i;
                     A.slot_of[p] = sl;
                     sh_slot_of[p] = sl;
                 }
                 const float a31 = __shfl_sync(0xffffffffu, a, 31), c31 = __shfl_sync(0xffffffffu, c, 31);
                 dr = __fmaf_ru(a31, dr, c31);
-                const int cnt = __popc(mask);
-                nf += cnt;
-                pend += cnt;
+                ncommit += __popc(mask);
                 sz += __shfl_sync(0xffffffffu, wsum, 31);
+                if (mask != 0xffffffffu) break;
             }
             if (lane == 0) {
-                if (pend > pend0) {
+                if (ncommit > 0) {
                     A.s_drift[sl] = (double)dr;
-                    A.s_nfeat[sl] = nf;
+                    A.s_nfeat[sl] = nf0 + ncommit;
                     A.s_size[sl] = sz;
-                    A.s_pend[sl] = pend;
+                    A.s_pend[sl] = pend0 + ncommit;
                     if (pend0 == 0) {
                         const int di = atomicAdd(&s_ndirty, 1);
                         A.s_didx[sl] = di;
@@ -1292,8 +1351,11 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
     const int D = s->cfg.dim;
     const float rel = (float)screen_rel(D);
     const float absc = (float)(2.0 * 2.384185791015625e-07);  // 2^-22 * 2
-    for (int64_t c0 = c_begin; c0 < c_end; c0 += s->B) {
-        const int B = (int)std::min<int64_t>(s->B, c_end - c0);
+    for (int64_t c0 = c_begin, B = 0; c0 < c_end; c0 += B) {
+        // young clusters have loose drift bounds: start a stream with small
+        // batches (fresh snapshots) and double up to the configured size
+        const int64_t grow = s->batch_no < 20 ? ((int64_t)64 << s->batch_no) : s->B;
+        B = (int)std::min<int64_t>(std::min<int64_t>(s->B, grow), c_end - c0);
         s->t_ms[6] += 1.0;
         // 1. snapshot screen
         s->tstart(1);
@@ -1379,7 +1441,7 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             A.sum_e1 = s->sum_e1.p;
             A.sum_lbr = s->sum_lbr.p;
             const PwPlan &P = *s->plan_host;
-            size_t smem = (size_t)s->B * (8 + 4 * 7 + 1) + 16 + sizeof(double) * (P.n_chains + P.n_leaves + P.n_ops + 8);
+            size_t smem = (size_t)s->B * (8 + 4 * 8 + 2 + 1) + 16 + sizeof(double) * (P.n_chains + P.n_leaves + P.n_ops + 8);
             auto kern = k_resolve<T>;
             FX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
             kern<<<1, RS_THREADS, smem, st>>>(A);
