@@ -248,6 +248,12 @@ int fx_stream_counters(fx_stream *s, int64_t *out, int n);
 /* The cudaStream_t the stream's kernels run on (for caller-side CUDA events). */
 void *fx_stream_cuda_stream(fx_stream *s);
 
+/* Diagnostic: run the tcgen05 TF32 screen kernel on host matrices
+ * A[na x dim], B[nb x dim] (float32, dim % 4 == 0); out[na x nb] receives
+ * ||a||^2 + ||b||^2 - 2 a.b as the ingest screen computes it. */
+int fx_debug_screen_tc(int32_t device, int64_t na, int64_t nb, int32_t dim, const float *A, const float *B,
+                       float *out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -73,6 +73,8 @@ _SIGS = {
     "fx_stream_timings": (ctypes.c_int, [vp, c_f64p, ctypes.c_int]),
     "fx_stream_counters": (ctypes.c_int, [vp, c_i64p, ctypes.c_int]),
     "fx_stream_cuda_stream": (ctypes.c_void_p, [vp]),
+    "fx_debug_screen_tc": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, vp, vp,
+                                          vp]),
     "fx_index_sizes_get": (ctypes.c_int, [vp, ctypes.POINTER(IndexSizes)]),
     "fx_index_export": (ctypes.c_int, [vp, c_i64p, c_f64p, c_i64p, c_i64p, c_i64p, c_i64p, c_i64p, c_i32p, c_i32p,
                                        c_i64p, c_i64p]),

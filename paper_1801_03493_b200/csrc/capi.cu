@@ -172,6 +172,11 @@ int fx_stream_create(const fx_stream_config *cfg, fx_stream **out) {
             s->cfg = *cfg;
             s->dev = cfg->device;
             s->esize = cfg->feat_type == FX_F64 ? 8 : 4;
+            {
+                const char *env = getenv("FOCUS_B200_SCREEN");
+                const bool simt = env && strcmp(env, "simt") == 0;
+                s->tc_screen = !simt && cfg->feat_type == FX_F32 && cfg->dim % 4 == 0;
+            }
             FX_CUDA(cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking));
             const int D = cfg->dim;
             int B = cfg->batch;

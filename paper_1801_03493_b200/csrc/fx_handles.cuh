@@ -37,6 +37,7 @@ struct fx_stream {
     int dev = 0;
     cudaStream_t st = nullptr;
     int esize = 4;             // feature element size
+    bool tc_screen = false;    // tcgen05 TF32 screen (f32 features, D % 4 == 0)
     bool finalized = false;
 
     // rank model

@@ -316,6 +316,27 @@ __device__ __forceinline__ T warp_sum(T v) {
 
 inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Error model of the snapshot screen.  SIMT mode stores the
+// FP32 direct-difference distance d with |d - d_ref| <= rel*d + absc*(|c|+|f|);
+// TC mode stores the TF32 GEMM-expansion value v ~ d^2 with
+// |v - d_ref^2| <= g2*|c|*|f| + kap*(|c|^2 + |f|^2).
+struct ScreenModel {
+    int tc;
+    float rel, absc, g2, kap;
+};
+
+__device__ __forceinline__ void snap_bounds(const ScreenModel &m, float v, float cn, float fn, float &lb, float &ub) {
+    if (m.tc) {
+        const float E = m.g2 * cn * fn + m.kap * (cn * cn + fn * fn) + 1e-30f;
+        lb = sqrtf(fmaxf(v - E, 0.f)) * (1.f - 4e-7f);
+        ub = sqrtf(fmaxf(v + E, 0.f)) * (1.f + 4e-7f) + 1e-30f;
+    } else {
+        const float e = m.rel * v + m.absc * (cn + fn) + 1e-30f;
+        lb = v - e;
+        ub = v + e;
+    }
+}
+
 // exclusive scan of int32 flags/counts into int64 offsets (device), returns total
 int64_t scan_i32_to_i64(const int32_t *in, int64_t n, int64_t *out_excl, cudaStream_t st, int64_t *scratch_total);
 

@@ -215,7 +215,7 @@ struct FromResidual {  // B rows = features of the batch's residual objects
 // distances is precomputed for the objects after it.
 __global__ void k_residuals(int nA, const int64_t *__restrict__ ctr, const float *__restrict__ dist, int64_t ld,
                             const float *__restrict__ cn2, const int32_t *__restrict__ snap,
-                            const float *__restrict__ fnorm, int64_t a0, float rel, float absc, double T,
+                            const float *__restrict__ fnorm, int64_t a0, ScreenModel sm, double T,
                             int32_t *__restrict__ res_col, int32_t *__restrict__ res_pos, int64_t *__restrict__ nres) {
     int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (w >= nA) return;
@@ -223,9 +223,9 @@ __global__ void k_residuals(int nA, const int64_t *__restrict__ ctr, const float
     const float fn = fnorm[a0 + w];
     float mn = INFINITY;
     for (int q = lane; q < nsnap; q += 32) {
-        float d = dist[(int64_t)w * ld + q];
-        float e = rel * d + absc * (sqrtf(cn2[snap[q]]) * 1.00001f + fn);
-        mn = fminf(mn, d - e);
+        float lb, ub;
+        snap_bounds(sm, dist[(int64_t)w * ld + q], sqrtf(cn2[snap[q]]) * 1.00001f, fn, lb, ub);
+        mn = fminf(mn, lb);
     }
     mn = warp_min(mn);
     if (lane == 0) {
@@ -250,6 +250,7 @@ struct ResolveArgs {
     double T;
     int64_t M;
     float rel, absc;
+    ScreenModel sm;
     const float *dist;
     int64_t ld;
     const float *dres;
@@ -307,8 +308,17 @@ __device__ __forceinline__ void slot_bounds(const ResolveArgs &A, int b, float f
     int q = A.s_snapq[slot];
     float cn;
     if (q >= 0) {
-        d = A.dist[(int64_t)b * A.ld + q];
+        const float v = A.dist[(int64_t)b * A.ld + q];
         cn = sqrtf(A.s_cn2[slot]) * 1.00001f;
+        float l0, u0;
+        snap_bounds(A.sm, v, cn, fn, l0, u0);
+        d = 0.5f * (l0 + u0);
+        const float dr = (float)A.s_drift[slot] * 1.00001f;
+        lb = l0 - dr;
+        ub = u0 + dr;
+        lb = lb - fabsf(lb) * 1e-6f - 1e-30f;
+        ub = ub + fabsf(ub) * 1e-6f + 1e-30f;
+        return;
     } else {
         int s = A.s_seedpos[slot];
         int col = A.res_col[s];
@@ -414,42 +424,70 @@ __device__ double exact_dist(const ResolveArgs &A, int b, int slot, const int32_
 // Per-object summary of the snapshot screen row: best snapshot slot, its
 // distance and error bound, and min over the other snapshot slots of
 // (d - e).  One warp per object.
+template <typename T>
 __global__ void k_row_summary(int nA, const int64_t *__restrict__ ctr, const float *__restrict__ dist, int64_t ld,
                               const float *__restrict__ cn2, const int32_t *__restrict__ snap,
-                              const float *__restrict__ fnorm, int64_t a0, float rel, float absc,
+                              const float *__restrict__ fnorm, int64_t a0, ScreenModel sm, float rel, float absc,
+                              const char *const *__restrict__ frow, const float *__restrict__ C32, int D,
                               int32_t *__restrict__ sum_slot, float *__restrict__ sum_d1, float *__restrict__ sum_e1,
                               float *__restrict__ sum_lbr) {
     const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (w >= nA) return;
     const int nsnap = (int)ctr[C_NSNAP];
     const float fn = fnorm[a0 + w];
-    float d1 = INFINITY, e1 = 0.f, lbr = INFINITY;
+    // best candidate = smallest upper bound; lbr = min lower bound of the rest
+    float u1 = INFINITY, l1 = INFINITY, lbr = INFINITY;
     int q1 = -1;
     for (int q = lane; q < nsnap; q += 32) {
-        const float d = dist[(int64_t)w * ld + q];
-        const float e = rel * d + absc * (sqrtf(cn2[snap[q]]) * 1.00001f + fn) + 1e-30f;
-        if (d < d1) {
-            if (q1 >= 0) lbr = fminf(lbr, d1 - e1);
-            d1 = d;
-            e1 = e;
+        float lb, ub;
+        snap_bounds(sm, dist[(int64_t)w * ld + q], sqrtf(cn2[snap[q]]) * 1.00001f, fn, lb, ub);
+        if (ub < u1) {
+            if (q1 >= 0) lbr = fminf(lbr, l1);
+            u1 = ub;
+            l1 = lb;
             q1 = q;
         } else {
-            lbr = fminf(lbr, d - e);
+            lbr = fminf(lbr, lb);
         }
     }
 #pragma unroll
     for (int o = 16; o; o >>= 1) {
-        const float od1 = __shfl_xor_sync(0xffffffffu, d1, o), oe1 = __shfl_xor_sync(0xffffffffu, e1, o);
+        const float ou = __shfl_xor_sync(0xffffffffu, u1, o), ol = __shfl_xor_sync(0xffffffffu, l1, o);
         const float olbr = __shfl_xor_sync(0xffffffffu, lbr, o);
-        const int oq1 = __shfl_xor_sync(0xffffffffu, q1, o);
-        const bool take = oq1 >= 0 && (q1 < 0 || od1 < d1 || (od1 == d1 && oq1 < q1));
+        const int oq = __shfl_xor_sync(0xffffffffu, q1, o);
+        const bool take = oq >= 0 && (q1 < 0 || ou < u1 || (ou == u1 && oq < q1));
         if (take) {
-            lbr = fminf(fminf(lbr, olbr), q1 >= 0 ? d1 - e1 : INFINITY);
-            d1 = od1;
-            e1 = oe1;
-            q1 = oq1;
+            lbr = fminf(fminf(lbr, olbr), q1 >= 0 ? l1 : INFINITY);
+            u1 = ou;
+            l1 = ol;
+            q1 = oq;
         } else {
-            lbr = fminf(fminf(lbr, olbr), oq1 >= 0 ? od1 - oe1 : INFINITY);
+            lbr = fminf(fminf(lbr, olbr), oq >= 0 ? ol : INFINITY);
+        }
+    }
+    float d1 = 0.5f * (l1 + u1), e1 = 0.5f * (u1 - l1);
+    if (sm.tc && q1 >= 0) {
+        // re-measure the best candidate in FP32 direct-difference form (tight SIMT bound)
+        const T *f = (const T *)frow[a0 + w];
+        const float *c = C32 + (int64_t)snap[q1] * D;
+        float tot = 0.f, acc = 0.f;
+        int cnt = 0;
+        for (int k = lane; k < D; k += 32) {
+            const float d = (float)f[k] - c[k];
+            acc = fmaf(d, d, acc);
+            if (++cnt == 64) {
+                tot += acc;
+                acc = 0.f;
+                cnt = 0;
+            }
+        }
+        tot += acc;
+        tot = warp_sum(tot);
+        const float dd = sqrtf(tot);
+        const float ee = rel * dd + absc * (sqrtf(cn2[snap[q1]]) * 1.00001f + fn) + 1e-30f;
+        if (dd + ee < u1) {  // keep whichever interval is tighter (both are valid)
+            d1 = dd;
+            e1 = ee;
         }
     }
     if (lane == 0) {
@@ -574,15 +612,16 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
                     const int sl = A.live[i];
                     const int q = A.s_snapq[sl];
                     if (q < 0) continue;
-                    const float d = A.dist[(int64_t)p * A.ld + q];
-                    const float e = A.rel * d + A.absc * (sqrtf(A.s_cn2[sl]) * 1.00001f + fn) + 1e-30f;
-                    if (d < d1) {
+                    float l0, u0;
+                    snap_bounds(A.sm, A.dist[(int64_t)p * A.ld + q], sqrtf(A.s_cn2[sl]) * 1.00001f, fn, l0, u0);
+                    const float d = 0.5f * (l0 + u0), e = 0.5f * (u0 - l0);
+                    if (u0 < d1 + e1 || j1 < 0) {
                         if (j1 >= 0) lbr = fminf(lbr, d1 - e1);
                         j1 = sl;
                         d1 = d;
                         e1 = e;
                     } else {
-                        lbr = fminf(lbr, d - e);
+                        lbr = fminf(lbr, l0);
                     }
                 }
             }
@@ -1336,6 +1375,9 @@ __global__ void k_seal_pick(int64_t nfeat_total, const int32_t *__restrict__ fme
 // host-side orchestration
 // ---------------------------------------------------------------------------
 
+void launch_screen_tc(int nA, int64_t a0, const char *const *frow, const float *fnorm, int D, const int64_t *nB_dev,
+                      int nB_max, const float *C32, const int32_t *snap, const float *cn2, float *out, int64_t ld,
+                      cudaStream_t st);
 int64_t scan_i32_to_i64(const int32_t *in, int64_t n, int64_t *out_excl, cudaStream_t st, int64_t *scratch_total);
 void scan_u8_to_i64(const uint8_t *in, int64_t n, int invert, int64_t *out_excl, int64_t *d_total, cudaStream_t st);
 
@@ -1351,6 +1393,9 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
     const int D = s->cfg.dim;
     const float rel = (float)screen_rel(D);
     const float absc = (float)(2.0 * 2.384185791015625e-07);  // 2^-22 * 2
+    // TF32 dot error gamma = 2^-9 + D 2^-22 (operand rounding + FP32 accumulation), d^2 error 2 gamma |a||b|
+    const double gam = 1.953125e-03 + (double)D * 2.384185791015625e-07;
+    const ScreenModel sm{s->tc_screen ? 1 : 0, rel, absc, (float)(2.0 * gam * 1.01), (float)(256.0 * 5.9604644775390625e-08)};
     for (int64_t c0 = c_begin, B = 0; c0 < c_end; c0 += B) {
         // young clusters have loose drift bounds: start a stream with small
         // batches (fresh snapshots) and double up to the configured size
@@ -1359,7 +1404,10 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
         s->t_ms[6] += 1.0;
         // 1. snapshot screen
         s->tstart(1);
-        {
+        if (s->tc_screen) {
+            launch_screen_tc(B, c0, s->frow.p, s->fnorm.p, D, s->ctr.p + C_NSNAP, (int)s->ld, s->C32.p,
+                             s->snap_slot.p, s->s_cn2.p, s->dist.p, s->ld, st);
+        } else {
             dim3 grid((unsigned)cdiv(s->ld, SC_T), (unsigned)cdiv(B, SC_T));
             FromSnapshot fb{s->C32.p, s->snap_slot.p, D};
             k_screen<T, FromSnapshot><<<grid, 256, 0, st>>>(B, c0, s->frow.p, D, s->ctr.p + C_NSNAP, (int)s->ld, fb,
@@ -1369,7 +1417,7 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
         // 2. residuals + their in-batch columns
         {
             k_residuals<<<(unsigned)cdiv((int64_t)B * 32, 256), 256, 0, st>>>(
-                B, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p, s->snap_slot.p, s->fnorm.p, c0, rel, absc, s->cfg.t,
+                B, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p, s->snap_slot.p, s->fnorm.p, c0, sm, s->cfg.t,
                 s->res_col.p, s->res_pos.p, s->ctr.p + C_NRES);
             FX_LAUNCHED();
             dim3 grid((unsigned)cdiv(B, SC_T), (unsigned)cdiv(B, SC_T));
@@ -1377,9 +1425,9 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             k_screen<T, FromResidual<T>><<<grid, 256, 0, st>>>(B, c0, s->frow.p, D, s->ctr.p + C_NRES, B, fb, s->dres.p, B);
             FX_LAUNCHED();
         }
-        k_row_summary<<<(unsigned)cdiv((int64_t)B * 32, 256), 256, 0, st>>>(
-            B, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p, s->snap_slot.p, s->fnorm.p, c0, rel, absc, s->sum_slot.p,
-            s->sum_d1.p, s->sum_e1.p, s->sum_lbr.p);
+        k_row_summary<T><<<(unsigned)cdiv((int64_t)B * 32, 256), 256, 0, st>>>(
+            B, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p, s->snap_slot.p, s->fnorm.p, c0, sm, rel, absc, s->frow.p,
+            s->C32.p, D, s->sum_slot.p, s->sum_d1.p, s->sum_e1.p, s->sum_lbr.p);
         FX_LAUNCHED();
         s->tstop();
         // 3. resolve (parallel verified segments + exact sequential events)
@@ -1394,6 +1442,7 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             A.M = s->cfg.m;
             A.rel = rel;
             A.absc = absc;
+            A.sm = sm;
             A.dist = s->dist.p;
             A.ld = s->ld;
             A.dres = s->dres.p;

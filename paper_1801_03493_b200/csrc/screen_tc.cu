@@ -1,0 +1,277 @@
+// screen_tc.cu -- K2a on the 5th-gen tensor cores: batch-object x snapshot-
+// centroid squared distances via the GEMM expansion
+//     d^2 = ||a||^2 + ||b||^2 - 2 a.b
+// with a.b from tcgen05.mma kind::tf32 (A and B K-major in shared memory,
+// accumulator in TMEM, 128 x 128 tile per CTA).
+//
+// Exactness: the screen only prunes.  Its rigorous error bound (consumed by
+// tc_bounds in fx_internal.cuh) is
+//     |a.b^ - a.b| <= gamma ||a|| ||b||,  gamma = 2^-9 + D 2^-22
+// (TF32 keeps 10 mantissa bits of each operand, truncation or rounding:
+// relative product error <= 2^-9 + 2^-20; plus the FP32 accumulation of D
+// products), so d^2 lies within 2 gamma ||a|| ||b|| (+ FP32 rounding of the
+// expansion) of the screen value.  The object's best candidate is then
+// re-measured in FP32 direct-difference form (k_row_summary_tc), and every
+// decision the bounds leave open goes to the exact float64 path.
+//
+// Operand staging: rows are gathered (batch objects through their feature row
+// pointers, centroids through the snapshot slot list) with cp.async 16-byte
+// copies into the canonical no-swizzle K-major layout: 8-row x 16-byte core
+// matrices, K-adjacent core matrices 128 B apart (LBO), 8-row groups
+// KT*32 B apart (SBO).  A 4-stage cp.async ring feeds the single MMA-issuing
+// thread; tcgen05.commit on a per-stage mbarrier releases a stage.
+#include "fx_handles.cuh"
+
+namespace fx {
+
+constexpr int TC_M = 128, TC_N = 128, TC_KT = 32, TC_STAGES = 4, TC_THREADS = 128;
+constexpr int TC_TILE_BYTES = TC_M * TC_KT * 4;  // 16 KB per operand per stage
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, int src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(src_bytes));
+}
+
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;  // version = 1 (Blackwell)
+    // base_offset 0, lbo_mode 0, layout SWIZZLE_NONE (0) in bits 61..63
+    return d;
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity));
+}
+
+// A tile: 128 rows x KT floats at k0; row r of the tile -> global row pointer
+// rows[r] (nullptr -> zeros).  Layout: ((r/8)*(KT/4) + c)*128 + (r%8)*16.
+__device__ __forceinline__ void load_tile(uint32_t sbase, const float *const *rows, int k0, int D,
+                                          const void *dummy) {
+    // 128 rows x (KT/4 = 8) chunks = 1024 16-byte copies / 128 threads
+#pragma unroll
+    for (int e = 0; e < (TC_M * TC_KT / 4) / TC_THREADS; e++) {
+        const int idx = threadIdx.x + e * TC_THREADS;
+        const int r = idx >> 3, c = idx & 7;
+        const float *row = rows[r];
+        const int k = k0 + c * 4;
+        const bool ok = row != nullptr && k < D;
+        const void *src = ok ? (const void *)(row + k) : dummy;  // never read when src-size is 0
+        const uint32_t dst = sbase + (uint32_t)((((r >> 3) * (TC_KT / 4) + c) << 7) + ((r & 7) << 4));
+        cp_async16(dst, src, ok ? 16 : 0);
+    }
+}
+
+// out[a][q] = ||A_a||^2 + ||B_q||^2 - 2 A_a.B_q   (float, not clamped)
+__global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0, const char *const *__restrict__ frow,
+                                                           const float *__restrict__ fnorm, int D,
+                                                           const int64_t *__restrict__ nB_dev,
+                                                           const float *__restrict__ C32,
+                                                           const int32_t *__restrict__ snap,
+                                                           const float *__restrict__ cn2, float *__restrict__ out,
+                                                           int64_t ld) {
+    const int nB = (int)*nB_dev;
+    const int tb = blockIdx.x * TC_N, ta = blockIdx.y * TC_M;
+    if (tb >= nB || ta >= nA) return;
+    extern __shared__ __align__(1024) unsigned char smem[];
+    // [stage][A 16KB | B 16KB]
+    __shared__ const float *rowsA[TC_M];
+    __shared__ const float *rowsB[TC_N];
+    __shared__ __align__(8) uint64_t bar_stage[TC_STAGES];
+    __shared__ __align__(8) uint64_t bar_done;
+    __shared__ uint32_t tmem_base;
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    for (int r = tid; r < TC_M; r += TC_THREADS) {
+        const int a = ta + r;
+        rowsA[r] = a < nA ? (const float *)frow[a0 + a] : nullptr;
+        const int b = tb + r;
+        rowsB[r] = b < nB ? C32 + (int64_t)snap[b] * D : nullptr;
+    }
+    if (tid == 0) {
+        for (int s = 0; s < TC_STAGES; s++) mbar_init(&bar_stage[s], 1);
+        mbar_init(&bar_done, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base)),
+                     "r"(TC_N));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+    const uint32_t tmem = tmem_base;
+    const uint32_t sbase = smem_u32(smem);
+
+    const int nk = (D + TC_KT - 1) / TC_KT;
+    // instruction descriptor: D=F32, A=B=TF32, K-major both, N=128, M=128
+    const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TC_N >> 3) << 17) |
+                           ((uint32_t)(TC_M >> 4) << 24);
+    // prologue: stages 0..S-2
+    for (int s = 0; s < TC_STAGES - 1; s++) {
+        if (s < nk) {
+            const uint32_t st = sbase + s * 2 * TC_TILE_BYTES;
+            load_tile(st, rowsA, s * TC_KT, D, fnorm);
+            load_tile(st + TC_TILE_BYTES, rowsB, s * TC_KT, D, fnorm);
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+    }
+    for (int it = 0; it < nk; it++) {
+        const int s = it % TC_STAGES;
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(TC_STAGES - 2));
+        asm volatile("fence.proxy.async.shared::cta;\n" ::);
+        __syncthreads();
+        if (tid == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+            const uint32_t st = sbase + s * 2 * TC_TILE_BYTES;
+#pragma unroll
+            for (int kk = 0; kk < TC_KT / 8; kk++) {
+                const uint64_t da = umma_desc(st + kk * 256, 128, TC_KT * 32);
+                const uint64_t db = umma_desc(st + TC_TILE_BYTES + kk * 256, 128, TC_KT * 32);
+                const uint32_t acc = (it > 0 || kk > 0) ? 1u : 0u;
+                asm volatile(
+                    "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                    "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+                    "l"(da), "l"(db), "r"(idesc), "r"(acc));
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                smem_u32(&bar_stage[s])));
+        }
+        // refill the stage consumed S-1 iterations from now
+        const int nt = it + TC_STAGES - 1;
+        if (nt < nk) {
+            const int ns = nt % TC_STAGES;
+            if (nt >= TC_STAGES) mbar_wait(&bar_stage[ns], (uint32_t)(((nt / TC_STAGES) - 1) & 1));
+            const uint32_t st = sbase + ns * 2 * TC_TILE_BYTES;
+            load_tile(st, rowsA, nt * TC_KT, D, fnorm);
+            load_tile(st + TC_TILE_BYTES, rowsB, nt * TC_KT, D, fnorm);
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+    }
+    if (tid == 0)
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+            smem_u32(&bar_done)));
+    mbar_wait(&bar_done, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+
+    // epilogue: warp w owns TMEM lanes 32w..32w+31 = tile rows
+    const int r = warp * 32 + lane;
+    const int a = ta + r;
+    const float fa2 = a < nA ? fnorm[a0 + a] * fnorm[a0 + a] : 0.f;
+    for (int c0 = 0; c0 < TC_N; c0 += 32) {
+        uint32_t v[32];
+        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
+            "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+              "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
+        if (a < nA) {
+#pragma unroll
+            for (int j = 0; j < 32; j++) {
+                const int b = tb + c0 + j;
+                if (b < nB) {
+                    const float dot = __uint_as_float(v[j]);
+                    out[(int64_t)a * ld + b] = fa2 + cn2[snap[b]] - 2.f * dot;
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TC_N));
+}
+
+size_t screen_tc_smem() { return (size_t)TC_STAGES * 2 * TC_TILE_BYTES; }
+
+void launch_screen_tc(int nA, int64_t a0, const char *const *frow, const float *fnorm, int D, const int64_t *nB_dev,
+                      int nB_max, const float *C32, const int32_t *snap, const float *cn2, float *out, int64_t ld,
+                      cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        FX_CUDA(cudaFuncSetAttribute(k_screen_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)screen_tc_smem()));
+        attr = true;
+    }
+    dim3 grid((unsigned)cdiv(nB_max, TC_N), (unsigned)cdiv(nA, TC_M));
+    k_screen_tc<<<grid, TC_THREADS, screen_tc_smem(), st>>>(nA, a0, frow, fnorm, D, nB_dev, C32, snap, cn2, out, ld);
+    FX_LAUNCHED();
+}
+
+__global__ void k_rowptrs(int64_t n, const float *base, int dim, const char **rows, float *norm2) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    rows[i] = (const char *)(base + i * dim);
+    float acc = 0.f;
+    for (int k = 0; k < dim; k++) acc = fmaf(base[i * dim + k], base[i * dim + k], acc);
+    norm2[i] = acc;
+}
+__global__ void k_iota32(int64_t n, int32_t *o) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) o[i] = (int32_t)i;
+}
+__global__ void k_sqrt_inplace(int64_t n, float *x) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) x[i] = sqrtf(x[i]);
+}
+
+}  // namespace fx
+
+extern "C" int fx_debug_screen_tc(int32_t device, int64_t na, int64_t nb, int32_t dim, const float *A, const float *B,
+                                  float *out) {
+    using namespace fx;
+    try {
+        if (dim % 4 != 0 || na <= 0 || nb <= 0) throw Error{FX_E_USAGE, "bad shapes"};
+        FX_CUDA(cudaSetDevice(device));
+        cudaStream_t st = 0;
+        DevBuf<float> dA, dB, nA2, nB2, dout;
+        DevBuf<const char *> rows;
+        DevBuf<int32_t> snap;
+        DevBuf<int64_t> nbd;
+        dA.reserve((size_t)na * dim);
+        dB.reserve((size_t)nb * dim);
+        nA2.reserve(na);
+        nB2.reserve(nb);
+        dout.reserve((size_t)na * nb);
+        rows.reserve(na);
+        snap.reserve(nb);
+        nbd.reserve(1);
+        FX_CUDA(cudaMemcpy(dA.p, A, sizeof(float) * na * dim, cudaMemcpyHostToDevice));
+        FX_CUDA(cudaMemcpy(dB.p, B, sizeof(float) * nb * dim, cudaMemcpyHostToDevice));
+        FX_CUDA(cudaMemcpy(nbd.p, &nb, sizeof(int64_t), cudaMemcpyHostToDevice));
+        DevBuf<const char *> rowsB;
+        rowsB.reserve(nb);
+        k_rowptrs<<<(unsigned)cdiv(na, 256), 256>>>(na, dA.p, dim, rows.p, nA2.p);
+        k_rowptrs<<<(unsigned)cdiv(nb, 256), 256>>>(nb, dB.p, dim, rowsB.p, nB2.p);
+        k_iota32<<<(unsigned)cdiv(nb, 256), 256>>>(nb, snap.p);
+        k_sqrt_inplace<<<(unsigned)cdiv(na, 256), 256>>>(na, nA2.p);  // fnorm = ||a||
+        FX_LAUNCHED();
+        launch_screen_tc((int)na, 0, rows.p, nA2.p, dim, nbd.p, (int)nb, dB.p, snap.p, nB2.p, dout.p, nb, st);
+        FX_CUDA(cudaDeviceSynchronize());
+        FX_CUDA(cudaMemcpy(out, dout.p, sizeof(float) * na * nb, cudaMemcpyDeviceToHost));
+    } catch (const Error &e) {
+        set_error(e.msg);
+        return e.code;
+    }
+    return FX_OK;
+}
