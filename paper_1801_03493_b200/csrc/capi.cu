@@ -122,11 +122,10 @@ fx_stream::~fx_stream() {
     }
     for (auto *b : owned_feats) delete b;
     delete plan_host;
-    if (st) cudaStreamDestroy(st);
+    // the CUDA stream is destroyed by fx_stream_destroy after the members'
+    // stream-ordered frees have been queued on it
 }
-fx_index::~fx_index() {
-    if (owns_stream && st) cudaStreamDestroy(st);
-}
+fx_index::~fx_index() {}  // stream destroyed by fx_index_destroy (see fx_stream)
 fx_session::~fx_session() {}
 
 #define FX_GUARD(...)                                   \
@@ -167,6 +166,7 @@ int fx_stream_create(const fx_stream_config *cfg, fx_stream **out) {
         if (cfg->dim < 1 || cfg->sig_dim < 0 || cfg->vocab < 1) throw Error{FX_E_USAGE, "bad dimensions"};
         if (cfg->feat_type != FX_F32 && cfg->feat_type != FX_F64) throw Error{FX_E_USAGE, "bad feat_type"};
         set_dev(cfg->device);
+        init_pool(cfg->device);
         fx_stream *s = new fx_stream();
         try {
             s->cfg = *cfg;
@@ -178,6 +178,7 @@ int fx_stream_create(const fx_stream_config *cfg, fx_stream **out) {
                 s->tc_screen = !simt && cfg->feat_type == FX_F32 && cfg->dim % 4 == 0;
             }
             FX_CUDA(cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking));
+            cur_stream() = s->st;
             const int D = cfg->dim;
             int B = cfg->batch;
             if (B <= 0) {
@@ -239,8 +240,12 @@ int fx_stream_destroy(fx_stream *s) {
     FX_GUARD({
         if (s) {
             set_dev(s->dev);
-            cudaStreamSynchronize(s->st);
-            delete s;
+            cudaStream_t st = s->st;
+            {
+                StreamGuard sg_(st);
+                delete s;
+            }
+            if (st) cudaStreamDestroy(st);  // destroyed once its queued frees complete
         }
     })
 }
@@ -249,6 +254,7 @@ int fx_stream_set_rank_model(fx_stream *s, const fx_rank_model *rm) {
     FX_GUARD({
         if (!s || !rm) throw Error{FX_E_USAGE, "null argument"};
         set_dev(s->dev);
+        StreamGuard sg_(s->st);
         const int K = s->cfg.k, V = s->cfg.vocab;
         s->gt = rm->ground_truth;
         s->seed = rm->seed;
@@ -268,6 +274,7 @@ int fx_stream_dup_flags(fx_stream *s, int64_t n, const int64_t *frame_ids, const
         if (!s) throw Error{FX_E_USAGE, "null stream"};
         if (n <= 0) return FX_OK;
         set_dev(s->dev);
+        StreamGuard sg_(s->st);
         const int S = s->cfg.sig_dim;
         DevBuf<int64_t> f;
         DevBuf<double> g;
@@ -375,6 +382,7 @@ static int ingest_common(fx_stream *s, int64_t n, const int64_t *object_ids, con
         if (n == 0) return FX_OK;
         if (!true_class && !topk) throw Error{FX_E_USAGE, "need true_class or topk"};
         set_dev(s->dev);
+        StreamGuard sg_(s->st);
         cudaStream_t st = s->st;
         const int D = s->cfg.dim, S = s->cfg.sig_dim, K = s->cfg.k;
         const bool compact = flags & FX_FEATS_COMPACT;
@@ -438,6 +446,7 @@ int fx_finalize(fx_stream *s, fx_index **out, fx_ingest_report *rep) {
         if (!s || !out) throw Error{FX_E_USAGE, "null argument"};
         if (s->finalized) throw Error{FX_E_USAGE, "stream already finalized"};
         set_dev(s->dev);
+        StreamGuard sg_(s->st);
         cudaStream_t st = s->st;
         const int D = s->cfg.dim;
         FX_CUDA(cudaMemcpyAsync(s->h_ctr, s->ctr.p, sizeof(int64_t) * C_COUNT, cudaMemcpyDeviceToHost, st));
@@ -531,6 +540,7 @@ int fx_stream_object_results(fx_stream *s, int32_t *cluster_of, uint8_t *is_dup,
     FX_GUARD({
         if (!s) throw Error{FX_E_USAGE, "null stream"};
         set_dev(s->dev);
+        StreamGuard sg_(s->st);
         const int64_t n = s->n_seen;
         d2h(cluster_of, s->cluster_of.p, n, s->st);
         d2h(is_dup, s->is_dup.p, n, s->st);
@@ -543,6 +553,7 @@ int fx_stream_timings(fx_stream *s, double *out, int n) {
     FX_GUARD({
         if (!s || !out) throw Error{FX_E_USAGE, "null argument"};
         set_dev(s->dev);
+        StreamGuard sg_(s->st);
         s->tcollect();
         for (int i = 0; i < n && i < 8; i++) out[i] = s->t_ms[i];
     })
@@ -552,6 +563,7 @@ int fx_stream_counters(fx_stream *s, int64_t *out, int n) {
     FX_GUARD({
         if (!s || !out) throw Error{FX_E_USAGE, "null argument"};
         set_dev(s->dev);
+        StreamGuard sg_(s->st);
         FX_CUDA(cudaMemcpyAsync(s->h_ctr, s->ctr.p, sizeof(int64_t) * C_COUNT, cudaMemcpyDeviceToHost, s->st));
         FX_CUDA(cudaStreamSynchronize(s->st));
         for (int i = 0; i < n && i < C_COUNT; i++) out[i] = s->h_ctr[i];
@@ -585,6 +597,7 @@ int fx_index_export(fx_index *ix, int64_t *cluster_ids, double *centroids, int64
     FX_GUARD({
         if (!ix) throw Error{FX_E_USAGE, "null index"};
         set_dev(ix->dev);
+        StreamGuard sg_(ix->st);
         cudaStream_t st = ix->st;
         const int64_t C = ix->C;
         d2h(cluster_ids, ix->cluster_ids.p, C, st);
@@ -619,12 +632,15 @@ int fx_index_build(int64_t C, int32_t vocab, int32_t k, int32_t dim, int32_t dev
         for (int64_t i = 1; i < C; i++)
             if (cluster_ids[i] < cluster_ids[i - 1]) throw Error{FX_E_USAGE, "cluster ids must be ascending"};
         set_dev(device);
+        init_pool(device);
+        StreamGuard sg_(nullptr);
         fx_index *ix = new fx_index();
         try {
             ix->dev = device;
             FX_CUDA(cudaStreamCreateWithFlags(&ix->st, cudaStreamNonBlocking));
             ix->owns_stream = true;
             cudaStream_t st = ix->st;
+            cur_stream() = st;
             ix->C = C;
             ix->D = dim;
             ix->V = vocab;
@@ -670,8 +686,13 @@ int fx_index_destroy(fx_index *ix) {
     FX_GUARD({
         if (ix) {
             set_dev(ix->dev);
-            cudaStreamSynchronize(ix->st);
-            delete ix;
+            cudaStream_t st = ix->st;
+            const bool own = ix->owns_stream;
+            {
+                StreamGuard sg_(st);
+                delete ix;
+            }
+            if (own && st) cudaStreamDestroy(st);
         }
     })
 }
@@ -684,6 +705,7 @@ int fx_lookup(fx_index *ix, int32_t class_enc, int32_t k_x, int64_t *out_ids, in
         *out_n = 0;
         if (class_enc < 0 || class_enc > ix->V) return FX_OK;  // postings.get(c, []) -> []
         set_dev(ix->dev);
+        StreamGuard sg_(ix->st);
         const int64_t a = ix->h_post_off[class_enc], b = ix->h_post_off[class_enc + 1];
         if (b == a) return FX_OK;
         std::vector<int32_t> cidx(b - a), rk(b - a);
@@ -707,6 +729,7 @@ int fx_session_create(fx_index *ix, const int32_t *rep_label, const int32_t *rep
     FX_GUARD({
         if (!ix || !out) throw Error{FX_E_USAGE, "null argument"};
         set_dev(ix->dev);
+        StreamGuard sg_(ix->st);
         fx_session *ss = new fx_session();
         try {
             ss->ix = ix;
@@ -750,6 +773,7 @@ int fx_query(fx_session *ss, int32_t class_enc, int32_t k_x, int32_t mode, int32
         if (mode == 1) kx = (int)ix->K;
         if (kx < 1 || kx > ix->K) throw Error{FX_E_KX_TOO_LARGE, "k_x outside [1, K]"};
         set_dev(ix->dev);
+        StreamGuard sg_(ix->st);
         run_query(ss, class_enc, kx, mode, keep_label, batch_step, has_range, t0, t1, res);
     })
 }
@@ -758,6 +782,7 @@ int fx_query_fetch(fx_session *ss, int64_t *frame_ids, int64_t *object_ids) {
     FX_GUARD({
         if (!ss) throw Error{FX_E_USAGE, "null session"};
         set_dev(ss->ix->dev);
+        StreamGuard sg_(ss->ix->st);
         d2h(frame_ids, ss->out_f.p, ss->nf, ss->ix->st);
         d2h(object_ids, ss->out_o.p, ss->no, ss->ix->st);
         FX_CUDA(cudaStreamSynchronize(ss->ix->st));

@@ -50,6 +50,19 @@ void count_launch();
 // device buffers
 // ---------------------------------------------------------------------------
 
+// Stream-ordered allocation from the device's default memory pool
+// (cudaMallocAsync / cudaFreeAsync): no device-wide synchronisation on free,
+// cached blocks are reused.  Every C-ABI entry point sets the stream its
+// handle works on (StreamGuard); DevBuf allocates and frees on it.
+cudaStream_t &cur_stream();
+void init_pool(int device);
+
+struct StreamGuard {
+    cudaStream_t prev;
+    explicit StreamGuard(cudaStream_t s) : prev(cur_stream()) { cur_stream() = s; }
+    ~StreamGuard() { cur_stream() = prev; }
+};
+
 template <typename T>
 struct DevBuf {
     T *p = nullptr;
@@ -59,7 +72,7 @@ struct DevBuf {
     DevBuf &operator=(const DevBuf &) = delete;
     ~DevBuf() { release(); }
     void release() {
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, cur_stream());
         p = nullptr;
         n = 0;
     }
@@ -68,7 +81,7 @@ struct DevBuf {
         if (want <= n && p) return;
         release();
         size_t bytes = sizeof(T) * (want ? want : 1);
-        FX_CUDA(cudaMalloc(&p, bytes));
+        FX_CUDA(cudaMallocAsync((void **)&p, bytes, cur_stream()));
         n = want ? want : 1;
     }
     // ensure capacity >= want, preserving the first `keep` elements
@@ -77,12 +90,9 @@ struct DevBuf {
         size_t cap = n ? n : 16;
         while (cap < want) cap *= 2;
         T *q = nullptr;
-        FX_CUDA(cudaMalloc(&q, sizeof(T) * cap));
+        FX_CUDA(cudaMallocAsync((void **)&q, sizeof(T) * cap, st));
         if (p && keep) FX_CUDA(cudaMemcpyAsync(q, p, sizeof(T) * keep, cudaMemcpyDeviceToDevice, st));
-        if (p) {
-            FX_CUDA(cudaStreamSynchronize(st));
-            cudaFree(p);
-        }
+        if (p) FX_CUDA(cudaFreeAsync(p, st));
         p = q;
         n = cap;
     }

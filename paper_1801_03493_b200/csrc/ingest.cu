@@ -137,8 +137,10 @@ __global__ void __launch_bounds__(256) k_screen(int nA, int64_t a0, const char *
                                                const int64_t *__restrict__ nB_dev, int nB_max, FB fb,
                                                float *__restrict__ out, int64_t ld) {
     const int nB = nB_dev ? (int)*nB_dev : nB_max;
-    const int tb = blockIdx.x * SC_T, ta = blockIdx.y * SC_T;
-    if (tb >= nB || ta >= nA) return;
+    // persistent over the (column, row) tiles that exist for the device-side nB
+    const int ncol = (nB + SC_T - 1) / SC_T, nrow = (nA + SC_T - 1) / SC_T;
+    for (int tile = blockIdx.x; tile < ncol * nrow; tile += gridDim.x) {
+    const int tb = (tile % ncol) * SC_T, ta = (tile / ncol) * SC_T;
     __shared__ float As[SC_K][SC_T + 1];
     __shared__ float Bs[SC_K][SC_T + 1];
     const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
@@ -193,6 +195,8 @@ __global__ void __launch_bounds__(256) k_screen(int nA, int64_t a0, const char *
             int b = tb + tx * 4 + j;
             if (b < nB) out[(int64_t)a * ld + b] = sqrtf(tot[i][j]);
         }
+    }
+    __syncthreads();
     }
 }
 
@@ -1247,15 +1251,29 @@ __global__ void __launch_bounds__(256) k_fold(int D, int64_t c0, const int64_t *
         __syncthreads();
         const int nch = min(256, p1 - cs);
         if (k < D) {
-            for (int i = 0; i < nch; i += 16) {
-                double v[16];
+            // software-pipelined: the next 16 rows are in flight while the
+            // current 16 are added (two register groups, 32 loads outstanding)
+            T va[16], vb[16];
 #pragma unroll
-                for (int j = 0; j < 16; j++) v[j] = to_d(__ldg(rows[(i + j) & 255] + k));
+            for (int j = 0; j < 16; j++) va[j] = __ldg(rows[j] + k);
+            for (int i = 0; i < nch; i += 32) {
+#pragma unroll
+                for (int j = 0; j < 16; j++) vb[j] = __ldg(rows[(i + 16 + j) & 255] + k);
 #pragma unroll
                 for (int j = 0; j < 16; j++) {
                     const unsigned char fl = (i + j < nch) ? first[i + j] : 2;
-                    const double add = dadd(s, v[j]);
-                    s = fl == 1 ? v[j] : (fl == 0 ? add : s);
+                    const double v = to_d(va[j]);
+                    const double add = dadd(s, v);
+                    s = fl == 1 ? v : (fl == 0 ? add : s);
+                }
+#pragma unroll
+                for (int j = 0; j < 16; j++) va[j] = __ldg(rows[(i + 32 + j) & 255] + k);
+#pragma unroll
+                for (int j = 0; j < 16; j++) {
+                    const unsigned char fl = (i + 16 + j < nch) ? first[i + 16 + j] : 2;
+                    const double v = to_d(vb[j]);
+                    const double add = dadd(s, v);
+                    s = fl == 1 ? v : (fl == 0 ? add : s);
                 }
             }
         }
@@ -1408,7 +1426,7 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             launch_screen_tc(B, c0, s->frow.p, s->fnorm.p, D, s->ctr.p + C_NSNAP, (int)s->ld, s->C32.p,
                              s->snap_slot.p, s->s_cn2.p, s->dist.p, s->ld, st);
         } else {
-            dim3 grid((unsigned)cdiv(s->ld, SC_T), (unsigned)cdiv(B, SC_T));
+            const unsigned grid = (unsigned)std::min<int64_t>(cdiv(s->ld, SC_T) * cdiv(B, SC_T), 148 * 8);
             FromSnapshot fb{s->C32.p, s->snap_slot.p, D};
             k_screen<T, FromSnapshot><<<grid, 256, 0, st>>>(B, c0, s->frow.p, D, s->ctr.p + C_NSNAP, (int)s->ld, fb,
                                                             s->dist.p, s->ld);
@@ -1420,7 +1438,7 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
                 B, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p, s->snap_slot.p, s->fnorm.p, c0, sm, s->cfg.t,
                 s->res_col.p, s->res_pos.p, s->ctr.p + C_NRES);
             FX_LAUNCHED();
-            dim3 grid((unsigned)cdiv(B, SC_T), (unsigned)cdiv(B, SC_T));
+            const unsigned grid = (unsigned)std::min<int64_t>(cdiv(B, SC_T) * cdiv(B, SC_T), 148 * 8);
             FromResidual<T> fb{s->frow.p, c0, s->res_pos.p};
             k_screen<T, FromResidual<T>><<<grid, 256, 0, st>>>(B, c0, s->frow.p, D, s->ctr.p + C_NRES, B, fb, s->dres.p, B);
             FX_LAUNCHED();
@@ -1492,7 +1510,12 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             const PwPlan &P = *s->plan_host;
             size_t smem = (size_t)s->B * (8 + 4 * 8 + 2 + 1) + 16 + sizeof(double) * (P.n_chains + P.n_leaves + P.n_ops + 8);
             auto kern = k_resolve<T>;
-            FX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            static size_t smem_set[2] = {0, 0};
+            size_t &cur = smem_set[sizeof(T) == 8];
+            if (smem > cur) {
+                FX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                cur = smem;
+            }
             kern<<<1, RS_THREADS, smem, st>>>(A);
             FX_LAUNCHED();
         }
@@ -1535,10 +1558,7 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             FX_LAUNCHED();
             s->tstop();
         }
-        if (s->pending.size() > 64) {
-            FX_CUDA(cudaStreamSynchronize(st));
-            s->tcollect();
-        }
+
     }
 }
 

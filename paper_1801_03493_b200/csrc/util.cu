@@ -9,6 +9,21 @@ namespace fx {
 static thread_local std::string g_last_error;
 static std::atomic<int64_t> g_launches{0};
 
+static thread_local cudaStream_t g_cur_stream = nullptr;
+cudaStream_t &cur_stream() { return g_cur_stream; }
+
+void init_pool(int device) {
+    static std::mutex mu;
+    static bool done[64] = {false};
+    std::lock_guard<std::mutex> lk(mu);
+    if (device < 0 || device >= 64 || done[device]) return;
+    cudaMemPool_t pool;
+    FX_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t thr = ~0ull;  // keep freed blocks cached in the pool
+    FX_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    done[device] = true;
+}
+
 void set_error(const std::string &msg) { g_last_error = msg; }
 const char *last_error() { return g_last_error.c_str(); }
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
@@ -184,8 +199,6 @@ static int64_t scan_generic(int64_t n, F get, int64_t *out_excl, cudaStream_t st
     if (sync) {
         FX_CUDA(cudaMemcpyAsync(&h, d_total, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
         FX_CUDA(cudaStreamSynchronize(st));
-    } else {
-        FX_CUDA(cudaStreamSynchronize(st));  // ts freed on return
     }
     return h;
 }
