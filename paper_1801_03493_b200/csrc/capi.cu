@@ -167,6 +167,7 @@ int fx_stream_create(const fx_stream_config *cfg, fx_stream **out) {
         if (cfg->feat_type != FX_F32 && cfg->feat_type != FX_F64) throw Error{FX_E_USAGE, "bad feat_type"};
         set_dev(cfg->device);
         init_pool(cfg->device);
+        StreamGuard sg_(nullptr);
         fx_stream *s = new fx_stream();
         try {
             s->cfg = *cfg;
@@ -759,7 +760,11 @@ int fx_session_create(fx_index *ix, const int32_t *rep_label, const int32_t *rep
 
 int fx_session_destroy(fx_session *ss) {
     FX_GUARD({
-        if (ss) delete ss;
+        if (ss) {
+            set_dev(ss->ix->dev);
+            StreamGuard sg_(ss->ix->st);
+            delete ss;
+        }
     })
 }
 
