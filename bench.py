@@ -203,6 +203,7 @@ def main():
     torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
+    host_split.update(ingest_call_ms=0.0, finalize_call_ms=0.0)
     launches0 = L.fx_kernel_launches()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
@@ -296,7 +297,7 @@ def main():
             "ingest": {"clusters": rep.clusters_emitted, "classified": rep.objects_classified,
                        "distance_computations": rep.distance_computations, "exact_rechecks": rep.exact_rechecks,
                        "fast_decisions": counters["fast"],
-                       "resolve_profile": {k: counters[k] for k in counters if k.startswith("cyc_")
+                       "resolve_profile": {k: counters[k] for k in counters if k.startswith(("cyc_", "conf_"))
                                            or k in ("windows", "seq_steps")}},
         }
         print(json.dumps(line))

@@ -275,7 +275,8 @@ struct ResolveArgs {
     int32_t *cluster_of, *mrank, *frank;
     const PwPlan *plan;
     int32_t *s_grp;
-    long long *prof;  // [8] cycles: A, B1B2, CD, confirm, E, seq; [6] windows, [7] seq steps
+    long long *prof;  // [16] cycles: A, B1B2, CD, confirm, E, seq; [6] windows, [7] seq steps; [8..15] confirms by batch bucket
+    int batch_no;
     const int32_t *sum_slot;
     const float *sum_d1, *sum_e1, *sum_lbr;
 };
@@ -502,7 +503,64 @@ __global__ void k_row_summary(int nA, const int64_t *__restrict__ ctr, const flo
     }
 }
 
+
+// ---- group-chain scans for the resolve's parallel segments -----------------
+// Element i of a group's stream-ordered member list joins with n = nf0 + i + 1
+// featured members; its drift map is d -> a d + c with a = 1 + 1/n (+ slack),
+// c = ub0/n (+ slack), fp32 rounded up.  One warp scans list indices [lo, hi).
+struct GroupCtx {
+    int off, nf0, sl;
+    float cn;
+};
+
+__device__ __forceinline__ void elem_map(const GroupCtx &G, int i, float ub0, float &a, float &c) {
+    const float inv = __frcp_ru((float)(G.nf0 + i + 1));
+    a = __fadd_ru(__fadd_ru(1.f, inv), 2.5e-7f);
+    c = __fadd_ru(__fmul_ru(ub0, inv), __fmul_ru(1e-13f, __fadd_ru(G.cn, ub0)) + 1e-30f);
+}
+
+__device__ __forceinline__ void warp_affine_scan(float &a, float &c, int &w, int lane) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const float ap = __shfl_up_sync(0xffffffffu, a, o), cp = __shfl_up_sync(0xffffffffu, c, o);
+        const int wp = __shfl_up_sync(0xffffffffu, w, o);
+        if (lane >= o) {
+            c = __fmaf_ru(a, cp, c);
+            a = __fmul_ru(a, ap);
+            w += wp;
+        }
+    }
+}
+
+// compose the maps of [lo, hi) -> (A, C); also the sum of member weights
+// 1 + dup_run (sizes, needed by the commit)
+__device__ void gc_compose(const GroupCtx &G, int lo, int hi, const int32_t *glist, const float *seg_ub0,
+                           const int32_t *dup_run, int64_t c0, float &A, float &C, int &W) {
+    const int lane = threadIdx.x & 31;
+    float Ac = 1.f, Cc = 0.f;
+    int Wc = 0;
+    for (int i0 = lo; i0 < hi; i0 += 32) {
+        const int i = i0 + lane;
+        float a = 1.f, c = 0.f;
+        int w = 0;
+        if (i < hi) {
+            const int p = glist[G.off + i];
+            elem_map(G, i, seg_ub0[p], a, c);
+            w = 1 + dup_run[c0 + p];
+        }
+        warp_affine_scan(a, c, w, lane);
+        const float a31 = __shfl_sync(0xffffffffu, a, 31), c31 = __shfl_sync(0xffffffffu, c, 31);
+        Cc = __fmaf_ru(a31, Cc, c31);
+        Ac = __fmul_ru(a31, Ac);
+        Wc += __shfl_sync(0xffffffffu, w, 31);
+    }
+    A = Ac;
+    C = Cc;
+    W = Wc;
+}
+
 constexpr int RS_MAXGRP = 1024;
+constexpr int RS_BIGGRP = 512;  // groups longer than this are scanned by all warps
 constexpr int RS_WIN0 = 64;
 
 __device__ __forceinline__ double drift_step(double dr, double ub, int nf, double cn) {
@@ -545,6 +603,9 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
     __shared__ double s_md1, s_md2;
     __shared__ int s_md1_slot;
     __shared__ double wmd1[RS_WARPS], wmd2[RS_WARPS];
+    __shared__ float wA[RS_WARPS], wC[RS_WARPS], wcarry[RS_WARPS + 1];
+    __shared__ int wW[RS_WARPS], wszc[RS_WARPS + 1];
+    __shared__ int grp_ncommit[RS_MAXGRP];
     __shared__ int wmds[RS_WARPS];
 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -582,7 +643,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
     for (int b = tid; b < B; b += blockDim.x) sh_slot_of[b] = -1;
     __syncthreads();
 
-    int b = 0, win = RS_WIN0;
+    int b = 0, win = min(B, 1024);
     while (b < B) {
         // =================== parallel segment: speculate every object in
         // [b, e_end) joins its nearest candidate, verify with bounds, commit
@@ -711,48 +772,87 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
                 if (g >= 0) glist[grp_off[g] + seg_nf[p]] = p;
             }
         __syncthreads();
-        // pass B2: drift bound along every group's chain.  One warp per group
-        // over its contiguous, stream-ordered member list; the recurrence
-        // d' = d (1 + 1/n) + ub0/n + slack is affine in d, so each 32-slice is an
-        // inclusive warp scan of affine maps (fp32, rounded up: every grouping
-        // yields an upper bound).
-        if (!overflow)
-        for (int g = wid; g < ngrp; g += RS_WARPS) {
-            const int sl = grp_slot[g];
-            float dr = __double2float_ru(A.s_drift[sl]);
-            const int nf0 = A.s_nfeat[sl];
-            const float cn = sqrtf(A.s_cn2[sl]) * 1.00001f;
-            const int off = grp_off[g], cnt = grp_cnt[g];
-            for (int i0 = 0; i0 < cnt; i0 += 32) {
-                const int i = i0 + lane;
-                const bool match = i < cnt;
-                const int p = match ? glist[off + i] : 0;
-                float a = 1.f, c = 0.f, ub0 = 0.f;
-                if (match) {
-                    ub0 = seg_ub0[p];
-                    const float inv = __frcp_ru((float)(nf0 + i + 1));
-                    a = __fadd_ru(__fadd_ru(1.f, inv), 2.5e-7f);
-                    c = __fadd_ru(__fmul_ru(ub0, inv), __fmul_ru(1e-13f, __fadd_ru(cn, ub0)) + 1e-30f);
-                    seg_nf[p] = nf0 + i;
-                }
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const float ap = __shfl_up_sync(0xffffffffu, a, o), cp = __shfl_up_sync(0xffffffffu, c, o);
-                    if (lane >= o) {
-                        c = __fmaf_ru(a, cp, c);
-                        a = __fmul_ru(a, ap);
-                    }
-                }
-                float ae = __shfl_up_sync(0xffffffffu, a, 1), ce = __shfl_up_sync(0xffffffffu, c, 1);
+        // pass B2: drift bound along every group's chain (stream order).  The
+        // recurrence d' = d (1 + 1/n) + ub0/n + slack is affine in d: each
+        // 32-slice is an inclusive warp scan of affine maps (fp32, rounded
+        // up -- every grouping yields an upper bound).  Long groups are split
+        // over all warps (compose per warp, carry across warps, apply).
+        if (!overflow) {
+            for (int g = 0; g < ngrp; g++) {
+                const int cnt = grp_cnt[g];
+                if (cnt <= RS_BIGGRP) continue;
+                const int sl = grp_slot[g];
+                GroupCtx G{grp_off[g], A.s_nfeat[sl], sl, sqrtf(A.s_cn2[sl]) * 1.00001f};
+                const int seg = (cnt + RS_WARPS - 1) / RS_WARPS;
+                const int lo = min(cnt, wid * seg), hi = min(cnt, lo + seg);
+                float Aw, Cw;
+                int Ww;
+                gc_compose(G, lo, hi, glist, seg_ub0, A.dup_run, A.c0, Aw, Cw, Ww);
                 if (lane == 0) {
-                    ae = 1.f;
-                    ce = 0.f;
+                    wA[wid] = Aw;
+                    wC[wid] = Cw;
                 }
-                if (match) seg_ub[p] = (double)__fadd_ru(ub0, __fmaf_ru(ae, dr, ce));
-                const float a31 = __shfl_sync(0xffffffffu, a, 31), c31 = __shfl_sync(0xffffffffu, c, 31);
-                dr = __fmaf_ru(a31, dr, c31);
+                __syncthreads();
+                if (tid == 0) {
+                    float d = __double2float_ru(A.s_drift[sl]);
+                    for (int w = 0; w < RS_WARPS; w++) {
+                        wcarry[w] = d;
+                        d = __fmaf_ru(wA[w], d, wC[w]);
+                    }
+                    grp_drift[g] = (double)d;
+                }
+                __syncthreads();
+                float dr = wcarry[wid];
+                for (int i0 = lo; i0 < hi; i0 += 32) {
+                    const int i = i0 + lane;
+                    float a = 1.f, c = 0.f, ub0 = 0.f;
+                    int w = 0, p = 0;
+                    if (i < hi) {
+                        p = glist[G.off + i];
+                        ub0 = seg_ub0[p];
+                        elem_map(G, i, ub0, a, c);
+                        seg_nf[p] = G.nf0 + i;
+                    }
+                    warp_affine_scan(a, c, w, lane);
+                    float ae = __shfl_up_sync(0xffffffffu, a, 1), ce = __shfl_up_sync(0xffffffffu, c, 1);
+                    if (lane == 0) {
+                        ae = 1.f;
+                        ce = 0.f;
+                    }
+                    if (i < hi) seg_ub[p] = (double)__fadd_ru(ub0, __fmaf_ru(ae, dr, ce));
+                    const float a31 = __shfl_sync(0xffffffffu, a, 31), c31 = __shfl_sync(0xffffffffu, c, 31);
+                    dr = __fmaf_ru(a31, dr, c31);
+                }
+                __syncthreads();
             }
-            if (lane == 0) grp_drift[g] = (double)dr;
+            for (int g = wid; g < ngrp; g += RS_WARPS) {
+                const int cnt = grp_cnt[g];
+                if (cnt > RS_BIGGRP) continue;
+                const int sl = grp_slot[g];
+                GroupCtx G{grp_off[g], A.s_nfeat[sl], sl, sqrtf(A.s_cn2[sl]) * 1.00001f};
+                float dr = __double2float_ru(A.s_drift[sl]);
+                for (int i0 = 0; i0 < cnt; i0 += 32) {
+                    const int i = i0 + lane;
+                    float a = 1.f, c = 0.f, ub0 = 0.f;
+                    int w = 0, p = 0;
+                    if (i < cnt) {
+                        p = glist[G.off + i];
+                        ub0 = seg_ub0[p];
+                        elem_map(G, i, ub0, a, c);
+                        seg_nf[p] = G.nf0 + i;
+                    }
+                    warp_affine_scan(a, c, w, lane);
+                    float ae = __shfl_up_sync(0xffffffffu, a, 1), ce = __shfl_up_sync(0xffffffffu, c, 1);
+                    if (lane == 0) {
+                        ae = 1.f;
+                        ce = 0.f;
+                    }
+                    if (i < cnt) seg_ub[p] = (double)__fadd_ru(ub0, __fmaf_ru(ae, dr, ce));
+                    const float a31 = __shfl_sync(0xffffffffu, a, 31), c31 = __shfl_sync(0xffffffffu, c, 31);
+                    dr = __fmaf_ru(a31, dr, c31);
+                }
+                if (lane == 0) grp_drift[g] = (double)dr;
+            }
         }
         __syncthreads();
         long long t2 = clock64();
@@ -837,7 +937,14 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
             f = s_fail;
             if (f >= e_end || seg_flag[f] != 1) break;
             const double dx = exact_dist<T>(A, f, seg_key[f], sh_slot_of, mlist, scratch, seg_nf[f]);
-            if (tid == 0) s_exact++;
+            if (tid == 0) {
+                s_exact++;
+                // diagnostics: batch bucket (0,1-7,8-15,16-31,32-63,64-127,128+) and young slots (nfeat < 16)
+                const int bn = A.batch_no;
+                const int bk = bn == 0 ? 0 : bn < 8 ? 1 : bn < 16 ? 2 : bn < 32 ? 3 : bn < 64 ? 4 : bn < 128 ? 5 : 6;
+                A.prof[8 + bk]++;
+                if (seg_nf[f] < 16) A.prof[15]++;
+            }
             if (dx > A.T) break;  // nearest is beyond T: the object seeds (sequential path)
             f++;
             __syncthreads();
@@ -847,75 +954,125 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
         long long t4 = clock64();
         if (tid == 0) A.prof[3] += t4 - t3;
         // pass E: commit [b, f) -- same maps as pass B2, applied to the slot state
-        for (int g = wid; g < ngrp; g += RS_WARPS) {
-            const int sl = grp_slot[g];
-            float dr = __double2float_ru(A.s_drift[sl]);
-            const int nf0 = A.s_nfeat[sl], pend0 = A.s_pend[sl];
-            int sz = A.s_size[sl];
-            const int cid = A.s_cid[sl];
-            const float cn = sqrtf(A.s_cn2[sl]) * 1.00001f;
-            const int off = grp_off[g], cnt = overflow ? 0 : grp_cnt[g];
-            int ncommit = 0;
-            for (int i0 = 0; i0 < cnt; i0 += 32) {
-                const int i = i0 + lane;
-                const int p = i < cnt ? glist[off + i] : INT_MAX;
-                const bool match = p < f;
-                const unsigned mask = __ballot_sync(0xffffffffu, match);
-                if (!mask) break;
-                float a = 1.f, c = 0.f;
-                int w = 0;
-                int64_t cc = 0;
-                if (match) {
-                    cc = A.c0 + p;
-                    const float ub0 = seg_ub0[p];
-                    const float inv = __frcp_ru((float)(nf0 + i + 1));
-                    a = __fadd_ru(__fadd_ru(1.f, inv), 2.5e-7f);
-                    c = __fadd_ru(__fmul_ru(ub0, inv), __fmul_ru(1e-13f, __fadd_ru(cn, ub0)) + 1e-30f);
-                    w = 1 + A.dup_run[cc];
-                }
-                int wsum = w;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const float ap = __shfl_up_sync(0xffffffffu, a, o), cp = __shfl_up_sync(0xffffffffu, c, o);
-                    const int wp = __shfl_up_sync(0xffffffffu, wsum, o);
-                    if (lane >= o) {
-                        c = __fmaf_ru(a, cp, c);
-                        a = __fmul_ru(a, ap);
-                        wsum += wp;
+        if (!overflow) {
+            // members of a group before f form a prefix of its (stream-ordered) list
+            for (int g = wid; g < ngrp; g += RS_WARPS) {
+                const int off = grp_off[g], cnt = grp_cnt[g];
+                int lo = 0, hi = cnt;  // first list index with p >= f
+                if (lane == 0) {
+                    while (lo < hi) {
+                        const int mid = (lo + hi) >> 1;
+                        if (glist[off + mid] < f) lo = mid + 1; else hi = mid;
                     }
+                    grp_ncommit[g] = lo;
                 }
-                if (match) {
-                    const int64_t obj = A.cls_obj[cc];
-                    A.cluster_of[obj] = cid;
-                    A.mrank[obj] = sz + wsum - w;
-                    A.frank[obj] = nf0 + i;
-                    A.pend_rank[p] = pend0 + i;
-                    A.slot_of[p] = sl;
-                    sh_slot_of[p] = sl;
-                }
-                const float a31 = __shfl_sync(0xffffffffu, a, 31), c31 = __shfl_sync(0xffffffffu, c, 31);
-                dr = __fmaf_ru(a31, dr, c31);
-                ncommit += __popc(mask);
-                sz += __shfl_sync(0xffffffffu, wsum, 31);
-                if (mask != 0xffffffffu) break;
             }
-            if (lane == 0) {
-                if (ncommit > 0) {
-                    A.s_drift[sl] = (double)dr;
-                    A.s_nfeat[sl] = nf0 + ncommit;
-                    A.s_size[sl] = sz;
-                    A.s_pend[sl] = pend0 + ncommit;
+            __syncthreads();
+            auto commit_range = [&](const GroupCtx &G, int cid, int lo, int hi, float dr, int sz, int pend0) {
+                for (int i0 = lo; i0 < hi; i0 += 32) {
+                    const int i = i0 + lane;
+                    float a = 1.f, c = 0.f;
+                    int w = 0, p = 0;
+                    int64_t cc = 0;
+                    if (i < hi) {
+                        p = glist[G.off + i];
+                        cc = A.c0 + p;
+                        elem_map(G, i, seg_ub0[p], a, c);
+                        w = 1 + A.dup_run[cc];
+                    }
+                    warp_affine_scan(a, c, w, lane);
+                    if (i < hi) {
+                        const int64_t obj = A.cls_obj[cc];
+                        A.cluster_of[obj] = cid;
+                        A.mrank[obj] = sz + w - (1 + A.dup_run[cc]);
+                        A.frank[obj] = G.nf0 + i;
+                        A.pend_rank[p] = pend0 + i;
+                        A.slot_of[p] = G.sl;
+                        sh_slot_of[p] = G.sl;
+                    }
+                    const float a31 = __shfl_sync(0xffffffffu, a, 31), c31 = __shfl_sync(0xffffffffu, c, 31);
+                    dr = __fmaf_ru(a31, dr, c31);
+                    sz += __shfl_sync(0xffffffffu, w, 31);
+                }
+                return dr;
+            };
+            for (int g = 0; g < ngrp; g++) {
+                const int n_c = grp_ncommit[g];
+                if (n_c <= RS_BIGGRP) continue;
+                const int sl = grp_slot[g];
+                GroupCtx G{grp_off[g], A.s_nfeat[sl], sl, sqrtf(A.s_cn2[sl]) * 1.00001f};
+                const int seg = (n_c + RS_WARPS - 1) / RS_WARPS;
+                const int lo = min(n_c, wid * seg), hi = min(n_c, lo + seg);
+                float Aw, Cw;
+                int Ww;
+                gc_compose(G, lo, hi, glist, seg_ub0, A.dup_run, A.c0, Aw, Cw, Ww);
+                if (lane == 0) {
+                    wA[wid] = Aw;
+                    wC[wid] = Cw;
+                    wW[wid] = Ww;
+                }
+                __syncthreads();
+                if (tid == 0) {
+                    float d = __double2float_ru(A.s_drift[sl]);
+                    int sz = A.s_size[sl];
+                    for (int w = 0; w < RS_WARPS; w++) {
+                        wcarry[w] = d;
+                        wszc[w] = sz;
+                        d = __fmaf_ru(wA[w], d, wC[w]);
+                        sz += wW[w];
+                    }
+                    wcarry[RS_WARPS] = d;
+                    wszc[RS_WARPS] = sz;
+                }
+                __syncthreads();
+                commit_range(G, A.s_cid[sl], lo, hi, wcarry[wid], wszc[wid], A.s_pend[sl]);
+                __syncthreads();
+                if (tid == 0) {
+                    const int pend0 = A.s_pend[sl];
+                    A.s_drift[sl] = (double)wcarry[RS_WARPS];
+                    A.s_nfeat[sl] = G.nf0 + n_c;
+                    A.s_size[sl] = wszc[RS_WARPS];
+                    A.s_pend[sl] = pend0 + n_c;
                     if (pend0 == 0) {
                         const int di = atomicAdd(&s_ndirty, 1);
                         A.s_didx[sl] = di;
                         A.dirty[di] = sl;
                     }
                 }
-                A.s_grp[sl] = -1;
+                __syncthreads();
+            }
+            for (int g = wid; g < ngrp; g += RS_WARPS) {
+                const int n_c = grp_ncommit[g];
+                const int sl = grp_slot[g];
+                if (n_c > 0 && n_c <= RS_BIGGRP) {
+                    GroupCtx G{grp_off[g], A.s_nfeat[sl], sl, sqrtf(A.s_cn2[sl]) * 1.00001f};
+                    const int pend0 = A.s_pend[sl];
+                    const int sz0 = A.s_size[sl];
+                    float Aw, Cw;
+                    int Ww;
+                    // sizes after the commit need the weight total: compose first (cheap for short groups)
+                    gc_compose(G, 0, n_c, glist, seg_ub0, A.dup_run, A.c0, Aw, Cw, Ww);
+                    const float d0 = __double2float_ru(A.s_drift[sl]);
+                    const float d1 = commit_range(G, A.s_cid[sl], 0, n_c, d0, sz0, pend0);
+                    if (lane == 0) {
+                        A.s_drift[sl] = (double)d1;
+                        A.s_nfeat[sl] = G.nf0 + n_c;
+                        A.s_size[sl] = sz0 + Ww;
+                        A.s_pend[sl] = pend0 + n_c;
+                        if (pend0 == 0) {
+                            const int di = atomicAdd(&s_ndirty, 1);
+                            A.s_didx[sl] = di;
+                            A.dirty[di] = sl;
+                        }
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) A.s_grp[sl] = -1;
             }
         }
         if (overflow) {
             __syncthreads();
+            for (int g = tid; g < ngrp; g += blockDim.x) A.s_grp[grp_slot[g]] = -1;
             for (int p = b + tid; p < e_end; p += blockDim.x) {
                 const int key = seg_key[p];
                 if (key >= 0 && A.s_grp[key] == RS_MAXGRP) A.s_grp[key] = -1;
@@ -1211,7 +1368,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
 // ---------------------------------------------------------------------------
 
 template <typename T>
-__global__ void __launch_bounds__(256) k_fold(int D, int64_t c0, const int64_t *__restrict__ ctr,
+__global__ void __launch_bounds__(64) k_fold(int D, int64_t c0, const int64_t *__restrict__ ctr,
                                               const int32_t *__restrict__ dirty, const int32_t *__restrict__ dirty_off,
                                               const int32_t *__restrict__ pend_list, const char *const *__restrict__ frow,
                                               double *__restrict__ S, float *__restrict__ C32,
@@ -1235,19 +1392,21 @@ __global__ void __launch_bounds__(256) k_fold(int D, int64_t c0, const int64_t *
     for (int cs = p0; cs < p1; cs += 256) {
         // stage the chunk's row pointers (members already folded by the
         // resolve's exact path are skipped)
-        const int p = cs + (int)threadIdx.x;
-        const T *r = nullptr;
-        unsigned char fst = 0;
-        if (p < p1) {
-            const int b = pend_list[p];
-            if (b >= fp) {
-                r = (const T *)frow[c0 + b];
-                fst = b == sp;
+        for (int t = threadIdx.x; t < 256; t += blockDim.x) {
+            const int p = cs + t;
+            const T *r = nullptr;
+            unsigned char fst = 0;
+            if (p < p1) {
+                const int b = pend_list[p];
+                if (b >= fp) {
+                    r = (const T *)frow[c0 + b];
+                    fst = b == sp;
+                }
             }
+            // padded / skipped members point at a valid row and are masked (flag 2)
+            rows[t] = r ? r : (const T *)frow[c0];
+            first[t] = r ? fst : 2;
         }
-        // padded / skipped members point at a valid row and are masked (flag 2)
-        rows[threadIdx.x] = r ? r : (const T *)frow[c0];
-        first[threadIdx.x] = r ? fst : 2;
         __syncthreads();
         const int nch = min(256, p1 - cs);
         if (k < D) {
@@ -1415,10 +1574,11 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
     const double gam = 1.953125e-03 + (double)D * 2.384185791015625e-07;
     const ScreenModel sm{s->tc_screen ? 1 : 0, rel, absc, (float)(2.0 * gam * 1.01), (float)(256.0 * 5.9604644775390625e-08)};
     for (int64_t c0 = c_begin, B = 0; c0 < c_end; c0 += B) {
-        // young clusters have loose drift bounds: start a stream with small
-        // batches (fresh snapshots) and double up to the configured size
-        const int64_t grow = s->batch_no < 20 ? ((int64_t)64 << s->batch_no) : s->B;
-        B = (int)std::min<int64_t>(std::min<int64_t>(s->B, grow), c_end - c0);
+        // the drift bound grows like (batch size / objects so far): keep batches
+        // at <= 1/4 of the stream's age so young clusters stay decidable by bounds
+        const int64_t age = std::max<int64_t>(c0, 0);
+        const int64_t cap = std::max<int64_t>(64, (age / 4 / 64) * 64);
+        B = (int)std::min<int64_t>(std::min<int64_t>(s->B, cap), c_end - c0);
         s->t_ms[6] += 1.0;
         // 1. snapshot screen
         s->tstart(1);
@@ -1438,7 +1598,7 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
                 B, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p, s->snap_slot.p, s->fnorm.p, c0, sm, s->cfg.t,
                 s->res_col.p, s->res_pos.p, s->ctr.p + C_NRES);
             FX_LAUNCHED();
-            const unsigned grid = (unsigned)std::min<int64_t>(cdiv(B, SC_T) * cdiv(B, SC_T), 148 * 8);
+            const unsigned grid = (unsigned)std::min<int64_t>(cdiv(B, SC_T) * cdiv(B, SC_T), 148);
             FromResidual<T> fb{s->frow.p, c0, s->res_pos.p};
             k_screen<T, FromResidual<T>><<<grid, 256, 0, st>>>(B, c0, s->frow.p, D, s->ctr.p + C_NRES, B, fb, s->dres.p, B);
             FX_LAUNCHED();
@@ -1503,6 +1663,7 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             A.plan = s->plan.p;
             A.s_grp = s->s_grp.p;
             A.prof = (long long *)s->prof.p;
+            A.batch_no = (int)s->batch_no;
             A.sum_slot = s->sum_slot.p;
             A.sum_d1 = s->sum_d1.p;
             A.sum_e1 = s->sum_e1.p;
@@ -1550,8 +1711,8 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             s->tstart(3);
             k_zero_cn2<<<(unsigned)cdiv(2 * s->B + 2, 256), 256, 0, st>>>(s->ctr.p, s->dirty.p, s->s_cn2.p);
             FX_LAUNCHED();
-            dim3 grid((unsigned)cdiv(D, 256), (unsigned)std::min<int64_t>(2 * (int64_t)B + 1, 1024));
-            k_fold<T><<<grid, 256, 0, st>>>(D, c0, s->ctr.p, s->dirty.p, s->dirty_off.p, s->pend_list.p, s->frow.p,
+            dim3 grid((unsigned)cdiv(D, 64), (unsigned)std::min<int64_t>(2 * (int64_t)B + 1, 512));
+            k_fold<T><<<grid, 64, 0, st>>>(D, c0, s->ctr.p, s->dirty.p, s->dirty_off.p, s->pend_list.p, s->frow.p,
                                             s->S.p, s->C32.p, s->s_nfeat.p, s->s_foldpos.p, s->s_seedpos.p,
                                             s->s_evicted.p, s->s_cid.p, s->s_size.p, s->s_cn2.p, s->fcent.p,
                                             s->cl_nfeat.p, s->cl_size.p);

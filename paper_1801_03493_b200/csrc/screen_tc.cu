@@ -85,7 +85,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
                                                            const float *__restrict__ C32,
                                                            const int32_t *__restrict__ snap,
                                                            const float *__restrict__ cn2, float *__restrict__ out,
-                                                           int64_t ld) {
+                                                           int64_t ld, int kchunk) {
+    // blockIdx.z selects the K range [z*kchunk, (z+1)*kchunk) (split-K when the
+    // tile grid alone cannot fill the machine; partials are atomically added)
     const int nB = (int)*nB_dev;
     const int tb = blockIdx.x * TC_N, ta = blockIdx.y * TC_M;
     if (tb >= nB || ta >= nA) return;
@@ -120,7 +122,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
     const uint32_t tmem = tmem_base;
     const uint32_t sbase = smem_u32(smem);
 
-    const int nk = (D + TC_KT - 1) / TC_KT;
+    const int kbeg = blockIdx.z * kchunk, kend = min(D, kbeg + kchunk);
+    const int nk = (kend - kbeg + TC_KT - 1) / TC_KT;
+    const bool split = gridDim.z > 1;
     // instruction descriptor: D=F32, A=B=TF32, K-major both, N=128, M=128
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TC_N >> 3) << 17) |
                            ((uint32_t)(TC_M >> 4) << 24);
@@ -128,8 +132,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
     for (int s = 0; s < TC_STAGES - 1; s++) {
         if (s < nk) {
             const uint32_t st = sbase + s * 2 * TC_TILE_BYTES;
-            load_tile(st, rowsA, s * TC_KT, D, fnorm);
-            load_tile(st + TC_TILE_BYTES, rowsB, s * TC_KT, D, fnorm);
+            load_tile(st, rowsA, kbeg + s * TC_KT, kend, fnorm);
+            load_tile(st + TC_TILE_BYTES, rowsB, kbeg + s * TC_KT, kend, fnorm);
         }
         asm volatile("cp.async.commit_group;\n" ::);
     }
@@ -160,8 +164,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
             const int ns = nt % TC_STAGES;
             if (nt >= TC_STAGES) mbar_wait(&bar_stage[ns], (uint32_t)(((nt / TC_STAGES) - 1) & 1));
             const uint32_t st = sbase + ns * 2 * TC_TILE_BYTES;
-            load_tile(st, rowsA, nt * TC_KT, D, fnorm);
-            load_tile(st + TC_TILE_BYTES, rowsB, nt * TC_KT, D, fnorm);
+            load_tile(st, rowsA, kbeg + nt * TC_KT, kend, fnorm);
+            load_tile(st + TC_TILE_BYTES, rowsB, kbeg + nt * TC_KT, kend, fnorm);
         }
         asm volatile("cp.async.commit_group;\n" ::);
     }
@@ -193,7 +197,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
                 const int b = tb + c0 + j;
                 if (b < nB) {
                     const float dot = __uint_as_float(v[j]);
-                    out[(int64_t)a * ld + b] = fa2 + cn2[snap[b]] - 2.f * dot;
+                    if (!split) {
+                        out[(int64_t)a * ld + b] = fa2 + cn2[snap[b]] - 2.f * dot;
+                    } else {
+                        atomicAdd(&out[(int64_t)a * ld + b], (blockIdx.z == 0 ? fa2 + cn2[snap[b]] : 0.f) - 2.f * dot);
+                    }
                 }
             }
         }
@@ -213,8 +221,14 @@ void launch_screen_tc(int nA, int64_t a0, const char *const *frow, const float *
         FX_CUDA(cudaFuncSetAttribute(k_screen_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)screen_tc_smem()));
         attr = true;
     }
-    dim3 grid((unsigned)cdiv(nB_max, TC_N), (unsigned)cdiv(nA, TC_M));
-    k_screen_tc<<<grid, TC_THREADS, screen_tc_smem(), st>>>(nA, a0, frow, fnorm, D, nB_dev, C32, snap, cn2, out, ld);
+    const int64_t tiles = cdiv(nB_max, TC_N) * cdiv(nA, TC_M);
+    int split = 1;
+    while (tiles * split * 2 <= 148 && D / (split * 2) >= 4 * TC_KT) split *= 2;
+    const int kchunk = (int)(cdiv(cdiv(D, split), TC_KT) * TC_KT);
+    if (split > 1) FX_CUDA(cudaMemsetAsync(out, 0, sizeof(float) * (size_t)nA * ld, st));
+    dim3 grid((unsigned)cdiv(nB_max, TC_N), (unsigned)cdiv(nA, TC_M), (unsigned)split);
+    k_screen_tc<<<grid, TC_THREADS, screen_tc_smem(), st>>>(nA, a0, frow, fnorm, D, nB_dev, C32, snap, cn2, out, ld,
+                                                            kchunk);
     FX_LAUNCHED();
 }
 
