@@ -192,6 +192,10 @@ def main():
         t2 = time.perf_counter()
         host_split["ingest_call_ms"] += (t1 - t0) * 1e3
         host_split["finalize_call_ms"] += (t2 - t1) * 1e3
+        if os.environ.get("BENCH_DEBUG"):
+            print(f"step: ingest {(t1 - t0) * 1e3:.1f} ms finalize {(t2 - t1) * 1e3:.1f} ms "
+                  + " ".join(f"{k}={v:.1f}" for k, v in s.timings().items() if k.startswith("host")),
+                  file=sys.stderr, flush=True)
         return out
 
     # warm-up
@@ -199,7 +203,8 @@ def main():
         s = make_stream()
         step(s)
         del s
-    streams = [make_stream() for _ in range(args.steps)]
+    # one step = create the stream engine, ingest the whole stream, finalize
+    # (seal + index build); the engine and its index are released right after
     torch.cuda.synchronize()
     if ws > 1:
         dist.barrier()
@@ -207,12 +212,19 @@ def main():
     launches0 = L.fx_kernel_launches()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    results = []
+    reports = []
+    last = None
     with Clocks(local) as clk:
-        ev0.record(torch.cuda.ExternalStream(streams[0].cuda_stream()))
-        for s in streams:
-            results.append(step(s))
-        ev1.record(torch.cuda.ExternalStream(streams[-1].cuda_stream()))
+        ev0.record()
+        for i in range(args.steps):
+            s = make_stream()
+            idx, rep_i = step(s)
+            reports.append(rep_i)
+            del idx
+            if i == args.steps - 1:
+                last = s
+            del s
+        ev1.record()
         torch.cuda.synchronize()
     launches = L.fx_kernel_launches() - launches0
     host_split = {k: v / args.steps for k, v in host_split.items()}
@@ -224,9 +236,9 @@ def main():
         t_ms = float(tt.item())
     ms_per_step = t_ms / args.steps
     value = W["n"] * ws * args.steps / (t_ms / 1e3)
-    rep = results[-1][1]
-    phases = streams[-1].timings()
-    counters = streams[-1].counters()
+    rep = reports[-1]
+    phases = last.timings()
+    counters = last.counters()
 
     # roofline of the dominant kernel (algorithmic bytes)
     D, n_cls = W["dim"], rep.objects_classified
@@ -251,7 +263,7 @@ def main():
 
     # end-to-end through the host-buffer C ABI
     e2e = None
-    if rank == 0 or True:
+    if args.e2e_steps > 0:
         ho = data.oids.cpu().pin_memory()
         hf = data.fids.cpu().pin_memory()
         hs = data.sigs.cpu().pin_memory()

@@ -6,6 +6,8 @@
 #include <algorithm>
 #include <climits>
 
+#include <chrono>
+
 #include "fx_handles.cuh"
 
 namespace fx {
@@ -113,7 +115,11 @@ void fx_stream::tcollect() {
 }
 
 fx_stream::~fx_stream() {
-    if (h_ctr_ring) cudaFreeHost(h_ctr_ring);
+    if (h_ctr_ring) {
+        for (auto &e : ring_ev)
+            if (e) cudaEventSynchronize(e);
+        pinned_return(h_ctr_ring);
+    }
     for (auto &e : ring_ev)
         if (e) cudaEventDestroy(e);
     for (auto &t : timers) {
@@ -204,7 +210,7 @@ int fx_stream_create(const fx_stream_config *cfg, fx_stream **out) {
             FX_CUDA(cudaMemsetAsync(s->s_cn2.p, 0, sizeof(float) * ns, s->st));
             FX_CUDA(cudaMemsetAsync(s->s_evicted.p, 0, sizeof(int32_t) * ns, s->st));
             FX_CUDA(cudaMemsetAsync(s->s_grp.p, 0xff, sizeof(int32_t) * ns, s->st));
-            FX_CUDA(cudaMallocHost(&s->h_ctr_ring, sizeof(int64_t) * 3 * C_COUNT));
+            s->h_ctr_ring = (int64_t *)pinned_borrow(sizeof(int64_t) * 3 * C_COUNT);
             for (int i = 0; i < 3; i++) FX_CUDA(cudaEventCreateWithFlags(&s->ring_ev[i], cudaEventDisableTiming));
             s->prof.reserve(16);
             FX_CUDA(cudaMemsetAsync(s->prof.p, 0, sizeof(int64_t) * 16, s->st));
@@ -296,6 +302,11 @@ static void ingest_chunk(fx_stream *s, int64_t n, const int64_t *d_oid, const in
     cudaStream_t st = s->st;
     const int K = s->cfg.k, S = s->cfg.sig_dim;
     const int64_t n0 = s->n_seen, need = n0 + n;
+    using hclock = std::chrono::steady_clock;
+    auto hms = [](hclock::time_point a, hclock::time_point b) {
+        return std::chrono::duration<double, std::milli>(b - a).count();
+    };
+    const auto h0 = hclock::now();
     // per-object arrays
     s->oid.grow(need, n0, st);
     s->fid.grow(need, n0, st);
@@ -304,6 +315,8 @@ static void ingest_chunk(fx_stream *s, int64_t n, const int64_t *d_oid, const in
     s->cluster_of.grow(need, n0, st);
     s->mrank.grow(need, n0, st);
     s->frank.grow(need, n0, st);
+    const auto h1 = hclock::now();
+    s->t_ms[12] += hms(h0, h1);
     FX_CUDA(cudaMemcpyAsync(s->oid.p + n0, d_oid, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, st));
     FX_CUDA(cudaMemcpyAsync(s->fid.p + n0, d_fid, sizeof(int64_t) * n, cudaMemcpyDeviceToDevice, st));
     // K0
@@ -329,6 +342,8 @@ static void ingest_chunk(fx_stream *s, int64_t n, const int64_t *d_oid, const in
     FX_CUDA(cudaMemcpyAsync(&h_first, first.p, sizeof(h_first), cudaMemcpyDeviceToHost, st));
     s->tstop();
     FX_CUDA(cudaStreamSynchronize(st));
+    const auto h2 = hclock::now();
+    s->t_ms[13] += hms(h1, h2);
     s->tstart(0);
     const int64_t lead = h_first == ~0ull ? n : (int64_t)h_first;
     const int64_t c0 = s->n_cls, cneed = c0 + nc;
@@ -364,6 +379,7 @@ static void ingest_chunk(fx_stream *s, int64_t n, const int64_t *d_oid, const in
             throw Error{FX_E_MISSING_TRUE_CLASS, "object " + std::to_string(bad) + " has no true class"};
         }
     }
+    s->t_ms[14] += hms(h2, hclock::now());
     // K2
     if (s->cfg.feat_type == FX_F64)
         run_batches<double>(s, c0, cneed);
@@ -556,7 +572,7 @@ int fx_stream_timings(fx_stream *s, double *out, int n) {
         set_dev(s->dev);
         StreamGuard sg_(s->st);
         s->tcollect();
-        for (int i = 0; i < n && i < 8; i++) out[i] = s->t_ms[i];
+        for (int i = 0; i < n && i < 16; i++) out[i] = s->t_ms[i];
     })
 }
 

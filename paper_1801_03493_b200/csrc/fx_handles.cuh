@@ -107,7 +107,7 @@ struct fx_stream {
     std::vector<Timer> timers;  // pool
     std::vector<int> pending;   // indices into timers awaiting collection
     int open_timer = -1;
-    double t_ms[8] = {0};
+    double t_ms[16] = {0};  // [0..6] device phases (fx_stream_timings), [8..14] host-side ms per section
     void tstart(int phase);
     void tstop();
     void tcollect();

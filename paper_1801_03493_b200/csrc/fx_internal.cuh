@@ -56,6 +56,11 @@ void count_launch();
 // handle works on (StreamGuard); DevBuf allocates and frees on it.
 cudaStream_t &cur_stream();
 void init_pool(int device);
+// Small pinned host blocks from a process-wide slab (cudaMallocHost pins pages
+// and can stall for a long time under host memory pressure; engines are
+// created and destroyed per stream, so they borrow instead).
+void *pinned_borrow(size_t bytes);
+void pinned_return(void *p);
 
 struct StreamGuard {
     cudaStream_t prev;

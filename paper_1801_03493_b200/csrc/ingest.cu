@@ -21,6 +21,7 @@
 // the batch's members to the float64 sums in order and refreshes the FP32
 // snapshot.  Seal (representatives) is deferred to finalize, exactly as the
 // reference's frozen-at-eviction centroids allow.
+#include <chrono>
 #include <climits>
 
 #include "fx_handles.cuh"
@@ -135,8 +136,9 @@ constexpr int SC_T = 64, SC_K = 32;
 template <typename TA, typename FB>
 __global__ void __launch_bounds__(256) k_screen(int nA, int64_t a0, const char *const *__restrict__ frow, int D,
                                                const int64_t *__restrict__ nB_dev, int nB_max, FB fb,
-                                               float *__restrict__ out, int64_t ld) {
+                                               float *__restrict__ out, int64_t ld, int nB_skip = -1) {
     const int nB = nB_dev ? (int)*nB_dev : nB_max;
+    if (nB <= nB_skip) return;  // few residual columns: k_res_cols handles them
     // persistent over the (column, row) tiles that exist for the device-side nB
     const int ncol = (nB + SC_T - 1) / SC_T, nrow = (nA + SC_T - 1) / SC_T;
     for (int tile = blockIdx.x; tile < ncol * nrow; tile += gridDim.x) {
@@ -239,6 +241,69 @@ __global__ void k_residuals(int nA, const int64_t *__restrict__ ctr, const float
             res_col[w] = col;
         } else {
             res_col[w] = -1;
+        }
+    }
+}
+
+// Residual columns when there are few of them (the common case: a batch has
+// 0..a handful of probable seeds).  dres[b][col] = FP32 direct-difference
+// distance between object b and residual `col`, needed only for b after the
+// residual's own position (the seed can only influence later objects).  One
+// warp per row; the residual rows are staged in shared memory RC_COLS at a
+// time.  Error model: each lane sums D/32 squared differences, flushing its
+// running partial every 64 terms, then a 5-level warp tree -- within the
+// SIMT screen model of screen_rel(D) for every D.
+constexpr int RC_MAX = 64, RC_COLS = 8;
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_res_cols(int nA, int64_t a0, const char *const *__restrict__ frow, int D,
+                                                 const int64_t *__restrict__ nres_dev,
+                                                 const int32_t *__restrict__ res_pos, float *__restrict__ out,
+                                                 int64_t ld) {
+    const int nres = (int)*nres_dev;
+    if (nres == 0 || nres > RC_MAX) return;
+    extern __shared__ float rc_s[];  // [RC_COLS][D]
+    __shared__ int s_pos[RC_COLS];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int cc = 0; cc < nres; cc += RC_COLS) {
+        const int ncol = min(RC_COLS, nres - cc);
+        __syncthreads();
+        if (threadIdx.x < RC_COLS) s_pos[threadIdx.x] = threadIdx.x < ncol ? res_pos[cc + threadIdx.x] : INT_MAX;
+        for (int e = threadIdx.x; e < ncol * D; e += blockDim.x) {
+            const int j = e / D, k = e - j * D;
+            rc_s[e] = (float)((const T *)frow[a0 + res_pos[cc + j]])[k];
+        }
+        __syncthreads();
+        int pmin = INT_MAX;
+#pragma unroll
+        for (int j = 0; j < RC_COLS; j++) pmin = min(pmin, s_pos[j]);
+        for (int b = pmin + 1 + blockIdx.x * nw + wid; b < nA; b += gridDim.x * nw) {
+            const T *f = (const T *)frow[a0 + b];
+            float tot[RC_COLS], acc[RC_COLS];
+#pragma unroll
+            for (int j = 0; j < RC_COLS; j++) tot[j] = acc[j] = 0.f;
+            int cnt = 0;
+            for (int k = lane; k < D; k += 32) {
+                const float x = (float)f[k];
+#pragma unroll
+                for (int j = 0; j < RC_COLS; j++) {
+                    const float d = x - rc_s[j * D + k];
+                    acc[j] = fmaf(d, d, acc[j]);
+                }
+                if (++cnt == 64) {
+#pragma unroll
+                    for (int j = 0; j < RC_COLS; j++) {
+                        tot[j] += acc[j];
+                        acc[j] = 0.f;
+                    }
+                    cnt = 0;
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < RC_COLS; j++) {
+                const float v = warp_sum(tot[j] + acc[j]);
+                if (lane == j && j < ncol && b > s_pos[j]) out[(int64_t)b * ld + cc + j] = sqrtf(v);
+            }
         }
     }
 }
@@ -1367,99 +1432,102 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
 // grid (ceil(D/256), ndirty)
 // ---------------------------------------------------------------------------
 
+// One CTA per (dirty slot, FD-dimension slice).  A slot's members must be
+// added in stream order (float64 rounding is order dependent), so each
+// dimension is one dependent dadd chain; what limits the chain is how fast
+// member rows arrive.  All FOLD_THREADS threads stream the slot's rows into a
+// FOLD_NS-stage shared-memory ring with cp.async (FOLD_R rows x FD dims per
+// stage, FOLD_R = 64 float / 32 double rows) while warp 0 (lane = dimension) walks the chain out of shared
+// memory.  The dominant cluster of a Zipf stream owns most of a batch, so the
+// ring keeps FOLD_NS * FOLD_R rows in flight for it instead of a handful.
+constexpr int FD = 32, FOLD_NS = 4, FOLD_THREADS = 128;
+
+__device__ __forceinline__ void cp_async_el(uint32_t dst, const void *src, bool ok, int bytes) {
+    if (bytes == 4)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 4 : 0));
+    else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 8 : 0));
+}
+
 template <typename T>
-__global__ void __launch_bounds__(64) k_fold(int D, int64_t c0, const int64_t *__restrict__ ctr,
-                                              const int32_t *__restrict__ dirty, const int32_t *__restrict__ dirty_off,
-                                              const int32_t *__restrict__ pend_list, const char *const *__restrict__ frow,
-                                              double *__restrict__ S, float *__restrict__ C32,
-                                              const int32_t *__restrict__ s_nfeat, const int32_t *__restrict__ s_foldpos,
-                                              const int32_t *__restrict__ s_seedpos, const int32_t *__restrict__ s_evicted,
-                                              const int32_t *__restrict__ s_cid, const int32_t *__restrict__ s_size,
-                                              float *__restrict__ s_cn2, double *__restrict__ fcent,
-                                              int32_t *__restrict__ cl_nfeat, int32_t *__restrict__ cl_size) {
-    __shared__ const T *rows[256];
-    __shared__ unsigned char first[256];
-    __shared__ float red[8];
+__global__ void __launch_bounds__(FOLD_THREADS) k_fold(int D, int64_t c0, const int64_t *__restrict__ ctr,
+                                                      const int32_t *__restrict__ dirty, const int32_t *__restrict__ dirty_off,
+                                                      const int32_t *__restrict__ pend_list, const char *const *__restrict__ frow,
+                                                      double *__restrict__ S, float *__restrict__ C32,
+                                                      const int32_t *__restrict__ s_nfeat, const int32_t *__restrict__ s_foldpos,
+                                                      const int32_t *__restrict__ s_seedpos, const int32_t *__restrict__ s_evicted,
+                                                      const int32_t *__restrict__ s_cid, const int32_t *__restrict__ s_size,
+                                                      float *__restrict__ s_cn2, double *__restrict__ fcent,
+                                                      int32_t *__restrict__ cl_nfeat, int32_t *__restrict__ cl_size) {
+    constexpr int FOLD_R = sizeof(T) == 4 ? 64 : 32;  // 32 KB ring for float, 32 KB for double
+    __shared__ __align__(16) T ring[FOLD_NS][FOLD_R][FD];
+    __shared__ unsigned char flag[FOLD_NS][FOLD_R];  // 0 add, 1 first (seed), 2 skip
     const int nd = (int)ctr[C_NDIRTY];
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int kbase = blockIdx.x * FD;
     for (int di = blockIdx.y; di < nd; di += gridDim.y) {
-    const int slot = dirty[di];
-    const int k = blockIdx.x * blockDim.x + threadIdx.x;
-    const int p0 = dirty_off[di], p1 = dirty_off[di + 1];
-    const int fp = s_foldpos[slot], sp = s_seedpos[slot];
-    const double n = (double)s_nfeat[slot];
-    float c2 = 0.f;
-    double s = k < D ? S[(int64_t)slot * D + k] : 0.0;
-    for (int cs = p0; cs < p1; cs += 256) {
-        // stage the chunk's row pointers (members already folded by the
-        // resolve's exact path are skipped)
-        for (int t = threadIdx.x; t < 256; t += blockDim.x) {
-            const int p = cs + t;
-            const T *r = nullptr;
-            unsigned char fst = 0;
-            if (p < p1) {
-                const int b = pend_list[p];
-                if (b >= fp) {
-                    r = (const T *)frow[c0 + b];
-                    fst = b == sp;
+        const int slot = dirty[di];
+        const int p0 = dirty_off[di], p1 = dirty_off[di + 1];
+        const int fp = s_foldpos[slot], sp = s_seedpos[slot];
+        const int nst = (p1 - p0 + FOLD_R - 1) / FOLD_R;
+        // stage j <- rows pend_list[p0 + j*R ...]; every thread copies R*FD/THREADS elements
+        auto issue = [&](int j) {
+            if (j < nst) {
+                const int buf = j % FOLD_NS;
+                for (int e = tid; e < FOLD_R * FD; e += FOLD_THREADS) {
+                    const int r = e / FD, c = e % FD;
+                    const int p = p0 + j * FOLD_R + r;
+                    const int k = kbase + c;
+                    int b = -1;
+                    if (p < p1) b = pend_list[p];
+                    const bool use = b >= fp && b >= 0;  // members folded by the resolve's exact path are skipped
+                    const T *src = use ? (const T *)frow[c0 + b] + k : (const T *)frow[c0];
+                    cp_async_el((uint32_t)__cvta_generic_to_shared(&ring[buf][r][c]), src, use && k < D, (int)sizeof(T));
+                    if (c == 0) flag[buf][r] = use ? (b == sp ? 1 : 0) : 2;
                 }
             }
-            // padded / skipped members point at a valid row and are masked (flag 2)
-            rows[t] = r ? r : (const T *)frow[c0];
-            first[t] = r ? fst : 2;
-        }
-        __syncthreads();
-        const int nch = min(256, p1 - cs);
-        if (k < D) {
-            // software-pipelined: the next 16 rows are in flight while the
-            // current 16 are added (two register groups, 32 loads outstanding)
-            T va[16], vb[16];
-#pragma unroll
-            for (int j = 0; j < 16; j++) va[j] = __ldg(rows[j] + k);
-            for (int i = 0; i < nch; i += 32) {
-#pragma unroll
-                for (int j = 0; j < 16; j++) vb[j] = __ldg(rows[(i + 16 + j) & 255] + k);
-#pragma unroll
-                for (int j = 0; j < 16; j++) {
-                    const unsigned char fl = (i + j < nch) ? first[i + j] : 2;
-                    const double v = to_d(va[j]);
-                    const double add = dadd(s, v);
-                    s = fl == 1 ? v : (fl == 0 ? add : s);
-                }
-#pragma unroll
-                for (int j = 0; j < 16; j++) va[j] = __ldg(rows[(i + 32 + j) & 255] + k);
-#pragma unroll
-                for (int j = 0; j < 16; j++) {
-                    const unsigned char fl = (i + 16 + j < nch) ? first[i + 16 + j] : 2;
-                    const double v = to_d(vb[j]);
-                    const double add = dadd(s, v);
-                    s = fl == 1 ? v : (fl == 0 ? add : s);
+            asm volatile("cp.async.commit_group;\n" ::);
+        };
+        for (int j = 0; j < FOLD_NS - 1; j++) issue(j);
+        const int k = kbase + lane;
+        double acc = (tid < 32 && k < D) ? S[(int64_t)slot * D + k] : 0.0;
+        for (int j = 0; j < nst; j++) {
+            asm volatile("cp.async.wait_group %0;\n" ::"n"(FOLD_NS - 2));
+            __syncthreads();
+            issue(j + FOLD_NS - 1);  // refills the buffer consumed in iteration j-1
+            if (tid < 32) {
+                const int buf = j % FOLD_NS;
+                const int nr = min(FOLD_R, p1 - p0 - j * FOLD_R);
+#pragma unroll 8
+                for (int r = 0; r < nr; r++) {
+                    const unsigned char fl = flag[buf][r];
+                    const double v = to_d(ring[buf][r][lane]);
+                    const double add = dadd(acc, v);
+                    acc = fl == 1 ? v : (fl == 0 ? add : acc);
                 }
             }
         }
-        __syncthreads();
-    }
-    if (k < D) {
-        S[(int64_t)slot * D + k] = s;
-        double cen = ddiv(s, n);
-        float c32 = (float)cen;
-        C32[(int64_t)slot * D + k] = c32;
-        c2 = c32 * c32;
-        if (s_evicted[slot]) fcent[(int64_t)s_cid[slot] * D + k] = cen;
-    }
-    // ||c||^2 partial
-    c2 = warp_sum(c2);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = c2;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        float t = 0.f;
-        for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += red[w];
-        atomicAdd(&s_cn2[slot], t);
-        if (blockIdx.x == 0 && s_evicted[slot]) {
-            cl_nfeat[s_cid[slot]] = s_nfeat[slot];
-            cl_size[s_cid[slot]] = s_size[slot];
+        asm volatile("cp.async.wait_group 0;\n" ::);
+        if (tid < 32) {
+            float c2 = 0.f;
+            if (k < D) {
+                S[(int64_t)slot * D + k] = acc;
+                const double cen = ddiv(acc, (double)s_nfeat[slot]);
+                const float c32 = (float)cen;
+                C32[(int64_t)slot * D + k] = c32;
+                c2 = c32 * c32;
+                if (s_evicted[slot]) fcent[(int64_t)s_cid[slot] * D + k] = cen;
+            }
+            c2 = warp_sum(c2);  // ||c||^2 partial of this slice
+            if (lane == 0) {
+                atomicAdd(&s_cn2[slot], c2);
+                if (blockIdx.x == 0 && s_evicted[slot]) {
+                    cl_nfeat[s_cid[slot]] = s_nfeat[slot];
+                    cl_size[s_cid[slot]] = s_size[slot];
+                }
+            }
         }
-    }
-    __syncthreads();
+        __syncthreads();  // the ring is reused by the next slot
     }
 }
 
@@ -1573,7 +1641,12 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
     // TF32 dot error gamma = 2^-9 + D 2^-22 (operand rounding + FP32 accumulation), d^2 error 2 gamma |a||b|
     const double gam = 1.953125e-03 + (double)D * 2.384185791015625e-07;
     const ScreenModel sm{s->tc_screen ? 1 : 0, rel, absc, (float)(2.0 * gam * 1.01), (float)(256.0 * 5.9604644775390625e-08)};
+    using hclock = std::chrono::steady_clock;
+    auto hms = [](hclock::time_point a, hclock::time_point b) {
+        return std::chrono::duration<double, std::milli>(b - a).count();
+    };
     for (int64_t c0 = c_begin, B = 0; c0 < c_end; c0 += B) {
+        const auto h0 = hclock::now();
         // the drift bound grows like (batch size / objects so far): keep batches
         // at <= 1/4 of the stream's age so young clusters stay decidable by bounds
         const int64_t age = std::max<int64_t>(c0, 0);
@@ -1598,9 +1671,22 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
                 B, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p, s->snap_slot.p, s->fnorm.p, c0, sm, s->cfg.t,
                 s->res_col.p, s->res_pos.p, s->ctr.p + C_NRES);
             FX_LAUNCHED();
+            const bool rc_ok = D <= 6144;  // RC_COLS staged rows fit in shared memory
+            if (rc_ok) {
+                const size_t smem = sizeof(float) * RC_COLS * D;
+                static size_t rc_set[2] = {0, 0};
+                size_t &cur = rc_set[sizeof(T) == 8];
+                if (smem > 48 * 1024 && smem > cur) {
+                    FX_CUDA(cudaFuncSetAttribute(k_res_cols<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                    cur = smem;
+                }
+                k_res_cols<T><<<148, 256, smem, st>>>(B, c0, s->frow.p, D, s->ctr.p + C_NRES, s->res_pos.p, s->dres.p, B);
+                FX_LAUNCHED();
+            }
             const unsigned grid = (unsigned)std::min<int64_t>(cdiv(B, SC_T) * cdiv(B, SC_T), 148);
             FromResidual<T> fb{s->frow.p, c0, s->res_pos.p};
-            k_screen<T, FromResidual<T>><<<grid, 256, 0, st>>>(B, c0, s->frow.p, D, s->ctr.p + C_NRES, B, fb, s->dres.p, B);
+            k_screen<T, FromResidual<T>><<<grid, 256, 0, st>>>(B, c0, s->frow.p, D, s->ctr.p + C_NRES, B, fb, s->dres.p, B,
+                                                               rc_ok ? RC_MAX : -1);
             FX_LAUNCHED();
         }
         k_row_summary<T><<<(unsigned)cdiv((int64_t)B * 32, 256), 256, 0, st>>>(
@@ -1608,6 +1694,8 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             s->C32.p, D, s->sum_slot.p, s->sum_d1.p, s->sum_e1.p, s->sum_lbr.p);
         FX_LAUNCHED();
         s->tstop();
+        const auto h1 = hclock::now();
+        s->t_ms[8] += hms(h0, h1);
         // 3. resolve (parallel verified segments + exact sequential events)
         s->tstart(2);
         {
@@ -1681,6 +1769,8 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             FX_LAUNCHED();
         }
         s->tstop();
+        const auto h2 = hclock::now();
+        s->t_ms[9] += hms(h1, h2);
         // 4. cluster-array capacity for final centroids of evicted clusters,
         //    without a per-batch host sync: each batch creates <= B clusters, so
         //    the count read back (asynchronously) two batches ago + 3B bounds it.
@@ -1706,20 +1796,25 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
                 s->cl_cap = cap;
             }
         }
+        const auto h3 = hclock::now();
+        s->t_ms[10] += hms(h2, h3);
         // 5. fold (persistent grid over the batch's dirty slots)
         {
             s->tstart(3);
             k_zero_cn2<<<(unsigned)cdiv(2 * s->B + 2, 256), 256, 0, st>>>(s->ctr.p, s->dirty.p, s->s_cn2.p);
             FX_LAUNCHED();
-            dim3 grid((unsigned)cdiv(D, 64), (unsigned)std::min<int64_t>(2 * (int64_t)B + 1, 512));
-            k_fold<T><<<grid, 64, 0, st>>>(D, c0, s->ctr.p, s->dirty.p, s->dirty_off.p, s->pend_list.p, s->frow.p,
+            // enough CTA rows for the usual dirty count; the kernel loops over the rest
+            const int64_t gx = cdiv(D, FD);
+            const int64_t gy = std::max<int64_t>(8, std::min<int64_t>(2 * (int64_t)B + 1, (148 * 12) / gx));
+            dim3 grid((unsigned)gx, (unsigned)gy);
+            k_fold<T><<<grid, FOLD_THREADS, 0, st>>>(D, c0, s->ctr.p, s->dirty.p, s->dirty_off.p, s->pend_list.p, s->frow.p,
                                             s->S.p, s->C32.p, s->s_nfeat.p, s->s_foldpos.p, s->s_seedpos.p,
                                             s->s_evicted.p, s->s_cid.p, s->s_size.p, s->s_cn2.p, s->fcent.p,
                                             s->cl_nfeat.p, s->cl_size.p);
             FX_LAUNCHED();
             s->tstop();
         }
-
+        s->t_ms[11] += hms(h3, hclock::now());
     }
 }
 

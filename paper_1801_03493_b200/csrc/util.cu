@@ -1,6 +1,7 @@
 // util.cu -- device prefix scans, the numpy pairwise-summation plan, error state.
 #include <atomic>
 #include <mutex>
+#include <vector>
 
 #include "fx_handles.cuh"
 
@@ -22,6 +23,32 @@ void init_pool(int device) {
     uint64_t thr = ~0ull;  // keep freed blocks cached in the pool
     FX_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
     done[device] = true;
+}
+
+namespace {
+constexpr size_t kPinBlock = 4096, kPinBlocks = 1024;
+std::mutex g_pin_mu;
+char *g_pin_slab = nullptr;
+std::vector<int> g_pin_free;
+}  // namespace
+
+void *pinned_borrow(size_t bytes) {
+    if (bytes > kPinBlock) throw Error{FX_E_INTERNAL, "pinned_borrow: block too large"};
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    if (!g_pin_slab) {
+        FX_CUDA(cudaMallocHost((void **)&g_pin_slab, kPinBlock * kPinBlocks));
+        for (int i = (int)kPinBlocks - 1; i >= 0; i--) g_pin_free.push_back(i);
+    }
+    if (g_pin_free.empty()) throw Error{FX_E_OOM, "pinned_borrow: slab exhausted"};
+    const int i = g_pin_free.back();
+    g_pin_free.pop_back();
+    return g_pin_slab + (size_t)i * kPinBlock;
+}
+
+void pinned_return(void *p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    g_pin_free.push_back((int)(((char *)p - g_pin_slab) / kPinBlock));
 }
 
 void set_error(const std::string &msg) { g_last_error = msg; }
