@@ -21,6 +21,7 @@ void launch_rank(fx_stream *s, int64_t c0, int64_t nc, const int32_t *d_tcls, un
 template <typename T>
 void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end);
 void launch_final_live(fx_stream *s);
+size_t resolve_smem(int Bc, const PwPlan &P);
 void launch_dup_members(fx_stream *s, int64_t n, const int64_t *d_excl_all, int64_t *d_anchor);
 void launch_seal(fx_stream *s, int64_t nfeat_total, const int32_t *fmem_cls, const int32_t *fmem_cid,
                  const int64_t *foff, unsigned long long *best_bits, double *dout, int *best_pos);
@@ -183,6 +184,8 @@ int fx_stream_create(const fx_stream_config *cfg, fx_stream **out) {
                 const char *env = getenv("FOCUS_B200_SCREEN");
                 const bool simt = env && strcmp(env, "simt") == 0;
                 s->tc_screen = !simt && cfg->feat_type == FX_F32 && cfg->dim % 4 == 0;
+                const char *chk = getenv("FOCUS_B200_CHECK");
+                s->debug_check = chk && strcmp(chk, "1") == 0;
             }
             FX_CUDA(cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking));
             cur_stream() = s->st;
@@ -193,6 +196,10 @@ int fx_stream_create(const fx_stream_config *cfg, fx_stream **out) {
                 B = (int)std::min<int64_t>(4096, std::max<int64_t>(256, b));
             }
             B = std::max(64, (B / 64) * 64);
+            s->plan_host = new PwPlan();
+            build_pw_plan(D, s->plan_host);
+            // k_resolve keeps per-object state of the whole batch in shared memory
+            while (B > 64 && resolve_smem(B, *s->plan_host) + 48 * 1024 > 227 * 1024) B -= 64;
             s->B = B;
             const int64_t max_slots_mem = (int64_t)(48e9 / (12.0 * D));
             int64_t live_cap = std::min<int64_t>(cfg->m, max_slots_mem);
@@ -230,8 +237,6 @@ int fx_stream_create(const fx_stream_config *cfg, fx_stream **out) {
             s->dirty.reserve(2 * B + 2);
             s->dirty_off.reserve(2 * B + 3);
             s->prev_sig.reserve(std::max(1, cfg->sig_dim));
-            s->plan_host = new PwPlan();
-            build_pw_plan(D, s->plan_host);
             s->plan.reserve(1);
             FX_CUDA(cudaMemcpyAsync(s->plan.p, s->plan_host, sizeof(PwPlan), cudaMemcpyHostToDevice, s->st));
             FX_CUDA(cudaStreamSynchronize(s->st));

@@ -569,64 +569,24 @@ __global__ void k_row_summary(int nA, const int64_t *__restrict__ ctr, const flo
 }
 
 
-// ---- group-chain scans for the resolve's parallel segments -----------------
-// Element i of a group's stream-ordered member list joins with n = nf0 + i + 1
-// featured members; its drift map is d -> a d + c with a = 1 + 1/n (+ slack),
-// c = ub0/n (+ slack), fp32 rounded up.  One warp scans list indices [lo, hi).
-struct GroupCtx {
-    int off, nf0, sl;
-    float cn;
-};
-
-__device__ __forceinline__ void elem_map(const GroupCtx &G, int i, float ub0, float &a, float &c) {
-    const float inv = __frcp_ru((float)(G.nf0 + i + 1));
-    a = __fadd_ru(__fadd_ru(1.f, inv), 2.5e-7f);
-    c = __fadd_ru(__fmul_ru(ub0, inv), __fmul_ru(1e-13f, __fadd_ru(G.cn, ub0)) + 1e-30f);
-}
-
-__device__ __forceinline__ void warp_affine_scan(float &a, float &c, int &w, int lane) {
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const float ap = __shfl_up_sync(0xffffffffu, a, o), cp = __shfl_up_sync(0xffffffffu, c, o);
-        const int wp = __shfl_up_sync(0xffffffffu, w, o);
-        if (lane >= o) {
-            c = __fmaf_ru(a, cp, c);
-            a = __fmul_ru(a, ap);
-            w += wp;
-        }
-    }
-}
-
-// compose the maps of [lo, hi) -> (A, C); also the sum of member weights
-// 1 + dup_run (sizes, needed by the commit)
-__device__ void gc_compose(const GroupCtx &G, int lo, int hi, const int32_t *glist, const float *seg_ub0,
-                           const int32_t *dup_run, int64_t c0, float &A, float &C, int &W) {
-    const int lane = threadIdx.x & 31;
-    float Ac = 1.f, Cc = 0.f;
-    int Wc = 0;
-    for (int i0 = lo; i0 < hi; i0 += 32) {
-        const int i = i0 + lane;
-        float a = 1.f, c = 0.f;
-        int w = 0;
-        if (i < hi) {
-            const int p = glist[G.off + i];
-            elem_map(G, i, seg_ub0[p], a, c);
-            w = 1 + dup_run[c0 + p];
-        }
-        warp_affine_scan(a, c, w, lane);
-        const float a31 = __shfl_sync(0xffffffffu, a, 31), c31 = __shfl_sync(0xffffffffu, c, 31);
-        Cc = __fmaf_ru(a31, Cc, c31);
-        Ac = __fmul_ru(a31, Ac);
-        Wc += __shfl_sync(0xffffffffu, w, 31);
-    }
-    A = Ac;
-    C = Cc;
-    W = Wc;
-}
-
 constexpr int RS_MAXGRP = 1024;
-constexpr int RS_BIGGRP = 512;  // groups longer than this are scanned by all warps
+constexpr int RS_WCNT_BYTES = RS_WARPS * RS_MAXGRP * 2;
 constexpr int RS_WIN0 = 64;
+
+// Closed-form drift bound for a group's chain inside one window: before its
+// (i+1)-th join the slot's centroid is within d_i of the reference the
+// hypothesis bounds refer to, where each join moves the centroid by
+// (f - c)/n' and |f - c| <= U + d (U = largest hypothesis bound of the group):
+//   d_i + U <= (d0 + U) prod_{m<i} (1 + 1/(nf0+m+1)) = (d0 + U)(nf0+i+1)/(nf0+1)
+// so d_i <= d0 r + U i/(nf0+1), r = (nf0+i+1)/(nf0+1); the float64 rounding of
+// each join (8 u (|c| + d + ub), as in drift_step) is added, amplified by r.
+__device__ __forceinline__ float drift_cf(float d0, float U, int nf0, int i, float cn) {
+    const double n1 = (double)nf0 + 1.0;
+    const double r = (n1 + (double)i) / n1;
+    const double core = (double)d0 * r + (double)U * ((double)i / n1);
+    const double slack = (double)i * 8.0 * 1.1102230246251565e-16 * ((double)cn + 2.0 * core + 2.0 * (double)U) * r;
+    return __double2float_ru((core + slack) * (1.0 + 1e-12));
+}
 
 __device__ __forceinline__ double drift_step(double dr, double ub, int nf, double cn) {
     // ||c_new - c_old|| <= ub / nf in exact arithmetic (c' - c = (f - c)/n');
@@ -639,14 +599,14 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int B = A.B;
     const int BC = A.Bcap;  // layout by capacity (multiple of 64): every array stays aligned
-    double *seg_ub = (double *)smem_raw;                  // [B] UB of the hypothesis
-    int32_t *sh_slot_of = (int32_t *)(seg_ub + BC);        // [B]
+    unsigned short *wcnt = (unsigned short *)smem_raw;    // [RS_WARPS][RS_MAXGRP] per-warp group counts
+    int32_t *sh_slot_of = (int32_t *)(smem_raw + RS_WCNT_BYTES);  // [B]
     int *mlist = (int *)(sh_slot_of + BC);                 // [B]
     int32_t *seg_key = (int32_t *)(mlist + BC);            // [B] hypothesis slot
     float *seg_ub0 = (float *)(seg_key + BC);              // [B] d1 + e1
     float *seg_lbr = (float *)(seg_ub0 + BC);              // [B] min over others of d - e
     int32_t *seedlist = (int32_t *)(seg_lbr + BC);         // [B] in-batch seed slots
-    int32_t *seg_nf = seedlist + BC;                       // [B] featured count before p
+    int32_t *seg_nf = seedlist + BC;                       // [B] rank inside the hypothesis group
     int32_t *glist = seg_nf + BC;                         // [B] group-ordered positions
     short *seg_grp = (short *)(glist + BC);               // [B]
     unsigned char *seg_flag = (unsigned char *)(seg_grp + BC);  // [B]
@@ -661,17 +621,13 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
     __shared__ int s_best_slot;
     __shared__ float s_ub_used;
     __shared__ int grp_slot[RS_MAXGRP];
-    __shared__ int grp_cnt[RS_MAXGRP], grp_off[RS_MAXGRP];
-    __shared__ double grp_drift[RS_MAXGRP];
+    __shared__ int grp_cnt[RS_MAXGRP], grp_off[RS_MAXGRP], grp_ncommit[RS_MAXGRP], grp_nf0[RS_MAXGRP];
+    __shared__ float grp_drift[RS_MAXGRP], grp_U[RS_MAXGRP], grp_d0[RS_MAXGRP], grp_cn[RS_MAXGRP];
     __shared__ int s_ngrp, s_fail;
-    (void)0;
     __shared__ double s_md1, s_md2;
     __shared__ int s_md1_slot;
     __shared__ double wmd1[RS_WARPS], wmd2[RS_WARPS];
-    __shared__ float wA[RS_WARPS], wC[RS_WARPS], wcarry[RS_WARPS + 1];
-    __shared__ int wW[RS_WARPS], wszc[RS_WARPS + 1];
-    __shared__ int grp_ncommit[RS_MAXGRP];
-    __shared__ int wmds[RS_WARPS];
+    __shared__ int wmds[RS_WARPS], wsv[RS_WARPS], wsh[RS_WARPS];
 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     int64_t *ctr = A.ctr;
@@ -775,11 +731,15 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
             seg_ub0[p] = (d1 + e1) * 1.000001f + 1e-30f;
             seg_lbr[p] = lbr - fabsf(lbr) * 1e-6f - 1e-30f;
         }
-        for (int g = tid; g < RS_MAXGRP; g += blockDim.x) grp_cnt[g] = 0;
+        for (int g = tid; g < RS_MAXGRP; g += blockDim.x) {
+            grp_cnt[g] = 0;
+            grp_U[g] = 0.f;
+        }
         __syncthreads();
         long long t1 = clock64();
         if (tid == 0) A.prof[0] += t1 - t0;
-        // pass B1: distinct hypothesis slots -> group ids
+        // pass B1: distinct hypothesis slots -> group ids; per group the
+        // largest hypothesis upper bound (it bounds every member's join step)
         for (int p = b + tid; p < e_end; p += blockDim.x) {
             const int key = seg_key[p];
             if (key < 0) continue;
@@ -795,129 +755,77 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
         for (int p = b + tid; p < e_end; p += blockDim.x) {
             const int key = seg_key[p];
             const int g = key >= 0 ? A.s_grp[key] : -1;
-            seg_grp[p] = (short)((g >= 0 && g < RS_MAXGRP) ? g : -1);
+            const bool ok = g >= 0 && g < RS_MAXGRP;
+            seg_grp[p] = (short)(ok ? g : -1);
+            if (ok) atomicMax((int *)&grp_U[g], __float_as_int(seg_ub0[p]));  // ub0 > 0
+        }
+        for (int g = tid; g < ngrp; g += blockDim.x) {
+            const int sl = grp_slot[g];
+            grp_nf0[g] = A.s_nfeat[sl];
+            grp_d0[g] = __double2float_ru(A.s_drift[sl]);
+            grp_cn[g] = sqrtf(A.s_cn2[sl]) * 1.00001f;
         }
         __syncthreads();
-        // stable rank of every object inside its group (warp 0, 32-slices in order)
-        if (wid == 0 && !overflow) {
-            for (int p0 = b; p0 < e_end; p0 += 32) {
+        // pass B2: stable rank of every object inside its group.  Each warp
+        // ranks a contiguous chunk (match per 32-slice, warp-private counts),
+        // an exclusive scan over warps per group gives the chunk bases.
+        const int nwin = e_end - b;
+        const int cs = ((nwin + RS_WARPS * 32 - 1) / (RS_WARPS * 32)) * 32;
+        if (!overflow) {
+            for (int e = tid; e < RS_WARPS * ngrp; e += blockDim.x) wcnt[e] = 0;
+            __syncthreads();
+            const int lo = b + wid * cs, hi = min(e_end, lo + cs);
+            for (int p0 = lo; p0 < hi; p0 += 32) {
                 const int p = p0 + lane;
-                const int g = p < e_end ? seg_grp[p] : -1;
+                const int g = p < hi ? seg_grp[p] : -1;
                 const unsigned act = __ballot_sync(0xffffffffu, g >= 0);
-                unsigned peers = 0;
-                int r = 0;
+                unsigned lower = 0, peers = 0;
                 if (g >= 0) {
                     peers = __match_any_sync(act, g);
-                    r = grp_cnt[g] + __popc(peers & ((1u << lane) - 1u));
-                    seg_nf[p] = r;
+                    lower = peers & ((1u << lane) - 1u);
+                    seg_nf[p] = wcnt[wid * ngrp + g] + __popc(lower);
                 }
                 __syncwarp();
-                if (g >= 0 && (peers & ((1u << lane) - 1u)) == 0) grp_cnt[g] += __popc(peers);
+                if (g >= 0 && lower == 0) wcnt[wid * ngrp + g] += (unsigned short)__popc(peers);
                 __syncwarp();
             }
-            // exclusive prefix over groups
-            int run = 0;
-            for (int g0 = 0; g0 < ngrp; g0 += 32) {
-                const int g = g0 + lane;
-                const int c = g < ngrp ? grp_cnt[g] : 0;
-                int x = c;
+            __syncthreads();
+            for (int g = tid; g < ngrp; g += blockDim.x) {
+                int run = 0;
+                for (int w = 0; w < RS_WARPS; w++) {
+                    const int c = wcnt[w * ngrp + g];
+                    wcnt[w * ngrp + g] = (unsigned short)run;
+                    run += c;
+                }
+                grp_cnt[g] = run;
+            }
+            __syncthreads();
+            for (int p = b + tid; p < e_end; p += blockDim.x) {
+                const int g = seg_grp[p];
+                if (g >= 0) seg_nf[p] += wcnt[((p - b) / cs) * ngrp + g];
+            }
+            if (wid == 0) {  // exclusive prefix over groups
+                int run = 0;
+                for (int g0 = 0; g0 < ngrp; g0 += 32) {
+                    const int g = g0 + lane;
+                    const int c = g < ngrp ? grp_cnt[g] : 0;
+                    int x = c;
 #pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const int y = __shfl_up_sync(0xffffffffu, x, o);
-                    if (lane >= o) x += y;
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const int y = __shfl_up_sync(0xffffffffu, x, o);
+                        if (lane >= o) x += y;
+                    }
+                    if (g < ngrp) grp_off[g] = run + x - c;
+                    run += __shfl_sync(0xffffffffu, x, 31);
                 }
-                if (g < ngrp) grp_off[g] = run + x - c;
-                run += __shfl_sync(0xffffffffu, x, 31);
             }
-        }
-        __syncthreads();
-        if (!overflow)
+            __syncthreads();
             for (int p = b + tid; p < e_end; p += blockDim.x) {
                 const int g = seg_grp[p];
                 if (g >= 0) glist[grp_off[g] + seg_nf[p]] = p;
             }
-        __syncthreads();
-        // pass B2: drift bound along every group's chain (stream order).  The
-        // recurrence d' = d (1 + 1/n) + ub0/n + slack is affine in d: each
-        // 32-slice is an inclusive warp scan of affine maps (fp32, rounded
-        // up -- every grouping yields an upper bound).  Long groups are split
-        // over all warps (compose per warp, carry across warps, apply).
-        if (!overflow) {
-            for (int g = 0; g < ngrp; g++) {
-                const int cnt = grp_cnt[g];
-                if (cnt <= RS_BIGGRP) continue;
-                const int sl = grp_slot[g];
-                GroupCtx G{grp_off[g], A.s_nfeat[sl], sl, sqrtf(A.s_cn2[sl]) * 1.00001f};
-                const int seg = (cnt + RS_WARPS - 1) / RS_WARPS;
-                const int lo = min(cnt, wid * seg), hi = min(cnt, lo + seg);
-                float Aw, Cw;
-                int Ww;
-                gc_compose(G, lo, hi, glist, seg_ub0, A.dup_run, A.c0, Aw, Cw, Ww);
-                if (lane == 0) {
-                    wA[wid] = Aw;
-                    wC[wid] = Cw;
-                }
-                __syncthreads();
-                if (tid == 0) {
-                    float d = __double2float_ru(A.s_drift[sl]);
-                    for (int w = 0; w < RS_WARPS; w++) {
-                        wcarry[w] = d;
-                        d = __fmaf_ru(wA[w], d, wC[w]);
-                    }
-                    grp_drift[g] = (double)d;
-                }
-                __syncthreads();
-                float dr = wcarry[wid];
-                for (int i0 = lo; i0 < hi; i0 += 32) {
-                    const int i = i0 + lane;
-                    float a = 1.f, c = 0.f, ub0 = 0.f;
-                    int w = 0, p = 0;
-                    if (i < hi) {
-                        p = glist[G.off + i];
-                        ub0 = seg_ub0[p];
-                        elem_map(G, i, ub0, a, c);
-                        seg_nf[p] = G.nf0 + i;
-                    }
-                    warp_affine_scan(a, c, w, lane);
-                    float ae = __shfl_up_sync(0xffffffffu, a, 1), ce = __shfl_up_sync(0xffffffffu, c, 1);
-                    if (lane == 0) {
-                        ae = 1.f;
-                        ce = 0.f;
-                    }
-                    if (i < hi) seg_ub[p] = (double)__fadd_ru(ub0, __fmaf_ru(ae, dr, ce));
-                    const float a31 = __shfl_sync(0xffffffffu, a, 31), c31 = __shfl_sync(0xffffffffu, c, 31);
-                    dr = __fmaf_ru(a31, dr, c31);
-                }
-                __syncthreads();
-            }
-            for (int g = wid; g < ngrp; g += RS_WARPS) {
-                const int cnt = grp_cnt[g];
-                if (cnt > RS_BIGGRP) continue;
-                const int sl = grp_slot[g];
-                GroupCtx G{grp_off[g], A.s_nfeat[sl], sl, sqrtf(A.s_cn2[sl]) * 1.00001f};
-                float dr = __double2float_ru(A.s_drift[sl]);
-                for (int i0 = 0; i0 < cnt; i0 += 32) {
-                    const int i = i0 + lane;
-                    float a = 1.f, c = 0.f, ub0 = 0.f;
-                    int w = 0, p = 0;
-                    if (i < cnt) {
-                        p = glist[G.off + i];
-                        ub0 = seg_ub0[p];
-                        elem_map(G, i, ub0, a, c);
-                        seg_nf[p] = G.nf0 + i;
-                    }
-                    warp_affine_scan(a, c, w, lane);
-                    float ae = __shfl_up_sync(0xffffffffu, a, 1), ce = __shfl_up_sync(0xffffffffu, c, 1);
-                    if (lane == 0) {
-                        ae = 1.f;
-                        ce = 0.f;
-                    }
-                    if (i < cnt) seg_ub[p] = (double)__fadd_ru(ub0, __fmaf_ru(ae, dr, ce));
-                    const float a31 = __shfl_sync(0xffffffffu, a, 31), c31 = __shfl_sync(0xffffffffu, c, 31);
-                    dr = __fmaf_ru(a31, dr, c31);
-                }
-                if (lane == 0) grp_drift[g] = (double)dr;
-            }
+            for (int g = tid; g < ngrp; g += blockDim.x)
+                grp_drift[g] = drift_cf(grp_d0[g], grp_U[g], grp_nf0[g], grp_cnt[g], grp_cn[g]);
         }
         __syncthreads();
         long long t2 = clock64();
@@ -929,7 +837,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
             for (int i = tid; i < L; i += blockDim.x) {
                 const int sl = A.live[i];
                 const int g = A.s_grp[sl];
-                const double d = (g >= 0 && g < RS_MAXGRP) ? grp_drift[g] : A.s_drift[sl];
+                const double d = (g >= 0 && g < RS_MAXGRP) ? (double)grp_drift[g] : A.s_drift[sl];
                 if (d > m1) {
                     m2 = m1;
                     m1 = d;
@@ -980,7 +888,9 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
             const int key = seg_key[p];
             unsigned char fl = 2;
             if (key >= 0 && !overflow) {
-                const double ub = seg_ub[p];
+                const int g = seg_grp[p];
+                const double ub =
+                    (double)seg_ub0[p] + (double)drift_cf(grp_d0[g], grp_U[g], grp_nf0[g], seg_nf[p], grp_cn[g]);
                 const double md = (key == s_md1_slot) ? s_md2 : s_md1;
                 const double lbo = (double)seg_lbr[p] - md * 1.000001;
                 if (lbo > ub) fl = ub <= A.T ? 0 : 1;
@@ -1001,14 +911,15 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
             __syncthreads();
             f = s_fail;
             if (f >= e_end || seg_flag[f] != 1) break;
-            const double dx = exact_dist<T>(A, f, seg_key[f], sh_slot_of, mlist, scratch, seg_nf[f]);
+            const double dx =
+                exact_dist<T>(A, f, seg_key[f], sh_slot_of, mlist, scratch, grp_nf0[seg_grp[f]] + seg_nf[f]);
             if (tid == 0) {
                 s_exact++;
                 // diagnostics: batch bucket (0,1-7,8-15,16-31,32-63,64-127,128+) and young slots (nfeat < 16)
                 const int bn = A.batch_no;
                 const int bk = bn == 0 ? 0 : bn < 8 ? 1 : bn < 16 ? 2 : bn < 32 ? 3 : bn < 64 ? 4 : bn < 128 ? 5 : 6;
                 A.prof[8 + bk]++;
-                if (seg_nf[f] < 16) A.prof[15]++;
+                if (grp_nf0[seg_grp[f]] + seg_nf[f] < 16) A.prof[15]++;
             }
             if (dx > A.T) break;  // nearest is beyond T: the object seeds (sequential path)
             f++;
@@ -1018,85 +929,98 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
         for (int p = f + tid; p < e_end; p += blockDim.x) sh_slot_of[p] = -1;
         long long t4 = clock64();
         if (tid == 0) A.prof[3] += t4 - t3;
-        // pass E: commit [b, f) -- same maps as pass B2, applied to the slot state
+        // pass E: commit [b, f).  Members of a group before f form a prefix of
+        // its stream-ordered list; member i of group g gets featured rank
+        // nf0 + i, pending rank pend0 + i and member rank size0 + i + (dups
+        // attached to the group's earlier members: segmented scan over glist).
         if (!overflow) {
-            // members of a group before f form a prefix of its (stream-ordered) list
-            for (int g = wid; g < ngrp; g += RS_WARPS) {
+            for (int g = tid; g < ngrp; g += blockDim.x) {
                 const int off = grp_off[g], cnt = grp_cnt[g];
                 int lo = 0, hi = cnt;  // first list index with p >= f
-                if (lane == 0) {
-                    while (lo < hi) {
-                        const int mid = (lo + hi) >> 1;
-                        if (glist[off + mid] < f) lo = mid + 1; else hi = mid;
+                while (lo < hi) {
+                    const int mid = (lo + hi) >> 1;
+                    if (glist[off + mid] < f) lo = mid + 1; else hi = mid;
+                }
+                grp_ncommit[g] = lo;
+            }
+            const int nlist = ngrp ? grp_off[ngrp - 1] + grp_cnt[ngrp - 1] : 0;
+            // segmented exclusive scan of dup_run over glist -> mlist[j]
+            {
+                const int per = (nlist + RS_THREADS - 1) / RS_THREADS;
+                const int jlo = min(nlist, tid * per), jhi = min(nlist, jlo + per);
+                int run = 0, head = 0;
+                for (int j = jlo; j < jhi; j++) {
+                    const int p = glist[j];
+                    if (j == 0 || seg_grp[glist[j - 1]] != seg_grp[p]) {
+                        run = 0;
+                        head = 1;
                     }
-                    grp_ncommit[g] = lo;
+                    mlist[j] = run;
+                    run += A.dup_run[A.c0 + p];
+                }
+                int v = run, h = head;  // inclusive warp scan, segmented operator
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int vp = __shfl_up_sync(0xffffffffu, v, o), hp = __shfl_up_sync(0xffffffffu, h, o);
+                    if (lane >= o) {
+                        if (!h) v += vp;
+                        h |= hp;
+                    }
+                }
+                if (lane == 31) {
+                    wsv[wid] = v;
+                    wsh[wid] = h;
+                }
+                int ve = __shfl_up_sync(0xffffffffu, v, 1), he = __shfl_up_sync(0xffffffffu, h, 1);
+                if (lane == 0) {
+                    ve = 0;
+                    he = 0;
+                }
+                __syncthreads();
+                if (tid == 0) {  // exclusive scan over warps
+                    int cv = 0, ch = 0;
+                    for (int w = 0; w < RS_WARPS; w++) {
+                        const int tv = wsv[w], th = wsh[w];
+                        wsv[w] = cv;
+                        wsh[w] = ch;
+                        cv = th ? tv : cv + tv;
+                        ch |= th;
+                    }
+                }
+                __syncthreads();
+                const int carry = he ? ve : wsv[wid] + ve;  // combine(warp prefix, lane prefix)
+                for (int j = jlo; j < jhi; j++) {
+                    if (j == 0 || seg_grp[glist[j - 1]] != seg_grp[glist[j]]) break;
+                    mlist[j] += carry;
                 }
             }
             __syncthreads();
-            auto commit_range = [&](const GroupCtx &G, int cid, int lo, int hi, float dr, int sz, int pend0) {
-                for (int i0 = lo; i0 < hi; i0 += 32) {
-                    const int i = i0 + lane;
-                    float a = 1.f, c = 0.f;
-                    int w = 0, p = 0;
-                    int64_t cc = 0;
-                    if (i < hi) {
-                        p = glist[G.off + i];
-                        cc = A.c0 + p;
-                        elem_map(G, i, seg_ub0[p], a, c);
-                        w = 1 + A.dup_run[cc];
-                    }
-                    warp_affine_scan(a, c, w, lane);
-                    if (i < hi) {
-                        const int64_t obj = A.cls_obj[cc];
-                        A.cluster_of[obj] = cid;
-                        A.mrank[obj] = sz + w - (1 + A.dup_run[cc]);
-                        A.frank[obj] = G.nf0 + i;
-                        A.pend_rank[p] = pend0 + i;
-                        A.slot_of[p] = G.sl;
-                        sh_slot_of[p] = G.sl;
-                    }
-                    const float a31 = __shfl_sync(0xffffffffu, a, 31), c31 = __shfl_sync(0xffffffffu, c, 31);
-                    dr = __fmaf_ru(a31, dr, c31);
-                    sz += __shfl_sync(0xffffffffu, w, 31);
-                }
-                return dr;
-            };
-            for (int g = 0; g < ngrp; g++) {
-                const int n_c = grp_ncommit[g];
-                if (n_c <= RS_BIGGRP) continue;
+            for (int j = tid; j < nlist; j += blockDim.x) {
+                const int p = glist[j];
+                const int g = seg_grp[p];
+                const int i = j - grp_off[g];
+                if (i >= grp_ncommit[g]) continue;
                 const int sl = grp_slot[g];
-                GroupCtx G{grp_off[g], A.s_nfeat[sl], sl, sqrtf(A.s_cn2[sl]) * 1.00001f};
-                const int seg = (n_c + RS_WARPS - 1) / RS_WARPS;
-                const int lo = min(n_c, wid * seg), hi = min(n_c, lo + seg);
-                float Aw, Cw;
-                int Ww;
-                gc_compose(G, lo, hi, glist, seg_ub0, A.dup_run, A.c0, Aw, Cw, Ww);
-                if (lane == 0) {
-                    wA[wid] = Aw;
-                    wC[wid] = Cw;
-                    wW[wid] = Ww;
-                }
-                __syncthreads();
-                if (tid == 0) {
-                    float d = __double2float_ru(A.s_drift[sl]);
-                    int sz = A.s_size[sl];
-                    for (int w = 0; w < RS_WARPS; w++) {
-                        wcarry[w] = d;
-                        wszc[w] = sz;
-                        d = __fmaf_ru(wA[w], d, wC[w]);
-                        sz += wW[w];
-                    }
-                    wcarry[RS_WARPS] = d;
-                    wszc[RS_WARPS] = sz;
-                }
-                __syncthreads();
-                commit_range(G, A.s_cid[sl], lo, hi, wcarry[wid], wszc[wid], A.s_pend[sl]);
-                __syncthreads();
-                if (tid == 0) {
+                const int64_t cc = A.c0 + p;
+                const int64_t obj = A.cls_obj[cc];
+                A.cluster_of[obj] = A.s_cid[sl];
+                A.mrank[obj] = A.s_size[sl] + i + mlist[j];
+                A.frank[obj] = grp_nf0[g] + i;
+                A.pend_rank[p] = A.s_pend[sl] + i;
+                A.slot_of[p] = sl;
+                sh_slot_of[p] = sl;
+            }
+            __syncthreads();
+            for (int g = tid; g < ngrp; g += blockDim.x) {
+                const int n_c = grp_ncommit[g];
+                const int sl = grp_slot[g];
+                if (n_c > 0) {
+                    const int jl = grp_off[g] + n_c - 1;
+                    const int dups = mlist[jl] + A.dup_run[A.c0 + glist[jl]];
                     const int pend0 = A.s_pend[sl];
-                    A.s_drift[sl] = (double)wcarry[RS_WARPS];
-                    A.s_nfeat[sl] = G.nf0 + n_c;
-                    A.s_size[sl] = wszc[RS_WARPS];
+                    A.s_drift[sl] = (double)drift_cf(grp_d0[g], grp_U[g], grp_nf0[g], n_c, grp_cn[g]);
+                    A.s_nfeat[sl] = grp_nf0[g] + n_c;
+                    A.s_size[sl] += n_c + dups;
                     A.s_pend[sl] = pend0 + n_c;
                     if (pend0 == 0) {
                         const int di = atomicAdd(&s_ndirty, 1);
@@ -1104,35 +1028,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
                         A.dirty[di] = sl;
                     }
                 }
-                __syncthreads();
-            }
-            for (int g = wid; g < ngrp; g += RS_WARPS) {
-                const int n_c = grp_ncommit[g];
-                const int sl = grp_slot[g];
-                if (n_c > 0 && n_c <= RS_BIGGRP) {
-                    GroupCtx G{grp_off[g], A.s_nfeat[sl], sl, sqrtf(A.s_cn2[sl]) * 1.00001f};
-                    const int pend0 = A.s_pend[sl];
-                    const int sz0 = A.s_size[sl];
-                    float Aw, Cw;
-                    int Ww;
-                    // sizes after the commit need the weight total: compose first (cheap for short groups)
-                    gc_compose(G, 0, n_c, glist, seg_ub0, A.dup_run, A.c0, Aw, Cw, Ww);
-                    const float d0 = __double2float_ru(A.s_drift[sl]);
-                    const float d1 = commit_range(G, A.s_cid[sl], 0, n_c, d0, sz0, pend0);
-                    if (lane == 0) {
-                        A.s_drift[sl] = (double)d1;
-                        A.s_nfeat[sl] = G.nf0 + n_c;
-                        A.s_size[sl] = sz0 + Ww;
-                        A.s_pend[sl] = pend0 + n_c;
-                        if (pend0 == 0) {
-                            const int di = atomicAdd(&s_ndirty, 1);
-                            A.s_didx[sl] = di;
-                            A.dirty[di] = sl;
-                        }
-                    }
-                }
-                __syncwarp();
-                if (lane == 0) A.s_grp[sl] = -1;
+                A.s_grp[sl] = -1;
             }
         }
         if (overflow) {
@@ -1435,18 +1331,37 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
 // One CTA per (dirty slot, FD-dimension slice).  A slot's members must be
 // added in stream order (float64 rounding is order dependent), so each
 // dimension is one dependent dadd chain; what limits the chain is how fast
-// member rows arrive.  All FOLD_THREADS threads stream the slot's rows into a
-// FOLD_NS-stage shared-memory ring with cp.async (FOLD_R rows x FD dims per
-// stage, FOLD_R = 64 float / 32 double rows) while warp 0 (lane = dimension) walks the chain out of shared
-// memory.  The dominant cluster of a Zipf stream owns most of a batch, so the
-// ring keeps FOLD_NS * FOLD_R rows in flight for it instead of a handful.
-constexpr int FD = 32, FOLD_NS = 4, FOLD_THREADS = 128;
+// member rows arrive.  Warp-specialised pipeline: warp 0 (lane = dimension)
+// walks the chain out of a FOLD_NS-buffer shared-memory ring; producer warp
+// w (1..FOLD_NS) owns buffer w-1 and fills it with every FOLD_NS-th stage of
+// R rows x FD dims (gather the rows' pointers, cp.async the slices, wait,
+// then publish with an mbarrier arrive).  So FOLD_NS * R rows are in flight
+// for the dominant cluster of a Zipf stream, which owns most of a batch.
+constexpr int FD = 32, FOLD_NS = 4, FOLD_THREADS = 32 * (1 + FOLD_NS);
+template <typename T>
+constexpr int fold_rows() { return sizeof(T) == 4 ? 128 : 64; }  // 16 KB per stage either way
+template <typename T>
+constexpr size_t fold_smem() { return (size_t)FOLD_NS * fold_rows<T>() * FD * sizeof(T); }
 
 __device__ __forceinline__ void cp_async_el(uint32_t dst, const void *src, bool ok, int bytes) {
     if (bytes == 4)
         asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 4 : 0));
     else
         asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(dst), "l"(src), "r"(ok ? 8 : 0));
+}
+__device__ __forceinline__ void fbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"((uint32_t)__cvta_generic_to_shared(bar)), "r"(count));
+}
+__device__ __forceinline__ void fbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"((uint32_t)__cvta_generic_to_shared(bar)) : "memory");
+}
+__device__ __forceinline__ void fbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile(
+        "{\n.reg .pred p;\nFW_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra FW_%=;\n}\n" ::"r"((uint32_t)__cvta_generic_to_shared(bar)),
+        "r"(parity)
+        : "memory");
 }
 
 template <typename T>
@@ -1459,56 +1374,43 @@ __global__ void __launch_bounds__(FOLD_THREADS) k_fold(int D, int64_t c0, const 
                                                       const int32_t *__restrict__ s_cid, const int32_t *__restrict__ s_size,
                                                       float *__restrict__ s_cn2, double *__restrict__ fcent,
                                                       int32_t *__restrict__ cl_nfeat, int32_t *__restrict__ cl_size) {
-    constexpr int FOLD_R = sizeof(T) == 4 ? 64 : 32;  // 32 KB ring for float, 32 KB for double
-    __shared__ __align__(16) T ring[FOLD_NS][FOLD_R][FD];
-    __shared__ unsigned char flag[FOLD_NS][FOLD_R];  // 0 add, 1 first (seed), 2 skip
+    constexpr int R = fold_rows<T>();
+    extern __shared__ __align__(16) unsigned char fold_raw[];
+    T *ring = (T *)fold_raw;                                                // [NS][R][FD]
+    __shared__ __align__(8) uint64_t full[FOLD_NS], empty[FOLD_NS];
     const int nd = (int)ctr[C_NDIRTY];
-    const int tid = threadIdx.x, lane = tid & 31;
-    const int kbase = blockIdx.x * FD;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int k = blockIdx.x * FD + lane;
+    // barrier phases run on across the slots this CTA folds: global stage G
+    // (counted over all of them) uses buffer G % NS, as its (G / NS)-th fill
+    if (tid < FOLD_NS) {
+        fbar_init(&full[tid], 1);
+        fbar_init(&empty[tid], 1);
+    }
+    __syncthreads();
+    int J0 = 0;
     for (int di = blockIdx.y; di < nd; di += gridDim.y) {
         const int slot = dirty[di];
         const int p0 = dirty_off[di], p1 = dirty_off[di + 1];
-        const int fp = s_foldpos[slot], sp = s_seedpos[slot];
-        const int nst = (p1 - p0 + FOLD_R - 1) / FOLD_R;
-        // stage j <- rows pend_list[p0 + j*R ...]; every thread copies R*FD/THREADS elements
-        auto issue = [&](int j) {
-            if (j < nst) {
-                const int buf = j % FOLD_NS;
-                for (int e = tid; e < FOLD_R * FD; e += FOLD_THREADS) {
-                    const int r = e / FD, c = e % FD;
-                    const int p = p0 + j * FOLD_R + r;
-                    const int k = kbase + c;
-                    int b = -1;
-                    if (p < p1) b = pend_list[p];
-                    const bool use = b >= fp && b >= 0;  // members folded by the resolve's exact path are skipped
-                    const T *src = use ? (const T *)frow[c0 + b] + k : (const T *)frow[c0];
-                    cp_async_el((uint32_t)__cvta_generic_to_shared(&ring[buf][r][c]), src, use && k < D, (int)sizeof(T));
-                    if (c == 0) flag[buf][r] = use ? (b == sp ? 1 : 0) : 2;
-                }
-            }
-            asm volatile("cp.async.commit_group;\n" ::);
-        };
-        for (int j = 0; j < FOLD_NS - 1; j++) issue(j);
-        const int k = kbase + lane;
-        double acc = (tid < 32 && k < D) ? S[(int64_t)slot * D + k] : 0.0;
-        for (int j = 0; j < nst; j++) {
-            asm volatile("cp.async.wait_group %0;\n" ::"n"(FOLD_NS - 2));
-            __syncthreads();
-            issue(j + FOLD_NS - 1);  // refills the buffer consumed in iteration j-1
-            if (tid < 32) {
-                const int buf = j % FOLD_NS;
-                const int nr = min(FOLD_R, p1 - p0 - j * FOLD_R);
+        const int nst = (p1 - p0 + R - 1) / R;
+        if (wid == 0) {
+            // consumer: the float64 chain, one dimension per lane.  Every row is
+            // a plain add: a slot seeded in this batch starts from -0.0 (its
+            // seed row then lands exactly: -0 + v = v, like the reference's
+            // sum = feature.copy()), skipped rows hold -0.0 (x + -0 = x for
+            // every x), so the chain is one dadd per row (~18 cycles on B200).
+            const int fp = s_foldpos[slot], sp = s_seedpos[slot];
+            double acc = (sp >= 0 && sp >= fp) ? -0.0 : (k < D ? S[(int64_t)slot * D + k] : 0.0);
+            for (int j = 0; j < nst; j++) {
+                const int G = J0 + j, buf = G % FOLD_NS;
+                fbar_wait(&full[buf], (uint32_t)((G / FOLD_NS) & 1));
+                const int nr = min(R, p1 - p0 - j * R);
+                const T *rb = ring + (size_t)buf * R * FD + lane;
 #pragma unroll 8
-                for (int r = 0; r < nr; r++) {
-                    const unsigned char fl = flag[buf][r];
-                    const double v = to_d(ring[buf][r][lane]);
-                    const double add = dadd(acc, v);
-                    acc = fl == 1 ? v : (fl == 0 ? add : acc);
-                }
+                for (int r = 0; r < nr; r++) acc = dadd(acc, to_d(rb[r * FD]));
+                __syncwarp();
+                if (lane == 0) fbar_arrive(&empty[buf]);
             }
-        }
-        asm volatile("cp.async.wait_group 0;\n" ::);
-        if (tid < 32) {
             float c2 = 0.f;
             if (k < D) {
                 S[(int64_t)slot * D + k] = acc;
@@ -1526,8 +1428,49 @@ __global__ void __launch_bounds__(FOLD_THREADS) k_fold(int D, int64_t c0, const 
                     cl_size[s_cid[slot]] = s_size[slot];
                 }
             }
+        } else {
+            // producer for buffer w: global stages G = w (mod NS)
+            const int w = wid - 1;
+            const int fp = s_foldpos[slot];
+            for (int j = (w - J0 % FOLD_NS + FOLD_NS) % FOLD_NS; j < nst; j += FOLD_NS) {
+                const int G = J0 + j;
+                if (G >= FOLD_NS) fbar_wait(&empty[w], (uint32_t)(((G / FOLD_NS) - 1) & 1));
+                const int rbase = p0 + j * R, nr = min(R, p1 - rbase);
+                T *dst = ring + (size_t)w * R * FD;
+                // lane l gathers the pointers of rows l, l+32, ... (coalesced,
+                // independent loads), then the warp broadcasts them row by row
+                const T *rp[R / 32];
+#pragma unroll
+                for (int c = 0; c < R / 32; c++) {
+                    const int row = c * 32 + lane;
+                    const int bq = row < nr ? pend_list[rbase + row] : -1;
+                    rp[c] = (const T *)(intptr_t)bq;  // stash the position; resolved below
+                }
+#pragma unroll
+                for (int c = 0; c < R / 32; c++) {
+                    const int bq = (int)(intptr_t)rp[c];
+                    rp[c] = bq >= fp ? (const T *)frow[c0 + bq] : nullptr;
+                }
+#pragma unroll
+                for (int c = 0; c < R / 32; c++) {
+                    for (int i = 0; i < 32; i++) {
+                        const int row = c * 32 + i;
+                        if (row >= nr) break;
+                        const T *src = (const T *)__shfl_sync(0xffffffffu, (unsigned long long)rp[c], i);
+                        T *d = dst + (size_t)row * FD + lane;
+                        if (src != nullptr)
+                            cp_async_el((uint32_t)__cvta_generic_to_shared(d), (const void *)(src + k), k < D,
+                                        (int)sizeof(T));
+                        else
+                            *d = (T)(-0.0);  // member already folded by the resolve's exact path
+                    }
+                }
+                asm volatile("cp.async.wait_all;\n" ::: "memory");
+                __syncwarp();
+                if (lane == 0) fbar_arrive(&full[w]);
+            }
         }
-        __syncthreads();  // the ring is reused by the next slot
+        J0 += nst;
     }
 }
 
@@ -1632,6 +1575,11 @@ static double screen_rel(int D) {
     return 2.0 * (g / 2.0 + u) + 1e-12;
 }
 
+// dynamic shared memory of k_resolve for batch capacity Bc (static smem ~39 KB on top)
+size_t resolve_smem(int Bc, const PwPlan &P) {
+    return (size_t)RS_WCNT_BYTES + (size_t)Bc * (8 * 4 + 2 + 1) + 16 + sizeof(double) * (P.n_chains + P.n_leaves + P.n_ops + 8);
+}
+
 template <typename T>
 void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
     cudaStream_t st = s->st;
@@ -1645,6 +1593,8 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
     auto hms = [](hclock::time_point a, hclock::time_point b) {
         return std::chrono::duration<double, std::milli>(b - a).count();
     };
+    std::vector<double> chk_expect;
+    std::vector<int32_t> chk_slots;
     for (int64_t c0 = c_begin, B = 0; c0 < c_end; c0 += B) {
         const auto h0 = hclock::now();
         // the drift bound grows like (batch size / objects so far): keep batches
@@ -1757,7 +1707,7 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             A.sum_e1 = s->sum_e1.p;
             A.sum_lbr = s->sum_lbr.p;
             const PwPlan &P = *s->plan_host;
-            size_t smem = (size_t)s->B * (8 + 4 * 8 + 2 + 1) + 16 + sizeof(double) * (P.n_chains + P.n_leaves + P.n_ops + 8);
+            size_t smem = resolve_smem(s->B, P);
             auto kern = k_resolve<T>;
             static size_t smem_set[2] = {0, 0};
             size_t &cur = smem_set[sizeof(T) == 8];
@@ -1798,6 +1748,55 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
         }
         const auto h3 = hclock::now();
         s->t_ms[10] += hms(h2, h3);
+        if (s->debug_check) {  // FOCUS_B200_CHECK=1: host-side invariants of the resolve output
+            FX_CUDA(cudaStreamSynchronize(st));
+            int64_t hc[C_COUNT];
+            FX_CUDA(cudaMemcpy(hc, s->ctr.p, sizeof(hc), cudaMemcpyDeviceToHost));
+            const int nd = (int)hc[C_NDIRTY];
+            std::vector<int32_t> dr(nd), doff(nd + 1), pl(B), so(B), seedp(s->nslots), foldp(s->nslots);
+            FX_CUDA(cudaMemcpy(dr.data(), s->dirty.p, 4 * nd, cudaMemcpyDeviceToHost));
+            FX_CUDA(cudaMemcpy(doff.data(), s->dirty_off.p, 4 * (nd + 1), cudaMemcpyDeviceToHost));
+            FX_CUDA(cudaMemcpy(pl.data(), s->pend_list.p, 4 * B, cudaMemcpyDeviceToHost));
+            FX_CUDA(cudaMemcpy(so.data(), s->slot_of.p, 4 * B, cudaMemcpyDeviceToHost));
+            FX_CUDA(cudaMemcpy(seedp.data(), s->s_seedpos.p, 4 * s->nslots, cudaMemcpyDeviceToHost));
+            FX_CUDA(cudaMemcpy(foldp.data(), s->s_foldpos.p, 4 * s->nslots, cudaMemcpyDeviceToHost));
+            std::vector<int> seen(s->nslots, 0);
+            for (int i = 0; i < nd; i++) {
+                const int sl = dr[i];
+                if (seen[sl]++) fprintf(stderr, "CHECK batch %ld: slot %d dirty twice\n", (long)s->batch_no, sl);
+                for (int p = doff[i]; p < doff[i + 1]; p++) {
+                    const int b = pl[p];
+                    if (b < 0 || b >= B || so[b] != sl || (p > doff[i] && b <= pl[p - 1]))
+                        fprintf(stderr, "CHECK batch %ld: slot %d row %d -> pos %d (slot_of %d)\n", (long)s->batch_no, sl,
+                                p - doff[i], b, (b >= 0 && b < B) ? so[b] : -9);
+                }
+                if (seedp[sl] >= 0 && doff[i + 1] > doff[i] && seedp[sl] >= foldp[sl] && pl[doff[i]] != seedp[sl])
+                    fprintf(stderr, "CHECK batch %ld: seed slot %d first row %d != seed %d\n", (long)s->batch_no, sl,
+                            pl[doff[i]], seedp[sl]);
+            }
+            if (doff[nd] != B) fprintf(stderr, "CHECK batch %ld: %d pending rows for %ld objects\n", (long)s->batch_no, doff[nd], (long)B);
+            if (s->batch_no < 3) fprintf(stderr, "CHECK batch %ld: %d dirty slots ok\n", (long)s->batch_no, nd);
+            // expected sums of the dirty slots after the fold (host, sequential float64)
+            std::vector<const char *> fr(B);
+            FX_CUDA(cudaMemcpy(fr.data(), s->frow.p + c0, sizeof(void *) * B, cudaMemcpyDeviceToHost));
+            chk_expect.assign((size_t)nd * D, 0.0);
+            chk_slots = dr;
+            std::vector<double> srow(D);
+            std::vector<T> frw(D);
+            for (int i = 0; i < nd; i++) {
+                const int sl = dr[i];
+                FX_CUDA(cudaMemcpy(srow.data(), s->S.p + (size_t)sl * D, 8 * D, cudaMemcpyDeviceToHost));
+                bool fresh = seedp[sl] >= 0 && seedp[sl] >= foldp[sl];
+                for (int p = doff[i]; p < doff[i + 1]; p++) {
+                    const int b = pl[p];
+                    if (b < foldp[sl]) continue;
+                    FX_CUDA(cudaMemcpy(frw.data(), fr[b], sizeof(T) * D, cudaMemcpyDeviceToHost));
+                    for (int k = 0; k < D; k++) srow[k] = fresh ? (double)frw[k] : srow[k] + (double)frw[k];
+                    fresh = false;
+                }
+                std::copy(srow.begin(), srow.end(), chk_expect.begin() + (size_t)i * D);
+            }
+        }
         // 5. fold (persistent grid over the batch's dirty slots)
         {
             s->tstart(3);
@@ -1807,12 +1806,32 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             const int64_t gx = cdiv(D, FD);
             const int64_t gy = std::max<int64_t>(8, std::min<int64_t>(2 * (int64_t)B + 1, (148 * 12) / gx));
             dim3 grid((unsigned)gx, (unsigned)gy);
-            k_fold<T><<<grid, FOLD_THREADS, 0, st>>>(D, c0, s->ctr.p, s->dirty.p, s->dirty_off.p, s->pend_list.p, s->frow.p,
+            static bool fold_attr[2] = {false, false};
+            if (!fold_attr[sizeof(T) == 8]) {
+                FX_CUDA(cudaFuncSetAttribute(k_fold<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fold_smem<T>()));
+                fold_attr[sizeof(T) == 8] = true;
+            }
+            k_fold<T><<<grid, FOLD_THREADS, fold_smem<T>(), st>>>(D, c0, s->ctr.p, s->dirty.p, s->dirty_off.p, s->pend_list.p, s->frow.p,
                                             s->S.p, s->C32.p, s->s_nfeat.p, s->s_foldpos.p, s->s_seedpos.p,
                                             s->s_evicted.p, s->s_cid.p, s->s_size.p, s->s_cn2.p, s->fcent.p,
                                             s->cl_nfeat.p, s->cl_size.p);
             FX_LAUNCHED();
             s->tstop();
+        }
+        if (s->debug_check) {
+            FX_CUDA(cudaStreamSynchronize(st));
+            std::vector<double> srow(D);
+            int nbad = 0;
+            for (size_t i = 0; i < chk_slots.size(); i++) {
+                FX_CUDA(cudaMemcpy(srow.data(), s->S.p + (size_t)chk_slots[i] * D, 8 * D, cudaMemcpyDeviceToHost));
+                for (int k = 0; k < D; k++)
+                    if (memcmp(&srow[k], &chk_expect[i * D + k], 8) != 0) {
+                        if (nbad++ < 5)
+                            fprintf(stderr, "CHECK batch %ld: fold slot %d dim %d got %.17g want %.17g\n",
+                                    (long)s->batch_no, chk_slots[i], k, srow[k], chk_expect[i * D + k]);
+                        break;
+                    }
+            }
         }
         s->t_ms[11] += hms(h3, hclock::now());
     }
