@@ -570,22 +570,86 @@ __global__ void k_row_summary(int nA, const int64_t *__restrict__ ctr, const flo
 
 
 constexpr int RS_MAXGRP = 1024;
-constexpr int RS_WCNT_BYTES = RS_WARPS * RS_MAXGRP * 2;
+constexpr int RS_RANKW = 8;  // warps that rank a window (per-warp group counters)
+constexpr int RS_WCNT_BYTES = RS_RANKW * RS_MAXGRP * 2;
 constexpr int RS_WIN0 = 64;
 
-// Closed-form drift bound for a group's chain inside one window: before its
-// (i+1)-th join the slot's centroid is within d_i of the reference the
-// hypothesis bounds refer to, where each join moves the centroid by
-// (f - c)/n' and |f - c| <= U + d (U = largest hypothesis bound of the group):
-//   d_i + U <= (d0 + U) prod_{m<i} (1 + 1/(nf0+m+1)) = (d0 + U)(nf0+i+1)/(nf0+1)
-// so d_i <= d0 r + U i/(nf0+1), r = (nf0+i+1)/(nf0+1); the float64 rounding of
-// each join (8 u (|c| + d + ub), as in drift_step) is added, amplified by r.
-__device__ __forceinline__ float drift_cf(float d0, float U, int nf0, int i, float cn) {
-    const double n1 = (double)nf0 + 1.0;
-    const double r = (n1 + (double)i) / n1;
-    const double core = (double)d0 * r + (double)U * ((double)i / n1);
-    const double slack = (double)i * 8.0 * 1.1102230246251565e-16 * ((double)cn + 2.0 * core + 2.0 * (double)U) * r;
+// Drift bound for a group inside one window.  With c_ref the point the
+// hypothesis bounds refer to (snapshot centroid, or the seed's feature) and
+// c_w the slot's centroid at window start (|c_w - c_ref| <= d0, nf0 featured
+// members), after i more joins the centroid is the exact mean
+//   c_i = (nf0 c_w + sum_{q<i} f_q) / (nf0 + i),
+// so |c_i - c_ref| <= (nf0 d0 + sum_{q<i} |f_q - c_ref|) / (nf0 + i) and
+// |f_q - c_ref| <= ub0_q (P = that sum of bounds).  The float64 rounding of
+// the i running-sum adds and of the two divisions adds at most
+// (i + 4) 4u (2|c| + d0 + U) (u = 2^-53, U = largest ub0 of the group).
+__device__ __forceinline__ float drift_avg(float d0, int nf0, float P, int i, float cn, float U) {
+    const double n = (double)nf0 + (double)i;
+    const double core = ((double)nf0 * (double)d0 + (double)P) / n;
+    const double slack = ((double)i + 4.0) * 4.0 * 1.1102230246251565e-16 * (2.0 * (double)cn + (double)d0 + (double)U);
     return __double2float_ru((core + slack) * (1.0 + 1e-12));
+}
+
+// Segmented exclusive scan (fp32, every add rounded up -> an upper bound of
+// the exact sum) of val[list[j]] over list positions j in [0, n); a segment
+// starts where the group id changes.  Whole block; out[j] by list position.
+__device__ void seg_scan_ub(int n, const int32_t *list, const short *grp, const float *val, float *out, float *wsf,
+                            int *wsh) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nthr = blockDim.x;
+    const int per = (n + nthr - 1) / nthr;
+    const int jlo = min(n, tid * per), jhi = min(n, jlo + per);
+    float run = 0.f;
+    int head = 0;
+    for (int j = jlo; j < jhi; j++) {
+        const int p = list[j];
+        if (j == 0 || grp[list[j - 1]] != grp[p]) {
+            run = 0.f;
+            head = 1;
+        }
+        out[j] = run;
+        run = __fadd_ru(run, val[p]);
+    }
+    float v = run;
+    int h = head;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const float vp = __shfl_up_sync(0xffffffffu, v, o);
+        const int hp = __shfl_up_sync(0xffffffffu, h, o);
+        if (lane >= o) {
+            if (!h) v = __fadd_ru(v, vp);
+            h |= hp;
+        }
+    }
+    if (lane == 31) {
+        wsf[wid] = v;
+        wsh[wid] = h;
+    }
+    float ve = __shfl_up_sync(0xffffffffu, v, 1);
+    int he = __shfl_up_sync(0xffffffffu, h, 1);
+    if (lane == 0) {
+        ve = 0.f;
+        he = 0;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        float cv = 0.f;
+        int ch = 0;
+        for (int w = 0; w < (nthr >> 5); w++) {
+            const float tv = wsf[w];
+            const int th = wsh[w];
+            wsf[w] = cv;
+            wsh[w] = ch;
+            cv = th ? tv : __fadd_ru(cv, tv);
+            ch |= th;
+        }
+    }
+    __syncthreads();
+    const float carry = he ? ve : __fadd_ru(wsf[wid], ve);
+    for (int j = jlo; j < jhi; j++) {
+        if (j == 0 || grp[list[j - 1]] != grp[list[j]]) break;
+        out[j] = __fadd_ru(out[j], carry);
+    }
+    __syncthreads();
 }
 
 __device__ __forceinline__ double drift_step(double dr, double ub, int nf, double cn) {
@@ -599,7 +663,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int B = A.B;
     const int BC = A.Bcap;  // layout by capacity (multiple of 64): every array stays aligned
-    unsigned short *wcnt = (unsigned short *)smem_raw;    // [RS_WARPS][RS_MAXGRP] per-warp group counts
+    unsigned short *wcnt = (unsigned short *)smem_raw;    // [RS_RANKW][RS_MAXGRP] per-warp group counts
     int32_t *sh_slot_of = (int32_t *)(smem_raw + RS_WCNT_BYTES);  // [B]
     int *mlist = (int *)(sh_slot_of + BC);                 // [B]
     int32_t *seg_key = (int32_t *)(mlist + BC);            // [B] hypothesis slot
@@ -608,7 +672,8 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
     int32_t *seedlist = (int32_t *)(seg_lbr + BC);         // [B] in-batch seed slots
     int32_t *seg_nf = seedlist + BC;                       // [B] rank inside the hypothesis group
     int32_t *glist = seg_nf + BC;                         // [B] group-ordered positions
-    short *seg_grp = (short *)(glist + BC);               // [B]
+    float *seg_P = (float *)(glist + BC);                 // [B] by list position: sum of ub0 over earlier group members
+    short *seg_grp = (short *)(seg_P + BC);               // [B]
     unsigned char *seg_flag = (unsigned char *)(seg_grp + BC);  // [B]
     double *scratch = (double *)(seg_flag + BC);          // pairwise scratch
     __shared__ Cand red[RS_WARPS];
@@ -628,6 +693,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
     __shared__ int s_md1_slot;
     __shared__ double wmd1[RS_WARPS], wmd2[RS_WARPS];
     __shared__ int wmds[RS_WARPS], wsv[RS_WARPS], wsh[RS_WARPS];
+    __shared__ float wsf[RS_WARPS];
 
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     int64_t *ctr = A.ctr;
@@ -770,11 +836,11 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
         // ranks a contiguous chunk (match per 32-slice, warp-private counts),
         // an exclusive scan over warps per group gives the chunk bases.
         const int nwin = e_end - b;
-        const int cs = ((nwin + RS_WARPS * 32 - 1) / (RS_WARPS * 32)) * 32;
+        const int cs = ((nwin + RS_RANKW * 32 - 1) / (RS_RANKW * 32)) * 32;
         if (!overflow) {
-            for (int e = tid; e < RS_WARPS * ngrp; e += blockDim.x) wcnt[e] = 0;
+            for (int e = tid; e < RS_RANKW * ngrp; e += blockDim.x) wcnt[e] = 0;
             __syncthreads();
-            const int lo = b + wid * cs, hi = min(e_end, lo + cs);
+            const int lo = wid < RS_RANKW ? b + wid * cs : e_end, hi = min(e_end, lo + cs);
             for (int p0 = lo; p0 < hi; p0 += 32) {
                 const int p = p0 + lane;
                 const int g = p < hi ? seg_grp[p] : -1;
@@ -792,7 +858,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
             __syncthreads();
             for (int g = tid; g < ngrp; g += blockDim.x) {
                 int run = 0;
-                for (int w = 0; w < RS_WARPS; w++) {
+                for (int w = 0; w < RS_RANKW; w++) {
                     const int c = wcnt[w * ngrp + g];
                     wcnt[w * ngrp + g] = (unsigned short)run;
                     run += c;
@@ -824,8 +890,16 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
                 const int g = seg_grp[p];
                 if (g >= 0) glist[grp_off[g] + seg_nf[p]] = p;
             }
-            for (int g = tid; g < ngrp; g += blockDim.x)
-                grp_drift[g] = drift_cf(grp_d0[g], grp_U[g], grp_nf0[g], grp_cnt[g], grp_cn[g]);
+            __syncthreads();
+            // per object: sum of the hypothesis bounds of the group's earlier
+            // members (segmented exclusive scan over glist, fp32 rounded up)
+            const int nlist = ngrp ? grp_off[ngrp - 1] + grp_cnt[ngrp - 1] : 0;
+            seg_scan_ub(nlist, glist, seg_grp, seg_ub0, seg_P, wsf, wsh);
+            for (int g = tid; g < ngrp; g += blockDim.x) {
+                const int jl = grp_off[g] + grp_cnt[g] - 1;
+                const float Ptot = __fadd_ru(seg_P[jl], seg_ub0[glist[jl]]);
+                grp_drift[g] = drift_avg(grp_d0[g], grp_nf0[g], Ptot, grp_cnt[g], grp_cn[g], grp_U[g]);
+            }
         }
         __syncthreads();
         long long t2 = clock64();
@@ -889,8 +963,9 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
             unsigned char fl = 2;
             if (key >= 0 && !overflow) {
                 const int g = seg_grp[p];
-                const double ub =
-                    (double)seg_ub0[p] + (double)drift_cf(grp_d0[g], grp_U[g], grp_nf0[g], seg_nf[p], grp_cn[g]);
+                const int i = seg_nf[p];
+                const double ub = (double)seg_ub0[p] +
+                                  (double)drift_avg(grp_d0[g], grp_nf0[g], seg_P[grp_off[g] + i], i, grp_cn[g], grp_U[g]);
                 const double md = (key == s_md1_slot) ? s_md2 : s_md1;
                 const double lbo = (double)seg_lbr[p] - md * 1.000001;
                 if (lbo > ub) fl = ub <= A.T ? 0 : 1;
@@ -1018,7 +1093,8 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
                     const int jl = grp_off[g] + n_c - 1;
                     const int dups = mlist[jl] + A.dup_run[A.c0 + glist[jl]];
                     const int pend0 = A.s_pend[sl];
-                    A.s_drift[sl] = (double)drift_cf(grp_d0[g], grp_U[g], grp_nf0[g], n_c, grp_cn[g]);
+                    const float Pc = __fadd_ru(seg_P[jl], seg_ub0[glist[jl]]);
+                    A.s_drift[sl] = (double)drift_avg(grp_d0[g], grp_nf0[g], Pc, n_c, grp_cn[g], grp_U[g]);
                     A.s_nfeat[sl] = grp_nf0[g] + n_c;
                     A.s_size[sl] += n_c + dups;
                     A.s_pend[sl] = pend0 + n_c;
@@ -1577,7 +1653,7 @@ static double screen_rel(int D) {
 
 // dynamic shared memory of k_resolve for batch capacity Bc (static smem ~39 KB on top)
 size_t resolve_smem(int Bc, const PwPlan &P) {
-    return (size_t)RS_WCNT_BYTES + (size_t)Bc * (8 * 4 + 2 + 1) + 16 + sizeof(double) * (P.n_chains + P.n_leaves + P.n_ops + 8);
+    return (size_t)RS_WCNT_BYTES + (size_t)Bc * (9 * 4 + 2 + 1) + 16 + sizeof(double) * (P.n_chains + P.n_leaves + P.n_ops + 8);
 }
 
 template <typename T>
