@@ -730,7 +730,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
     for (int b = tid; b < B; b += blockDim.x) sh_slot_of[b] = -1;
     __syncthreads();
 
-    int b = 0, win = min(B, 1024);
+    int b = 0, win = B;  // first window: the whole batch (failures shrink it)
     while (b < B) {
         // =================== parallel segment: speculate every object in
         // [b, e_end) joins its nearest candidate, verify with bounds, commit
@@ -1691,6 +1691,8 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
                                                             s->dist.p, s->ld);
             FX_LAUNCHED();
         }
+        s->tstop();
+        s->tstart(7);  // residual detection + columns
         // 2. residuals + their in-batch columns
         {
             k_residuals<<<(unsigned)cdiv((int64_t)B * 32, 256), 256, 0, st>>>(
@@ -1715,6 +1717,8 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
                                                                rc_ok ? RC_MAX : -1);
             FX_LAUNCHED();
         }
+        s->tstop();
+        s->tstart(15);  // row summary (+ fp32 refine of the best candidate)
         k_row_summary<T><<<(unsigned)cdiv((int64_t)B * 32, 256), 256, 0, st>>>(
             B, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p, s->snap_slot.p, s->fnorm.p, c0, sm, rel, absc, s->frow.p,
             s->C32.p, D, s->sum_slot.p, s->sum_d1.p, s->sum_e1.p, s->sum_lbr.p);
