@@ -361,6 +361,7 @@ static void ingest_chunk(fx_stream *s, int64_t n, const int64_t *d_oid, const in
         k_lead_dups<<<1, 256, 0, st>>>(lead, s->ctr.p, s->live.p, s->s_cid.p, s->s_size.p, s->cl_size.p);
         FX_LAUNCHED();
     }
+    if (((uintptr_t)d_feats % 16) != 0 || ((int64_t)s->cfg.dim * s->esize) % 16 != 0) s->rows_aligned16 = false;
     launch_compact(s, n, n0, c0, s->is_dup.p + n0, excl.p, d_feats, compact);
     launch_fnorm(s, c0, nc);
     // K1: top-K

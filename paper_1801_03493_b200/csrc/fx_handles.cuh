@@ -39,7 +39,8 @@ struct fx_stream {
     int esize = 4;             // feature element size
     bool tc_screen = false;    // tcgen05 TF32 screen (f32 features, D % 4 == 0)
     bool finalized = false;
-    bool debug_check = false;  // FOCUS_B200_CHECK=1: per-batch host-side invariant checks (slow)
+    bool debug_check = false;
+    bool rows_aligned16 = true;  // every feature row pointer so far is 16-byte aligned  // FOCUS_B200_CHECK=1: per-batch host-side invariant checks (slow)
 
     // rank model
     bool has_rm = false;

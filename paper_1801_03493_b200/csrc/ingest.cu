@@ -569,6 +569,128 @@ __global__ void k_row_summary(int nA, const int64_t *__restrict__ ctr, const flo
 }
 
 
+// Fused per-row pass for FP32 features with D % 4 == 0, D <= 128 * NV and
+// 16-byte aligned rows (one warp per batch object, row held in registers as
+// NV float4 per lane, lane l owning elements 4 (l + 32 j) .. +3):
+//   * row summary of the snapshot screen (best candidate by upper bound, its
+//     interval, min lower bound of the rest), as k_row_summary;
+//   * FP32 direct-difference re-measure of the best candidate when the TF32
+//     interval is not already decisive (u1 > 0.85 T or the rest within 2 u1);
+//   * the row's in-batch distance columns to residuals at earlier positions
+//     (<= RC_MAX residuals; more go to the tiled SIMT kernel), as k_res_cols.
+// Each lane sums at most 4 NV <= 64 squared differences sequentially, then a
+// 5-level warp tree: within the SIMT screen model screen_rel(D).
+template <int NV>
+__global__ void __launch_bounds__(256) k_rowpass(int nA, int64_t a0, const char *const *__restrict__ frow, int D,
+                                                const int64_t *__restrict__ ctr, const float *__restrict__ dist,
+                                                int64_t ld, const float *__restrict__ cn2, const int32_t *__restrict__ snap,
+                                                const float *__restrict__ fnorm, ScreenModel sm, float rel, float absc,
+                                                const float *__restrict__ C32, double T, const int32_t *__restrict__ res_pos,
+                                                float *__restrict__ dres, int64_t ldr, int32_t *__restrict__ sum_slot,
+                                                float *__restrict__ sum_d1, float *__restrict__ sum_e1,
+                                                float *__restrict__ sum_lbr) {
+    __shared__ int s_rpos[RC_MAX];
+    __shared__ int s_pmin;
+    const int nsnap = (int)ctr[C_NSNAP];
+    const int nres_all = (int)ctr[C_NRES];
+    const int nres = nres_all <= RC_MAX ? nres_all : 0;  // more: the tiled kernel writes the columns
+    if (threadIdx.x == 0) s_pmin = INT_MAX;
+    __syncthreads();
+    for (int r = threadIdx.x; r < nres; r += blockDim.x) {
+        s_rpos[r] = res_pos[r];
+        atomicMin(&s_pmin, res_pos[r]);
+    }
+    __syncthreads();
+    const int pmin = s_pmin;
+    const int lane = threadIdx.x & 31;
+    const int nw = blockDim.x >> 5;
+    for (int w = blockIdx.x * nw + (threadIdx.x >> 5); w < nA; w += gridDim.x * nw) {
+        const float fn = fnorm[a0 + w];
+        float u1 = INFINITY, l1 = INFINITY, lbr = INFINITY;
+        int q1 = -1;
+        for (int q = lane; q < nsnap; q += 32) {
+            float lb, ub;
+            snap_bounds(sm, dist[(int64_t)w * ld + q], sqrtf(cn2[snap[q]]) * 1.00001f, fn, lb, ub);
+            if (ub < u1) {
+                if (q1 >= 0) lbr = fminf(lbr, l1);
+                u1 = ub;
+                l1 = lb;
+                q1 = q;
+            } else {
+                lbr = fminf(lbr, lb);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const float ou = __shfl_xor_sync(0xffffffffu, u1, o), ol = __shfl_xor_sync(0xffffffffu, l1, o);
+            const float olbr = __shfl_xor_sync(0xffffffffu, lbr, o);
+            const int oq = __shfl_xor_sync(0xffffffffu, q1, o);
+            const bool take = oq >= 0 && (q1 < 0 || ou < u1 || (ou == u1 && oq < q1));
+            if (take) {
+                lbr = fminf(fminf(lbr, olbr), q1 >= 0 ? l1 : INFINITY);
+                u1 = ou;
+                l1 = ol;
+                q1 = oq;
+            } else {
+                lbr = fminf(fminf(lbr, olbr), oq >= 0 ? ol : INFINITY);
+            }
+        }
+        float d1 = 0.5f * (l1 + u1), e1 = 0.5f * (u1 - l1);
+        const bool refine = sm.tc && q1 >= 0;  // a tight ub0 keeps the resolve's drift bounds small
+        const bool cols = nres > 0 && w > pmin;
+        if (refine || cols) {
+            const float4 *f4 = (const float4 *)frow[a0 + w];
+            float4 x[NV];
+#pragma unroll
+            for (int j = 0; j < NV; j++) {
+                const int e = lane + 32 * j;
+                x[j] = (4 * e < D) ? __ldg(f4 + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            auto dist_to = [&](const float4 *c4) {
+                float acc = 0.f;
+#pragma unroll
+                for (int j = 0; j < NV; j++) {
+                    const int e = lane + 32 * j;
+                    if (4 * e < D) {
+                        const float4 c = __ldg(c4 + e);
+                        float d = x[j].x - c.x;
+                        acc = fmaf(d, d, acc);
+                        d = x[j].y - c.y;
+                        acc = fmaf(d, d, acc);
+                        d = x[j].z - c.z;
+                        acc = fmaf(d, d, acc);
+                        d = x[j].w - c.w;
+                        acc = fmaf(d, d, acc);
+                    }
+                }
+                return sqrtf(warp_sum(acc));
+            };
+            if (refine) {
+                const float dd = dist_to((const float4 *)(C32 + (int64_t)snap[q1] * D));
+                const float ee = rel * dd + absc * (sqrtf(cn2[snap[q1]]) * 1.00001f + fn) + 1e-30f;
+                if (dd + ee < u1) {  // keep whichever interval is tighter (both are valid)
+                    d1 = dd;
+                    e1 = ee;
+                }
+            }
+            if (cols) {
+                for (int r = 0; r < nres; r++) {
+                    const int rp = s_rpos[r];
+                    if (rp >= w) continue;
+                    const float v = dist_to((const float4 *)frow[a0 + rp]);
+                    if (lane == 0) dres[(int64_t)w * ldr + r] = v;
+                }
+            }
+        }
+        if (lane == 0) {
+            sum_slot[w] = q1 >= 0 ? snap[q1] : -1;
+            sum_d1[w] = d1;
+            sum_e1[w] = e1;
+            sum_lbr[w] = lbr;
+        }
+    }
+}
+
 constexpr int RS_MAXGRP = 1024;
 constexpr int RS_RANKW = 8;  // warps that rank a window (per-warp group counters)
 constexpr int RS_WCNT_BYTES = RS_RANKW * RS_MAXGRP * 2;
@@ -1671,6 +1793,8 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
     };
     std::vector<double> chk_expect;
     std::vector<int32_t> chk_slots;
+    // fused row pass: FP32 rows, D % 4 == 0, D <= 2048, 16-byte aligned rows
+    const bool rowpass = sizeof(T) == 4 && D % 4 == 0 && D <= 2048 && s->rows_aligned16;
     for (int64_t c0 = c_begin, B = 0; c0 < c_end; c0 += B) {
         const auto h0 = hclock::now();
         // the drift bound grows like (batch size / objects so far): keep batches
@@ -1700,7 +1824,7 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
                 s->res_col.p, s->res_pos.p, s->ctr.p + C_NRES);
             FX_LAUNCHED();
             const bool rc_ok = D <= 6144;  // RC_COLS staged rows fit in shared memory
-            if (rc_ok) {
+            if (rc_ok && !rowpass) {
                 const size_t smem = sizeof(float) * RC_COLS * D;
                 static size_t rc_set[2] = {0, 0};
                 size_t &cur = rc_set[sizeof(T) == 8];
@@ -1719,10 +1843,25 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
         }
         s->tstop();
         s->tstart(15);  // row summary (+ fp32 refine of the best candidate)
+        if (rowpass) {
+            const unsigned grid = (unsigned)std::min<int64_t>(cdiv((int64_t)B * 32, 256), 148 * 8);
+            if (D <= 1024)
+                k_rowpass<8><<<grid, 256, 0, st>>>(B, c0, s->frow.p, D, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p,
+                                                   s->snap_slot.p, s->fnorm.p, sm, rel, absc, s->C32.p, s->cfg.t,
+                                                   s->res_pos.p, s->dres.p, B, s->sum_slot.p, s->sum_d1.p, s->sum_e1.p,
+                                                   s->sum_lbr.p);
+            else
+                k_rowpass<16><<<grid, 256, 0, st>>>(B, c0, s->frow.p, D, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p,
+                                                    s->snap_slot.p, s->fnorm.p, sm, rel, absc, s->C32.p, s->cfg.t,
+                                                    s->res_pos.p, s->dres.p, B, s->sum_slot.p, s->sum_d1.p, s->sum_e1.p,
+                                                    s->sum_lbr.p);
+            FX_LAUNCHED();
+        } else {
         k_row_summary<T><<<(unsigned)cdiv((int64_t)B * 32, 256), 256, 0, st>>>(
-            B, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p, s->snap_slot.p, s->fnorm.p, c0, sm, rel, absc, s->frow.p,
-            s->C32.p, D, s->sum_slot.p, s->sum_d1.p, s->sum_e1.p, s->sum_lbr.p);
-        FX_LAUNCHED();
+                B, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p, s->snap_slot.p, s->fnorm.p, c0, sm, rel, absc, s->frow.p,
+                s->C32.p, D, s->sum_slot.p, s->sum_d1.p, s->sum_e1.p, s->sum_lbr.p);
+            FX_LAUNCHED();
+        }
         s->tstop();
         const auto h1 = hclock::now();
         s->t_ms[8] += hms(h0, h1);
