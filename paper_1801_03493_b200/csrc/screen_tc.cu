@@ -20,11 +20,18 @@
 // matrices, K-adjacent core matrices 128 B apart (LBO), 8-row groups
 // KT*32 B apart (SBO).  A 4-stage cp.async ring feeds the single MMA-issuing
 // thread; tcgen05.commit on a per-stage mbarrier releases a stage.
+#include <algorithm>
+#include <cstdlib>
+
+#include <cooperative_groups.h>
+
 #include "fx_handles.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace fx {
 
-constexpr int TC_M = 128, TC_N = 128, TC_KT = 32, TC_STAGES = 4, TC_THREADS = 128;
+constexpr int TC_M = 128, TC_N = 128, TC_KT = 32, TC_STAGES = 6, TC_THREADS = 128;
 constexpr int TC_TILE_BYTES = TC_M * TC_KT * 4;  // 16 KB per operand per stage
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
@@ -85,7 +92,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
                                                            const float *__restrict__ C32,
                                                            const int32_t *__restrict__ snap,
                                                            const float *__restrict__ cn2, float *__restrict__ out,
-                                                           int64_t ld, int kchunk) {
+                                                           int64_t ld, int kchunk, int dbg) {
     // blockIdx.z selects the K range [z*kchunk, (z+1)*kchunk) (split-K when the
     // tile grid alone cannot fill the machine; partials are atomically added)
     const int nB = (int)*nB_dev;
@@ -123,14 +130,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
     const uint32_t sbase = smem_u32(smem);
 
     const int kbeg = blockIdx.z * kchunk, kend = min(D, kbeg + kchunk);
-    const int nk = (kend - kbeg + TC_KT - 1) / TC_KT;
-    const bool split = gridDim.z > 1;
+    const int nk = kend > kbeg ? (kend - kbeg + TC_KT - 1) / TC_KT : 0;
     // instruction descriptor: D=F32, A=B=TF32, K-major both, N=128, M=128
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TC_N >> 3) << 17) |
                            ((uint32_t)(TC_M >> 4) << 24);
     // prologue: stages 0..S-2
     for (int s = 0; s < TC_STAGES - 1; s++) {
-        if (s < nk) {
+        if (s < nk && !(dbg & 1)) {
             const uint32_t st = sbase + s * 2 * TC_TILE_BYTES;
             load_tile(st, rowsA, kbeg + s * TC_KT, kend, fnorm);
             load_tile(st + TC_TILE_BYTES, rowsB, kbeg + s * TC_KT, kend, fnorm);
@@ -142,7 +148,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
         asm volatile("cp.async.wait_group %0;\n" ::"n"(TC_STAGES - 2));
         asm volatile("fence.proxy.async.shared::cta;\n" ::);
         __syncthreads();
-        if (tid == 0) {
+        if (tid == 0 && !(dbg & 2)) {
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
             const uint32_t st = sbase + s * 2 * TC_TILE_BYTES;
 #pragma unroll
@@ -162,23 +168,30 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
         const int nt = it + TC_STAGES - 1;
         if (nt < nk) {
             const int ns = nt % TC_STAGES;
-            if (nt >= TC_STAGES) mbar_wait(&bar_stage[ns], (uint32_t)(((nt / TC_STAGES) - 1) & 1));
+            if (nt >= TC_STAGES && !(dbg & 2)) mbar_wait(&bar_stage[ns], (uint32_t)(((nt / TC_STAGES) - 1) & 1));
             const uint32_t st = sbase + ns * 2 * TC_TILE_BYTES;
-            load_tile(st, rowsA, kbeg + nt * TC_KT, kend, fnorm);
-            load_tile(st + TC_TILE_BYTES, rowsB, kbeg + nt * TC_KT, kend, fnorm);
+            if (!(dbg & 1)) {
+                load_tile(st, rowsA, kbeg + nt * TC_KT, kend, fnorm);
+                load_tile(st + TC_TILE_BYTES, rowsB, kbeg + nt * TC_KT, kend, fnorm);
+            }
         }
         asm volatile("cp.async.commit_group;\n" ::);
     }
-    if (tid == 0)
+    if (tid == 0 && !(dbg & 2))
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
             smem_u32(&bar_done)));
-    mbar_wait(&bar_done, 0);
+    if (!(dbg & 2)) mbar_wait(&bar_done, 0);
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
 
-    // epilogue: warp w owns TMEM lanes 32w..32w+31 = tile rows
+    // epilogue: warp w owns TMEM lanes 32w..32w+31 = tile rows.  The partial
+    // dot products go to a [128][TC_N+1] tile in this CTA's (now idle)
+    // pipeline shared memory; the split-K CTAs of one output tile form a
+    // thread-block cluster, and CTA rank z reduces rows z*128/split.. of the
+    // tile over every CTA's shared memory (DSMEM, fixed order), adds the norms
+    // and writes the rows coalesced.  No atomics, no pre-zeroed output.
+    constexpr int TS = TC_N + 4;  // 16-byte aligned rows for the v4 DSMEM reads
+    float *tile = (float *)smem;
     const int r = warp * 32 + lane;
-    const int a = ta + r;
-    const float fa2 = a < nA ? fnorm[a0 + a] * fnorm[a0 + a] : 0.f;
     for (int c0 = 0; c0 < TC_N; c0 += 32) {
         uint32_t v[32];
         const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
@@ -191,22 +204,44 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
               "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
-        if (a < nA) {
 #pragma unroll
-            for (int j = 0; j < 32; j++) {
-                const int b = tb + c0 + j;
-                if (b < nB) {
-                    const float dot = __uint_as_float(v[j]);
-                    if (!split) {
-                        out[(int64_t)a * ld + b] = fa2 + cn2[snap[b]] - 2.f * dot;
-                    } else {
-                        atomicAdd(&out[(int64_t)a * ld + b], (blockIdx.z == 0 ? fa2 + cn2[snap[b]] : 0.f) - 2.f * dot);
-                    }
-                }
-            }
-        }
+        for (int j = 0; j < 32; j++) tile[r * TS + c0 + j] = ((dbg & 2) || nk == 0) ? 0.f : __uint_as_float(v[j]);
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+    const int split = gridDim.z;
+    cg::cluster_group cluster = cg::this_cluster();
+    cluster.sync();
+    const int rank = (int)cluster.block_rank();
+    const int rows_per = TC_M / split;
+    const int ncol = min(TC_N, nB - tb);
+    const int nc4 = (ncol + 3) >> 2;
+    const float *part[8];
+#pragma unroll
+    for (int q = 0; q < 8; q++) part[q] = q < split ? cluster.map_shared_rank(tile, q) : tile;
+    for (int e = tid; e < rows_per * nc4; e += TC_THREADS) {
+        const int rr = rank * rows_per + e / nc4, c = (e % nc4) * 4;
+        const int a = ta + rr;
+        if (a >= nA) continue;
+        float4 dot = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+        for (int q = 0; q < 8; q++) {
+            if (q < split) {
+                const float4 x = *(const float4 *)(part[q] + rr * TS + c);
+                dot.x += x.x;
+                dot.y += x.y;
+                dot.z += x.z;
+                dot.w += x.w;
+            }
+        }
+        const float fa = fnorm[a0 + a];
+        const float fa2 = fa * fa;
+        float *o = out + (int64_t)a * ld + tb + c;
+        const float d4[4] = {dot.x, dot.y, dot.z, dot.w};
+#pragma unroll
+        for (int j = 0; j < 4; j++)
+            if (c + j < ncol) o[j] = fa2 + cn2[snap[tb + c + j]] - 2.f * d4[j];
+    }
+    cluster.sync();  // keep this CTA's shared memory alive until every CTA of the cluster has read it
     __syncthreads();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TC_N));
 }
@@ -221,14 +256,28 @@ void launch_screen_tc(int nA, int64_t a0, const char *const *frow, const float *
         FX_CUDA(cudaFuncSetAttribute(k_screen_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)screen_tc_smem()));
         attr = true;
     }
+    static const int dbg = getenv("FOCUS_B200_TCDBG") ? atoi(getenv("FOCUS_B200_TCDBG")) : 0;
+    static const int split_env = getenv("FOCUS_B200_TCSPLIT") ? atoi(getenv("FOCUS_B200_TCSPLIT")) : 0;
     const int64_t tiles = cdiv(nB_max, TC_N) * cdiv(nA, TC_M);
     int split = 1;
     while (tiles * split * 2 <= 148 && D / (split * 2) >= 4 * TC_KT) split *= 2;
+    if (split_env > 0) split = split_env;
+    split = std::min(split, 8);  // split-K CTAs of a tile form one (portable-size) cluster
+    while (TC_M % split) split--;
     const int kchunk = (int)(cdiv(cdiv(D, split), TC_KT) * TC_KT);
-    if (split > 1) FX_CUDA(cudaMemsetAsync(out, 0, sizeof(float) * (size_t)nA * ld, st));
-    dim3 grid((unsigned)cdiv(nB_max, TC_N), (unsigned)cdiv(nA, TC_M), (unsigned)split);
-    k_screen_tc<<<grid, TC_THREADS, screen_tc_smem(), st>>>(nA, a0, frow, fnorm, D, nB_dev, C32, snap, cn2, out, ld,
-                                                            kchunk);
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3((unsigned)cdiv(nB_max, TC_N), (unsigned)cdiv(nA, TC_M), (unsigned)split);
+    lc.blockDim = dim3(TC_THREADS);
+    lc.dynamicSmemBytes = screen_tc_smem();
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 1;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = (unsigned)split;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    FX_CUDA(cudaLaunchKernelEx(&lc, k_screen_tc, nA, a0, frow, fnorm, D, nB_dev, C32, snap, cn2, out, ld, kchunk, dbg));
     FX_LAUNCHED();
 }
 

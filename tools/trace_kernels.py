@@ -1,0 +1,44 @@
+"""Per-kernel device time of one C2 stream ingest + finalize, traced with
+CUPTI through torch.profiler (real pipelined run, not ncu-serialised).
+GPU box only:  python tools/trace_kernels.py [n_objects]"""
+import collections
+import os
+import sys
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+import torch
+from torch.profiler import ProfilerActivity, profile
+
+import paper_1801_03493_b200 as fx
+from paper_1801_03493_b200 import _lib, synth
+
+n = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000
+data = synth.generate(n, dim=2048, vocab=1000, n_stream_classes=100, seed=0)
+torch.cuda.synchronize()
+prof = fx.make_default_profiles(1000)["cheap"]
+
+
+def run():
+    s = fx.ingest.Stream(2048, 16, 1000, 4, 7.5, 100, 0.01, _lib.FX_F32, 0, 0)
+    s.set_rank_model(prof, 0)
+    s.ingest_device(n, data.oids.data_ptr(), data.fids.data_ptr(), data.sigs.data_ptr(), data.feats.data_ptr(),
+                    data.true_class.data_ptr())
+    s.finalize()
+    torch.cuda.synchronize()
+
+
+run()
+with profile(activities=[ProfilerActivity.CUDA]) as p:
+    run()
+agg = collections.defaultdict(lambda: [0, 0.0])
+tmin, tmax = None, None
+for e in p.events():
+    if e.device_type == torch.autograd.DeviceType.CUDA:
+        name = e.name.split("(")[0].replace("void ", "")
+        agg[name][0] += 1
+        agg[name][1] += e.device_time_total if hasattr(e, "device_time_total") else e.cuda_time_total
+tot = sum(v[1] for v in agg.values())
+print(f"total kernel/memcpy time {tot / 1e3:.2f} ms")
+for k, v in sorted(agg.items(), key=lambda x: -x[1][1])[:25]:
+    print(f"{k[:60]:60s} {v[0]:6d} {v[1] / 1e3:9.3f} ms  avg {v[1] / v[0]:8.2f} us")
