@@ -101,6 +101,21 @@ int fx_stream_create(const fx_stream_config *cfg, fx_stream **out);
 int fx_stream_destroy(fx_stream *s);
 int fx_stream_set_rank_model(fx_stream *s, const fx_rank_model *rm);
 
+/* K1b cheap-CNN classifier head (north star kernel 1; no reference function:
+ * it is what a classify_fn plugged into ingest.py:52-61,73 computes):
+ * logits = feature . W^T + bias over `vocab` classes, top-k by descending
+ * logit (ties -> smaller class id).  W: vocab x dim float32 row-major, bias:
+ * vocab float32 or NULL (host pointers, copied).  Once set, fx_ingest needs
+ * neither true_class nor topk; FP32 features, dim % 4 == 0, k <= 16. */
+int fx_stream_set_fc_head(fx_stream *s, int32_t vocab, const float *W, const float *bias);
+
+/* K1b standalone over n dense float32 feature rows (host pointers):
+ * out_topk[n*k] classes, out_conf[n*k] softmax confidences (may be NULL),
+ * out_flag[n] 1 where float64 logits among ranks 1..k+1 are within their
+ * error bound of each other (may be NULL). */
+int fx_fc_topk(int32_t device, int64_t n, int32_t dim, int32_t vocab, int32_t k, const float *feats, const float *W,
+               const float *bias, int32_t *out_topk, float *out_conf, uint8_t *out_flag);
+
 /* pixel_diff over a chunk (ingest.py:37-47), continuing from the previous
  * chunk's last object; does not consume the chunk.  out_is_dup[n]. */
 int fx_stream_dup_flags(fx_stream *s, int64_t n, const int64_t *frame_ids, const double *sigs,

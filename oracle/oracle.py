@@ -387,3 +387,49 @@ class OracleSession:
             cids = lookup(self.by_id, self.postings, self.k, OTHER_CLASS, None)
             return self._collect(cids, OTHER_CLASS, time_range, keep_label=class_id)
         return self.execute_query(class_id, k_x, time_range)
+
+
+# ---------------------------------------------------------------------------
+# K1b FC classifier head (north star kernel 1).  There
+# is no reference function: the head is a classify_fn for the reference's
+# plugin point (ingest.py:52-61,73).  This is its float64 restatement.
+# ---------------------------------------------------------------------------
+
+def fc_logits(feats, W, b=None) -> np.ndarray:
+    """logits = f W^T + b in float64 (fp32 inputs upcast, as numpy would)."""
+    L = np.asarray(feats, np.float64) @ np.asarray(W, np.float64).T
+    if b is not None:
+        L = L + np.asarray(b, np.float64)
+    return L
+
+
+def fc_topk(feats, W, b, k: int, rel_margin: float = 1e-9):
+    """Top-k classes by descending float64 logit, ties -> smaller class id
+    (stable sort of -logit).  Also returns a flag per object where two logits
+    among ranks 1..k+1 are within rel_margin * max(1, |logit|) of each other --
+    the objects whose order depends on float64 rounding (BLAS summation order
+    here, the device's own order there), excluded from bit-exact comparison."""
+    L = fc_logits(feats, W, b)
+    order = np.argsort(-L, axis=1, kind="stable")
+    top = order[:, :k].astype(np.int32)
+    kk = min(k + 1, L.shape[1])
+    vals = np.take_along_axis(L, order[:, :kk], axis=1)
+    gaps = vals[:, :-1] - vals[:, 1:]
+    scale = np.maximum(1.0, np.abs(vals[:, :-1]))
+    flag = (gaps <= rel_margin * scale).any(axis=1) if kk > 1 else np.zeros(L.shape[0], bool)
+    return top, flag
+
+
+def fc_classify_fn(W, b=None):
+    """A classify_fn(profile, obj, seed) for the reference ingest_stream that
+    ranks classes with the FC head on the object's (already extracted, float32)
+    feature: the reference pipeline then runs unchanged on the head's top-K."""
+    def fn(profile, obj, seed):
+        from focusidx.core import RankedClassification  # reference type, imported lazily
+        f = np.asarray(obj.feature, np.float32)
+        L = fc_logits(f[None, :], W, b)[0]
+        order = np.argsort(-L, kind="stable")
+        m = L.max()
+        conf = np.exp(L[order] - m) / np.sum(np.exp(L - m))
+        return RankedClassification(tuple((int(c), float(p)) for c, p in zip(order, conf)), f)
+    return fn

@@ -5,7 +5,7 @@ libfocus_b200.so (hand-written sm_100a CUDA behind a C ABI,
 include/focus_b200.h).  There is no CPU fallback.
 """
 
-from .classifiers import (GENERIC_CHEAP, GROUND_TRUTH, SPECIALIZED, ClassifierProfile, RankModel,
+from .classifiers import (GENERIC_CHEAP, GROUND_TRUTH, SPECIALIZED, ClassifierProfile, FCHead, RankModel,
                           extract_feature, ground_truth_label, make_default_profiles, specialize_profile)
 from .clustering import Cluster
 from .core import (OTHER_CLASS, AccuracyTarget, Config, DetectedObject, RankedClassification, decode_class,

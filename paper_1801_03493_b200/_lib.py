@@ -65,6 +65,9 @@ _SIGS = {
     "fx_stream_create": (ctypes.c_int, [ctypes.POINTER(StreamConfig), ctypes.POINTER(vp)]),
     "fx_stream_destroy": (ctypes.c_int, [vp]),
     "fx_stream_set_rank_model": (ctypes.c_int, [vp, ctypes.POINTER(RankModelC)]),
+    "fx_stream_set_fc_head": (ctypes.c_int, [vp, ctypes.c_int32, vp, vp]),
+    "fx_fc_topk": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, vp, vp,
+                                  vp, c_i32p, vp, c_u8p]),
     "fx_stream_dup_flags": (ctypes.c_int, [vp, ctypes.c_int64, c_i64p, c_f64p, c_u8p]),
     "fx_ingest": (ctypes.c_int, [vp, ctypes.c_int64, c_i64p, c_i64p, c_f64p, vp, c_i32p, c_i32p, ctypes.c_int32]),
     "fx_ingest_device": (ctypes.c_int, [vp, ctypes.c_int64, vp, vp, vp, vp, vp, vp, ctypes.c_int32]),

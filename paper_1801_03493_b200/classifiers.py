@@ -24,7 +24,7 @@ from functools import lru_cache
 import numpy as np
 
 from .core import OTHER_CLASS, DetectedObject, encode_class
-from .errors import DataError, EmptyHistogram, MissingTrueClass
+from .errors import DataError, DimensionMismatch, EmptyHistogram, MissingTrueClass, UsageError
 
 GROUND_TRUTH = "GROUND_TRUTH"
 GENERIC_CHEAP = "GENERIC_CHEAP"
@@ -208,3 +208,41 @@ def device_tables(profile: ClassifierProfile, seed: int, k: int):
     """(thresholds u64[k], emit_map i32[V], fillers i32[(V+1)*k]) for K1a."""
     return _device_tables(profile.kind, profile.vocab, profile.class_set, profile.rank_model.p1,
                           profile.rank_model.rho, seed, k)
+
+
+class FCHead:
+    """K1b: the cheap-CNN classifier head of the north star (no reference
+    function; a classify_fn for ingest.py:52-61,73).  logits = f W^T + b over
+    W.shape[0] classes; the top-k by descending logit (ties -> smaller class id)
+    are the object's ranked classes and the extracted feature is what gets
+    clustered.  Runs only on the device: pass it as `classify_fn` to
+    ingest_stream, or call `topk` on a batch of feature rows."""
+
+    def __init__(self, W, b=None):
+        self.W = np.ascontiguousarray(W, np.float32)
+        self.b = None if b is None else np.ascontiguousarray(b, np.float32)
+        if self.W.ndim != 2 or (self.b is not None and self.b.shape != (self.W.shape[0],)):
+            raise ValueError("W must be (vocab, dim) and b (vocab,)")
+
+    @property
+    def vocab(self) -> int:
+        return int(self.W.shape[0])
+
+    def topk(self, feats, k: int, device: int | None = None):
+        """(topk int32[n, k], confidences float32[n, k], margin flags bool[n]) on the device."""
+        from . import _lib
+        F = np.ascontiguousarray(feats, np.float32)
+        n, D = F.shape
+        if D != self.W.shape[1]:
+            raise DimensionMismatch(f"feature dim {D} != head dim {self.W.shape[1]}")
+        tk = np.empty((n, k), np.int32)
+        conf = np.empty((n, k), np.float32)
+        flag = np.empty(n, np.uint8)
+        L = _lib.load()
+        _lib.check(L.fx_fc_topk(_lib.device() if device is None else device, n, D, self.vocab, k, _lib.pv(F),
+                                _lib.pv(self.W), None if self.b is None else _lib.pv(self.b), _lib.p32(tk),
+                                _lib.pv(conf), _lib.pu8(flag)))
+        return tk, conf, flag.astype(bool)
+
+    def __call__(self, profile, obj, seed):
+        raise UsageError("FCHead runs on the device: pass it as classify_fn to ingest_stream or call .topk()")

@@ -22,6 +22,11 @@ template <typename T>
 void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end);
 void launch_final_live(fx_stream *s);
 size_t resolve_smem(int Bc, const PwPlan &P);
+void launch_fc_head(int64_t n, int64_t c0, const char *const *frow, const int64_t *cls_obj, const float *fnorm, int D,
+                    int V, int K, const float *W, const float *wnorm, const float *bias, int32_t *topk, float *conf,
+                    uint8_t *flag, unsigned long long *nflag, cudaStream_t st);
+void launch_row_norms(int64_t rows, int D, const float *X, float *out, cudaStream_t st);
+void launch_rowptrs(int64_t rows, int64_t row_bytes, const char *base, const char **out, cudaStream_t st);
 void launch_dup_members(fx_stream *s, int64_t n, const int64_t *d_excl_all, int64_t *d_anchor);
 void launch_seal(fx_stream *s, int64_t nfeat_total, const int32_t *fmem_cls, const int32_t *fmem_cid,
                  const int64_t *foff, unsigned long long *best_bits, double *dout, int *best_pos);
@@ -281,6 +286,77 @@ int fx_stream_set_rank_model(fx_stream *s, const fx_rank_model *rm) {
     })
 }
 
+int fx_stream_set_fc_head(fx_stream *s, int32_t vocab, const float *W, const float *bias) {
+    FX_GUARD({
+        if (!s || !W) throw Error{FX_E_USAGE, "null argument"};
+        if (vocab < 1 || vocab > s->cfg.vocab) throw Error{FX_E_USAGE, "fc head vocab outside [1, stream vocab]"};
+        if (s->cfg.feat_type != FX_F32 || s->cfg.dim % 4 != 0)
+            throw Error{FX_E_USAGE, "fc head needs float32 features with dim % 4 == 0"};
+        if (s->cfg.k > 16 || s->cfg.k > vocab) throw Error{FX_E_K_OUT_OF_RANGE, "fc head: k must be <= min(16, vocab)"};
+        set_dev(s->dev);
+        StreamGuard sg_(s->st);
+        const int D = s->cfg.dim;
+        s->fc_W.reserve((size_t)vocab * D);
+        s->fc_wnorm.reserve(vocab);
+        h2d(s->fc_W.p, W, (int64_t)vocab * D, s->st);
+        if (bias) {
+            s->fc_bias.reserve(vocab);
+            h2d(s->fc_bias.p, bias, vocab, s->st);
+        } else {
+            s->fc_bias.release();
+        }
+        launch_row_norms(vocab, D, s->fc_W.p, s->fc_wnorm.p, s->st);
+        FX_CUDA(cudaStreamSynchronize(s->st));
+        s->fc_V = vocab;
+        s->has_fc = true;
+    })
+}
+
+int fx_fc_topk(int32_t device, int64_t n, int32_t dim, int32_t vocab, int32_t k, const float *feats, const float *W,
+               const float *bias, int32_t *out_topk, float *out_conf, uint8_t *out_flag) {
+    FX_GUARD({
+        if (!feats || !W || !out_topk) throw Error{FX_E_USAGE, "null argument"};
+        if (dim < 4 || dim % 4 != 0 || vocab < 1) throw Error{FX_E_USAGE, "bad shapes"};
+        if (k < 1 || k > 16 || k > vocab) throw Error{FX_E_K_OUT_OF_RANGE, "k must be in [1, min(16, vocab)]"};
+        if (n <= 0) return FX_OK;
+        set_dev(device);
+        init_pool(device);
+        cudaStream_t st;
+        FX_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        {
+            StreamGuard sg_(st);
+            DevBuf<float> F, Wd, wn, bd, fn, cf;
+            DevBuf<const char *> rows;
+            DevBuf<int32_t> tk;
+            DevBuf<uint8_t> fl;
+            F.reserve((size_t)n * dim);
+            Wd.reserve((size_t)vocab * dim);
+            wn.reserve(vocab);
+            fn.reserve(n);
+            rows.reserve(n);
+            tk.reserve((size_t)n * k);
+            cf.reserve((size_t)n * k);
+            fl.reserve(n);
+            h2d(F.p, feats, n * dim, st);
+            h2d(Wd.p, W, (int64_t)vocab * dim, st);
+            if (bias) {
+                bd.reserve(vocab);
+                h2d(bd.p, bias, vocab, st);
+            }
+            launch_row_norms(vocab, dim, Wd.p, wn.p, st);
+            launch_row_norms(n, dim, F.p, fn.p, st);
+            launch_rowptrs(n, (int64_t)dim * 4, (const char *)F.p, rows.p, st);
+            launch_fc_head(n, 0, rows.p, nullptr, fn.p, dim, vocab, k, Wd.p, wn.p, bias ? bd.p : nullptr, tk.p, cf.p,
+                           fl.p, nullptr, st);
+            d2h(out_topk, tk.p, n * k, st);
+            d2h(out_conf, cf.p, n * k, st);
+            d2h(out_flag, fl.p, n, st);
+            FX_CUDA(cudaStreamSynchronize(st));
+        }
+        FX_CUDA(cudaStreamDestroy(st));
+    })
+}
+
 int fx_stream_dup_flags(fx_stream *s, int64_t n, const int64_t *frame_ids, const double *sigs, uint8_t *out) {
     FX_GUARD({
         if (!s) throw Error{FX_E_USAGE, "null stream"};
@@ -365,7 +441,13 @@ static void ingest_chunk(fx_stream *s, int64_t n, const int64_t *d_oid, const in
     launch_compact(s, n, n0, c0, s->is_dup.p + n0, excl.p, d_feats, compact);
     launch_fnorm(s, c0, nc);
     // K1: top-K
-    if (d_topk) {
+    if (!d_topk && s->has_fc) {
+        if (!s->rows_aligned16) throw Error{FX_E_USAGE, "fc head needs 16-byte aligned feature rows"};
+        launch_fc_head(nc, c0, s->frow.p, s->cls_obj.p, s->fnorm.p, s->cfg.dim, s->fc_V, K, s->fc_W.p, s->fc_wnorm.p,
+                       s->fc_bias.n ? s->fc_bias.p : nullptr, s->topk.p, nullptr, nullptr,
+                       (unsigned long long *)(s->ctr.p + C_FCFLAG), st);
+        s->tstop();
+    } else if (d_topk) {
         FX_CUDA(cudaMemcpyAsync(s->topk.p + n0 * K, d_topk, sizeof(int32_t) * n * K, cudaMemcpyDeviceToDevice, st));
         s->tstop();
     } else {
@@ -403,7 +485,7 @@ static int ingest_common(fx_stream *s, int64_t n, const int64_t *object_ids, con
         if (s->finalized) throw Error{FX_E_USAGE, "stream already finalized"};
         if (n < 0) throw Error{FX_E_USAGE, "negative n"};
         if (n == 0) return FX_OK;
-        if (!true_class && !topk) throw Error{FX_E_USAGE, "need true_class or topk"};
+        if (!true_class && !topk && !s->has_fc) throw Error{FX_E_USAGE, "need true_class, topk or an fc head"};
         set_dev(s->dev);
         StreamGuard sg_(s->st);
         cudaStream_t st = s->st;

@@ -1,0 +1,387 @@
+// fc_head.cu -- K1b: the cheap-CNN classifier head of the north star
+// (no reference function -- it plugs in through the
+// reference's classify_fn hook, ingest.py:52-61,73):
+//     logits = f W^T + b,  top-K classes by descending logit (ties -> smaller
+//     class id), softmax confidences of the K emitted classes.
+//
+// Two kernels per batch of objects:
+//   k_fc_tc    tcgen05.mma kind::tf32, 128 objects x 256 classes per CTA,
+//              accumulator in TMEM; the epilogue keeps, per object and class
+//              tile, the FC_KC largest TF32 logits, the largest upper bound
+//              of every class it dropped (tail), and a logsumexp partial.
+//   k_fc_merge one warp per object: candidates whose upper bound reaches the
+//              K-th largest lower bound are re-scored in float64 (products
+//              of fp32 values are exact in float64; sums round at 2^-53), the
+//              top K taken in float64 order.  If a dropped class could still
+//              reach the top K (tail >= K-th lower bound) every class is
+//              re-scored.  Objects whose float64 logits among ranks 1..K+1
+//              are closer than the float64 error bound are flagged (the
+//              margin the north star allows; the order of an exact tie is
+//              decided by class id as in a stable sort).
+// TF32 error bound per logit: |l~ - l| <= gamma ||f|| ||w_v|| + 2^-22 |l~|,
+// gamma = 2^-9 + D 2^-22 (as for the distance screen, screen_tc.cu).
+#include <algorithm>
+#include <cfloat>
+#include <climits>
+
+#include "fx_handles.cuh"
+#include "tc_common.cuh"
+
+namespace fx {
+
+constexpr int FC_M = 128, FC_N = 256, FC_STAGES = 4, FC_THREADS = 128, FC_KC = 16;
+constexpr int FC_A_BYTES = FC_M * TC_KT * 4, FC_B_BYTES = FC_N * TC_KT * 4;
+
+struct FcTile {  // per (object, class tile) result of k_fc_tc
+    float val[FC_KC];
+    int idx[FC_KC];
+    float tail;        // max over dropped classes of (logit~ + err)
+    float lse_m, lse_s;  // logsumexp partial: max logit~, sum exp(l~ - max)
+};
+
+__global__ void __launch_bounds__(FC_THREADS, 1) k_fc_tc(int n, int64_t a0, const char *const *__restrict__ frow,
+                                                        const float *__restrict__ fnorm, int D, int V,
+                                                        const float *__restrict__ W, const float *__restrict__ wnorm,
+                                                        const float *__restrict__ bias, float gamma,
+                                                        FcTile *__restrict__ out) {
+    const int tv = blockIdx.x * FC_N, ta = blockIdx.y * FC_M;
+    extern __shared__ __align__(1024) unsigned char smem[];
+    __shared__ const float *rowsA[FC_M];
+    __shared__ const float *rowsB[FC_N];
+    __shared__ __align__(8) uint64_t bar_stage[FC_STAGES];
+    __shared__ __align__(8) uint64_t bar_done;
+    __shared__ uint32_t tmem_base;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    for (int r = tid; r < FC_M; r += FC_THREADS) rowsA[r] = ta + r < n ? (const float *)frow[a0 + ta + r] : nullptr;
+    for (int r = tid; r < FC_N; r += FC_THREADS) rowsB[r] = tv + r < V ? W + (int64_t)(tv + r) * D : nullptr;
+    if (tid == 0) {
+        for (int s = 0; s < FC_STAGES; s++) mbar_init(&bar_stage[s], 1);
+        mbar_init(&bar_done, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base)),
+                     "r"(FC_N));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+    const uint32_t tmem = tmem_base;
+    const uint32_t sbase = smem_u32(smem);
+    const int nk = (D + TC_KT - 1) / TC_KT;
+    constexpr uint32_t idesc = idesc_tf32(FC_M, FC_N);
+    constexpr int SB = FC_A_BYTES + FC_B_BYTES;
+    for (int s = 0; s < FC_STAGES - 1; s++) {
+        if (s < nk) {
+            load_tile<FC_M, FC_THREADS>(sbase + s * SB, rowsA, s * TC_KT, D, fnorm);
+            load_tile<FC_N, FC_THREADS>(sbase + s * SB + FC_A_BYTES, rowsB, s * TC_KT, D, fnorm);
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+    }
+    for (int it = 0; it < nk; it++) {
+        const int s = it % FC_STAGES;
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(FC_STAGES - 2));
+        asm volatile("fence.proxy.async.shared::cta;\n" ::);
+        __syncthreads();
+        if (tid == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+            const uint32_t st = sbase + s * SB;
+#pragma unroll
+            for (int kk = 0; kk < TC_KT / 8; kk++) {
+                const uint64_t da = umma_desc(st + kk * 256, 128, TC_KT * 32);
+                const uint64_t db = umma_desc(st + FC_A_BYTES + kk * 256, 128, TC_KT * 32);
+                const uint32_t acc = (it > 0 || kk > 0) ? 1u : 0u;
+                asm volatile(
+                    "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                    "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+                    "l"(da), "l"(db), "r"(idesc), "r"(acc));
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                smem_u32(&bar_stage[s])));
+        }
+        const int nt = it + FC_STAGES - 1;
+        if (nt < nk) {
+            const int ns = nt % FC_STAGES;
+            if (nt >= FC_STAGES) mbar_wait(&bar_stage[ns], (uint32_t)(((nt / FC_STAGES) - 1) & 1));
+            load_tile<FC_M, FC_THREADS>(sbase + ns * SB, rowsA, nt * TC_KT, D, fnorm);
+            load_tile<FC_N, FC_THREADS>(sbase + ns * SB + FC_A_BYTES, rowsB, nt * TC_KT, D, fnorm);
+        }
+        asm volatile("cp.async.commit_group;\n" ::);
+    }
+    if (tid == 0)
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+            smem_u32(&bar_done)));
+    mbar_wait(&bar_done, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+
+    // epilogue: thread = object row; keep the FC_KC largest logits (sorted
+    // descending, ties -> smaller class id) in registers
+    const int a = ta + warp * 32 + lane;
+    const float fn = a < n ? fnorm[a0 + a] : 0.f;
+    float kv[FC_KC];
+    int ki[FC_KC];
+#pragma unroll
+    for (int j = 0; j < FC_KC; j++) {
+        kv[j] = -FLT_MAX;
+        ki[j] = -1;
+    }
+    float tail = -FLT_MAX, m = -FLT_MAX, ssum = 0.f;
+    for (int c0 = 0; c0 < FC_N; c0 += 32) {
+        uint32_t v[32];
+        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
+            "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+              "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
+#pragma unroll 4
+        for (int j = 0; j < 32; j++) {
+            const int cls = tv + c0 + j;
+            if (a >= n || cls >= V) break;
+            const float l = __uint_as_float(v[j]) + (bias ? bias[cls] : 0.f);
+            // logsumexp partial (confidences only)
+            if (l > m) {
+                ssum = ssum * __expf(m - l) + 1.f;
+                m = l;
+            } else {
+                ssum += __expf(l - m);
+            }
+            float x = l;
+            int xi = cls;
+            if (x > kv[FC_KC - 1]) {
+                // the dropped element's upper bound feeds the tail
+                const int di = ki[FC_KC - 1];
+                if (di >= 0) tail = fmaxf(tail, kv[FC_KC - 1] + gamma * fn * wnorm[di] + fabsf(kv[FC_KC - 1]) * 2.4e-7f);
+#pragma unroll
+                for (int q = 0; q < FC_KC; q++) {  // insertion, strict > keeps the earlier (smaller) id first
+                    if (x > kv[q]) {
+                        const float tvv = kv[q];
+                        const int tii = ki[q];
+                        kv[q] = x;
+                        ki[q] = xi;
+                        x = tvv;
+                        xi = tii;
+                    }
+                }
+            } else {
+                tail = fmaxf(tail, x + gamma * fn * wnorm[cls] + fabsf(x) * 2.4e-7f);
+            }
+        }
+    }
+    if (a < n) {
+        FcTile *o = out + (int64_t)a * gridDim.x + blockIdx.x;
+#pragma unroll
+        for (int j = 0; j < FC_KC; j++) {
+            o->val[j] = kv[j];
+            o->idx[j] = ki[j];
+        }
+        o->tail = tail;
+        o->lse_m = m;
+        o->lse_s = ssum;
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(FC_N));
+}
+
+// float64 logit of class v for feature row f (warp-cooperative; result in all lanes)
+__device__ __forceinline__ double fc_logit64(const float *f, const float *w, int D, double b) {
+    double acc = 0.0;
+    for (int k = threadIdx.x & 31; k < D; k += 32) acc = fma((double)f[k], (double)w[k], acc);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    return acc + b;
+}
+
+constexpr int FC_MAXC = 64;  // candidates re-scored per object before the all-class fallback
+
+__global__ void __launch_bounds__(256) k_fc_merge(int n, int64_t a0, const char *const *__restrict__ frow,
+                                                 const int64_t *__restrict__ cls_obj, const float *__restrict__ fnorm,
+                                                 int D, int V, int K, const float *__restrict__ W,
+                                                 const float *__restrict__ wnorm, const float *__restrict__ bias,
+                                                 float gamma, int ntile, const FcTile *__restrict__ tiles,
+                                                 int32_t *__restrict__ topk, float *__restrict__ conf,
+                                                 uint8_t *__restrict__ flag, unsigned long long *__restrict__ nflag) {
+    __shared__ int s_idx[8][FC_MAXC];
+    const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int w = blockIdx.x * 8 + wib;
+    if (w >= n) return;
+    const float fn = fnorm[a0 + w];
+    const float *f = (const float *)frow[a0 + w];
+    const FcTile *t = tiles + (int64_t)w * ntile;
+    // K-th largest lower bound among the tiles' kept candidates (K rounds of
+    // warp argmax; the slots chosen so far are parked in s_idx)
+    const int nc = ntile * FC_KC;
+    float lbk = -FLT_MAX;
+    for (int r = 0; r < K; r++) {
+        float best = -FLT_MAX;
+        int bslot = -1;
+        for (int e = lane; e < nc; e += 32) {
+            const int ti = e / FC_KC, j = e % FC_KC;
+            const int cls = t[ti].idx[j];
+            if (cls < 0) continue;
+            bool done = false;
+            for (int q = 0; q < r; q++) done |= (s_idx[wib][q] == e);
+            const float lv = t[ti].val[j];
+            const float lb = lv - gamma * fn * wnorm[cls] - fabsf(lv) * 2.4e-7f;
+            if (!done && lb > best) {
+                best = lb;
+                bslot = e;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+            const int os = __shfl_xor_sync(0xffffffffu, bslot, o);
+            if (ob > best || (ob == best && os >= 0 && (bslot < 0 || os < bslot))) {
+                best = ob;
+                bslot = os;
+            }
+        }
+        __syncwarp();
+        if (lane == 0) s_idx[wib][r] = bslot;
+        __syncwarp();
+        lbk = best;
+    }
+    // candidates: kept classes whose upper bound reaches lbk
+    float maxtail = -FLT_MAX;
+    for (int ti = 0; ti < ntile; ti++) maxtail = fmaxf(maxtail, t[ti].tail);
+    bool all = maxtail >= lbk;
+    int ncand = 0;
+    if (!all) {
+        for (int e0 = 0; e0 < nc; e0 += 32) {
+            const int e = e0 + lane;
+            bool take = false;
+            int cls = -1;
+            if (e < nc) {
+                const int ti = e / FC_KC, j = e % FC_KC;
+                cls = t[ti].idx[j];
+                if (cls >= 0) {
+                    const float lv = t[ti].val[j];
+                    take = lv + gamma * fn * wnorm[cls] + fabsf(lv) * 2.4e-7f >= lbk;
+                }
+            }
+            const unsigned m = __ballot_sync(0xffffffffu, take);
+            if (take) {
+                const int pos = ncand + __popc(m & ((1u << lane) - 1u));
+                if (pos < FC_MAXC) s_idx[wib][pos] = cls;
+            }
+            ncand += __popc(m);
+        }
+        if (ncand > FC_MAXC) all = true;
+    }
+    __syncwarp();
+    // float64 re-score, selection of the top K (+1 for the margin check)
+    double bv[17];
+    int bi[17];
+#pragma unroll
+    for (int j = 0; j < 17; j++) {
+        bv[j] = -DBL_MAX;
+        bi[j] = INT_MAX;
+    }
+    const int K1 = K + 1 < 17 ? K + 1 : 17;
+    auto offer = [&](double x, int xi) {
+#pragma unroll
+        for (int q = 0; q < 17; q++) {
+            if (q < K1 && (x > bv[q] || (x == bv[q] && xi < bi[q]))) {
+                const double tv = bv[q];
+                const int ti = bi[q];
+                bv[q] = x;
+                bi[q] = xi;
+                x = tv;
+                xi = ti;
+            }
+        }
+    };
+    const int nscore = all ? V : ncand;
+    for (int c = 0; c < nscore; c++) {
+        const int cls = all ? c : s_idx[wib][c];
+        const double l = fc_logit64(f, W + (int64_t)cls * D, D, bias ? (double)bias[cls] : 0.0);
+        offer(l, cls);  // lane 0's value decides (its reduction order is fixed)
+    }
+    // margin flag: the float64 error of a logit is <= (D + 8) 2^-53 ||f|| ||w|| + the bias add
+    bool flagged = false;
+    const double ue = ((double)D + 8.0) * 1.1102230246251565e-16 * (double)fn * 1.0001;
+    for (int q = 0; q + 1 < K1 && q + 1 < nscore; q++) {
+        const double e1 = ue * (double)wnorm[bi[q]] + fabs(bv[q]) * 2.3e-16;
+        const double e2 = ue * (double)wnorm[bi[q + 1]] + fabs(bv[q + 1]) * 2.3e-16;
+        if (bv[q] - bv[q + 1] <= 2.0 * (e1 + e2)) flagged = true;
+    }
+    if (lane == 0) {
+        // logsumexp over all classes from the tiles' partials (TF32 logits; confidences only)
+        float M = -FLT_MAX;
+        for (int ti = 0; ti < ntile; ti++) M = fmaxf(M, t[ti].lse_m);
+        float S = 0.f;
+        for (int ti = 0; ti < ntile; ti++) S += t[ti].lse_s * __expf(t[ti].lse_m - M);
+        const float lse = M + __logf(S);
+        const int64_t obj = cls_obj ? cls_obj[a0 + w] : a0 + w;
+        for (int j = 0; j < K; j++) {
+            topk[obj * K + j] = bi[j];
+            if (conf) conf[obj * K + j] = __expf((float)bv[j] - lse);
+        }
+        if (flag) flag[obj] = flagged ? 1 : 0;
+        if (flagged && nflag) atomicAdd(nflag, 1ull);
+    }
+}
+
+__global__ void k_row_norms(int64_t rows, int D, const float *__restrict__ X, float *__restrict__ out) {
+    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (w >= rows) return;
+    float acc = 0.f;
+    for (int k = lane; k < D; k += 32) acc = fmaf(X[w * D + k], X[w * D + k], acc);
+    acc = warp_sum(acc);
+    if (lane == 0) out[w] = sqrtf(acc) * 1.00001f;  // rounded up: an upper bound of ||w||
+}
+
+// K1b over classified objects [c0, c0 + n) of a stream (topk written by object index)
+void launch_fc_head(int64_t n, int64_t c0, const char *const *frow, const int64_t *cls_obj, const float *fnorm, int D,
+                    int V, int K, const float *W, const float *wnorm, const float *bias, int32_t *topk, float *conf,
+                    uint8_t *flag, unsigned long long *nflag, cudaStream_t st) {
+    if (n <= 0) return;
+    if (K > 16 || K > V) throw Error{FX_E_K_OUT_OF_RANGE, "fc head: k must be <= min(16, vocab)"};
+    static bool attr = false;
+    const size_t smem = (size_t)FC_STAGES * (FC_A_BYTES + FC_B_BYTES);
+    if (!attr) {
+        FX_CUDA(cudaFuncSetAttribute(k_fc_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    const int ntile = (int)cdiv(V, FC_N);
+    const float gamma = (float)((1.953125e-03 + (double)D * 2.384185791015625e-07) * 1.01);
+    DevBuf<FcTile> tiles;
+    const int64_t CH = 1 << 16;  // objects per pass (bounds the tile scratch)
+    tiles.reserve((size_t)std::min<int64_t>(n, CH) * ntile);
+    for (int64_t b = 0; b < n; b += CH) {
+        const int64_t m = std::min<int64_t>(CH, n - b);
+        dim3 grid((unsigned)ntile, (unsigned)cdiv(m, FC_M));
+        k_fc_tc<<<grid, FC_THREADS, smem, st>>>((int)m, c0 + b, frow, fnorm, D, V, W, wnorm, bias, gamma, tiles.p);
+        FX_LAUNCHED();
+        k_fc_merge<<<(unsigned)cdiv(m, 8), 256, 0, st>>>((int)m, c0 + b, frow, cls_obj, fnorm, D, V, K, W, wnorm, bias,
+                                                        gamma, ntile, tiles.p, topk, conf, flag, nflag);
+        FX_LAUNCHED();
+    }
+}
+
+__global__ void k_dense_rowptrs(int64_t rows, int64_t row_bytes, const char *base, const char **out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < rows) out[i] = base + i * row_bytes;
+}
+
+void launch_rowptrs(int64_t rows, int64_t row_bytes, const char *base, const char **out, cudaStream_t st) {
+    if (rows <= 0) return;
+    k_dense_rowptrs<<<(unsigned)cdiv(rows, 256), 256, 0, st>>>(rows, row_bytes, base, out);
+    FX_LAUNCHED();
+}
+
+void launch_row_norms(int64_t rows, int D, const float *X, float *out, cudaStream_t st) {
+    if (rows <= 0) return;
+    k_row_norms<<<(unsigned)cdiv(rows * 32, 256), 256, 0, st>>>(rows, D, X, out);
+    FX_LAUNCHED();
+}
+
+}  // namespace fx

@@ -23,6 +23,7 @@ enum Ctr {
     C_NDIRTY,          // slots touched/evicted in the current batch
     C_ERR,             // internal error flag
     C_FAST,            // objects decided by the certain (screen-bounded) path
+    C_FCFLAG,          // K1b: objects whose top-K sits within the float64 logit margin
     C_COUNT
 };
 
@@ -48,6 +49,10 @@ struct fx_stream {
     uint64_t seed = 0;
     fx::DevBuf<uint64_t> rm_thr;
     fx::DevBuf<int32_t> rm_emit, rm_fill;
+    // K1b classifier head
+    bool has_fc = false;
+    int fc_V = 0;
+    fx::DevBuf<float> fc_W, fc_wnorm, fc_bias;
 
     // per-object arrays (grow)
     int64_t n_seen = 0, n_cls = 0;

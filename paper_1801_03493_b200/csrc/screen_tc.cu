@@ -26,64 +26,14 @@
 #include <cooperative_groups.h>
 
 #include "fx_handles.cuh"
+#include "tc_common.cuh"
 
 namespace cg = cooperative_groups;
 
 namespace fx {
 
-constexpr int TC_M = 128, TC_N = 128, TC_KT = 32, TC_STAGES = 6, TC_THREADS = 128;
+constexpr int TC_M = 128, TC_N = 128, TC_STAGES = 6, TC_THREADS = 128;
 constexpr int TC_TILE_BYTES = TC_M * TC_KT * 4;  // 16 KB per operand per stage
-
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-    return (uint32_t)__cvta_generic_to_shared(p);
-}
-
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, int src_bytes) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(src_bytes));
-}
-
-__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
-    uint64_t d = 0;
-    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
-    d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
-    d |= (uint64_t)1 << 46;  // version = 1 (Blackwell)
-    // base_offset 0, lbo_mode 0, layout SWIZZLE_NONE (0) in bits 61..63
-    return d;
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT_%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT_%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity));
-}
-
-// A tile: 128 rows x KT floats at k0; row r of the tile -> global row pointer
-// rows[r] (nullptr -> zeros).  Layout: ((r/8)*(KT/4) + c)*128 + (r%8)*16.
-__device__ __forceinline__ void load_tile(uint32_t sbase, const float *const *rows, int k0, int D,
-                                          const void *dummy) {
-    // 128 rows x (KT/4 = 8) chunks = 1024 16-byte copies / 128 threads
-#pragma unroll
-    for (int e = 0; e < (TC_M * TC_KT / 4) / TC_THREADS; e++) {
-        const int idx = threadIdx.x + e * TC_THREADS;
-        const int r = idx >> 3, c = idx & 7;
-        const float *row = rows[r];
-        const int k = k0 + c * 4;
-        const bool ok = row != nullptr && k < D;
-        const void *src = ok ? (const void *)(row + k) : dummy;  // never read when src-size is 0
-        const uint32_t dst = sbase + (uint32_t)((((r >> 3) * (TC_KT / 4) + c) << 7) + ((r & 7) << 4));
-        cp_async16(dst, src, ok ? 16 : 0);
-    }
-}
 
 // out[a][q] = ||A_a||^2 + ||B_q||^2 - 2 A_a.B_q   (float, not clamped)
 __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0, const char *const *__restrict__ frow,
@@ -138,8 +88,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
     for (int s = 0; s < TC_STAGES - 1; s++) {
         if (s < nk && !(dbg & 1)) {
             const uint32_t st = sbase + s * 2 * TC_TILE_BYTES;
-            load_tile(st, rowsA, kbeg + s * TC_KT, kend, fnorm);
-            load_tile(st + TC_TILE_BYTES, rowsB, kbeg + s * TC_KT, kend, fnorm);
+            load_tile<TC_M, TC_THREADS>(st, rowsA, kbeg + s * TC_KT, kend, fnorm);
+            load_tile<TC_N, TC_THREADS>(st + TC_TILE_BYTES, rowsB, kbeg + s * TC_KT, kend, fnorm);
         }
         asm volatile("cp.async.commit_group;\n" ::);
     }
@@ -171,8 +121,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
             if (nt >= TC_STAGES && !(dbg & 2)) mbar_wait(&bar_stage[ns], (uint32_t)(((nt / TC_STAGES) - 1) & 1));
             const uint32_t st = sbase + ns * 2 * TC_TILE_BYTES;
             if (!(dbg & 1)) {
-                load_tile(st, rowsA, kbeg + nt * TC_KT, kend, fnorm);
-                load_tile(st + TC_TILE_BYTES, rowsB, kbeg + nt * TC_KT, kend, fnorm);
+                load_tile<TC_M, TC_THREADS>(st, rowsA, kbeg + nt * TC_KT, kend, fnorm);
+                load_tile<TC_N, TC_THREADS>(st + TC_TILE_BYTES, rowsB, kbeg + nt * TC_KT, kend, fnorm);
             }
         }
         asm volatile("cp.async.commit_group;\n" ::);

@@ -77,6 +77,13 @@ class Stream:
                              fillers=_lib.p32(fill))
         _lib.check(self.L.fx_stream_set_rank_model(self.handle, ctypes.byref(rm)))
 
+    def set_fc_head(self, head):
+        """Use the K1b FC classifier head (classifiers.FCHead) for top-K."""
+        W = np.ascontiguousarray(head.W, np.float32)
+        b = None if head.b is None else np.ascontiguousarray(head.b, np.float32)
+        self._keep += [W, b]
+        _lib.check(self.L.fx_stream_set_fc_head(self.handle, W.shape[0], _lib.pv(W), None if b is None else _lib.pv(b)))
+
     def dup_flags(self, fids: np.ndarray, sigs: np.ndarray) -> np.ndarray:
         n = fids.size
         out = np.zeros(n, np.uint8)
@@ -109,7 +116,7 @@ class Stream:
         return cl, dup.astype(bool), tk.reshape(n, k)
 
     COUNTERS = ("nlive", "next_cid", "dc", "nfree", "nevict_total", "exact", "nsnap", "nres", "ninserted",
-                "nevict_batch", "ndefer", "nod", "last_cid", "ndirty", "err", "fast",
+                "nevict_batch", "ndefer", "nod", "last_cid", "ndirty", "err", "fast", "fc_flagged",
                 "cyc_passA", "cyc_passB", "cyc_passCD", "cyc_confirm", "cyc_passE", "cyc_seq", "windows", "seq_steps",
                 "conf_b0", "conf_b1_7", "conf_b8_15", "conf_b16_31", "conf_b32_63", "conf_b64_127", "conf_b128",
                 "conf_young")
@@ -152,7 +159,7 @@ def _f32_exact(x: np.ndarray) -> bool:
 
 def ingest_arrays(oids, fids, sigs, feats, cfg: Config, profile, *, vocab: int, seed: int = 0,
                   pixel_eps: float = DEFAULT_PIXEL_EPS, true_class=None, topk=None, compact: bool = False,
-                  stream_id: str = "synthetic", device: int | None = None, batch: int = 0):
+                  stream_id: str = "synthetic", device: int | None = None, batch: int = 0, fc_head=None):
     """Array-level ingest: the C-ABI call with host buffers.  `feats` rows are
     the extracted features (float32 or float64); `true_class` (int32, -2 =
     unlabeled) drives the device rank model, or `topk` (n x k encoded, OTHER =
@@ -167,7 +174,9 @@ def ingest_arrays(oids, fids, sigs, feats, cfg: Config, profile, *, vocab: int, 
     feat_type = _lib.FX_F64 if feats.dtype == np.float64 else _lib.FX_F32
     feats = np.ascontiguousarray(feats)
     st = Stream(D, S, vocab, cfg.k, cfg.t, cfg.m, pixel_eps, feat_type, device, batch)
-    if topk is None:
+    if fc_head is not None:
+        st.set_fc_head(fc_head)
+    elif topk is None:
         st.set_rank_model(profile, seed)
     if n:
         st.ingest(oids, fids, sigs, feats,
@@ -210,7 +219,12 @@ def ingest_stream(header, stream, cfg: Config, profiles, pixel_eps: float = DEFA
     st = Stream(1, S, 1, 1, 0.0, 1, pixel_eps, _lib.FX_F32, None, 64)  # K0 only
     dup = st.dup_flags(fids, sigs) if n else np.zeros(0, bool)
     keep = np.flatnonzero(~dup)
-    if classify_fn is not None:
+    fc_head = classify_fn if isinstance(classify_fn, classifiers.FCHead) else None
+    if fc_head is not None:
+        # K1b on the device: the head sees the extracted features and emits top-K
+        topk, tcls = None, None
+        rows = [classifiers.extract_feature(profile, objs[i], seed) for i in keep.tolist()]
+    elif classify_fn is not None:
         topk = np.zeros((n, K), np.int32)
         rows = []
         for i in keep.tolist():
@@ -230,7 +244,10 @@ def ingest_stream(header, stream, cfg: Config, profiles, pixel_eps: float = DEFA
     if all(np.asarray(r).dtype == np.float32 for r in rows) or _f32_exact(F):
         F = F.astype(np.float32)
     del st
+    if fc_head is not None:
+        F = F.astype(np.float32)
     idx, report, _ = ingest_arrays(oids, fids, sigs, F, cfg, profile, vocab=V, seed=seed, pixel_eps=pixel_eps,
-                                   true_class=tcls, topk=topk, compact=True, stream_id=header.stream_id)
+                                   true_class=tcls, topk=topk, compact=True, stream_id=header.stream_id,
+                                   fc_head=fc_head)
     idx.header = IndexHeader(stream_id=header.stream_id, dim=D, vocab=V, n_objects=n, config=cfg)
     return idx, report
