@@ -148,12 +148,15 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--n", type=int, default=WORKLOAD["n"])
+    ap.add_argument("--objects", dest="n", type=int, default=WORKLOAD["n"], help="objects per stream")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--cpu-sample", type=int, default=20000)
     ap.add_argument("--ref-sample", type=int, default=20000)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--batch", type=int, default=0)
+    ap.add_argument("--queries", type=int, default=-1, help="classes queried (x3 k_x values); -1 = every class, 0 = skip")
+    ap.add_argument("--backend", default="nccl", help="process-group backend for N > 1 (nccl; gloo for checks)")
+    ap.add_argument("--no-fc", action="store_true", help="skip the K1b FC head sub-benchmark")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -165,10 +168,15 @@ def main():
     from paper_1801_03493_b200 import _lib, synth
 
     ws, rank, local = _dist()
+    if os.environ.get("FOCUS_B200_ONE_GPU"):  # multi-rank logic check on a 1-GPU box (with --backend gloo)
+        local = 0
     torch.cuda.set_device(local)
     fx.set_device(local)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(args.backend)
     W = dict(WORKLOAD, n=args.n)
     data = synth.generate(W["n"], dim=W["dim"], vocab=W["vocab"], n_stream_classes=W["n_stream_classes"], seed=rank)
     torch.cuda.synchronize()
@@ -213,24 +221,24 @@ def main():
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     reports = []
-    last = None
+    last = last_idx = None
     with Clocks(local) as clk:
         ev0.record()
         for i in range(args.steps):
             s = make_stream()
             idx, rep_i = step(s)
             reports.append(rep_i)
-            del idx
             if i == args.steps - 1:
-                last = s
-            del s
+                last, last_idx = s, idx
+            del s, idx
         ev1.record()
         torch.cuda.synchronize()
     launches = L.fx_kernel_launches() - launches0
     host_split = {k: v / args.steps for k, v in host_split.items()}
     t_ms = ev0.elapsed_time(ev1)
+    dev_red = "cuda" if args.backend == "nccl" else "cpu"
     if ws > 1:
-        tt = torch.tensor([t_ms], device="cuda")
+        tt = torch.tensor([t_ms], device=dev_red)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         dist.barrier()
         t_ms = float(tt.item())
@@ -240,25 +248,40 @@ def main():
     phases = last.timings()
     counters = last.counters()
 
-    # roofline of the dominant kernel (algorithmic bytes)
+    # roofline: algorithmic bytes per launch / average launch
+    # duration from the library's CUDA events on its own stream.  The headline
+    # kernel is the K2 TF32 screen (the clustering kernel the north star names;
+    # it streams every classified feature once from HBM); the other kernels
+    # are listed with theirs.  The dominant phase by time is the resolve, a
+    # single-CTA latency-bound pass with no meaningful byte roofline.
     D, n_cls = W["dim"], rep.objects_classified
     nb = max(1.0, phases["batches"])
-    algo = {
-        "screen": 4.0 * D * n_cls,                   # features streamed once
-        "resolve": 4.0 * counters["dc"],             # screen distances consumed
-        "fold": 4.0 * D * n_cls,                     # features re-read into the float64 sums
-        "seal": 4.0 * D * n_cls,                     # every featured member vs its centroid
-        "k0_k1a": 128.0 * rep.objects_seen + (12.0 + 4 * W["k"]) * n_cls,
-        "index": 12.0 * W["k"] * n_cls,
-    }
-    dom = max(algo, key=lambda k: phases.get(k, 0.0))
     peak, peak_kind = _peaks()
-    dom_ms = phases[dom]
-    achieved = algo[dom] / (dom_ms / 1e3) / 1e9 if dom_ms > 0 else 0.0
-    roofline = {"kernel": dom, "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
-                "launches_per_step": int(nb) if dom in ("screen", "resolve", "fold") else 1,
-                "phase_ms_per_step": {k: v for k, v in phases.items() if k != "batches"},
+    feat_bytes = 4.0 * D * n_cls
+    kern = {  # phase -> (algorithmic bytes per step, what)
+        "screen": (feat_bytes + 4.0 * counters["dc"], "k_screen_tc: features streamed once + distance row written"),
+        "screen_summary": (feat_bytes, "k_rowpass: each feature row re-read once (refine + residual columns)"),
+        "fold": (feat_bytes + 8.0 * D * phases["batches"] * 100, "k_fold: member rows into the float64 sums"),
+        "seal": (feat_bytes, "k_seal_dist: every featured member vs its final centroid"),
+        "k0_k1a": (128.0 * rep.objects_seen + (12.0 + 4 * W["k"]) * n_cls, "K0 pixel diff + K1a rank top-K"),
+        "index": (12.0 * W["k"] * n_cls, "K3 class sets + postings"),
+    }
+    rl = {}
+    for k, (byts, what) in kern.items():
+        ms = phases.get(k, 0.0)
+        if ms > 0:
+            ach = byts / (ms / 1e3) / 1e9
+            rl[k] = {"what": what, "ms_per_step": ms, "achieved_gbs": ach, "frac": ach / peak}
+    scr_ms = phases["screen"]
+    scr_ach = kern["screen"][0] / (scr_ms / 1e3) / 1e9
+    roofline = {"kernel": "k_screen_tc (K2 TF32 distance screen)", "bound": "hbm", "achieved": scr_ach, "peak": peak,
+                "unit": "GB/s", "frac": scr_ach / peak, "traffic": None, "peak_kind": peak_kind,
+                "launches_per_step": int(nb), "bytes_per_launch": kern["screen"][0] / nb,
+                "avg_launch_us": scr_ms * 1e3 / nb,
+                "per_kernel": rl,
+                "phase_ms_per_step": {k: v for k, v in phases.items() if k != "batches" and not k.startswith("host")},
+                "dominant_phase": max(("screen", "screen_resid", "screen_summary", "resolve", "fold", "seal"),
+                                      key=lambda k: phases.get(k, 0.0)),
                 "host_wall_ms_per_step": host_split}
 
     # end-to-end through the host-buffer C ABI
@@ -286,9 +309,99 @@ def main():
             if i > 0:
                 e_times.append(t1 - t0)
             del s, dix
-        e2e_v = W["n"] * ws / float(np.mean(e_times))
+        et = float(np.mean(e_times))
+        if ws > 1:
+            tt = torch.tensor([et], device=dev_red)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            et = float(tt.item())
+        e2e_v = W["n"] * ws / et
         e2e = {"value": e2e_v, "unit": "objects/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "timing": "host wall clock around fx_ingest(host ptrs)+fx_finalize+index export, pinned inputs"}
+               "timing": "host wall clock around fx_ingest(host ptrs; H2D chunked and overlapped with the ingest)"
+                         " + fx_finalize + index export, pinned inputs, max over ranks"}
+
+    # C5-style query latency on the ingested index: lookup(k_x) -> GT verify ->
+    # member expansion, fresh session per query; over N ranks every query is
+    # answered for all N streams and merged with the NCCL all-gathers
+    # (paper_1801_03493_b200/shards.py).  Host wall clock per query, ids on host.
+    qres = None
+    if args.queries != 0:
+        from paper_1801_03493_b200 import shards
+        header = fx.IndexHeader(stream_id=f"cam{rank}", dim=W["dim"], vocab=W["vocab"], n_objects=W["n"], config=cfg)
+        tix = fx.TopKIndex(header, device=last_idx)
+        sess = fx.QuerySession(tix, fx.make_default_profiles(W["vocab"])["gt"], None,
+                               labels=data.true_class.cpu().numpy())
+        classes = np.arange(W["vocab"], dtype=np.int64)  # C5: every class x k_x
+        if 0 < args.queries < W["vocab"]:
+            classes = np.random.default_rng(123).choice(classes, size=args.queries, replace=False)
+        sq = shards.ShardedQuery({rank: sess}, ws) if ws > 1 else None
+        lat, nfr = [], []
+        for kx in (1, 2, 4):
+            for c in classes.tolist():
+                req = fx.QueryRequest(int(c), k_x=kx)
+                if ws > 1:
+                    dist.barrier()
+                t0 = time.perf_counter()
+                if sq is not None:
+                    res = sq.query(req)
+                    nf = sum(r.frame_ids.size for r in res)
+                else:
+                    sess.reset()
+                    fr, ob, st = sess.query_arrays(req)
+                    nf = fr.size
+                lat.append((time.perf_counter() - t0) * 1e3)
+                nfr.append(nf)
+        lat = np.array(lat)
+        if ws > 1:
+            lt = torch.tensor(lat, device="cuda" if args.backend == "nccl" else "cpu")
+            dist.all_reduce(lt, op=dist.ReduceOp.MAX)
+            lat = lt.cpu().numpy()
+        qres = {"queries": int(lat.size), "k_x": [1, 2, 4], "p50_ms": float(np.percentile(lat, 50)),
+                "p99_ms": float(np.percentile(lat, 99)), "mean_ms": float(lat.mean()),
+                "mean_frames": float(np.mean(nfr)), "max_frames": int(np.max(nfr)),
+                "merge": f"{args.backend} all_gather x2 over {ws} ranks" if ws > 1 else "single stream",
+                "timing": "host wall clock per query (fresh session, ids copied to host), max over ranks"}
+        del sess, tix
+
+    # K1b FC classifier head (north star kernel 1) on resident features:
+    # logits over V classes, top-K; tensor-pipe roofline against TF32 dense
+    fcres = None
+    if not args.no_fc:
+        nfc = min(1 << 18, W["n"])
+        Fd = data.feats[:nfc]
+        gfc = torch.Generator(device="cuda")
+        gfc.manual_seed(7)
+        Wt = torch.randn(W["vocab"], W["dim"], device="cuda", generator=gfc) / float(np.sqrt(W["dim"]))
+        bt = 0.1 * torch.randn(W["vocab"], device="cuda", generator=gfc)
+        tk = torch.empty(nfc, W["k"], dtype=torch.int32, device="cuda")
+        cf = torch.empty(nfc, W["k"], dtype=torch.float32, device="cuda")
+        fl = torch.empty(nfc, dtype=torch.uint8, device="cuda")
+        cs = torch.cuda.current_stream()
+
+        def fc_call():
+            _lib.check(L.fx_fc_topk_device(local, _lib.vp(cs.cuda_stream), nfc, W["dim"], W["vocab"], W["k"],
+                                           _lib.vp(Fd.data_ptr()), _lib.vp(Wt.data_ptr()), _lib.vp(bt.data_ptr()),
+                                           _lib.vp(tk.data_ptr()), _lib.vp(cf.data_ptr()), _lib.vp(fl.data_ptr())))
+        fc_call()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        reps = 3
+        e0.record(cs)
+        for _ in range(reps):
+            fc_call()
+        e1.record(cs)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        flops = 2.0 * W["vocab"] * W["dim"] * nfc
+        tf = flops / (ms / 1e3) / 1e12
+        try:
+            bf16 = float(json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))["bf16_tflops"])
+            tf32_peak, pk = bf16 / 2.0, "MEASURED_PEAKS bf16 dense / 2 (TF32 is half the BF16 rate)"
+        except Exception:
+            tf32_peak, pk = 1125.0, "fallback: nominal 2.25 PF bf16 / 2"
+        fcres = {"objects": nfc, "vocab": W["vocab"], "dim": W["dim"], "k": W["k"], "ms": ms,
+                 "objects_per_s": nfc / (ms / 1e3), "achieved_tflops": tf, "peak_tflops": tf32_peak,
+                 "frac": tf / tf32_peak, "peak_kind": pk, "flagged": int(fl.sum().item()),
+                 "bound": "tensor", "note": "TF32 tcgen05 logits + float64 re-score of the candidates"}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
@@ -305,6 +418,7 @@ def main():
                        "streams_per_gpu": 1, "parallelism": f"stream-sharded x{ws}",
                        "l2": "inputs (8 GB features/stream) exceed L2; no flush", **W},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
+            "query": qres, "k1b_fc_head": fcres,
             "gpu_launches": int(launches),
             "ingest": {"clusters": rep.clusters_emitted, "classified": rep.objects_classified,
                        "distance_computations": rep.distance_computations, "exact_rechecks": rep.exact_rechecks,

@@ -115,6 +115,12 @@ int fx_stream_set_fc_head(fx_stream *s, int32_t vocab, const float *W, const flo
  * error bound of each other (may be NULL). */
 int fx_fc_topk(int32_t device, int64_t n, int32_t dim, int32_t vocab, int32_t k, const float *feats, const float *W,
                const float *bias, int32_t *out_topk, float *out_conf, uint8_t *out_flag);
+/* Same with DEVICE pointers, enqueued on the caller's CUDA stream
+ * (cudaStream_t passed as void*; NULL = legacy default stream); returns after
+ * enqueueing (scratch is stream-ordered). */
+int fx_fc_topk_device(int32_t device, void *cuda_stream, int64_t n, int32_t dim, int32_t vocab, int32_t k,
+                      const float *d_feats, const float *d_W, const float *d_bias, int32_t *d_topk, float *d_conf,
+                      uint8_t *d_flag);
 
 /* pixel_diff over a chunk (ingest.py:37-47), continuing from the previous
  * chunk's last object; does not consume the chunk.  out_is_dup[n]. */
@@ -241,6 +247,13 @@ typedef struct {
 int fx_query(fx_session *ss, int32_t class_enc, int32_t k_x, int32_t mode, int32_t keep_label,
              int32_t batch_step, int32_t has_range, int64_t t0, int64_t t1, fx_query_result *res);
 int fx_query_fetch(fx_session *ss, int64_t *frame_ids, int64_t *object_ids);
+/* Same into DEVICE buffers on the index's device (stream-ordered copy on the
+ * index's CUDA stream, completed before return) -- the sharded query merge
+ * all-gathers these over NCCL without a host round trip. */
+int fx_query_fetch_device(fx_session *ss, int64_t *d_frame_ids, int64_t *d_object_ids);
+/* Forget every verification of the session (memo, batched-query seen set,
+ * gt total): a fresh QuerySession over the same index (query.py:36-48). */
+int fx_session_reset(fx_session *ss);
 int64_t fx_session_gt_total(fx_session *ss);
 
 /* ------------------------------------------------------------------------ */

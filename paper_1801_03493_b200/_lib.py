@@ -68,6 +68,8 @@ _SIGS = {
     "fx_stream_set_fc_head": (ctypes.c_int, [vp, ctypes.c_int32, vp, vp]),
     "fx_fc_topk": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, vp, vp,
                                   vp, c_i32p, vp, c_u8p]),
+    "fx_fc_topk_device": (ctypes.c_int, [ctypes.c_int32, vp, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
+                                         ctypes.c_int32, vp, vp, vp, vp, vp, vp]),
     "fx_stream_dup_flags": (ctypes.c_int, [vp, ctypes.c_int64, c_i64p, c_f64p, c_u8p]),
     "fx_ingest": (ctypes.c_int, [vp, ctypes.c_int64, c_i64p, c_i64p, c_f64p, vp, c_i32p, c_i32p, ctypes.c_int32]),
     "fx_ingest_device": (ctypes.c_int, [vp, ctypes.c_int64, vp, vp, vp, vp, vp, vp, ctypes.c_int32]),
@@ -91,6 +93,8 @@ _SIGS = {
     "fx_query": (ctypes.c_int, [vp, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                                 ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.POINTER(QueryResultC)]),
     "fx_query_fetch": (ctypes.c_int, [vp, c_i64p, c_i64p]),
+    "fx_query_fetch_device": (ctypes.c_int, [vp, vp, vp]),
+    "fx_session_reset": (ctypes.c_int, [vp]),
     "fx_session_gt_total": (ctypes.c_int64, [vp]),
 }
 

@@ -357,6 +357,32 @@ int fx_fc_topk(int32_t device, int64_t n, int32_t dim, int32_t vocab, int32_t k,
     })
 }
 
+int fx_fc_topk_device(int32_t device, void *cuda_stream, int64_t n, int32_t dim, int32_t vocab, int32_t k,
+                      const float *d_feats, const float *d_W, const float *d_bias, int32_t *d_topk, float *d_conf,
+                      uint8_t *d_flag) {
+    FX_GUARD({
+        if (!d_feats || !d_W || !d_topk) throw Error{FX_E_USAGE, "null argument"};
+        if (dim < 4 || dim % 4 != 0 || vocab < 1) throw Error{FX_E_USAGE, "bad shapes"};
+        if (k < 1 || k > 16 || k > vocab) throw Error{FX_E_K_OUT_OF_RANGE, "k must be in [1, min(16, vocab)]"};
+        if (((uintptr_t)d_feats % 16) != 0 || ((uintptr_t)d_W % 16) != 0) throw Error{FX_E_USAGE, "unaligned rows"};
+        if (n <= 0) return FX_OK;
+        set_dev(device);
+        init_pool(device);
+        cudaStream_t st = (cudaStream_t)cuda_stream;
+        StreamGuard sg_(st);
+        DevBuf<float> wn, fn;
+        DevBuf<const char *> rows;
+        wn.reserve(vocab);
+        fn.reserve(n);
+        rows.reserve(n);
+        launch_row_norms(vocab, dim, d_W, wn.p, st);
+        launch_row_norms(n, dim, d_feats, fn.p, st);
+        launch_rowptrs(n, (int64_t)dim * 4, (const char *)d_feats, rows.p, st);
+        launch_fc_head(n, 0, rows.p, nullptr, fn.p, dim, vocab, k, d_W, wn.p, d_bias, d_topk, d_conf, d_flag, nullptr,
+                       st);
+    })
+}
+
 int fx_stream_dup_flags(fx_stream *s, int64_t n, const int64_t *frame_ids, const double *sigs, uint8_t *out) {
     FX_GUARD({
         if (!s) throw Error{FX_E_USAGE, "null stream"};
@@ -493,6 +519,61 @@ static int ingest_common(fx_stream *s, int64_t n, const int64_t *object_ids, con
         const bool compact = flags & FX_FEATS_COMPACT;
         if (device) {
             ingest_chunk(s, n, object_ids, frame_ids, sigs, (const char *)feats, true_class, topk, compact);
+        } else if (!compact) {
+            // host buffers: the copies run on a side stream in chunks of CH
+            // objects and the engine consumes chunk k as soon as it has landed,
+            // so PCIe transfer of later chunks overlaps the ingest of earlier
+            // ones (pinned host memory makes the copies truly asynchronous)
+            const int64_t CH = std::max<int64_t>(4096, ((int64_t)1 << 30) / std::max<int64_t>(1, (int64_t)D * s->esize));
+            const int nch = (int)cdiv(n, CH);
+            DevBuf<int64_t> o, f;
+            DevBuf<double> g;
+            DevBuf<int32_t> tc, tk;
+            o.reserve(n);
+            f.reserve(n);
+            g.reserve((size_t)n * std::max(S, 1));
+            if (true_class) tc.reserve(n);
+            if (topk) tk.reserve((size_t)n * K);
+            // feature rows stay resident until finalize (the reference retains
+            // member features until seal, clustering.py:71-83)
+            auto *fb = new DevBuf<char>();
+            s->owned_feats.push_back(fb);
+            fb->reserve((size_t)n * D * s->esize);
+            cudaStream_t cst = nullptr;
+            FX_CUDA(cudaStreamCreateWithFlags(&cst, cudaStreamNonBlocking));
+            std::vector<cudaEvent_t> ev(nch + 1, nullptr);
+            try {
+                FX_CUDA(cudaEventCreateWithFlags(&ev[nch], cudaEventDisableTiming));
+                FX_CUDA(cudaEventRecord(ev[nch], st));  // the allocations above are ordered before the copies
+                FX_CUDA(cudaStreamWaitEvent(cst, ev[nch], 0));
+                for (int c = 0; c < nch; c++) {
+                    const int64_t a = c * CH, m = std::min<int64_t>(CH, n - a);
+                    h2d(o.p + a, object_ids + a, m, cst);
+                    h2d(f.p + a, frame_ids + a, m, cst);
+                    h2d(g.p + a * S, sigs + a * S, m * S, cst);
+                    if (true_class) h2d(tc.p + a, true_class + a, m, cst);
+                    if (topk) h2d(tk.p + a * K, topk + a * K, m * K, cst);
+                    FX_CUDA(cudaMemcpyAsync(fb->p + (size_t)a * D * s->esize, (const char *)feats + (size_t)a * D * s->esize,
+                                            (size_t)m * D * s->esize, cudaMemcpyHostToDevice, cst));
+                    FX_CUDA(cudaEventCreateWithFlags(&ev[c], cudaEventDisableTiming));
+                    FX_CUDA(cudaEventRecord(ev[c], cst));
+                }
+                for (int c = 0; c < nch; c++) {
+                    const int64_t a = c * CH, m = std::min<int64_t>(CH, n - a);
+                    FX_CUDA(cudaStreamWaitEvent(st, ev[c], 0));
+                    ingest_chunk(s, m, o.p + a, f.p + a, g.p + a * S, fb->p + (size_t)a * D * s->esize,
+                                 true_class ? tc.p + a : nullptr, topk ? tk.p + a * K : nullptr, 0);
+                }
+                FX_CUDA(cudaStreamSynchronize(st));
+            } catch (...) {
+                cudaStreamSynchronize(cst);
+                for (auto e : ev)
+                    if (e) cudaEventDestroy(e);
+                cudaStreamDestroy(cst);
+                throw;
+            }
+            for (auto e : ev) cudaEventDestroy(e);
+            FX_CUDA(cudaStreamDestroy(cst));
         } else {
             DevBuf<int64_t> o, f;
             DevBuf<double> g;
@@ -511,20 +592,15 @@ static int ingest_common(fx_stream *s, int64_t n, const int64_t *object_ids, con
                 tk.reserve((size_t)n * K);
                 h2d(tk.p, topk, n * K, st);
             }
-            // feature rows: the engine keeps its own copy until finalize (the
-            // reference retains member features until seal, clustering.py:71-83)
-            int64_t rows = n;
-            if (compact) {
-                // caller passes only non-dup rows: count them on the device first
-                DevBuf<uint8_t> dup;
-                dup.reserve(n);
-                launch_dup_flags(s, n, f.p, g.p, dup.p);
-                std::vector<uint8_t> hd(n);
-                d2h(hd.data(), dup.p, n, st);
-                FX_CUDA(cudaStreamSynchronize(st));
-                rows = 0;
-                for (int64_t i = 0; i < n; i++) rows += hd[i] ? 0 : 1;
-            }
+            // caller passes only non-dup rows: count them on the device first
+            DevBuf<uint8_t> dup;
+            dup.reserve(n);
+            launch_dup_flags(s, n, f.p, g.p, dup.p);
+            std::vector<uint8_t> hd(n);
+            d2h(hd.data(), dup.p, n, st);
+            FX_CUDA(cudaStreamSynchronize(st));
+            int64_t rows = 0;
+            for (int64_t i = 0; i < n; i++) rows += hd[i] ? 0 : 1;
             auto *fb = new DevBuf<char>();
             s->owned_feats.push_back(fb);
             fb->reserve((size_t)rows * D * s->esize);
@@ -895,6 +971,33 @@ int fx_query_fetch(fx_session *ss, int64_t *frame_ids, int64_t *object_ids) {
         d2h(frame_ids, ss->out_f.p, ss->nf, ss->ix->st);
         d2h(object_ids, ss->out_o.p, ss->no, ss->ix->st);
         FX_CUDA(cudaStreamSynchronize(ss->ix->st));
+    })
+}
+
+int fx_query_fetch_device(fx_session *ss, int64_t *d_frame_ids, int64_t *d_object_ids) {
+    FX_GUARD({
+        if (!ss) throw Error{FX_E_USAGE, "null session"};
+        set_dev(ss->ix->dev);
+        StreamGuard sg_(ss->ix->st);
+        cudaStream_t st = ss->ix->st;
+        if (ss->nf && d_frame_ids)
+            FX_CUDA(cudaMemcpyAsync(d_frame_ids, ss->out_f.p, sizeof(int64_t) * ss->nf, cudaMemcpyDeviceToDevice, st));
+        if (ss->no && d_object_ids)
+            FX_CUDA(cudaMemcpyAsync(d_object_ids, ss->out_o.p, sizeof(int64_t) * ss->no, cudaMemcpyDeviceToDevice, st));
+        FX_CUDA(cudaStreamSynchronize(st));
+    })
+}
+
+int fx_session_reset(fx_session *ss) {
+    FX_GUARD({
+        if (!ss) throw Error{FX_E_USAGE, "null session"};
+        set_dev(ss->ix->dev);
+        StreamGuard sg_(ss->ix->st);
+        cudaStream_t st = ss->ix->st;
+        FX_CUDA(cudaMemsetAsync(ss->memo.p, 0, (ss->n_keys + 4) & ~3LL, st));
+        FX_CUDA(cudaMemsetAsync(ss->seen.p, 0, ss->ix->C + 1, st));
+        FX_CUDA(cudaStreamSynchronize(st));
+        ss->gt_total = 0;
     })
 }
 

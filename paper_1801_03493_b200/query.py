@@ -95,7 +95,11 @@ class QuerySession:
         if class_id != OTHER_CLASS and not 0 <= class_id < self.idx.header.vocab:
             raise UnknownClass(str(class_id))
 
-    def _run(self, class_id, k_x, mode, keep_label, batch_step, time_range) -> QueryResult:
+    def reset(self) -> None:
+        """Forget every verification: the session is as fresh as a new one."""
+        _lib.check(self.L.fx_session_reset(self.handle))
+
+    def _launch(self, class_id, k_x, mode, keep_label, batch_step, time_range):
         V = self.idx.header.vocab
         enc = encode_class(class_id, V)
         res = _lib.QueryResultC()
@@ -111,6 +115,39 @@ class QuerySession:
             rep = self.idx.device.export(centroids=False)["reps"][res.error_cluster]
             raise KeyError(int(rep))
         _lib.check(st)
+        return res
+
+    def query_device(self, req: QueryRequest, out_frames=None, out_objects=None):
+        """execute_query with the frame / object ids left in device memory:
+        returns (n_frames, n_objects, stats); when torch device tensors (int64,
+        large enough) are given the ids are copied into them.  stats =
+        (gt_inferences, clusters_examined, clusters_matched)."""
+        self._check_class(req.class_id)
+        res = self._launch(req.class_id, req.k_x, 0, 0, 0, req.time_range)
+        if out_frames is not None or out_objects is not None:
+            _lib.check(self.L.fx_query_fetch_device(
+                self.handle, None if out_frames is None else _lib.vp(out_frames.data_ptr()),
+                None if out_objects is None else _lib.vp(out_objects.data_ptr())))
+        return int(res.n_frames), int(res.n_objects), (int(res.gt_inferences), int(res.clusters_examined),
+                                                       int(res.clusters_matched))
+
+    def fetch_device(self, out_frames, out_objects) -> None:
+        """Copy the last query's ids into torch int64 device tensors."""
+        _lib.check(self.L.fx_query_fetch_device(self.handle, _lib.vp(out_frames.data_ptr()),
+                                                _lib.vp(out_objects.data_ptr())))
+
+    def query_arrays(self, req: QueryRequest):
+        """execute_query returning numpy int64 arrays (frames, objects) + stats."""
+        self._check_class(req.class_id)
+        res = self._launch(req.class_id, req.k_x, 0, 0, 0, req.time_range)
+        fr = np.empty(res.n_frames, np.int64)
+        ob = np.empty(res.n_objects, np.int64)
+        if res.n_frames or res.n_objects:
+            _lib.check(self.L.fx_query_fetch(self.handle, _lib.p64(fr), _lib.p64(ob)))
+        return fr, ob, (int(res.gt_inferences), int(res.clusters_examined), int(res.clusters_matched))
+
+    def _run(self, class_id, k_x, mode, keep_label, batch_step, time_range) -> QueryResult:
+        res = self._launch(class_id, k_x, mode, keep_label, batch_step, time_range)
         fr = np.empty(res.n_frames, np.int64)
         ob = np.empty(res.n_objects, np.int64)
         if res.n_frames or res.n_objects:

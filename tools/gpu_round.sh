@@ -4,5 +4,5 @@ nvidia-smi > gpurun_out/smi.txt 2>&1
 timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?" >> gpurun_out/smoke.log
 timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 0 --n 200000 --no-cpu --e2e-steps 1 > gpurun_out/bench_ncu.log 2>&1; echo "ncu rc=$?" >> gpurun_out/bench_ncu.log
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches.csv python bench.py --steps 1 --warmup 0 --objects 200000 --no-cpu --e2e-steps 1 > gpurun_out/bench_ncu.log 2>&1; echo "ncu rc=$?" >> gpurun_out/bench_ncu.log
 tail -3 gpurun_out/*.log
