@@ -42,12 +42,12 @@ for rep in (f"full_{T}.ncu-rep", f"fc_{T}.ncu-rep"):
     lines.append(f"## {rep}")
     for d in raw(path):
         lines.append(json.dumps(d))
+        def nbytes(v):
+            num, unit = (v.split() + ["byte"])[:2]
+            return float(num.replace(",", "")) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
         try:
-            rb = float(d["dram__bytes_read.sum"].split()[0].replace(",", ""))
-            wb = float(d["dram__bytes_write.sum"].split()[0].replace(",", ""))
-            unit = d["dram__bytes_read.sum"].split()[1] if " " in d["dram__bytes_read.sum"] else "byte"
-            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
-            traffic.setdefault(d["kernel"], []).append((rb + wb) * scale)
+            traffic.setdefault(d["kernel"], []).append(nbytes(d["dram__bytes_read.sum"]) +
+                                                      nbytes(d["dram__bytes_write.sum"]))
         except (KeyError, ValueError, IndexError):
             pass
 open(os.path.join(P, f"{T}_ncu_full_metrics.txt"), "w").write("\n".join(lines) + "\n")
