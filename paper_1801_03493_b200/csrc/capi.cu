@@ -224,8 +224,8 @@ int fx_stream_create(const fx_stream_config *cfg, fx_stream **out) {
             FX_CUDA(cudaMemsetAsync(s->s_grp.p, 0xff, sizeof(int32_t) * ns, s->st));
             s->h_ctr_ring = (int64_t *)pinned_borrow(sizeof(int64_t) * 3 * C_COUNT);
             for (int i = 0; i < 3; i++) FX_CUDA(cudaEventCreateWithFlags(&s->ring_ev[i], cudaEventDisableTiming));
-            s->prof.reserve(16);
-            FX_CUDA(cudaMemsetAsync(s->prof.p, 0, sizeof(int64_t) * 16, s->st));
+            s->prof.reserve(24);
+            FX_CUDA(cudaMemsetAsync(s->prof.p, 0, sizeof(int64_t) * 24, s->st));
             s->ctr.reserve(C_COUNT);
             FX_CUDA(cudaMemsetAsync(s->ctr.p, 0, sizeof(int64_t) * C_COUNT, s->st));
             k_init_free<<<(unsigned)cdiv(ns, 256), 256, 0, s->st>>>(ns, s->free_stack.p);
@@ -749,9 +749,9 @@ int fx_stream_counters(fx_stream *s, int64_t *out, int n) {
         FX_CUDA(cudaStreamSynchronize(s->st));
         for (int i = 0; i < n && i < C_COUNT; i++) out[i] = s->h_ctr[i];
         if (n > C_COUNT) {
-            int64_t pr[16];
+            int64_t pr[24];
             FX_CUDA(cudaMemcpy(pr, s->prof.p, sizeof(pr), cudaMemcpyDeviceToHost));
-            for (int i = C_COUNT; i < n && i < C_COUNT + 16; i++) out[i] = pr[i - C_COUNT];
+            for (int i = C_COUNT; i < n && i < C_COUNT + 24; i++) out[i] = pr[i - C_COUNT];
         }
     })
 }

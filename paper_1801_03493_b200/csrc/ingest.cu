@@ -1487,6 +1487,22 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
     // ---- epilogue: pending-member CSR for k_fold, snapshot for next batch
     __syncthreads();
     if (tid == 0) {
+        // the slot with the most pending rows goes first (k_fold gives it its own grid row)
+        int best = 0, bc = -1;
+        for (int i = 0; i < s_ndirty; i++) {
+            const int c = A.s_pend[A.dirty[i]];
+            if (c > bc) {
+                bc = c;
+                best = i;
+            }
+        }
+        if (best > 0) {
+            const int a0 = A.dirty[0], a1 = A.dirty[best];
+            A.dirty[0] = a1;
+            A.dirty[best] = a0;
+            A.s_didx[a1] = 0;
+            A.s_didx[a0] = best;
+        }
         int acc = 0;
         for (int i = 0; i < s_ndirty; i++) {
             A.dirty_off[i] = acc;
@@ -1535,7 +1551,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
 // R rows x FD dims (gather the rows' pointers, cp.async the slices, wait,
 // then publish with an mbarrier arrive).  So FOLD_NS * R rows are in flight
 // for the dominant cluster of a Zipf stream, which owns most of a batch.
-constexpr int FD = 32, FOLD_NS = 4, FOLD_THREADS = 32 * (1 + FOLD_NS);
+constexpr int FD = 32, FOLD_NS = 6, FOLD_THREADS = 32 * (1 + FOLD_NS);
 template <typename T>
 constexpr int fold_rows() { return sizeof(T) == 4 ? 128 : 64; }  // 16 KB per stage either way
 template <typename T>
@@ -1571,7 +1587,8 @@ __global__ void __launch_bounds__(FOLD_THREADS) k_fold(int D, int64_t c0, const 
                                                       const int32_t *__restrict__ s_seedpos, const int32_t *__restrict__ s_evicted,
                                                       const int32_t *__restrict__ s_cid, const int32_t *__restrict__ s_size,
                                                       float *__restrict__ s_cn2, double *__restrict__ fcent,
-                                                      int32_t *__restrict__ cl_nfeat, int32_t *__restrict__ cl_size) {
+                                                      int32_t *__restrict__ cl_nfeat, int32_t *__restrict__ cl_size,
+                                                      long long *__restrict__ fprof) {
     constexpr int R = fold_rows<T>();
     extern __shared__ __align__(16) unsigned char fold_raw[];
     T *ring = (T *)fold_raw;                                                // [NS][R][FD]
@@ -1587,7 +1604,11 @@ __global__ void __launch_bounds__(FOLD_THREADS) k_fold(int D, int64_t c0, const 
     }
     __syncthreads();
     int J0 = 0;
-    for (int di = blockIdx.y; di < nd; di += gridDim.y) {
+    // grid row 0 folds only dirty[0] -- the slot with the most pending rows
+    // (the resolve puts it first), so its long chain starts at once; the
+    // other rows share the remaining slots
+    const int dstart = blockIdx.y, dstep = blockIdx.y == 0 ? nd : (int)gridDim.y - 1;
+    for (int di = dstart; di < nd; di += dstep) {
         const int slot = dirty[di];
         const int p0 = dirty_off[di], p1 = dirty_off[di + 1];
         const int nst = (p1 - p0 + R - 1) / R;
@@ -1599,15 +1620,30 @@ __global__ void __launch_bounds__(FOLD_THREADS) k_fold(int D, int64_t c0, const 
             // every x), so the chain is one dadd per row (~18 cycles on B200).
             const int fp = s_foldpos[slot], sp = s_seedpos[slot];
             double acc = (sp >= 0 && sp >= fp) ? -0.0 : (k < D ? S[(int64_t)slot * D + k] : 0.0);
+            const bool prof = fprof && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0;
+            long long tw = 0, tc = 0, t0 = prof ? clock64() : 0;
             for (int j = 0; j < nst; j++) {
                 const int G = J0 + j, buf = G % FOLD_NS;
+                long long ta = prof ? clock64() : 0;
                 fbar_wait(&full[buf], (uint32_t)((G / FOLD_NS) & 1));
+                long long tb = prof ? clock64() : 0;
                 const int nr = min(R, p1 - p0 - j * R);
                 const T *rb = ring + (size_t)buf * R * FD + lane;
 #pragma unroll 8
                 for (int r = 0; r < nr; r++) acc = dadd(acc, to_d(rb[r * FD]));
                 __syncwarp();
                 if (lane == 0) fbar_arrive(&empty[buf]);
+                if (prof) {
+                    tw += tb - ta;
+                    tc += clock64() - tb;
+                }
+            }
+            if (prof) {
+                atomicAdd((unsigned long long *)&fprof[0], (unsigned long long)tw);
+                atomicAdd((unsigned long long *)&fprof[1], (unsigned long long)tc);
+                atomicAdd((unsigned long long *)&fprof[2], (unsigned long long)(clock64() - t0));
+                atomicAdd((unsigned long long *)&fprof[3], (unsigned long long)(p1 - p0));
+                atomicAdd((unsigned long long *)&fprof[4], 1ull);
             }
             float c2 = 0.f;
             if (k < D) {
@@ -1627,28 +1663,28 @@ __global__ void __launch_bounds__(FOLD_THREADS) k_fold(int D, int64_t c0, const 
                 }
             }
         } else {
-            // producer for buffer w: global stages G = w (mod NS)
+            // producer for buffer w: global stages G = w (mod NS).  The row
+            // pointers of a stage are gathered before its buffer is free
+            // (lane l loads rows l, l+32, ...: coalesced, independent), so a
+            // refill costs only the copies once the consumer releases it.
             const int w = wid - 1;
             const int fp = s_foldpos[slot];
-            for (int j = (w - J0 % FOLD_NS + FOLD_NS) % FOLD_NS; j < nst; j += FOLD_NS) {
-                const int G = J0 + j;
-                if (G >= FOLD_NS) fbar_wait(&empty[w], (uint32_t)(((G / FOLD_NS) - 1) & 1));
+            auto gather = [&](int j, const T **rp) {
                 const int rbase = p0 + j * R, nr = min(R, p1 - rbase);
+                int bq[R / 32];
+#pragma unroll
+                for (int c = 0; c < R / 32; c++) bq[c] = (j < nst && c * 32 + lane < nr) ? pend_list[rbase + c * 32 + lane] : -1;
+#pragma unroll
+                for (int c = 0; c < R / 32; c++) rp[c] = bq[c] >= fp ? (const T *)frow[c0 + bq[c]] : nullptr;
+            };
+            const T *rp[R / 32];
+            int j = (w - J0 % FOLD_NS + FOLD_NS) % FOLD_NS;
+            gather(j, rp);
+            for (; j < nst; j += FOLD_NS) {
+                const int G = J0 + j;
+                const int nr = min(R, p1 - p0 - j * R);
+                if (G >= FOLD_NS) fbar_wait(&empty[w], (uint32_t)(((G / FOLD_NS) - 1) & 1));
                 T *dst = ring + (size_t)w * R * FD;
-                // lane l gathers the pointers of rows l, l+32, ... (coalesced,
-                // independent loads), then the warp broadcasts them row by row
-                const T *rp[R / 32];
-#pragma unroll
-                for (int c = 0; c < R / 32; c++) {
-                    const int row = c * 32 + lane;
-                    const int bq = row < nr ? pend_list[rbase + row] : -1;
-                    rp[c] = (const T *)(intptr_t)bq;  // stash the position; resolved below
-                }
-#pragma unroll
-                for (int c = 0; c < R / 32; c++) {
-                    const int bq = (int)(intptr_t)rp[c];
-                    rp[c] = bq >= fp ? (const T *)frow[c0 + bq] : nullptr;
-                }
 #pragma unroll
                 for (int c = 0; c < R / 32; c++) {
                     for (int i = 0; i < 32; i++) {
@@ -1663,6 +1699,7 @@ __global__ void __launch_bounds__(FOLD_THREADS) k_fold(int D, int64_t c0, const 
                             *d = (T)(-0.0);  // member already folded by the resolve's exact path
                     }
                 }
+                gather(j + FOLD_NS, rp);  // next stage's pointers while these copies fly
                 asm volatile("cp.async.wait_all;\n" ::: "memory");
                 __syncwarp();
                 if (lane == 0) fbar_arrive(&full[w]);
@@ -2033,7 +2070,7 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             k_fold<T><<<grid, FOLD_THREADS, fold_smem<T>(), st>>>(D, c0, s->ctr.p, s->dirty.p, s->dirty_off.p, s->pend_list.p, s->frow.p,
                                             s->S.p, s->C32.p, s->s_nfeat.p, s->s_foldpos.p, s->s_seedpos.p,
                                             s->s_evicted.p, s->s_cid.p, s->s_size.p, s->s_cn2.p, s->fcent.p,
-                                            s->cl_nfeat.p, s->cl_size.p);
+                                            s->cl_nfeat.p, s->cl_size.p, (long long *)(s->prof.p + 16));
             FX_LAUNCHED();
             s->tstop();
         }

@@ -119,7 +119,7 @@ class Stream:
                 "nevict_batch", "ndefer", "nod", "last_cid", "ndirty", "err", "fast", "fc_flagged",
                 "cyc_passA", "cyc_passB", "cyc_passCD", "cyc_confirm", "cyc_passE", "cyc_seq", "windows", "seq_steps",
                 "conf_b0", "conf_b1_7", "conf_b8_15", "conf_b16_31", "conf_b32_63", "conf_b64_127", "conf_b128",
-                "conf_young")
+                "conf_young", "fold_wait_cyc", "fold_chain_cyc", "fold_slot_cyc", "fold_rows", "fold_slots")
     PHASES = ("k0_k1a", "screen", "resolve", "fold", "seal", "index", "batches", "screen_resid",
               "host_screen", "host_resolve", "host_ring", "host_fold", "host_grow", "host_k0", "host_k1",
               "screen_summary")
