@@ -92,7 +92,7 @@ struct fx_stream {
     fx::DevBuf<float> dres;    // [B*B]
     fx::DevBuf<int32_t> res_col, res_pos;
     fx::DevBuf<float> dod;     // [B*B] on-demand columns
-    fx::DevBuf<int32_t> slot_of, pend_rank, evict_slot, evict_cid, dirty, dirty_off, pend_list, sum_slot;
+    fx::DevBuf<int32_t> slot_of, pend_rank, evict_slot, evict_cid, dirty, dirty_off, pend_list, sum_slot, sum_q;
     fx::DevBuf<float> sum_d1, sum_e1, sum_lbr;
     // per-cluster results (grow with clusters)
     int64_t cl_cap = 0;

@@ -342,7 +342,7 @@ struct ResolveArgs {
     int32_t *s_grp;
     long long *prof;  // [16] cycles: A, B1B2, CD, confirm, E, seq; [6] windows, [7] seq steps; [8..15] confirms by batch bucket
     int batch_no;
-    const int32_t *sum_slot;
+    const int32_t *sum_slot, *sum_q;
     const float *sum_d1, *sum_e1, *sum_lbr;
 };
 
@@ -499,7 +499,8 @@ __global__ void k_row_summary(int nA, const int64_t *__restrict__ ctr, const flo
                               const float *__restrict__ cn2, const int32_t *__restrict__ snap,
                               const float *__restrict__ fnorm, int64_t a0, ScreenModel sm, float rel, float absc,
                               const char *const *__restrict__ frow, const float *__restrict__ C32, int D,
-                              int32_t *__restrict__ sum_slot, float *__restrict__ sum_d1, float *__restrict__ sum_e1,
+                              int32_t *__restrict__ sum_slot, int32_t *__restrict__ sum_q, float *__restrict__ sum_d1,
+                              float *__restrict__ sum_e1,
                               float *__restrict__ sum_lbr) {
     const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (w >= nA) return;
@@ -562,6 +563,7 @@ __global__ void k_row_summary(int nA, const int64_t *__restrict__ ctr, const flo
     }
     if (lane == 0) {
         sum_slot[w] = q1 >= 0 ? snap[q1] : -1;
+        sum_q[w] = q1;
         sum_d1[w] = d1;
         sum_e1[w] = e1;
         sum_lbr[w] = lbr;
@@ -587,6 +589,7 @@ __global__ void __launch_bounds__(256) k_rowpass(int nA, int64_t a0, const char 
                                                 const float *__restrict__ fnorm, ScreenModel sm, float rel, float absc,
                                                 const float *__restrict__ C32, double T, const int32_t *__restrict__ res_pos,
                                                 float *__restrict__ dres, int64_t ldr, int32_t *__restrict__ sum_slot,
+                                                int32_t *__restrict__ sum_q,
                                                 float *__restrict__ sum_d1, float *__restrict__ sum_e1,
                                                 float *__restrict__ sum_lbr) {
     __shared__ int s_rpos[RC_MAX];
@@ -684,6 +687,7 @@ __global__ void __launch_bounds__(256) k_rowpass(int nA, int64_t a0, const char 
         }
         if (lane == 0) {
             sum_slot[w] = q1 >= 0 ? snap[q1] : -1;
+            sum_q[w] = q1;
             sum_d1[w] = d1;
             sum_e1[w] = e1;
             sum_lbr[w] = lbr;
@@ -691,7 +695,7 @@ __global__ void __launch_bounds__(256) k_rowpass(int nA, int64_t a0, const char 
     }
 }
 
-constexpr int RS_MAXGRP = 1024;
+constexpr int RS_MAXGRP = 512;
 constexpr int RS_RANKW = 8;  // warps that rank a window (per-warp group counters)
 constexpr int RS_WCNT_BYTES = RS_RANKW * RS_MAXGRP * 2;
 constexpr int RS_WIN0 = 64;
@@ -809,6 +813,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
     __shared__ float s_ub_used;
     __shared__ int grp_slot[RS_MAXGRP];
     __shared__ int grp_cnt[RS_MAXGRP], grp_off[RS_MAXGRP], grp_ncommit[RS_MAXGRP], grp_nf0[RS_MAXGRP];
+    __shared__ int grp_cid[RS_MAXGRP], grp_size0[RS_MAXGRP], grp_pend0[RS_MAXGRP];
     __shared__ float grp_drift[RS_MAXGRP], grp_U[RS_MAXGRP], grp_d0[RS_MAXGRP], grp_cn[RS_MAXGRP];
     __shared__ int s_ngrp, s_fail;
     __shared__ double s_md1, s_md2;
@@ -865,11 +870,15 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
             s_fail = e_end;
             A.prof[6]++;
         }
-        // pass A: hypothesis per object (snapshot summary + in-batch seeds)
+        // pass A: hypothesis per object (snapshot summary + in-batch seeds).
+        // With no in-batch seed and no eviction yet every hypothesis is a
+        // snapshot slot: its snapshot index is the group id (no slot map).
+        const bool qkeys = s_nseeds == 0 && !s_any_evicted && nsnap <= RS_MAXGRP;
         if (s_nseeds == 0 && !s_any_evicted) {
             for (int p = b + tid; p < e_end; p += blockDim.x) {
                 const float d1 = A.sum_d1[p], e1 = A.sum_e1[p], lbr = A.sum_lbr[p];
                 seg_key[p] = (L > 0) ? A.sum_slot[p] : -1;
+                if (qkeys) seg_grp[p] = (short)((L > 0) ? A.sum_q[p] : -1);
                 seg_ub0[p] = (d1 + e1) * 1.000001f + 1e-30f;
                 seg_lbr[p] = lbr - fabsf(lbr) * 1e-6f - 1e-30f;
             }
@@ -928,30 +937,43 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
         if (tid == 0) A.prof[0] += t1 - t0;
         // pass B1: distinct hypothesis slots -> group ids; per group the
         // largest hypothesis upper bound (it bounds every member's join step)
-        for (int p = b + tid; p < e_end; p += blockDim.x) {
-            const int key = seg_key[p];
-            if (key < 0) continue;
-            if (A.s_grp[key] == -1 && atomicCAS(&A.s_grp[key], -1, -2) == -1) {
-                int g = atomicAdd(&s_ngrp, 1);
-                if (g < RS_MAXGRP) grp_slot[g] = key;
-                A.s_grp[key] = g < RS_MAXGRP ? g : RS_MAXGRP;
+        if (qkeys) {
+            if (tid == 0) s_ngrp = nsnap;
+            for (int g = tid; g < nsnap; g += blockDim.x) grp_slot[g] = A.snap_slot[g];
+        } else {
+            for (int p = b + tid; p < e_end; p += blockDim.x) {
+                const int key = seg_key[p];
+                if (key < 0) continue;
+                if (A.s_grp[key] == -1 && atomicCAS(&A.s_grp[key], -1, -2) == -1) {
+                    int g = atomicAdd(&s_ngrp, 1);
+                    if (g < RS_MAXGRP) grp_slot[g] = key;
+                    A.s_grp[key] = g < RS_MAXGRP ? g : RS_MAXGRP;
+                }
             }
         }
         __syncthreads();
         const int ngrp = min(s_ngrp, RS_MAXGRP);
         const bool overflow = s_ngrp > RS_MAXGRP;
         for (int p = b + tid; p < e_end; p += blockDim.x) {
-            const int key = seg_key[p];
-            const int g = key >= 0 ? A.s_grp[key] : -1;
-            const bool ok = g >= 0 && g < RS_MAXGRP;
-            seg_grp[p] = (short)(ok ? g : -1);
-            if (ok) atomicMax((int *)&grp_U[g], __float_as_int(seg_ub0[p]));  // ub0 > 0
+            int g;
+            if (qkeys) {
+                g = seg_grp[p];
+            } else {
+                const int key = seg_key[p];
+                g = key >= 0 ? A.s_grp[key] : -1;
+                g = (g >= 0 && g < RS_MAXGRP) ? g : -1;
+                seg_grp[p] = (short)g;
+            }
+            if (g >= 0) atomicMax((int *)&grp_U[g], __float_as_int(seg_ub0[p]));  // ub0 > 0
         }
         for (int g = tid; g < ngrp; g += blockDim.x) {
             const int sl = grp_slot[g];
             grp_nf0[g] = A.s_nfeat[sl];
             grp_d0[g] = __double2float_ru(A.s_drift[sl]);
             grp_cn[g] = sqrtf(A.s_cn2[sl]) * 1.00001f;
+            grp_cid[g] = A.s_cid[sl];
+            grp_size0[g] = A.s_size[sl];
+            grp_pend0[g] = A.s_pend[sl];
         }
         __syncthreads();
         // pass B2: stable rank of every object inside its group.  Each warp
@@ -1019,7 +1041,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
             seg_scan_ub(nlist, glist, seg_grp, seg_ub0, seg_P, wsf, wsh);
             for (int g = tid; g < ngrp; g += blockDim.x) {
                 const int jl = grp_off[g] + grp_cnt[g] - 1;
-                const float Ptot = __fadd_ru(seg_P[jl], seg_ub0[glist[jl]]);
+                const float Ptot = grp_cnt[g] > 0 ? __fadd_ru(seg_P[jl], seg_ub0[glist[jl]]) : 0.f;
                 grp_drift[g] = drift_avg(grp_d0[g], grp_nf0[g], Ptot, grp_cnt[g], grp_cn[g], grp_U[g]);
             }
         }
@@ -1032,8 +1054,8 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
             int m1s = -1;
             for (int i = tid; i < L; i += blockDim.x) {
                 const int sl = A.live[i];
-                const int g = A.s_grp[sl];
-                const double d = (g >= 0 && g < RS_MAXGRP) ? (double)grp_drift[g] : A.s_drift[sl];
+                const int g = qkeys ? A.s_snapq[sl] : A.s_grp[sl];
+                const double d = (g >= 0 && g < RS_MAXGRP && g < ngrp && !overflow) ? (double)grp_drift[g] : A.s_drift[sl];
                 if (d > m1) {
                     m2 = m1;
                     m1 = d;
@@ -1200,10 +1222,10 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
                 const int sl = grp_slot[g];
                 const int64_t cc = A.c0 + p;
                 const int64_t obj = A.cls_obj[cc];
-                A.cluster_of[obj] = A.s_cid[sl];
-                A.mrank[obj] = A.s_size[sl] + i + mlist[j];
+                A.cluster_of[obj] = grp_cid[g];
+                A.mrank[obj] = grp_size0[g] + i + mlist[j];
                 A.frank[obj] = grp_nf0[g] + i;
-                A.pend_rank[p] = A.s_pend[sl] + i;
+                A.pend_rank[p] = grp_pend0[g] + i;
                 A.slot_of[p] = sl;
                 sh_slot_of[p] = sl;
             }
@@ -1226,7 +1248,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
                         A.dirty[di] = sl;
                     }
                 }
-                A.s_grp[sl] = -1;
+                if (!qkeys) A.s_grp[sl] = -1;
             }
         }
         if (overflow) {
@@ -1885,18 +1907,20 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             if (D <= 1024)
                 k_rowpass<8><<<grid, 256, 0, st>>>(B, c0, s->frow.p, D, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p,
                                                    s->snap_slot.p, s->fnorm.p, sm, rel, absc, s->C32.p, s->cfg.t,
-                                                   s->res_pos.p, s->dres.p, B, s->sum_slot.p, s->sum_d1.p, s->sum_e1.p,
+                                                   s->res_pos.p, s->dres.p, B, s->sum_slot.p, s->sum_q.p, s->sum_d1.p,
+                                                   s->sum_e1.p,
                                                    s->sum_lbr.p);
             else
                 k_rowpass<16><<<grid, 256, 0, st>>>(B, c0, s->frow.p, D, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p,
                                                     s->snap_slot.p, s->fnorm.p, sm, rel, absc, s->C32.p, s->cfg.t,
-                                                    s->res_pos.p, s->dres.p, B, s->sum_slot.p, s->sum_d1.p, s->sum_e1.p,
+                                                    s->res_pos.p, s->dres.p, B, s->sum_slot.p, s->sum_q.p, s->sum_d1.p,
+                                                   s->sum_e1.p,
                                                     s->sum_lbr.p);
             FX_LAUNCHED();
         } else {
         k_row_summary<T><<<(unsigned)cdiv((int64_t)B * 32, 256), 256, 0, st>>>(
                 B, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p, s->snap_slot.p, s->fnorm.p, c0, sm, rel, absc, s->frow.p,
-                s->C32.p, D, s->sum_slot.p, s->sum_d1.p, s->sum_e1.p, s->sum_lbr.p);
+                s->C32.p, D, s->sum_slot.p, s->sum_q.p, s->sum_d1.p, s->sum_e1.p, s->sum_lbr.p);
             FX_LAUNCHED();
         }
         s->tstop();
@@ -1959,6 +1983,7 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             A.prof = (long long *)s->prof.p;
             A.batch_no = (int)s->batch_no;
             A.sum_slot = s->sum_slot.p;
+            A.sum_q = s->sum_q.p;
             A.sum_d1 = s->sum_d1.p;
             A.sum_e1 = s->sum_e1.p;
             A.sum_lbr = s->sum_lbr.p;
