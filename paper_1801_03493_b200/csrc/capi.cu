@@ -200,7 +200,7 @@ int fx_stream_create(const fx_stream_config *cfg, fx_stream **out) {
                 int64_t b = ((int64_t)1 << 26) / std::max<int64_t>(cfg->m, 1);
                 B = (int)std::min<int64_t>(4096, std::max<int64_t>(256, b));
             }
-            B = std::max(64, (B / 64) * 64);
+            B = std::max(64, (std::min(B, 4096) / 64) * 64);  // k_resolve windows are <= 4096 objects
             s->plan_host = new PwPlan();
             build_pw_plan(D, s->plan_host);
             // k_resolve keeps per-object state of the whole batch in shared memory

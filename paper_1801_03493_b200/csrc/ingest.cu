@@ -875,6 +875,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
         // snapshot slot: its snapshot index is the group id (no slot map).
         const bool qkeys = s_nseeds == 0 && !s_any_evicted && nsnap <= RS_MAXGRP;
         if (s_nseeds == 0 && !s_any_evicted) {
+#pragma unroll 4
             for (int p = b + tid; p < e_end; p += blockDim.x) {
                 const float d1 = A.sum_d1[p], e1 = A.sum_e1[p], lbr = A.sum_lbr[p];
                 seg_key[p] = (L > 0) ? A.sum_slot[p] : -1;
@@ -1168,14 +1169,22 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
                 const int per = (nlist + RS_THREADS - 1) / RS_THREADS;
                 const int jlo = min(nlist, tid * per), jhi = min(nlist, jlo + per);
                 int run = 0, head = 0;
-                for (int j = jlo; j < jhi; j++) {
+                constexpr int PERMAX = (4096 + RS_THREADS - 1) / RS_THREADS;  // windows never exceed 4096 objects
+                int dr[PERMAX];
+                const int32_t *__restrict__ dup_run = A.dup_run + A.c0;
+#pragma unroll
+                for (int u = 0; u < PERMAX; u++) dr[u] = jlo + u < jhi ? dup_run[glist[jlo + u]] : 0;  // loads in flight together
+#pragma unroll
+                for (int u = 0; u < PERMAX; u++) {
+                    const int j = jlo + u;
+                    if (j >= jhi) break;
                     const int p = glist[j];
                     if (j == 0 || seg_grp[glist[j - 1]] != seg_grp[p]) {
                         run = 0;
                         head = 1;
                     }
                     mlist[j] = run;
-                    run += A.dup_run[A.c0 + p];
+                    run += dr[u];
                 }
                 int v = run, h = head;  // inclusive warp scan, segmented operator
 #pragma unroll
@@ -1214,20 +1223,39 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
                 }
             }
             __syncthreads();
-            for (int j = tid; j < nlist; j += blockDim.x) {
-                const int p = glist[j];
-                const int g = seg_grp[p];
-                const int i = j - grp_off[g];
-                if (i >= grp_ncommit[g]) continue;
-                const int sl = grp_slot[g];
-                const int64_t cc = A.c0 + p;
-                const int64_t obj = A.cls_obj[cc];
-                A.cluster_of[obj] = grp_cid[g];
-                A.mrank[obj] = grp_size0[g] + i + mlist[j];
-                A.frank[obj] = grp_nf0[g] + i;
-                A.pend_rank[p] = grp_pend0[g] + i;
-                A.slot_of[p] = sl;
-                sh_slot_of[p] = sl;
+            {
+                // per-object writes; the object-index loads of 4 list entries are
+                // issued together (restrict: the outputs never alias the inputs)
+                const int64_t *__restrict__ cls_obj = A.cls_obj + A.c0;
+                int32_t *__restrict__ cluster_of = A.cluster_of;
+                int32_t *__restrict__ mrank = A.mrank;
+                int32_t *__restrict__ frank = A.frank;
+                int32_t *__restrict__ pend_rank = A.pend_rank;
+                int32_t *__restrict__ slot_of = A.slot_of;
+                for (int j0 = tid; j0 < nlist; j0 += 4 * RS_THREADS) {
+                    int64_t obj[4];
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const int j = j0 + u * RS_THREADS;
+                        obj[u] = j < nlist ? cls_obj[glist[j]] : 0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; u++) {
+                        const int j = j0 + u * RS_THREADS;
+                        if (j >= nlist) break;
+                        const int p = glist[j];
+                        const int g = seg_grp[p];
+                        const int i = j - grp_off[g];
+                        if (i >= grp_ncommit[g]) continue;
+                        const int sl = grp_slot[g];
+                        cluster_of[obj[u]] = grp_cid[g];
+                        mrank[obj[u]] = grp_size0[g] + i + mlist[j];
+                        frank[obj[u]] = grp_nf0[g] + i;
+                        pend_rank[p] = grp_pend0[g] + i;
+                        slot_of[p] = sl;
+                        sh_slot_of[p] = sl;
+                    }
+                }
             }
             __syncthreads();
             for (int g = tid; g < ngrp; g += blockDim.x) {
