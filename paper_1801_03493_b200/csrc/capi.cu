@@ -465,7 +465,7 @@ static void ingest_chunk(fx_stream *s, int64_t n, const int64_t *d_oid, const in
     }
     if (((uintptr_t)d_feats % 16) != 0 || ((int64_t)s->cfg.dim * s->esize) % 16 != 0) s->rows_aligned16 = false;
     launch_compact(s, n, n0, c0, s->is_dup.p + n0, excl.p, d_feats, compact);
-    launch_fnorm(s, c0, nc);
+    if (!s->tc_screen || s->has_fc) launch_fnorm(s, c0, nc);  // else the TC screen computes the batch's norms
     // K1: top-K
     if (!d_topk && s->has_fc) {
         if (!s->rows_aligned16) throw Error{FX_E_USAGE, "fc head needs 16-byte aligned feature rows"};

@@ -309,10 +309,39 @@ __global__ void k_minmax(int64_t n, const int64_t *__restrict__ a, const int64_t
         bmin = y < bmin ? y : bmin;
         bmax = y > bmax ? y : bmax;
     }
-    atomicMin(&out[0], amin);
-    atomicMax(&out[1], amax);
-    atomicMin(&out[2], bmin);
-    atomicMax(&out[3], bmax);
+    // warp, then block reduction: one atomic per block and value (not per thread)
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        unsigned long long t = __shfl_xor_sync(0xffffffffu, amin, o);
+        amin = t < amin ? t : amin;
+        t = __shfl_xor_sync(0xffffffffu, amax, o);
+        amax = t > amax ? t : amax;
+        t = __shfl_xor_sync(0xffffffffu, bmin, o);
+        bmin = t < bmin ? t : bmin;
+        t = __shfl_xor_sync(0xffffffffu, bmax, o);
+        bmax = t > bmax ? t : bmax;
+    }
+    __shared__ unsigned long long red[4][32];
+    const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        red[0][w] = amin;
+        red[1][w] = amax;
+        red[2][w] = bmin;
+        red[3][w] = bmax;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < nw; i++) {
+            amin = red[0][i] < amin ? red[0][i] : amin;
+            amax = red[1][i] > amax ? red[1][i] : amax;
+            bmin = red[2][i] < bmin ? red[2][i] : bmin;
+            bmax = red[3][i] > bmax ? red[3][i] : bmax;
+        }
+        atomicMin(&out[0], amin);
+        atomicMax(&out[1], amax);
+        atomicMin(&out[2], bmin);
+        atomicMax(&out[3], bmax);
+    }
 }
 
 // duplicate cluster id check over ascending-sorted ids

@@ -1850,7 +1850,7 @@ __global__ void k_seal_pick(int64_t nfeat_total, const int32_t *__restrict__ fme
 
 void launch_screen_tc(int nA, int64_t a0, const char *const *frow, const float *fnorm, int D, const int64_t *nB_dev,
                       int nB_max, const float *C32, const int32_t *snap, const float *cn2, float *out, int64_t ld,
-                      cudaStream_t st);
+                      cudaStream_t st, float *fnorm_out);
 int64_t scan_i32_to_i64(const int32_t *in, int64_t n, int64_t *out_excl, cudaStream_t st, int64_t *scratch_total);
 void scan_u8_to_i64(const uint8_t *in, int64_t n, int invert, int64_t *out_excl, int64_t *d_total, cudaStream_t st);
 
@@ -1893,8 +1893,9 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
         // 1. snapshot screen
         s->tstart(1);
         if (s->tc_screen) {
+            // the screen also produces ||f|| of the batch rows (fnorm) unless an earlier pass did
             launch_screen_tc(B, c0, s->frow.p, s->fnorm.p, D, s->ctr.p + C_NSNAP, (int)s->ld, s->C32.p,
-                             s->snap_slot.p, s->s_cn2.p, s->dist.p, s->ld, st);
+                             s->snap_slot.p, s->s_cn2.p, s->dist.p, s->ld, st, s->has_fc ? nullptr : s->fnorm.p);
         } else {
             const unsigned grid = (unsigned)std::min<int64_t>(cdiv(s->ld, SC_T) * cdiv(B, SC_T), 148 * 8);
             FromSnapshot fb{s->C32.p, s->snap_slot.p, D};

@@ -42,11 +42,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
                                                            const float *__restrict__ C32,
                                                            const int32_t *__restrict__ snap,
                                                            const float *__restrict__ cn2, float *__restrict__ out,
-                                                           int64_t ld, int kchunk, int dbg) {
+                                                           int64_t ld, int kchunk, int dbg, float *__restrict__ fnorm_out) {
     // blockIdx.z selects the K range [z*kchunk, (z+1)*kchunk) (split-K when the
     // tile grid alone cannot fill the machine; partials are atomically added)
     const int nB = (int)*nB_dev;
     const int tb = blockIdx.x * TC_N, ta = blockIdx.y * TC_M;
+    if (nB == 0 && fnorm_out && blockIdx.x == 0 && blockIdx.z == 0 && ta + (int)threadIdx.x < nA) {
+        // empty snapshot (stream start): no screen, but the batch still needs ||f||
+        const float *row = (const float *)frow[a0 + ta + threadIdx.x];
+        float tot = 0.f;
+        for (int k0 = 0; k0 < D; k0 += TC_KT) {
+            float p = 0.f;
+            for (int k = k0; k < min(D, k0 + TC_KT); k++) p = fmaf(row[k], row[k], p);
+            tot += p;
+        }
+        fnorm_out[a0 + ta + threadIdx.x] = sqrtf(tot);
+    }
     if (tb >= nB || ta >= nA) return;
     extern __shared__ __align__(1024) unsigned char smem[];
     // [stage][A 16KB | B 16KB]
@@ -93,11 +104,25 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
         }
         asm volatile("cp.async.commit_group;\n" ::);
     }
+    float a2 = 0.f;  // ||A_row||^2 of this thread's row over the CTA's K range (fp32, per-stage partials)
     for (int it = 0; it < nk; it++) {
         const int s = it % TC_STAGES;
         asm volatile("cp.async.wait_group %0;\n" ::"n"(TC_STAGES - 2));
         asm volatile("fence.proxy.async.shared::cta;\n" ::);
         __syncthreads();
+        {  // the row norm rides along: row tid's 32 values of this stage (stable until its refill)
+            const unsigned char *stg = smem + s * 2 * TC_TILE_BYTES;
+            float p = 0.f;
+#pragma unroll
+            for (int c = 0; c < TC_KT / 4; c++) {
+                const float4 x = *(const float4 *)(stg + ((((tid >> 3) * (TC_KT / 4) + c) << 7) + ((tid & 7) << 4)));
+                p = fmaf(x.x, x.x, p);
+                p = fmaf(x.y, x.y, p);
+                p = fmaf(x.z, x.z, p);
+                p = fmaf(x.w, x.w, p);
+            }
+            a2 += p;
+        }
         if (tid == 0 && !(dbg & 2)) {
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
             const uint32_t st = sbase + s * 2 * TC_TILE_BYTES;
@@ -157,6 +182,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
 #pragma unroll
         for (int j = 0; j < 32; j++) tile[r * TS + c0 + j] = ((dbg & 2) || nk == 0) ? 0.f : __uint_as_float(v[j]);
     }
+    tile[r * TS + TC_N] = a2;
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
     const int split = gridDim.z;
     cg::cluster_group cluster = cg::this_cluster();
@@ -173,6 +199,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
         const int a = ta + rr;
         if (a >= nA) continue;
         float4 dot = make_float4(0.f, 0.f, 0.f, 0.f);
+        float fa2 = 0.f;
 #pragma unroll
         for (int q = 0; q < 8; q++) {
             if (q < split) {
@@ -181,10 +208,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
                 dot.y += x.y;
                 dot.z += x.z;
                 dot.w += x.w;
+                fa2 += part[q][rr * TS + TC_N];
             }
         }
-        const float fa = fnorm[a0 + a];
-        const float fa2 = fa * fa;
+        if (c == 0 && fnorm_out) fnorm_out[a0 + a] = sqrtf(fa2);
         float *o = out + (int64_t)a * ld + tb + c;
         const float d4[4] = {dot.x, dot.y, dot.z, dot.w};
 #pragma unroll
@@ -200,7 +227,7 @@ size_t screen_tc_smem() { return (size_t)TC_STAGES * 2 * TC_TILE_BYTES; }
 
 void launch_screen_tc(int nA, int64_t a0, const char *const *frow, const float *fnorm, int D, const int64_t *nB_dev,
                       int nB_max, const float *C32, const int32_t *snap, const float *cn2, float *out, int64_t ld,
-                      cudaStream_t st) {
+                      cudaStream_t st, float *fnorm_out) {
     static bool attr = false;
     if (!attr) {
         FX_CUDA(cudaFuncSetAttribute(k_screen_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)screen_tc_smem()));
@@ -227,7 +254,8 @@ void launch_screen_tc(int nA, int64_t a0, const char *const *frow, const float *
     at[0].val.clusterDim.z = (unsigned)split;
     lc.attrs = at;
     lc.numAttrs = 1;
-    FX_CUDA(cudaLaunchKernelEx(&lc, k_screen_tc, nA, a0, frow, fnorm, D, nB_dev, C32, snap, cn2, out, ld, kchunk, dbg));
+    FX_CUDA(cudaLaunchKernelEx(&lc, k_screen_tc, nA, a0, frow, fnorm, D, nB_dev, C32, snap, cn2, out, ld, kchunk, dbg,
+                               fnorm_out));
     FX_LAUNCHED();
 }
 
@@ -279,7 +307,7 @@ extern "C" int fx_debug_screen_tc(int32_t device, int64_t na, int64_t nb, int32_
         k_iota32<<<(unsigned)cdiv(nb, 256), 256>>>(nb, snap.p);
         k_sqrt_inplace<<<(unsigned)cdiv(na, 256), 256>>>(na, nA2.p);  // fnorm = ||a||
         FX_LAUNCHED();
-        launch_screen_tc((int)na, 0, rows.p, nA2.p, dim, nbd.p, (int)nb, dB.p, snap.p, nB2.p, dout.p, nb, st);
+        launch_screen_tc((int)na, 0, rows.p, nA2.p, dim, nbd.p, (int)nb, dB.p, snap.p, nB2.p, dout.p, nb, st, nullptr);
         FX_CUDA(cudaDeviceSynchronize());
         FX_CUDA(cudaMemcpy(out, dout.p, sizeof(float) * na * nb, cudaMemcpyDeviceToHost));
     } catch (const Error &e) {
