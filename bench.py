@@ -245,8 +245,14 @@ def main():
     ms_per_step = t_ms / args.steps
     value = W["n"] * ws * args.steps / (t_ms / 1e3)
     rep = reports[-1]
-    phases = last.timings()
-    counters = last.counters()
+    # per-phase breakdown from one extra, instrumented run of the same step
+    # (the timed steps run without the phase events, which sit between kernels)
+    inst = make_stream()
+    inst.set_timing(True)
+    step(inst)
+    phases = inst.timings()
+    counters = inst.counters()
+    del inst
 
     # roofline: algorithmic bytes per launch / average launch
     # duration from the library's CUDA events on its own stream.  The headline

@@ -270,6 +270,9 @@ int64_t fx_kernel_launches(void);
  * out[2] K2 resolve, out[3] K2 fold, out[4] seal, out[5] index build (K3),
  * out[6] number of clustering batches. */
 int fx_stream_timings(fx_stream *s, double *out, int n);
+/* Per-phase timers are off by default (their events sit between kernels);
+ * on = 1 records them for every later batch (also FOCUS_B200_TIMERS=1). */
+int fx_stream_set_timing(fx_stream *s, int32_t on);
 /* Engine counters: live, clusters, distance_computations, ... (see
  * fx_handles.cuh Ctr); out[i] for i < n. */
 int fx_stream_counters(fx_stream *s, int64_t *out, int n);

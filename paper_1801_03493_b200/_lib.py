@@ -76,6 +76,7 @@ _SIGS = {
     "fx_finalize": (ctypes.c_int, [vp, ctypes.POINTER(vp), ctypes.POINTER(IngestReportC)]),
     "fx_stream_object_results": (ctypes.c_int, [vp, c_i32p, c_u8p, c_i32p]),
     "fx_stream_timings": (ctypes.c_int, [vp, c_f64p, ctypes.c_int]),
+    "fx_stream_set_timing": (ctypes.c_int, [vp, ctypes.c_int32]),
     "fx_stream_counters": (ctypes.c_int, [vp, c_i64p, ctypes.c_int]),
     "fx_stream_cuda_stream": (ctypes.c_void_p, [vp]),
     "fx_debug_screen_tc": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32, vp, vp,

@@ -85,6 +85,7 @@ using namespace fx;
 // ---------------------------------------------------------------------------
 
 void fx_stream::tstart(int phase) {
+    if (!timing) return;
     int idx = -1;
     for (size_t i = 0; i < timers.size(); i++) {
         if (timers[i].phase < 0) {
@@ -104,7 +105,7 @@ void fx_stream::tstart(int phase) {
     open_timer = idx;
 }
 void fx_stream::tstop() {
-    if (open_timer < 0) return;
+    if (!timing || open_timer < 0) return;
     FX_CUDA(cudaEventRecord(timers[open_timer].b, st));
     pending.push_back(open_timer);
     open_timer = -1;
@@ -191,6 +192,8 @@ int fx_stream_create(const fx_stream_config *cfg, fx_stream **out) {
                 s->tc_screen = !simt && cfg->feat_type == FX_F32 && cfg->dim % 4 == 0;
                 const char *chk = getenv("FOCUS_B200_CHECK");
                 s->debug_check = chk && strcmp(chk, "1") == 0;
+                const char *tm = getenv("FOCUS_B200_TIMERS");
+                s->timing = tm && strcmp(tm, "1") == 0;
             }
             FX_CUDA(cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking));
             cur_stream() = s->st;
@@ -737,6 +740,13 @@ int fx_stream_timings(fx_stream *s, double *out, int n) {
         StreamGuard sg_(s->st);
         s->tcollect();
         for (int i = 0; i < n && i < 16; i++) out[i] = s->t_ms[i];
+    })
+}
+
+int fx_stream_set_timing(fx_stream *s, int32_t on) {
+    FX_GUARD({
+        if (!s) throw Error{FX_E_USAGE, "null stream"};
+        s->timing = on != 0;
     })
 }
 

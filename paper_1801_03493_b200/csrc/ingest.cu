@@ -344,6 +344,7 @@ struct ResolveArgs {
     int batch_no;
     const int32_t *sum_slot, *sum_q;
     const float *sum_d1, *sum_e1, *sum_lbr;
+    int64_t *h_ring;  // pinned host slot (UVA): counters the host reads two batches later
 };
 
 constexpr int RS_THREADS = 512;
@@ -1583,7 +1584,13 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
         ctr[C_NINSERTED] = s_inserted;
         ctr[C_LAST_CID] = A.s_cid[sh_slot_of[B - 1]];
         ctr[C_NRES] = 0;
+        if (A.h_ring) {  // zero-copy readback (no memcpy in the stream)
+            A.h_ring[C_NEXT_CID] = s_next_cid;
+            __threadfence_system();
+        }
     }
+    // the fold re-accumulates ||c||^2 of the slots it refreshes
+    for (int i = tid; i < s_ndirty; i += blockDim.x) A.s_cn2[A.dirty[i]] = 0.f;
 }
 
 // ---------------------------------------------------------------------------
@@ -1759,11 +1766,6 @@ __global__ void __launch_bounds__(FOLD_THREADS) k_fold(int D, int64_t c0, const 
     }
 }
 
-__global__ void k_zero_cn2(const int64_t *__restrict__ ctr, const int32_t *__restrict__ dirty, float *__restrict__ s_cn2) {
-    // (grid sized for the maximum dirty count; the device count bounds it)
-    int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < (int)ctr[C_NDIRTY]) s_cn2[dirty[i]] = 0.f;
-}
 
 // finalize: live clusters' final centroids and sizes
 __global__ void k_final_live(int D, const int64_t *__restrict__ ctr, const int32_t *__restrict__ live,
@@ -1850,7 +1852,8 @@ __global__ void k_seal_pick(int64_t nfeat_total, const int32_t *__restrict__ fme
 
 void launch_screen_tc(int nA, int64_t a0, const char *const *frow, const float *fnorm, int D, const int64_t *nB_dev,
                       int nB_max, const float *C32, const int32_t *snap, const float *cn2, float *out, int64_t ld,
-                      cudaStream_t st, float *fnorm_out);
+                      cudaStream_t st, float *fnorm_out, ScreenModel sm, double T, int32_t *res_col,
+                      int32_t *res_pos, int64_t *nres);
 int64_t scan_i32_to_i64(const int32_t *in, int64_t n, int64_t *out_excl, cudaStream_t st, int64_t *scratch_total);
 void scan_u8_to_i64(const uint8_t *in, int64_t n, int invert, int64_t *out_excl, int64_t *d_total, cudaStream_t st);
 
@@ -1891,11 +1894,15 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
         B = (int)std::min<int64_t>(std::min<int64_t>(s->B, cap), c_end - c0);
         s->t_ms[6] += 1.0;
         // 1. snapshot screen
+        bool fused_res = false;
         s->tstart(1);
         if (s->tc_screen) {
             // the screen also produces ||f|| of the batch rows (fnorm) unless an earlier pass did
+            // fused: residual detection when the snapshot fits one column tile
+            fused_res = s->ld <= 128;
             launch_screen_tc(B, c0, s->frow.p, s->fnorm.p, D, s->ctr.p + C_NSNAP, (int)s->ld, s->C32.p,
-                             s->snap_slot.p, s->s_cn2.p, s->dist.p, s->ld, st, s->has_fc ? nullptr : s->fnorm.p);
+                             s->snap_slot.p, s->s_cn2.p, s->dist.p, s->ld, st, s->has_fc ? nullptr : s->fnorm.p, sm,
+                             s->cfg.t, fused_res ? s->res_col.p : nullptr, s->res_pos.p, s->ctr.p + C_NRES);
         } else {
             const unsigned grid = (unsigned)std::min<int64_t>(cdiv(s->ld, SC_T) * cdiv(B, SC_T), 148 * 8);
             FromSnapshot fb{s->C32.p, s->snap_slot.p, D};
@@ -1907,10 +1914,12 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
         s->tstart(7);  // residual detection + columns
         // 2. residuals + their in-batch columns
         {
-            k_residuals<<<(unsigned)cdiv((int64_t)B * 32, 256), 256, 0, st>>>(
-                B, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p, s->snap_slot.p, s->fnorm.p, c0, sm, s->cfg.t,
-                s->res_col.p, s->res_pos.p, s->ctr.p + C_NRES);
-            FX_LAUNCHED();
+            if (!fused_res) {
+                k_residuals<<<(unsigned)cdiv((int64_t)B * 32, 256), 256, 0, st>>>(
+                    B, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p, s->snap_slot.p, s->fnorm.p, c0, sm, s->cfg.t,
+                    s->res_col.p, s->res_pos.p, s->ctr.p + C_NRES);
+                FX_LAUNCHED();
+            }
             const bool rc_ok = D <= 6144;  // RC_COLS staged rows fit in shared memory
             if (rc_ok && !rowpass) {
                 const size_t smem = sizeof(float) * RC_COLS * D;
@@ -2016,6 +2025,7 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             A.sum_d1 = s->sum_d1.p;
             A.sum_e1 = s->sum_e1.p;
             A.sum_lbr = s->sum_lbr.p;
+            A.h_ring = s->h_ctr_ring + (s->batch_no % 3) * C_COUNT;
             const PwPlan &P = *s->plan_host;
             size_t smem = resolve_smem(s->B, P);
             auto kern = k_resolve<T>;
@@ -2035,9 +2045,7 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
         //    without a per-batch host sync: each batch creates <= B clusters, so
         //    the count read back (asynchronously) two batches ago + 3B bounds it.
         {
-            const int slot_k = (int)(s->batch_no % 3);
-            FX_CUDA(cudaMemcpyAsync(s->h_ctr_ring + slot_k * C_COUNT, s->ctr.p, sizeof(int64_t) * C_COUNT,
-                                    cudaMemcpyDeviceToHost, st));
+            const int slot_k = (int)(s->batch_no % 3);  // written by the resolve itself (A.h_ring)
             FX_CUDA(cudaEventRecord(s->ring_ev[slot_k], st));
             int64_t known = 0;
             if (s->batch_no >= 2) {
@@ -2110,8 +2118,6 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
         // 5. fold (persistent grid over the batch's dirty slots)
         {
             s->tstart(3);
-            k_zero_cn2<<<(unsigned)cdiv(2 * s->B + 2, 256), 256, 0, st>>>(s->ctr.p, s->dirty.p, s->s_cn2.p);
-            FX_LAUNCHED();
             // enough CTA rows for the usual dirty count; the kernel loops over the rest
             const int64_t gx = cdiv(D, FD);
             const int64_t gy = std::max<int64_t>(8, std::min<int64_t>(2 * (int64_t)B + 1, (148 * 12) / gx));

@@ -37,26 +37,35 @@ constexpr int TC_TILE_BYTES = TC_M * TC_KT * 4;  // 16 KB per operand per stage
 
 // out[a][q] = ||A_a||^2 + ||B_q||^2 - 2 A_a.B_q   (float, not clamped)
 __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0, const char *const *__restrict__ frow,
-                                                           const float *__restrict__ fnorm, int D,
+                                                           const float *fnorm, int D,  // aliases fnorm_out
                                                            const int64_t *__restrict__ nB_dev,
                                                            const float *__restrict__ C32,
                                                            const int32_t *__restrict__ snap,
                                                            const float *__restrict__ cn2, float *__restrict__ out,
-                                                           int64_t ld, int kchunk, int dbg, float *__restrict__ fnorm_out) {
+                                                           int64_t ld, int kchunk, int dbg, float *__restrict__ fnorm_out,
+                                                           ScreenModel sm, double T, int32_t *__restrict__ res_col,
+                                                           int32_t *__restrict__ res_pos, int64_t *__restrict__ nres) {
     // blockIdx.z selects the K range [z*kchunk, (z+1)*kchunk) (split-K when the
     // tile grid alone cannot fill the machine; partials are atomically added)
     const int nB = (int)*nB_dev;
     const int tb = blockIdx.x * TC_N, ta = blockIdx.y * TC_M;
-    if (nB == 0 && fnorm_out && blockIdx.x == 0 && blockIdx.z == 0 && ta + (int)threadIdx.x < nA) {
+    if (nB == 0 && blockIdx.x == 0 && blockIdx.z == 0 && ta + (int)threadIdx.x < nA) {
         // empty snapshot (stream start): no screen, but the batch still needs ||f||
-        const float *row = (const float *)frow[a0 + ta + threadIdx.x];
-        float tot = 0.f;
-        for (int k0 = 0; k0 < D; k0 += TC_KT) {
-            float p = 0.f;
-            for (int k = k0; k < min(D, k0 + TC_KT); k++) p = fmaf(row[k], row[k], p);
-            tot += p;
+        if (fnorm_out) {
+            const float *row = (const float *)frow[a0 + ta + threadIdx.x];
+            float tot = 0.f;
+            for (int k0 = 0; k0 < D; k0 += TC_KT) {
+                float p = 0.f;
+                for (int k = k0; k < min(D, k0 + TC_KT); k++) p = fmaf(row[k], row[k], p);
+                tot += p;
+            }
+            fnorm_out[a0 + ta + threadIdx.x] = sqrtf(tot);
         }
-        fnorm_out[a0 + ta + threadIdx.x] = sqrtf(tot);
+        if (res_col) {  // no live cluster: every object is a probable seed
+            const int col = (int)atomicAdd((unsigned long long *)nres, 1ull);
+            res_pos[col] = ta + threadIdx.x;
+            res_col[ta + threadIdx.x] = col;
+        }
     }
     if (tb >= nB || ta >= nA) return;
     extern __shared__ __align__(1024) unsigned char smem[];
@@ -218,6 +227,32 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
         for (int j = 0; j < 4; j++)
             if (c + j < ncol) o[j] = fa2 + cn2[snap[tb + c + j]] - 2.f * d4[j];
     }
+    if (res_col) {
+        // fused residual detection (one column tile = the whole snapshot):
+        // objects with no snapshot centroid whose lower bound is <= T
+        __syncthreads();  // this CTA's rows of `out` and fnorm are written
+        for (int rr = rank * rows_per + warp; rr < (rank + 1) * rows_per; rr += TC_THREADS / 32) {
+            const int a = ta + rr;
+            if (a >= nA) continue;
+            const float fn = fnorm[a0 + a];  // written above by this CTA (or by the norm pass)
+            float mn = INFINITY;
+            for (int q = lane; q < nB; q += 32) {
+                float lb, ub;
+                snap_bounds(sm, out[(int64_t)a * ld + q], sqrtf(cn2[snap[q]]) * 1.00001f, fn, lb, ub);
+                mn = fminf(mn, lb);
+            }
+            mn = warp_min(mn);
+            if (lane == 0) {
+                if ((double)mn > T) {
+                    const int col = (int)atomicAdd((unsigned long long *)nres, 1ull);
+                    res_pos[col] = a;
+                    res_col[a] = col;
+                } else {
+                    res_col[a] = -1;
+                }
+            }
+        }
+    }
     cluster.sync();  // keep this CTA's shared memory alive until every CTA of the cluster has read it
     __syncthreads();
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TC_N));
@@ -227,7 +262,9 @@ size_t screen_tc_smem() { return (size_t)TC_STAGES * 2 * TC_TILE_BYTES; }
 
 void launch_screen_tc(int nA, int64_t a0, const char *const *frow, const float *fnorm, int D, const int64_t *nB_dev,
                       int nB_max, const float *C32, const int32_t *snap, const float *cn2, float *out, int64_t ld,
-                      cudaStream_t st, float *fnorm_out) {
+                      cudaStream_t st, float *fnorm_out, ScreenModel sm, double T, int32_t *res_col,
+                      int32_t *res_pos, int64_t *nres) {
+    if (nB_max > TC_N) res_col = nullptr;  // fused residual detection needs the whole snapshot in one tile
     static bool attr = false;
     if (!attr) {
         FX_CUDA(cudaFuncSetAttribute(k_screen_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)screen_tc_smem()));
@@ -255,7 +292,7 @@ void launch_screen_tc(int nA, int64_t a0, const char *const *frow, const float *
     lc.attrs = at;
     lc.numAttrs = 1;
     FX_CUDA(cudaLaunchKernelEx(&lc, k_screen_tc, nA, a0, frow, fnorm, D, nB_dev, C32, snap, cn2, out, ld, kchunk, dbg,
-                               fnorm_out));
+                               fnorm_out, sm, T, res_col, res_pos, nres));
     FX_LAUNCHED();
 }
 
@@ -307,7 +344,8 @@ extern "C" int fx_debug_screen_tc(int32_t device, int64_t na, int64_t nb, int32_
         k_iota32<<<(unsigned)cdiv(nb, 256), 256>>>(nb, snap.p);
         k_sqrt_inplace<<<(unsigned)cdiv(na, 256), 256>>>(na, nA2.p);  // fnorm = ||a||
         FX_LAUNCHED();
-        launch_screen_tc((int)na, 0, rows.p, nA2.p, dim, nbd.p, (int)nb, dB.p, snap.p, nB2.p, dout.p, nb, st, nullptr);
+        launch_screen_tc((int)na, 0, rows.p, nA2.p, dim, nbd.p, (int)nb, dB.p, snap.p, nB2.p, dout.p, nb, st, nullptr,
+                         ScreenModel{}, 0.0, nullptr, nullptr, nullptr);
         FX_CUDA(cudaDeviceSynchronize());
         FX_CUDA(cudaMemcpy(out, dout.p, sizeof(float) * na * nb, cudaMemcpyDeviceToHost));
     } catch (const Error &e) {

@@ -124,6 +124,10 @@ class Stream:
               "host_screen", "host_resolve", "host_ring", "host_fold", "host_grow", "host_k0", "host_k1",
               "screen_summary")
 
+    def set_timing(self, on: bool = True) -> None:
+        """Record per-phase CUDA-event timers (off by default: they add gaps)."""
+        _lib.check(self.L.fx_stream_set_timing(self.handle, 1 if on else 0))
+
     def counters(self) -> dict:
         out = np.zeros(len(self.COUNTERS), np.int64)
         _lib.check(self.L.fx_stream_counters(self.handle, _lib.p64(out), out.size))

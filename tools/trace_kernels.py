@@ -42,3 +42,19 @@ tot = sum(v[1] for v in agg.values())
 print(f"total kernel/memcpy time {tot / 1e3:.2f} ms")
 for k, v in sorted(agg.items(), key=lambda x: -x[1][1])[:25]:
     print(f"{k[:60]:60s} {v[0]:6d} {v[1] / 1e3:9.3f} ms  avg {v[1] / v[0]:8.2f} us")
+
+# idle gaps between consecutive device activities (the engine runs on one stream)
+ev = sorted([(e.time_range.start, e.time_range.end, e.name.split("(")[0].replace("void ", ""))
+             for e in p.events() if e.device_type == torch.autograd.DeviceType.CUDA], key=lambda x: x[0])
+gaps = collections.defaultdict(lambda: [0, 0.0])
+span = ev[-1][1] - ev[0][0] if ev else 0
+for a, b in zip(ev, ev[1:]):
+    g = b[0] - a[1]
+    if g > 0:
+        key = f"{a[2][:28]} -> {b[2][:28]}"
+        gaps[key][0] += 1
+        gaps[key][1] += g
+tg = sum(v[1] for v in gaps.values())
+print(f"\ndevice span {span / 1e3:.2f} ms, idle gaps {tg / 1e3:.2f} ms")
+for k, v in sorted(gaps.items(), key=lambda x: -x[1][1])[:15]:
+    print(f"{k:62s} {v[0]:6d} {v[1] / 1e3:8.3f} ms  avg {v[1] / v[0]:7.2f} us")
