@@ -203,6 +203,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
     const float *part[8];
 #pragma unroll
     for (int q = 0; q < 8; q++) part[q] = q < split ? cluster.map_shared_rank(tile, q) : tile;
+    __shared__ int rowmin[TC_M];  // min screen lower bound per row (non-negative float bits)
+    for (int i = tid; i < TC_M; i += TC_THREADS) rowmin[i] = 0x7f800000;  // +inf
+    __syncthreads();
     for (int e = tid; e < rows_per * nc4; e += TC_THREADS) {
         const int rr = rank * rows_per + e / nc4, c = (e % nc4) * 4;
         const int a = ta + rr;
@@ -223,33 +226,35 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
         if (c == 0 && fnorm_out) fnorm_out[a0 + a] = sqrtf(fa2);
         float *o = out + (int64_t)a * ld + tb + c;
         const float d4[4] = {dot.x, dot.y, dot.z, dot.w};
+        float mn = INFINITY;
+        const float fn = sqrtf(fa2);
 #pragma unroll
         for (int j = 0; j < 4; j++)
-            if (c + j < ncol) o[j] = fa2 + cn2[snap[tb + c + j]] - 2.f * d4[j];
+            if (c + j < ncol) {
+                const float c2 = cn2[snap[tb + c + j]];
+                const float v = fa2 + c2 - 2.f * d4[j];
+                o[j] = v;
+                if (res_col) {
+                    float lb, ub;
+                    snap_bounds(sm, v, sqrtf(c2) * 1.00001f, fnorm_out ? fn : fnorm[a0 + a], lb, ub);
+                    mn = fminf(mn, lb);
+                }
+            }
+        if (res_col) atomicMin(&rowmin[rr], __float_as_int(fmaxf(mn, 0.f)));
     }
     if (res_col) {
         // fused residual detection (one column tile = the whole snapshot):
         // objects with no snapshot centroid whose lower bound is <= T
-        __syncthreads();  // this CTA's rows of `out` and fnorm are written
-        for (int rr = rank * rows_per + warp; rr < (rank + 1) * rows_per; rr += TC_THREADS / 32) {
+        __syncthreads();
+        for (int rr = rank * rows_per + tid; rr < (rank + 1) * rows_per; rr += TC_THREADS) {
             const int a = ta + rr;
             if (a >= nA) continue;
-            const float fn = fnorm[a0 + a];  // written above by this CTA (or by the norm pass)
-            float mn = INFINITY;
-            for (int q = lane; q < nB; q += 32) {
-                float lb, ub;
-                snap_bounds(sm, out[(int64_t)a * ld + q], sqrtf(cn2[snap[q]]) * 1.00001f, fn, lb, ub);
-                mn = fminf(mn, lb);
-            }
-            mn = warp_min(mn);
-            if (lane == 0) {
-                if ((double)mn > T) {
-                    const int col = (int)atomicAdd((unsigned long long *)nres, 1ull);
-                    res_pos[col] = a;
-                    res_col[a] = col;
-                } else {
-                    res_col[a] = -1;
-                }
+            if ((double)__int_as_float(rowmin[rr]) > T) {
+                const int col = (int)atomicAdd((unsigned long long *)nres, 1ull);
+                res_pos[col] = a;
+                res_col[a] = col;
+            } else {
+                res_col[a] = -1;
             }
         }
     }
