@@ -1537,34 +1537,79 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
 
     // ---- epilogue: pending-member CSR for k_fold, snapshot for next batch
     __syncthreads();
-    if (tid == 0) {
-        // the slot with the most pending rows goes first (k_fold gives it its own grid row)
-        int best = 0, bc = -1;
-        for (int i = 0; i < s_ndirty; i++) {
+    {
+        // pending counts of the dirty slots (parallel loads), the largest slot
+        // moved first (k_fold gives it its own grid row), offsets by a scan
+        int *cnt = mlist;  // mlist + seg_key: 2 * BC ints of scratch, >= the dirty count
+        const int nd = s_ndirty;
+        int bc = -1, bi = 0;
+        for (int i = tid; i < nd; i += blockDim.x) {
             const int c = A.s_pend[A.dirty[i]];
+            cnt[i] = c;
             if (c > bc) {
                 bc = c;
-                best = i;
+                bi = i;
             }
         }
-        if (best > 0) {
-            const int a0 = A.dirty[0], a1 = A.dirty[best];
-            A.dirty[0] = a1;
-            A.dirty[best] = a0;
-            A.s_didx[a1] = 0;
-            A.s_didx[a0] = best;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) {
+            const int oc = __shfl_xor_sync(0xffffffffu, bc, o), oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (oc > bc || (oc == bc && oi < bi)) {
+                bc = oc;
+                bi = oi;
+            }
         }
-        int acc = 0;
-        for (int i = 0; i < s_ndirty; i++) {
-            A.dirty_off[i] = acc;
-            acc += A.s_pend[A.dirty[i]];
+        if (lane == 0) {
+            wsv[wid] = bc;
+            wsh[wid] = bi;
         }
-        A.dirty_off[s_ndirty] = acc;
-    }
-    __syncthreads();
-    for (int bb = tid; bb < B; bb += blockDim.x) {
-        const int slot = sh_slot_of[bb];
-        A.pend_list[A.dirty_off[A.s_didx[slot]] + A.pend_rank[bb]] = bb;
+        __syncthreads();
+        if (tid == 0) {
+            int best = 0, bcc = -1;
+            for (int w = 0; w < RS_WARPS; w++)
+                if (wsv[w] > bcc || (wsv[w] == bcc && wsh[w] < best)) {
+                    bcc = wsv[w];
+                    best = wsh[w];
+                }
+            if (best > 0 && nd > 0) {
+                const int a0 = A.dirty[0], a1 = A.dirty[best];
+                A.dirty[0] = a1;
+                A.dirty[best] = a0;
+                A.s_didx[a1] = 0;
+                A.s_didx[a0] = best;
+                const int t = cnt[0];
+                cnt[0] = cnt[best];
+                cnt[best] = t;
+            }
+        }
+        __syncthreads();
+        if (wid == 0) {  // exclusive scan of the counts
+            int run = 0;
+            for (int i0 = 0; i0 < nd; i0 += 32) {
+                const int i = i0 + lane;
+                const int c = i < nd ? cnt[i] : 0;
+                int x = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const int y = __shfl_up_sync(0xffffffffu, x, o);
+                    if (lane >= o) x += y;
+                }
+                if (i < nd) {
+                    A.dirty_off[i] = run + x - c;
+                    cnt[i] = run + x - c;
+                }
+                run += __shfl_sync(0xffffffffu, x, 31);
+            }
+            if (lane == 0) A.dirty_off[nd] = run;
+        }
+        __syncthreads();
+        const int32_t *__restrict__ s_didx = A.s_didx;
+        const int32_t *__restrict__ pend_rank = A.pend_rank;
+        int32_t *__restrict__ pend_list = A.pend_list;
+        for (int bb = tid; bb < B; bb += blockDim.x) {
+            const int slot = sh_slot_of[bb];
+            pend_list[cnt[s_didx[slot]] + pend_rank[bb]] = bb;
+        }
     }
     for (int q = tid; q < s_L; q += blockDim.x) A.snap_slot[q] = A.live[q];
     __syncthreads();
