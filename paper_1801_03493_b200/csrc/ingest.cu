@@ -697,7 +697,10 @@ __global__ void __launch_bounds__(256) k_rowpass(int nA, int64_t a0, const char 
 }
 
 constexpr int RS_MAXGRP = 512;
-constexpr int RS_RANKW = 8;  // warps that rank a window (per-warp group counters)
+constexpr int RS_RANKW = 8;
+#ifndef RS_UB_SCAN
+#define RS_UB_SCAN 1  // 0: i*U instead of per-object prefix sums of hypothesis bounds (tighter drift, one more scan)
+#endif  // warps that rank a window (per-warp group counters)
 constexpr int RS_WCNT_BYTES = RS_RANKW * RS_MAXGRP * 2;
 constexpr int RS_WIN0 = 64;
 
@@ -1040,10 +1043,11 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
             // per object: sum of the hypothesis bounds of the group's earlier
             // members (segmented exclusive scan over glist, fp32 rounded up)
             const int nlist = ngrp ? grp_off[ngrp - 1] + grp_cnt[ngrp - 1] : 0;
-            seg_scan_ub(nlist, glist, seg_grp, seg_ub0, seg_P, wsf, wsh);
+            if (RS_UB_SCAN) seg_scan_ub(nlist, glist, seg_grp, seg_ub0, seg_P, wsf, wsh);
             for (int g = tid; g < ngrp; g += blockDim.x) {
                 const int jl = grp_off[g] + grp_cnt[g] - 1;
-                const float Ptot = grp_cnt[g] > 0 ? __fadd_ru(seg_P[jl], seg_ub0[glist[jl]]) : 0.f;
+                const float Ptot = !RS_UB_SCAN ? __fmul_ru((float)grp_cnt[g], grp_U[g])
+                                   : grp_cnt[g] > 0 ? __fadd_ru(seg_P[jl], seg_ub0[glist[jl]]) : 0.f;
                 grp_drift[g] = drift_avg(grp_d0[g], grp_nf0[g], Ptot, grp_cnt[g], grp_cn[g], grp_U[g]);
             }
         }
@@ -1110,8 +1114,8 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
             if (key >= 0 && !overflow) {
                 const int g = seg_grp[p];
                 const int i = seg_nf[p];
-                const double ub = (double)seg_ub0[p] +
-                                  (double)drift_avg(grp_d0[g], grp_nf0[g], seg_P[grp_off[g] + i], i, grp_cn[g], grp_U[g]);
+                const float Pi = RS_UB_SCAN ? seg_P[grp_off[g] + i] : __fmul_ru((float)i, grp_U[g]);
+                const double ub = (double)seg_ub0[p] + (double)drift_avg(grp_d0[g], grp_nf0[g], Pi, i, grp_cn[g], grp_U[g]);
                 const double md = (key == s_md1_slot) ? s_md2 : s_md1;
                 const double lbo = (double)seg_lbr[p] - md * 1.000001;
                 if (lbo > ub) fl = ub <= A.T ? 0 : 1;
@@ -1266,7 +1270,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
                     const int jl = grp_off[g] + n_c - 1;
                     const int dups = mlist[jl] + A.dup_run[A.c0 + glist[jl]];
                     const int pend0 = A.s_pend[sl];
-                    const float Pc = __fadd_ru(seg_P[jl], seg_ub0[glist[jl]]);
+                    const float Pc = RS_UB_SCAN ? __fadd_ru(seg_P[jl], seg_ub0[glist[jl]]) : __fmul_ru((float)n_c, grp_U[g]);
                     A.s_drift[sl] = (double)drift_avg(grp_d0[g], grp_nf0[g], Pc, n_c, grp_cn[g], grp_U[g]);
                     A.s_nfeat[sl] = grp_nf0[g] + n_c;
                     A.s_size[sl] += n_c + dups;
