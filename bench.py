@@ -157,6 +157,8 @@ def main():
     ap.add_argument("--queries", type=int, default=-1, help="classes queried (x3 k_x values); -1 = every class, 0 = skip")
     ap.add_argument("--backend", default="nccl", help="process-group backend for N > 1 (nccl; gloo for checks)")
     ap.add_argument("--no-fc", action="store_true", help="skip the K1b FC head sub-benchmark")
+    ap.add_argument("--multi-streams", type=int, default=8, help="concurrent engines for the C4-shape line (<=1: skip)")
+    ap.add_argument("--multi-objects", type=int, default=1_000_000, help="objects per engine in the C4-shape line")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -376,6 +378,47 @@ def main():
                 "timing": "host wall clock per query (fresh session, ids copied to host), max over ranks"}
         del sess, tix
 
+    # C4 shape on this GPU: several stream engines ingesting concurrently
+    # ("the 1/2/4-GPU points of C4 run 8/4/2 engines per GPU"),
+    # one host thread per engine, each on its own CUDA stream; the streams are
+    # the device-generated stream of this rank with distinct seeds.
+    msres = None
+    if args.multi_streams > 1:
+        from concurrent.futures import ThreadPoolExecutor
+        nms = args.multi_streams
+        nobj = min(W["n"], args.multi_objects)
+        datas = [synth.generate(nobj, dim=W["dim"], vocab=W["vocab"], n_stream_classes=W["n_stream_classes"],
+                                seed=1000 + rank * nms + j) for j in range(nms)]
+        torch.cuda.synchronize()
+
+        def one(j):
+            fx.set_device(local)
+            d = datas[j]
+            sj = fx.ingest.Stream(W["dim"], 16, W["vocab"], W["k"], W["t"], W["m"], 0.01, _lib.FX_F32, local,
+                                  args.batch)
+            sj.set_rank_model(prof, 0)
+            sj.ingest_device(nobj, d.oids.data_ptr(), d.fids.data_ptr(), d.sigs.data_ptr(), d.feats.data_ptr(),
+                             d.true_class.data_ptr())
+            ix, rp = sj.finalize()
+            del ix, sj
+            return rp.objects_seen
+
+        with ThreadPoolExecutor(max_workers=nms) as pool:
+            list(pool.map(one, range(nms)))  # warm-up
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            seen = sum(pool.map(one, range(nms)))
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+        if ws > 1:
+            tt = torch.tensor([dt], device=dev_red)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            dt = float(tt.item())
+        msres = {"streams_per_gpu": nms, "objects_per_stream": nobj, "objects_per_s": seen * ws / dt,
+                 "wall_s": dt, "note": "C4 shape: concurrent engines per GPU (host thread + CUDA stream each), "
+                                       "inputs resident, wall clock, max over ranks"}
+        del datas
+
     # K1b FC classifier head (north star kernel 1) on resident features:
     # logits over V classes, top-K; tensor-pipe roofline against TF32 dense
     fcres = None
@@ -432,7 +475,7 @@ def main():
                        "streams_per_gpu": 1, "parallelism": f"stream-sharded x{ws}",
                        "l2": "inputs (8 GB features/stream) exceed L2; no flush", **W},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
-            "query": qres, "k1b_fc_head": fcres,
+            "query": qres, "k1b_fc_head": fcres, "multi_stream": msres,
             "gpu_launches": int(launches),
             "ingest": {"clusters": rep.clusters_emitted, "classified": rep.objects_classified,
                        "distance_computations": rep.distance_computations, "exact_rechecks": rep.exact_rechecks,
