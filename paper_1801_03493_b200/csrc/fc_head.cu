@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <climits>
+#include <cstdlib>
 
 #include "fx_handles.cuh"
 #include "tc_common.cuh"
@@ -43,7 +44,7 @@ __global__ void __launch_bounds__(FC_THREADS, 1) k_fc_tc(int n, int64_t a0, cons
                                                         const float *__restrict__ fnorm, int D, int V,
                                                         const float *__restrict__ W, const float *__restrict__ wnorm,
                                                         const float *__restrict__ bias, float gamma,
-                                                        FcTile *__restrict__ out) {
+                                                        FcTile *__restrict__ out, int dbg) {
     const int tv = blockIdx.x * FC_N, ta = blockIdx.y * FC_M;
     extern __shared__ __align__(1024) unsigned char smem[];
     __shared__ const float *rowsA[FC_M];
@@ -73,7 +74,7 @@ __global__ void __launch_bounds__(FC_THREADS, 1) k_fc_tc(int n, int64_t a0, cons
     constexpr uint32_t idesc = idesc_tf32(FC_M, FC_N);
     constexpr int SB = FC_A_BYTES + FC_B_BYTES;
     for (int s = 0; s < FC_STAGES - 1; s++) {
-        if (s < nk) {
+        if (s < nk && !(dbg & 1)) {
             load_tile<FC_M, FC_THREADS>(sbase + s * SB, rowsA, s * TC_KT, D, fnorm);
             load_tile<FC_N, FC_THREADS>(sbase + s * SB + FC_A_BYTES, rowsB, s * TC_KT, D, fnorm);
         }
@@ -84,7 +85,7 @@ __global__ void __launch_bounds__(FC_THREADS, 1) k_fc_tc(int n, int64_t a0, cons
         asm volatile("cp.async.wait_group %0;\n" ::"n"(FC_STAGES - 2));
         asm volatile("fence.proxy.async.shared::cta;\n" ::);
         __syncthreads();
-        if (tid == 0) {
+        if (tid == 0 && !(dbg & 2)) {
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
             const uint32_t st = sbase + s * SB;
 #pragma unroll
@@ -103,16 +104,18 @@ __global__ void __launch_bounds__(FC_THREADS, 1) k_fc_tc(int n, int64_t a0, cons
         const int nt = it + FC_STAGES - 1;
         if (nt < nk) {
             const int ns = nt % FC_STAGES;
-            if (nt >= FC_STAGES) mbar_wait(&bar_stage[ns], (uint32_t)(((nt / FC_STAGES) - 1) & 1));
-            load_tile<FC_M, FC_THREADS>(sbase + ns * SB, rowsA, nt * TC_KT, D, fnorm);
-            load_tile<FC_N, FC_THREADS>(sbase + ns * SB + FC_A_BYTES, rowsB, nt * TC_KT, D, fnorm);
+            if (nt >= FC_STAGES && !(dbg & 2)) mbar_wait(&bar_stage[ns], (uint32_t)(((nt / FC_STAGES) - 1) & 1));
+            if (!(dbg & 1)) {
+                load_tile<FC_M, FC_THREADS>(sbase + ns * SB, rowsA, nt * TC_KT, D, fnorm);
+                load_tile<FC_N, FC_THREADS>(sbase + ns * SB + FC_A_BYTES, rowsB, nt * TC_KT, D, fnorm);
+            }
         }
         asm volatile("cp.async.commit_group;\n" ::);
     }
-    if (tid == 0)
+    if (tid == 0 && !(dbg & 2))
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
             smem_u32(&bar_done)));
-    mbar_wait(&bar_done, 0);
+    if (!(dbg & 2)) mbar_wait(&bar_done, 0);
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
 
     // epilogue: thread = object row; keep the FC_KC largest logits (sorted
@@ -190,9 +193,18 @@ __global__ void __launch_bounds__(FC_THREADS, 1) k_fc_tc(int n, int64_t a0, cons
 }
 
 // float64 logit of class v for feature row f (warp-cooperative; result in all lanes)
+// (rows 16-byte aligned, D % 4 == 0: float4 loads, two independent chains per lane)
 __device__ __forceinline__ double fc_logit64(const float *f, const float *w, int D, double b) {
-    double acc = 0.0;
-    for (int k = threadIdx.x & 31; k < D; k += 32) acc = fma((double)f[k], (double)w[k], acc);
+    const float4 *f4 = (const float4 *)f, *w4 = (const float4 *)w;
+    double a0 = 0.0, a1 = 0.0;
+    for (int k = threadIdx.x & 31; k < (D >> 2); k += 32) {
+        const float4 x = __ldg(f4 + k), y = __ldg(w4 + k);
+        a0 = fma((double)x.x, (double)y.x, a0);
+        a1 = fma((double)x.y, (double)y.y, a1);
+        a0 = fma((double)x.z, (double)y.z, a0);
+        a1 = fma((double)x.w, (double)y.w, a1);
+    }
+    double acc = a0 + a1;
 #pragma unroll
     for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     return acc + b;
@@ -208,6 +220,10 @@ __global__ void __launch_bounds__(256) k_fc_merge(int n, int64_t a0, const char 
                                                  int32_t *__restrict__ topk, float *__restrict__ conf,
                                                  uint8_t *__restrict__ flag, unsigned long long *__restrict__ nflag) {
     __shared__ int s_idx[8][FC_MAXC];
+    __shared__ float s_lb[8][FC_MAXC], s_ub[8][FC_MAXC];
+    __shared__ unsigned char s_need[8][FC_MAXC];
+    __shared__ double s_bv[8][17];
+    __shared__ int s_bi[8][17];
     const int wib = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int w = blockIdx.x * 8 + wib;
     if (w >= n) return;
@@ -269,49 +285,75 @@ __global__ void __launch_bounds__(256) k_fc_merge(int n, int64_t a0, const char 
             const unsigned m = __ballot_sync(0xffffffffu, take);
             if (take) {
                 const int pos = ncand + __popc(m & ((1u << lane) - 1u));
-                if (pos < FC_MAXC) s_idx[wib][pos] = cls;
+                if (pos < FC_MAXC) {
+                    const int ti = e / FC_KC, j = e % FC_KC;
+                    const float lv = t[ti].val[j];
+                    const float err = gamma * fn * wnorm[cls] + fabsf(lv) * 2.4e-7f;
+                    s_idx[wib][pos] = cls;
+                    s_lb[wib][pos] = lv - err;
+                    s_ub[wib][pos] = lv + err;
+                }
             }
             ncand += __popc(m);
         }
         if (ncand > FC_MAXC) all = true;
     }
     __syncwarp();
-    // float64 re-score, selection of the top K (+1 for the margin check)
-    double bv[17];
-    int bi[17];
-#pragma unroll
-    for (int j = 0; j < 17; j++) {
-        bv[j] = -DBL_MAX;
-        bi[j] = INT_MAX;
-    }
-    const int K1 = K + 1 < 17 ? K + 1 : 17;
-    auto offer = [&](double x, int xi) {
-#pragma unroll
-        for (int q = 0; q < 17; q++) {
-            if (q < K1 && (x > bv[q] || (x == bv[q] && xi < bi[q]))) {
-                const double tv = bv[q];
-                const int ti = bi[q];
-                bv[q] = x;
-                bi[q] = xi;
-                x = tv;
-                xi = ti;
-            }
+    // only candidates whose TF32 interval overlaps another candidate's need
+    // their float64 value: disjoint intervals are already ordered (and far
+    // outside the float64 margin)
+    if (!all) {
+        for (int c = lane; c < ncand; c += 32) {
+            bool ov = false;
+            for (int o = 0; o < ncand; o++)
+                ov |= o != c && s_lb[wib][o] <= s_ub[wib][c] && s_lb[wib][c] <= s_ub[wib][o];
+            s_need[wib][c] = ov ? 1 : 0;
         }
-    };
+        __syncwarp();
+    }
+    // float64 re-score, selection of the top K (+1 for the margin check):
+    // the sorted list lives in shared memory, lane 0 inserts
+    double *bv = s_bv[wib];
+    int *bi = s_bi[wib];
+    const int K1 = K + 1 < 17 ? K + 1 : 17;
+    if (lane < 17) {
+        bv[lane] = -DBL_MAX;
+        bi[lane] = INT_MAX;
+    }
+    __syncwarp();
     const int nscore = all ? V : ncand;
     for (int c = 0; c < nscore; c++) {
         const int cls = all ? c : s_idx[wib][c];
-        const double l = fc_logit64(f, W + (int64_t)cls * D, D, bias ? (double)bias[cls] : 0.0);
-        offer(l, cls);  // lane 0's value decides (its reduction order is fixed)
+        double l;
+        if (all || s_need[wib][c])
+            l = fc_logit64(f, W + (int64_t)cls * D, D, bias ? (double)bias[cls] : 0.0);
+        else
+            l = 0.5 * ((double)s_lb[wib][c] + (double)s_ub[wib][c]);  // disjoint interval: its order is certain
+        if (lane == 0) {  // lane 0's value decides (its reduction order is fixed)
+            double x = l;
+            int xi = cls;
+            for (int q = 0; q < K1; q++) {
+                if (x > bv[q] || (x == bv[q] && xi < bi[q])) {
+                    const double tv = bv[q];
+                    const int ti = bi[q];
+                    bv[q] = x;
+                    bi[q] = xi;
+                    x = tv;
+                    xi = ti;
+                }
+            }
+        }
+        __syncwarp();
     }
     // margin flag: the float64 error of a logit is <= (D + 8) 2^-53 ||f|| ||w|| + the bias add
     bool flagged = false;
     const double ue = ((double)D + 8.0) * 1.1102230246251565e-16 * (double)fn * 1.0001;
-    for (int q = 0; q + 1 < K1 && q + 1 < nscore; q++) {
-        const double e1 = ue * (double)wnorm[bi[q]] + fabs(bv[q]) * 2.3e-16;
-        const double e2 = ue * (double)wnorm[bi[q + 1]] + fabs(bv[q + 1]) * 2.3e-16;
-        if (bv[q] - bv[q + 1] <= 2.0 * (e1 + e2)) flagged = true;
-    }
+    if (lane == 0)
+        for (int q = 0; q + 1 < K1 && q + 1 < nscore; q++) {
+            const double e1 = ue * (double)wnorm[bi[q]] + fabs(bv[q]) * 2.3e-16;
+            const double e2 = ue * (double)wnorm[bi[q + 1]] + fabs(bv[q + 1]) * 2.3e-16;
+            if (bv[q] - bv[q + 1] <= 2.0 * (e1 + e2)) flagged = true;
+        }
     if (lane == 0) {
         // logsumexp over all classes from the tiles' partials (TF32 logits; confidences only)
         float M = -FLT_MAX;
@@ -359,7 +401,8 @@ void launch_fc_head(int64_t n, int64_t c0, const char *const *frow, const int64_
     for (int64_t b = 0; b < n; b += CH) {
         const int64_t m = std::min<int64_t>(CH, n - b);
         dim3 grid((unsigned)ntile, (unsigned)cdiv(m, FC_M));
-        k_fc_tc<<<grid, FC_THREADS, smem, st>>>((int)m, c0 + b, frow, fnorm, D, V, W, wnorm, bias, gamma, tiles.p);
+        static const int dbg = getenv("FOCUS_B200_FCDBG") ? atoi(getenv("FOCUS_B200_FCDBG")) : 0;
+        k_fc_tc<<<grid, FC_THREADS, smem, st>>>((int)m, c0 + b, frow, fnorm, D, V, W, wnorm, bias, gamma, tiles.p, dbg);
         FX_LAUNCHED();
         k_fc_merge<<<(unsigned)cdiv(m, 8), 256, 0, st>>>((int)m, c0 + b, frow, cls_obj, fnorm, D, V, K, W, wnorm, bias,
                                                         gamma, ntile, tiles.p, topk, conf, flag, nflag);
