@@ -119,9 +119,25 @@ __global__ void __launch_bounds__(FC_THREADS, 1) k_fc_tc(int n, int64_t a0, cons
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
 
     // epilogue: thread = object row; keep the FC_KC largest logits (sorted
-    // descending, ties -> smaller class id) in registers
+    // descending, ties -> smaller class id) in registers.  The tail (largest
+    // upper bound of a dropped class) uses the largest logit dropped and the
+    // tile's largest ||w|| (one max per logit); the logsumexp partial is a
+    // second pass over TMEM once the row maximum is known (no exp chain).
     const int a = ta + warp * 32 + lane;
     const float fn = a < n ? fnorm[a0 + a] : 0.f;
+    __shared__ float s_wmax[FC_THREADS / 32];
+    {
+        float wm = 0.f;
+        for (int c = tid; c < FC_N; c += FC_THREADS)
+            if (tv + c < V) wm = fmaxf(wm, wnorm[tv + c]);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) wm = fmaxf(wm, __shfl_xor_sync(0xffffffffu, wm, o));
+        if (lane == 0) s_wmax[warp] = wm;
+        __syncthreads();
+    }
+    float wmax = 0.f;
+#pragma unroll
+    for (int w = 0; w < FC_THREADS / 32; w++) wmax = fmaxf(wmax, s_wmax[w]);
     float kv[FC_KC];
     int ki[FC_KC];
 #pragma unroll
@@ -129,9 +145,8 @@ __global__ void __launch_bounds__(FC_THREADS, 1) k_fc_tc(int n, int64_t a0, cons
         kv[j] = -FLT_MAX;
         ki[j] = -1;
     }
-    float tail = -FLT_MAX, m = -FLT_MAX, ssum = 0.f;
-    for (int c0 = 0; c0 < FC_N; c0 += 32) {
-        uint32_t v[32];
+    float dropped = -FLT_MAX;
+    auto tmem_row = [&](int c0, uint32_t *v) {
         const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
@@ -142,24 +157,18 @@ __global__ void __launch_bounds__(FC_THREADS, 1) k_fc_tc(int n, int64_t a0, cons
               "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
+    };
+    for (int c0 = 0; c0 < FC_N; c0 += 32) {
+        uint32_t v[32];
+        tmem_row(c0, v);
 #pragma unroll 4
         for (int j = 0; j < 32; j++) {
             const int cls = tv + c0 + j;
             if (a >= n || cls >= V) break;
-            const float l = __uint_as_float(v[j]) + (bias ? bias[cls] : 0.f);
-            // logsumexp partial (confidences only)
-            if (l > m) {
-                ssum = ssum * __expf(m - l) + 1.f;
-                m = l;
-            } else {
-                ssum += __expf(l - m);
-            }
-            float x = l;
+            float x = __uint_as_float(v[j]) + (bias ? bias[cls] : 0.f);
             int xi = cls;
             if (x > kv[FC_KC - 1]) {
-                // the dropped element's upper bound feeds the tail
-                const int di = ki[FC_KC - 1];
-                if (di >= 0) tail = fmaxf(tail, kv[FC_KC - 1] + gamma * fn * wnorm[di] + fabsf(kv[FC_KC - 1]) * 2.4e-7f);
+                dropped = fmaxf(dropped, kv[FC_KC - 1]);
 #pragma unroll
                 for (int q = 0; q < FC_KC; q++) {  // insertion, strict > keeps the earlier (smaller) id first
                     if (x > kv[q]) {
@@ -172,10 +181,23 @@ __global__ void __launch_bounds__(FC_THREADS, 1) k_fc_tc(int n, int64_t a0, cons
                     }
                 }
             } else {
-                tail = fmaxf(tail, x + gamma * fn * wnorm[cls] + fabsf(x) * 2.4e-7f);
+                dropped = fmaxf(dropped, x);
             }
         }
     }
+    const float tail = dropped == -FLT_MAX ? -FLT_MAX : dropped + gamma * fn * wmax + fabsf(dropped) * 2.4e-7f;
+    const float m = kv[0];
+    float ssum = 0.f;
+    if (!(dbg & 4))
+        for (int c0 = 0; c0 < FC_N; c0 += 32) {
+            uint32_t v[32];
+            tmem_row(c0, v);
+#pragma unroll
+            for (int j = 0; j < 32; j++) {
+                const int cls = tv + c0 + j;
+                if (a < n && cls < V) ssum += __expf(__uint_as_float(v[j]) + (bias ? bias[cls] : 0.f) - m);
+            }
+        }
     if (a < n) {
         FcTile *o = out + (int64_t)a * gridDim.x + blockIdx.x;
 #pragma unroll
