@@ -32,7 +32,7 @@ namespace cg = cooperative_groups;
 
 namespace fx {
 
-constexpr int TC_M = 128, TC_N = 128, TC_STAGES = 6, TC_THREADS = 128;
+constexpr int TC_M = 128, TC_N = 128, TC_STAGES = 6, TC_THREADS = 256;  // warps 4-7 only help load
 constexpr int TC_TILE_BYTES = TC_M * TC_KT * 4;  // 16 KB per operand per stage
 
 // out[a][q] = ||A_a||^2 + ||B_q||^2 - 2 A_a.B_q   (float, not clamped)
@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
     // tile grid alone cannot fill the machine; partials are atomically added)
     const int nB = (int)*nB_dev;
     const int tb = blockIdx.x * TC_N, ta = blockIdx.y * TC_M;
-    if (nB == 0 && blockIdx.x == 0 && blockIdx.z == 0 && ta + (int)threadIdx.x < nA) {
+    if (nB == 0 && blockIdx.x == 0 && blockIdx.z == 0 && threadIdx.x < TC_M && ta + (int)threadIdx.x < nA) {
         // empty snapshot (stream start): no screen, but the batch still needs ||f||
         if (fnorm_out) {
             const float *row = (const float *)frow[a0 + ta + threadIdx.x];
@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
         asm volatile("cp.async.wait_group %0;\n" ::"n"(TC_STAGES - 2));
         asm volatile("fence.proxy.async.shared::cta;\n" ::);
         __syncthreads();
-        {  // the row norm rides along: row tid's 32 values of this stage (stable until its refill)
+        if (tid < TC_M) {  // the row norm rides along: row tid's 32 values of this stage (stable until its refill)
             const unsigned char *stg = smem + s * 2 * TC_TILE_BYTES;
             float p = 0.f;
 #pragma unroll
@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
     constexpr int TS = TC_N + 4;  // 16-byte aligned rows for the v4 DSMEM reads
     float *tile = (float *)smem;
     const int r = warp * 32 + lane;
-    for (int c0 = 0; c0 < TC_N; c0 += 32) {
+    for (int c0 = 0; c0 < TC_N && warp < TC_M / 32; c0 += 32) {
         uint32_t v[32];
         const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
         asm volatile(
@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
 #pragma unroll
         for (int j = 0; j < 32; j++) tile[r * TS + c0 + j] = ((dbg & 2) || nk == 0) ? 0.f : __uint_as_float(v[j]);
     }
-    tile[r * TS + TC_N] = a2;
+    if (warp < TC_M / 32) tile[r * TS + TC_N] = a2;
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
     const int split = gridDim.z;
     cg::cluster_group cluster = cg::this_cluster();
