@@ -324,7 +324,7 @@ struct ResolveArgs {
     int64_t ld;
     const float *dres;
     int64_t ldr;
-    const int32_t *res_col;
+    const int32_t *res_col, *res_pos;
     float *dod;
     const char *const *frow;
     const float *fnorm;
@@ -819,7 +819,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
     __shared__ int grp_cnt[RS_MAXGRP], grp_off[RS_MAXGRP], grp_ncommit[RS_MAXGRP], grp_nf0[RS_MAXGRP];
     __shared__ int grp_cid[RS_MAXGRP], grp_size0[RS_MAXGRP], grp_pend0[RS_MAXGRP];
     __shared__ float grp_drift[RS_MAXGRP], grp_U[RS_MAXGRP], grp_d0[RS_MAXGRP], grp_cn[RS_MAXGRP];
-    __shared__ int s_ngrp, s_fail;
+    __shared__ int s_ngrp, s_fail, s_wseeds;
     __shared__ double s_md1, s_md2;
     __shared__ int s_md1_slot;
     __shared__ double wmd1[RS_WARPS], wmd2[RS_WARPS];
@@ -836,6 +836,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
         int nd = (int)ctr[C_NDEFER];
         for (int i = 0; i < nd; i++) A.free_stack[s_nfree++] = A.defer_free[i];
         s_ndefer = 0;
+        s_wseeds = 0;
         s_nevict = 0;
         s_nod = 0;
         s_ndirty = 0;
@@ -886,6 +887,13 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
                 if (qkeys) seg_grp[p] = (short)((L > 0) ? A.sum_q[p] : -1);
                 seg_ub0[p] = (d1 + e1) * 1.000001f + 1e-30f;
                 seg_lbr[p] = lbr - fabsf(lbr) * 1e-6f - 1e-30f;
+                const float lball = (L > 0) ? fminf(d1 - e1, lbr) : INFINITY;
+                if (A.res_col[p] >= 0 && (double)lball > A.T) {
+                    // probable seed: no candidate can join it; kept out of the groups
+                    seg_key[p] = -1;
+                    if (qkeys) seg_grp[p] = -1;
+                    seg_lbr[p] = lball - fabsf(lball) * 1e-6f - 1e-30f;
+                }
             }
         } else
         for (int p = b + tid; p < e_end; p += blockDim.x) {
@@ -932,6 +940,11 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
             seg_key[p] = (L > 0) ? j1 : -1;
             seg_ub0[p] = (d1 + e1) * 1.000001f + 1e-30f;
             seg_lbr[p] = lbr - fabsf(lbr) * 1e-6f - 1e-30f;
+            const float lball = (L > 0) ? fminf(d1 - e1, lbr) : INFINITY;
+            if (A.res_col[p] >= 0 && (double)lball > A.T) {  // probable seed (see above)
+                seg_key[p] = -1;
+                seg_lbr[p] = lball - fabsf(lball) * 1e-6f - 1e-30f;
+            }
         }
         for (int g = tid; g < RS_MAXGRP; g += blockDim.x) {
             grp_cnt[g] = 0;
@@ -1108,17 +1121,46 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
         }
         // pass D: certainty check -> 0 certain, 1 only the T test is open
         // (confirmable by one exact distance), 2 anything else
+        //         3 certain seed (no live centroid and no earlier probable seed of
+        //         this window within T; the window's seeds keep L <= M).
+        //         Probable seeds earlier in the window are candidates of every
+        //         later object: their in-batch distance columns (dres) bound it.
+        const int nres_w = (int)A.ctr[C_NRES];
         for (int p = b + tid; p < e_end; p += blockDim.x) {
             const int key = seg_key[p];
             unsigned char fl = 2;
+            double ub = INFINITY;
+            const bool seedc = key < 0 && A.res_col[p] >= 0 && !overflow;
             if (key >= 0 && !overflow) {
                 const int g = seg_grp[p];
                 const int i = seg_nf[p];
                 const float Pi = RS_UB_SCAN ? seg_P[grp_off[g] + i] : __fmul_ru((float)i, grp_U[g]);
-                const double ub = (double)seg_ub0[p] + (double)drift_avg(grp_d0[g], grp_nf0[g], Pi, i, grp_cn[g], grp_U[g]);
+                ub = (double)seg_ub0[p] + (double)drift_avg(grp_d0[g], grp_nf0[g], Pi, i, grp_cn[g], grp_U[g]);
                 const double md = (key == s_md1_slot) ? s_md2 : s_md1;
                 const double lbo = (double)seg_lbr[p] - md * 1.000001;
                 if (lbo > ub) fl = ub <= A.T ? 0 : 1;
+            } else if (seedc) {
+                if ((double)seg_lbr[p] - s_md1 * 1.000001 > A.T) fl = 3;
+            }
+            if (fl != 2 && nres_w > 0) {
+                const float fnp = A.fnorm[A.c0 + p];
+                int kbefore = 0;
+                for (int q = 0; q < nres_w; q++) {
+                    const int pq = A.res_pos[q];
+                    if (pq < b || pq >= p) continue;
+                    if (A.res_col[pq] < 0 || seg_key[pq] >= 0) continue;  // not a probable seed of this window
+                    kbefore++;
+                    const float d = A.dres[(int64_t)p * A.ldr + q];
+                    const float lb = d - (A.rel * d + A.absc * (fnp + A.fnorm[A.c0 + pq])) - 1e-30f;
+                    const double bound = fl == 3 ? A.T : ub;
+                    if (!((double)(lb - fabsf(lb) * 1e-6f) > bound)) {
+                        fl = 2;
+                        break;
+                    }
+                }
+                if (fl == 3 && (int64_t)L + kbefore + 1 > A.M) fl = 2;  // would evict: sequential step
+            } else if (fl == 3 && (int64_t)L + 1 > A.M) {
+                fl = 2;
             }
             seg_flag[p] = fl;
             sh_slot_of[p] = key;  // tentative, for materialisation by the exact path
@@ -1132,7 +1174,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
             if (tid == 0) s_fail = e_end;
             __syncthreads();
             for (int p = f + tid; p < e_end; p += blockDim.x)
-                if (seg_flag[p]) atomicMin(&s_fail, p);
+                if (seg_flag[p] == 1 || seg_flag[p] == 2) atomicMin(&s_fail, p);
             __syncthreads();
             f = s_fail;
             if (f >= e_end || seg_flag[f] != 1) break;
@@ -1290,6 +1332,57 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
             for (int p = b + tid; p < e_end; p += blockDim.x) {
                 const int key = seg_key[p];
                 if (key >= 0 && A.s_grp[key] == RS_MAXGRP) A.s_grp[key] = -1;
+            }
+        }
+        // certain seeds of [b, f), in stream order: the k-th takes the next free
+        // slot and cluster id (clustering.py:122-125) and is appended to live
+        if (!overflow && nres_w > 0) {
+            __syncthreads();
+            for (int p = b + tid; p < f; p += blockDim.x) {
+                if (seg_flag[p] != 3) continue;
+                int k = 0;
+                for (int q = 0; q < nres_w; q++) {
+                    const int pq = A.res_pos[q];
+                    k += (pq >= b && pq < p && seg_flag[pq] == 3) ? 1 : 0;
+                }
+                const int slot = A.free_stack[s_nfree - 1 - k];
+                const int cid = (int)(s_next_cid + k);
+                const int64_t cc = A.c0 + p;
+                const int64_t obj = A.cls_obj[cc];
+                A.s_cid[slot] = cid;
+                A.s_nfeat[slot] = 1;
+                A.s_size[slot] = 1 + A.dup_run[cc];  // dedup members following the seed join it
+                A.s_drift[slot] = 0.0;
+                A.s_cn2[slot] = A.fnorm[cc] * A.fnorm[cc];
+                A.s_snapq[slot] = -1;
+                A.s_seedpos[slot] = p;
+                A.s_foldpos[slot] = p;
+                A.s_pend[slot] = 1;
+                A.s_evicted[slot] = 0;
+                A.s_odcol[slot] = -1;
+                A.s_grp[slot] = -1;
+                A.live[L + k] = slot;
+                A.live_pos[slot] = L + k;
+                seedlist[s_nseeds + k] = slot;
+                const int di = atomicAdd(&s_ndirty, 1);
+                A.s_didx[slot] = di;
+                A.dirty[di] = slot;
+                A.pend_rank[p] = 0;
+                A.slot_of[p] = slot;
+                sh_slot_of[p] = slot;
+                A.cluster_of[obj] = cid;
+                A.mrank[obj] = 0;
+                A.frank[obj] = 0;
+                atomicAdd(&s_wseeds, 1);
+                atomicAdd((unsigned long long *)&s_dc, (unsigned long long)(f - 1 - p));  // later objects see it
+            }
+            __syncthreads();
+            if (tid == 0 && s_wseeds > 0) {
+                s_L += s_wseeds;
+                s_nseeds += s_wseeds;
+                s_next_cid += s_wseeds;
+                s_nfree -= s_wseeds;
+                s_wseeds = 0;
             }
         }
         if (tid == 0) {
@@ -2031,6 +2124,7 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             A.dres = s->dres.p;
             A.ldr = B;
             A.res_col = s->res_col.p;
+            A.res_pos = s->res_pos.p;
             A.dod = s->dod.p;
             A.frow = s->frow.p;
             A.fnorm = s->fnorm.p;
