@@ -242,6 +242,10 @@ int fx_stream_create(const fx_stream_config *cfg, fx_stream **out) {
                             &s->pend_list, &s->sum_slot, &s->sum_q})
                 b->reserve(B + 1);
             for (auto *b : {&s->sum_d1, &s->sum_e1, &s->sum_lbr}) b->reserve(B + 1);
+            for (auto *b : {&s->ev_pos, &s->ev_vic}) b->reserve(B + 1);
+            s->cid_slot.reserve(4 * (size_t)B);
+            s->s_fjoin.reserve(ns);
+            FX_CUDA(cudaMemsetAsync(s->s_fjoin.p, 0x7f, sizeof(int32_t) * ns, s->st));
             s->dirty.reserve(2 * B + 2);
             s->dirty_off.reserve(2 * B + 3);
             s->prev_sig.reserve(std::max(1, cfg->sig_dim));

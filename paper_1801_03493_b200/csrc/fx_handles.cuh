@@ -24,6 +24,7 @@ enum Ctr {
     C_ERR,             // internal error flag
     C_FAST,            // objects decided by the certain (screen-bounded) path
     C_FCFLAG,          // K1b: objects whose top-K sits within the float64 logit margin
+    C_EVCUR,           // eviction cursor: every cid below it is evicted or has size > 1
     C_COUNT
 };
 
@@ -95,6 +96,9 @@ struct fx_stream {
     fx::DevBuf<float> dod;     // [B*B] on-demand columns
     fx::DevBuf<int32_t> slot_of, pend_rank, evict_slot, evict_cid, dirty, dirty_off, pend_list, sum_slot, sum_q;
     fx::DevBuf<float> sum_d1, sum_e1, sum_lbr;
+    fx::DevBuf<int32_t> cid_slot;        // [>= clusters created + 3B] slot of each cluster id
+    fx::DevBuf<int32_t> s_fjoin;         // [nslots] first join position inside a window (scratch, INT_MAX)
+    fx::DevBuf<int32_t> ev_pos, ev_vic;  // [B+1] window seed positions / eviction victims
     // per-cluster results (grow with clusters)
     int64_t cl_cap = 0;
     fx::DevBuf<double> fcent;      // [cl_cap*D] final centroids

@@ -337,6 +337,7 @@ struct ResolveArgs {
     int32_t *live, *live_pos, *free_stack, *defer_free, *snap_slot;
     int64_t *ctr;
     int32_t *slot_of, *pend_rank, *evict_slot, *evict_cid, *dirty, *dirty_off, *pend_list;
+    int32_t *cid_slot, *s_fjoin, *ev_pos, *ev_vic;  // eviction FIFO: slot of each cid, first join, plan
     int32_t *cluster_of, *mrank, *frank;
     const PwPlan *plan;
     int32_t *s_grp;
@@ -788,6 +789,41 @@ __device__ __forceinline__ double drift_step(double dr, double ub, int nf, doubl
     return dr + ub / nf + 8.0 * 1.1102230246251565e-16 * (cn + dr + ub) + 1e-300;
 }
 
+// Ordered block compaction of [lo, hi) (hi - lo <= 4096): out[r] = the r-th i
+// with pred(i).  Returns the count (every thread).
+template <class Pred>
+__device__ int rs_compact(int lo, int hi, Pred pred, int32_t *out, int *wsv, int *s_tot) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int per = (hi - lo + RS_THREADS - 1) / RS_THREADS;
+    const int i0 = min(hi, lo + tid * per), i1 = min(hi, i0 + per);
+    int c = 0;
+    for (int i = i0; i < i1; i++) c += pred(i) ? 1 : 0;
+    int v = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int t = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += t;
+    }
+    if (lane == 31) wsv[wid] = v;
+    __syncthreads();
+    if (tid == 0) {
+        int a = 0;
+        for (int w = 0; w < RS_WARPS; w++) {
+            const int t = wsv[w];
+            wsv[w] = a;
+            a += t;
+        }
+        *s_tot = a;
+    }
+    __syncthreads();
+    int r = wsv[wid] + v - c;
+    for (int i = i0; i < i1; i++)
+        if (pred(i)) out[r++] = i;
+    const int tot = *s_tot;
+    __syncthreads();
+    return tot;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -819,7 +855,8 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
     __shared__ int grp_cnt[RS_MAXGRP], grp_off[RS_MAXGRP], grp_ncommit[RS_MAXGRP], grp_nf0[RS_MAXGRP];
     __shared__ int grp_cid[RS_MAXGRP], grp_size0[RS_MAXGRP], grp_pend0[RS_MAXGRP];
     __shared__ float grp_drift[RS_MAXGRP], grp_U[RS_MAXGRP], grp_d0[RS_MAXGRP], grp_cn[RS_MAXGRP];
-    __shared__ int s_ngrp, s_fail, s_wseeds;
+    __shared__ int s_ngrp, s_fail, s_tot, s_nold, s_conf, s_scan, s_cfirst;
+    __shared__ unsigned s_zmask[128];  // window seeds without dedup followers (bit k)
     __shared__ double s_md1, s_md2;
     __shared__ int s_md1_slot;
     __shared__ double wmd1[RS_WARPS], wmd2[RS_WARPS];
@@ -836,7 +873,6 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
         int nd = (int)ctr[C_NDEFER];
         for (int i = 0; i < nd; i++) A.free_stack[s_nfree++] = A.defer_free[i];
         s_ndefer = 0;
-        s_wseeds = 0;
         s_nevict = 0;
         s_nod = 0;
         s_ndirty = 0;
@@ -900,6 +936,25 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
             const float fn = A.fnorm[A.c0 + p];
             int j1 = A.sum_slot[p];
             float d1 = A.sum_d1[p], e1 = A.sum_e1[p], lbr = A.sum_lbr[p];
+            if (s_any_evicted && j1 >= 0 && A.s_evicted[j1] && A.res_col[p] >= 0) {
+                // probable-seed pre-test before any rescan: the snapshot summary
+                // bounds a superset of the live clusters
+                float lb = fminf(d1 - e1, lbr);
+                for (int k = 0; k < s_nseeds && (double)lb > A.T; k++) {
+                    const int sl = seedlist[k];
+                    if (A.s_evicted[sl]) continue;
+                    const int s = A.s_seedpos[sl];
+                    const int col = A.res_col[s];
+                    const float d = col >= 0 ? A.dres[(int64_t)p * A.ldr + col] : A.dod[(int64_t)A.s_odcol[sl] * B + p];
+                    lb = fminf(lb, d - (A.rel * d + A.absc * (A.fnorm[A.c0 + s] + fn) + 1e-30f));
+                }
+                if ((double)lb > A.T) {
+                    seg_key[p] = -1;
+                    seg_ub0[p] = INFINITY;
+                    seg_lbr[p] = lb - fabsf(lb) * 1e-6f - 1e-30f;
+                    continue;
+                }
+            }
             if (s_any_evicted && (j1 < 0 || A.s_evicted[j1])) {
                 j1 = -1;
                 d1 = INFINITY;
@@ -1122,7 +1177,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
         // pass D: certainty check -> 0 certain, 1 only the T test is open
         // (confirmable by one exact distance), 2 anything else
         //         3 certain seed (no live centroid and no earlier probable seed of
-        //         this window within T; the window's seeds keep L <= M).
+        //         this window within T; evictions it causes are planned below).
         //         Probable seeds earlier in the window are candidates of every
         //         later object: their in-batch distance columns (dres) bound it.
         const int nres_w = (int)A.ctr[C_NRES];
@@ -1144,12 +1199,10 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
             }
             if (fl != 2 && nres_w > 0) {
                 const float fnp = A.fnorm[A.c0 + p];
-                int kbefore = 0;
                 for (int q = 0; q < nres_w; q++) {
                     const int pq = A.res_pos[q];
                     if (pq < b || pq >= p) continue;
                     if (A.res_col[pq] < 0 || seg_key[pq] >= 0) continue;  // not a probable seed of this window
-                    kbefore++;
                     const float d = A.dres[(int64_t)p * A.ldr + q];
                     const float lb = d - (A.rel * d + A.absc * (fnp + A.fnorm[A.c0 + pq])) - 1e-30f;
                     const double bound = fl == 3 ? A.T : ub;
@@ -1158,9 +1211,6 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
                         break;
                     }
                 }
-                if (fl == 3 && (int64_t)L + kbefore + 1 > A.M) fl = 2;  // would evict: sequential step
-            } else if (fl == 3 && (int64_t)L + 1 > A.M) {
-                fl = 2;
             }
             seg_flag[p] = fl;
             sh_slot_of[p] = key;  // tentative, for materialisation by the exact path
@@ -1193,6 +1243,152 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
             __syncthreads();
         }
         __syncthreads();
+        // ---- evictions caused by the certain seeds of [b, f) (clustering.py:139-144).
+        // The victim is the live cluster of minimum (size, first in live order =
+        // cid); the new seed has size 1 at that moment, so every victim has size
+        // 1: it is the head of the FIFO of live size-1 clusters in cid order.
+        // That FIFO holds the size-1 clusters of earlier windows (scanned from
+        // the persistent cursor ctr[C_EVCUR]; every cid below it is evicted or
+        // larger) ahead of this window's seeds that keep size 1.  An earlier
+        // cluster joined inside the window would leave the FIFO at its join:
+        // the window is cut at the eviction that reaches it (sequential step).
+        int ws = 0, k0 = 0, nev = 0, nold = 0;
+        if (!overflow && nres_w > 0) {
+            ws = rs_compact(b, f, [&](int p) { return seg_flag[p] == 3; }, A.ev_pos, wsv, &s_tot);
+            k0 = (int)min((int64_t)ws, max((int64_t)0, A.M - (int64_t)L));  // seeds k >= k0 evict
+            nev = ws - k0;
+        }
+        if (nev > 0) {
+            const int f0 = f;
+            for (int p = b + tid; p < f0; p += blockDim.x) {
+                const int key = seg_key[p];
+                if (key >= 0) atomicMin(&A.s_fjoin[key], p);
+            }
+            if (tid == 0) {
+                s_nold = 0;
+                s_conf = 0;
+                s_scan = (int)ctr[C_EVCUR];
+            }
+            __syncthreads();
+            const int cid_end = (int)s_next_cid;  // first cid of this window's seeds
+            while (true) {
+                const int base = s_scan, n0 = s_nold;
+                if (n0 >= nev || s_conf || base >= cid_end) break;
+                const int cid = base + tid;
+                bool valid = false, conf = false;
+                int slot = -1;
+                if (cid < cid_end) {
+                    slot = A.cid_slot[cid];
+                    valid = A.s_cid[slot] == cid && !A.s_evicted[slot] && A.s_size[slot] == 1;
+                    conf = valid && A.s_fjoin[slot] < f0;
+                }
+                if (tid == 0) s_cfirst = RS_THREADS;
+                __syncthreads();
+                if (conf) atomicMin(&s_cfirst, tid);
+                __syncthreads();
+                const bool take = valid && tid < s_cfirst;
+                const unsigned m = __ballot_sync(0xffffffffu, take);
+                if (lane == 0) wsv[wid] = __popc(m);
+                __syncthreads();
+                if (tid == 0) {
+                    int a = 0;
+                    for (int w = 0; w < RS_WARPS; w++) {
+                        const int t = wsv[w];
+                        wsv[w] = a;
+                        a += t;
+                    }
+                    s_tot = a;
+                }
+                __syncthreads();
+                const int r = n0 + wsv[wid] + __popc(m & ((1u << lane) - 1));
+                if (take && r < nev) {
+                    A.ev_vic[r] = slot;
+                    if (r == nev - 1) s_scan = cid + 1;
+                }
+                __syncthreads();
+                if (tid == 0) {
+                    if (n0 + s_tot >= nev) {
+                        s_nold = nev;
+                    } else {
+                        s_nold = n0 + s_tot;
+                        if (s_cfirst < RS_THREADS) {
+                            s_conf = 1;
+                            s_scan = base + s_cfirst;
+                        } else {
+                            s_scan = min(base + RS_THREADS, cid_end);
+                        }
+                    }
+                }
+                __syncthreads();
+            }
+            nold = s_nold;
+            if (s_conf) {  // cut at the eviction that would take the joined cluster
+                f = A.ev_pos[k0 + nold];
+                ws = k0 + nold;
+                nev = nold;
+            }
+            if (tid == 0) ctr[C_EVCUR] = s_scan;
+            for (int p = b + tid; p < f0; p += blockDim.x) {
+                const int key = seg_key[p];
+                if (key >= 0) A.s_fjoin[key] = 0x7fffffff;
+            }
+            if (nev > nold) {
+                // pops past the earlier windows' FIFO: this window's seeds.  Seed
+                // k pushes itself; an evicting seed pops the head (itself when the
+                // queue was empty); a seed with dedup followers that is not popped
+                // leaves (size > 1).  Queue length w -> max(w + a, c) per seed,
+                // composed by a warp scan.
+                for (int i = tid; i < 128; i += blockDim.x) s_zmask[i] = 0;
+                __syncthreads();
+                for (int k = tid; k < ws; k += blockDim.x)
+                    if (A.dup_run[A.c0 + A.ev_pos[k]] == 0) atomicOr(&s_zmask[k >> 5], 1u << (k & 31));
+                __syncthreads();
+                if (wid == 0) {
+                    int *entry = (int *)seg_lbr;  // free after pass D
+                    constexpr int NEG = -(1 << 28);
+                    const int kw = k0 + nold;
+                    const int fr = s_nfree;
+                    int w = 0, ne = 0, nr = 0;
+                    for (int c = 0; c < ws; c += 32) {
+                        const int k = c + lane;
+                        const bool in = k < ws;
+                        const int z = in ? (int)((s_zmask[k >> 5] >> (k & 31)) & 1u) : 0;
+                        const bool wpop = in && k >= kw;
+                        int a = wpop ? z - 1 : z, cc = wpop ? 0 : NEG;
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const int ap = __shfl_up_sync(0xffffffffu, a, o), cp = __shfl_up_sync(0xffffffffu, cc, o);
+                            if (lane >= o) {
+                                cc = max(cp + a, cc);
+                                a = ap + a;
+                            }
+                        }
+                        int ae = __shfl_up_sync(0xffffffffu, a, 1), ce = __shfl_up_sync(0xffffffffu, cc, 1);
+                        if (lane == 0) {
+                            ae = 0;
+                            ce = NEG;
+                        }
+                        const int wb = max(w + ae, ce);  // queue length before seed k
+                        const bool self = wpop && wb == 0;
+                        const bool ent = in && z && !self;
+                        const bool pop = wpop && !self;
+                        const unsigned me = __ballot_sync(0xffffffffu, ent), mp = __ballot_sync(0xffffffffu, pop);
+                        const unsigned lt = (1u << lane) - 1;
+                        if (ent) entry[ne + __popc(me & lt)] = k;
+                        __syncwarp();
+                        if (wpop) {
+                            const int kv = self ? k : entry[nr + __popc(mp & lt)];
+                            A.ev_vic[k - k0] = A.free_stack[fr - 1 - kv];
+                        }
+                        w = max(w + __shfl_sync(0xffffffffu, a, 31), __shfl_sync(0xffffffffu, cc, 31));
+                        ne += __popc(me);
+                        nr += __popc(mp);
+                        __syncwarp();
+                    }
+                }
+            }
+            __syncthreads();
+        }
         for (int p = f + tid; p < e_end; p += blockDim.x) sh_slot_of[p] = -1;
         long long t4 = clock64();
         if (tid == 0) A.prof[3] += t4 - t3;
@@ -1335,16 +1531,12 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
             }
         }
         // certain seeds of [b, f), in stream order: the k-th takes the next free
-        // slot and cluster id (clustering.py:122-125) and is appended to live
-        if (!overflow && nres_w > 0) {
+        // slot and cluster id (clustering.py:122-125); the planned victims are
+        // evicted and the surviving seeds fill their live positions, then append
+        if (ws > 0) {
             __syncthreads();
-            for (int p = b + tid; p < f; p += blockDim.x) {
-                if (seg_flag[p] != 3) continue;
-                int k = 0;
-                for (int q = 0; q < nres_w; q++) {
-                    const int pq = A.res_pos[q];
-                    k += (pq >= b && pq < p && seg_flag[pq] == 3) ? 1 : 0;
-                }
+            for (int k = tid; k < ws; k += blockDim.x) {
+                const int p = A.ev_pos[k];
                 const int slot = A.free_stack[s_nfree - 1 - k];
                 const int cid = (int)(s_next_cid + k);
                 const int64_t cc = A.c0 + p;
@@ -1361,8 +1553,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
                 A.s_evicted[slot] = 0;
                 A.s_odcol[slot] = -1;
                 A.s_grp[slot] = -1;
-                A.live[L + k] = slot;
-                A.live_pos[slot] = L + k;
+                A.cid_slot[cid] = slot;
                 seedlist[s_nseeds + k] = slot;
                 const int di = atomicAdd(&s_ndirty, 1);
                 A.s_didx[slot] = di;
@@ -1373,16 +1564,41 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
                 A.cluster_of[obj] = cid;
                 A.mrank[obj] = 0;
                 A.frank[obj] = 0;
-                atomicAdd(&s_wseeds, 1);
-                atomicAdd((unsigned long long *)&s_dc, (unsigned long long)(f - 1 - p));  // later objects see it
+                // later objects of the window see it while the live count grows
+                if (k < k0) atomicAdd((unsigned long long *)&s_dc, (unsigned long long)(f - 1 - p));
             }
             __syncthreads();
-            if (tid == 0 && s_wseeds > 0) {
-                s_L += s_wseeds;
-                s_nseeds += s_wseeds;
-                s_next_cid += s_wseeds;
-                s_nfree -= s_wseeds;
-                s_wseeds = 0;
+            for (int i = tid; i < nev; i += blockDim.x) {
+                const int v = A.ev_vic[i];
+                A.s_evicted[v] = 1;
+                A.evict_slot[s_nevict + i] = v;
+                A.evict_cid[s_nevict + i] = A.s_cid[v];
+                A.defer_free[s_ndefer + i] = v;
+                if (A.s_pend[v] == 0) {  // untouched this batch but needs its final centroid
+                    const int di = atomicAdd(&s_ndirty, 1);
+                    A.s_didx[v] = di;
+                    A.dirty[di] = v;
+                }
+            }
+            __syncthreads();
+            const int fr = s_nfree;
+            const int nsv = rs_compact(0, ws, [&](int k) { return !A.s_evicted[A.free_stack[fr - 1 - k]]; }, A.ev_pos,
+                                       wsv, &s_tot);
+            for (int t = tid; t < nsv; t += blockDim.x) {
+                const int slot = A.free_stack[fr - 1 - A.ev_pos[t]];
+                const int pos = t < nold ? A.live_pos[A.ev_vic[t]] : L + (t - nold);
+                A.live[pos] = slot;
+                A.live_pos[slot] = pos;
+            }
+            __syncthreads();
+            if (tid == 0) {
+                s_L = L + nsv - nold;
+                s_nseeds += ws;
+                s_next_cid += ws;
+                s_nfree -= ws;
+                s_nevict += nev;
+                s_ndefer += nev;
+                if (nev > 0) s_any_evicted = 1;
             }
         }
         if (tid == 0) {
@@ -1522,6 +1738,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
                 slot = A.free_stack[--s_nfree];
                 int cid = (int)s_next_cid++;
                 A.s_cid[slot] = cid;
+                A.cid_slot[cid] = slot;
                 A.s_nfeat[slot] = 1;
                 A.s_size[slot] = 1;
                 A.s_drift[slot] = 0.0;
@@ -2153,6 +2370,10 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             A.pend_rank = s->pend_rank.p;
             A.evict_slot = s->evict_slot.p;
             A.evict_cid = s->evict_cid.p;
+            A.cid_slot = s->cid_slot.p;
+            A.s_fjoin = s->s_fjoin.p;
+            A.ev_pos = s->ev_pos.p;
+            A.ev_vic = s->ev_vic.p;
             A.dirty = s->dirty.p;
             A.dirty_off = s->dirty_off.p;
             A.pend_list = s->pend_list.p;
@@ -2206,6 +2427,7 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
                 s->cl_size.grow(cap, s->cl_cap, st);
                 s->cl_cap = cap;
             }
+            if (need > (int64_t)s->cid_slot.n) s->cid_slot.grow((size_t)need, s->cid_slot.n, st);
         }
         const auto h3 = hclock::now();
         s->t_ms[10] += hms(h2, h3);

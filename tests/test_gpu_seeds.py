@@ -1,6 +1,7 @@
 """Seed-heavy streams (the C3 "small T" shape): most objects seed, probable
-seeds are decided in parallel inside a resolve window, windows stop where a
-seed would push the live count past M (eviction -> sequential step).  The
+seeds are decided in parallel inside a resolve window, together with the
+evictions they cause once the live count reaches M (victims taken from the
+FIFO of live size-1 clusters; a window is cut where a victim was joined).  The
 device ingest must equal the CPU oracle bit for bit: cluster of every
 object, distance_computations, float64 centroid bits, representatives."""
 
@@ -15,8 +16,9 @@ pytestmark = pytest.mark.gpu
 fx = pytest.importorskip("paper_1801_03493_b200")
 
 
-def _run(seed, t, m, dim, n=2500, classes=400, batch=0):
-    spec = streamgen.Spec(n_objects=n, dim=dim, vocab=500, n_stream_classes=classes, seed=seed)
+def _run(seed, t, m, dim, n=2500, classes=400, batch=0, dup_rate=0.2):
+    spec = streamgen.Spec(n_objects=n, dim=dim, vocab=500, n_stream_classes=classes, seed=seed,
+                          duplicate_rate=dup_rate)
     st = streamgen.generate(spec)
     prof = O.default_profiles(spec.vocab)["cheap"]
     dup = O.dup_flags(st.fids, st.sigs, 0.01)
@@ -49,3 +51,14 @@ def _run(seed, t, m, dim, n=2500, classes=400, batch=0):
 ])
 def test_seed_heavy_streams_match_oracle(seed, t, m, dim, batch):
     _run(seed, t, m, dim, batch=batch)
+
+
+@pytest.mark.parametrize("seed,t,m,dim,batch,classes,dup", [
+    (36, 1.4, 200, 128, 256, 400, 0.2),   # joins and evictions mixed: joined size-1 clusters cut windows
+    (37, 0.5, 300, 64, 512, 400, 0.0),    # no dedup: every seed keeps size 1, FIFO of earlier windows
+    (38, 0.5, 300, 64, 512, 400, 0.6),    # heavy dedup: size-1 FIFO drains, seeds evict each other / themselves
+    (39, 1.0, 64, 64, 0, 60, 0.3),        # few classes, tiny M: long-lived large clusters never evicted
+    (40, 0.5, 1000, 32, 128, 400, 0.2),   # M crossed inside the 8th batch, then every batch evicts
+])
+def test_window_evictions_match_oracle(seed, t, m, dim, batch, classes, dup):
+    _run(seed, t, m, dim, n=4000, classes=classes, batch=batch, dup_rate=dup)
