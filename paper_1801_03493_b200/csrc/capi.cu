@@ -244,6 +244,9 @@ int fx_stream_create(const fx_stream_config *cfg, fx_stream **out) {
             for (auto *b : {&s->sum_d1, &s->sum_e1, &s->sum_lbr}) b->reserve(B + 1);
             for (auto *b : {&s->ev_pos, &s->ev_vic}) b->reserve(B + 1);
             s->cid_slot.reserve(4 * (size_t)B);
+            s->rowmin.reserve(B + 1);
+            FX_CUDA(cudaMemsetAsync(s->rowmin.p, 0x7f, sizeof(int32_t) * (B + 1), s->st));
+            s->snorm.reserve(s->ld);
             s->s_fjoin.reserve(ns);
             FX_CUDA(cudaMemsetAsync(s->s_fjoin.p, 0x7f, sizeof(int32_t) * ns, s->st));
             s->dirty.reserve(2 * B + 2);

@@ -96,6 +96,8 @@ struct fx_stream {
     fx::DevBuf<float> dod;     // [B*B] on-demand columns
     fx::DevBuf<int32_t> slot_of, pend_rank, evict_slot, evict_cid, dirty, dirty_off, pend_list, sum_slot, sum_q;
     fx::DevBuf<float> sum_d1, sum_e1, sum_lbr;
+    fx::DevBuf<int32_t> rowmin;          // [B+1] multi-tile TC screen: min lower bound per row (float bits)
+    fx::DevBuf<float> snorm;             // [ld] snapshot column norms (TC screen)
     fx::DevBuf<int32_t> cid_slot;        // [>= clusters created + 3B] slot of each cluster id
     fx::DevBuf<int32_t> s_fjoin;         // [nslots] first join position inside a window (scratch, INT_MAX)
     fx::DevBuf<int32_t> ev_pos, ev_vic;  // [B+1] window seed positions / eviction victims

@@ -385,11 +385,14 @@ static void build_class_sets(fx_index *ix, E src, int64_t n_entries_in, cudaStre
             table.reserve((size_t)nbig * V1);
             FX_CUDA(cudaMemsetAsync(table.p, 0xff, sizeof(uint32_t) * nbig * V1, st));
             int64_t max_chunks = cdiv(n_entries_in, CHUNK_BIG);
-            dim3 grid((unsigned)std::max<int64_t>(1, max_chunks), (unsigned)nbig);
             size_t smem = sizeof(uint32_t) * V1;
             FX_CUDA(cudaFuncSetAttribute(k_classes_big_acc<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-            k_classes_big_acc<E><<<grid, 256, smem, st>>>(nbig, big_list.p, src, V1, table.p);
-            FX_LAUNCHED();
+            for (int64_t off = 0; off < nbig; off += 65535) {  // grid y is limited to 65535
+                const int64_t nb = std::min<int64_t>(65535, nbig - off);
+                dim3 grid((unsigned)std::max<int64_t>(1, max_chunks), (unsigned)nb);
+                k_classes_big_acc<E><<<grid, 256, smem, st>>>(nb, big_list.p + off, src, V1, table.p + off * V1);
+                FX_LAUNCHED();
+            }
             k_classes_big_emit<E><<<(unsigned)nbig, 1024, 0, st>>>(nbig, big_list.p, src, V1, table.p, tmp_cls.p,
                                                                    tmp_rank.p, cnt.p);
             FX_LAUNCHED();

@@ -493,34 +493,45 @@ __device__ double exact_dist(const ResolveArgs &A, int b, int slot, const int32_
     return __dsqrt_rn(dadd(0.0, tot));
 }
 
-// Per-object summary of the snapshot screen row: best snapshot slot, its
-// distance and error bound, and min over the other snapshot slots of
-// (d - e).  One warp per object.
-template <typename T>
-__global__ void k_row_summary(int nA, const int64_t *__restrict__ ctr, const float *__restrict__ dist, int64_t ld,
-                              const float *__restrict__ cn2, const int32_t *__restrict__ snap,
-                              const float *__restrict__ fnorm, int64_t a0, ScreenModel sm, float rel, float absc,
-                              const char *const *__restrict__ frow, const float *__restrict__ C32, int D,
-                              int32_t *__restrict__ sum_slot, int32_t *__restrict__ sum_q, float *__restrict__ sum_d1,
-                              float *__restrict__ sum_e1,
-                              float *__restrict__ sum_lbr) {
-    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-    if (w >= nA) return;
-    const int nsnap = (int)ctr[C_NSNAP];
-    const float fn = fnorm[a0 + w];
-    // best candidate = smallest upper bound; lbr = min lower bound of the rest
-    float u1 = INFINITY, l1 = INFINITY, lbr = INFINITY;
-    int q1 = -1;
-    for (int q = lane; q < nsnap; q += 32) {
-        float lb, ub;
-        snap_bounds(sm, dist[(int64_t)w * ld + q], sqrtf(cn2[snap[q]]) * 1.00001f, fn, lb, ub);
-        if (ub < u1) {
-            if (q1 >= 0) lbr = fminf(lbr, l1);
-            u1 = ub;
-            l1 = lb;
-            q1 = q;
-        } else {
-            lbr = fminf(lbr, lb);
+// Scan of one screen row (one warp): best snapshot candidate by upper bound
+// (ties: lower snapshot index), its interval, min lower bound of the rest.
+// U loads per lane in flight; snorm (written by the TC screen) replaces the
+// two-level gather cn2[snap[q]] when present.
+__device__ __forceinline__ void row_scan(const float *__restrict__ drow, int nsnap, const float *__restrict__ cn2,
+                                         const int32_t *__restrict__ snap, const float *__restrict__ snorm,
+                                         ScreenModel sm, float fn, int lane, float &u1, float &l1, float &lbr, int &q1) {
+    constexpr int U = 8;
+    u1 = INFINITY;
+    l1 = INFINITY;
+    lbr = INFINITY;
+    q1 = -1;
+    for (int q0 = 0; q0 < nsnap; q0 += 32 * U) {
+        float dv[U], nv[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int q = q0 + lane + 32 * u;
+            dv[u] = q < nsnap ? drow[q] : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int q = q0 + lane + 32 * u;
+            nv[u] = q < nsnap ? (snorm ? snorm[q] : sqrtf(cn2[snap[q]]) * 1.00001f) : 0.f;
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int q = q0 + lane + 32 * u;
+            if (q < nsnap) {
+                float lb, ub;
+                snap_bounds(sm, dv[u], nv[u], fn, lb, ub);
+                if (ub < u1) {
+                    if (q1 >= 0) lbr = fminf(lbr, l1);
+                    u1 = ub;
+                    l1 = lb;
+                    q1 = q;
+                } else {
+                    lbr = fminf(lbr, lb);
+                }
+            }
         }
     }
 #pragma unroll
@@ -538,6 +549,44 @@ __global__ void k_row_summary(int nA, const int64_t *__restrict__ ctr, const flo
             lbr = fminf(fminf(lbr, olbr), oq >= 0 ? ol : INFINITY);
         }
     }
+}
+
+// Residual flags from the per-row minimum screen lower bound the multi-tile TC
+// screen accumulated in rowmin (float bits); resets rowmin for the next batch.
+__global__ void k_res_from_min(int nA, int *__restrict__ rowmin, double T, int32_t *__restrict__ res_col,
+                               int32_t *__restrict__ res_pos, int64_t *__restrict__ nres) {
+    const int a = blockIdx.x * blockDim.x + threadIdx.x;
+    if (a >= nA) return;
+    const float mn = __int_as_float(rowmin[a]);
+    rowmin[a] = 0x7f7f7f7f;
+    if ((double)mn > T) {
+        const int col = (int)atomicAdd((unsigned long long *)nres, 1ull);
+        res_pos[col] = a;
+        res_col[a] = col;
+    } else {
+        res_col[a] = -1;
+    }
+}
+
+// Per-object summary of the snapshot screen row: best snapshot slot, its
+// distance and error bound, and min over the other snapshot slots of
+// (d - e).  One warp per object.
+template <typename T>
+__global__ void k_row_summary(int nA, const int64_t *__restrict__ ctr, const float *__restrict__ dist, int64_t ld,
+                              const float *__restrict__ cn2, const int32_t *__restrict__ snap,
+                              const float *__restrict__ fnorm, int64_t a0, ScreenModel sm, float rel, float absc,
+                              const char *const *__restrict__ frow, const float *__restrict__ C32, int D,
+                              int32_t *__restrict__ sum_slot, int32_t *__restrict__ sum_q, float *__restrict__ sum_d1,
+                              float *__restrict__ sum_e1, float *__restrict__ sum_lbr,
+                              const float *__restrict__ snorm) {
+    const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+    if (w >= nA) return;
+    const int nsnap = (int)ctr[C_NSNAP];
+    const float fn = fnorm[a0 + w];
+    // best candidate = smallest upper bound; lbr = min lower bound of the rest
+    float u1, l1, lbr;
+    int q1;
+    row_scan(dist + (int64_t)w * ld, nsnap, cn2, snap, snorm, sm, fn, lane, u1, l1, lbr, q1);
     float d1 = 0.5f * (l1 + u1), e1 = 0.5f * (u1 - l1);
     if (sm.tc && q1 >= 0) {
         // re-measure the best candidate in FP32 direct-difference form (tight SIMT bound)
@@ -593,7 +642,7 @@ __global__ void __launch_bounds__(256) k_rowpass(int nA, int64_t a0, const char 
                                                 float *__restrict__ dres, int64_t ldr, int32_t *__restrict__ sum_slot,
                                                 int32_t *__restrict__ sum_q,
                                                 float *__restrict__ sum_d1, float *__restrict__ sum_e1,
-                                                float *__restrict__ sum_lbr) {
+                                                float *__restrict__ sum_lbr, const float *__restrict__ snorm) {
     __shared__ int s_rpos[RC_MAX];
     __shared__ int s_pmin;
     const int nsnap = (int)ctr[C_NSNAP];
@@ -611,35 +660,9 @@ __global__ void __launch_bounds__(256) k_rowpass(int nA, int64_t a0, const char 
     const int nw = blockDim.x >> 5;
     for (int w = blockIdx.x * nw + (threadIdx.x >> 5); w < nA; w += gridDim.x * nw) {
         const float fn = fnorm[a0 + w];
-        float u1 = INFINITY, l1 = INFINITY, lbr = INFINITY;
-        int q1 = -1;
-        for (int q = lane; q < nsnap; q += 32) {
-            float lb, ub;
-            snap_bounds(sm, dist[(int64_t)w * ld + q], sqrtf(cn2[snap[q]]) * 1.00001f, fn, lb, ub);
-            if (ub < u1) {
-                if (q1 >= 0) lbr = fminf(lbr, l1);
-                u1 = ub;
-                l1 = lb;
-                q1 = q;
-            } else {
-                lbr = fminf(lbr, lb);
-            }
-        }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-            const float ou = __shfl_xor_sync(0xffffffffu, u1, o), ol = __shfl_xor_sync(0xffffffffu, l1, o);
-            const float olbr = __shfl_xor_sync(0xffffffffu, lbr, o);
-            const int oq = __shfl_xor_sync(0xffffffffu, q1, o);
-            const bool take = oq >= 0 && (q1 < 0 || ou < u1 || (ou == u1 && oq < q1));
-            if (take) {
-                lbr = fminf(fminf(lbr, olbr), q1 >= 0 ? l1 : INFINITY);
-                u1 = ou;
-                l1 = ol;
-                q1 = oq;
-            } else {
-                lbr = fminf(fminf(lbr, olbr), oq >= 0 ? ol : INFINITY);
-            }
-        }
+        float u1, l1, lbr;
+        int q1;
+        row_scan(dist + (int64_t)w * ld, nsnap, cn2, snap, snorm, sm, fn, lane, u1, l1, lbr, q1);
         float d1 = 0.5f * (l1 + u1), e1 = 0.5f * (u1 - l1);
         const bool refine = sm.tc && q1 >= 0;  // a tight ub0 keeps the resolve's drift bounds small
         const bool cols = nres > 0 && w > pmin;
@@ -2131,14 +2154,14 @@ __global__ void k_final_live(int D, const int64_t *__restrict__ ctr, const int32
                              const double *__restrict__ S, const int32_t *__restrict__ s_nfeat,
                              const int32_t *__restrict__ s_cid, const int32_t *__restrict__ s_size,
                              double *__restrict__ fcent, int32_t *__restrict__ cl_nfeat, int32_t *__restrict__ cl_size) {
-    const int i = blockIdx.y;
+    const int i = blockIdx.x;  // live index on x: L can exceed the 65535 limit of grid y
     if (i >= (int)ctr[C_NLIVE]) return;
     const int slot = live[i];
     const int cid = s_cid[slot];
     const double n = (double)s_nfeat[slot];
-    for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < D; k += gridDim.x * blockDim.x)
+    for (int k = blockIdx.y * blockDim.x + threadIdx.x; k < D; k += gridDim.y * blockDim.x)
         fcent[(int64_t)cid * D + k] = ddiv(S[(int64_t)slot * D + k], n);
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (blockIdx.y == 0 && threadIdx.x == 0) {
         cl_nfeat[cid] = s_nfeat[slot];
         cl_size[cid] = s_size[slot];
     }
@@ -2212,7 +2235,7 @@ __global__ void k_seal_pick(int64_t nfeat_total, const int32_t *__restrict__ fme
 void launch_screen_tc(int nA, int64_t a0, const char *const *frow, const float *fnorm, int D, const int64_t *nB_dev,
                       int nB_max, const float *C32, const int32_t *snap, const float *cn2, float *out, int64_t ld,
                       cudaStream_t st, float *fnorm_out, ScreenModel sm, double T, int32_t *res_col,
-                      int32_t *res_pos, int64_t *nres);
+                      int32_t *res_pos, int64_t *nres, int *rowmin_g, float *snorm);
 int64_t scan_i32_to_i64(const int32_t *in, int64_t n, int64_t *out_excl, cudaStream_t st, int64_t *scratch_total);
 void scan_u8_to_i64(const uint8_t *in, int64_t n, int invert, int64_t *out_excl, int64_t *d_total, cudaStream_t st);
 
@@ -2261,7 +2284,8 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             fused_res = s->ld <= 128;
             launch_screen_tc(B, c0, s->frow.p, s->fnorm.p, D, s->ctr.p + C_NSNAP, (int)s->ld, s->C32.p,
                              s->snap_slot.p, s->s_cn2.p, s->dist.p, s->ld, st, s->has_fc ? nullptr : s->fnorm.p, sm,
-                             s->cfg.t, fused_res ? s->res_col.p : nullptr, s->res_pos.p, s->ctr.p + C_NRES);
+                             s->cfg.t, fused_res ? s->res_col.p : nullptr, s->res_pos.p, s->ctr.p + C_NRES,
+                             s->rowmin.p, s->snorm.p);
         } else {
             const unsigned grid = (unsigned)std::min<int64_t>(cdiv(s->ld, SC_T) * cdiv(B, SC_T), 148 * 8);
             FromSnapshot fb{s->C32.p, s->snap_slot.p, D};
@@ -2273,7 +2297,11 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
         s->tstart(7);  // residual detection + columns
         // 2. residuals + their in-batch columns
         {
-            if (!fused_res) {
+            if (!fused_res && s->tc_screen) {
+                k_res_from_min<<<(unsigned)cdiv(B, 256), 256, 0, st>>>(B, s->rowmin.p, s->cfg.t, s->res_col.p,
+                                                                      s->res_pos.p, s->ctr.p + C_NRES);
+                FX_LAUNCHED();
+            } else if (!fused_res) {
                 k_residuals<<<(unsigned)cdiv((int64_t)B * 32, 256), 256, 0, st>>>(
                     B, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p, s->snap_slot.p, s->fnorm.p, c0, sm, s->cfg.t,
                     s->res_col.p, s->res_pos.p, s->ctr.p + C_NRES);
@@ -2299,25 +2327,24 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
         }
         s->tstop();
         s->tstart(15);  // row summary (+ fp32 refine of the best candidate)
+        const float *snorm = s->tc_screen ? s->snorm.p : nullptr;
         if (rowpass) {
             const unsigned grid = (unsigned)std::min<int64_t>(cdiv((int64_t)B * 32, 256), 148 * 8);
             if (D <= 1024)
                 k_rowpass<8><<<grid, 256, 0, st>>>(B, c0, s->frow.p, D, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p,
                                                    s->snap_slot.p, s->fnorm.p, sm, rel, absc, s->C32.p, s->cfg.t,
                                                    s->res_pos.p, s->dres.p, B, s->sum_slot.p, s->sum_q.p, s->sum_d1.p,
-                                                   s->sum_e1.p,
-                                                   s->sum_lbr.p);
+                                                   s->sum_e1.p, s->sum_lbr.p, snorm);
             else
                 k_rowpass<16><<<grid, 256, 0, st>>>(B, c0, s->frow.p, D, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p,
                                                     s->snap_slot.p, s->fnorm.p, sm, rel, absc, s->C32.p, s->cfg.t,
                                                     s->res_pos.p, s->dres.p, B, s->sum_slot.p, s->sum_q.p, s->sum_d1.p,
-                                                   s->sum_e1.p,
-                                                    s->sum_lbr.p);
+                                                   s->sum_e1.p, s->sum_lbr.p, snorm);
             FX_LAUNCHED();
         } else {
         k_row_summary<T><<<(unsigned)cdiv((int64_t)B * 32, 256), 256, 0, st>>>(
                 B, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p, s->snap_slot.p, s->fnorm.p, c0, sm, rel, absc, s->frow.p,
-                s->C32.p, D, s->sum_slot.p, s->sum_q.p, s->sum_d1.p, s->sum_e1.p, s->sum_lbr.p);
+                s->C32.p, D, s->sum_slot.p, s->sum_q.p, s->sum_d1.p, s->sum_e1.p, s->sum_lbr.p, snorm);
             FX_LAUNCHED();
         }
         s->tstop();
@@ -2560,7 +2587,7 @@ void launch_final_live(fx_stream *s) {
     const int D = s->cfg.dim;
     int64_t L = s->h_ctr[C_NLIVE];
     if (L <= 0) return;
-    dim3 grid((unsigned)cdiv(D, 256), (unsigned)L);
+    dim3 grid((unsigned)L, (unsigned)cdiv(D, 256));
     k_final_live<<<grid, 256, 0, s->st>>>(D, s->ctr.p, s->live.p, s->S.p, s->s_nfeat.p, s->s_cid.p, s->s_size.p,
                                           s->fcent.p, s->cl_nfeat.p, s->cl_size.p);
     FX_LAUNCHED();

@@ -44,12 +44,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
                                                            const float *__restrict__ cn2, float *__restrict__ out,
                                                            int64_t ld, int kchunk, int dbg, float *__restrict__ fnorm_out,
                                                            ScreenModel sm, double T, int32_t *__restrict__ res_col,
-                                                           int32_t *__restrict__ res_pos, int64_t *__restrict__ nres) {
+                                                           int32_t *__restrict__ res_pos, int64_t *__restrict__ nres,
+                                                           int *__restrict__ rowmin_g, float *__restrict__ snorm) {
     // blockIdx.z selects the K range [z*kchunk, (z+1)*kchunk) (split-K when the
-    // tile grid alone cannot fill the machine; partials are atomically added)
+    // tile grid alone cannot fill the machine; partials are atomically added).
+    // blockIdx.x = column tile * row tiles + row tile: the CTAs that share a
+    // snapshot tile run back to back, so it streams from HBM once per batch.
     const int nB = (int)*nB_dev;
-    const int tb = blockIdx.x * TC_N, ta = blockIdx.y * TC_M;
-    if (nB == 0 && blockIdx.x == 0 && blockIdx.z == 0 && threadIdx.x < TC_M && ta + (int)threadIdx.x < nA) {
+    const int nrt = (nA + TC_M - 1) / TC_M;
+    const int tb = (int)(blockIdx.x / nrt) * TC_N, ta = (int)(blockIdx.x % nrt) * TC_M;
+    if (nB == 0 && tb == 0 && blockIdx.z == 0 && threadIdx.x < TC_M && ta + (int)threadIdx.x < nA) {
         // empty snapshot (stream start): no screen, but the batch still needs ||f||
         if (fnorm_out) {
             const float *row = (const float *)frow[a0 + ta + threadIdx.x];
@@ -234,15 +238,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
                 const float c2 = cn2[snap[tb + c + j]];
                 const float v = fa2 + c2 - 2.f * d4[j];
                 o[j] = v;
-                if (res_col) {
+                if (res_col || rowmin_g) {
                     float lb, ub;
                     snap_bounds(sm, v, sqrtf(c2) * 1.00001f, fnorm_out ? fn : fnorm[a0 + a], lb, ub);
                     mn = fminf(mn, lb);
                 }
             }
-        if (res_col) atomicMin(&rowmin[rr], __float_as_int(fmaxf(mn, 0.f)));
+        if (res_col || rowmin_g) atomicMin(&rowmin[rr], __float_as_int(fmaxf(mn, 0.f)));
     }
-    if (res_col) {
+    if (snorm && ta == 0 && rank == 0)
+        for (int c = tid; c < ncol; c += TC_THREADS) snorm[tb + c] = sqrtf(cn2[snap[tb + c]]) * 1.00001f;
+    if (rowmin_g) {
+        // several column tiles: per-row minimum across CTAs (k_res_from_min flags the residuals)
+        __syncthreads();
+        for (int rr = rank * rows_per + tid; rr < (rank + 1) * rows_per; rr += TC_THREADS)
+            if (ta + rr < nA) atomicMin(&rowmin_g[ta + rr], rowmin[rr]);
+    } else if (res_col) {
         // fused residual detection (one column tile = the whole snapshot):
         // objects with no snapshot centroid whose lower bound is <= T
         __syncthreads();
@@ -268,8 +279,10 @@ size_t screen_tc_smem() { return (size_t)TC_STAGES * 2 * TC_TILE_BYTES; }
 void launch_screen_tc(int nA, int64_t a0, const char *const *frow, const float *fnorm, int D, const int64_t *nB_dev,
                       int nB_max, const float *C32, const int32_t *snap, const float *cn2, float *out, int64_t ld,
                       cudaStream_t st, float *fnorm_out, ScreenModel sm, double T, int32_t *res_col,
-                      int32_t *res_pos, int64_t *nres) {
-    if (nB_max > TC_N) res_col = nullptr;  // fused residual detection needs the whole snapshot in one tile
+                      int32_t *res_pos, int64_t *nres, int *rowmin_g, float *snorm) {
+    // residual detection inside one tile, or across tiles through rowmin_g
+    if (nB_max > TC_N) res_col = nullptr;
+    else rowmin_g = nullptr;
     static bool attr = false;
     if (!attr) {
         FX_CUDA(cudaFuncSetAttribute(k_screen_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)screen_tc_smem()));
@@ -285,7 +298,7 @@ void launch_screen_tc(int nA, int64_t a0, const char *const *frow, const float *
     while (TC_M % split) split--;
     const int kchunk = (int)(cdiv(cdiv(D, split), TC_KT) * TC_KT);
     cudaLaunchConfig_t lc = {};
-    lc.gridDim = dim3((unsigned)cdiv(nB_max, TC_N), (unsigned)cdiv(nA, TC_M), (unsigned)split);
+    lc.gridDim = dim3((unsigned)(cdiv(nB_max, TC_N) * cdiv(nA, TC_M)), 1, (unsigned)split);
     lc.blockDim = dim3(TC_THREADS);
     lc.dynamicSmemBytes = screen_tc_smem();
     lc.stream = st;
@@ -297,7 +310,7 @@ void launch_screen_tc(int nA, int64_t a0, const char *const *frow, const float *
     lc.attrs = at;
     lc.numAttrs = 1;
     FX_CUDA(cudaLaunchKernelEx(&lc, k_screen_tc, nA, a0, frow, fnorm, D, nB_dev, C32, snap, cn2, out, ld, kchunk, dbg,
-                               fnorm_out, sm, T, res_col, res_pos, nres));
+                               fnorm_out, sm, T, res_col, res_pos, nres, rowmin_g, snorm));
     FX_LAUNCHED();
 }
 
@@ -350,7 +363,7 @@ extern "C" int fx_debug_screen_tc(int32_t device, int64_t na, int64_t nb, int32_
         k_sqrt_inplace<<<(unsigned)cdiv(na, 256), 256>>>(na, nA2.p);  // fnorm = ||a||
         FX_LAUNCHED();
         launch_screen_tc((int)na, 0, rows.p, nA2.p, dim, nbd.p, (int)nb, dB.p, snap.p, nB2.p, dout.p, nb, st, nullptr,
-                         ScreenModel{}, 0.0, nullptr, nullptr, nullptr);
+                         ScreenModel{}, 0.0, nullptr, nullptr, nullptr, nullptr, nullptr);
         FX_CUDA(cudaDeviceSynchronize());
         FX_CUDA(cudaMemcpy(out, dout.p, sizeof(float) * na * nb, cudaMemcpyDeviceToHost));
     } catch (const Error &e) {

@@ -13,6 +13,8 @@ torch.cuda.synchronize()
 prof = fx.make_default_profiles(1000)["cheap"]
 for rep in range(2):
     s = fx.ingest.Stream(2048, 16, 1000, 4, t, m, 0.01, _lib.FX_F32, 0, 0)
+    if rep == 1:
+        s.set_timing(True)
     s.set_rank_model(prof, 0)
     t0 = time.perf_counter()
     s.ingest_device(n, d.oids.data_ptr(), d.fids.data_ptr(), d.sigs.data_ptr(), d.feats.data_ptr(), d.true_class.data_ptr())
@@ -21,3 +23,7 @@ for rep in range(2):
     c = s.counters()
     print(f"n={n} m={m} t={t}: {n / dt:.0f} obj/s ({dt:.2f} s) clusters={r.clusters_emitted} live={c['nlive']} "
           f"exact={r.exact_rechecks} seq={c['seq_steps']} windows={c['windows']}", flush=True)
+    if rep == 1:
+        tm = s.timings()
+        print({k: round(v, 1) for k, v in tm.items() if v}, flush=True)
+        print({k: v for k, v in c.items() if k.startswith("cyc") or k in ("windows", "seq_steps", "nevict_total")}, flush=True)

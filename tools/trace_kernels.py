@@ -1,6 +1,6 @@
 """Per-kernel device time of one C2 stream ingest + finalize, traced with
 CUPTI through torch.profiler (real pipelined run, not ncu-serialised).
-GPU box only:  python tools/trace_kernels.py [n_objects]"""
+GPU box only:  python tools/trace_kernels.py [n_objects [T [M]]]  (C3 shape: 300000 5.0 100000)"""
 import collections
 import os
 import sys
@@ -14,13 +14,15 @@ import paper_1801_03493_b200 as fx
 from paper_1801_03493_b200 import _lib, synth
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 1_000_000
+T = float(sys.argv[2]) if len(sys.argv) > 2 else 7.5
+M = int(sys.argv[3]) if len(sys.argv) > 3 else 100
 data = synth.generate(n, dim=2048, vocab=1000, n_stream_classes=100, seed=0)
 torch.cuda.synchronize()
 prof = fx.make_default_profiles(1000)["cheap"]
 
 
 def run():
-    s = fx.ingest.Stream(2048, 16, 1000, 4, 7.5, 100, 0.01, _lib.FX_F32, 0, 0)
+    s = fx.ingest.Stream(2048, 16, 1000, 4, T, M, 0.01, _lib.FX_F32, 0, 0)
     s.set_rank_model(prof, 0)
     s.ingest_device(n, data.oids.data_ptr(), data.fids.data_ptr(), data.sigs.data_ptr(), data.feats.data_ptr(),
                     data.true_class.data_ptr())
