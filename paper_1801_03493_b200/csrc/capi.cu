@@ -46,9 +46,12 @@ void run_query(fx_session *ss, int class_enc, int k_x, int mode, int keep_label,
                int64_t t0, int64_t t1, fx_query_result *res);
 void session_alloc_bits(fx_session *ss);
 
-__global__ void k_first_cls(int64_t n, const uint8_t *__restrict__ is_dup, unsigned long long *__restrict__ out) {
+// first classified object of the chunk: the one non-duplicate with no
+// classified object before it (excl = exclusive count of classified objects)
+__global__ void k_first_cls(int64_t n, const uint8_t *__restrict__ is_dup, const int64_t *__restrict__ excl,
+                            unsigned long long *__restrict__ out) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (i < n && !is_dup[i]) atomicMin(out, (unsigned long long)i);
+    if (i < n && !is_dup[i] && excl[i] == 0) *out = (unsigned long long)i;
 }
 
 // leading dups of a chunk attach to the previous chunk's last classified cluster
@@ -453,7 +456,7 @@ static void ingest_chunk(fx_stream *s, int64_t n, const int64_t *d_oid, const in
     DevBuf<unsigned long long> first;
     first.reserve(1);
     FX_CUDA(cudaMemsetAsync(first.p, 0xff, sizeof(unsigned long long), st));
-    k_first_cls<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(n, s->is_dup.p + n0, first.p);
+    k_first_cls<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(n, s->is_dup.p + n0, excl.p, first.p);
     FX_LAUNCHED();
     unsigned long long h_first = 0;
     FX_CUDA(cudaMemcpyAsync(&h_first, first.p, sizeof(h_first), cudaMemcpyDeviceToHost, st));
@@ -475,6 +478,7 @@ static void ingest_chunk(fx_stream *s, int64_t n, const int64_t *d_oid, const in
     }
     if (((uintptr_t)d_feats % 16) != 0 || ((int64_t)s->cfg.dim * s->esize) % 16 != 0) s->rows_aligned16 = false;
     launch_compact(s, n, n0, c0, s->is_dup.p + n0, excl.p, d_feats, compact);
+    s->arows = compact ? nc : n;
     if (!s->tc_screen || s->has_fc) launch_fnorm(s, c0, nc);  // else the TC screen computes the batch's norms
     // K1: top-K
     if (!d_topk && s->has_fc) {

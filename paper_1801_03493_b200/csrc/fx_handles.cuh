@@ -98,6 +98,11 @@ struct fx_stream {
     fx::DevBuf<float> sum_d1, sum_e1, sum_lbr;
     fx::DevBuf<int32_t> rowmin;          // [B+1] multi-tile TC screen: min lower bound per row (float bits)
     fx::DevBuf<float> snorm;             // [ld] snapshot column norms (TC screen)
+    const char *abase = nullptr;         // feature rows of the current ingest call (TMA tensor map)
+    int64_t arows = 0, a_cbase = 0, a_obj0 = 0;
+    bool a_compact = false;
+    fx::DevBuf<int32_t> orow;            // [rows of the call] classified index of each object row, -1: duplicate
+    fx::DevBuf<float> C32q;              // [ld*D] FP32 snapshot packed in snapshot order (TMA screen)
     fx::DevBuf<int32_t> cid_slot;        // [>= clusters created + 3B] slot of each cluster id
     fx::DevBuf<int32_t> s_fjoin;         // [nslots] first join position inside a window (scratch, INT_MAX)
     fx::DevBuf<int32_t> ev_pos, ev_vic;  // [B+1] window seed positions / eviction victims

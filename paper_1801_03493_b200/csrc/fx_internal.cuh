@@ -6,6 +6,7 @@
 // into FMA) in numpy's summation order, so results are bit-identical.
 #pragma once
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 

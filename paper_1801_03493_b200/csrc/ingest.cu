@@ -61,10 +61,11 @@ __global__ void k_dup_flags(int64_t n, int S, const int64_t *__restrict__ fid, c
 __global__ void k_compact_cls(int64_t n, int64_t obj_base, int64_t cls_base, const uint8_t *__restrict__ is_dup,
                               const int64_t *__restrict__ excl, const char *feat_base, int64_t row_bytes,
                               int compact, int64_t *__restrict__ cls_obj, const char **__restrict__ frow,
-                              int32_t *__restrict__ dup_run) {
+                              int32_t *__restrict__ dup_run, int32_t *__restrict__ orow) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= n) return;
     int64_t e = excl[i];
+    if (orow) orow[i] = is_dup[i] ? -1 : (int32_t)(cls_base + e);  // object row -> classified index
     if (!is_dup[i]) {
         int64_t c = cls_base + e;
         cls_obj[c] = obj_base + i;
@@ -2202,7 +2203,15 @@ __global__ void __launch_bounds__(256) k_seal_dist(int64_t nfeat_total, int D, c
     const int wpb = blockDim.x >> 5, w = threadIdx.x >> 5;
     const int per = plan->n_chains + plan->n_leaves + plan->n_ops;
     double *scr = sscratch + w * per;
-    for (int64_t m = (int64_t)blockIdx.x * wpb + w; m < nfeat_total; m += (int64_t)gridDim.x * wpb) {
+    // each warp takes a contiguous run of members (members are grouped by
+    // cluster): the per-cluster minimum is kept in a register and published
+    // with one atomic per cluster run, not one per member
+    const int64_t nw = (int64_t)gridDim.x * wpb, gw = (int64_t)blockIdx.x * wpb + w;
+    const int64_t chunk = (nfeat_total + nw - 1) / nw;
+    const int64_t m0 = gw * chunk, m1 = min(nfeat_total, m0 + chunk);
+    int cur = -1;
+    unsigned long long best = ~0ull;
+    for (int64_t m = m0; m < m1; m++) {
         const int cid = fmem_cid[m];
         const T *f = (const T *)frow[fmem_cls[m]];
         const double *c = fcent + (int64_t)cid * D;
@@ -2213,9 +2222,15 @@ __global__ void __launch_bounds__(256) k_seal_dist(int64_t nfeat_total, int D, c
         double d = __dsqrt_rn(s);
         if ((threadIdx.x & 31) == 0) {
             dout[m] = d;
-            atomicMin(&best_bits[cid], (unsigned long long)__double_as_longlong(d));
+            if (cid != cur) {
+                if (cur >= 0) atomicMin(&best_bits[cur], best);
+                cur = cid;
+                best = ~0ull;
+            }
+            best = min(best, (unsigned long long)__double_as_longlong(d));
         }
     }
+    if ((threadIdx.x & 31) == 0 && cur >= 0) atomicMin(&best_bits[cur], best);
 }
 
 __global__ void k_seal_pick(int64_t nfeat_total, const int32_t *__restrict__ fmem_cid, const int64_t *__restrict__ foff,
@@ -2235,7 +2250,9 @@ __global__ void k_seal_pick(int64_t nfeat_total, const int32_t *__restrict__ fme
 void launch_screen_tc(int nA, int64_t a0, const char *const *frow, const float *fnorm, int D, const int64_t *nB_dev,
                       int nB_max, const float *C32, const int32_t *snap, const float *cn2, float *out, int64_t ld,
                       cudaStream_t st, float *fnorm_out, ScreenModel sm, double T, int32_t *res_col,
-                      int32_t *res_pos, int64_t *nres, int *rowmin_g, float *snorm);
+                      int32_t *res_pos, int64_t *nres, int *rowmin_g, float *snorm,
+                      const CUtensorMap *tmA, const CUtensorMap *tmB, int rbase, int nR, const int32_t *rmap);
+bool make_rows_map(CUtensorMap *tm, const void *base, int64_t rows, int D, int64_t row_bytes, int box_rows);
 int64_t scan_i32_to_i64(const int32_t *in, int64_t n, int64_t *out_excl, cudaStream_t st, int64_t *scratch_total);
 void scan_u8_to_i64(const uint8_t *in, int64_t n, int invert, int64_t *out_excl, int64_t *d_total, cudaStream_t st);
 
@@ -2250,6 +2267,29 @@ size_t resolve_smem(int Bc, const PwPlan &P) {
     return (size_t)RS_WCNT_BYTES + (size_t)Bc * (9 * 4 + 2 + 1) + 16 + sizeof(double) * (P.n_chains + P.n_leaves + P.n_ops + 8);
 }
 
+// FP32 snapshot packed in snapshot order (TMA boxes of the TC screen need
+// consecutive rows): C32q[q] = C32[snap[q]], q < nsnap.
+__global__ void k_snap_pack(const int64_t *__restrict__ ctr, const int32_t *__restrict__ snap,
+                            const float *__restrict__ C32, float *__restrict__ C32q, int D) {
+    const int nsnap = (int)ctr[C_NSNAP];
+    const int n4 = D >> 2;
+    for (int q = blockIdx.x; q < nsnap; q += gridDim.x) {
+        const float4 *src = (const float4 *)(C32 + (int64_t)snap[q] * D);
+        float4 *dst = (float4 *)(C32q + (int64_t)q * D);
+        for (int k = threadIdx.x; k < n4; k += blockDim.x) dst[k] = src[k];
+    }
+}
+
+// object rows (relative to the ingest call's feature rows) of the first and
+// last classified object of each batch
+__global__ void k_batch_rows(int nb, const int64_t *__restrict__ cfirst, const int64_t *__restrict__ clast,
+                             const int64_t *__restrict__ cls_obj, int64_t obj0, int64_t *__restrict__ out) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= nb) return;
+    out[2 * i] = cls_obj[cfirst[i]] - obj0;
+    out[2 * i + 1] = cls_obj[clast[i]] - obj0;
+}
+
 template <typename T>
 void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
     cudaStream_t st = s->st;
@@ -2259,6 +2299,47 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
     // TF32 dot error gamma = 2^-9 + D 2^-22 (operand rounding + FP32 accumulation), d^2 error 2 gamma |a||b|
     const double gam = 1.953125e-03 + (double)D * 2.384185791015625e-07;
     const ScreenModel sm{s->tc_screen ? 1 : 0, rel, absc, (float)(2.0 * gam * 1.01), (float)(256.0 * 5.9604644775390625e-08)};
+    // TMA operand staging for the TC screen (fp32 rows, 16-byte aligned): A
+    // boxes over the ingest call's feature rows, B boxes over the packed snapshot
+    CUtensorMap tmA, tmB;
+    static const bool tma_off = getenv("FOCUS_B200_TCLOAD") && std::string(getenv("FOCUS_B200_TCLOAD")) == "cp";
+    bool tma = s->tc_screen && sizeof(T) == 4 && !tma_off && s->abase && s->rows_aligned16 && D % 4 == 0;
+    if (tma) {
+        s->C32q.reserve((size_t)s->ld * D);
+        tma = make_rows_map(&tmA, s->abase, s->arows, D, (int64_t)D * 4, 128) &&
+              make_rows_map(&tmB, s->C32q.p, s->ld, D, (int64_t)D * 4, 128);
+    }
+    // batch boundaries (as the loop below forms them) and, for features with
+    // duplicate rows, each batch's span of object rows (one readback per call)
+    std::vector<int64_t> bfirst, blast, brows;
+    if (tma) {
+        for (int64_t c0 = c_begin, B = 0; c0 < c_end; c0 += B) {
+            const int64_t cap = std::max<int64_t>(64, (std::max<int64_t>(c0, 0) / 4 / 64) * 64);
+            B = std::min<int64_t>(std::min<int64_t>(s->B, cap), c_end - c0);
+            bfirst.push_back(c0);
+            blast.push_back(c0 + B - 1);
+        }
+        const int nb = (int)bfirst.size();
+        brows.resize(2 * (size_t)nb);
+        if (s->a_compact) {
+            for (int i = 0; i < nb; i++) {
+                brows[2 * i] = bfirst[i] - s->a_cbase;
+                brows[2 * i + 1] = blast[i] - s->a_cbase;
+            }
+        } else if (nb > 0) {
+            DevBuf<int64_t> d_in, d_out;
+            d_in.reserve(2 * (size_t)nb);
+            d_out.reserve(2 * (size_t)nb);
+            FX_CUDA(cudaMemcpyAsync(d_in.p, bfirst.data(), sizeof(int64_t) * nb, cudaMemcpyHostToDevice, st));
+            FX_CUDA(cudaMemcpyAsync(d_in.p + nb, blast.data(), sizeof(int64_t) * nb, cudaMemcpyHostToDevice, st));
+            k_batch_rows<<<(unsigned)cdiv(nb, 256), 256, 0, st>>>(nb, d_in.p, d_in.p + nb, s->cls_obj.p, s->a_obj0,
+                                                                 d_out.p);
+            FX_LAUNCHED();
+            FX_CUDA(cudaMemcpyAsync(brows.data(), d_out.p, sizeof(int64_t) * 2 * nb, cudaMemcpyDeviceToHost, st));
+            FX_CUDA(cudaStreamSynchronize(st));
+        }
+    }
+    int bi = 0;
     using hclock = std::chrono::steady_clock;
     auto hms = [](hclock::time_point a, hclock::time_point b) {
         return std::chrono::duration<double, std::milli>(b - a).count();
@@ -2267,7 +2348,7 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
     std::vector<int32_t> chk_slots;
     // fused row pass: FP32 rows, D % 4 == 0, D <= 2048, 16-byte aligned rows
     const bool rowpass = sizeof(T) == 4 && D % 4 == 0 && D <= 2048 && s->rows_aligned16;
-    for (int64_t c0 = c_begin, B = 0; c0 < c_end; c0 += B) {
+    for (int64_t c0 = c_begin, B = 0; c0 < c_end; c0 += B, bi++) {
         const auto h0 = hclock::now();
         // the drift bound grows like (batch size / objects so far): keep batches
         // at <= 1/4 of the stream's age so young clusters stay decidable by bounds
@@ -2282,10 +2363,19 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             // the screen also produces ||f|| of the batch rows (fnorm) unless an earlier pass did
             // fused: residual detection when the snapshot fits one column tile
             fused_res = s->ld <= 128;
+            int rbase = 0, nR = B;
+            if (tma) {
+                rbase = (int)brows[2 * bi];
+                nR = (int)(brows[2 * bi + 1] - brows[2 * bi] + 1);
+                k_snap_pack<<<(unsigned)std::min<int64_t>(s->ld, 148 * 4), 128, 0, st>>>(s->ctr.p, s->snap_slot.p,
+                                                                                        s->C32.p, s->C32q.p, D);
+                FX_LAUNCHED();
+            }
             launch_screen_tc(B, c0, s->frow.p, s->fnorm.p, D, s->ctr.p + C_NSNAP, (int)s->ld, s->C32.p,
                              s->snap_slot.p, s->s_cn2.p, s->dist.p, s->ld, st, s->has_fc ? nullptr : s->fnorm.p, sm,
                              s->cfg.t, fused_res ? s->res_col.p : nullptr, s->res_pos.p, s->ctr.p + C_NRES,
-                             s->rowmin.p, s->snorm.p);
+                             s->rowmin.p, s->snorm.p, tma ? &tmA : nullptr, tma ? &tmB : nullptr, rbase, nR,
+                             s->a_compact ? nullptr : s->orow.p);
         } else {
             const unsigned grid = (unsigned)std::min<int64_t>(cdiv(s->ld, SC_T) * cdiv(B, SC_T), 148 * 8);
             FromSnapshot fb{s->C32.p, s->snap_slot.p, D};
@@ -2558,8 +2648,14 @@ void launch_dup_flags(fx_stream *s, int64_t n, const int64_t *d_fid, const doubl
 void launch_compact(fx_stream *s, int64_t n, int64_t obj_base, int64_t cls_base, const uint8_t *d_dup,
                     const int64_t *d_excl, const char *feat_base, int compact) {
     const int64_t row_bytes = (int64_t)s->cfg.dim * s->esize;
+    s->orow.grow(n, 0, s->st);
     k_compact_cls<<<(unsigned)cdiv(n, 256), 256, 0, s->st>>>(n, obj_base, cls_base, d_dup, d_excl, feat_base,
-                                                             row_bytes, compact, s->cls_obj.p, s->frow.p, s->dup_run.p);
+                                                             row_bytes, compact, s->cls_obj.p, s->frow.p, s->dup_run.p,
+                                                             compact ? nullptr : s->orow.p);
+    s->abase = feat_base;
+    s->a_compact = compact != 0;
+    s->a_cbase = cls_base;
+    s->a_obj0 = obj_base;
     FX_LAUNCHED();
     k_dup_runs<<<(unsigned)cdiv(n, 256), 256, 0, s->st>>>(n, cls_base, d_dup, d_excl, s->dup_run.p);
     FX_LAUNCHED();

@@ -22,8 +22,11 @@
 // thread; tcgen05.commit on a per-stage mbarrier releases a stage.
 #include <algorithm>
 #include <cstdlib>
+#include <string>
 
 #include <cooperative_groups.h>
+#include <cuda.h>
+#include <cudaTypedefs.h>
 
 #include "fx_handles.cuh"
 #include "tc_common.cuh"
@@ -35,7 +38,24 @@ namespace fx {
 constexpr int TC_M = 128, TC_N = 128, TC_STAGES = 6, TC_THREADS = 256;  // warps 4-7 only help load
 constexpr int TC_TILE_BYTES = TC_M * TC_KT * 4;  // 16 KB per operand per stage
 
+// Operand staging by TMA (TMA = true): one 2-D tiled box (32 fp32 x 128 rows,
+// SWIZZLE_128B K-major: 8-row x 128 B atoms, 16-byte chunk c of row r at
+// c ^ (r % 8)) per operand and stage.  A = consecutive feature rows of the
+// ingest call (tmA): with compact features the batch's rows themselves, else
+// the object rows spanning the batch, duplicates included -- rmap gives each
+// object row's classified index (-1: duplicate, its outputs are dropped).
+// B = the snapshot packed in snapshot order (tmB over C32q, k_snap_pack).
+// One producer thread, one MMA-issuing thread, four warps that fold the row
+// norms out of each stage; per-stage full barriers count bytes (expect_tx),
+// empty barriers the MMA commit plus the four norm warps.
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+    // K-major SWIZZLE_128B: SBO = 1024 B between 8-row atoms, LBO unused (1), version 1, layout 2
+    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+           ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
 // out[a][q] = ||A_a||^2 + ||B_q||^2 - 2 A_a.B_q   (float, not clamped)
+template <bool TMA>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0, const char *const *__restrict__ frow,
                                                            const float *fnorm, int D,  // aliases fnorm_out
                                                            const int64_t *__restrict__ nB_dev,
@@ -45,50 +65,70 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
                                                            int64_t ld, int kchunk, int dbg, float *__restrict__ fnorm_out,
                                                            ScreenModel sm, double T, int32_t *__restrict__ res_col,
                                                            int32_t *__restrict__ res_pos, int64_t *__restrict__ nres,
-                                                           int *__restrict__ rowmin_g, float *__restrict__ snorm) {
+                                                           int *__restrict__ rowmin_g, float *__restrict__ snorm,
+                                                           const __grid_constant__ CUtensorMap tmA,
+                                                           const __grid_constant__ CUtensorMap tmB, int rbase, int nR,
+                                                           const int32_t *__restrict__ rmap) {
     // blockIdx.z selects the K range [z*kchunk, (z+1)*kchunk) (split-K when the
     // tile grid alone cannot fill the machine; partials are atomically added).
     // blockIdx.x = column tile * row tiles + row tile: the CTAs that share a
     // snapshot tile run back to back, so it streams from HBM once per batch.
     const int nB = (int)*nB_dev;
-    const int nrt = (nA + TC_M - 1) / TC_M;
+    // tile rows: batch rows (rmap == nullptr) or the object rows rbase.. of tmA
+    const int nrt = (nR + TC_M - 1) / TC_M;
     const int tb = (int)(blockIdx.x / nrt) * TC_N, ta = (int)(blockIdx.x % nrt) * TC_M;
-    if (nB == 0 && tb == 0 && blockIdx.z == 0 && threadIdx.x < TC_M && ta + (int)threadIdx.x < nA) {
+    auto row_cls = [&](int tr) {  // batch-local classified index of tile-space row tr, -1: none
+        if (tr >= nR) return -1;
+        if (!rmap) return tr < nA ? tr : -1;
+        const int c = rmap[rbase + tr];
+        return c >= 0 ? (int)(c - a0) : -1;
+    };
+    if (nB == 0 && tb == 0 && blockIdx.z == 0 && threadIdx.x < TC_M) {
         // empty snapshot (stream start): no screen, but the batch still needs ||f||
-        if (fnorm_out) {
-            const float *row = (const float *)frow[a0 + ta + threadIdx.x];
+        const int a = row_cls(ta + threadIdx.x);
+        if (a >= 0 && fnorm_out) {
+            const float *row = (const float *)frow[a0 + a];
             float tot = 0.f;
             for (int k0 = 0; k0 < D; k0 += TC_KT) {
                 float p = 0.f;
                 for (int k = k0; k < min(D, k0 + TC_KT); k++) p = fmaf(row[k], row[k], p);
                 tot += p;
             }
-            fnorm_out[a0 + ta + threadIdx.x] = sqrtf(tot);
+            fnorm_out[a0 + a] = sqrtf(tot);
         }
-        if (res_col) {  // no live cluster: every object is a probable seed
+        if (a >= 0 && res_col) {  // no live cluster: every object is a probable seed
             const int col = (int)atomicAdd((unsigned long long *)nres, 1ull);
-            res_pos[col] = ta + threadIdx.x;
-            res_col[ta + threadIdx.x] = col;
+            res_pos[col] = a;
+            res_col[a] = col;
         }
     }
-    if (tb >= nB || ta >= nA) return;
-    extern __shared__ __align__(1024) unsigned char smem[];
-    // [stage][A 16KB | B 16KB]
+    if (tb >= nB || ta >= nR || (dbg & 8)) return;
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    // [stage][A 16KB | B 16KB], 1024-byte aligned (SWIZZLE_128B atoms)
+    unsigned char *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     __shared__ const float *rowsA[TC_M];
     __shared__ const float *rowsB[TC_N];
+    __shared__ int rcls[TC_M];  // batch-local classified index of each tile row, -1: none
     __shared__ __align__(8) uint64_t bar_stage[TC_STAGES];
+    __shared__ __align__(8) uint64_t bar_full[TC_STAGES];
     __shared__ __align__(8) uint64_t bar_done;
     __shared__ uint32_t tmem_base;
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     for (int r = tid; r < TC_M; r += TC_THREADS) {
-        const int a = ta + r;
-        rowsA[r] = a < nA ? (const float *)frow[a0 + a] : nullptr;
-        const int b = tb + r;
-        rowsB[r] = b < nB ? C32 + (int64_t)snap[b] * D : nullptr;
+        const int a = row_cls(ta + r);
+        rcls[r] = a;
+        if (!TMA) {
+            const int b = tb + r;
+            rowsA[r] = a >= 0 ? (const float *)frow[a0 + a] : nullptr;
+            rowsB[r] = b < nB ? C32 + (int64_t)snap[b] * D : nullptr;
+        }
     }
     if (tid == 0) {
-        for (int s = 0; s < TC_STAGES; s++) mbar_init(&bar_stage[s], 1);
+        for (int s = 0; s < TC_STAGES; s++) {
+            mbar_init(&bar_stage[s], TMA ? 5 : 1);
+            mbar_init(&bar_full[s], 1);
+        }
         mbar_init(&bar_done, 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
     }
@@ -108,68 +148,143 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
     // instruction descriptor: D=F32, A=B=TF32, K-major both, N=128, M=128
     const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TC_N >> 3) << 17) |
                            ((uint32_t)(TC_M >> 4) << 24);
-    // prologue: stages 0..S-2
-    for (int s = 0; s < TC_STAGES - 1; s++) {
-        if (s < nk && !(dbg & 1)) {
-            const uint32_t st = sbase + s * 2 * TC_TILE_BYTES;
-            load_tile<TC_M, TC_THREADS>(st, rowsA, kbeg + s * TC_KT, kend, fnorm);
-            load_tile<TC_N, TC_THREADS>(st + TC_TILE_BYTES, rowsB, kbeg + s * TC_KT, kend, fnorm);
-        }
-        asm volatile("cp.async.commit_group;\n" ::);
-    }
     float a2 = 0.f;  // ||A_row||^2 of this thread's row over the CTA's K range (fp32, per-stage partials)
-    for (int it = 0; it < nk; it++) {
-        const int s = it % TC_STAGES;
-        asm volatile("cp.async.wait_group %0;\n" ::"n"(TC_STAGES - 2));
-        asm volatile("fence.proxy.async.shared::cta;\n" ::);
-        __syncthreads();
-        if (tid < TC_M) {  // the row norm rides along: row tid's 32 values of this stage (stable until its refill)
-            const unsigned char *stg = smem + s * 2 * TC_TILE_BYTES;
-            float p = 0.f;
-#pragma unroll
-            for (int c = 0; c < TC_KT / 4; c++) {
-                const float4 x = *(const float4 *)(stg + ((((tid >> 3) * (TC_KT / 4) + c) << 7) + ((tid & 7) << 4)));
-                p = fmaf(x.x, x.x, p);
-                p = fmaf(x.y, x.y, p);
-                p = fmaf(x.z, x.z, p);
-                p = fmaf(x.w, x.w, p);
-            }
-            a2 += p;
-        }
-        if (tid == 0 && !(dbg & 2)) {
-            asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
-            const uint32_t st = sbase + s * 2 * TC_TILE_BYTES;
-#pragma unroll
-            for (int kk = 0; kk < TC_KT / 8; kk++) {
-                const uint64_t da = umma_desc(st + kk * 256, 128, TC_KT * 32);
-                const uint64_t db = umma_desc(st + TC_TILE_BYTES + kk * 256, 128, TC_KT * 32);
-                const uint32_t acc = (it > 0 || kk > 0) ? 1u : 0u;
+    if (TMA) {
+        if (warp == 4 && lane == 0) {  // producer: one 128-row box of A and of B per stage
+            asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmA) : "memory");
+            asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmB) : "memory");
+            for (int it = 0; it < nk; it++) {
+                const int s = it % TC_STAGES;
+                if (it >= TC_STAGES) mbar_wait(&bar_stage[s], (uint32_t)(((it / TC_STAGES) - 1) & 1));
+                const uint32_t st = sbase + s * 2 * TC_TILE_BYTES;
+                const uint32_t fb = smem_u32(&bar_full[s]);
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(fb), "r"(2 * TC_TILE_BYTES)
+                             : "memory");
+                const int k = kbeg + it * TC_KT;
                 asm volatile(
-                    "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                    "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
-                    "l"(da), "l"(db), "r"(idesc), "r"(acc));
+                    "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+                    "%3}], [%4];\n" ::"r"(st),
+                    "l"(&tmA), "r"(k), "r"(rbase + ta), "r"(fb)
+                    : "memory");
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+                    "%3}], [%4];\n" ::"r"(st + TC_TILE_BYTES),
+                    "l"(&tmB), "r"(k), "r"(tb), "r"(fb)
+                    : "memory");
             }
-            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                smem_u32(&bar_stage[s])));
-        }
-        // refill the stage consumed S-1 iterations from now
-        const int nt = it + TC_STAGES - 1;
-        if (nt < nk) {
-            const int ns = nt % TC_STAGES;
-            if (nt >= TC_STAGES && !(dbg & 2)) mbar_wait(&bar_stage[ns], (uint32_t)(((nt / TC_STAGES) - 1) & 1));
-            const uint32_t st = sbase + ns * 2 * TC_TILE_BYTES;
-            if (!(dbg & 1)) {
-                load_tile<TC_M, TC_THREADS>(st, rowsA, kbeg + nt * TC_KT, kend, fnorm);
-                load_tile<TC_N, TC_THREADS>(st + TC_TILE_BYTES, rowsB, kbeg + nt * TC_KT, kend, fnorm);
+        } else if (warp == 5) {  // MMA issue
+            for (int it = 0; it < nk; it++) {
+                const int s = it % TC_STAGES;
+                mbar_wait(&bar_full[s], (uint32_t)((it / TC_STAGES) & 1));
+                if (lane == 0) {
+                    asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+                    const uint32_t st = sbase + s * 2 * TC_TILE_BYTES;
+#pragma unroll
+                    for (int kk = 0; kk < TC_KT / 8; kk++) {
+                        const uint64_t da = umma_desc_sw128(st + kk * 32);
+                        const uint64_t db = umma_desc_sw128(st + TC_TILE_BYTES + kk * 32);
+                        const uint32_t acc = (it > 0 || kk > 0) ? 1u : 0u;
+                        asm volatile(
+                            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                            "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+                            "l"(da), "l"(db), "r"(idesc), "r"(acc));
+                    }
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                        smem_u32(&bar_stage[s])));
+                }
+                __syncwarp();
+            }
+            if (lane == 0)
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                    smem_u32(&bar_done)));
+        } else if (warp < 4) {  // row norms: row tid's 8 chunks of 16 B in the swizzled atom
+            for (int it = 0; it < nk; it++) {
+                const int s = it % TC_STAGES;
+                mbar_wait(&bar_full[s], (uint32_t)((it / TC_STAGES) & 1));
+                const unsigned char *row = smem + s * 2 * TC_TILE_BYTES + (tid >> 3) * 1024 + (tid & 7) * 128;
+                float p = 0.f;
+#pragma unroll
+                for (int c = 0; c < TC_KT / 4; c++) {
+                    const float4 x = *(const float4 *)(row + ((c ^ (tid & 7)) << 4));
+                    p = fmaf(x.x, x.x, p);
+                    p = fmaf(x.y, x.y, p);
+                    p = fmaf(x.z, x.z, p);
+                    p = fmaf(x.w, x.w, p);
+                }
+                a2 += p;
+                __syncwarp();
+                if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&bar_stage[s])));
             }
         }
-        asm volatile("cp.async.commit_group;\n" ::);
+    } else {
+        auto kof = [&](int i) { return kbeg + i * TC_KT; };
+        // prologue: stages 0..S-2
+        for (int s = 0; s < TC_STAGES - 1; s++) {
+            if (s < nk && !(dbg & 1)) {
+                const uint32_t st = sbase + s * 2 * TC_TILE_BYTES;
+                load_tile<TC_M, TC_THREADS>(st, rowsA, kof(s), kend, fnorm);
+                load_tile<TC_N, TC_THREADS>(st + TC_TILE_BYTES, rowsB, kof(s), kend, fnorm);
+            }
+            asm volatile("cp.async.commit_group;\n" ::);
+        }
+        for (int it = 0; it < nk; it++) {
+            const int s = it % TC_STAGES;
+            asm volatile("cp.async.wait_group %0;\n" ::"n"(TC_STAGES - 2));
+            asm volatile("fence.proxy.async.shared::cta;\n" ::);
+            __syncthreads();
+            if (tid < TC_M) {  // the row norm rides along: row tid's 32 values of this stage (stable until its refill)
+                const unsigned char *stg = smem + s * 2 * TC_TILE_BYTES;
+                float p = 0.f;
+#pragma unroll
+                for (int c = 0; c < TC_KT / 4; c++) {
+                    const float4 x = *(const float4 *)(stg + ((((tid >> 3) * (TC_KT / 4) + c) << 7) + ((tid & 7) << 4)));
+                    p = fmaf(x.x, x.x, p);
+                    p = fmaf(x.y, x.y, p);
+                    p = fmaf(x.z, x.z, p);
+                    p = fmaf(x.w, x.w, p);
+                }
+                a2 += p;
+            }
+            if (tid == 0 && !(dbg & 2)) {
+                asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+                const uint32_t st = sbase + s * 2 * TC_TILE_BYTES;
+#pragma unroll
+                for (int kk = 0; kk < TC_KT / 8; kk++) {
+                    const uint64_t da = umma_desc(st + kk * 256, 128, TC_KT * 32);
+                    const uint64_t db = umma_desc(st + TC_TILE_BYTES + kk * 256, 128, TC_KT * 32);
+                    const uint32_t acc = (it > 0 || kk > 0) ? 1u : 0u;
+                    asm volatile(
+                        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+                        "l"(da), "l"(db), "r"(idesc), "r"(acc));
+                }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                    smem_u32(&bar_stage[s])));
+            }
+            // refill the stage consumed S-1 iterations from now
+            const int nt = it + TC_STAGES - 1;
+            if (nt < nk) {
+                const int ns = nt % TC_STAGES;
+                if (nt >= TC_STAGES && !(dbg & 2)) mbar_wait(&bar_stage[ns], (uint32_t)(((nt / TC_STAGES) - 1) & 1));
+                const uint32_t st = sbase + ns * 2 * TC_TILE_BYTES;
+                if (!(dbg & 1)) {
+                    load_tile<TC_M, TC_THREADS>(st, rowsA, kof(nt), kend, fnorm);
+                    load_tile<TC_N, TC_THREADS>(st + TC_TILE_BYTES, rowsB, kof(nt), kend, fnorm);
+                }
+            }
+            asm volatile("cp.async.commit_group;\n" ::);
+        }
     }
-    if (tid == 0 && !(dbg & 2))
+    if (!TMA && tid == 0 && !(dbg & 2))
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
             smem_u32(&bar_done)));
     if (!(dbg & 2)) mbar_wait(&bar_done, 0);
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+    if (dbg & 4) {  // timing probe: no epilogue
+        __syncthreads();
+        if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TC_N));
+        return;
+    }
 
     // epilogue: warp w owns TMEM lanes 32w..32w+31 = tile rows.  The partial
     // dot products go to a [128][TC_N+1] tile in this CTA's (now idle)
@@ -212,8 +327,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
     __syncthreads();
     for (int e = tid; e < rows_per * nc4; e += TC_THREADS) {
         const int rr = rank * rows_per + e / nc4, c = (e % nc4) * 4;
-        const int a = ta + rr;
-        if (a >= nA) continue;
+        const int a = rcls[rr];
+        if (a < 0) continue;
         float4 dot = make_float4(0.f, 0.f, 0.f, 0.f);
         float fa2 = 0.f;
 #pragma unroll
@@ -252,14 +367,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
         // several column tiles: per-row minimum across CTAs (k_res_from_min flags the residuals)
         __syncthreads();
         for (int rr = rank * rows_per + tid; rr < (rank + 1) * rows_per; rr += TC_THREADS)
-            if (ta + rr < nA) atomicMin(&rowmin_g[ta + rr], rowmin[rr]);
+            if (rcls[rr] >= 0) atomicMin(&rowmin_g[rcls[rr]], rowmin[rr]);
     } else if (res_col) {
         // fused residual detection (one column tile = the whole snapshot):
         // objects with no snapshot centroid whose lower bound is <= T
         __syncthreads();
         for (int rr = rank * rows_per + tid; rr < (rank + 1) * rows_per; rr += TC_THREADS) {
-            const int a = ta + rr;
-            if (a >= nA) continue;
+            const int a = rcls[rr];
+            if (a < 0) continue;
             if ((double)__int_as_float(rowmin[rr]) > T) {
                 const int col = (int)atomicAdd((unsigned long long *)nres, 1ull);
                 res_pos[col] = a;
@@ -274,23 +389,55 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TC_N));
 }
 
-size_t screen_tc_smem() { return (size_t)TC_STAGES * 2 * TC_TILE_BYTES; }
+size_t screen_tc_smem() { return (size_t)TC_STAGES * 2 * TC_TILE_BYTES + 1024; }
+
+// 2-D tensor map over fp32 rows for tile::gather4 (box 32 x 1, SWIZZLE_128B).
+// False when the driver rejects it (alignment): the caller keeps cp.async.
+bool make_rows_map(CUtensorMap *tm, const void *base, int64_t rows, int D, int64_t row_bytes, int box_rows) {
+    static PFN_cuTensorMapEncodeTiled fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void **)&fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            fn = nullptr;
+        if (!fn) return false;
+    }
+    if (rows <= 0 || ((uintptr_t)base & 15) || (row_bytes & 15)) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)row_bytes};
+    cuuint32_t box[2] = {(cuuint32_t)TC_KT, (cuuint32_t)box_rows};
+    cuuint32_t es[2] = {1, 1};
+    return fn(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void *>(base), dims, strides, box, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
 
 void launch_screen_tc(int nA, int64_t a0, const char *const *frow, const float *fnorm, int D, const int64_t *nB_dev,
                       int nB_max, const float *C32, const int32_t *snap, const float *cn2, float *out, int64_t ld,
                       cudaStream_t st, float *fnorm_out, ScreenModel sm, double T, int32_t *res_col,
-                      int32_t *res_pos, int64_t *nres, int *rowmin_g, float *snorm) {
+                      int32_t *res_pos, int64_t *nres, int *rowmin_g, float *snorm, const CUtensorMap *tmA,
+                      const CUtensorMap *tmB, int rbase, int nR, const int32_t *rmap) {
     // residual detection inside one tile, or across tiles through rowmin_g
     if (nB_max > TC_N) res_col = nullptr;
     else rowmin_g = nullptr;
     static bool attr = false;
     if (!attr) {
-        FX_CUDA(cudaFuncSetAttribute(k_screen_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)screen_tc_smem()));
+        FX_CUDA(cudaFuncSetAttribute(k_screen_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)screen_tc_smem()));
+        FX_CUDA(cudaFuncSetAttribute(k_screen_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)screen_tc_smem()));
         attr = true;
     }
+    const bool tma = tmA && tmB;
+    static const CUtensorMap zero_map = {};
     static const int dbg = getenv("FOCUS_B200_TCDBG") ? atoi(getenv("FOCUS_B200_TCDBG")) : 0;
     static const int split_env = getenv("FOCUS_B200_TCSPLIT") ? atoi(getenv("FOCUS_B200_TCSPLIT")) : 0;
-    const int64_t tiles = cdiv(nB_max, TC_N) * cdiv(nA, TC_M);
+    if (!tma) {  // cp.async staging gathers the batch rows themselves
+        rbase = 0;
+        nR = nA;
+        rmap = nullptr;
+    }
+    const int64_t tiles = cdiv(nB_max, TC_N) * cdiv(nR, TC_M);
     int split = 1;
     while (tiles * split * 2 <= 148 && D / (split * 2) >= 4 * TC_KT) split *= 2;
     if (split_env > 0) split = split_env;
@@ -298,7 +445,7 @@ void launch_screen_tc(int nA, int64_t a0, const char *const *frow, const float *
     while (TC_M % split) split--;
     const int kchunk = (int)(cdiv(cdiv(D, split), TC_KT) * TC_KT);
     cudaLaunchConfig_t lc = {};
-    lc.gridDim = dim3((unsigned)(cdiv(nB_max, TC_N) * cdiv(nA, TC_M)), 1, (unsigned)split);
+    lc.gridDim = dim3((unsigned)(cdiv(nB_max, TC_N) * cdiv(nR, TC_M)), 1, (unsigned)split);
     lc.blockDim = dim3(TC_THREADS);
     lc.dynamicSmemBytes = screen_tc_smem();
     lc.stream = st;
@@ -309,8 +456,9 @@ void launch_screen_tc(int nA, int64_t a0, const char *const *frow, const float *
     at[0].val.clusterDim.z = (unsigned)split;
     lc.attrs = at;
     lc.numAttrs = 1;
-    FX_CUDA(cudaLaunchKernelEx(&lc, k_screen_tc, nA, a0, frow, fnorm, D, nB_dev, C32, snap, cn2, out, ld, kchunk, dbg,
-                               fnorm_out, sm, T, res_col, res_pos, nres, rowmin_g, snorm));
+    FX_CUDA(cudaLaunchKernelEx(&lc, tma ? k_screen_tc<true> : k_screen_tc<false>, nA, a0, frow, fnorm, D, nB_dev, C32,
+                               snap, cn2, out, ld, kchunk, dbg, fnorm_out, sm, T, res_col, res_pos, nres, rowmin_g,
+                               snorm, tma ? *tmA : zero_map, tma ? *tmB : zero_map, rbase, nR, rmap));
     FX_LAUNCHED();
 }
 
@@ -362,8 +510,14 @@ extern "C" int fx_debug_screen_tc(int32_t device, int64_t na, int64_t nb, int32_
         k_iota32<<<(unsigned)cdiv(nb, 256), 256>>>(nb, snap.p);
         k_sqrt_inplace<<<(unsigned)cdiv(na, 256), 256>>>(na, nA2.p);  // fnorm = ||a||
         FX_LAUNCHED();
+        CUtensorMap tmA, tmB;
+        const char *mode = getenv("FOCUS_B200_TCLOAD");
+        const bool tma = !(mode && std::string(mode) == "cp") &&
+                         make_rows_map(&tmA, dA.p, na, dim, (int64_t)dim * 4, TC_M) &&
+                         make_rows_map(&tmB, dB.p, nb, dim, (int64_t)dim * 4, TC_N);
         launch_screen_tc((int)na, 0, rows.p, nA2.p, dim, nbd.p, (int)nb, dB.p, snap.p, nB2.p, dout.p, nb, st, nullptr,
-                         ScreenModel{}, 0.0, nullptr, nullptr, nullptr, nullptr, nullptr);
+                         ScreenModel{}, 0.0, nullptr, nullptr, nullptr, nullptr, nullptr, tma ? &tmA : nullptr,
+                         tma ? &tmB : nullptr, 0, (int)na, nullptr);
         FX_CUDA(cudaDeviceSynchronize());
         FX_CUDA(cudaMemcpy(out, dout.p, sizeof(float) * na * nb, cudaMemcpyDeviceToHost));
     } catch (const Error &e) {

@@ -47,11 +47,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
 template <int NR, int NT>
 __device__ __forceinline__ void load_tile(uint32_t sbase, const float *const *rows, int k0, int D,
                                           const void *dummy) {
-    // NR rows x (KT/4 = 8) chunks of 16 bytes over NT threads
+    // NR rows x (KT/4 = 8) chunks of 16 bytes over NT threads.  A warp takes
+    // 8 rows x 4 chunks: its 32 shared-memory writes fall in 8 distinct
+    // 16-byte bank groups (4 wavefronts, the minimum for 512 bytes); 4 rows x
+    // 8 chunks would hit only 4 groups (8 wavefronts).
 #pragma unroll
     for (int e = 0; e < (NR * TC_KT / 4) / NT; e++) {
         const int idx = threadIdx.x + e * NT;
-        const int r = idx >> 3, c = idx & 7;
+        const int lane = idx & 31, wq = idx >> 5;
+        const int r = ((wq >> 1) << 3) + (lane & 7), c = ((wq & 1) << 2) + (lane >> 3);
         const float *row = rows[r];
         const int k = k0 + c * 4;
         const bool ok = row != nullptr && k < D;
