@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <utility>
 #include <vector>
 
 #include "../../include/focus_b200.h"
@@ -46,6 +47,32 @@ struct Error {
     } while (0)
 
 void count_launch();
+
+// Programmatic dependent launch for the per-batch kernel chain (screen ->
+// residual columns -> row pass -> resolve -> fold -> next batch's pack):
+// the next kernel is launched while this one runs, its CTAs park in
+// griddepcontrol.wait until this grid has finished and flushed, so the
+// launch latency between dependent kernels is hidden.  Every kernel of the
+// chain calls pdl_enter() first (a no-op when launched without the attribute).
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+}
+
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args &&...args) {
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = grid;
+    lc.blockDim = block;
+    lc.dynamicSmemBytes = smem;
+    lc.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    FX_CUDA(cudaLaunchKernelEx(&lc, kern, std::forward<Args>(args)...));
+}
 
 // ---------------------------------------------------------------------------
 // device buffers

@@ -138,6 +138,7 @@ template <typename TA, typename FB>
 __global__ void __launch_bounds__(256) k_screen(int nA, int64_t a0, const char *const *__restrict__ frow, int D,
                                                const int64_t *__restrict__ nB_dev, int nB_max, FB fb,
                                                float *__restrict__ out, int64_t ld, int nB_skip = -1) {
+    pdl_enter();
     const int nB = nB_dev ? (int)*nB_dev : nB_max;
     if (nB <= nB_skip) return;  // few residual columns: k_res_cols handles them
     // persistent over the (column, row) tiles that exist for the device-side nB
@@ -224,6 +225,7 @@ __global__ void k_residuals(int nA, const int64_t *__restrict__ ctr, const float
                             const float *__restrict__ cn2, const int32_t *__restrict__ snap,
                             const float *__restrict__ fnorm, int64_t a0, ScreenModel sm, double T,
                             int32_t *__restrict__ res_col, int32_t *__restrict__ res_pos, int64_t *__restrict__ nres) {
+    pdl_enter();
     int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (w >= nA) return;
     const int nsnap = (int)ctr[C_NSNAP];
@@ -556,6 +558,7 @@ __device__ __forceinline__ void row_scan(const float *__restrict__ drow, int nsn
 // screen accumulated in rowmin (float bits); resets rowmin for the next batch.
 __global__ void k_res_from_min(int nA, int *__restrict__ rowmin, double T, int32_t *__restrict__ res_col,
                                int32_t *__restrict__ res_pos, int64_t *__restrict__ nres) {
+    pdl_enter();
     const int a = blockIdx.x * blockDim.x + threadIdx.x;
     if (a >= nA) return;
     const float mn = __int_as_float(rowmin[a]);
@@ -580,6 +583,7 @@ __global__ void k_row_summary(int nA, const int64_t *__restrict__ ctr, const flo
                               int32_t *__restrict__ sum_slot, int32_t *__restrict__ sum_q, float *__restrict__ sum_d1,
                               float *__restrict__ sum_e1, float *__restrict__ sum_lbr,
                               const float *__restrict__ snorm) {
+    pdl_enter();
     const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
     if (w >= nA) return;
     const int nsnap = (int)ctr[C_NSNAP];
@@ -644,6 +648,7 @@ __global__ void __launch_bounds__(256) k_rowpass(int nA, int64_t a0, const char 
                                                 int32_t *__restrict__ sum_q,
                                                 float *__restrict__ sum_d1, float *__restrict__ sum_e1,
                                                 float *__restrict__ sum_lbr, const float *__restrict__ snorm) {
+    pdl_enter();
     __shared__ int s_rpos[RC_MAX];
     __shared__ int s_pmin;
     const int nsnap = (int)ctr[C_NSNAP];
@@ -850,6 +855,7 @@ __device__ int rs_compact(int lo, int hi, Pred pred, int32_t *out, int *wsv, int
 
 template <typename T>
 __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
+    pdl_enter();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int B = A.B;
     const int BC = A.Bcap;  // layout by capacity (multiple of 64): every array stays aligned
@@ -2029,6 +2035,7 @@ __global__ void __launch_bounds__(FOLD_THREADS) k_fold(int D, int64_t c0, const 
                                                       float *__restrict__ s_cn2, double *__restrict__ fcent,
                                                       int32_t *__restrict__ cl_nfeat, int32_t *__restrict__ cl_size,
                                                       long long *__restrict__ fprof) {
+    pdl_enter();
     constexpr int R = fold_rows<T>();
     extern __shared__ __align__(16) unsigned char fold_raw[];
     T *ring = (T *)fold_raw;                                                // [NS][R][FD]
@@ -2271,6 +2278,7 @@ size_t resolve_smem(int Bc, const PwPlan &P) {
 // consecutive rows): C32q[q] = C32[snap[q]], q < nsnap.
 __global__ void k_snap_pack(const int64_t *__restrict__ ctr, const int32_t *__restrict__ snap,
                             const float *__restrict__ C32, float *__restrict__ C32q, int D) {
+    pdl_enter();
     const int nsnap = (int)ctr[C_NSNAP];
     const int n4 = D >> 2;
     for (int q = blockIdx.x; q < nsnap; q += gridDim.x) {
@@ -2367,7 +2375,7 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             if (tma) {
                 rbase = (int)brows[2 * bi];
                 nR = (int)(brows[2 * bi + 1] - brows[2 * bi] + 1);
-                k_snap_pack<<<(unsigned)std::min<int64_t>(s->ld, 148 * 4), 128, 0, st>>>(s->ctr.p, s->snap_slot.p,
+                launch_pdl(k_snap_pack, dim3((unsigned)std::min<int64_t>(s->ld, 148 * 4)), dim3(128), 0, st, s->ctr.p, s->snap_slot.p,
                                                                                         s->C32.p, s->C32q.p, D);
                 FX_LAUNCHED();
             }
@@ -2388,11 +2396,11 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
         // 2. residuals + their in-batch columns
         {
             if (!fused_res && s->tc_screen) {
-                k_res_from_min<<<(unsigned)cdiv(B, 256), 256, 0, st>>>(B, s->rowmin.p, s->cfg.t, s->res_col.p,
+                launch_pdl(k_res_from_min, dim3((unsigned)cdiv(B, 256)), dim3(256), 0, st, B, s->rowmin.p, s->cfg.t, s->res_col.p,
                                                                       s->res_pos.p, s->ctr.p + C_NRES);
                 FX_LAUNCHED();
             } else if (!fused_res) {
-                k_residuals<<<(unsigned)cdiv((int64_t)B * 32, 256), 256, 0, st>>>(
+                launch_pdl(k_residuals, dim3((unsigned)cdiv((int64_t)B * 32, 256)), dim3(256), 0, st, 
                     B, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p, s->snap_slot.p, s->fnorm.p, c0, sm, s->cfg.t,
                     s->res_col.p, s->res_pos.p, s->ctr.p + C_NRES);
                 FX_LAUNCHED();
@@ -2411,7 +2419,7 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             }
             const unsigned grid = (unsigned)std::min<int64_t>(cdiv(B, SC_T) * cdiv(B, SC_T), 148);
             FromResidual<T> fb{s->frow.p, c0, s->res_pos.p};
-            k_screen<T, FromResidual<T>><<<grid, 256, 0, st>>>(B, c0, s->frow.p, D, s->ctr.p + C_NRES, B, fb, s->dres.p, B,
+            launch_pdl(k_screen<T, FromResidual<T>>, dim3(grid), dim3(256), 0, st, B, c0, s->frow.p, D, s->ctr.p + C_NRES, B, fb, s->dres.p, B,
                                                                rc_ok ? RC_MAX : -1);
             FX_LAUNCHED();
         }
@@ -2421,18 +2429,18 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
         if (rowpass) {
             const unsigned grid = (unsigned)std::min<int64_t>(cdiv((int64_t)B * 32, 256), 148 * 8);
             if (D <= 1024)
-                k_rowpass<8><<<grid, 256, 0, st>>>(B, c0, s->frow.p, D, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p,
+                launch_pdl(k_rowpass<8>, dim3(grid), dim3(256), 0, st, B, c0, s->frow.p, D, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p,
                                                    s->snap_slot.p, s->fnorm.p, sm, rel, absc, s->C32.p, s->cfg.t,
                                                    s->res_pos.p, s->dres.p, B, s->sum_slot.p, s->sum_q.p, s->sum_d1.p,
                                                    s->sum_e1.p, s->sum_lbr.p, snorm);
             else
-                k_rowpass<16><<<grid, 256, 0, st>>>(B, c0, s->frow.p, D, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p,
+                launch_pdl(k_rowpass<16>, dim3(grid), dim3(256), 0, st, B, c0, s->frow.p, D, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p,
                                                     s->snap_slot.p, s->fnorm.p, sm, rel, absc, s->C32.p, s->cfg.t,
                                                     s->res_pos.p, s->dres.p, B, s->sum_slot.p, s->sum_q.p, s->sum_d1.p,
                                                    s->sum_e1.p, s->sum_lbr.p, snorm);
             FX_LAUNCHED();
         } else {
-        k_row_summary<T><<<(unsigned)cdiv((int64_t)B * 32, 256), 256, 0, st>>>(
+        launch_pdl(k_row_summary<T>, dim3((unsigned)cdiv((int64_t)B * 32, 256)), dim3(256), 0, st, 
                 B, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p, s->snap_slot.p, s->fnorm.p, c0, sm, rel, absc, s->frow.p,
                 s->C32.p, D, s->sum_slot.p, s->sum_q.p, s->sum_d1.p, s->sum_e1.p, s->sum_lbr.p, snorm);
             FX_LAUNCHED();
@@ -2516,7 +2524,7 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
                 FX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
                 cur = smem;
             }
-            kern<<<1, RS_THREADS, smem, st>>>(A);
+            launch_pdl(kern, dim3(1), dim3(RS_THREADS), smem, st, A);
             FX_LAUNCHED();
         }
         s->tstop();
@@ -2609,7 +2617,7 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
                 FX_CUDA(cudaFuncSetAttribute(k_fold<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fold_smem<T>()));
                 fold_attr[sizeof(T) == 8] = true;
             }
-            k_fold<T><<<grid, FOLD_THREADS, fold_smem<T>(), st>>>(D, c0, s->ctr.p, s->dirty.p, s->dirty_off.p, s->pend_list.p, s->frow.p,
+            launch_pdl(k_fold<T>, dim3(grid), dim3(FOLD_THREADS), fold_smem<T>(), st, D, c0, s->ctr.p, s->dirty.p, s->dirty_off.p, s->pend_list.p, s->frow.p,
                                             s->S.p, s->C32.p, s->s_nfeat.p, s->s_foldpos.p, s->s_seedpos.p,
                                             s->s_evicted.p, s->s_cid.p, s->s_size.p, s->s_cn2.p, s->fcent.p,
                                             s->cl_nfeat.p, s->cl_size.p, (long long *)(s->prof.p + 16));
