@@ -26,3 +26,19 @@ def test_tc_screen_matches_float64_within_bound(na, nb, dim):
     assert np.all(err <= bound), float((err / bound).max())
     # and it really is a tensor-core GEMM, not garbage: typical error far below the bound
     assert np.median(err / bound) < 0.2
+
+
+@pytest.mark.parametrize("na,nb,dim", [(1000, 300, 2048), (130, 7, 200), (77, 129, 64), (4096, 101, 2048)])
+def test_tma_and_cp_async_staging_bit_identical(na, nb, dim, monkeypatch):
+    """TMA tiled boxes (SWIZZLE_128B) and the cp.async fallback stage the same
+    operands in the same K order: the screen values must agree bit for bit."""
+    rng = np.random.default_rng(7 * na + dim)
+    A = rng.standard_normal((na, dim)).astype(np.float32)
+    B = rng.standard_normal((nb, dim)).astype(np.float32)
+    outs = {}
+    for mode in ("cp", "tma"):
+        monkeypatch.setenv("FOCUS_B200_TCLOAD", mode)
+        out = np.empty((na, nb), np.float32)
+        _lib.check(_lib.load().fx_debug_screen_tc(0, na, nb, dim, _lib.pv(A), _lib.pv(B), _lib.pv(out)))
+        outs[mode] = out
+    assert np.array_equal(outs["cp"].view(np.uint32), outs["tma"].view(np.uint32))
