@@ -202,6 +202,20 @@ int fx_index_build(int64_t n_clusters, int32_t vocab, int32_t k, int32_t dim, in
                    fx_index **out);
 int fx_index_destroy(fx_index *ix);
 
+/* index.save (index.py:88-131, FOCUSIDX/1): writes to `path` exactly the
+ * bytes of the reference's _render -- `head` (magic, stream_id=, D=, V=, n=,
+ * config lines and "[CLUSTERS]\n", built by the caller), one line per
+ * cluster in id order (centroid %.9g, members, frames, class:rank by encoded
+ * class), "[POSTINGS]", the non-empty postings by encoded class and the
+ * CRC32 trailer.  Arrays in the fx_index_export layout (host memory;
+ * centroids required).  Host-only: runs without a GPU.  threads <= 0: all
+ * hardware threads. */
+int fx_index_write(const char *path, const char *head, int64_t head_len, int64_t n_clusters, int32_t dim,
+                   int32_t vocab, const int64_t *cluster_ids, const double *centroids, const int64_t *reps,
+                   const int64_t *mem_off, const int64_t *mem_oid, const int64_t *mem_fid,
+                   const int64_t *cls_off, const int32_t *cls_id, const int32_t *cls_rank,
+                   const int64_t *post_off, const int64_t *post_cluster, int32_t threads);
+
 /* index.lookup (index.py:75-85): cluster ids posted under class_enc with
  * best rank <= k_x (k_x <= 0 -> K), ascending.  Two-call sizing: pass
  * out_ids = NULL to get *out_n. */

@@ -9,9 +9,9 @@ from .classifiers import (GENERIC_CHEAP, GROUND_TRUTH, SPECIALIZED, ClassifierPr
                           extract_feature, ground_truth_label, make_default_profiles, specialize_profile)
 from .clustering import Cluster
 from .core import (OTHER_CLASS, AccuracyTarget, Config, DetectedObject, RankedClassification, decode_class,
-                   encode_class, validate_config)
+                   encode_class, format_config, parse_config, validate_config)
 from .errors import *  # noqa: F401,F403
-from .index import IndexHeader, TopKIndex, build, lookup
+from .index import IndexHeader, TopKIndex, build, load, lookup, save
 from .ingest import DEFAULT_PIXEL_EPS, IngestReport, StreamHeader, ingest_arrays, ingest_stream, pixel_diff
 from .query import QueryRequest, QueryResult, QuerySession
 from ._lib import set_device

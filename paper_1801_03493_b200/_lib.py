@@ -88,6 +88,9 @@ _SIGS = {
                                       c_i64p, c_f64p, c_i64p, c_i64p, c_i64p, c_i64p, c_i64p, c_i32p, c_i32p,
                                       ctypes.POINTER(vp)]),
     "fx_index_destroy": (ctypes.c_int, [vp]),
+    "fx_index_write": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
+                                      ctypes.c_int32, c_i64p, c_f64p, c_i64p, c_i64p, c_i64p, c_i64p, c_i64p, c_i32p,
+                                      c_i32p, c_i64p, c_i64p, ctypes.c_int32]),
     "fx_lookup": (ctypes.c_int, [vp, ctypes.c_int32, ctypes.c_int32, c_i64p, ctypes.c_int64, c_i64p]),
     "fx_session_create": (ctypes.c_int, [vp, c_i32p, c_i32p, ctypes.c_int64, c_u8p, ctypes.POINTER(vp)]),
     "fx_session_destroy": (ctypes.c_int, [vp]),

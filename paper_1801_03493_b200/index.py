@@ -16,8 +16,10 @@ import numpy as np
 
 from . import _lib
 from .clustering import Cluster
-from .core import Config, decode_class, encode_class
-from .errors import KxTooLarge
+import os
+
+from .core import Config, decode_class, encode_class, format_config, parse_config
+from .errors import ChecksumMismatch, DataError, DuplicateClusterId, FormatVersionMismatch, KxTooLarge
 
 
 @dataclass(frozen=True)
@@ -174,6 +176,8 @@ def lookup(idx: TopKIndex, class_id: int, k_x: int | None = None) -> list:
     enc = encode_class(class_id, V)
     if enc < 0 or enc > V:
         return []
+    if idx.device is None:  # e.g. loaded from a file: post it on the device once
+        idx.device = build(list(idx.clusters.values()), idx.header).device
     L = _lib.load()
     n = ctypes.c_int64(0)
     _lib.check(L.fx_lookup(idx.device.handle, enc, kx, None, 0, ctypes.byref(n)))
@@ -183,4 +187,132 @@ def lookup(idx: TopKIndex, class_id: int, k_x: int | None = None) -> list:
     return out.tolist()
 
 
-__all__ = ["IndexHeader", "TopKIndex", "DeviceIndex", "build", "lookup", "decode_class"]
+# -- serialization: FOCUSIDX/1 (index.py:88-204) ------------------------------
+
+_MAGIC = "FOCUSIDX/1"
+
+
+def _cluster_arrays(clusters, V: int, D: int) -> dict:
+    """fx_index_export layout of Python Cluster records."""
+    cl = list(clusters)
+    C = len(cl)
+    mem_off = np.zeros(C + 1, np.int64)
+    cls_off = np.zeros(C + 1, np.int64)
+    for i, c in enumerate(cl):
+        mem_off[i + 1] = mem_off[i] + len(c.member_object_ids)
+        cls_off[i + 1] = cls_off[i] + len(c.class_best_rank)
+    return dict(
+        cluster_ids=np.array([c.cluster_id for c in cl], np.int64),
+        reps=np.array([-1 if c.centroid_member_id is None else c.centroid_member_id for c in cl], np.int64),
+        centroids=np.ascontiguousarray(np.array([np.asarray(c.centroid, np.float64) for c in cl],
+                                                np.float64).reshape(C, D)),
+        mem_off=mem_off,
+        mem_oid=np.fromiter((o for c in cl for o in c.member_object_ids), np.int64, int(mem_off[-1])),
+        mem_fid=np.fromiter((f for c in cl for f in c.frame_ids), np.int64, int(mem_off[-1])),
+        cls_off=cls_off,
+        cls_id=np.fromiter((encode_class(k, V) for c in cl for k in c.class_best_rank), np.int32, int(cls_off[-1])),
+        cls_rank=np.fromiter((r for c in cl for r in c.class_best_rank.values()), np.int32, int(cls_off[-1])))
+
+
+def _posting_arrays(postings: dict, V: int) -> dict:
+    off = np.zeros(V + 2, np.int64)
+    by_enc = {encode_class(c, V): ids for c, ids in postings.items()}
+    for enc in range(V + 1):
+        off[enc + 1] = off[enc] + len(by_enc.get(enc, ()))
+    ids = np.fromiter((x for enc in range(V + 1) for x in by_enc.get(enc, ())), np.int64, int(off[-1]))
+    return dict(post_off=off, post_cluster=ids)
+
+
+def save(idx: TopKIndex, path, threads: int = 0) -> None:
+    """index.save (index.py:122-128): the reference's FOCUSIDX/1 bytes, rendered
+    by the native writer (fx_index_write), written to a temp file in the same
+    directory and renamed into place."""
+    h = idx.header
+    V, D = h.vocab, h.dim
+    head = "\n".join([_MAGIC, f"stream_id={h.stream_id}", f"D={D}", f"V={V}", f"n={h.n_objects}",
+                      format_config(h.config).rstrip("\n"), "[CLUSTERS]"]) + "\n"
+    ex = idx.device.export(centroids=True) if idx.device is not None else None
+    if idx._clusters is not None or ex is None or "centroids" not in ex:
+        ca = _cluster_arrays(idx.clusters.values(), V, D)
+    else:
+        ca = ex
+    pa = _posting_arrays(idx.postings, V) if idx._postings is not None or ex is None else ex
+    hb = head.encode("utf-8")
+    tmp = f"{path}.tmp.{os.getpid()}"
+    try:
+        _lib.check(_lib.load().fx_index_write(
+            os.fsencode(tmp), hb, len(hb), len(ca["cluster_ids"]), D, V, _lib.p64(ca["cluster_ids"]),
+            _lib.pf64(ca["centroids"]), _lib.p64(ca["reps"]), _lib.p64(ca["mem_off"]), _lib.p64(ca["mem_oid"]),
+            _lib.p64(ca["mem_fid"]), _lib.p64(ca["cls_off"]), _lib.p32(ca["cls_id"]), _lib.p32(ca["cls_rank"]),
+            _lib.p64(pa["post_off"]), _lib.p64(pa["post_cluster"]), int(threads)))
+        os.replace(tmp, path)
+    finally:
+        if os.path.exists(tmp):
+            os.unlink(tmp)
+
+
+def load(path) -> TopKIndex:
+    """index.load (index.py:131-204): CRC32 trailer and magic checked first,
+    then header, cluster records and postings; the same errors as the
+    reference (ChecksumMismatch, FormatVersionMismatch, DataError,
+    DuplicateClusterId).  The device index is built on first lookup."""
+    import zlib
+    with open(path, "r", encoding="utf-8") as fh:
+        data = fh.read()
+    head, nl, last = data.rstrip("\n").rpartition("\n")
+    if not last.startswith("CRC32:"):
+        raise ChecksumMismatch("missing CRC32 trailer")
+    body = head + nl
+    expect = last[len("CRC32:"):]
+    actual = f"{zlib.crc32(body.encode('utf-8')) & 0xFFFFFFFF:08x}"
+    if actual != expect:
+        raise ChecksumMismatch(f"CRC mismatch: file says {expect}, computed {actual}")
+    lines = body.splitlines()
+    if not lines or lines[0] != _MAGIC:
+        raise FormatVersionMismatch(f"index file must start with {_MAGIC}")
+    kv, config_lines = {}, []
+    i = 1
+    while i < len(lines) and lines[i] != "[CLUSTERS]":
+        key, _, value = lines[i].partition("=")
+        if key in ("stream_id", "D", "V", "n"):
+            kv[key] = value
+        else:
+            config_lines.append(lines[i])
+        i += 1
+    if i >= len(lines):
+        raise DataError("index file has no [CLUSTERS] section")
+    try:
+        vocab = int(kv["V"])
+        header = IndexHeader(stream_id=kv["stream_id"], dim=int(kv["D"]), vocab=vocab, n_objects=int(kv["n"]),
+                             config=parse_config("\n".join(config_lines)))
+    except (KeyError, ValueError) as exc:
+        raise DataError(f"bad index header: {exc}") from exc
+    clusters = {}
+    i += 1
+    while i < len(lines) and lines[i] != "[POSTINGS]":
+        parts = lines[i].split("|")
+        if len(parts) != 6:
+            raise DataError(f"bad cluster record: {lines[i]!r}")
+        cid = int(parts[0])
+        if cid in clusters:
+            raise DuplicateClusterId(str(cid))
+        ranks = {}
+        if parts[5]:
+            for item in parts[5].split(","):
+                cls, _, rank = item.partition(":")
+                ranks[decode_class(int(cls), vocab)] = int(rank)
+        clusters[cid] = Cluster(cluster_id=cid, centroid=np.array([float(x) for x in parts[2].split(",")]),
+                                member_object_ids=[int(x) for x in parts[3].split(",")],
+                                frame_ids=[int(x) for x in parts[4].split(",")], class_best_rank=ranks,
+                                centroid_member_id=None if parts[1] == "" else int(parts[1]), sealed=True)
+        i += 1
+    if i >= len(lines):
+        raise DataError("index file has no [POSTINGS] section")
+    postings = {}
+    for line in lines[i + 1:]:
+        cls, _, ids = line.partition("|")
+        postings[decode_class(int(cls), vocab)] = [int(x) for x in ids.split(",")]
+    return TopKIndex(header=header, clusters=clusters, postings=postings)
+
+
+__all__ = ["IndexHeader", "TopKIndex", "DeviceIndex", "build", "lookup", "decode_class", "save", "load"]

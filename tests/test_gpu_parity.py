@@ -167,3 +167,22 @@ def test_random_configs_match_oracle(seed, t, m, dim):
     cen = np.array([cc.centroid for cc in ref.clusters])
     assert np.array_equal(ex["centroids"].view(np.uint64), cen.view(np.uint64))
     assert ex["reps"].tolist() == [cc.centroid_member_id for cc in ref.clusters]
+
+
+@pytest.mark.parametrize("name", ["small_d64", "spec_d32", "gt_d8", "f64_d16"])
+def test_saved_index_file_equals_reference_file(name, tmp_path):
+    """Device ingest -> fx.save: the FOCUSIDX/1 bytes the reference's
+    index.save wrote for the same stream (tests/golden/index_<case>.focusidx)."""
+    import os
+    c = GU.load(name)
+    golden = os.path.join(GU.GOLDEN, f"index_{name}.focusidx")
+    with open(golden, "rb") as fh:
+        want = fh.read()
+    stream_id = want.split(b"\n")[1].decode().partition("=")[2]
+    st = c.stream
+    idx, rep, _ = fx.ingest_arrays(st.oids, st.fids, st.sigs, c.feats, _cfg(c), _profile(c), vocab=c.spec.vocab,
+                                   seed=c.extra["seed"], pixel_eps=c.pixel_eps,
+                                   true_class=st.true_class.astype(np.int32), stream_id=stream_id)
+    out = tmp_path / "idx.focusidx"
+    fx.save(idx, str(out))
+    assert out.read_bytes() == want
