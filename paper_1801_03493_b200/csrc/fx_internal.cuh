@@ -59,6 +59,8 @@ __device__ __forceinline__ void pdl_enter() {
     asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
 }
 
+bool pdl_enabled();  // FOCUS_B200_NOPDL=1 turns programmatic dependent launch off (diagnostics)
+
 template <typename... KArgs, typename... Args>
 void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args &&...args) {
     cudaLaunchConfig_t lc = {};
@@ -70,7 +72,7 @@ void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cuda
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
     lc.attrs = at;
-    lc.numAttrs = 1;
+    lc.numAttrs = pdl_enabled() ? 1 : 0;
     FX_CUDA(cudaLaunchKernelEx(&lc, kern, std::forward<Args>(args)...));
 }
 

@@ -36,10 +36,6 @@ namespace cg = cooperative_groups;
 namespace fx {
 
 constexpr int TC_M = 128, TC_N = 128, TC_STAGES = 6, TC_THREADS = 256;  // warps 4-7 only help load
-// TMA staging keeps fewer stages in flight: 3 x 32 KB lets two CTAs share an SM
-constexpr int TC_STAGES_TMA = 3;
-template <bool TMA>
-constexpr int tc_stages() { return TMA ? TC_STAGES_TMA : TC_STAGES; }
 constexpr int TC_TILE_BYTES = TC_M * TC_KT * 4;  // 16 KB per operand per stage
 
 // Operand staging by TMA (TMA = true): one 2-D tiled box (32 fp32 x 128 rows,
@@ -60,7 +56,7 @@ __device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
 
 // out[a][q] = ||A_a||^2 + ||B_q||^2 - 2 A_a.B_q   (float, not clamped)
 template <bool TMA>
-__global__ void __launch_bounds__(TC_THREADS, TMA ? 2 : 1) k_screen_tc(int nA, int64_t a0, const char *const *__restrict__ frow,
+__global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0, const char *const *__restrict__ frow,
                                                            const float *fnorm, int D,  // aliases fnorm_out
                                                            const int64_t *__restrict__ nB_dev,
                                                            const float *__restrict__ C32,
@@ -114,8 +110,8 @@ __global__ void __launch_bounds__(TC_THREADS, TMA ? 2 : 1) k_screen_tc(int nA, i
     __shared__ const float *rowsA[TC_M];
     __shared__ const float *rowsB[TC_N];
     __shared__ int rcls[TC_M];  // batch-local classified index of each tile row, -1: none
-    __shared__ __align__(8) uint64_t bar_stage[tc_stages<TMA>()];
-    __shared__ __align__(8) uint64_t bar_full[tc_stages<TMA>()];
+    __shared__ __align__(8) uint64_t bar_stage[TC_STAGES];
+    __shared__ __align__(8) uint64_t bar_full[TC_STAGES];
     __shared__ __align__(8) uint64_t bar_done;
     __shared__ uint32_t tmem_base;
 
@@ -130,7 +126,7 @@ __global__ void __launch_bounds__(TC_THREADS, TMA ? 2 : 1) k_screen_tc(int nA, i
         }
     }
     if (tid == 0) {
-        for (int s = 0; s < tc_stages<TMA>(); s++) {
+        for (int s = 0; s < TC_STAGES; s++) {
             mbar_init(&bar_stage[s], TMA ? 5 : 1);
             mbar_init(&bar_full[s], 1);
         }
@@ -159,8 +155,8 @@ __global__ void __launch_bounds__(TC_THREADS, TMA ? 2 : 1) k_screen_tc(int nA, i
             asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmA) : "memory");
             asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmB) : "memory");
             for (int it = 0; it < nk; it++) {
-                const int s = it % tc_stages<TMA>();
-                if (it >= tc_stages<TMA>()) mbar_wait(&bar_stage[s], (uint32_t)(((it / tc_stages<TMA>()) - 1) & 1));
+                const int s = it % TC_STAGES;
+                if (it >= TC_STAGES) mbar_wait(&bar_stage[s], (uint32_t)(((it / TC_STAGES) - 1) & 1));
                 const uint32_t st = sbase + s * 2 * TC_TILE_BYTES;
                 const uint32_t fb = smem_u32(&bar_full[s]);
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(fb), "r"(2 * TC_TILE_BYTES)
@@ -179,8 +175,8 @@ __global__ void __launch_bounds__(TC_THREADS, TMA ? 2 : 1) k_screen_tc(int nA, i
             }
         } else if (warp == 5) {  // MMA issue
             for (int it = 0; it < nk; it++) {
-                const int s = it % tc_stages<TMA>();
-                mbar_wait(&bar_full[s], (uint32_t)((it / tc_stages<TMA>()) & 1));
+                const int s = it % TC_STAGES;
+                mbar_wait(&bar_full[s], (uint32_t)((it / TC_STAGES) & 1));
                 if (lane == 0) {
                     asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
                     const uint32_t st = sbase + s * 2 * TC_TILE_BYTES;
@@ -204,8 +200,8 @@ __global__ void __launch_bounds__(TC_THREADS, TMA ? 2 : 1) k_screen_tc(int nA, i
                     smem_u32(&bar_done)));
         } else if (warp < 4) {  // row norms: row tid's 8 chunks of 16 B in the swizzled atom
             for (int it = 0; it < nk; it++) {
-                const int s = it % tc_stages<TMA>();
-                mbar_wait(&bar_full[s], (uint32_t)((it / tc_stages<TMA>()) & 1));
+                const int s = it % TC_STAGES;
+                mbar_wait(&bar_full[s], (uint32_t)((it / TC_STAGES) & 1));
                 const unsigned char *row = smem + s * 2 * TC_TILE_BYTES + (tid >> 3) * 1024 + (tid & 7) * 128;
                 float p = 0.f;
 #pragma unroll
@@ -394,9 +390,9 @@ __global__ void __launch_bounds__(TC_THREADS, TMA ? 2 : 1) k_screen_tc(int nA, i
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TC_N));
 }
 
-size_t screen_tc_smem(bool tma = false) {
+size_t screen_tc_smem() {
     // pipeline stages; the epilogue's [128][TC_N+4] tile reuses them
-    const size_t pipe = (size_t)(tma ? TC_STAGES_TMA : TC_STAGES) * 2 * TC_TILE_BYTES;
+    const size_t pipe = (size_t)TC_STAGES * 2 * TC_TILE_BYTES;
     return std::max(pipe, (size_t)TC_M * (TC_N + 4) * 4) + 1024;
 }
 
@@ -431,10 +427,8 @@ void launch_screen_tc(int nA, int64_t a0, const char *const *frow, const float *
     else rowmin_g = nullptr;
     static bool attr = false;
     if (!attr) {
-        FX_CUDA(cudaFuncSetAttribute(k_screen_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)screen_tc_smem()));
-        FX_CUDA(cudaFuncSetAttribute(k_screen_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)screen_tc_smem(true)));
+        for (auto k : {k_screen_tc<false>, k_screen_tc<true>})
+            FX_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)screen_tc_smem()));
         attr = true;
     }
     const bool tma = tmA && tmB;
@@ -448,9 +442,7 @@ void launch_screen_tc(int nA, int64_t a0, const char *const *frow, const float *
     }
     const int64_t tiles = cdiv(nB_max, TC_N) * cdiv(nR, TC_M);
     int split = 1;
-    const int64_t slots = tma ? 2 * 148 : 148;  // co-resident CTAs (TMA: 2 per SM, split <= 4)
-    while (tiles * split * 2 <= slots && D / (split * 2) >= 4 * TC_KT) split *= 2;
-    if (tma) split = std::min(split, 4);
+    while (tiles * split * 2 <= 148 && D / (split * 2) >= 4 * TC_KT) split *= 2;
     if (split_env > 0) split = split_env;
     split = std::min(split, 8);  // split-K CTAs of a tile form one (portable-size) cluster
     while (TC_M % split) split--;
@@ -458,7 +450,7 @@ void launch_screen_tc(int nA, int64_t a0, const char *const *frow, const float *
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3((unsigned)(cdiv(nB_max, TC_N) * cdiv(nR, TC_M)), 1, (unsigned)split);
     lc.blockDim = dim3(TC_THREADS);
-    lc.dynamicSmemBytes = screen_tc_smem(tma);
+    lc.dynamicSmemBytes = screen_tc_smem();
     lc.stream = st;
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -468,7 +460,7 @@ void launch_screen_tc(int nA, int64_t a0, const char *const *frow, const float *
     at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // PDL: see pdl_enter
     at[1].val.programmaticStreamSerializationAllowed = 1;
     lc.attrs = at;
-    lc.numAttrs = 2;
+    lc.numAttrs = pdl_enabled() ? 2 : 1;
     FX_CUDA(cudaLaunchKernelEx(&lc, tma ? k_screen_tc<true> : k_screen_tc<false>, nA, a0, frow, fnorm, D, nB_dev, C32,
                                snap, cn2, out, ld, kchunk, dbg, fnorm_out, sm, T, res_col, res_pos, nres, rowmin_g,
                                snorm, tma ? *tmA : zero_map, tma ? *tmB : zero_map, rbase, nR, rmap));

@@ -240,3 +240,10 @@ void scan_u8_to_i64(const uint8_t *in, int64_t n, int invert, int64_t *out_excl,
 }
 
 }  // namespace fx
+
+namespace fx {
+bool pdl_enabled() {
+    static const bool on = !(getenv("FOCUS_B200_NOPDL") && atoi(getenv("FOCUS_B200_NOPDL")));
+    return on;
+}
+}  // namespace fx

@@ -28,7 +28,8 @@ def test_tc_screen_matches_float64_within_bound(na, nb, dim):
     assert np.median(err / bound) < 0.2
 
 
-@pytest.mark.parametrize("na,nb,dim", [(1000, 300, 2048), (130, 7, 200), (77, 129, 64), (4096, 101, 2048)])
+@pytest.mark.parametrize("na,nb,dim", [(1000, 300, 2048), (130, 7, 200), (77, 129, 64), (4096, 101, 2048),
+                                       (20000, 1000, 256), (6000, 800, 2048)])  # last two: several CTA waves
 def test_tma_and_cp_async_staging_bit_identical(na, nb, dim, monkeypatch):
     """TMA tiled boxes (SWIZZLE_128B) and the cp.async fallback stage the same
     operands in the same K order: the screen values must agree bit for bit."""

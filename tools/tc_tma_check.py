@@ -10,7 +10,7 @@ L.fx_debug_screen_tc.argtypes = [ctypes.c_int32, ctypes.c_int64, ctypes.c_int64,
                                  ctypes.c_void_p, ctypes.c_void_p]
 rng = np.random.default_rng(0)
 ok = True
-for na, nb, D in [(1000, 300, 2048), (4096, 101, 2048), (130, 7, 200), (77, 129, 64)]:
+for na, nb, D in [(1000, 300, 2048), (4096, 101, 2048), (130, 7, 200), (77, 129, 64), (20000, 1000, 256), (6000, 800, 2048)]:
     A = rng.standard_normal((na, D)).astype(np.float32)
     B = rng.standard_normal((nb, D)).astype(np.float32)
     outs = {}

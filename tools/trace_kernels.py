@@ -1,6 +1,8 @@
 """Per-kernel device time of one C2 stream ingest + finalize, traced with
 CUPTI through torch.profiler (real pipelined run, not ncu-serialised).
-GPU box only:  python tools/trace_kernels.py [n_objects [T [M]]]  (C3 shape: 300000 5.0 100000)"""
+GPU box only:  python tools/trace_kernels.py [n_objects [T [M]]]  (C3 shape: 300000 5.0 100000)
+Under programmatic dependent launch a kernel's traced duration includes the time its
+CTAs wait for the previous grid: set FOCUS_B200_NOPDL=1 for per-kernel attribution."""
 import collections
 import os
 import sys
