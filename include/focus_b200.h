@@ -35,6 +35,7 @@ typedef enum {
     FX_OK = 0,
     FX_E_USAGE = 1,                  /* UsageError            errors.py:8-9   */
     FX_E_DATA = 2,                   /* DataError             errors.py:12-13 */
+    FX_E_VALUE = 3,                  /* ValueError: bad number literal in a stream file (streamio.py:91-95) */
     FX_E_UNKNOWN_PROFILE = 10,       /* UnknownProfile        errors.py:18-19 */
     FX_E_K_OUT_OF_RANGE = 11,        /* KOutOfRange           errors.py:22-23 */
     FX_E_NON_POSITIVE_M = 12,        /* NonPositiveM          errors.py:26-27 */
@@ -42,6 +43,8 @@ typedef enum {
     FX_E_DIMENSION_MISMATCH = 30,    /* DimensionMismatch     errors.py:42-43 */
     FX_E_SIGNATURE_LENGTH = 31,      /* SignatureLengthMismatch errors.py:46-47 */
     FX_E_DUPLICATE_CLUSTER_ID = 40,  /* DuplicateClusterId    errors.py:52-53 */
+    FX_E_FORMAT_VERSION = 41,        /* FormatVersionMismatch errors.py:56-57 */
+    FX_E_CHECKSUM = 42,              /* ChecksumMismatch      errors.py:60-61 */
     FX_E_KX_TOO_LARGE = 50,          /* KxTooLarge            errors.py:66-67 */
     FX_E_UNKNOWN_CLASS = 51,         /* UnknownClass          errors.py:70-71 */
     FX_E_NON_MONOTONE_SCHEDULE = 52, /* NonMonotoneSchedule   errors.py:74-75 */
@@ -210,6 +213,22 @@ int fx_index_destroy(fx_index *ix);
  * CRC32 trailer.  Arrays in the fx_index_export layout (host memory;
  * centroids required).  Host-only: runs without a GPU.  threads <= 0: all
  * hardware threads. */
+/* streamio.read_stream (streamio.py:58-113), FOCUSSTREAM/1, decoded by host
+ * threads.  open: reads the file, checks magic and header, indexes the
+ * object lines (FX_E_FORMAT_VERSION, FX_E_DATA).  header: stream_id (NUL-
+ * terminated, cap bytes), fps, D, S, V, object count.  read: parses every
+ * object line into caller arrays -- object/frame ids, true class (decoded:
+ * OTHER = -1, unlabeled = -2), signatures (n x S float64), features (n x D,
+ * float32 if feats_f32 else float64); the first bad line in file order
+ * raises what the reference raises (FX_E_DATA, FX_E_VALUE).  Host-only. */
+typedef struct fx_stream_file fx_stream_file;
+int fx_stream_file_open(const char *path, fx_stream_file **out);
+int fx_stream_file_header(fx_stream_file *f, char *stream_id, int64_t cap, double *fps, int32_t *dim,
+                          int32_t *sig_dim, int32_t *vocab, int64_t *n_objects);
+int fx_stream_file_read(fx_stream_file *f, int64_t *object_ids, int64_t *frame_ids, int32_t *true_class,
+                        double *sigs, void *feats, int32_t feats_f32, int32_t threads);
+int fx_stream_file_close(fx_stream_file *f);
+
 int fx_index_write(const char *path, const char *head, int64_t head_len, int64_t n_clusters, int32_t dim,
                    int32_t vocab, const int64_t *cluster_ids, const double *centroids, const int64_t *reps,
                    const int64_t *mem_off, const int64_t *mem_oid, const int64_t *mem_fid,

@@ -88,6 +88,12 @@ _SIGS = {
                                       c_i64p, c_f64p, c_i64p, c_i64p, c_i64p, c_i64p, c_i64p, c_i32p, c_i32p,
                                       ctypes.POINTER(vp)]),
     "fx_index_destroy": (ctypes.c_int, [vp]),
+    "fx_stream_file_open": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(vp)]),
+    "fx_stream_file_header": (ctypes.c_int, [vp, ctypes.c_char_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_double),
+                                             ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
+                                             ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int64)]),
+    "fx_stream_file_read": (ctypes.c_int, [vp, c_i64p, c_i64p, c_i32p, c_f64p, vp, ctypes.c_int32, ctypes.c_int32]),
+    "fx_stream_file_close": (ctypes.c_int, [vp]),
     "fx_index_write": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
                                       ctypes.c_int32, c_i64p, c_f64p, c_i64p, c_i64p, c_i64p, c_i64p, c_i64p, c_i32p,
                                       c_i32p, c_i64p, c_i64p, ctypes.c_int32]),

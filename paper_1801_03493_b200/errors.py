@@ -78,6 +78,7 @@ class DeviceError(FocusError):
 STATUS = {
     1: UsageError,
     2: DataError,
+    3: ValueError,
     10: UnknownProfile,
     11: KOutOfRange,
     12: NonPositiveM,
@@ -85,6 +86,8 @@ STATUS = {
     30: DimensionMismatch,
     31: SignatureLengthMismatch,
     40: DuplicateClusterId,
+    41: FormatVersionMismatch,
+    42: ChecksumMismatch,
     50: KxTooLarge,
     51: UnknownClass,
     52: NonMonotoneSchedule,
