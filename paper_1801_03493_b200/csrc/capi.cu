@@ -24,7 +24,7 @@ void launch_final_live(fx_stream *s);
 size_t resolve_smem(int Bc, const PwPlan &P);
 void launch_fc_head(int64_t n, int64_t c0, const char *const *frow, const int64_t *cls_obj, const float *fnorm, int D,
                     int V, int K, const float *W, const float *wnorm, const float *bias, int32_t *topk, float *conf,
-                    uint8_t *flag, unsigned long long *nflag, cudaStream_t st);
+                    uint8_t *flag, unsigned long long *nflag, cudaStream_t st, const float *Xdense);
 void launch_row_norms(int64_t rows, int D, const float *X, float *out, cudaStream_t st);
 void launch_rowptrs(int64_t rows, int64_t row_bytes, const char *base, const char **out, cudaStream_t st);
 void launch_dup_members(fx_stream *s, int64_t n, const int64_t *d_excl_all, int64_t *d_anchor);
@@ -360,7 +360,7 @@ int fx_fc_topk(int32_t device, int64_t n, int32_t dim, int32_t vocab, int32_t k,
             launch_row_norms(n, dim, F.p, fn.p, st);
             launch_rowptrs(n, (int64_t)dim * 4, (const char *)F.p, rows.p, st);
             launch_fc_head(n, 0, rows.p, nullptr, fn.p, dim, vocab, k, Wd.p, wn.p, bias ? bd.p : nullptr, tk.p, cf.p,
-                           fl.p, nullptr, st);
+                           fl.p, nullptr, st, F.p);
             d2h(out_topk, tk.p, n * k, st);
             d2h(out_conf, cf.p, n * k, st);
             d2h(out_flag, fl.p, n, st);
@@ -392,7 +392,7 @@ int fx_fc_topk_device(int32_t device, void *cuda_stream, int64_t n, int32_t dim,
         launch_row_norms(n, dim, d_feats, fn.p, st);
         launch_rowptrs(n, (int64_t)dim * 4, (const char *)d_feats, rows.p, st);
         launch_fc_head(n, 0, rows.p, nullptr, fn.p, dim, vocab, k, d_W, wn.p, d_bias, d_topk, d_conf, d_flag, nullptr,
-                       st);
+                       st, d_feats);
     })
 }
 
@@ -485,7 +485,9 @@ static void ingest_chunk(fx_stream *s, int64_t n, const int64_t *d_oid, const in
         if (!s->rows_aligned16) throw Error{FX_E_USAGE, "fc head needs 16-byte aligned feature rows"};
         launch_fc_head(nc, c0, s->frow.p, s->cls_obj.p, s->fnorm.p, s->cfg.dim, s->fc_V, K, s->fc_W.p, s->fc_wnorm.p,
                        s->fc_bias.n ? s->fc_bias.p : nullptr, s->topk.p, nullptr, nullptr,
-                       (unsigned long long *)(s->ctr.p + C_FCFLAG), st);
+                       (unsigned long long *)(s->ctr.p + C_FCFLAG), st,
+                       s->a_compact && s->esize == 4 ? (const float *)s->abase + (c0 - s->a_cbase) * s->cfg.dim
+                                                       : nullptr);
         s->tstop();
     } else if (d_topk) {
         FX_CUDA(cudaMemcpyAsync(s->topk.p + n0 * K, d_topk, sizeof(int32_t) * n * K, cudaMemcpyDeviceToDevice, st));

@@ -24,6 +24,7 @@
 #include <cfloat>
 #include <climits>
 #include <cstdlib>
+#include <string>
 
 #include "fx_handles.cuh"
 #include "tc_common.cuh"
@@ -40,23 +41,37 @@ struct FcTile {  // per (object, class tile) result of k_fc_tc
     float lse_m, lse_s;  // logsumexp partial: max logit~, sum exp(l~ - max)
 };
 
+// TMA = true (objects' rows consecutive in memory): one SWIZZLE_128B tiled
+// box per operand and stage (A: 128 rows of tmA from row arow0 + ta, B: 256
+// class rows of tmW), issued by one producer thread; one MMA thread; per-
+// stage full barriers count bytes, empty barriers take the MMA commit.
+template <bool TMA>
 __global__ void __launch_bounds__(FC_THREADS, 1) k_fc_tc(int n, int64_t a0, const char *const *__restrict__ frow,
                                                         const float *__restrict__ fnorm, int D, int V,
                                                         const float *__restrict__ W, const float *__restrict__ wnorm,
                                                         const float *__restrict__ bias, float gamma,
-                                                        FcTile *__restrict__ out, int dbg) {
+                                                        FcTile *__restrict__ out, int dbg,
+                                                        const __grid_constant__ CUtensorMap tmA,
+                                                        const __grid_constant__ CUtensorMap tmW, int arow0) {
     const int tv = blockIdx.x * FC_N, ta = blockIdx.y * FC_M;
-    extern __shared__ __align__(1024) unsigned char smem[];
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // SWIZZLE_128B atoms
     __shared__ const float *rowsA[FC_M];
     __shared__ const float *rowsB[FC_N];
     __shared__ __align__(8) uint64_t bar_stage[FC_STAGES];
+    __shared__ __align__(8) uint64_t bar_full[FC_STAGES];
     __shared__ __align__(8) uint64_t bar_done;
     __shared__ uint32_t tmem_base;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    for (int r = tid; r < FC_M; r += FC_THREADS) rowsA[r] = ta + r < n ? (const float *)frow[a0 + ta + r] : nullptr;
-    for (int r = tid; r < FC_N; r += FC_THREADS) rowsB[r] = tv + r < V ? W + (int64_t)(tv + r) * D : nullptr;
+    if (!TMA) {
+        for (int r = tid; r < FC_M; r += FC_THREADS) rowsA[r] = ta + r < n ? (const float *)frow[a0 + ta + r] : nullptr;
+        for (int r = tid; r < FC_N; r += FC_THREADS) rowsB[r] = tv + r < V ? W + (int64_t)(tv + r) * D : nullptr;
+    }
     if (tid == 0) {
-        for (int s = 0; s < FC_STAGES; s++) mbar_init(&bar_stage[s], 1);
+        for (int s = 0; s < FC_STAGES; s++) {
+            mbar_init(&bar_stage[s], 1);
+            mbar_init(&bar_full[s], 1);
+        }
         mbar_init(&bar_done, 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
     }
@@ -73,48 +88,92 @@ __global__ void __launch_bounds__(FC_THREADS, 1) k_fc_tc(int n, int64_t a0, cons
     const int nk = (D + TC_KT - 1) / TC_KT;
     constexpr uint32_t idesc = idesc_tf32(FC_M, FC_N);
     constexpr int SB = FC_A_BYTES + FC_B_BYTES;
-    for (int s = 0; s < FC_STAGES - 1; s++) {
-        if (s < nk && !(dbg & 1)) {
-            load_tile<FC_M, FC_THREADS>(sbase + s * SB, rowsA, s * TC_KT, D, fnorm);
-            load_tile<FC_N, FC_THREADS>(sbase + s * SB + FC_A_BYTES, rowsB, s * TC_KT, D, fnorm);
-        }
-        asm volatile("cp.async.commit_group;\n" ::);
-    }
-    for (int it = 0; it < nk; it++) {
-        const int s = it % FC_STAGES;
-        asm volatile("cp.async.wait_group %0;\n" ::"n"(FC_STAGES - 2));
-        asm volatile("fence.proxy.async.shared::cta;\n" ::);
-        __syncthreads();
-        if (tid == 0 && !(dbg & 2)) {
-            asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
-            const uint32_t st = sbase + s * SB;
-#pragma unroll
-            for (int kk = 0; kk < TC_KT / 8; kk++) {
-                const uint64_t da = umma_desc(st + kk * 256, 128, TC_KT * 32);
-                const uint64_t db = umma_desc(st + FC_A_BYTES + kk * 256, 128, TC_KT * 32);
-                const uint32_t acc = (it > 0 || kk > 0) ? 1u : 0u;
+    if (TMA) {
+        if (warp == 0 && lane == 0) {  // producer
+            asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmA) : "memory");
+            asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmW) : "memory");
+            for (int it = 0; it < nk; it++) {
+                const int s = it % FC_STAGES;
+                if (it >= FC_STAGES) mbar_wait(&bar_stage[s], (uint32_t)(((it / FC_STAGES) - 1) & 1));
+                const uint32_t st = sbase + s * SB, fb = smem_u32(&bar_full[s]);
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(fb), "r"(SB) : "memory");
                 asm volatile(
-                    "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
-                    "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
-                    "l"(da), "l"(db), "r"(idesc), "r"(acc));
+                    "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+                    "%3}], [%4];\n" ::"r"(st),
+                    "l"(&tmA), "r"(it * TC_KT), "r"(arow0 + ta), "r"(fb)
+                    : "memory");
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+                    "%3}], [%4];\n" ::"r"(st + FC_A_BYTES),
+                    "l"(&tmW), "r"(it * TC_KT), "r"(tv), "r"(fb)
+                    : "memory");
+            }
+        } else if (warp == 1 && lane == 0) {  // MMA issue
+            for (int it = 0; it < nk; it++) {
+                const int s = it % FC_STAGES;
+                mbar_wait(&bar_full[s], (uint32_t)((it / FC_STAGES) & 1));
+                asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+                const uint32_t st = sbase + s * SB;
+#pragma unroll
+                for (int kk = 0; kk < TC_KT / 8; kk++) {
+                    const uint64_t da = umma_desc_sw128(st + kk * 32);
+                    const uint64_t db = umma_desc_sw128(st + FC_A_BYTES + kk * 32);
+                    const uint32_t acc = (it > 0 || kk > 0) ? 1u : 0u;
+                    asm volatile(
+                        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+                        "l"(da), "l"(db), "r"(idesc), "r"(acc));
+                }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                    smem_u32(&bar_stage[s])));
             }
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                smem_u32(&bar_stage[s])));
+                smem_u32(&bar_done)));
         }
-        const int nt = it + FC_STAGES - 1;
-        if (nt < nk) {
-            const int ns = nt % FC_STAGES;
-            if (nt >= FC_STAGES && !(dbg & 2)) mbar_wait(&bar_stage[ns], (uint32_t)(((nt / FC_STAGES) - 1) & 1));
-            if (!(dbg & 1)) {
-                load_tile<FC_M, FC_THREADS>(sbase + ns * SB, rowsA, nt * TC_KT, D, fnorm);
-                load_tile<FC_N, FC_THREADS>(sbase + ns * SB + FC_A_BYTES, rowsB, nt * TC_KT, D, fnorm);
+    } else {
+        for (int s = 0; s < FC_STAGES - 1; s++) {
+            if (s < nk && !(dbg & 1)) {
+                load_tile<FC_M, FC_THREADS>(sbase + s * SB, rowsA, s * TC_KT, D, fnorm);
+                load_tile<FC_N, FC_THREADS>(sbase + s * SB + FC_A_BYTES, rowsB, s * TC_KT, D, fnorm);
             }
+            asm volatile("cp.async.commit_group;\n" ::);
         }
-        asm volatile("cp.async.commit_group;\n" ::);
+        for (int it = 0; it < nk; it++) {
+            const int s = it % FC_STAGES;
+            asm volatile("cp.async.wait_group %0;\n" ::"n"(FC_STAGES - 2));
+            asm volatile("fence.proxy.async.shared::cta;\n" ::);
+            __syncthreads();
+            if (tid == 0 && !(dbg & 2)) {
+                asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+                const uint32_t st = sbase + s * SB;
+#pragma unroll
+                for (int kk = 0; kk < TC_KT / 8; kk++) {
+                    const uint64_t da = umma_desc(st + kk * 256, 128, TC_KT * 32);
+                    const uint64_t db = umma_desc(st + FC_A_BYTES + kk * 256, 128, TC_KT * 32);
+                    const uint32_t acc = (it > 0 || kk > 0) ? 1u : 0u;
+                    asm volatile(
+                        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+                        "l"(da), "l"(db), "r"(idesc), "r"(acc));
+                }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                    smem_u32(&bar_stage[s])));
+            }
+            const int nt = it + FC_STAGES - 1;
+            if (nt < nk) {
+                const int ns = nt % FC_STAGES;
+                if (nt >= FC_STAGES && !(dbg & 2)) mbar_wait(&bar_stage[ns], (uint32_t)(((nt / FC_STAGES) - 1) & 1));
+                if (!(dbg & 1)) {
+                    load_tile<FC_M, FC_THREADS>(sbase + ns * SB, rowsA, nt * TC_KT, D, fnorm);
+                    load_tile<FC_N, FC_THREADS>(sbase + ns * SB + FC_A_BYTES, rowsB, nt * TC_KT, D, fnorm);
+                }
+            }
+            asm volatile("cp.async.commit_group;\n" ::);
+        }
+        if (tid == 0 && !(dbg & 2))
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                smem_u32(&bar_done)));
     }
-    if (tid == 0 && !(dbg & 2))
-        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-            smem_u32(&bar_done)));
     if (!(dbg & 2)) mbar_wait(&bar_done, 0);
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
 
@@ -403,18 +462,27 @@ __global__ void k_row_norms(int64_t rows, int D, const float *__restrict__ X, fl
     if (lane == 0) out[w] = sqrtf(acc) * 1.00001f;  // rounded up: an upper bound of ||w||
 }
 
-// K1b over classified objects [c0, c0 + n) of a stream (topk written by object index)
+bool make_rows_map(CUtensorMap *tm, const void *base, int64_t rows, int D, int64_t row_bytes, int box_rows);
+
+// K1b over classified objects [c0, c0 + n) of a stream (topk written by object index).
+// Xdense: when the n objects' rows are the consecutive fp32 rows Xdense[0..n)
+// (standalone head, compact ingest), operands are staged by TMA.
 void launch_fc_head(int64_t n, int64_t c0, const char *const *frow, const int64_t *cls_obj, const float *fnorm, int D,
                     int V, int K, const float *W, const float *wnorm, const float *bias, int32_t *topk, float *conf,
-                    uint8_t *flag, unsigned long long *nflag, cudaStream_t st) {
+                    uint8_t *flag, unsigned long long *nflag, cudaStream_t st, const float *Xdense) {
     if (n <= 0) return;
     if (K > 16 || K > V) throw Error{FX_E_K_OUT_OF_RANGE, "fc head: k must be <= min(16, vocab)"};
     static bool attr = false;
-    const size_t smem = (size_t)FC_STAGES * (FC_A_BYTES + FC_B_BYTES);
+    const size_t smem = (size_t)FC_STAGES * (FC_A_BYTES + FC_B_BYTES) + 1024;
     if (!attr) {
-        FX_CUDA(cudaFuncSetAttribute(k_fc_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        FX_CUDA(cudaFuncSetAttribute(k_fc_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        FX_CUDA(cudaFuncSetAttribute(k_fc_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
+    static const bool tma_off = getenv("FOCUS_B200_TCLOAD") && std::string(getenv("FOCUS_B200_TCLOAD")) == "cp";
+    CUtensorMap tmA = {}, tmW = {};
+    const bool tma = Xdense && !tma_off && D % 4 == 0 && make_rows_map(&tmA, Xdense, n, D, (int64_t)D * 4, FC_M) &&
+                     make_rows_map(&tmW, W, V, D, (int64_t)D * 4, FC_N);
     const int ntile = (int)cdiv(V, FC_N);
     const float gamma = (float)((1.953125e-03 + (double)D * 2.384185791015625e-07) * 1.01);
     DevBuf<FcTile> tiles;
@@ -424,7 +492,8 @@ void launch_fc_head(int64_t n, int64_t c0, const char *const *frow, const int64_
         const int64_t m = std::min<int64_t>(CH, n - b);
         dim3 grid((unsigned)ntile, (unsigned)cdiv(m, FC_M));
         static const int dbg = getenv("FOCUS_B200_FCDBG") ? atoi(getenv("FOCUS_B200_FCDBG")) : 0;
-        k_fc_tc<<<grid, FC_THREADS, smem, st>>>((int)m, c0 + b, frow, fnorm, D, V, W, wnorm, bias, gamma, tiles.p, dbg);
+        (tma ? k_fc_tc<true> : k_fc_tc<false>)<<<grid, FC_THREADS, smem, st>>>(
+            (int)m, c0 + b, frow, fnorm, D, V, W, wnorm, bias, gamma, tiles.p, dbg, tmA, tmW, (int)b);
         FX_LAUNCHED();
         k_fc_merge<<<(unsigned)cdiv(m, 8), 256, 0, st>>>((int)m, c0 + b, frow, cls_obj, fnorm, D, V, K, W, wnorm, bias,
                                                         gamma, ntile, tiles.p, topk, conf, flag, nflag);

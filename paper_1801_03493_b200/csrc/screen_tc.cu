@@ -48,11 +48,6 @@ constexpr int TC_TILE_BYTES = TC_M * TC_KT * 4;  // 16 KB per operand per stage
 // One producer thread, one MMA-issuing thread, four warps that fold the row
 // norms out of each stage; per-stage full barriers count bytes (expect_tx),
 // empty barriers the MMA commit plus the four norm warps.
-__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
-    // K-major SWIZZLE_128B: SBO = 1024 B between 8-row atoms, LBO unused (1), version 1, layout 2
-    return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
-           ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
-}
 
 // out[a][q] = ||A_a||^2 + ||B_q||^2 - 2 A_a.B_q   (float, not clamped)
 template <bool TMA>
