@@ -82,6 +82,27 @@ def test_ingest_batch_size_invariance(name, batch):
     _check_against_golden(c, idx, rep, stream)
 
 
+@pytest.mark.parametrize("name", ["small_d64", "evict_d32", "f64_d16", "c2_prefix_d2048"])
+def test_pinned_host_inputs(name):
+    """Pinned host inputs (the e2e bench's case): chunked asynchronous H2D on a
+    side stream overlapped with the ingest of earlier chunks."""
+    import torch
+    c = GU.load(name)
+
+    def pinned(a):
+        t = torch.empty(a.shape, dtype=getattr(torch, str(a.dtype)), pin_memory=True)
+        t.numpy()[...] = a
+        return t
+
+    st = c.stream
+    keep = [pinned(np.ascontiguousarray(x)) for x in (st.oids, st.fids, st.sigs, c.feats,
+                                                      st.true_class.astype(np.int32))]
+    oids, fids, sigs, feats, tcls = (t.numpy() for t in keep)
+    idx, rep, stream = fx.ingest_arrays(oids, fids, sigs, feats, _cfg(c), _profile(c), vocab=c.spec.vocab,
+                                        seed=c.extra["seed"], pixel_eps=c.pixel_eps, true_class=tcls)
+    _check_against_golden(c, idx, rep, stream)
+
+
 @pytest.mark.parametrize("name", GU.case_names())
 def test_queries_match_reference_golden(name):
     c = GU.load(name)
