@@ -312,72 +312,131 @@ __global__ void __launch_bounds__(256) k_fc_merge(int n, int64_t a0, const char 
     const float *f = (const float *)frow[a0 + w];
     const FcTile *t = tiles + (int64_t)w * ntile;
     // K-th largest lower bound among the tiles' kept candidates (K rounds of
-    // warp argmax; the slots chosen so far are parked in s_idx)
+    // warp argmax), then the candidates: kept classes whose upper bound reaches
+    // it.  With <= 64 kept entries (V <= 1024) each lane holds its two in
+    // registers; otherwise the entries are re-read per round.
     const int nc = ntile * FC_KC;
     float lbk = -FLT_MAX;
-    for (int r = 0; r < K; r++) {
-        float best = -FLT_MAX;
-        int bslot = -1;
-        for (int e = lane; e < nc; e += 32) {
-            const int ti = e / FC_KC, j = e % FC_KC;
-            const int cls = t[ti].idx[j];
-            if (cls < 0) continue;
-            bool done = false;
-            for (int q = 0; q < r; q++) done |= (s_idx[wib][q] == e);
-            const float lv = t[ti].val[j];
-            const float lb = lv - gamma * fn * wnorm[cls] - fabsf(lv) * 2.4e-7f;
-            if (!done && lb > best) {
-                best = lb;
-                bslot = e;
-            }
-        }
-#pragma unroll
-        for (int o = 16; o; o >>= 1) {
-            const float ob = __shfl_xor_sync(0xffffffffu, best, o);
-            const int os = __shfl_xor_sync(0xffffffffu, bslot, o);
-            if (ob > best || (ob == best && os >= 0 && (bslot < 0 || os < bslot))) {
-                best = ob;
-                bslot = os;
-            }
-        }
-        __syncwarp();
-        if (lane == 0) s_idx[wib][r] = bslot;
-        __syncwarp();
-        lbk = best;
-    }
-    // candidates: kept classes whose upper bound reaches lbk
     float maxtail = -FLT_MAX;
     for (int ti = 0; ti < ntile; ti++) maxtail = fmaxf(maxtail, t[ti].tail);
-    bool all = maxtail >= lbk;
+    bool all;
     int ncand = 0;
-    if (!all) {
-        for (int e0 = 0; e0 < nc; e0 += 32) {
-            const int e = e0 + lane;
-            bool take = false;
-            int cls = -1;
-            if (e < nc) {
-                const int ti = e / FC_KC, j = e % FC_KC;
-                cls = t[ti].idx[j];
-                if (cls >= 0) {
-                    const float lv = t[ti].val[j];
-                    take = lv + gamma * fn * wnorm[cls] + fabsf(lv) * 2.4e-7f >= lbk;
-                }
-            }
-            const unsigned m = __ballot_sync(0xffffffffu, take);
-            if (take) {
-                const int pos = ncand + __popc(m & ((1u << lane) - 1u));
-                if (pos < FC_MAXC) {
-                    const int ti = e / FC_KC, j = e % FC_KC;
-                    const float lv = t[ti].val[j];
-                    const float err = gamma * fn * wnorm[cls] + fabsf(lv) * 2.4e-7f;
-                    s_idx[wib][pos] = cls;
-                    s_lb[wib][pos] = lv - err;
-                    s_ub[wib][pos] = lv + err;
-                }
-            }
-            ncand += __popc(m);
+    if (nc <= 64) {
+        int ecls[2];
+        float elv[2], elb[2], eub[2], ekb[2];  // ekb: the ranking bound, rounded as in the general path
+        bool taken[2] = {false, false};
+#pragma unroll
+        for (int u = 0; u < 2; u++) {
+            const int e = lane + 32 * u;
+            ecls[u] = e < nc ? t[e / FC_KC].idx[e % FC_KC] : -1;
+            elv[u] = e < nc ? t[e / FC_KC].val[e % FC_KC] : 0.f;
+            const float ge = ecls[u] >= 0 ? gamma * fn * wnorm[ecls[u]] : 0.f;
+            const float err = ge + fabsf(elv[u]) * 2.4e-7f;
+            ekb[u] = elv[u] - ge - fabsf(elv[u]) * 2.4e-7f;
+            elb[u] = elv[u] - err;
+            eub[u] = elv[u] + err;
         }
-        if (ncand > FC_MAXC) all = true;
+        for (int r = 0; r < K; r++) {
+            float best = -FLT_MAX;
+            int bslot = -1;
+#pragma unroll
+            for (int u = 0; u < 2; u++)
+                if (ecls[u] >= 0 && !taken[u] && ekb[u] > best) {
+                    best = ekb[u];
+                    bslot = lane + 32 * u;
+                }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+                const int os = __shfl_xor_sync(0xffffffffu, bslot, o);
+                if (ob > best || (ob == best && os >= 0 && (bslot < 0 || os < bslot))) {
+                    best = ob;
+                    bslot = os;
+                }
+            }
+            if (bslot == lane) taken[0] = true;
+            if (bslot == lane + 32) taken[1] = true;
+            lbk = best;
+        }
+        all = maxtail >= lbk;
+        if (!all) {
+#pragma unroll
+            for (int u = 0; u < 2; u++) {
+                const bool take = ecls[u] >= 0 && eub[u] >= lbk;
+                const unsigned m = __ballot_sync(0xffffffffu, take);
+                if (take) {
+                    const int pos = ncand + __popc(m & ((1u << lane) - 1u));
+                    if (pos < FC_MAXC) {
+                        s_idx[wib][pos] = ecls[u];
+                        s_lb[wib][pos] = elb[u];
+                        s_ub[wib][pos] = eub[u];
+                    }
+                }
+                ncand += __popc(m);
+            }
+            if (ncand > FC_MAXC) all = true;
+        }
+    } else {
+        for (int r = 0; r < K; r++) {
+            float best = -FLT_MAX;
+            int bslot = -1;
+            for (int e = lane; e < nc; e += 32) {
+                const int ti = e / FC_KC, j = e % FC_KC;
+                const int cls = t[ti].idx[j];
+                if (cls < 0) continue;
+                bool done = false;
+                for (int q = 0; q < r; q++) done |= (s_idx[wib][q] == e);
+                const float lv = t[ti].val[j];
+                const float lb = lv - gamma * fn * wnorm[cls] - fabsf(lv) * 2.4e-7f;
+                if (!done && lb > best) {
+                    best = lb;
+                    bslot = e;
+                }
+            }
+#pragma unroll
+            for (int o = 16; o; o >>= 1) {
+                const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+                const int os = __shfl_xor_sync(0xffffffffu, bslot, o);
+                if (ob > best || (ob == best && os >= 0 && (bslot < 0 || os < bslot))) {
+                    best = ob;
+                    bslot = os;
+                }
+            }
+            __syncwarp();
+            if (lane == 0) s_idx[wib][r] = bslot;
+            __syncwarp();
+            lbk = best;
+        }
+        all = maxtail >= lbk;
+        if (!all) {
+            for (int e0 = 0; e0 < nc; e0 += 32) {
+                const int e = e0 + lane;
+                bool take = false;
+                int cls = -1;
+                if (e < nc) {
+                    const int ti = e / FC_KC, j = e % FC_KC;
+                    cls = t[ti].idx[j];
+                    if (cls >= 0) {
+                        const float lv = t[ti].val[j];
+                        take = lv + gamma * fn * wnorm[cls] + fabsf(lv) * 2.4e-7f >= lbk;
+                    }
+                }
+                const unsigned m = __ballot_sync(0xffffffffu, take);
+                if (take) {
+                    const int pos = ncand + __popc(m & ((1u << lane) - 1u));
+                    if (pos < FC_MAXC) {
+                        const int ti = e / FC_KC, j = e % FC_KC;
+                        const float lv = t[ti].val[j];
+                        const float err = gamma * fn * wnorm[cls] + fabsf(lv) * 2.4e-7f;
+                        s_idx[wib][pos] = cls;
+                        s_lb[wib][pos] = lv - err;
+                        s_ub[wib][pos] = lv + err;
+                    }
+                }
+                ncand += __popc(m);
+            }
+            if (ncand > FC_MAXC) all = true;
+        }
     }
     __syncwarp();
     // only candidates whose TF32 interval overlaps another candidate's need
