@@ -225,8 +225,20 @@ __device__ double pw_sum_warp(const PwPlan &plan, F term, double *scratch) {
         } else {
             const int a = c - plan.leaf_chain0[L];
             const int end = len - (len % 8);
-            r = term(s + a);
-            for (int i = 8 + a; i < end; i += 8) r = dadd(r, term(s + i));
+            const int nt = (end - a + 7) / 8;  // terms a, a+8, ... < end (leaves hold <= 128 elements: nt <= 16)
+            if (nt <= 16) {
+                // every term's loads issued before the dependent adds (same add order)
+                double v[16];
+#pragma unroll
+                for (int t = 0; t < 16; t++) v[t] = t < nt ? term(s + a + 8 * t) : 0.0;
+                r = v[0];
+#pragma unroll
+                for (int t = 1; t < 16; t++)
+                    if (t < nt) r = dadd(r, v[t]);
+            } else {
+                r = term(s + a);
+                for (int i = 8 + a; i < end; i += 8) r = dadd(r, term(s + i));
+            }
         }
         chain[c] = r;
     }
