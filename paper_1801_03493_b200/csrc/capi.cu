@@ -132,12 +132,6 @@ fx_stream::~fx_stream() {
     }
     for (auto &e : ring_ev)
         if (e) cudaEventDestroy(e);
-    if (st2) {
-        cudaStreamSynchronize(st2);
-        cudaStreamDestroy(st2);
-    }
-    if (ev_pack) cudaEventDestroy(ev_pack);
-    if (ev_spec) cudaEventDestroy(ev_spec);
     for (auto &t : timers) {
         if (t.a) cudaEventDestroy(t.a);
         if (t.b) cudaEventDestroy(t.b);
@@ -204,12 +198,7 @@ int fx_stream_create(const fx_stream_config *cfg, fx_stream **out) {
                 const char *tm = getenv("FOCUS_B200_TIMERS");
                 s->timing = tm && strcmp(tm, "1") == 0;
             }
-            {  // the engine's stream runs at the highest priority: the single-CTA resolve
-               // must get an SM ahead of the pipelined screen on the side stream
-                int lo = 0, hi = 0;
-                FX_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-                FX_CUDA(cudaStreamCreateWithPriority(&s->st, cudaStreamNonBlocking, hi));
-            }
+            FX_CUDA(cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking));
             cur_stream() = s->st;
             const int D = cfg->dim;
             int B = cfg->batch;
@@ -258,9 +247,6 @@ int fx_stream_create(const fx_stream_config *cfg, fx_stream **out) {
             for (auto *b : {&s->sum_d1, &s->sum_e1, &s->sum_lbr}) b->reserve(B + 1);
             for (auto *b : {&s->ev_pos, &s->ev_vic}) b->reserve(B + 1);
             s->cid_slot.reserve(4 * (size_t)B);
-            s->nresb.reserve(2);
-            FX_CUDA(cudaMemsetAsync(s->nresb.p, 0, sizeof(int64_t) * 2, s->st));
-            s->nsnapq.reserve(2);
             s->rowmin.reserve(B + 1);
             FX_CUDA(cudaMemsetAsync(s->rowmin.p, 0x7f, sizeof(int32_t) * (B + 1), s->st));
             s->snorm.reserve(s->ld);
@@ -766,8 +752,7 @@ int fx_stream_timings(fx_stream *s, double *out, int n) {
         set_dev(s->dev);
         StreamGuard sg_(s->st);
         s->tcollect();
-        s->t_ms[16] = (double)s->n_stale;
-        for (int i = 0; i < n && i < 17; i++) out[i] = s->t_ms[i];
+        for (int i = 0; i < n && i < 16; i++) out[i] = s->t_ms[i];
     })
 }
 

@@ -25,7 +25,6 @@ enum Ctr {
     C_FAST,            // objects decided by the certain (screen-bounded) path
     C_FCFLAG,          // K1b: objects whose top-K sits within the float64 logit margin
     C_EVCUR,           // eviction cursor: every cid below it is evicted or has size > 1
-    C_LIVECHG,         // the last batch seeded or evicted (its live list changed)
     C_COUNT
 };
 
@@ -104,15 +103,6 @@ struct fx_stream {
     bool a_compact = false;
     fx::DevBuf<int32_t> orow;            // [rows of the call] classified index of each object row, -1: duplicate
     fx::DevBuf<float> C32q;              // [ld*D] FP32 snapshot packed in snapshot order (TMA screen)
-    // pipelined screen (run_batches): a second set of per-batch screen outputs,
-    // a second packed snapshot, per-buffer residual counts, the movement of the
-    // snapshot between two packs, and the side stream the screen runs on
-    fx::DevBuf<float> C32q1, cn2q, delta, dist1, dres1, sum_d1_1, sum_e1_1, sum_lbr_1, snorm1;
-    fx::DevBuf<int32_t> slotq, res_col1, res_pos1, sum_slot1, sum_q1, rowmin1, dmax;
-    fx::DevBuf<int64_t> nresb, nsnapq;   // [2] each
-    cudaStream_t st2 = nullptr;
-    cudaEvent_t ev_pack = nullptr, ev_spec = nullptr;
-    int64_t n_stale = 0;                 // batches resolved on a screen run one batch ahead
     fx::DevBuf<int32_t> cid_slot;        // [>= clusters created + 3B] slot of each cluster id
     fx::DevBuf<int32_t> s_fjoin;         // [nslots] first join position inside a window (scratch, INT_MAX)
     fx::DevBuf<int32_t> ev_pos, ev_vic;  // [B+1] window seed positions / eviction victims
@@ -136,9 +126,7 @@ struct fx_stream {
     std::vector<Timer> timers;  // pool
     std::vector<int> pending;   // indices into timers awaiting collection
     int open_timer = -1;
-    // [0..6] device phases (fx_stream_timings), [8..15] host-side ms per section,
-    // [16] batches resolved on a screen run one batch ahead
-    double t_ms[17] = {0};
+    double t_ms[16] = {0};  // [0..6] device phases (fx_stream_timings), [8..14] host-side ms per section
     void tstart(int phase);
     void tstop();
     void tcollect();

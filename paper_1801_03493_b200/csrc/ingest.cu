@@ -349,12 +349,6 @@ struct ResolveArgs {
     const int32_t *sum_slot, *sum_q;
     const float *sum_d1, *sum_e1, *sum_lbr;
     int64_t *h_ring;  // pinned host slot (UVA): counters the host reads two batches later
-    int64_t *nres;    // residual columns of this batch's screen buffer
-    // screened snapshot (packed by snapshot index q): its ||c||^2, and for a
-    // screen run one batch ahead (stale) the movement of every snapshot
-    // centroid since (delta[q], max dmax) that widens the screened intervals
-    const float *cn2q, *delta;
-    const int *dmax;  // float bits
 };
 
 constexpr int RS_THREADS = 512;
@@ -390,13 +384,9 @@ __device__ __forceinline__ void slot_bounds(const ResolveArgs &A, int b, float f
     float cn;
     if (q >= 0) {
         const float v = A.dist[(int64_t)b * A.ld + q];
-        cn = sqrtf(A.cn2q ? A.cn2q[q] : A.s_cn2[slot]) * 1.00001f;
+        cn = sqrtf(A.s_cn2[slot]) * 1.00001f;
         float l0, u0;
         snap_bounds(A.sm, v, cn, fn, l0, u0);
-        if (A.delta) {
-            l0 -= A.delta[q];
-            u0 += A.delta[q];
-        }
         d = 0.5f * (l0 + u0);
         const float dr = (float)A.s_drift[slot] * 1.00001f;
         lb = l0 - dr;
@@ -657,16 +647,12 @@ __global__ void __launch_bounds__(256) k_rowpass(int nA, int64_t a0, const char 
                                                 float *__restrict__ dres, int64_t ldr, int32_t *__restrict__ sum_slot,
                                                 int32_t *__restrict__ sum_q,
                                                 float *__restrict__ sum_d1, float *__restrict__ sum_e1,
-                                                float *__restrict__ sum_lbr, const float *__restrict__ snorm,
-                                                int packed, const int64_t *__restrict__ nsnap_dev,
-                                                const int64_t *__restrict__ nres_dev) {
-    // packed: C32 / cn2 / snap are the snapshot packed by snapshot index
-    // (k_snap_pack: rows, norms, slot list) with its own count nsnap_dev
+                                                float *__restrict__ sum_lbr, const float *__restrict__ snorm) {
     pdl_enter();
     __shared__ int s_rpos[RC_MAX];
     __shared__ int s_pmin;
-    const int nsnap = (int)(packed ? *nsnap_dev : ctr[C_NSNAP]);
-    const int nres_all = (int)*nres_dev;
+    const int nsnap = (int)ctr[C_NSNAP];
+    const int nres_all = (int)ctr[C_NRES];
     const int nres = nres_all <= RC_MAX ? nres_all : 0;  // more: the tiled kernel writes the columns
     if (threadIdx.x == 0) s_pmin = INT_MAX;
     __syncthreads();
@@ -714,9 +700,8 @@ __global__ void __launch_bounds__(256) k_rowpass(int nA, int64_t a0, const char 
                 return sqrtf(warp_sum(acc));
             };
             if (refine) {
-                const int cq = packed ? q1 : snap[q1];
-                const float dd = dist_to((const float4 *)(C32 + (int64_t)cq * D));
-                const float ee = rel * dd + absc * (sqrtf(cn2[cq]) * 1.00001f + fn) + 1e-30f;
+                const float dd = dist_to((const float4 *)(C32 + (int64_t)snap[q1] * D));
+                const float ee = rel * dd + absc * (sqrtf(cn2[snap[q1]]) * 1.00001f + fn) + 1e-30f;
                 if (dd + ee < u1) {  // keep whichever interval is tighter (both are valid)
                     d1 = dd;
                     e1 = ee;
@@ -870,9 +855,7 @@ __device__ int rs_compact(int lo, int hi, Pred pred, int32_t *out, int *wsv, int
 
 template <typename T>
 __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
-    // no early launch of the dependent fold: its CTAs would park on every SM
-    // and lock the side stream's screen of the next batch out of them
-    asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    pdl_enter();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int B = A.B;
     const int BC = A.Bcap;  // layout by capacity (multiple of 64): every array stays aligned
@@ -965,12 +948,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
         if (s_nseeds == 0 && !s_any_evicted) {
 #pragma unroll 4
             for (int p = b + tid; p < e_end; p += blockDim.x) {
-                const float d1 = A.sum_d1[p];
-                float e1 = A.sum_e1[p], lbr = A.sum_lbr[p];
-                if (A.delta && L > 0) {  // stale screen: widen by the snapshot's movement since
-                    e1 = __fadd_ru(e1, A.delta[A.sum_q[p]]);
-                    lbr = __fsub_rd(lbr, __int_as_float(*A.dmax));
-                }
+                const float d1 = A.sum_d1[p], e1 = A.sum_e1[p], lbr = A.sum_lbr[p];
                 seg_key[p] = (L > 0) ? A.sum_slot[p] : -1;
                 if (qkeys) seg_grp[p] = (short)((L > 0) ? A.sum_q[p] : -1);
                 seg_ub0[p] = (d1 + e1) * 1.000001f + 1e-30f;
@@ -988,10 +966,6 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
             const float fn = A.fnorm[A.c0 + p];
             int j1 = A.sum_slot[p];
             float d1 = A.sum_d1[p], e1 = A.sum_e1[p], lbr = A.sum_lbr[p];
-            if (A.delta && j1 >= 0) {
-                e1 = __fadd_ru(e1, A.delta[A.sum_q[p]]);
-                lbr = __fsub_rd(lbr, __int_as_float(*A.dmax));
-            }
             if (s_any_evicted && j1 >= 0 && A.s_evicted[j1] && A.res_col[p] >= 0) {
                 // probable-seed pre-test before any rescan: the snapshot summary
                 // bounds a superset of the live clusters
@@ -1020,12 +994,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
                     const int q = A.s_snapq[sl];
                     if (q < 0) continue;
                     float l0, u0;
-                    snap_bounds(A.sm, A.dist[(int64_t)p * A.ld + q], sqrtf(A.cn2q ? A.cn2q[q] : A.s_cn2[sl]) * 1.00001f,
-                                fn, l0, u0);
-                    if (A.delta) {
-                        l0 -= A.delta[q];
-                        u0 += A.delta[q];
-                    }
+                    snap_bounds(A.sm, A.dist[(int64_t)p * A.ld + q], sqrtf(A.s_cn2[sl]) * 1.00001f, fn, l0, u0);
                     const float d = 0.5f * (l0 + u0), e = 0.5f * (u0 - l0);
                     if (u0 < d1 + e1 || j1 < 0) {
                         if (j1 >= 0) lbr = fminf(lbr, d1 - e1);
@@ -1241,7 +1210,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
         //         this window within T; evictions it causes are planned below).
         //         Probable seeds earlier in the window are candidates of every
         //         later object: their in-batch distance columns (dres) bound it.
-        const int nres_w = (int)*A.nres;
+        const int nres_w = (int)A.ctr[C_NRES];
         for (int p = b + tid; p < e_end; p += blockDim.x) {
             const int key = seg_key[p];
             unsigned char fl = 2;
@@ -2003,11 +1972,9 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
         ctr[C_NEXT_CID] = s_next_cid;
         ctr[C_NINSERTED] = s_inserted;
         ctr[C_LAST_CID] = A.s_cid[sh_slot_of[B - 1]];
-        *A.nres = 0;
-        ctr[C_LIVECHG] = (s_nseeds > 0 || s_nevict > 0) ? 1 : 0;
+        ctr[C_NRES] = 0;
         if (A.h_ring) {  // zero-copy readback (no memcpy in the stream)
             A.h_ring[C_NEXT_CID] = s_next_cid;
-            A.h_ring[C_LIVECHG] = ctr[C_LIVECHG];
             __threadfence_system();
         }
     }
@@ -2310,50 +2277,14 @@ size_t resolve_smem(int Bc, const PwPlan &P) {
 // FP32 snapshot packed in snapshot order (TMA boxes of the TC screen need
 // consecutive rows): C32q[q] = C32[snap[q]], q < nsnap.
 __global__ void k_snap_pack(const int64_t *__restrict__ ctr, const int32_t *__restrict__ snap,
-                            const float *__restrict__ C32, float *__restrict__ C32q, int D,
-                            const float *__restrict__ cn2, float *__restrict__ cn2q, int32_t *__restrict__ slotq,
-                            int64_t *__restrict__ nsnapq) {
+                            const float *__restrict__ C32, float *__restrict__ C32q, int D) {
     pdl_enter();
     const int nsnap = (int)ctr[C_NSNAP];
     const int n4 = D >> 2;
-    if (blockIdx.x == 0 && threadIdx.x == 0) *nsnapq = nsnap;
     for (int q = blockIdx.x; q < nsnap; q += gridDim.x) {
-        const int sl = snap[q];
-        const float4 *src = (const float4 *)(C32 + (int64_t)sl * D);
+        const float4 *src = (const float4 *)(C32 + (int64_t)snap[q] * D);
         float4 *dst = (float4 *)(C32q + (int64_t)q * D);
         for (int k = threadIdx.x; k < n4; k += blockDim.x) dst[k] = src[k];
-        if (threadIdx.x == 0) {
-            cn2q[q] = cn2[sl];
-            slotq[q] = sl;
-        }
-    }
-}
-
-// Movement of every snapshot centroid between two packs of the same slot
-// list (a stale screen's snapshot Pold and the current Pnew): delta[q] >=
-// ||Pnew[q] - Pold[q]|| (fp32, rounded up), and their maximum in *dmax
-// (non-negative float bits, atomicMax; *dmax zeroed by the caller).
-__global__ void k_snap_delta(const int64_t *__restrict__ nsnapq, const float *__restrict__ Pnew,
-                             const float *__restrict__ Pold, int D, float *__restrict__ delta, int *__restrict__ dmax) {
-    pdl_enter();
-    const int nsnap = (int)*nsnapq;
-    const int lane = threadIdx.x & 31;
-    for (int q = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < nsnap; q += (gridDim.x * blockDim.x) >> 5) {
-        const float *a = Pnew + (int64_t)q * D, *b = Pold + (int64_t)q * D;
-        float acc = 0.f;
-        for (int k = lane; k < D; k += 32) {
-            const float d = a[k] - b[k];
-            acc = fmaf(d, d, acc);
-        }
-        acc = warp_sum(acc);
-        if (lane == 0) {
-            // fp32 sum of D squares: relative error <= (D + 2) 2^-24; the
-            // difference a - b is exact for values within a factor 2 (Sterbenz)
-            // and otherwise rounds by <= 2^-24 |a - b|
-            const float v = sqrtf(acc * (1.0f + (float)(D + 8) * 6.0e-8f)) * 1.00001f + 1e-30f;
-            delta[q] = v;
-            atomicMax(dmax, __float_as_int(v));
-        }
     }
 }
 
@@ -2425,141 +2356,6 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
     std::vector<int32_t> chk_slots;
     // fused row pass: FP32 rows, D % 4 == 0, D <= 2048, 16-byte aligned rows
     const bool rowpass = sizeof(T) == 4 && D % 4 == 0 && D <= 2048 && s->rows_aligned16;
-    // Per-batch screen outputs (distance rows, residual columns, row
-    // summaries) live in one of two buffers, the snapshot the screen reads in
-    // one of two packs.  Pipelined (TMA screen): while the single-CTA resolve
-    // of batch k runs, the screen / residual columns / row pass of batch k+1
-    // run on a side stream against the pack taken before batch k; if batch k
-    // then seeds nothing and evicts nothing (same live list), the resolve of
-    // k+1 uses them with every screened interval widened by how far each
-    // snapshot centroid moved since that pack (k_snap_delta), else the screen
-    // of k+1 is redone on the fresh pack.
-    struct SBuf {
-        float *dist, *dres, *d1, *e1, *lbr, *snorm;
-        int32_t *res_col, *res_pos, *slot, *q, *rowmin;
-        int64_t *nres;
-    };
-    // opt-in (FOCUS_B200_PIPE=1): measured slower on C2 -- the concurrent
-    // screen slows the latency-bound resolve (+8 us) and the snapshot-delta
-    // pass sits on the critical path
-    static const bool pipe_on = getenv("FOCUS_B200_PIPE") && atoi(getenv("FOCUS_B200_PIPE")) == 1;
-    const bool pipe = tma && rowpass && pipe_on && s->debug_check == 0 && c_end - c_begin > s->B;
-    SBuf sb[2];
-    sb[0] = {s->dist.p, s->dres.p, s->sum_d1.p, s->sum_e1.p, s->sum_lbr.p, s->snorm.p, s->res_col.p,
-             s->res_pos.p, s->sum_slot.p, s->sum_q.p, s->rowmin.p, s->nresb.p};
-    CUtensorMap tmBk[2];
-    float *C32qk[2] = {s->C32q.p, nullptr};
-    if (tma) {
-        tmBk[0] = tmB;
-        s->cn2q.reserve(2 * (size_t)s->ld);
-        s->slotq.reserve(2 * (size_t)s->ld);
-    }
-    if (pipe) {
-        const size_t Bc = s->B + 1;
-        s->C32q1.reserve((size_t)s->ld * D);
-        s->dist1.reserve((size_t)s->B * s->ld);
-        s->dres1.reserve((size_t)s->B * s->B);
-        for (auto *b : {&s->sum_d1_1, &s->sum_e1_1, &s->sum_lbr_1}) b->reserve(Bc);
-        s->snorm1.reserve(s->ld);
-        s->delta.reserve(s->ld);
-        for (auto *b : {&s->res_col1, &s->res_pos1, &s->sum_slot1, &s->sum_q1}) b->reserve(Bc);
-        if (!s->rowmin1.p) {
-            s->rowmin1.reserve(Bc);
-            FX_CUDA(cudaMemsetAsync(s->rowmin1.p, 0x7f, sizeof(int32_t) * Bc, st));
-        }
-        s->dmax.reserve(1);
-        if (!s->st2) {
-            int lo = 0, hi = 0;
-            FX_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-            FX_CUDA(cudaStreamCreateWithPriority(&s->st2, cudaStreamNonBlocking, lo));  // lowest priority
-        }
-        if (!s->ev_pack) FX_CUDA(cudaEventCreateWithFlags(&s->ev_pack, cudaEventDisableTiming));
-        if (!s->ev_spec) FX_CUDA(cudaEventCreateWithFlags(&s->ev_spec, cudaEventDisableTiming));
-        sb[1] = {s->dist1.p, s->dres1.p, s->sum_d1_1.p, s->sum_e1_1.p, s->sum_lbr_1.p, s->snorm1.p, s->res_col1.p,
-                 s->res_pos1.p, s->sum_slot1.p, s->sum_q1.p, s->rowmin1.p, s->nresb.p + 1};
-        C32qk[1] = s->C32q1.p;
-        if (!make_rows_map(&tmBk[1], s->C32q1.p, s->ld, D, (int64_t)D * 4, 128)) throw Error{FX_E_CUDA, "tensor map"};
-    }
-    // screen -> residual columns -> row pass of batch (c0, B) into buffer `bf`,
-    // against pack `pk` (TMA) or the slot-ordered snapshot, on stream `sx`
-    auto screen_chain = [&](int bf, int pk, int64_t c0, int B, int bix, cudaStream_t sx) {
-        const SBuf &o = sb[bf];
-        bool fused_res = false;
-        if (s->tc_screen) {
-            // the screen also produces ||f|| of the batch rows (fnorm) unless an earlier pass did
-            // fused: residual detection when the snapshot fits one column tile
-            fused_res = s->ld <= 128;
-            int rbase = 0, nR = B;
-            if (tma) {
-                rbase = (int)brows[2 * bix];
-                nR = (int)(brows[2 * bix + 1] - brows[2 * bix] + 1);
-            }
-            launch_screen_tc(B, c0, s->frow.p, s->fnorm.p, D, tma ? s->nsnapq.p + pk : s->ctr.p + C_NSNAP, (int)s->ld,
-                             s->C32.p, tma ? nullptr : s->snap_slot.p, tma ? s->cn2q.p + pk * s->ld : s->s_cn2.p,
-                             o.dist, s->ld, sx, s->has_fc ? nullptr : s->fnorm.p, sm, s->cfg.t,
-                             fused_res ? o.res_col : nullptr, o.res_pos, o.nres, o.rowmin, o.snorm,
-                             tma ? &tmA : nullptr, tma ? &tmBk[pk] : nullptr, rbase, nR,
-                             s->a_compact ? nullptr : s->orow.p);
-        } else {
-            const unsigned grid = (unsigned)std::min<int64_t>(cdiv(s->ld, SC_T) * cdiv(B, SC_T), 148 * 8);
-            FromSnapshot fb{s->C32.p, s->snap_slot.p, D};
-            k_screen<T, FromSnapshot><<<grid, 256, 0, sx>>>(B, c0, s->frow.p, D, s->ctr.p + C_NSNAP, (int)s->ld, fb,
-                                                            o.dist, s->ld);
-            FX_LAUNCHED();
-        }
-        // residuals + their in-batch columns
-        if (!fused_res && s->tc_screen) {
-            launch_pdl(k_res_from_min, dim3((unsigned)cdiv(B, 256)), dim3(256), 0, sx, B, o.rowmin, s->cfg.t,
-                       o.res_col, o.res_pos, o.nres);
-        } else if (!fused_res) {
-            launch_pdl(k_residuals, dim3((unsigned)cdiv((int64_t)B * 32, 256)), dim3(256), 0, sx, B, s->ctr.p, o.dist,
-                       s->ld, s->s_cn2.p, s->snap_slot.p, s->fnorm.p, c0, sm, s->cfg.t, o.res_col, o.res_pos, o.nres);
-        }
-        const bool rc_ok = D <= 6144;  // RC_COLS staged rows fit in shared memory
-        if (rc_ok && !rowpass) {
-            const size_t smem = sizeof(float) * RC_COLS * D;
-            static size_t rc_set[2] = {0, 0};
-            size_t &cur = rc_set[sizeof(T) == 8];
-            if (smem > 48 * 1024 && smem > cur) {
-                FX_CUDA(cudaFuncSetAttribute(k_res_cols<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                cur = smem;
-            }
-            k_res_cols<T><<<148, 256, smem, sx>>>(B, c0, s->frow.p, D, o.nres, o.res_pos, o.dres, B);
-            FX_LAUNCHED();
-        }
-        {
-            const unsigned grid = (unsigned)std::min<int64_t>(cdiv(B, SC_T) * cdiv(B, SC_T), 148);
-            FromResidual<T> fb{s->frow.p, c0, o.res_pos};
-            launch_pdl(k_screen<T, FromResidual<T>>, dim3(grid), dim3(256), 0, sx, B, c0, s->frow.p, D,
-                       (const int64_t *)o.nres, B, fb, o.dres, (int64_t)B, rc_ok ? RC_MAX : -1);
-        }
-        // row summary (+ fp32 refine of the best candidate)
-        const float *snorm = s->tc_screen ? o.snorm : nullptr;
-        const float *c32 = tma ? C32qk[pk] : s->C32.p;
-        const float *cn2 = tma ? s->cn2q.p + pk * s->ld : s->s_cn2.p;
-        const int32_t *snp = tma ? s->slotq.p + pk * s->ld : s->snap_slot.p;
-        const int64_t *nsd = s->nsnapq.p + pk;
-        if (rowpass) {
-            const unsigned grid = (unsigned)std::min<int64_t>(cdiv((int64_t)B * 32, 256), 148 * 8);
-            if (D <= 1024)
-                launch_pdl(k_rowpass<8>, dim3(grid), dim3(256), 0, sx, B, c0, s->frow.p, D, (const int64_t *)s->ctr.p,
-                           (const float *)o.dist, s->ld, cn2, snp, (const float *)s->fnorm.p, sm, rel, absc, c32,
-                           s->cfg.t, (const int32_t *)o.res_pos, o.dres, (int64_t)B, o.slot, o.q, o.d1, o.e1, o.lbr,
-                           snorm, tma ? 1 : 0, nsd, (const int64_t *)o.nres);
-            else
-                launch_pdl(k_rowpass<16>, dim3(grid), dim3(256), 0, sx, B, c0, s->frow.p, D, (const int64_t *)s->ctr.p,
-                           (const float *)o.dist, s->ld, cn2, snp, (const float *)s->fnorm.p, sm, rel, absc, c32,
-                           s->cfg.t, (const int32_t *)o.res_pos, o.dres, (int64_t)B, o.slot, o.q, o.d1, o.e1, o.lbr,
-                           snorm, tma ? 1 : 0, nsd, (const int64_t *)o.nres);
-        } else {
-            launch_pdl(k_row_summary<T>, dim3((unsigned)cdiv((int64_t)B * 32, 256)), dim3(256), 0, sx, B, s->ctr.p,
-                       o.dist, s->ld, s->s_cn2.p, s->snap_slot.p, s->fnorm.p, c0, sm, rel, absc, s->frow.p, s->C32.p, D,
-                       o.slot, o.q, o.d1, o.e1, o.lbr, snorm);
-        }
-    };
-    int pk_prev = 1;            // pack taken before the previous batch
-    bool spec = false;          // a speculative screen of the current batch is in flight
-    int spec_buf = 0, spec_pk = 0;
     for (int64_t c0 = c_begin, B = 0; c0 < c_end; c0 += B, bi++) {
         const auto h0 = hclock::now();
         // the drift bound grows like (batch size / objects so far): keep batches
@@ -2568,61 +2364,93 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
         const int64_t cap = std::max<int64_t>(64, (age / 4 / 64) * 64);
         B = (int)std::min<int64_t>(std::min<int64_t>(s->B, cap), c_end - c0);
         s->t_ms[6] += 1.0;
+        // 1. snapshot screen
+        bool fused_res = false;
         s->tstart(1);
-        // 1. pack the snapshot (state after the previous batch's fold)
-        const int pn = pipe ? pk_prev ^ 1 : 0;
-        if (tma) {
-            launch_pdl(k_snap_pack, dim3((unsigned)std::min<int64_t>(s->ld, 148 * 4)), dim3(128), 0, st,
-                       (const int64_t *)s->ctr.p, (const int32_t *)s->snap_slot.p, (const float *)s->C32.p, C32qk[pn],
-                       D, (const float *)s->s_cn2.p, s->cn2q.p + pn * s->ld, s->slotq.p + pn * s->ld, s->nsnapq.p + pn);
-            if (pipe) FX_CUDA(cudaEventRecord(s->ev_pack, st));
-        }
-        // 2. this batch's screen: the speculative one if the live list did not change since its pack
-        bool stale = false;
-        int bf = pipe ? (int)(bi & 1) : 0, pk_used = pn;
-        bool last_clean = false;  // the previous batch kept its live list (predicts the next one)
-        if (pipe && bi > 0) {
-            const int prev = (int)((s->batch_no + 2) % 3);  // ring slot of the previous batch's resolve
-            FX_CUDA(cudaEventSynchronize(s->ring_ev[prev]));
-            last_clean = s->h_ctr_ring[prev * C_COUNT + C_LIVECHG] == 0;
-        }
-        if (spec) {
-            stale = last_clean;
-            FX_CUDA(cudaStreamWaitEvent(st, s->ev_spec, 0));
-            bf = spec_buf;
-            if (stale) {
-                pk_used = spec_pk;
-                FX_CUDA(cudaMemsetAsync(s->dmax.p, 0, sizeof(int32_t), st));
-                launch_pdl(k_snap_delta, dim3(148 * 2), dim3(256), 0, st, (const int64_t *)(s->nsnapq.p + pn),
-                           C32qk[pn], C32qk[spec_pk], D, s->delta.p, s->dmax.p);
-                s->n_stale++;
+        if (s->tc_screen) {
+            // the screen also produces ||f|| of the batch rows (fnorm) unless an earlier pass did
+            // fused: residual detection when the snapshot fits one column tile
+            fused_res = s->ld <= 128;
+            int rbase = 0, nR = B;
+            if (tma) {
+                rbase = (int)brows[2 * bi];
+                nR = (int)(brows[2 * bi + 1] - brows[2 * bi] + 1);
+                launch_pdl(k_snap_pack, dim3((unsigned)std::min<int64_t>(s->ld, 148 * 4)), dim3(128), 0, st, s->ctr.p, s->snap_slot.p,
+                                                                                        s->C32.p, s->C32q.p, D);
+                FX_LAUNCHED();
             }
+            launch_screen_tc(B, c0, s->frow.p, s->fnorm.p, D, s->ctr.p + C_NSNAP, (int)s->ld, s->C32.p,
+                             s->snap_slot.p, s->s_cn2.p, s->dist.p, s->ld, st, s->has_fc ? nullptr : s->fnorm.p, sm,
+                             s->cfg.t, fused_res ? s->res_col.p : nullptr, s->res_pos.p, s->ctr.p + C_NRES,
+                             s->rowmin.p, s->snorm.p, tma ? &tmA : nullptr, tma ? &tmB : nullptr, rbase, nR,
+                             s->a_compact ? nullptr : s->orow.p);
+        } else {
+            const unsigned grid = (unsigned)std::min<int64_t>(cdiv(s->ld, SC_T) * cdiv(B, SC_T), 148 * 8);
+            FromSnapshot fb{s->C32.p, s->snap_slot.p, D};
+            k_screen<T, FromSnapshot><<<grid, 256, 0, st>>>(B, c0, s->frow.p, D, s->ctr.p + C_NSNAP, (int)s->ld, fb,
+                                                            s->dist.p, s->ld);
+            FX_LAUNCHED();
         }
-        if (!stale) {
-            if (spec) FX_CUDA(cudaMemsetAsync(sb[bf].nres, 0, sizeof(int64_t), st));  // drop the speculative columns
-            screen_chain(bf, pn, c0, B, bi, st);
+        s->tstop();
+        s->tstart(7);  // residual detection + columns
+        // 2. residuals + their in-batch columns
+        {
+            if (!fused_res && s->tc_screen) {
+                launch_pdl(k_res_from_min, dim3((unsigned)cdiv(B, 256)), dim3(256), 0, st, B, s->rowmin.p, s->cfg.t, s->res_col.p,
+                                                                      s->res_pos.p, s->ctr.p + C_NRES);
+                FX_LAUNCHED();
+            } else if (!fused_res) {
+                launch_pdl(k_residuals, dim3((unsigned)cdiv((int64_t)B * 32, 256)), dim3(256), 0, st, 
+                    B, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p, s->snap_slot.p, s->fnorm.p, c0, sm, s->cfg.t,
+                    s->res_col.p, s->res_pos.p, s->ctr.p + C_NRES);
+                FX_LAUNCHED();
+            }
+            const bool rc_ok = D <= 6144;  // RC_COLS staged rows fit in shared memory
+            if (rc_ok && !rowpass) {
+                const size_t smem = sizeof(float) * RC_COLS * D;
+                static size_t rc_set[2] = {0, 0};
+                size_t &cur = rc_set[sizeof(T) == 8];
+                if (smem > 48 * 1024 && smem > cur) {
+                    FX_CUDA(cudaFuncSetAttribute(k_res_cols<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                    cur = smem;
+                }
+                k_res_cols<T><<<148, 256, smem, st>>>(B, c0, s->frow.p, D, s->ctr.p + C_NRES, s->res_pos.p, s->dres.p, B);
+                FX_LAUNCHED();
+            }
+            const unsigned grid = (unsigned)std::min<int64_t>(cdiv(B, SC_T) * cdiv(B, SC_T), 148);
+            FromResidual<T> fb{s->frow.p, c0, s->res_pos.p};
+            launch_pdl(k_screen<T, FromResidual<T>>, dim3(grid), dim3(256), 0, st, B, c0, s->frow.p, D, s->ctr.p + C_NRES, B, fb, s->dres.p, B,
+                                                               rc_ok ? RC_MAX : -1);
+            FX_LAUNCHED();
+        }
+        s->tstop();
+        s->tstart(15);  // row summary (+ fp32 refine of the best candidate)
+        const float *snorm = s->tc_screen ? s->snorm.p : nullptr;
+        if (rowpass) {
+            const unsigned grid = (unsigned)std::min<int64_t>(cdiv((int64_t)B * 32, 256), 148 * 8);
+            if (D <= 1024)
+                launch_pdl(k_rowpass<8>, dim3(grid), dim3(256), 0, st, B, c0, s->frow.p, D, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p,
+                                                   s->snap_slot.p, s->fnorm.p, sm, rel, absc, s->C32.p, s->cfg.t,
+                                                   s->res_pos.p, s->dres.p, B, s->sum_slot.p, s->sum_q.p, s->sum_d1.p,
+                                                   s->sum_e1.p, s->sum_lbr.p, snorm);
+            else
+                launch_pdl(k_rowpass<16>, dim3(grid), dim3(256), 0, st, B, c0, s->frow.p, D, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p,
+                                                    s->snap_slot.p, s->fnorm.p, sm, rel, absc, s->C32.p, s->cfg.t,
+                                                    s->res_pos.p, s->dres.p, B, s->sum_slot.p, s->sum_q.p, s->sum_d1.p,
+                                                   s->sum_e1.p, s->sum_lbr.p, snorm);
+            FX_LAUNCHED();
+        } else {
+        launch_pdl(k_row_summary<T>, dim3((unsigned)cdiv((int64_t)B * 32, 256)), dim3(256), 0, st, 
+                B, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p, s->snap_slot.p, s->fnorm.p, c0, sm, rel, absc, s->frow.p,
+                s->C32.p, D, s->sum_slot.p, s->sum_q.p, s->sum_d1.p, s->sum_e1.p, s->sum_lbr.p, snorm);
+            FX_LAUNCHED();
         }
         s->tstop();
         const auto h1 = hclock::now();
         s->t_ms[8] += hms(h0, h1);
-        // 3. speculative screen of the next batch on the side stream, against this pack
-        spec = false;
-        if (pipe && c0 + B < c_end && (bi == 0 || last_clean)) {
-            const int64_t n0 = c0 + B;
-            const int64_t cap1 = std::max<int64_t>(64, (n0 / 4 / 64) * 64);
-            const int B1 = (int)std::min<int64_t>(std::min<int64_t>(s->B, cap1), c_end - n0);
-            FX_CUDA(cudaStreamWaitEvent(s->st2, s->ev_pack, 0));
-            screen_chain(bf ^ 1, pn, n0, B1, bi + 1, s->st2);
-            FX_CUDA(cudaEventRecord(s->ev_spec, s->st2));
-            spec = true;
-            spec_buf = bf ^ 1;
-            spec_pk = pn;
-        }
-        pk_prev = pn;
-        // 4. resolve (parallel verified segments + exact sequential events)
+        // 3. resolve (parallel verified segments + exact sequential events)
         s->tstart(2);
         {
-            const SBuf &o = sb[bf];
             ResolveArgs A;
             A.B = B;
             A.Bcap = s->B;
@@ -2633,16 +2461,12 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             A.rel = rel;
             A.absc = absc;
             A.sm = sm;
-            A.dist = o.dist;
+            A.dist = s->dist.p;
             A.ld = s->ld;
-            A.dres = o.dres;
+            A.dres = s->dres.p;
             A.ldr = B;
-            A.res_col = o.res_col;
-            A.res_pos = o.res_pos;
-            A.nres = o.nres;
-            A.cn2q = tma ? s->cn2q.p + pk_used * s->ld : nullptr;
-            A.delta = stale ? s->delta.p : nullptr;
-            A.dmax = s->dmax.p;
+            A.res_col = s->res_col.p;
+            A.res_pos = s->res_pos.p;
             A.dod = s->dod.p;
             A.frow = s->frow.p;
             A.fnorm = s->fnorm.p;
@@ -2685,11 +2509,11 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             A.s_grp = s->s_grp.p;
             A.prof = (long long *)s->prof.p;
             A.batch_no = (int)s->batch_no;
-            A.sum_slot = o.slot;
-            A.sum_q = o.q;
-            A.sum_d1 = o.d1;
-            A.sum_e1 = o.e1;
-            A.sum_lbr = o.lbr;
+            A.sum_slot = s->sum_slot.p;
+            A.sum_q = s->sum_q.p;
+            A.sum_d1 = s->sum_d1.p;
+            A.sum_e1 = s->sum_e1.p;
+            A.sum_lbr = s->sum_lbr.p;
             A.h_ring = s->h_ctr_ring + (s->batch_no % 3) * C_COUNT;
             const PwPlan &P = *s->plan_host;
             size_t smem = resolve_smem(s->B, P);

@@ -346,7 +346,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
 #pragma unroll
         for (int j = 0; j < 4; j++)
             if (c + j < ncol) {
-                const float c2 = snap ? cn2[snap[tb + c + j]] : cn2[tb + c + j];  // no list: packed norms
+                const float c2 = cn2[snap[tb + c + j]];
                 const float v = fa2 + c2 - 2.f * d4[j];
                 o[j] = v;
                 if (res_col || rowmin_g) {
@@ -358,8 +358,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
         if (res_col || rowmin_g) atomicMin(&rowmin[rr], __float_as_int(fmaxf(mn, 0.f)));
     }
     if (snorm && ta == 0 && rank == 0)
-        for (int c = tid; c < ncol; c += TC_THREADS)
-            snorm[tb + c] = sqrtf(snap ? cn2[snap[tb + c]] : cn2[tb + c]) * 1.00001f;
+        for (int c = tid; c < ncol; c += TC_THREADS) snorm[tb + c] = sqrtf(cn2[snap[tb + c]]) * 1.00001f;
     if (rowmin_g) {
         // several column tiles: per-row minimum across CTAs (k_res_from_min flags the residuals)
         __syncthreads();

@@ -116,13 +116,13 @@ class Stream:
         return cl, dup.astype(bool), tk.reshape(n, k)
 
     COUNTERS = ("nlive", "next_cid", "dc", "nfree", "nevict_total", "exact", "nsnap", "nres", "ninserted",
-                "nevict_batch", "ndefer", "nod", "last_cid", "ndirty", "err", "fast", "fc_flagged", "ev_cursor", "live_changed",
+                "nevict_batch", "ndefer", "nod", "last_cid", "ndirty", "err", "fast", "fc_flagged", "ev_cursor",
                 "cyc_passA", "cyc_passB", "cyc_passCD", "cyc_confirm", "cyc_passE", "cyc_seq", "windows", "seq_steps",
                 "conf_b0", "conf_b1_7", "conf_b8_15", "conf_b16_31", "conf_b32_63", "conf_b64_127", "conf_b128",
                 "conf_young", "fold_wait_cyc", "fold_chain_cyc", "fold_slot_cyc", "fold_rows", "fold_slots")
     PHASES = ("k0_k1a", "screen", "resolve", "fold", "seal", "index", "batches", "screen_resid",
               "host_screen", "host_resolve", "host_ring", "host_fold", "host_grow", "host_k0", "host_k1",
-              "screen_summary", "stale_batches")
+              "screen_summary")
 
     def set_timing(self, on: bool = True) -> None:
         """Record per-phase CUDA-event timers (off by default: they add gaps)."""
