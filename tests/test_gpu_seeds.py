@@ -62,3 +62,11 @@ def test_seed_heavy_streams_match_oracle(seed, t, m, dim, batch):
 ])
 def test_window_evictions_match_oracle(seed, t, m, dim, batch, classes, dup):
     _run(seed, t, m, dim, n=4000, classes=classes, batch=batch, dup_rate=dup)
+
+
+@pytest.mark.timeout(600)
+def test_large_saturated_stream_many_cta_waves():
+    """30 k objects against up to 5 k live clusters: the TMA screen runs
+    several CTA waves over many snapshot column tiles (residuals found by the
+    cross-tile row minimum), every batch evicts through the size-1 FIFO."""
+    _run(41, 0.5, 5000, 64, n=30000, classes=500, batch=0, dup_rate=0.2)
