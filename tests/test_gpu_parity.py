@@ -207,3 +207,16 @@ def test_saved_index_file_equals_reference_file(name, tmp_path):
     out = tmp_path / "idx.focusidx"
     fx.save(idx, str(out))
     assert out.read_bytes() == want
+
+
+def test_lookup_on_loaded_index_file():
+    """fx.load (reference parser) then fx.lookup: the device index is posted on
+    first lookup; every class x k_x equals the filter of the file's class ranks."""
+    import os
+    path = os.path.join(GU.GOLDEN, "index_spec_d32.focusidx")
+    idx = fx.load(path)
+    V = idx.header.vocab
+    for cls in list(range(V)) + [fx.OTHER_CLASS]:
+        for kx in range(1, idx.header.k + 1):
+            want = sorted(cid for cid, c in idx.clusters.items() if c.class_best_rank.get(cls, 10 ** 9) <= kx)
+            assert fx.lookup(idx, cls, kx) == want, (cls, kx)
