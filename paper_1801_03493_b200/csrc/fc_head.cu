@@ -531,7 +531,8 @@ void launch_fc_head(int64_t n, int64_t c0, const char *const *frow, const int64_
                     uint8_t *flag, unsigned long long *nflag, cudaStream_t st, const float *Xdense) {
     if (n <= 0) return;
     if (K > 16 || K > V) throw Error{FX_E_K_OUT_OF_RANGE, "fc head: k must be <= min(16, vocab)"};
-    static bool attr = false;
+    static bool attr_set[64] = {};
+    bool &attr = attr_set[dev_slot()];
     const size_t smem = (size_t)FC_STAGES * (FC_A_BYTES + FC_B_BYTES) + 1024;
     if (!attr) {
         FX_CUDA(cudaFuncSetAttribute(k_fc_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

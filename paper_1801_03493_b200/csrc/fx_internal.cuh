@@ -48,6 +48,14 @@ struct Error {
 
 void count_launch();
 
+// cudaFuncSetAttribute applies per device: launchers remember what they set
+// per device ordinal (a process may drive several GPUs)
+inline int dev_slot() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return d < 0 ? 0 : (d > 63 ? 63 : d);
+}
+
 // Programmatic dependent launch for the per-batch kernel chain (screen ->
 // residual columns -> row pass -> resolve -> fold -> next batch's pack):
 // the next kernel is launched while this one runs, its CTAs park in

@@ -2414,8 +2414,8 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             const bool rc_ok = D <= 6144;  // RC_COLS staged rows fit in shared memory
             if (rc_ok && !rowpass) {
                 const size_t smem = sizeof(float) * RC_COLS * D;
-                static size_t rc_set[2] = {0, 0};
-                size_t &cur = rc_set[sizeof(T) == 8];
+                static size_t rc_set[64] = {};
+                size_t &cur = rc_set[dev_slot()];
                 if (smem > 48 * 1024 && smem > cur) {
                     FX_CUDA(cudaFuncSetAttribute(k_res_cols<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
                     cur = smem;
@@ -2524,8 +2524,8 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             const PwPlan &P = *s->plan_host;
             size_t smem = resolve_smem(s->B, P);
             auto kern = k_resolve<T>;
-            static size_t smem_set[2] = {0, 0};
-            size_t &cur = smem_set[sizeof(T) == 8];
+            static size_t smem_set[64] = {};
+            size_t &cur = smem_set[dev_slot()];
             if (smem > cur) {
                 FX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
                 cur = smem;
@@ -2618,10 +2618,10 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             const int64_t gx = cdiv(D, FD);
             const int64_t gy = std::max<int64_t>(8, std::min<int64_t>(2 * (int64_t)B + 1, (148 * 12) / gx));
             dim3 grid((unsigned)gx, (unsigned)gy);
-            static bool fold_attr[2] = {false, false};
-            if (!fold_attr[sizeof(T) == 8]) {
+            static bool fold_attr[64] = {};
+            if (!fold_attr[dev_slot()]) {
                 FX_CUDA(cudaFuncSetAttribute(k_fold<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fold_smem<T>()));
-                fold_attr[sizeof(T) == 8] = true;
+                fold_attr[dev_slot()] = true;
             }
             launch_pdl(k_fold<T>, dim3(grid), dim3(FOLD_THREADS), fold_smem<T>(), st, D, c0, s->ctr.p, s->dirty.p, s->dirty_off.p, s->pend_list.p, s->frow.p,
                                             s->S.p, s->C32.p, s->s_nfeat.p, s->s_foldpos.p, s->s_seedpos.p,

@@ -436,7 +436,8 @@ void launch_screen_tc(int nA, int64_t a0, const char *const *frow, const float *
     // residual detection inside one tile, or across tiles through rowmin_g
     if (nB_max > TC_N) res_col = nullptr;
     else rowmin_g = nullptr;
-    static bool attr = false;
+    static bool attr_set[64] = {};
+    bool &attr = attr_set[dev_slot()];
     if (!attr) {
         for (auto k : {k_screen_tc<false>, k_screen_tc<true>})
             FX_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)screen_tc_smem()));
