@@ -648,12 +648,7 @@ __global__ void __launch_bounds__(256) k_rowpass(int nA, int64_t a0, const char 
                                                 int32_t *__restrict__ sum_q,
                                                 float *__restrict__ sum_d1, float *__restrict__ sum_e1,
                                                 float *__restrict__ sum_lbr, const float *__restrict__ snorm) {
-    // PDL: the inputs (screen rows, norms, residual list) come from kernels
-    // before the immediately preceding one (the tiled residual columns, whose
-    // output this kernel neither reads nor shares), so the row pass runs
-    // alongside it and waits for it only before exiting -- the resolve after
-    // this grid still sees every earlier grid complete
-    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
+    pdl_enter();
     __shared__ int s_rpos[RC_MAX];
     __shared__ int s_pmin;
     const int nsnap = (int)ctr[C_NSNAP];
@@ -729,7 +724,6 @@ __global__ void __launch_bounds__(256) k_rowpass(int nA, int64_t a0, const char 
             sum_lbr[w] = lbr;
         }
     }
-    asm volatile("griddepcontrol.wait;\n" ::: "memory");
 }
 
 constexpr int RS_MAXGRP = 512;
