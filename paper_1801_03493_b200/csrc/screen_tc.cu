@@ -64,12 +64,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
                                                            const __grid_constant__ CUtensorMap tmA,
                                                            const __grid_constant__ CUtensorMap tmB, int rbase, int nR,
                                                            const int32_t *__restrict__ rmap) {
-    // PDL: with TMA staging only the snapshot pack (operand B) comes from the
-    // previous kernel -- the setup, the TMEM allocation and the first stages'
-    // feature rows proceed while it finishes; the producer waits before its
-    // first B load.  The cp.async path waits here.
-    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
-    if (!TMA) asm volatile("griddepcontrol.wait;\n" ::: "memory");
+    pdl_enter();
     // blockIdx.z selects the K range [z*kchunk, (z+1)*kchunk) (split-K when the
     // tile grid alone cannot fill the machine; partials are atomically added).
     // blockIdx.x = column tile * row tiles + row tile: the CTAs that share a
@@ -154,35 +149,24 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
         if (warp == 4 && lane == 0) {  // producer: one 128-row box of A and of B per stage
             asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmA) : "memory");
             asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmB) : "memory");
-            auto load = [&](const CUtensorMap *tm, uint32_t dst, int k, int row, uint32_t fb) {
-                asm volatile(
-                    "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
-                    "%3}], [%4];\n" ::"r"(dst),
-                    "l"(tm), "r"(k), "r"(row), "r"(fb)
-                    : "memory");
-            };
-            // first stages: feature rows now, snapshot rows once the pack is done
-            const int n0 = nk < TC_STAGES ? nk : TC_STAGES;
-            for (int it = 0; it < n0; it++) {
-                const uint32_t fb = smem_u32(&bar_full[it]);
-                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(fb), "r"(2 * TC_TILE_BYTES)
-                             : "memory");
-                load(&tmA, sbase + it * 2 * TC_TILE_BYTES, kbeg + it * TC_KT, rbase + ta, fb);
-            }
-            asm volatile("griddepcontrol.wait;\n" ::: "memory");
-            for (int it = 0; it < n0; it++)
-                load(&tmB, sbase + it * 2 * TC_TILE_BYTES + TC_TILE_BYTES, kbeg + it * TC_KT, tb,
-                     smem_u32(&bar_full[it]));
-            for (int it = n0; it < nk; it++) {
+            for (int it = 0; it < nk; it++) {
                 const int s = it % TC_STAGES;
-                mbar_wait(&bar_stage[s], (uint32_t)(((it / TC_STAGES) - 1) & 1));
+                if (it >= TC_STAGES) mbar_wait(&bar_stage[s], (uint32_t)(((it / TC_STAGES) - 1) & 1));
                 const uint32_t st = sbase + s * 2 * TC_TILE_BYTES;
                 const uint32_t fb = smem_u32(&bar_full[s]);
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(fb), "r"(2 * TC_TILE_BYTES)
                              : "memory");
                 const int k = kbeg + it * TC_KT;
-                load(&tmA, st, k, rbase + ta, fb);
-                load(&tmB, st + TC_TILE_BYTES, k, tb, fb);
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+                    "%3}], [%4];\n" ::"r"(st),
+                    "l"(&tmA), "r"(k), "r"(rbase + ta), "r"(fb)
+                    : "memory");
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+                    "%3}], [%4];\n" ::"r"(st + TC_TILE_BYTES),
+                    "l"(&tmB), "r"(k), "r"(tb), "r"(fb)
+                    : "memory");
             }
         } else if (warp == 5) {  // MMA issue
             for (int it = 0; it < nk; it++) {
