@@ -31,7 +31,7 @@
 
 namespace fx {
 
-constexpr int FC_M = 128, FC_N = 256, FC_STAGES = 4, FC_THREADS = 128, FC_KC = 16;
+constexpr int FC_M = 128, FC_N = 256, FC_STAGES = 4, FC_THREADS = 256, FC_KC = 16;
 constexpr int FC_A_BYTES = FC_M * TC_KT * 4, FC_B_BYTES = FC_N * TC_KT * 4;
 
 struct FcTile {  // per (object, class tile) result of k_fc_tc
@@ -177,12 +177,15 @@ __global__ void __launch_bounds__(FC_THREADS, 1) k_fc_tc(int n, int64_t a0, cons
     if (!(dbg & 2)) mbar_wait(&bar_done, 0);
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
 
-    // epilogue: thread = object row; keep the FC_KC largest logits (sorted
-    // descending, ties -> smaller class id) in registers.  The tail (largest
-    // upper bound of a dropped class) uses the largest logit dropped and the
-    // tile's largest ||w|| (one max per logit); the logsumexp partial is a
-    // second pass over TMEM once the row maximum is known (no exp chain).
-    const int a = ta + warp * 32 + lane;
+    // epilogue: warps w and w+4 share TMEM lanes 32(w%4).. (object rows) and
+    // take one half of the 256 classes each; a thread keeps the FC_KC largest
+    // logits of its half (sorted descending, ties -> smaller class id), the
+    // largest dropped logit and a logsumexp partial, then the upper half hands
+    // its list to the lower one through shared memory (its class ids are all
+    // larger, so inserting after keeps the tie order).  The tail (largest
+    // upper bound of a dropped class) uses the tile's largest ||w||.
+    const int quad = warp & 3, half = warp >> 2;
+    const int a = ta + quad * 32 + lane;
     const float fn = a < n ? fnorm[a0 + a] : 0.f;
     __shared__ float s_wmax[FC_THREADS / 32];
     {
@@ -206,7 +209,7 @@ __global__ void __launch_bounds__(FC_THREADS, 1) k_fc_tc(int n, int64_t a0, cons
     }
     float dropped = -FLT_MAX;
     auto tmem_row = [&](int c0, uint32_t *v) {
-        const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
+        const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)c0;
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
             "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
@@ -217,38 +220,39 @@ __global__ void __launch_bounds__(FC_THREADS, 1) k_fc_tc(int n, int64_t a0, cons
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
     };
-    for (int c0 = 0; c0 < FC_N; c0 += 32) {
+    auto insert = [&](float x, int xi) {  // strict > keeps the earlier (smaller) id first
+        if (x > kv[FC_KC - 1]) {
+            dropped = fmaxf(dropped, kv[FC_KC - 1]);
+#pragma unroll
+            for (int q = 0; q < FC_KC; q++) {
+                if (x > kv[q]) {
+                    const float tvv = kv[q];
+                    const int tii = ki[q];
+                    kv[q] = x;
+                    ki[q] = xi;
+                    x = tvv;
+                    xi = tii;
+                }
+            }
+        } else {
+            dropped = fmaxf(dropped, x);
+        }
+    };
+    constexpr int HC = FC_N / 2;
+    for (int c0 = half * HC; c0 < (half + 1) * HC; c0 += 32) {
         uint32_t v[32];
         tmem_row(c0, v);
 #pragma unroll 4
         for (int j = 0; j < 32; j++) {
             const int cls = tv + c0 + j;
             if (a >= n || cls >= V) break;
-            float x = __uint_as_float(v[j]) + (bias ? bias[cls] : 0.f);
-            int xi = cls;
-            if (x > kv[FC_KC - 1]) {
-                dropped = fmaxf(dropped, kv[FC_KC - 1]);
-#pragma unroll
-                for (int q = 0; q < FC_KC; q++) {  // insertion, strict > keeps the earlier (smaller) id first
-                    if (x > kv[q]) {
-                        const float tvv = kv[q];
-                        const int tii = ki[q];
-                        kv[q] = x;
-                        ki[q] = xi;
-                        x = tvv;
-                        xi = tii;
-                    }
-                }
-            } else {
-                dropped = fmaxf(dropped, x);
-            }
+            insert(__uint_as_float(v[j]) + (bias ? bias[cls] : 0.f), cls);
         }
     }
-    const float tail = dropped == -FLT_MAX ? -FLT_MAX : dropped + gamma * fn * wmax + fabsf(dropped) * 2.4e-7f;
-    const float m = kv[0];
+    float m = kv[0];
     float ssum = 0.f;
     if (!(dbg & 4))
-        for (int c0 = 0; c0 < FC_N; c0 += 32) {
+        for (int c0 = half * HC; c0 < (half + 1) * HC; c0 += 32) {
             uint32_t v[32];
             tmem_row(c0, v);
 #pragma unroll
@@ -257,16 +261,49 @@ __global__ void __launch_bounds__(FC_THREADS, 1) k_fc_tc(int n, int64_t a0, cons
                 if (a < n && cls < V) ssum += __expf(__uint_as_float(v[j]) + (bias ? bias[cls] : 0.f) - m);
             }
         }
-    if (a < n) {
-        FcTile *o = out + (int64_t)a * gridDim.x + blockIdx.x;
+    // upper half -> lower half (pipeline shared memory is idle now)
+    float *hv = (float *)smem;                       // [128][FC_KC]
+    int *hi = (int *)(hv + FC_M * FC_KC);            // [128][FC_KC]
+    float *hx = (float *)(hi + FC_M * FC_KC);        // [128][3]: dropped, m, ssum
+    const int r = quad * 32 + lane;
+    __syncthreads();
+    if (half == 1) {
 #pragma unroll
         for (int j = 0; j < FC_KC; j++) {
-            o->val[j] = kv[j];
-            o->idx[j] = ki[j];
+            hv[r * FC_KC + j] = kv[j];
+            hi[r * FC_KC + j] = ki[j];
         }
-        o->tail = tail;
-        o->lse_m = m;
-        o->lse_s = ssum;
+        hx[r * 3 + 0] = dropped;
+        hx[r * 3 + 1] = m;
+        hx[r * 3 + 2] = ssum;
+    }
+    __syncthreads();
+    if (half == 0) {
+        for (int j = 0; j < FC_KC; j++) {
+            const float x = hv[r * FC_KC + j];
+            if (!(x > kv[FC_KC - 1])) {  // sorted: the rest are no larger
+                dropped = fmaxf(dropped, x);
+                break;
+            }
+            insert(x, hi[r * FC_KC + j]);
+        }
+        dropped = fmaxf(dropped, hx[r * 3 + 0]);
+        const float m1 = hx[r * 3 + 1], s1 = hx[r * 3 + 2];
+        const float mm = fmaxf(m, m1);
+        ssum = (ssum > 0.f ? ssum * __expf(m - mm) : 0.f) + (s1 > 0.f ? s1 * __expf(m1 - mm) : 0.f);
+        m = kv[0];
+        const float tail = dropped == -FLT_MAX ? -FLT_MAX : dropped + gamma * fn * wmax + fabsf(dropped) * 2.4e-7f;
+        if (a < n) {
+            FcTile *o = out + (int64_t)a * gridDim.x + blockIdx.x;
+#pragma unroll
+            for (int j = 0; j < FC_KC; j++) {
+                o->val[j] = kv[j];
+                o->idx[j] = ki[j];
+            }
+            o->tail = tail;
+            o->lse_m = m;
+            o->lse_s = ssum;
+        }
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
     __syncthreads();
