@@ -239,6 +239,7 @@ __global__ void __launch_bounds__(FC_THREADS, 1) k_fc_tc(int n, int64_t a0, cons
         }
     };
     constexpr int HC = FC_N / 2;
+    float m = -FLT_MAX, ssum = 0.f;  // online logsumexp partial (one TMEM pass)
     for (int c0 = half * HC; c0 < (half + 1) * HC; c0 += 32) {
         uint32_t v[32];
         tmem_row(c0, v);
@@ -246,21 +247,16 @@ __global__ void __launch_bounds__(FC_THREADS, 1) k_fc_tc(int n, int64_t a0, cons
         for (int j = 0; j < 32; j++) {
             const int cls = tv + c0 + j;
             if (a >= n || cls >= V) break;
-            insert(__uint_as_float(v[j]) + (bias ? bias[cls] : 0.f), cls);
+            const float x = __uint_as_float(v[j]) + (bias ? bias[cls] : 0.f);
+            if (x > m) {
+                ssum = ssum * __expf(m - x) + 1.f;
+                m = x;
+            } else {
+                ssum += __expf(x - m);
+            }
+            insert(x, cls);
         }
     }
-    float m = kv[0];
-    float ssum = 0.f;
-    if (!(dbg & 4))
-        for (int c0 = half * HC; c0 < (half + 1) * HC; c0 += 32) {
-            uint32_t v[32];
-            tmem_row(c0, v);
-#pragma unroll
-            for (int j = 0; j < 32; j++) {
-                const int cls = tv + c0 + j;
-                if (a < n && cls < V) ssum += __expf(__uint_as_float(v[j]) + (bias ? bias[cls] : 0.f) - m);
-            }
-        }
     // upper half -> lower half (pipeline shared memory is idle now)
     float *hv = (float *)smem;                       // [128][FC_KC]
     int *hi = (int *)(hv + FC_M * FC_KC);            // [128][FC_KC]
