@@ -159,6 +159,8 @@ def main():
     ap.add_argument("--no-fc", action="store_true", help="skip the K1b FC head sub-benchmark")
     ap.add_argument("--multi-streams", type=int, default=8, help="concurrent engines for the C4-shape line (<=1: skip)")
     ap.add_argument("--multi-objects", type=int, default=1_000_000, help="objects per engine in the C4-shape line")
+    ap.add_argument("--c3-objects", type=int, default=300_000,
+                    help="objects of the C3-shape line (T=5, M=100k: every object seeds; 0 = skip)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -424,6 +426,40 @@ def main():
                                        "inputs resident, wall clock (median of 3 runs), max over ranks"}
         del datas
 
+    # C3 shape (BASELINE configs[2]: M = 100 k, T = 5 -- every object seeds,
+    # the live set saturates at 100 k and every batch evicts) on a bounded
+    # prefix, inputs resident; parity of this path: tests/test_gpu_seeds.py
+    c3res = None
+    if args.c3_objects > 0:
+        n3 = args.c3_objects
+        d3 = synth.generate(n3, dim=W["dim"], vocab=W["vocab"], n_stream_classes=W["n_stream_classes"],
+                            seed=1 + rank)
+        torch.cuda.synchronize()
+        t3 = []
+        for _ in range(2):  # the first run pays the allocations of the 100 k-slot engine
+            s3 = fx.ingest.Stream(W["dim"], 16, W["vocab"], W["k"], 5.0, 100_000, 0.01, _lib.FX_F32, local, 0)
+            s3.set_rank_model(prof, 0)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            s3.ingest_device(n3, d3.oids.data_ptr(), d3.fids.data_ptr(), d3.sigs.data_ptr(), d3.feats.data_ptr(),
+                             d3.true_class.data_ptr())
+            ix3, rp3 = s3.finalize()
+            torch.cuda.synchronize()
+            t3.append(time.perf_counter() - t0)
+            c3c = s3.counters()
+            del ix3, s3
+        dt3 = min(t3)
+        if ws > 1:
+            tt = torch.tensor([dt3], device=dev_red)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            dt3 = float(tt.item())
+        c3res = {"objects_per_stream": n3, "objects_per_s": n3 * ws / dt3, "wall_s": dt3,
+                 "clusters": rp3.clusters_emitted, "evictions": int(c3c["nevict_total"]),
+                 "distance_computations": rp3.distance_computations,
+                 "note": "C3 shape: T=5.0, M=100000 (every object seeds, live set saturated), "
+                         "wall clock incl. engine create/finalize, inputs resident, best of 2"}
+        del d3
+
     # K1b FC classifier head (north star kernel 1) on resident features:
     # logits over V classes, top-K; tensor-pipe roofline against TF32 dense
     fcres = None
@@ -480,7 +516,7 @@ def main():
                        "streams_per_gpu": 1, "parallelism": f"stream-sharded x{ws}",
                        "l2": "inputs (8 GB features/stream) exceed L2; no flush", **W},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
-            "query": qres, "k1b_fc_head": fcres, "multi_stream": msres,
+            "query": qres, "k1b_fc_head": fcres, "multi_stream": msres, "c3_shape": c3res,
             "gpu_launches": int(launches),
             "ingest": {"clusters": rep.clusters_emitted, "classified": rep.objects_classified,
                        "distance_computations": rep.distance_computations, "exact_rechecks": rep.exact_rechecks,
