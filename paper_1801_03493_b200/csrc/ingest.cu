@@ -666,6 +666,18 @@ __global__ void __launch_bounds__(256) k_rowpass(int nA, int64_t a0, const char 
     const int nw = blockDim.x >> 5;
     for (int w = blockIdx.x * nw + (threadIdx.x >> 5); w < nA; w += gridDim.x * nw) {
         const float fn = fnorm[a0 + w];
+        // the row's features are needed whenever the TC screen ran (refine):
+        // their loads fly while the distance row is scanned
+        const float4 *f4 = (const float4 *)frow[a0 + w];
+        float4 x[NV];
+        const bool pre = sm.tc && nsnap > 0;
+        if (pre) {
+#pragma unroll
+            for (int j = 0; j < NV; j++) {
+                const int e = lane + 32 * j;
+                x[j] = (4 * e < D) ? __ldg(f4 + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+        }
         float u1, l1, lbr;
         int q1;
         row_scan(dist + (int64_t)w * ld, nsnap, cn2, snap, snorm, sm, fn, lane, u1, l1, lbr, q1);
@@ -673,12 +685,12 @@ __global__ void __launch_bounds__(256) k_rowpass(int nA, int64_t a0, const char 
         const bool refine = sm.tc && q1 >= 0;  // a tight ub0 keeps the resolve's drift bounds small
         const bool cols = nres > 0 && w > pmin;
         if (refine || cols) {
-            const float4 *f4 = (const float4 *)frow[a0 + w];
-            float4 x[NV];
+            if (!pre) {
 #pragma unroll
-            for (int j = 0; j < NV; j++) {
-                const int e = lane + 32 * j;
-                x[j] = (4 * e < D) ? __ldg(f4 + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+                for (int j = 0; j < NV; j++) {
+                    const int e = lane + 32 * j;
+                    x[j] = (4 * e < D) ? __ldg(f4 + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
             }
             auto dist_to = [&](const float4 *c4) {
                 float acc = 0.f;
