@@ -2011,7 +2011,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
 // for the dominant cluster of a Zipf stream, which owns most of a batch.
 constexpr int FD = 32, FOLD_NS = 6, FOLD_THREADS = 32 * (1 + FOLD_NS);
 template <typename T>
-constexpr int fold_rows() { return sizeof(T) == 4 ? 64 : 32; }  // 8 KB per stage either way
+constexpr int fold_rows() { return sizeof(T) == 4 ? 64 : 32; }  // 8 KB per stage (32 rows: slower, 128: later first stage)
 template <typename T>
 constexpr size_t fold_smem() { return (size_t)FOLD_NS * fold_rows<T>() * FD * sizeof(T); }
 
