@@ -105,6 +105,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
     __shared__ const float *rowsA[TC_M];
     __shared__ const float *rowsB[TC_N];
     __shared__ int rcls[TC_M];  // batch-local classified index of each tile row, -1: none
+    __shared__ float cn2t[TC_N];  // ||c||^2 of the tile's snapshot columns (gathered once)
     __shared__ __align__(8) uint64_t bar_stage[TC_STAGES];
     __shared__ __align__(8) uint64_t bar_full[TC_STAGES];
     __shared__ __align__(8) uint64_t bar_done;
@@ -114,6 +115,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
     for (int r = tid; r < TC_M; r += TC_THREADS) {
         const int a = row_cls(ta + r);
         rcls[r] = a;
+        cn2t[r] = tb + r < nB ? cn2[snap[tb + r]] : 0.f;
         if (!TMA) {
             const int b = tb + r;
             rowsA[r] = a >= 0 ? (const float *)frow[a0 + a] : nullptr;
@@ -346,7 +348,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
 #pragma unroll
         for (int j = 0; j < 4; j++)
             if (c + j < ncol) {
-                const float c2 = cn2[snap[tb + c + j]];
+                const float c2 = cn2t[c + j];
                 const float v = fa2 + c2 - 2.f * d4[j];
                 o[j] = v;
                 if (res_col || rowmin_g) {
@@ -358,7 +360,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
         if (res_col || rowmin_g) atomicMin(&rowmin[rr], __float_as_int(fmaxf(mn, 0.f)));
     }
     if (snorm && ta == 0 && rank == 0)
-        for (int c = tid; c < ncol; c += TC_THREADS) snorm[tb + c] = sqrtf(cn2[snap[tb + c]]) * 1.00001f;
+        for (int c = tid; c < ncol; c += TC_THREADS) snorm[tb + c] = sqrtf(cn2t[c]) * 1.00001f;
     if (rowmin_g) {
         // several column tiles: per-row minimum across CTAs (k_res_from_min flags the residuals)
         __syncthreads();
