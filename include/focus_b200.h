@@ -49,6 +49,8 @@ typedef enum {
     FX_E_UNKNOWN_CLASS = 51,         /* UnknownClass          errors.py:70-71 */
     FX_E_NON_MONOTONE_SCHEDULE = 52, /* NonMonotoneSchedule   errors.py:74-75 */
     FX_E_MISSING_OBJECT = 60,        /* KeyError: objects[rep] absent (query.py:58) */
+    FX_E_NEED_LABELS = 70,           /* not an error: fx_query needs GT labels of some
+                                        representatives first (fx_session_needed) */
     FX_E_CUDA = 90,                  /* CUDA runtime / launch failure */
     FX_E_OOM = 91,                   /* device allocation failed */
     FX_E_INTERNAL = 99
@@ -124,6 +126,12 @@ int fx_fc_topk(int32_t device, int64_t n, int32_t dim, int32_t vocab, int32_t k,
 int fx_fc_topk_device(int32_t device, void *cuda_stream, int64_t n, int32_t dim, int32_t vocab, int32_t k,
                       const float *d_feats, const float *d_W, const float *d_bias, int32_t *d_topk, float *d_conf,
                       uint8_t *d_flag);
+
+/* pixel_diff (ingest.py:37-47) of every object against its predecessor in
+ * a sequence, without an engine: out_is_dup[0] = 0, out_is_dup[i] =
+ * pixel_diff(obj[i-1], obj[i], eps).  sigs[n * sig_dim] float64. */
+int fx_dup_flags(int32_t device, int64_t n, int32_t sig_dim, const int64_t *frame_ids, const double *sigs,
+                 double eps, uint8_t *out_is_dup);
 
 /* pixel_diff over a chunk (ingest.py:37-47), continuing from the previous
  * chunk's last object; does not consume the chunk.  out_is_dup[n]. */
@@ -251,13 +259,33 @@ typedef struct fx_session fx_session;
  * each cluster's representative (classifiers.py:161-165), or
  *   -2 = representative object has no true class (MissingTrueClass on touch),
  *   -3 = representative object missing from `objects` (KeyError on touch),
- *   -4 = cluster has no representative.
+ *   -4 = cluster has no representative,
+ *   -5 = not known yet: fx_query returns FX_E_NEED_LABELS when a candidate
+ *        has it (labels are produced lazily, like _verify, query.py:53-60).
+ *   rep_label == NULL: every label starts at -5.
  * rep_key[C]: memo key per cluster (equal keys share one GT inference, the
  *   session memo is keyed by representative object id, query.py:53-60);
- *   keys are dense 0..n_keys-1.
- * other_map[V] (may be NULL): 1 if ingest_profile.map_class(c) == OTHER. */
+ *   keys are dense 0..n_keys-1.  rep_key == NULL: key = cluster index
+ *   (representatives of distinct clusters are distinct objects).
+ * other_map[V] (may be NULL): 1 if ingest_profile.map_class(c) == OTHER;
+ *   labels outside [0, V) map to OTHER (classifiers.py:103-107). */
 int fx_session_create(fx_index *ix, const int32_t *rep_label, const int32_t *rep_key,
                       int64_t n_keys, const uint8_t *other_map, fx_session **out);
+/* Set labels of n clusters (cluster indexes, host arrays). */
+int fx_session_set_labels(fx_session *ss, int64_t n, const int32_t *cluster_idx, const int32_t *labels);
+/* Labels from a dense host table indexed by object id - oid_base
+ * (labels[i] = GT label of object oid_base + i, -2 = unlabeled); gathered
+ * for every representative on the device (reps outside the table -> -3). */
+int fx_session_gather_labels(fx_session *ss, const int32_t *labels, int64_t oid_base, int64_t n);
+/* After FX_E_NEED_LABELS: *n = number of candidate clusters whose label is
+ * unknown; cluster_idx (may be NULL) receives them. */
+int fx_session_needed(fx_session *ss, int32_t *cluster_idx, int64_t *n);
+/* Representative object id per cluster index (-1 = none), host array [C]. */
+int fx_index_reps(fx_index *ix, int64_t *reps);
+/* A seen set for one batched_query (query.py:139-154): each generator owns
+ * one, so interleaved generators do not share state. */
+int fx_session_seen_open(fx_session *ss, int32_t *seen_id);
+int fx_session_seen_close(fx_session *ss, int32_t seen_id);
 int fx_session_destroy(fx_session *ss);
 
 typedef struct {
@@ -273,8 +301,9 @@ typedef struct {
  *   mode 0: plain execute_query(class_enc, k_x, range);
  *   mode 1: keep_label path of query_other (OTHER postings, k_x = K,
  *           keep clusters whose GT label == keep_label);
- *   batch_step: 0 = independent query; 1 = first step of batched_query
- *           (resets the seen set); 2 = later step (skip seen clusters).
+ *   batch_step: 0 = independent query; s > 0 = a step of the batched
+ *           query whose seen set is fx_session_seen_open's id s - 1 (skip
+ *           clusters in it, then add the candidates to it).
  * has_range/t0/t1: inclusive frame range filter.  Results stay in the
  * session until fx_query_fetch. */
 int fx_query(fx_session *ss, int32_t class_enc, int32_t k_x, int32_t mode, int32_t keep_label,

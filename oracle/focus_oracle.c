@@ -56,6 +56,41 @@ static double pw_sum_block(const double *a, int64_t n) {
     }
 }
 
+/* pw_sum_block over x[i] = (c[i] - f[i])^2 without materialising x: the same
+ * operations in the same order (bit-identical), fused for the distance rows. */
+static double pw_sqdiff_block(const double *c, const double *f, int64_t n) {
+    if (n < 8) {
+        double res = 0.0;
+        for (int64_t i = 0; i < n; i++) {
+            const double x = c[i] - f[i];
+            res += x * x;
+        }
+        return res;
+    } else if (n <= 128) {
+        double r[8];
+        int64_t i;
+        for (int j = 0; j < 8; j++) {
+            const double x = c[j] - f[j];
+            r[j] = x * x;
+        }
+        for (i = 8; i < n - (n % 8); i += 8)
+            for (int j = 0; j < 8; j++) {
+                const double x = c[i + j] - f[i + j];
+                r[j] += x * x;
+            }
+        double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        for (; i < n; i++) {
+            const double x = c[i] - f[i];
+            res += x * x;
+        }
+        return res;
+    } else {
+        int64_t n2 = n / 2;
+        n2 -= n2 % 8;
+        return pw_sqdiff_block(c, f, n2) + pw_sqdiff_block(c + n2, f + n2, n - n2);
+    }
+}
+
 /* add.reduce of a contiguous float64 row: identity 0.0 plus one pairwise sum
  * over the whole row (verified against numpy 2.3.5 up to n = 70001 in
  * tests/test_oracle.py; the ufunc hands a contiguous unbuffered row over in
@@ -278,6 +313,7 @@ typedef struct {
     int64_t *live; /* ascending cluster ids */
     int64_t nlive, caplive;
     int64_t distance_computations;
+    int64_t margin_t, margin_tie; /* objects within MARGIN_REL of T / of a tie */
     double *dbuf, *diff, *tdiff;
     int64_t dbuf_cap;
     int nthreads;
@@ -323,12 +359,7 @@ ORC_API void orc_engine_free(orc_engine *e) {
 
 /* ||c - f||_2 exactly as np.linalg.norm(centroids - feature, axis=1). */
 static double orc_dist(orc_engine *e, const double *c, const double *f) {
-    int d = e->dim;
-    for (int k = 0; k < d; k++) {
-        double x = c[k] - f[k];
-        e->diff[k] = x * x;
-    }
-    return sqrt(orc_pairwise_sum(e->diff, d));
+    return sqrt(0.0 + pw_sqdiff_block(c, f, e->dim));
 }
 
 /* Cluster.seal (clustering.py:71-83): rep = featured member nearest the
@@ -386,15 +417,8 @@ ORC_API int64_t orc_insert(orc_engine *e, int64_t row, int64_t oid, int64_t fid,
          * (bit-identical to the serial loop; each distance is one pairwise sum) */
         if (e->nthreads > 1 && e->nlive * (int64_t)e->dim >= 65536) {
 #pragma omp parallel for num_threads(e->nthreads) schedule(static)
-            for (int64_t j = 0; j < e->nlive; j++) {
-                double *tmp = e->tdiff + (size_t)omp_get_thread_num() * e->dim;
-                const double *c = e->cl[e->live[j]].centroid;
-                for (int k = 0; k < e->dim; k++) {
-                    double x = c[k] - f[k];
-                    tmp[k] = x * x;
-                }
-                e->dbuf[j] = sqrt(orc_pairwise_sum(tmp, e->dim));
-            }
+            for (int64_t j = 0; j < e->nlive; j++)
+                e->dbuf[j] = sqrt(0.0 + pw_sqdiff_block(e->cl[e->live[j]].centroid, f, e->dim));
         } else {
             for (int64_t j = 0; j < e->nlive; j++)
                 e->dbuf[j] = orc_dist(e, e->cl[e->live[j]].centroid, f);
@@ -403,6 +427,16 @@ ORC_API int64_t orc_insert(orc_engine *e, int64_t row, int64_t oid, int64_t fid,
         int64_t idx = 0;
         for (int64_t j = 1; j < e->nlive; j++)
             if (e->dbuf[j] < e->dbuf[idx]) idx = j; /* np.argmin: first minimum */
+        /* north-star margin accounting (not a reference quantity): the nearest
+         * distance within 1e-5 relative of T, or of the runner-up (a tie) */
+        {
+            const double d1 = e->dbuf[idx];
+            double d2 = INFINITY;
+            for (int64_t j = 0; j < e->nlive; j++)
+                if (j != idx && e->dbuf[j] < d2) d2 = e->dbuf[j];
+            if (fabs(d1 - e->t) <= 1e-5 * e->t) e->margin_t++;
+            if (d2 - d1 <= 1e-5 * d1) e->margin_tie++;
+        }
         if (e->dbuf[idx] <= e->t) {
             target = e->live[idx];
             distance = e->dbuf[idx];
@@ -470,6 +504,11 @@ ORC_API void orc_finalize(orc_engine *e) {
 ORC_API int64_t orc_n_clusters(orc_engine *e) { return e->ncl; }
 ORC_API int64_t orc_n_live(orc_engine *e) { return e->nlive; }
 ORC_API int64_t orc_distance_computations(orc_engine *e) { return e->distance_computations; }
+/* [objects whose nearest distance is within 1e-5 relative of T, ... of a tie] */
+ORC_API void orc_margin_counts(orc_engine *e, int64_t out[2]) {
+    out[0] = e->margin_t;
+    out[1] = e->margin_tie;
+}
 
 /* sizes: [n_members, n_featured, rep, n_classes] */
 ORC_API void orc_cluster_info(orc_engine *e, int64_t cid, int64_t out[4]) {

@@ -75,6 +75,8 @@ def lib():
         for name in ("orc_n_clusters", "orc_distance_computations", "orc_n_live"):
             getattr(L, name).restype = ctypes.c_int64
             getattr(L, name).argtypes = [ctypes.c_void_p]
+        L.orc_margin_counts.restype = None
+        L.orc_margin_counts.argtypes = [ctypes.c_void_p, _i64p]
         L.orc_cluster_info.restype = None
         L.orc_cluster_info.argtypes = [ctypes.c_void_p, ctypes.c_int64, _i64p]
         L.orc_cluster_export.restype = None
@@ -237,6 +239,8 @@ class OracleIngest:
     distance_computations: int
     objects_seen: int
     objects_classified: int
+    margin_t: int = 0    # nearest distance within 1e-5 relative of T (north-star margin accounting)
+    margin_tie: int = 0  # runner-up within 1e-5 relative of the nearest (a tie)
 
 
 def ingest(oids, fids, sigs, feats, topk, k: int, t: float, m: int, pixel_eps: float = 0.01,
@@ -277,10 +281,12 @@ def ingest(oids, fids, sigs, feats, topk, k: int, t: float, m: int, pixel_eps: f
                                           dict(zip(cl.tolist(), rk.tolist())),
                                           None if rep < 0 else rep, ins.tolist()))
         dc = L.orc_distance_computations(h)
+        mg = np.zeros(2, dtype=np.int64)
+        L.orc_margin_counts(h, _p(mg, _i64p))
     finally:
         L.orc_engine_free(h)
     classified = int(n - dup[1:].sum()) if n else 0
-    return OracleIngest(dup.astype(bool), tk, out, clusters, dc, n, classified)
+    return OracleIngest(dup.astype(bool), tk, out, clusters, dc, n, classified, int(mg[0]), int(mg[1]))
 
 
 # -- index (index.py:60-85) --------------------------------------------------

@@ -23,6 +23,7 @@ c_f64p = ctypes.POINTER(ctypes.c_double)
 vp = ctypes.c_void_p
 
 FX_F32, FX_F64 = 0, 1
+FX_E_NEED_LABELS = 70
 FX_FEATS_COMPACT = 1
 
 
@@ -70,6 +71,8 @@ _SIGS = {
                                   vp, c_i32p, vp, c_u8p]),
     "fx_fc_topk_device": (ctypes.c_int, [ctypes.c_int32, vp, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                                          ctypes.c_int32, vp, vp, vp, vp, vp, vp]),
+    "fx_dup_flags": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int64, ctypes.c_int32, c_i64p, c_f64p, ctypes.c_double,
+                                    c_u8p]),
     "fx_stream_dup_flags": (ctypes.c_int, [vp, ctypes.c_int64, c_i64p, c_f64p, c_u8p]),
     "fx_ingest": (ctypes.c_int, [vp, ctypes.c_int64, c_i64p, c_i64p, c_f64p, vp, c_i32p, c_i32p, ctypes.c_int32]),
     "fx_ingest_device": (ctypes.c_int, [vp, ctypes.c_int64, vp, vp, vp, vp, vp, vp, ctypes.c_int32]),
@@ -105,6 +108,12 @@ _SIGS = {
     "fx_query_fetch": (ctypes.c_int, [vp, c_i64p, c_i64p]),
     "fx_query_fetch_device": (ctypes.c_int, [vp, vp, vp]),
     "fx_session_reset": (ctypes.c_int, [vp]),
+    "fx_session_set_labels": (ctypes.c_int, [vp, ctypes.c_int64, c_i32p, c_i32p]),
+    "fx_session_gather_labels": (ctypes.c_int, [vp, c_i32p, ctypes.c_int64, ctypes.c_int64]),
+    "fx_session_needed": (ctypes.c_int, [vp, c_i32p, c_i64p]),
+    "fx_session_seen_open": (ctypes.c_int, [vp, c_i32p]),
+    "fx_session_seen_close": (ctypes.c_int, [vp, ctypes.c_int32]),
+    "fx_index_reps": (ctypes.c_int, [vp, c_i64p]),
     "fx_session_gt_total": (ctypes.c_int64, [vp]),
 }
 

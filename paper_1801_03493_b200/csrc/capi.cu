@@ -10,6 +10,8 @@
 
 #include "fx_handles.cuh"
 
+#include <mutex>
+
 namespace fx {
 const char *last_error();
 int64_t launches();
@@ -45,6 +47,16 @@ void build_index_from_csr(fx_index *ix, const int64_t *d_off, const int32_t *d_c
 void run_query(fx_session *ss, int class_enc, int k_x, int mode, int keep_label, int batch_step, int has_range,
                int64_t t0, int64_t t1, fx_query_result *res);
 void session_alloc_bits(fx_session *ss);
+void launch_dup_flags_raw(int64_t n, int S, const int64_t *d_fid, const double *d_sig, double eps, uint8_t *d_out,
+                          cudaStream_t st);
+void session_gather_labels(fx_session *ss, const int32_t *labels, int64_t base, int64_t n);
+void session_set_labels(fx_session *ss, int64_t n, const int32_t *cidx, const int32_t *labels);
+int64_t index_lookup(fx_index *ix, int class_enc, int k_x, int64_t *out_ids, int64_t cap);
+
+__global__ void k_fill_i32(int64_t n, int32_t v, int32_t *__restrict__ out) {
+    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) out[i] = v;
+}
 
 // first classified object of the chunk: the one non-duplicate with no
 // classified object before it (excl = exclusive count of classified objects)
@@ -142,7 +154,9 @@ fx_stream::~fx_stream() {
     // stream-ordered frees have been queued on it
 }
 fx_index::~fx_index() {}  // stream destroyed by fx_index_destroy (see fx_stream)
-fx_session::~fx_session() {}
+fx_session::~fx_session() {
+    for (auto *b : seen_sets) delete b;
+}
 
 #define FX_GUARD(...)                                   \
     try {                                               \
@@ -393,6 +407,41 @@ int fx_fc_topk_device(int32_t device, void *cuda_stream, int64_t n, int32_t dim,
         launch_rowptrs(n, (int64_t)dim * 4, (const char *)d_feats, rows.p, st);
         launch_fc_head(n, 0, rows.p, nullptr, fn.p, dim, vocab, k, d_W, wn.p, d_bias, d_topk, d_conf, d_flag, nullptr,
                        st, d_feats);
+    })
+}
+
+// pixel_diff (ingest.py:37-47) over a sequence, no engine: a per-device
+// utility stream (the drop-in `pixel_diff` of one pair, and ingest_stream's
+// dup pass before the rows are marshalled)
+static cudaStream_t util_stream(int device) {
+    static std::mutex mu;
+    static cudaStream_t st[64] = {};
+    std::lock_guard<std::mutex> lk(mu);
+    const int d = device & 63;
+    if (!st[d]) FX_CUDA(cudaStreamCreateWithFlags(&st[d], cudaStreamNonBlocking));
+    return st[d];
+}
+
+int fx_dup_flags(int32_t device, int64_t n, int32_t sig_dim, const int64_t *frame_ids, const double *sigs, double eps,
+                 uint8_t *out) {
+    FX_GUARD({
+        if (n <= 0) return FX_OK;
+        if (!frame_ids || !out || sig_dim < 0 || (sig_dim > 0 && !sigs)) throw Error{FX_E_USAGE, "bad argument"};
+        set_dev(device);
+        init_pool(device);
+        cudaStream_t st = util_stream(device);
+        StreamGuard sg_(st);
+        DevBuf<int64_t> f;
+        DevBuf<double> g;
+        DevBuf<uint8_t> o;
+        f.reserve(n);
+        g.reserve((size_t)n * std::max(sig_dim, 1));
+        o.reserve(n);
+        h2d(f.p, frame_ids, n, st);
+        if (sig_dim) h2d(g.p, sigs, n * sig_dim, st);
+        launch_dup_flags_raw(n, sig_dim, f.p, g.p, eps, o.p, st);
+        d2h(out, o.p, n, st);
+        FX_CUDA(cudaStreamSynchronize(st));
     })
 }
 
@@ -904,27 +953,24 @@ int fx_index_destroy(fx_index *ix) {
 int fx_lookup(fx_index *ix, int32_t class_enc, int32_t k_x, int64_t *out_ids, int64_t cap, int64_t *out_n) {
     FX_GUARD({
         if (!ix || !out_n) throw Error{FX_E_USAGE, "null argument"};
-        const int kx = k_x == -1 ? (int)ix->K : k_x;  // -1 = None -> K (index.py:77-79)
-        if (kx < 1 || kx > ix->K) throw Error{FX_E_KX_TOO_LARGE, "k_x outside [1, K]"};
+        if (k_x < 1 || k_x > ix->K) throw Error{FX_E_KX_TOO_LARGE, "k_x outside [1, K]"};
         *out_n = 0;
         if (class_enc < 0 || class_enc > ix->V) return FX_OK;  // postings.get(c, []) -> []
         set_dev(ix->dev);
         StreamGuard sg_(ix->st);
-        const int64_t a = ix->h_post_off[class_enc], b = ix->h_post_off[class_enc + 1];
-        if (b == a) return FX_OK;
-        std::vector<int32_t> cidx(b - a), rk(b - a);
-        std::vector<int64_t> ids(ix->C);
-        d2h(cidx.data(), ix->post_cidx.p + a, b - a, ix->st);
-        d2h(rk.data(), ix->post_rank.p + a, b - a, ix->st);
-        d2h(ids.data(), ix->cluster_ids.p, ix->C, ix->st);
-        FX_CUDA(cudaStreamSynchronize(ix->st));
-        int64_t m = 0;
-        for (int64_t i = 0; i < b - a; i++) {
-            if (rk[i] > kx) continue;
-            if (out_ids && m < cap) out_ids[m] = ids[cidx[i]];
-            m++;
+        *out_n = index_lookup(ix, class_enc, k_x, out_ids, out_ids ? cap : 0);
+    })
+}
+
+int fx_index_reps(fx_index *ix, int64_t *reps) {
+    FX_GUARD({
+        if (!ix || !reps) throw Error{FX_E_USAGE, "null argument"};
+        set_dev(ix->dev);
+        StreamGuard sg_(ix->st);
+        if (ix->C) {
+            d2h(reps, ix->reps.p, ix->C, ix->st);
+            FX_CUDA(cudaStreamSynchronize(ix->st));
         }
-        *out_n = m;
     })
 }
 
@@ -937,16 +983,18 @@ int fx_session_create(fx_index *ix, const int32_t *rep_label, const int32_t *rep
         fx_session *ss = new fx_session();
         try {
             ss->ix = ix;
-            ss->n_keys = n_keys;
             const int64_t C = ix->C;
+            ss->keyed = rep_key != nullptr;
+            ss->n_keys = rep_key ? n_keys : C;
             ss->rep_label.reserve(C + 1);
-            ss->rep_key.reserve(C + 1);
-            h2d(ss->rep_label.p, rep_label, C, ix->st);
-            h2d(ss->rep_key.p, rep_key, C, ix->st);
-            ss->memo.reserve((n_keys + 4) & ~3LL);
-            FX_CUDA(cudaMemsetAsync(ss->memo.p, 0, (n_keys + 4) & ~3LL, ix->st));
-            ss->seen.reserve(C + 1);
-            FX_CUDA(cudaMemsetAsync(ss->seen.p, 0, C + 1, ix->st));
+            if (rep_label) h2d(ss->rep_label.p, rep_label, C, ix->st);
+            else if (C) k_fill_i32<<<(unsigned)cdiv(C, 256), 256, 0, ix->st>>>(C, -5, ss->rep_label.p);
+            if (rep_key) {
+                ss->rep_key.reserve(C + 1);
+                h2d(ss->rep_key.p, rep_key, C, ix->st);
+            }
+            ss->memo.reserve((ss->n_keys + 4) & ~3LL);
+            FX_CUDA(cudaMemsetAsync(ss->memo.p, 0, (ss->n_keys + 4) & ~3LL, ix->st));
             ss->other_map.reserve(ix->V + 1);
             ss->has_other = other_map != nullptr;
             if (other_map) h2d(ss->other_map.p, other_map, ix->V, ix->st);
@@ -977,7 +1025,7 @@ int fx_query(fx_session *ss, int32_t class_enc, int32_t k_x, int32_t mode, int32
         if (!ss || !res) throw Error{FX_E_USAGE, "null argument"};
         fx_index *ix = ss->ix;
         if (class_enc < 0 || class_enc > ix->V) throw Error{FX_E_UNKNOWN_CLASS, "unknown class"};
-        int kx = k_x == -1 ? (int)ix->K : k_x;
+        int kx = k_x;
         if (mode == 1) kx = (int)ix->K;
         if (kx < 1 || kx > ix->K) throw Error{FX_E_KX_TOO_LARGE, "k_x outside [1, K]"};
         set_dev(ix->dev);
@@ -1018,9 +1066,73 @@ int fx_session_reset(fx_session *ss) {
         StreamGuard sg_(ss->ix->st);
         cudaStream_t st = ss->ix->st;
         FX_CUDA(cudaMemsetAsync(ss->memo.p, 0, (ss->n_keys + 4) & ~3LL, st));
-        FX_CUDA(cudaMemsetAsync(ss->seen.p, 0, ss->ix->C + 1, st));
         FX_CUDA(cudaStreamSynchronize(st));
         ss->gt_total = 0;
+    })
+}
+
+int fx_session_set_labels(fx_session *ss, int64_t n, const int32_t *cluster_idx, const int32_t *labels) {
+    FX_GUARD({
+        if (!ss || (n > 0 && (!cluster_idx || !labels))) throw Error{FX_E_USAGE, "null argument"};
+        set_dev(ss->ix->dev);
+        StreamGuard sg_(ss->ix->st);
+        session_set_labels(ss, n, cluster_idx, labels);
+    })
+}
+
+int fx_session_gather_labels(fx_session *ss, const int32_t *labels, int64_t oid_base, int64_t n) {
+    FX_GUARD({
+        if (!ss || (n > 0 && !labels) || n < 0) throw Error{FX_E_USAGE, "bad argument"};
+        set_dev(ss->ix->dev);
+        StreamGuard sg_(ss->ix->st);
+        session_gather_labels(ss, labels, oid_base, n);
+    })
+}
+
+int fx_session_needed(fx_session *ss, int32_t *cluster_idx, int64_t *n) {
+    FX_GUARD({
+        if (!ss || !n) throw Error{FX_E_USAGE, "null argument"};
+        *n = ss->n_need;
+        if (cluster_idx && ss->n_need) {
+            set_dev(ss->ix->dev);
+            StreamGuard sg_(ss->ix->st);
+            d2h(cluster_idx, ss->need.p, ss->n_need, ss->ix->st);
+            FX_CUDA(cudaStreamSynchronize(ss->ix->st));
+        }
+    })
+}
+
+int fx_session_seen_open(fx_session *ss, int32_t *seen_id) {
+    FX_GUARD({
+        if (!ss || !seen_id) throw Error{FX_E_USAGE, "null argument"};
+        set_dev(ss->ix->dev);
+        StreamGuard sg_(ss->ix->st);
+        auto *b = new DevBuf<uint8_t>();
+        try {
+            b->reserve(ss->ix->C + 1);
+            FX_CUDA(cudaMemsetAsync(b->p, 0, ss->ix->C + 1, ss->ix->st));
+            FX_CUDA(cudaStreamSynchronize(ss->ix->st));
+        } catch (...) {
+            delete b;
+            throw;
+        }
+        size_t i = 0;
+        while (i < ss->seen_sets.size() && ss->seen_sets[i]) i++;
+        if (i == ss->seen_sets.size()) ss->seen_sets.push_back(b);
+        else ss->seen_sets[i] = b;
+        *seen_id = (int32_t)i;
+    })
+}
+
+int fx_session_seen_close(fx_session *ss, int32_t seen_id) {
+    FX_GUARD({
+        if (!ss) throw Error{FX_E_USAGE, "null session"};
+        if (seen_id < 0 || seen_id >= (int32_t)ss->seen_sets.size() || !ss->seen_sets[seen_id])
+            throw Error{FX_E_USAGE, "seen set not open"};
+        set_dev(ss->ix->dev);
+        StreamGuard sg_(ss->ix->st);
+        delete ss->seen_sets[seen_id];
+        ss->seen_sets[seen_id] = nullptr;
     })
 }
 

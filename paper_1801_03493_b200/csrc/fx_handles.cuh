@@ -159,13 +159,16 @@ struct fx_session {
     int64_t n_keys = 0;
     int64_t gt_total = 0;
     bool has_other = false;
+    bool keyed = false;  // rep_key given (else key = cluster index)
     fx::DevBuf<int32_t> rep_label, rep_key;
-    fx::DevBuf<uint8_t> memo, other_map, seen;
+    fx::DevBuf<uint8_t> memo, other_map;
     fx::DevBuf<uint32_t> fbits, obits;
     fx::DevBuf<int64_t> wprefix_f, wprefix_o;
     fx::DevBuf<int64_t> out_f, out_o;
-    fx::DevBuf<int32_t> cand, matched;
+    fx::DevBuf<int32_t> cand, matched, need;
     fx::DevBuf<int64_t> qctr;
+    std::vector<fx::DevBuf<uint8_t> *> seen_sets;  // batched queries (fx_session_seen_open)
+    int64_t n_need = 0;
     fx::DevBuf<int64_t> h_pinned_dummy;
     int64_t nf = 0, no = 0;
     ~fx_session();

@@ -80,7 +80,9 @@ __global__ void __launch_bounds__(512) k_classes_small(int64_t C, E src, int32_t
             if (i < len) {
                 int cl, r;
                 src.get(c, b0 + i, cl, r);
-                k = ((uint32_t)cl << 8) | (uint32_t)(r & 0xff);
+                // cl < 0: a classifier emitted fewer than K classes (the
+                // reference merges only the classes emitted, clustering.py:65-69)
+                if (cl >= 0) k = ((uint32_t)cl << 8) | (uint32_t)(r & 0xff);
             }
             key[i] = k;
         }
@@ -109,7 +111,7 @@ __global__ void __launch_bounds__(512) k_classes_small(int64_t C, E src, int32_t
             int base = 0;
             for (int i0 = 0; i0 < len; i0 += 32) {
                 int i = i0 + threadIdx.x;
-                bool head = i < len && (i == 0 || (key[i] >> 8) != (key[i - 1] >> 8));
+                bool head = i < len && key[i] != 0xffffffffu && (i == 0 || (key[i] >> 8) != (key[i - 1] >> 8));
                 unsigned m = __ballot_sync(0xffffffffu, head);
                 if (head) {
                     int p = base + __popc(m & ((1u << threadIdx.x) - 1u));
@@ -141,7 +143,7 @@ __global__ void __launch_bounds__(256) k_classes_big_acc(int64_t nbig, const int
     for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) {
         int cl, r;
         src.get(c, e, cl, r);
-        atomicMin(&tab[cl], (uint32_t)r);
+        if (cl >= 0) atomicMin(&tab[cl], (uint32_t)r);
     }
     __syncthreads();
     uint32_t *g = table + bi * (int64_t)V1;

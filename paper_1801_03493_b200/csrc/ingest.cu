@@ -2665,6 +2665,12 @@ void launch_dup_flags(fx_stream *s, int64_t n, const int64_t *d_fid, const doubl
     FX_LAUNCHED();
 }
 
+void launch_dup_flags_raw(int64_t n, int S, const int64_t *d_fid, const double *d_sig, double eps, uint8_t *d_out,
+                          cudaStream_t st) {
+    k_dup_flags<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(n, S, d_fid, d_sig, 0, 0, nullptr, eps, d_out);
+    FX_LAUNCHED();
+}
+
 void launch_compact(fx_stream *s, int64_t n, int64_t obj_base, int64_t cls_base, const uint8_t *d_dup,
                     const int64_t *d_excl, const char *feat_base, int compact) {
     const int64_t row_bytes = (int64_t)s->cfg.dim * s->esize;

@@ -151,10 +151,20 @@ def pixel_diff(prev, cur, eps: float) -> bool:
         raise SignatureLengthMismatch(f"{a.shape[0]} vs {b.shape[0]}")
     if cur.frame_id - prev.frame_id > 1:
         return False
-    s = Stream(dim=1, sig_dim=a.shape[0], vocab=1, k=1, t=0.0, m=1, pixel_eps=eps, batch=64)
-    flags = s.dup_flags(np.array([prev.frame_id, cur.frame_id], np.int64),
-                        np.ascontiguousarray(np.stack([a, b])))
-    return bool(flags[1])
+    return bool(dup_flags(np.array([prev.frame_id, cur.frame_id], np.int64), np.stack([a, b]), eps)[1])
+
+
+def dup_flags(fids: np.ndarray, sigs: np.ndarray, eps: float, device: int | None = None) -> np.ndarray:
+    """K0 over a whole sequence: is_dup[i] = pixel_diff(obj[i-1], obj[i], eps)."""
+    fids = np.ascontiguousarray(fids, np.int64)
+    n = fids.size
+    S = sigs.shape[1] if sigs.ndim == 2 else 0
+    sigs = np.ascontiguousarray(sigs, np.float64).reshape(n, S)
+    out = np.zeros(n, np.uint8)
+    if n:
+        _lib.check(_lib.load().fx_dup_flags(_lib.device() if device is None else device, n, S, _lib.p64(fids),
+                                            _lib.pf64(sigs), float(eps), _lib.pu8(out)))
+    return out.astype(bool)
 
 
 def _f32_exact(x: np.ndarray) -> bool:
@@ -220,8 +230,7 @@ def ingest_stream(header, stream, cfg: Config, profiles, pixel_eps: float = DEFA
     sigs = np.zeros((n, S), np.float64)
     for i, o in enumerate(objs):
         sigs[i, :slen[i]] = o.pixel_signature
-    st = Stream(1, S, 1, 1, 0.0, 1, pixel_eps, _lib.FX_F32, None, 64)  # K0 only
-    dup = st.dup_flags(fids, sigs) if n else np.zeros(0, bool)
+    dup = dup_flags(fids, sigs, pixel_eps)
     keep = np.flatnonzero(~dup)
     fc_head = classify_fn if isinstance(classify_fn, classifiers.FCHead) else None
     if fc_head is not None:
@@ -229,7 +238,9 @@ def ingest_stream(header, stream, cfg: Config, profiles, pixel_eps: float = DEFA
         topk, tcls = None, None
         rows = [classifiers.extract_feature(profile, objs[i], seed) for i in keep.tolist()]
     elif classify_fn is not None:
-        topk = np.zeros((n, K), np.int32)
+        # -1 = no class at that rank: a classifier may emit fewer than K
+        # classes and the reference merges only those (clustering.py:65-69)
+        topk = np.full((n, K), -1, np.int32)
         rows = []
         for i in keep.tolist():
             rc = classify_fn(profile, objs[i], seed).top(K)
@@ -247,7 +258,6 @@ def ingest_stream(header, stream, cfg: Config, profiles, pixel_eps: float = DEFA
     F = np.array(rows, dtype=np.float64).reshape(len(rows), D) if rows else np.zeros((0, D))
     if all(np.asarray(r).dtype == np.float32 for r in rows) or _f32_exact(F):
         F = F.astype(np.float32)
-    del st
     if fc_head is not None:
         F = F.astype(np.float32)
     idx, report, _ = ingest_arrays(oids, fids, sigs, F, cfg, profile, vocab=V, seed=seed, pixel_eps=pixel_eps,

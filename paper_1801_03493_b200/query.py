@@ -17,7 +17,7 @@ import numpy as np
 from . import _lib
 from .classifiers import GROUND_TRUTH, SPECIALIZED
 from .core import OTHER_CLASS, encode_class
-from .errors import MissingTrueClass, NonMonotoneSchedule, UnknownClass
+from .errors import KxTooLarge, MissingTrueClass, NonMonotoneSchedule, UnknownClass
 
 
 @dataclass(frozen=True)
@@ -41,7 +41,16 @@ _NO_LABEL, _NO_OBJECT, _NO_REP = -2, -3, -4
 
 
 class QuerySession:
-    """Read-only device index + the verification oracle for one session."""
+    """Read-only device index + the verification oracle for one session.
+
+    Construction is O(1) in Python: GT labels of representatives are produced
+    lazily, like the reference's ``_verify`` (query.py:53-60) -- the device
+    query lists the candidates whose label it does not know yet, the session
+    reads just those from ``objects`` and re-issues the query (nothing is
+    applied before that).  ``labels`` (optional, not a reference argument): a
+    dense array of GT labels indexed by object id (-2 = unlabeled), gathered
+    for every representative on the device in one pass.
+    """
 
     def __init__(self, idx, gt_profile, objects, ingest_profile=None, labels=None):
         if gt_profile.kind != GROUND_TRUTH:
@@ -50,43 +59,65 @@ class QuerySession:
         self.gt_profile = gt_profile
         self.objects = objects
         self.ingest_profile = ingest_profile
+        self._labels = labels
         self.L = _lib.load()
-        ex = idx.device.export(centroids=False)
-        reps = ex["reps"]
-        C = reps.size
-        label = np.empty(C, np.int32)
-        key = np.empty(C, np.int32)
-        keys = {}
-        for i, r in enumerate(reps.tolist()):
-            if r < 0:
-                label[i] = _NO_REP
-                key[i] = keys.setdefault(("none", i), len(keys))
-                continue
-            key[i] = keys.setdefault(r, len(keys))
-            if labels is not None:
-                label[i] = labels[r]
-                continue
-            obj = objects.get(r) if hasattr(objects, "get") else None
-            if obj is None and r not in objects:
-                label[i] = _NO_OBJECT
-            else:
-                obj = objects[r]
-                label[i] = _NO_LABEL if obj.true_class is None else obj.true_class
-        self._rep_label = label
+        if idx.device is None:  # e.g. index.load(): post it on the device once (index.py:135-204)
+            from .index import build
+            idx.device = build(list(idx.clusters.values()), idx.header).device
+        dev = idx.device
+        C = int(dev.sizes.n_clusters)
+        reps = np.empty(C, np.int64)
+        if C:
+            _lib.check(self.L.fx_index_reps(dev.handle, _lib.p64(reps)))
+        self._reps = reps
+        # memo key = representative object id (query.py:53-60); representatives
+        # of distinct clusters are distinct objects unless the index was built
+        # by hand, in which case equal representatives share one key
+        key, n_keys = None, C
+        have = reps[reps >= 0]
+        if np.unique(have).size != have.size:
+            _, inv = np.unique(np.where(reps >= 0, reps, -1 - np.arange(C)), return_inverse=True)
+            key, n_keys = inv.astype(np.int32), int(inv.max()) + 1 if C else 0
         other = None
         V = idx.header.vocab
         if ingest_profile is not None and ingest_profile.kind == SPECIALIZED:
-            cs = set(ingest_profile.class_set)
-            other = np.array([0 if c in cs else 1 for c in range(V)], np.uint8)
+            other = np.ones(V, np.uint8)
+            cs = np.array([c for c in ingest_profile.class_set if 0 <= c < V], np.int64)
+            other[cs] = 0
         h = _lib.vp()
-        _lib.check(self.L.fx_session_create(idx.device.handle, _lib.p32(label), _lib.p32(key), len(keys),
+        _lib.check(self.L.fx_session_create(dev.handle, None, None if key is None else _lib.p32(key), n_keys,
                                             _lib.pu8(other) if other is not None else None, ctypes.byref(h)))
         self.handle = h
+        if isinstance(labels, np.ndarray):
+            lab = np.ascontiguousarray(labels, np.int32)
+            _lib.check(self.L.fx_session_gather_labels(h, _lib.p32(lab), 0, lab.size))
 
     def __del__(self):
         h, self.handle = getattr(self, "handle", None), None
         if h is not None and _lib._lib is not None:
             _lib._lib.fx_session_destroy(h)
+
+    def _label_of(self, r: int) -> int:
+        """ground_truth_label(objects[r]) encoded (classifiers.py:161-165)."""
+        if r < 0:
+            return _NO_REP
+        src = self._labels if self._labels is not None else self.objects
+        if self._labels is not None:
+            lab = src.get(r, _NO_OBJECT) if hasattr(src, "get") else _NO_OBJECT
+            return _NO_LABEL if lab is None else int(lab)
+        try:
+            obj = src[r]
+        except (KeyError, IndexError, TypeError):
+            return _NO_OBJECT
+        return _NO_LABEL if obj.true_class is None else int(obj.true_class)
+
+    def _supply_labels(self) -> None:
+        n = ctypes.c_int64(0)
+        _lib.check(self.L.fx_session_needed(self.handle, None, ctypes.byref(n)))
+        cidx = np.empty(n.value, np.int32)
+        _lib.check(self.L.fx_session_needed(self.handle, _lib.p32(cidx), ctypes.byref(n)))
+        lab = np.fromiter((self._label_of(r) for r in self._reps[cidx].tolist()), np.int32, cidx.size)
+        _lib.check(self.L.fx_session_set_labels(self.handle, cidx.size, _lib.p32(cidx), _lib.p32(lab)))
 
     def gt_inferences_total(self) -> int:
         return int(self.L.fx_session_gt_total(self.handle))
@@ -105,15 +136,22 @@ class QuerySession:
         res = _lib.QueryResultC()
         has = time_range is not None
         t0, t1 = (int(time_range[0]), int(time_range[1])) if has else (0, 0)
-        kx = -1 if k_x is None else int(k_x)
-        st = self.L.fx_query(self.handle, enc, kx, mode, int(keep_label), batch_step, 1 if has else 0, t0, t1,
-                             ctypes.byref(res))
+        K = self.idx.header.k
+        kx = K if (k_x is None or mode == 1) else k_x
+        if not 1 <= kx <= K:  # index.lookup (index.py:77-80)
+            raise KxTooLarge(f"k_x={kx} outside [1, {K}]")
+        while True:
+            st = self.L.fx_query(self.handle, enc, int(kx), mode, int(keep_label), batch_step, 1 if has else 0,
+                                 t0, t1, ctypes.byref(res))
+            if st != _lib.FX_E_NEED_LABELS:
+                break
+            self._supply_labels()
         if st == 20:  # MissingTrueClass names the representative object
-            rep = self.idx.device.export(centroids=False)["reps"][res.error_cluster]
-            raise MissingTrueClass(f"object {int(rep)} has no true class")
+            rep = int(self._reps[res.error_cluster])
+            raise MissingTrueClass(f"object {rep} has no true class")
         if st == 60:
-            rep = self.idx.device.export(centroids=False)["reps"][res.error_cluster]
-            raise KeyError(int(rep))
+            rep = int(self._reps[res.error_cluster])
+            raise KeyError(None if rep < 0 else rep)
         _lib.check(st)
         return res
 
@@ -182,5 +220,11 @@ class QuerySession:
         if not sched or any(b <= a for a, b in zip(sched, sched[1:])):
             raise NonMonotoneSchedule(str(sched))
         self._check_class(req.class_id)
-        for i, kx in enumerate(sched):
-            yield self._run(req.class_id, kx, 0, 0, 1 if i == 0 else 2, req.time_range)
+        sid = ctypes.c_int32(0)
+        _lib.check(self.L.fx_session_seen_open(self.handle, ctypes.byref(sid)))
+        try:  # this generator's own seen set (query.py:149)
+            for kx in sched:
+                yield self._run(req.class_id, kx, 0, 0, sid.value + 1, req.time_range)
+        finally:
+            if getattr(self, "handle", None) is not None:
+                self.L.fx_session_seen_close(self.handle, sid.value)
