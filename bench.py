@@ -93,15 +93,19 @@ def _dist():
     return ws, rank, local
 
 
-def cpu_sample(n_sample: int, seed: int, threads: int):
+def cpu_sample(n_sample: int, seed: int, threads: int, h: dict | None = None):
     """Time the CPU oracle port (reference algorithm restated in C + numpy) on
-    the first n_sample objects of the workload.  Returns objects/s."""
+    the first n_sample objects of the workload (`h`: the GPU arm's own stream
+    copied to the host; else the same generator on the CPU).  Returns objects/s."""
     from oracle import oracle as O
-    from paper_1801_03493_b200 import synth
-    st = synth.generate(n_sample, dim=WORKLOAD["dim"], vocab=WORKLOAD["vocab"],
-                        n_stream_classes=WORKLOAD["n_stream_classes"], seed=seed, device="cpu")
-    oids, fids = st.oids.numpy(), st.fids.numpy()
-    sigs, feats, tcls = st.sigs.numpy(), st.feats.numpy(), st.true_class.numpy()
+    if h is None:
+        from paper_1801_03493_b200 import synth
+        st = synth.generate(n_sample, dim=WORKLOAD["dim"], vocab=WORKLOAD["vocab"],
+                            n_stream_classes=WORKLOAD["n_stream_classes"], seed=seed, device="cpu")
+        h = dict(oids=st.oids.numpy(), fids=st.fids.numpy(), sigs=st.sigs.numpy(), feats=st.feats.numpy(),
+                 true_class=st.true_class.numpy())
+    oids, fids = h["oids"][:n_sample], h["fids"][:n_sample]
+    sigs, feats, tcls = h["sigs"][:n_sample], h["feats"][:n_sample], h["true_class"][:n_sample]
     prof = O.default_profiles(WORKLOAD["vocab"])["cheap"]
     O.set_threads(threads)
     k = WORKLOAD["k"]
@@ -116,17 +120,158 @@ def cpu_sample(n_sample: int, seed: int, threads: int):
     return n_sample / dt, dt, len(res.clusters)
 
 
+def _focusidx():
+    """The unmodified reference package from baseline/_ref (pip-installed
+    there once; it travels with the repo snapshot), or None."""
+    ref = os.path.join(REPO, "baseline", "_ref")
+    if os.path.isdir(os.path.join(ref, "focusidx")) and ref not in sys.path:
+        sys.path.append(ref)
+    try:
+        import focusidx  # noqa: F401
+        from focusidx import classifiers, clustering, core, index, ingest, query, streamio
+        return dict(classifiers=classifiers, clustering=clustering, core=core, index=index, ingest=ingest,
+                    query=query, streamio=streamio)
+    except Exception:
+        return None
+
+
+def reference_python_ingest(h: dict, n: int):
+    """The reference's own ingest_stream (focusidx, unmodified, 1 core) on the
+    first n objects of the host stream: the rank-model cheap profile with
+    feature noise 0 (the rows already are the cheap CNN's output, as on the
+    device), seed 0.  Returns (objects/s, seconds, clusters) or None."""
+    R = _focusidx()
+    if R is None:
+        return None
+    from dataclasses import replace
+    V = WORKLOAD["vocab"]
+    profs = R["classifiers"].make_default_profiles(V)
+    profs["cheap"] = replace(profs["cheap"], feature_noise_sigma=0.0)
+    DO = R["core"].DetectedObject
+    objs = [DO(int(h["oids"][i]), int(h["fids"][i]), 0.0, h["sigs"][i], h["feats"][i], int(h["true_class"][i]))
+            for i in range(n)]
+    cfg = R["core"].Config("cheap", k=WORKLOAD["k"], l_s=V, t=WORKLOAD["t"], m=WORKLOAD["m"])
+    hdr = R["streamio"].StreamHeader("cam0", 30.0, WORKLOAD["dim"], h["sigs"].shape[1], V)
+    t0 = time.perf_counter()
+    idx, rep = R["ingest"].ingest_stream(hdr, objs, cfg, profs, 0.01, 0)
+    dt = time.perf_counter() - t0
+    return n / dt, dt, rep.clusters_emitted
+
+
+def parity_and_c5(data, W, local, args):
+    """Rank 0, after the timed region: (1) the bench's own stream ingested on
+    the device at K = 4 vs the CPU oracle, bit for bit (oracle/scale_parity.py);
+    (2) C5 (BASELINE configs[4]): the same stream ingested at K = 8, every
+    class x k_x in {1,2,4,8} queried with a FRESH QuerySession, each result
+    compared with the oracle session; (3) the CPU query latency beside it (the
+    oracle port and, when baseline/_ref holds it, the reference's own
+    QuerySession)."""
+    import paper_1801_03493_b200 as fx
+    from oracle import oracle as O
+    from oracle import scale_parity as SP
+    n, V, t, m = W["n"], W["vocab"], W["t"], W["m"]
+    prof = fx.make_default_profiles(V)["cheap"]
+    t0 = time.perf_counter()
+    dev4 = SP.device_ingest(data, n, W["k"], t, m, V, prof, device=local)
+    h = SP.host_stream(data, n)
+    t1 = time.perf_counter()
+    ref8 = SP.oracle_ingest(h, 8, t, m, V, threads=os.cpu_count())
+    t2 = time.perf_counter()
+    par = SP.compare(dev4, SP.derive_k(ref8, W["k"]), V)
+    del dev4
+    par.update(oracle_s=round(t2 - t1, 2), oracle_threads=os.cpu_count(),
+               note="the timed workload's stream (all objects), device K=4 ingest vs the CPU oracle run at K=8 "
+                    "(K=4 expectations derived: top-K prefix, class ranks <= 4; clustering is K-independent)")
+    # C5: K = 8 index, fresh session per query, parity per query
+    s8 = fx.ingest.Stream(W["dim"], 16, V, 8, t, m, 0.01, fx._lib.FX_F32, local, 0)
+    s8.set_rank_model(prof, 0)
+    s8.ingest_device(n, data.oids.data_ptr(), data.fids.data_ptr(), data.sigs.data_ptr(), data.feats.data_ptr(),
+                     data.true_class.data_ptr())
+    dix8, _ = s8.finalize()
+    cfg8 = fx.Config("cheap", k=8, l_s=V, t=t, m=m)
+    tix = fx.TopKIndex(fx.IndexHeader("cam0", W["dim"], V, n, cfg8), device=dix8)
+    labels = h["true_class"].astype(np.int32)
+    gt = fx.make_default_profiles(V)["gt"]
+    osess = O.OracleSession(ref8.clusters, 8, V, dict(zip(h["oids"].tolist(), labels.tolist())))
+    classes = list(range(V)) if args.queries < 0 else list(range(min(V, args.queries)))
+    lat, bad, nq, frames = [], 0, 0, []
+    for kx in (1, 2, 4, 8):
+        for c in classes:
+            q0 = time.perf_counter()
+            sess = fx.QuerySession(tix, gt, None, labels=labels)
+            fr, ob, st = sess.query_arrays(fx.QueryRequest(c, k_x=kx))
+            lat.append((time.perf_counter() - q0) * 1e3)
+            del sess
+            osess.cache = {}
+            exp = osess.execute_query(c, kx)
+            nq += 1
+            frames.append(fr.size)
+            if (not np.array_equal(fr, np.asarray(exp["frame_ids"], np.int64))
+                    or not np.array_equal(ob, np.asarray(exp["object_ids"], np.int64))
+                    or st != (exp["gt_inferences"], exp["clusters_examined"], exp["clusters_matched"])):
+                bad += 1
+    lat = np.array(lat)
+    c5 = {"queries": nq, "k_x": [1, 2, 4, 8], "index_k": 8, "classes": len(classes),
+          "p50_ms": float(np.percentile(lat, 50)), "p99_ms": float(np.percentile(lat, 99)),
+          "mean_ms": float(lat.mean()), "max_frames": int(max(frames)), "mean_frames": float(np.mean(frames)),
+          "parity": {"queries_checked": nq, "mismatches": bad},
+          "timing": "host wall clock per query: fresh QuerySession (labels gathered on the device) + lookup + "
+                    "verify + expansion + ids copied to host"}
+    # CPU query latency beside it (fresh session per query)
+    cpu_q = {}
+    sub = classes if len(classes) <= 200 else list(range(0, V, max(1, V // 200)))
+    ql = []
+    for kx in (1, 2, 4, 8):
+        for c in sub:
+            q0 = time.perf_counter()
+            osess.cache = {}
+            osess.execute_query(c, kx)
+            ql.append((time.perf_counter() - q0) * 1e3)
+    cpu_q["oracle_port"] = {"p50_ms": float(np.percentile(ql, 50)), "p99_ms": float(np.percentile(ql, 99)),
+                            "mean_ms": float(np.mean(ql)), "queries": len(ql), "cores": 1}
+    R = _focusidx()
+    if R is not None:
+        Cl = R["clustering"].Cluster
+        rcl = [Cl(cluster_id=c.cluster_id, centroid=np.zeros(1), member_object_ids=list(c.member_object_ids),
+                  frame_ids=list(c.frame_ids), class_best_rank=dict(c.class_best_rank),
+                  centroid_member_id=c.centroid_member_id, sealed=True) for c in ref8.clusters]
+        ridx = R["index"].build(rcl, R["index"].IndexHeader("cam0", W["dim"], V, n, R["core"].Config(
+            "cheap", k=8, l_s=V, t=t, m=m)))
+        DO = R["core"].DetectedObject
+        objs = {c.centroid_member_id: DO(c.centroid_member_id, 0, 0.0, np.zeros(1), np.zeros(1),
+                                         int(labels[c.centroid_member_id])) for c in ref8.clusters}
+        rgt = R["classifiers"].make_default_profiles(V)["gt"]
+        ql = []
+        for kx in (1, 2, 4, 8):
+            for c in sub:
+                q0 = time.perf_counter()
+                R["query"].QuerySession(ridx, rgt, objs).execute_query(R["query"].QueryRequest(c, k_x=kx))
+                ql.append((time.perf_counter() - q0) * 1e3)
+        cpu_q["reference_python"] = {"p50_ms": float(np.percentile(ql, 50)), "p99_ms": float(np.percentile(ql, 99)),
+                                     "mean_ms": float(np.mean(ql)), "queries": len(ql), "cores": 1,
+                                     "what": "focusidx.query.QuerySession (unmodified, baseline/_ref) over the "
+                                             "same K=8 index, fresh session per query"}
+    c5["cpu_baseline"] = cpu_q
+    del tix, dix8, s8
+    return par, c5, h
+
+
 def run_reference(args):
     ws, rank, _ = _dist()
     if rank != 0:
         return
     threads = os.cpu_count() or 1
     n_sample = args.ref_sample
+    from paper_1801_03493_b200 import synth
+    st = synth.generate(n_sample, dim=WORKLOAD["dim"], vocab=WORKLOAD["vocab"],
+                        n_stream_classes=WORKLOAD["n_stream_classes"], seed=0, device="cpu")
+    h = dict(oids=st.oids.numpy(), fids=st.fids.numpy(), sigs=st.sigs.numpy(), feats=st.feats.numpy(),
+             true_class=st.true_class.numpy())
     for _ in range(args.warmup):
-        cpu_sample(n_sample, 0, threads)
+        cpu_sample(n_sample, 0, threads, h)
     vals = []
     for _ in range(args.steps):
-        v, dt, ncl = cpu_sample(n_sample, 0, threads)
+        v, dt, ncl = cpu_sample(n_sample, 0, threads, h)
         vals.append(v)
     value = float(np.mean(vals))
     line = {
@@ -134,9 +279,11 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": n_sample / value * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"C2 prefix: first {n_sample} objects of 1 stream (D=2048, V=1000, K=4, T=7.5, "
-                               f"M=100); CPU oracle port of the reference focusidx path", **WORKLOAD},
+                               f"M=100); the reference algorithm as the C/OpenMP oracle port (oracle/), "
+                               f"{threads} host threads on the per-insert distance row -- a stronger baseline "
+                               f"than the single-threaded reference Python", **WORKLOAD},
         "cpu_baseline": {"value": value, "unit": "objects/s", "cores": threads, "kind": "port",
-                         "sample": f"first {n_sample} objects of the C2 stream per step"},
+                         "sample": f"first {n_sample} objects of the C2 stream per step, {threads} threads"},
         "e2e": {"value": value, "unit": "objects/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -150,8 +297,12 @@ def main():
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--objects", dest="n", type=int, default=WORKLOAD["n"], help="objects per stream")
     ap.add_argument("--e2e-steps", type=int, default=2)
-    ap.add_argument("--cpu-sample", type=int, default=20000)
-    ap.add_argument("--ref-sample", type=int, default=20000)
+    ap.add_argument("--cpu-sample", type=int, default=200000,
+                    help="objects of the single-core oracle-port cpu_baseline (BASELINE.md §2: 200k prefix)")
+    ap.add_argument("--ref-python-sample", type=int, default=10000,
+                    help="objects of the unmodified reference Python ingest timed beside it (0 = skip)")
+    ap.add_argument("--ref-sample", type=int, default=50000)
+    ap.add_argument("--no-check", action="store_true", help="skip the parity + C5 legs (oracle on the host)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--queries", type=int, default=-1, help="classes queried (x3 k_x values); -1 = every class, 0 = skip")
@@ -162,6 +313,15 @@ def main():
     ap.add_argument("--c3-objects", type=int, default=300_000,
                     help="objects of the C3-shape line (T=5, M=100k: every object seeds; 0 = skip)")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl != "reference":
+        # one process per GPU: re-launch this command under torch.distributed.run
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        sys.exit(subprocess.call(cmd))
     if args.impl == "reference":
         return run_reference(args)
 
@@ -501,12 +661,26 @@ def main():
                  "frac": tf / tf32_peak, "peak_kind": pk, "flagged": int(fl.sum().item()),
                  "bound": "tensor", "note": "TF32 tcgen05 logits + float64 re-score of the candidates"}
 
+    parity = c5 = h = None
+    if rank == 0 and not args.no_check:
+        parity, c5, h = parity_and_c5(data, W, local, args)
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:
-        v, dt, ncl = cpu_sample(args.cpu_sample, 0, 1)
+        nsamp = min(args.cpu_sample, W["n"])
+        v, dt, ncl = cpu_sample(nsamp, 0, 1, h)
         cpu = {"value": v, "unit": "objects/s", "cores": 1, "kind": "port",
-               "sample": f"first {args.cpu_sample} objects of the C2 stream ({dt:.1f} s, single thread)"}
-
+               "sample": f"first {nsamp} objects of the timed C2 stream ({dt:.1f} s, single thread: the C "
+                         f"oracle port, 1 core per stream as BASELINE.md §2 states)"}
+        if args.ref_python_sample > 0:
+            if h is None:
+                from oracle import scale_parity as SP
+                h = SP.host_stream(data, min(W["n"], args.ref_python_sample))
+            rp = reference_python_ingest(h, min(args.ref_python_sample, h["oids"].size))
+            if rp is not None:
+                cpu["reference_python"] = {
+                    "value": rp[0], "unit": "objects/s", "cores": 1, "clusters": rp[2],
+                    "sample": f"first {min(args.ref_python_sample, h['oids'].size)} objects of the same stream "
+                              f"({rp[1]:.1f} s): focusidx.ingest.ingest_stream, unmodified (baseline/_ref)"}
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "objects/s", "n_gpus": ws, "steps": args.steps,
@@ -516,7 +690,8 @@ def main():
                        "streams_per_gpu": 1, "parallelism": f"stream-sharded x{ws}",
                        "l2": "inputs (8 GB features/stream) exceed L2; no flush", **W},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
-            "query": qres, "k1b_fc_head": fcres, "multi_stream": msres, "c3_shape": c3res,
+            "query": qres, "c5_query_sweep": c5, "parity": parity, "k1b_fc_head": fcres, "multi_stream": msres,
+            "c3_shape": c3res,
             "gpu_launches": int(launches),
             "ingest": {"clusters": rep.clusters_emitted, "classified": rep.objects_classified,
                        "distance_computations": rep.distance_computations, "exact_rechecks": rep.exact_rechecks,

@@ -66,6 +66,20 @@ def oracle_ingest(h: dict, k: int, t: float, m: int, vocab: int, seed: int = 0, 
     return O.ingest(h["oids"], h["fids"], h["sigs"], h["feats"], topk, k, t, m, is_dup=dup)
 
 
+def derive_k(ref, k: int):
+    """The oracle result of the same stream ingested with a smaller K.
+
+    Clustering never reads the top-K (tuner.py:10-12), top(K) is a prefix of
+    the ranked list (core.py:60-61) and a class's best rank is the minimum
+    position over the members' lists (clustering.py:65-69), so the K-run's
+    top-K rows are the first K columns and its class sets are the entries of
+    rank <= K.  One oracle run at the largest K checks every smaller K."""
+    from dataclasses import replace
+    cl = [replace(c, class_best_rank={cc: r for cc, r in c.class_best_rank.items() if r <= k})
+          for c in ref.clusters]
+    return replace(ref, topk=np.ascontiguousarray(ref.topk[:, :k]), clusters=cl)
+
+
 def compare(dev: dict, ref, vocab: int) -> dict:
     """Field-by-field mismatch counts (0 everywhere = bit-exact)."""
     mism = {}

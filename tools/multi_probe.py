@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--streams", default="1,2,4,8")
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--serial", action="store_true", help="one host thread runs the engines one after another")
+    ap.add_argument("--counters", action="store_true", help="print each engine's resolve/fold counters")
     ap.add_argument("--trace", type=int, default=0, help="CUPTI-trace this many extra runs at the largest N")
     a = ap.parse_args()
     ns = [int(x) for x in a.streams.split(",")]
@@ -43,6 +44,11 @@ def main():
         t2 = time.perf_counter()
         ix, rp = s.finalize()
         t3 = time.perf_counter()
+        if a.counters:
+            c = s.counters()
+            print(f"  engine {j}: " + " ".join(f"{k}={c[k]}" for k in (
+                "windows", "seq_steps", "exact", "fast", "cyc_passA", "cyc_passB", "cyc_passCD", "cyc_passE",
+                "cyc_seq", "fold_wait_cyc", "fold_chain_cyc", "fold_slot_cyc", "fold_rows")), flush=True)
         del ix, s
         t4 = time.perf_counter()
         return (t1 - t0, t2 - t1, t3 - t2, t4 - t3)
