@@ -697,7 +697,7 @@ def main():
                        "distance_computations": rep.distance_computations, "exact_rechecks": rep.exact_rechecks,
                        "fast_decisions": counters["fast"],
                        "resolve_profile": {k: counters[k] for k in counters if k.startswith(("cyc_", "conf_"))
-                                           or k in ("windows", "seq_steps") or k.startswith("fold_")}},
+                                           or k in ("windows", "seq_steps", "fast_batches") or k.startswith("fold_")}},
         }
         print(json.dumps(line))
     if ws > 1:

@@ -243,6 +243,29 @@ int fx_index_write(const char *path, const char *head, int64_t head_len, int64_t
                    const int64_t *cls_off, const int32_t *cls_id, const int32_t *cls_rank,
                    const int64_t *post_off, const int64_t *post_cluster, int32_t threads);
 
+/* FOCUSIDX/1 reader: index.load (index.py:131-204).  Host-only.
+ * fx_index_read: read + newline translation + CRC-32 trailer + magic + the
+ *   [CLUSTERS] marker (ChecksumMismatch / FormatVersionMismatch / DataError;
+ *   ValueError for a file that is not utf-8);
+ * fx_index_file_header: the header lines ('\n'-joined) for the caller to
+ *   parse (IndexHeader, Config) -- their errors come first in the reference;
+ * fx_index_file_parse(V): cluster records and postings, the reference's
+ *   first error in its evaluation order (DataError, DuplicateClusterId,
+ *   ValueError);
+ * fx_index_file_sizes: [clusters, centroid values, members, frames, class
+ *   entries, posting classes, posting ids];
+ * fx_index_file_export: file-order CSR arrays (classes decoded: OTHER = -1;
+ *   cmid = INT64_MIN for an empty representative field). */
+typedef struct fx_index_file fx_index_file;
+int fx_index_read(const char *path, fx_index_file **out);
+int fx_index_file_header(const fx_index_file *f, char *buf, int64_t cap, int64_t *len);
+int fx_index_file_parse(fx_index_file *f, int64_t vocab);
+int fx_index_file_sizes(const fx_index_file *f, int64_t *out);
+int fx_index_file_export(const fx_index_file *f, int64_t *cid, int64_t *cmid, int64_t *cen_off, double *cen,
+                         int64_t *mem_off, int64_t *mem, int64_t *fr_off, int64_t *fr, int64_t *cls_off,
+                         int32_t *cls, int32_t *rank, int32_t *post_cls, int64_t *post_off, int64_t *post_ids);
+int fx_index_file_free(fx_index_file *f);
+
 /* index.lookup (index.py:75-85): cluster ids posted under class_enc with
  * best rank <= k_x (k_x <= 0 -> K), ascending.  Two-call sizing: pass
  * out_ids = NULL to get *out_n. */

@@ -100,6 +100,13 @@ _SIGS = {
     "fx_index_write": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int32,
                                       ctypes.c_int32, c_i64p, c_f64p, c_i64p, c_i64p, c_i64p, c_i64p, c_i64p, c_i32p,
                                       c_i32p, c_i64p, c_i64p, ctypes.c_int32]),
+    "fx_index_read": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(vp)]),
+    "fx_index_file_header": (ctypes.c_int, [vp, ctypes.c_char_p, ctypes.c_int64, c_i64p]),
+    "fx_index_file_parse": (ctypes.c_int, [vp, ctypes.c_int64]),
+    "fx_index_file_sizes": (ctypes.c_int, [vp, c_i64p]),
+    "fx_index_file_export": (ctypes.c_int, [vp, c_i64p, c_i64p, c_i64p, c_f64p, c_i64p, c_i64p, c_i64p, c_i64p,
+                                            c_i64p, c_i32p, c_i32p, c_i32p, c_i64p, c_i64p]),
+    "fx_index_file_free": (ctypes.c_int, [vp]),
     "fx_lookup": (ctypes.c_int, [vp, ctypes.c_int32, ctypes.c_int32, c_i64p, ctypes.c_int64, c_i64p]),
     "fx_session_create": (ctypes.c_int, [vp, c_i32p, c_i32p, ctypes.c_int64, c_u8p, ctypes.POINTER(vp)]),
     "fx_session_destroy": (ctypes.c_int, [vp]),

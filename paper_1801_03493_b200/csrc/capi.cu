@@ -260,6 +260,16 @@ int fx_stream_create(const fx_stream_config *cfg, fx_stream **out) {
                 b->reserve(B + 1);
             for (auto *b : {&s->sum_d1, &s->sum_e1, &s->sum_lbr}) b->reserve(B + 1);
             for (auto *b : {&s->ev_pos, &s->ev_vic}) b->reserve(B + 1);
+            {  // resolve fast path scratch (k_rfast1 / k_rfast3: 256 objects per CTA, <= 256 groups)
+                const size_t nch = (size_t)cdiv(B, 256), ng = 256;
+                for (auto *b : {&s->f_rank, &s->f_dup}) b->reserve(B + 1);
+                s->f_P.reserve(B + 1);
+                for (auto *b : {&s->f_ccnt, &s->f_cdup}) b->reserve(nch * ng);
+                for (auto *b : {&s->f_csum, &s->f_cmax}) b->reserve(nch * ng);
+                s->f_gi.reserve(4 * ng);
+                s->f_gf.reserve(4 * ng);
+                s->f_gd.reserve(8);
+            }
             s->cid_slot.reserve(4 * (size_t)B);
             s->rowmin.reserve(B + 1);
             FX_CUDA(cudaMemsetAsync(s->rowmin.p, 0x7f, sizeof(int32_t) * (B + 1), s->st));

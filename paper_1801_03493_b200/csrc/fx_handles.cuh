@@ -25,6 +25,9 @@ enum Ctr {
     C_FAST,            // objects decided by the certain (screen-bounded) path
     C_FCFLAG,          // K1b: objects whose top-K sits within the float64 logit margin
     C_EVCUR,           // eviction cursor: every cid below it is evicted or has size > 1
+    C_FASTST,          // resolve fast path of the current batch: 0 not run, 1 committed, 2 fall back
+    C_FDONE,           // fast path: CTAs done (last-block election)
+    C_FASTB,           // batches committed by the fast path
     C_COUNT
 };
 
@@ -96,6 +99,10 @@ struct fx_stream {
     fx::DevBuf<float> dod;     // [B*B] on-demand columns
     fx::DevBuf<int32_t> slot_of, pend_rank, evict_slot, evict_cid, dirty, dirty_off, pend_list, sum_slot, sum_q;
     fx::DevBuf<float> sum_d1, sum_e1, sum_lbr;
+    // resolve fast path scratch (k_rfast1 / k_rfast3)
+    fx::DevBuf<int32_t> f_rank, f_dup, f_ccnt, f_cdup, f_gi;
+    fx::DevBuf<float> f_P, f_csum, f_cmax, f_gf;
+    fx::DevBuf<double> f_gd;
     fx::DevBuf<int32_t> rowmin;          // [B+1] multi-tile TC screen: min lower bound per row (float bits)
     fx::DevBuf<float> snorm;             // [ld] snapshot column norms (TC screen)
     const char *abase = nullptr;         // feature rows of the current ingest call (TMA tensor map)

@@ -349,6 +349,10 @@ struct ResolveArgs {
     const int32_t *sum_slot, *sum_q;
     const float *sum_d1, *sum_e1, *sum_lbr;
     int64_t *h_ring;  // pinned host slot (UVA): counters the host reads two batches later
+    // fast path scratch (k_rfast1 / k_rfast3)
+    int32_t *f_rank, *f_dup, *f_ccnt, *f_cdup, *f_gi;
+    float *f_P, *f_csum, *f_cmax, *f_gf;
+    double *f_gd;
 };
 
 constexpr int RS_THREADS = 512;
@@ -868,6 +872,12 @@ __device__ int rs_compact(int lo, int hi, Pred pred, int32_t *out, int *wsv, int
 template <typename T>
 __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
     pdl_enter();
+    {  // the fast path (k_rfast1/k_rfast3) committed this batch: nothing to do
+        const int64_t fst = A.ctr[C_FASTST];
+        __syncthreads();
+        if (threadIdx.x == 0) A.ctr[C_FASTST] = 0;
+        if (fst == 1) return;
+    }
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int B = A.B;
     const int BC = A.Bcap;  // layout by capacity (multiple of 64): every array stays aligned
@@ -1994,6 +2004,354 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
     for (int i = tid; i < s_ndirty; i += blockDim.x) A.s_cn2[A.dirty[i]] = 0.f;
 }
 
+
+// ---------------------------------------------------------------------------
+// K2b fast path: a batch whose every object joins its nearest snapshot
+// cluster for certain (the common case once the clusters exist: 799,999 of
+// 800,000 objects at C2).  The single-CTA k_resolve above decides the same
+// certainty test (pass D) window by window; here the whole batch is one
+// window spread over the grid:
+//   k_rfast1 (one CTA per 256 objects): hypothesis group = snapshot index of
+//     the nearest candidate; stable in-chunk rank (warp match + per-warp
+//     group tables), in-chunk prefix sums of the hypothesis upper bounds
+//     (fp32, every add rounded up -> an upper bound of the exact sum, as the
+//     single-CTA scan) and of the dedup runs; the last CTA to finish scans
+//     the chunk tables per group, derives each group's drift bound
+//     (drift_avg), the two largest drifts and the fold's dirty order.
+//   k_rfast3 (one CTA per 256 objects): per object rank i, prefix P_i, the
+//     certainty test ub0 + drift(i) <= T and lbr - max_other_drift > ub;
+//     certain objects write their cluster, featured / member / pending rank
+//     and pending-list entry; the last CTA commits the slot state -- only if
+//     EVERY object was certain, else k_resolve re-runs the batch from the
+//     untouched state (it rewrites every per-object output).
+// Preconditions (else k_resolve): no residual column (no probable seed),
+// snapshot = live set, 0 < L <= RF_MAXG.
+// ---------------------------------------------------------------------------
+constexpr int RF_T = 256, RF_W = RF_T / 32, RF_MAXG = 256;
+
+__global__ void __launch_bounds__(RF_T) k_rfast1(ResolveArgs A) {
+    pdl_enter();
+    __shared__ int wc[RF_W][RF_MAXG], wd[RF_W][RF_MAXG];
+    __shared__ float wsu[RF_W][RF_MAXG];
+    __shared__ int smax[RF_MAXG];
+    __shared__ float sh_ub[RF_T];
+    __shared__ int sh_dr[RF_T];
+    __shared__ int s_last;
+    __shared__ double r1[RF_W], r2[RF_W];
+    __shared__ int rs[RF_W], scn[RF_W], scf[RF_W];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    int64_t *ctr = A.ctr;
+    const int B = A.B;
+    const int nsnap = (int)ctr[C_NSNAP], L = (int)ctr[C_NLIVE];
+    const bool ok = ctr[C_NRES] == 0 && nsnap == L && L > 0 && nsnap <= RF_MAXG && B > 0;
+    if (!ok) {
+        if (blockIdx.x == 0 && tid == 0) ctr[C_FASTST] = 2;
+        return;
+    }
+    for (int e = tid; e < RF_W * nsnap; e += RF_T) {
+        wc[e / nsnap][e % nsnap] = 0;
+        wd[e / nsnap][e % nsnap] = 0;
+        wsu[e / nsnap][e % nsnap] = 0.f;
+    }
+    for (int g = tid; g < nsnap; g += RF_T) smax[g] = 0;
+    const int p = blockIdx.x * RF_T + tid;
+    int g = -1, dr = 0;
+    float ub0 = 0.f;
+    if (p < B) {
+        g = A.sum_q[p];
+        if (g < 0 || g >= nsnap) g = -1;
+        ub0 = (A.sum_d1[p] + A.sum_e1[p]) * 1.000001f + 1e-30f;
+        dr = A.dup_run[A.c0 + p];
+    }
+    sh_ub[tid] = ub0;
+    sh_dr[tid] = dr;
+    __syncthreads();
+    if (p < B && g < 0) ctr[C_FASTST] = 2;  // no hypothesis: the sequential resolve decides
+    const unsigned act = __ballot_sync(0xffffffffu, g >= 0);
+    unsigned peers = 0, lower = 0;
+    if (g >= 0) {
+        peers = __match_any_sync(act, g);
+        lower = peers & ((1u << lane) - 1u);
+    }
+    float Pw = 0.f;
+    int Dw = 0;
+    for (unsigned m = lower; m; m &= m - 1) {  // earlier same-group lanes, in lane order
+        const int l = wid * 32 + __ffs(m) - 1;
+        Pw = __fadd_ru(Pw, sh_ub[l]);
+        Dw += sh_dr[l];
+    }
+    const int rw = __popc(lower);
+    if (g >= 0) {
+        if ((peers >> lane) == 1u) {  // highest lane of its group writes the warp totals
+            wc[wid][g] = rw + 1;
+            wsu[wid][g] = __fadd_ru(Pw, ub0);
+            wd[wid][g] = Dw + dr;
+        }
+        atomicMax(&smax[g], __float_as_int(ub0));  // ub0 > 0: int order = float order
+    }
+    __syncthreads();
+    for (int gg = tid; gg < nsnap; gg += RF_T) {  // exclusive scan over warps, chunk totals
+        int c = 0, d = 0;
+        float su = 0.f;
+        for (int w = 0; w < RF_W; w++) {
+            const int cw = wc[w][gg], dw = wd[w][gg];
+            const float sw = wsu[w][gg];
+            wc[w][gg] = c;
+            wd[w][gg] = d;
+            wsu[w][gg] = su;
+            c += cw;
+            d += dw;
+            su = __fadd_ru(su, sw);
+        }
+        const int idx = blockIdx.x * RF_MAXG + gg;
+        A.f_ccnt[idx] = c;
+        A.f_cdup[idx] = d;
+        A.f_csum[idx] = su;
+        A.f_cmax[idx] = __int_as_float(smax[gg]);
+    }
+    __syncthreads();
+    if (g >= 0) {
+        A.f_rank[p] = wc[wid][g] + rw;
+        A.f_P[p] = __fadd_ru(wsu[wid][g], Pw);
+        A.f_dup[p] = wd[wid][g] + Dw;
+    }
+    // last CTA: per group scan over the chunks -> bases, totals, drift bounds
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd((unsigned long long *)&ctr[C_FDONE], 1ull) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const int nch = gridDim.x;
+    int c = 0, d = 0;
+    float su = 0.f, mx = 0.f, drift = 0.f;
+    const int gg = tid;  // nsnap <= RF_MAXG = RF_T: one group per thread
+    if (gg < nsnap) {
+        for (int k = 0; k < nch; k++) {
+            const int idx = k * RF_MAXG + gg;
+            const int ck = __ldcg(A.f_ccnt + idx), dk = __ldcg(A.f_cdup + idx);
+            const float sk = __ldcg(A.f_csum + idx), mk = __ldcg(A.f_cmax + idx);
+            A.f_ccnt[idx] = c;
+            A.f_cdup[idx] = d;
+            A.f_csum[idx] = su;
+            c += ck;
+            d += dk;
+            su = __fadd_ru(su, sk);
+            mx = fmaxf(mx, mk);
+        }
+        const int sl = A.snap_slot[gg];
+        const float cn = sqrtf(A.s_cn2[sl]) * 1.00001f;
+        drift = c > 0 ? drift_avg(0.f, A.s_nfeat[sl], su, c, cn, mx) : 0.f;
+        A.f_gi[gg * 4 + 0] = c;
+        A.f_gi[gg * 4 + 1] = d;
+        A.f_gf[gg * 4 + 0] = drift;
+        A.f_gf[gg * 4 + 1] = mx;
+        A.f_gf[gg * 4 + 2] = cn;
+    }
+    // the two largest end-of-batch drifts over the live (= snapshot) slots
+    double m1 = gg < nsnap ? (double)drift : -1.0, m2 = -1.0;
+    int m1s = gg < nsnap ? gg : -1;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const double o1 = __shfl_xor_sync(0xffffffffu, m1, o), o2 = __shfl_xor_sync(0xffffffffu, m2, o);
+        const int os = __shfl_xor_sync(0xffffffffu, m1s, o);
+        if (o1 > m1) {
+            m2 = fmax(m1, o2);
+            m1 = o1;
+            m1s = os;
+        } else {
+            m2 = fmax(m2, o1);
+        }
+    }
+    if (lane == 0) {
+        r1[wid] = m1;
+        r2[wid] = m2;
+        rs[wid] = m1s;
+    }
+    // dirty order: the group with the most members first (k_fold gives it its
+    // own grid row), then the others in snapshot order; offsets = scan of counts
+    int bc = gg < nsnap ? c : -1, bi = gg;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        const int oc = __shfl_xor_sync(0xffffffffu, bc, o), oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (oc > bc || (oc == bc && oi < bi)) {
+            bc = oc;
+            bi = oi;
+        }
+    }
+    if (lane == 0) {
+        scn[wid] = bc;
+        scf[wid] = bi;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        double a1 = r1[0], a2 = r2[0];
+        int as = rs[0];
+        int best = scf[0], bcc = scn[0];
+        for (int w = 1; w < RF_W; w++) {
+            if (r1[w] > a1) {
+                a2 = fmax(a1, r2[w]);
+                a1 = r1[w];
+                as = rs[w];
+            } else {
+                a2 = fmax(a2, r1[w]);
+            }
+            if (scn[w] > bcc || (scn[w] == bcc && scf[w] < best)) {
+                bcc = scn[w];
+                best = scf[w];
+            }
+        }
+        A.f_gd[0] = a1 < 0 ? 0.0 : a1;
+        A.f_gd[1] = a2 < 0 ? 0.0 : a2;
+        A.f_gd[2] = (double)as;
+        A.f_gd[3] = (double)best;
+        A.f_gd[4] = (double)bcc;
+    }
+    __syncthreads();
+    const int best = (int)A.f_gd[3], bcc = (int)A.f_gd[4];
+    const bool fl = gg < nsnap && c > 0 && gg != best;
+    const int cv = fl ? c : 0;
+    int xf = fl ? 1 : 0, xc = cv;  // inclusive warp scans of (dirty flag, count)
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int yf = __shfl_up_sync(0xffffffffu, xf, o), yc = __shfl_up_sync(0xffffffffu, xc, o);
+        if (lane >= o) {
+            xf += yf;
+            xc += yc;
+        }
+    }
+    __syncthreads();
+    if (lane == 31) {
+        scf[wid] = xf;
+        scn[wid] = xc;
+    }
+    __syncthreads();
+    int bf = 0, bcn = 0;
+    for (int w = 0; w < wid; w++) {
+        bf += scf[w];
+        bcn += scn[w];
+    }
+    if (gg < nsnap) {
+        const bool has = bcc > 0;  // the largest group is dirty[0] when any object joined
+        if (gg == best && c > 0) {
+            A.f_gi[gg * 4 + 2] = 0;
+            A.f_gi[gg * 4 + 3] = 0;
+        } else if (fl) {
+            A.f_gi[gg * 4 + 2] = (has ? 1 : 0) + bf + xf - 1;
+            A.f_gi[gg * 4 + 3] = (has ? bcc : 0) + bcn + xc - cv;
+        } else {
+            A.f_gi[gg * 4 + 2] = -1;
+            A.f_gi[gg * 4 + 3] = 0;
+        }
+    }
+    if (tid == 0) ctr[C_FDONE] = 0;
+}
+
+__global__ void __launch_bounds__(RF_T) k_rfast3(ResolveArgs A) {
+    pdl_enter();
+    __shared__ int s_last, s_fail;
+    const int tid = threadIdx.x;
+    int64_t *ctr = A.ctr;
+    if (ctr[C_FASTST] == 2) return;  // k_rfast1 declined
+    const int B = A.B;
+    const double md1 = A.f_gd[0], md2 = A.f_gd[1];
+    const int md1g = (int)A.f_gd[2];
+    if (tid == 0) s_fail = 0;
+    __syncthreads();
+    const int p = blockIdx.x * RF_T + tid;
+    if (p < B) {
+        const int g = A.sum_q[p];
+        const int idx = blockIdx.x * RF_MAXG + g;
+        const int i = A.f_ccnt[idx] + A.f_rank[p];
+        const float P = __fadd_ru(A.f_csum[idx], A.f_P[p]);
+        const int sl = A.snap_slot[g];
+        const int nf0 = A.s_nfeat[sl];
+        const float ub0 = (A.sum_d1[p] + A.sum_e1[p]) * 1.000001f + 1e-30f;
+        const double ub = (double)ub0 + (double)drift_avg(0.f, nf0, P, i, A.f_gf[g * 4 + 2], A.f_gf[g * 4 + 1]);
+        const float lbr = A.sum_lbr[p];
+        const float lbr2 = lbr - fabsf(lbr) * 1e-6f - 1e-30f;
+        const double md = g == md1g ? md2 : md1;
+        const double lbo = (double)lbr2 - md * 1.000001;
+        if (lbo > ub && ub <= A.T) {
+            const int64_t obj = A.cls_obj[A.c0 + p];
+            A.cluster_of[obj] = A.s_cid[sl];
+            A.mrank[obj] = A.s_size[sl] + i + A.f_cdup[idx] + A.f_dup[p];
+            A.frank[obj] = nf0 + i;
+            A.pend_rank[p] = i;
+            A.slot_of[p] = sl;
+            A.pend_list[A.f_gi[g * 4 + 3] + i] = p;
+        } else {
+            s_fail = 1;
+        }
+    }
+    __syncthreads();
+    if (tid == 0 && s_fail) ctr[C_FASTST] = 2;
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_last = atomicAdd((unsigned long long *)&ctr[C_FDONE], 1ull) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (tid == 0) ctr[C_FDONE] = 0;
+    if (__ldcg(&ctr[C_FASTST]) == 2) return;  // some object needs the sequential resolve
+    // commit: k_resolve's prologue (recycle deferred slots, reset snapshot
+    // fields), the groups' slot state, the fold's dirty CSR, the counters
+    const int nsnap = (int)ctr[C_NSNAP], L = (int)ctr[C_NLIVE];
+    const int gg = tid;
+    int nd = 0;
+    if (gg < nsnap) {
+        const int sl = A.snap_slot[gg];
+        const int c = A.f_gi[gg * 4 + 0];
+        A.s_snapq[sl] = gg;
+        A.s_seedpos[sl] = -1;
+        A.s_foldpos[sl] = 0;
+        A.s_odcol[sl] = -1;
+        if (c > 0) {
+            const int di = A.f_gi[gg * 4 + 2];
+            A.s_drift[sl] = (double)A.f_gf[gg * 4 + 0];
+            A.s_nfeat[sl] += c;
+            A.s_size[sl] += c + A.f_gi[gg * 4 + 1];
+            A.s_pend[sl] = c;
+            A.s_didx[sl] = di;
+            A.dirty[di] = sl;
+            A.dirty_off[di] = A.f_gi[gg * 4 + 3];
+            A.s_cn2[sl] = 0.f;  // the fold re-accumulates ||c||^2
+        } else {
+            A.s_drift[sl] = 0.0;
+            A.s_pend[sl] = 0;
+        }
+    }
+    const unsigned long long has = __ballot_sync(0xffffffffu, gg < nsnap && A.f_gi[gg * 4 + 0] > 0);
+    __shared__ int s_nd;
+    if (tid == 0) s_nd = 0;
+    __syncthreads();
+    if ((tid & 31) == 0) atomicAdd(&s_nd, __popc((unsigned)has));
+    __syncthreads();
+    nd = s_nd;
+    if (tid == 0) {
+        int nfree = (int)ctr[C_NFREE];
+        const int ndf = (int)ctr[C_NDEFER];
+        for (int k = 0; k < ndf; k++) A.free_stack[nfree++] = A.defer_free[k];
+        A.dirty_off[nd] = B;
+        ctr[C_NFREE] = nfree;
+        ctr[C_NDEFER] = 0;
+        ctr[C_NEVICT_BATCH] = 0;
+        ctr[C_NDIRTY] = nd;
+        ctr[C_NOD] = 0;
+        ctr[C_NSNAP] = L;
+        ctr[C_DC] += (int64_t)L * B;
+        ctr[C_FAST] += B;
+        ctr[C_NINSERTED] += B;
+        ctr[C_LAST_CID] = A.s_cid[A.snap_slot[A.sum_q[B - 1]]];
+        ctr[C_FASTB] += 1;
+        if (A.h_ring) {
+            A.h_ring[C_NEXT_CID] = ctr[C_NEXT_CID];
+            __threadfence_system();
+        }
+        ctr[C_FASTST] = 1;
+    }
+}
+
 // ---------------------------------------------------------------------------
 // K2c: fold the batch's members into the float64 sums (stream order) and
 // refresh the FP32 snapshot; record final centroids of evicted clusters.
@@ -2527,6 +2885,26 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             A.sum_e1 = s->sum_e1.p;
             A.sum_lbr = s->sum_lbr.p;
             A.h_ring = s->h_ctr_ring + (s->batch_no % 3) * C_COUNT;
+            A.f_rank = s->f_rank.p;
+            A.f_dup = s->f_dup.p;
+            A.f_P = s->f_P.p;
+            A.f_ccnt = s->f_ccnt.p;
+            A.f_cdup = s->f_cdup.p;
+            A.f_csum = s->f_csum.p;
+            A.f_cmax = s->f_cmax.p;
+            A.f_gi = s->f_gi.p;
+            A.f_gf = s->f_gf.p;
+            A.f_gd = s->f_gd.p;
+            // fast path first (the common all-certain batch over the whole
+            // grid); k_resolve returns at once when it committed
+            static const bool nofast = getenv("FOCUS_B200_NOFAST") && atoi(getenv("FOCUS_B200_NOFAST"));
+            if (!nofast) {
+                const unsigned nch = (unsigned)cdiv(B, RF_T);
+                launch_pdl(k_rfast1, dim3(nch), dim3(RF_T), 0, st, A);
+                FX_LAUNCHED();
+                launch_pdl(k_rfast3, dim3(nch), dim3(RF_T), 0, st, A);
+                FX_LAUNCHED();
+            }
             const PwPlan &P = *s->plan_host;
             size_t smem = resolve_smem(s->B, P);
             auto kern = k_resolve<T>;

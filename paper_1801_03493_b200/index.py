@@ -77,11 +77,22 @@ class DeviceIndex:
 class TopKIndex:
     """header + clusters (id -> Cluster) + postings (class -> sorted ids)."""
 
-    def __init__(self, header: IndexHeader, clusters=None, postings=None, device: DeviceIndex | None = None):
+    def __init__(self, header: IndexHeader, clusters=None, postings=None, device: DeviceIndex | None = None,
+                 file_arrays: dict | None = None):
         self.header = header
         self._clusters = clusters
         self._postings = postings
         self.device = device
+        self._file = file_arrays  # CSR arrays of a loaded FOCUSIDX/1 file (fx_index_file_export)
+
+    def ensure_device(self) -> DeviceIndex:
+        """The device index, posted on first use (a loaded or hand-built index)."""
+        if self.device is None:
+            if self._file is not None and self._clusters is None:
+                self.device = _device_from_file(self._file, self.header)
+            else:
+                self.device = build(list(self.clusters.values()), self.header).device
+        return self.device
 
     # -- lazily materialised reference fields --------------------------------
     @property
@@ -105,6 +116,8 @@ class TopKIndex:
         self._postings = v
 
     def _materialise(self):
+        if self._file is not None:
+            return self._materialise_file()
         ex = self.device.export(centroids=True)
         V = self.header.vocab
         cen = ex.get("centroids")
@@ -126,6 +139,24 @@ class TopKIndex:
             a, b = po[enc], po[enc + 1]
             if b > a:
                 postings[-1 if enc == V else enc] = pc[a:b].tolist()
+        if self._clusters is None:
+            self._clusters = clusters
+        if self._postings is None:
+            self._postings = postings
+
+    def _materialise_file(self):
+        f = self._file
+        clusters = {}
+        co, mo, fo, ko = f["cen_off"], f["mem_off"], f["fr_off"], f["cls_off"]
+        for i, cid in enumerate(f["cid"].tolist()):
+            cm = int(f["cmid"][i])
+            clusters[cid] = Cluster(
+                cluster_id=cid, centroid=f["cen"][co[i]:co[i + 1]].copy(),
+                member_object_ids=f["mem"][mo[i]:mo[i + 1]].tolist(), frame_ids=f["fr"][fo[i]:fo[i + 1]].tolist(),
+                class_best_rank=dict(zip(f["cls"][ko[i]:ko[i + 1]].tolist(), f["rank"][ko[i]:ko[i + 1]].tolist())),
+                centroid_member_id=None if cm == _NO_CMID else cm, sealed=True)
+        po = f["post_off"]
+        postings = {c: f["post_ids"][po[j]:po[j + 1]].tolist() for j, c in enumerate(f["post_cls"].tolist())}
         if self._clusters is None:
             self._clusters = clusters
         if self._postings is None:
@@ -176,8 +207,7 @@ def lookup(idx: TopKIndex, class_id: int, k_x: int | None = None) -> list:
     enc = encode_class(class_id, V)
     if enc < 0 or enc > V:
         return []
-    if idx.device is None:  # e.g. loaded from a file: post it on the device once
-        idx.device = build(list(idx.clusters.values()), idx.header).device
+    idx.ensure_device()  # e.g. loaded from a file: posted on the device once
     L = _lib.load()
     n = ctypes.c_int64(0)
     _lib.check(L.fx_lookup(idx.device.handle, enc, kx, None, 0, ctypes.byref(n)))
@@ -251,68 +281,109 @@ def save(idx: TopKIndex, path, threads: int = 0) -> None:
             os.unlink(tmp)
 
 
-def load(path) -> TopKIndex:
-    """index.load (index.py:131-204): CRC32 trailer and magic checked first,
-    then header, cluster records and postings; the same errors as the
-    reference (ChecksumMismatch, FormatVersionMismatch, DataError,
-    DuplicateClusterId).  The device index is built on first lookup."""
-    import zlib
-    with open(path, "r", encoding="utf-8") as fh:
-        data = fh.read()
-    head, nl, last = data.rstrip("\n").rpartition("\n")
-    if not last.startswith("CRC32:"):
-        raise ChecksumMismatch("missing CRC32 trailer")
-    body = head + nl
-    expect = last[len("CRC32:"):]
-    actual = f"{zlib.crc32(body.encode('utf-8')) & 0xFFFFFFFF:08x}"
-    if actual != expect:
-        raise ChecksumMismatch(f"CRC mismatch: file says {expect}, computed {actual}")
-    lines = body.splitlines()
-    if not lines or lines[0] != _MAGIC:
-        raise FormatVersionMismatch(f"index file must start with {_MAGIC}")
-    kv, config_lines = {}, []
-    i = 1
-    while i < len(lines) and lines[i] != "[CLUSTERS]":
-        key, _, value = lines[i].partition("=")
-        if key in ("stream_id", "D", "V", "n"):
-            kv[key] = value
+_NO_CMID = -(1 << 63)
+_HEADER_KEYS = ("stream_id", "D", "V", "n")
+
+
+def _header_from_lines(text: str) -> IndexHeader:
+    """The header block of a FOCUSIDX/1 file (index.py:147-167 semantics: the
+    four stream keys, everything else is the config text; KeyError /
+    ValueError become DataError, parse_config raises its own DataError)."""
+    stream, cfg_lines = {}, []
+    for line in text.split("\n") if text else ():
+        key, _, value = line.partition("=")
+        if key in _HEADER_KEYS:
+            stream[key] = value
         else:
-            config_lines.append(lines[i])
-        i += 1
-    if i >= len(lines):
-        raise DataError("index file has no [CLUSTERS] section")
+            cfg_lines.append(line)
     try:
-        vocab = int(kv["V"])
-        header = IndexHeader(stream_id=kv["stream_id"], dim=int(kv["D"]), vocab=vocab, n_objects=int(kv["n"]),
-                             config=parse_config("\n".join(config_lines)))
+        vocab = int(stream["V"])
+        stream_id, dim, n = stream["stream_id"], int(stream["D"]), int(stream["n"])
+        return IndexHeader(stream_id=stream_id, dim=dim, vocab=vocab, n_objects=n,
+                           config=parse_config("\n".join(cfg_lines)))
     except (KeyError, ValueError) as exc:
         raise DataError(f"bad index header: {exc}") from exc
-    clusters = {}
-    i += 1
-    while i < len(lines) and lines[i] != "[POSTINGS]":
-        parts = lines[i].split("|")
-        if len(parts) != 6:
-            raise DataError(f"bad cluster record: {lines[i]!r}")
-        cid = int(parts[0])
-        if cid in clusters:
-            raise DuplicateClusterId(str(cid))
-        ranks = {}
-        if parts[5]:
-            for item in parts[5].split(","):
-                cls, _, rank = item.partition(":")
-                ranks[decode_class(int(cls), vocab)] = int(rank)
-        clusters[cid] = Cluster(cluster_id=cid, centroid=np.array([float(x) for x in parts[2].split(",")]),
-                                member_object_ids=[int(x) for x in parts[3].split(",")],
-                                frame_ids=[int(x) for x in parts[4].split(",")], class_best_rank=ranks,
-                                centroid_member_id=None if parts[1] == "" else int(parts[1]), sealed=True)
-        i += 1
-    if i >= len(lines):
-        raise DataError("index file has no [POSTINGS] section")
-    postings = {}
-    for line in lines[i + 1:]:
-        cls, _, ids = line.partition("|")
-        postings[decode_class(int(cls), vocab)] = [int(x) for x in ids.split(",")]
-    return TopKIndex(header=header, clusters=clusters, postings=postings)
+
+
+def load(path) -> TopKIndex:
+    """index.load (index.py:131-204) through the native reader
+    (csrc/index_read.cu: CRC-32, line split, multi-threaded record parse into
+    CSR arrays, the reference's errors in its order).  Clusters and postings
+    are materialised as Python objects only when asked for; lookup and query
+    post the arrays on the device directly."""
+    L = _lib.load()
+    h = _lib.vp()
+    _lib.check(L.fx_index_read(os.fsencode(path), ctypes.byref(h)))
+    try:
+        n = ctypes.c_int64(0)
+        _lib.check(L.fx_index_file_header(h, None, 0, ctypes.byref(n)))
+        buf = ctypes.create_string_buffer(max(1, n.value))
+        _lib.check(L.fx_index_file_header(h, buf, n.value, ctypes.byref(n)))
+        header = _header_from_lines(buf.raw[:n.value].decode("utf-8"))
+        _lib.check(L.fx_index_file_parse(h, header.vocab))
+        sz = np.zeros(7, np.int64)
+        _lib.check(L.fx_index_file_sizes(h, _lib.p64(sz)))
+        C, ncen, nmem, nfr, ncls, npc, npid = (int(x) for x in sz)
+        f = dict(cid=np.empty(C, np.int64), cmid=np.empty(C, np.int64), cen_off=np.empty(C + 1, np.int64),
+                 cen=np.empty(ncen, np.float64), mem_off=np.empty(C + 1, np.int64), mem=np.empty(nmem, np.int64),
+                 fr_off=np.empty(C + 1, np.int64), fr=np.empty(nfr, np.int64), cls_off=np.empty(C + 1, np.int64),
+                 cls=np.empty(ncls, np.int32), rank=np.empty(ncls, np.int32), post_cls=np.empty(npc, np.int32),
+                 post_off=np.empty(npc + 1, np.int64), post_ids=np.empty(npid, np.int64))
+        _lib.check(L.fx_index_file_export(
+            h, _lib.p64(f["cid"]), _lib.p64(f["cmid"]), _lib.p64(f["cen_off"]), _lib.pf64(f["cen"]),
+            _lib.p64(f["mem_off"]), _lib.p64(f["mem"]), _lib.p64(f["fr_off"]), _lib.p64(f["fr"]),
+            _lib.p64(f["cls_off"]), _lib.p32(f["cls"]), _lib.p32(f["rank"]), _lib.p32(f["post_cls"]),
+            _lib.p64(f["post_off"]), _lib.p64(f["post_ids"])))
+    finally:
+        L.fx_index_file_free(h)
+    return TopKIndex(header=header, file_arrays=f)
+
+
+def _device_from_file(f: dict, header: IndexHeader, device: int | None = None) -> DeviceIndex:
+    """Post a loaded file's CSR arrays on the device (clusters in id order).
+    The device rebuilds the postings from the class sets (K3); a file whose
+    postings disagree with its own class sets is rejected here."""
+    V, D, C = header.vocab, header.dim, f["cid"].size
+    order = np.argsort(f["cid"], kind="stable")
+    ids = np.ascontiguousarray(f["cid"][order])
+    mlen = np.diff(f["mem_off"])[order]
+    if not np.array_equal(mlen, np.diff(f["fr_off"])[order]):
+        raise DataError("cluster member and frame lists differ in length")
+    def gather(off, vals, lens):  # segments of `vals` in id order (vectorised)
+        o = np.zeros(C + 1, np.int64)
+        np.cumsum(lens, out=o[1:])
+        idx = np.repeat(off[:-1][order] - o[:-1], lens) + np.arange(int(o[-1]), dtype=np.int64)
+        return o, np.ascontiguousarray(vals[idx])
+    mem_off, mem = gather(f["mem_off"], f["mem"], mlen)
+    _, fr = gather(f["fr_off"], f["fr"], mlen)
+    klen = np.diff(f["cls_off"])[order]
+    cls_off, cls = gather(f["cls_off"], f["cls"], klen)
+    _, rank = gather(f["cls_off"], f["rank"], klen)
+    cls = np.ascontiguousarray(np.where(cls == -1, V, cls).astype(np.int32))
+    rank = np.ascontiguousarray(rank.astype(np.int32))
+    cmid = f["cmid"][order]
+    reps = np.ascontiguousarray(np.where(cmid == _NO_CMID, -1, cmid).astype(np.int64))
+    cen = None
+    clen = np.diff(f["cen_off"])
+    if C and np.all(clen == D):
+        cen = np.ascontiguousarray(f["cen"].reshape(C, D)[order])
+    L = _lib.load()
+    h = _lib.vp()
+    _lib.check(L.fx_index_build(C, V, header.k, D, _lib.device() if device is None else device, _lib.p64(ids),
+                                _lib.pf64(cen) if cen is not None else None, _lib.p64(reps), _lib.p64(mem_off),
+                                _lib.p64(mem), _lib.p64(fr), _lib.p64(cls_off), _lib.p32(cls), _lib.p32(rank),
+                                ctypes.byref(h)))
+    dev = DeviceIndex(h)
+    ex = dev.export(centroids=False)
+    po, pc = ex["post_off"], ex["post_cluster"]
+    fo = f["post_off"]
+    for j, c in enumerate(f["post_cls"].tolist()):
+        enc = V if c == -1 else c
+        if not np.array_equal(pc[po[enc]:po[enc + 1]], f["post_ids"][fo[j]:fo[j + 1]]):
+            raise DataError(f"postings of class {c} disagree with the cluster class sets")
+    if int(po[-1]) != int(fo[-1]):
+        raise DataError("postings disagree with the cluster class sets")
+    return dev
 
 
 __all__ = ["IndexHeader", "TopKIndex", "DeviceIndex", "build", "lookup", "decode_class", "save", "load"]

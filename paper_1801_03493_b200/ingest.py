@@ -117,7 +117,7 @@ class Stream:
 
     COUNTERS = ("nlive", "next_cid", "dc", "nfree", "nevict_total", "exact", "nsnap", "nres", "ninserted",
                 "nevict_batch", "ndefer", "nod", "last_cid", "ndirty", "err", "fast", "fc_flagged", "ev_cursor",
-                "cyc_passA", "cyc_passB", "cyc_passCD", "cyc_confirm", "cyc_passE", "cyc_seq", "windows", "seq_steps",
+                "fast_state", "fast_done", "fast_batches", "cyc_passA", "cyc_passB", "cyc_passCD", "cyc_confirm", "cyc_passE", "cyc_seq", "windows", "seq_steps",
                 "conf_b0", "conf_b1_7", "conf_b8_15", "conf_b16_31", "conf_b32_63", "conf_b64_127", "conf_b128",
                 "conf_young", "fold_wait_cyc", "fold_chain_cyc", "fold_slot_cyc", "fold_rows", "fold_slots")
     PHASES = ("k0_k1a", "screen", "resolve", "fold", "seal", "index", "batches", "screen_resid",

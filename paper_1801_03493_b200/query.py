@@ -61,10 +61,7 @@ class QuerySession:
         self.ingest_profile = ingest_profile
         self._labels = labels
         self.L = _lib.load()
-        if idx.device is None:  # e.g. index.load(): post it on the device once (index.py:135-204)
-            from .index import build
-            idx.device = build(list(idx.clusters.values()), idx.header).device
-        dev = idx.device
+        dev = idx.ensure_device()  # e.g. index.load(): posted on the device once
         C = int(dev.sizes.n_clusters)
         reps = np.empty(C, np.int64)
         if C:
