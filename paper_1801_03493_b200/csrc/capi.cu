@@ -86,6 +86,14 @@ __global__ void k_lead_dups(int64_t lead, const int64_t *__restrict__ ctr, const
     if (threadIdx.x == 0 && !found) cl_size[cid] += (int)lead;
 }
 
+}  // namespace fx
+namespace fx {
+// make the engine's main stream wait for the lagged exact chain (st2)
+void chain_join(fx_stream *s) {
+    for (int i = 0; i < 2; i++)
+        if (s->chain_pending[i]) FX_CUDA(cudaStreamWaitEvent(s->st, s->ev_ch[i], 0));
+}
+
 __global__ void k_init_free(int64_t nslots, int32_t *__restrict__ free_stack) {
     int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i < nslots) free_stack[i] = (int32_t)(nslots - 1 - i);
@@ -137,6 +145,11 @@ void fx_stream::tcollect() {
 }
 
 fx_stream::~fx_stream() {
+    if (st2) cudaStreamSynchronize(st2);  // the lagged chain reads engine buffers
+    for (auto &e : ev_tf)
+        if (e) cudaEventDestroy(e);
+    for (auto &e : ev_ch)
+        if (e) cudaEventDestroy(e);
     if (h_ctr_ring) {
         for (auto &e : ring_ev)
             if (e) cudaEventSynchronize(e);
@@ -226,7 +239,7 @@ int fx_stream_create(const fx_stream_config *cfg, fx_stream **out) {
             // k_resolve keeps per-object state of the whole batch in shared memory
             while (B > 64 && resolve_smem(B, *s->plan_host) + 48 * 1024 > 227 * 1024) B -= 64;
             s->B = B;
-            const int64_t max_slots_mem = (int64_t)(48e9 / (12.0 * D));
+            const int64_t max_slots_mem = (int64_t)(48e9 / (20.0 * D));  // S + S_tree + C32
             int64_t live_cap = std::min<int64_t>(cfg->m, max_slots_mem);
             s->nslots = live_cap + B + 1;
             s->ld = std::max<int64_t>(1, live_cap + 1);
@@ -239,6 +252,25 @@ int fx_stream_create(const fx_stream_config *cfg, fx_stream **out) {
                 b->reserve(ns);
             s->s_drift.reserve(ns);
             s->s_cn2.reserve(ns);
+            {  // snapshot tree fold + lagged exact chain (k_tfold / k_fold on st2)
+                FX_CUDA(cudaStreamCreateWithFlags(&s->st2, cudaStreamNonBlocking));
+                for (int i = 0; i < 2; i++) {
+                    FX_CUDA(cudaEventCreateWithFlags(&s->ev_tf[i], cudaEventDisableTiming));
+                    FX_CUDA(cudaEventCreateWithFlags(&s->ev_ch[i], cudaEventDisableTiming));
+                }
+                s->S_tree.reserve((size_t)ns * D);
+                s->s_abs.reserve(ns);
+                s->s_sdev.reserve(ns);
+                FX_CUDA(cudaMemsetAsync(s->s_sdev.p, 0, sizeof(double) * ns, s->st));
+                const size_t nd = 2 * (size_t)B + 3, gx = (size_t)cdiv(D, 32);
+                s->tf_cn2.reserve(nd * gx);
+                s->tf_cnt.reserve(nd);
+                FX_CUDA(cudaMemsetAsync(s->tf_cnt.p, 0, sizeof(int32_t) * nd, s->st));
+                s->cd_meta.reserve(2 * 8 * nd);
+                s->cd_off.reserve(2 * nd);
+                s->cd_rows.reserve(2 * (size_t)B);
+                s->cd_nd.reserve(2);
+            }
             FX_CUDA(cudaMemsetAsync(s->s_cn2.p, 0, sizeof(float) * ns, s->st));
             FX_CUDA(cudaMemsetAsync(s->s_evicted.p, 0, sizeof(int32_t) * ns, s->st));
             FX_CUDA(cudaMemsetAsync(s->s_grp.p, 0xff, sizeof(int32_t) * ns, s->st));
@@ -294,12 +326,13 @@ int fx_stream_destroy(fx_stream *s) {
     FX_GUARD({
         if (s) {
             set_dev(s->dev);
-            cudaStream_t st = s->st;
+            cudaStream_t st = s->st, st2 = s->st2;
             {
                 StreamGuard sg_(st);
                 delete s;
             }
             if (st) cudaStreamDestroy(st);  // destroyed once its queued frees complete
+            if (st2) cudaStreamDestroy(st2);
         }
     })
 }
@@ -532,6 +565,7 @@ static void ingest_chunk(fx_stream *s, int64_t n, const int64_t *d_oid, const in
     s->dup_run.grow(cneed, c0, st);
     if (lead > 0 && c0 > 0) {
         // dups at the head of the chunk follow the previous chunk's last classified object
+        chain_join(s);  // an evicted cluster's size is written by the chain
         k_lead_dups<<<1, 256, 0, st>>>(lead, s->ctr.p, s->live.p, s->s_cid.p, s->s_size.p, s->cl_size.p);
         FX_LAUNCHED();
     }
@@ -705,6 +739,7 @@ int fx_finalize(fx_stream *s, fx_index **out, fx_ingest_report *rep) {
         StreamGuard sg_(s->st);
         cudaStream_t st = s->st;
         const int D = s->cfg.dim;
+        chain_join(s);  // final centroids read the exact sums
         FX_CUDA(cudaMemcpyAsync(s->h_ctr, s->ctr.p, sizeof(int64_t) * C_COUNT, cudaMemcpyDeviceToHost, st));
         FX_CUDA(cudaStreamSynchronize(st));
         if (s->h_ctr[C_ERR]) throw Error{FX_E_INTERNAL, "resolve: candidate list overflow"};
@@ -829,6 +864,7 @@ int fx_stream_counters(fx_stream *s, int64_t *out, int n) {
         StreamGuard sg_(s->st);
         FX_CUDA(cudaMemcpyAsync(s->h_ctr, s->ctr.p, sizeof(int64_t) * C_COUNT, cudaMemcpyDeviceToHost, s->st));
         FX_CUDA(cudaStreamSynchronize(s->st));
+        FX_CUDA(cudaStreamSynchronize(s->st2));  // fold profile counters
         for (int i = 0; i < n && i < C_COUNT; i++) out[i] = s->h_ctr[i];
         if (n > C_COUNT) {
             int64_t pr[24];

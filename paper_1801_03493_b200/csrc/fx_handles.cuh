@@ -103,6 +103,17 @@ struct fx_stream {
     fx::DevBuf<int32_t> f_rank, f_dup, f_ccnt, f_cdup, f_gi;
     fx::DevBuf<float> f_P, f_csum, f_cmax, f_gf;
     fx::DevBuf<double> f_gd;
+    // snapshot tree fold (k_tfold) + lagged exact chain (k_fold on st2)
+    fx::DevBuf<double> S_tree;             // [nslots*D] running sums in the tree fold's order
+    fx::DevBuf<double> s_abs, s_sdev;      // [nslots] sum of member norms; bound on |snapshot - exact centroid|
+    fx::DevBuf<float> tf_cn2;              // [(2B+2) * gx] per-slice ||c||^2 partials
+    fx::DevBuf<int32_t> tf_cnt;            // [2B+2] CTAs done per dirty slot (last-block election)
+    fx::DevBuf<int32_t> cd_meta, cd_off;   // [2][8][2B+3], [2][2B+3] chain descriptors (double buffered)
+    fx::DevBuf<const char *> cd_rows;      // [2][B] member rows of the chain (nullptr: already in S)
+    fx::DevBuf<int64_t> cd_nd;             // [2] dirty slots of the chain
+    cudaStream_t st2 = nullptr;            // the exact float64 chain runs here, one batch behind
+    cudaEvent_t ev_tf[2] = {nullptr, nullptr}, ev_ch[2] = {nullptr, nullptr};
+    bool chain_pending[2] = {false, false};
     fx::DevBuf<int32_t> rowmin;          // [B+1] multi-tile TC screen: min lower bound per row (float bits)
     fx::DevBuf<float> snorm;             // [ld] snapshot column norms (TC screen)
     const char *abase = nullptr;         // feature rows of the current ingest call (TMA tensor map)

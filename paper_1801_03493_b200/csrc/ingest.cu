@@ -349,6 +349,7 @@ struct ResolveArgs {
     const int32_t *sum_slot, *sum_q;
     const float *sum_d1, *sum_e1, *sum_lbr;
     int64_t *h_ring;  // pinned host slot (UVA): counters the host reads two batches later
+    const double *s_sdev;  // per slot: bound on |snapshot centroid - exact centroid| (k_tfold)
     // fast path scratch (k_rfast1 / k_rfast3)
     int32_t *f_rank, *f_dup, *f_ccnt, *f_cdup, *f_gi;
     float *f_P, *f_csum, *f_cmax, *f_gf;
@@ -945,7 +946,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
         A.s_foldpos[sl] = 0;
         A.s_pend[sl] = 0;
         A.s_odcol[sl] = -1;
-        A.s_drift[sl] = 0.0;
+        A.s_drift[sl] = A.s_sdev[sl];  // the snapshot's distance from the exact centroid (k_tfold)
     }
     for (int b = tid; b < B; b += blockDim.x) sh_slot_of[b] = -1;
     __syncthreads();
@@ -2141,12 +2142,14 @@ __global__ void __launch_bounds__(RF_T) k_rfast1(ResolveArgs A) {
         }
         const int sl = A.snap_slot[gg];
         const float cn = sqrtf(A.s_cn2[sl]) * 1.00001f;
-        drift = c > 0 ? drift_avg(0.f, A.s_nfeat[sl], su, c, cn, mx) : 0.f;
+        const float d0 = __double2float_ru(A.s_sdev[sl]);  // k_resolve's prologue: s_drift = s_sdev
+        drift = c > 0 ? drift_avg(d0, A.s_nfeat[sl], su, c, cn, mx) : d0;
         A.f_gi[gg * 4 + 0] = c;
         A.f_gi[gg * 4 + 1] = d;
         A.f_gf[gg * 4 + 0] = drift;
         A.f_gf[gg * 4 + 1] = mx;
         A.f_gf[gg * 4 + 2] = cn;
+        A.f_gf[gg * 4 + 3] = d0;
     }
     // the two largest end-of-batch drifts over the live (= snapshot) slots
     double m1 = gg < nsnap ? (double)drift : -1.0, m2 = -1.0;
@@ -2267,7 +2270,8 @@ __global__ void __launch_bounds__(RF_T) k_rfast3(ResolveArgs A) {
         const int sl = A.snap_slot[g];
         const int nf0 = A.s_nfeat[sl];
         const float ub0 = (A.sum_d1[p] + A.sum_e1[p]) * 1.000001f + 1e-30f;
-        const double ub = (double)ub0 + (double)drift_avg(0.f, nf0, P, i, A.f_gf[g * 4 + 2], A.f_gf[g * 4 + 1]);
+        const double ub =
+            (double)ub0 + (double)drift_avg(A.f_gf[g * 4 + 3], nf0, P, i, A.f_gf[g * 4 + 2], A.f_gf[g * 4 + 1]);
         const float lbr = A.sum_lbr[p];
         const float lbr2 = lbr - fabsf(lbr) * 1e-6f - 1e-30f;
         const double md = g == md1g ? md2 : md1;
@@ -2317,7 +2321,7 @@ __global__ void __launch_bounds__(RF_T) k_rfast3(ResolveArgs A) {
             A.dirty_off[di] = A.f_gi[gg * 4 + 3];
             A.s_cn2[sl] = 0.f;  // the fold re-accumulates ||c||^2
         } else {
-            A.s_drift[sl] = 0.0;
+            A.s_drift[sl] = A.s_sdev[sl];
             A.s_pend[sl] = 0;
         }
     }
@@ -2394,23 +2398,157 @@ __device__ __forceinline__ void fbar_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
 }
 
+// Chain descriptor: what k_tfold hands the lagged exact chain for one batch
+// (double buffered: batch b uses buffer b % 2).  meta rows: slot, featured
+// count after the batch, fold position, seed position, evicted, cluster id,
+// size.  rows: the members to add in stream order (nullptr: already in S --
+// folded by the resolve's exact path).
+enum CdMeta { CD_SLOT = 0, CD_NFEAT, CD_FP, CD_SP, CD_EV, CD_CID, CD_SIZE, CD_NMETA = 8 };
+struct ChainDesc {
+    const int64_t *nd;
+    const int32_t *meta;  // [CD_NMETA][ldm]
+    int ldm;
+    const int32_t *off;
+    const char *const *rows;
+};
+
+// ---------------------------------------------------------------------------
+// K2c': snapshot tree fold (main stream, right after the resolve).  The next
+// batch's screen needs the FP32 snapshot of every moved centroid, not the
+// reference's sequential float64 sum: each dirty slot's rows are added in a
+// fixed tree order into S_tree (float64), C32 = fp32(S_tree / n), and the
+// distance between that centroid and the reference's exact one is bounded
+// (Higham: any summation order of n terms is within gamma_n sum |x_i| of the
+// real sum, coordinate-wise, so the two float64 sums differ by at most
+// 2 gamma_n sum_i ||x_i|| in 2-norm) and handed to the resolve as the slot's
+// starting drift.  The reference's own sum (clustering.py:56-59) is still
+// computed bit for bit -- by the chain below, one batch behind, off the
+// critical path.  This kernel also writes the chain's descriptor.
+// grid (ceil(D/32), rows): row 0 takes dirty[0] (the largest slot), the
+// others stride over the rest; 8 warps x 4 interleaved accumulators per
+// 32-column slice, combined in a fixed order (deterministic).
+// ---------------------------------------------------------------------------
+constexpr int TF_T = 256;
+
 template <typename T>
-__global__ void __launch_bounds__(FOLD_THREADS) k_fold(int D, int64_t c0, const int64_t *__restrict__ ctr,
-                                                      const int32_t *__restrict__ dirty, const int32_t *__restrict__ dirty_off,
-                                                      const int32_t *__restrict__ pend_list, const char *const *__restrict__ frow,
-                                                      double *__restrict__ S, float *__restrict__ C32,
-                                                      const int32_t *__restrict__ s_nfeat, const int32_t *__restrict__ s_foldpos,
-                                                      const int32_t *__restrict__ s_seedpos, const int32_t *__restrict__ s_evicted,
-                                                      const int32_t *__restrict__ s_cid, const int32_t *__restrict__ s_size,
-                                                      float *__restrict__ s_cn2, double *__restrict__ fcent,
-                                                      int32_t *__restrict__ cl_nfeat, int32_t *__restrict__ cl_size,
-                                                      long long *__restrict__ fprof) {
+__global__ void __launch_bounds__(TF_T) k_tfold(int D, int64_t c0, int B, const int64_t *__restrict__ ctr,
+                                                const int32_t *__restrict__ dirty, const int32_t *__restrict__ dirty_off,
+                                                const int32_t *__restrict__ pend_list, const char *const *__restrict__ frow,
+                                                const float *__restrict__ fnorm, const int32_t *__restrict__ s_nfeat,
+                                                const int32_t *__restrict__ s_foldpos, const int32_t *__restrict__ s_seedpos,
+                                                const int32_t *__restrict__ s_evicted, const int32_t *__restrict__ s_cid,
+                                                const int32_t *__restrict__ s_size, double *__restrict__ S_tree,
+                                                float *__restrict__ C32, float *__restrict__ s_cn2,
+                                                double *__restrict__ s_abs, double *__restrict__ s_sdev,
+                                                float *__restrict__ tf_cn2, int32_t *__restrict__ tf_cnt,
+                                                int64_t *__restrict__ cd_nd, int32_t *__restrict__ cd_meta, int ldm,
+                                                int32_t *__restrict__ cd_off, const char **__restrict__ cd_rows) {
     pdl_enter();
+    __shared__ double part[TF_T / 32][32];
+    __shared__ double s_fn[TF_T / 32];
+    __shared__ int s_last;
+    const int nd = (int)ctr[C_NDIRTY];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int gx = gridDim.x;
+    const int k = blockIdx.x * 32 + lane;
+    if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) {
+        *cd_nd = nd;
+        cd_off[nd] = dirty_off[nd];
+    }
+    const int dstart = blockIdx.y, dstep = blockIdx.y == 0 ? nd : (int)gridDim.y - 1;
+    for (int di = dstart; di < nd; di += dstep) {
+        const int slot = dirty[di];
+        const int j0 = dirty_off[di], j1 = dirty_off[di + 1];
+        const int fp = s_foldpos[slot], sp = s_seedpos[slot], ev = s_evicted[slot];
+        const int n = s_nfeat[slot];
+        if (blockIdx.x == 0) {  // the chain's descriptor of this slot
+            for (int j = j0 + tid; j < j1; j += TF_T) {
+                const int p = pend_list[j];
+                cd_rows[j] = p >= fp ? frow[c0 + p] : nullptr;
+            }
+            if (tid == 0) {
+                cd_off[di] = j0;
+                cd_meta[CD_SLOT * ldm + di] = slot;
+                cd_meta[CD_NFEAT * ldm + di] = n;
+                cd_meta[CD_FP * ldm + di] = fp;
+                cd_meta[CD_SP * ldm + di] = sp;
+                cd_meta[CD_EV * ldm + di] = ev;
+                cd_meta[CD_CID * ldm + di] = s_cid[slot];
+                cd_meta[CD_SIZE * ldm + di] = s_size[slot];
+            }
+        }
+        if (ev) continue;  // evicted: no snapshot (its exact centroid comes from the chain)
+        const bool fresh = sp >= 0;  // seeded in this batch: S_tree starts empty
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        double fsum = 0.0;
+        int r = 0;
+        for (int j = j0 + wid; j < j1; j += TF_T / 32, r++) {
+            const int p = pend_list[j];
+            const T *row = (const T *)frow[c0 + p];
+            if (k < D) acc[r & 3] = dadd(acc[r & 3], to_d(row[k]));
+            if (blockIdx.x == 0 && lane == 0) fsum += (double)fnorm[c0 + p];
+        }
+        part[wid][lane] = dadd(dadd(acc[0], acc[1]), dadd(acc[2], acc[3]));
+        if (blockIdx.x == 0 && lane == 0) s_fn[wid] = fsum;
+        __syncthreads();
+        if (wid == 0) {
+            double t = part[0][lane];
+#pragma unroll
+            for (int w = 1; w < TF_T / 32; w++) t = dadd(t, part[w][lane]);
+            float c2 = 0.f;
+            if (k < D) {
+                const double sum = fresh ? t : dadd(S_tree[(int64_t)slot * D + k], t);
+                S_tree[(int64_t)slot * D + k] = sum;
+                const float c32 = (float)ddiv(sum, (double)n);
+                C32[(int64_t)slot * D + k] = c32;
+                c2 = c32 * c32;
+            }
+            c2 = warp_sum(c2);
+            if (lane == 0) {
+                tf_cn2[(int64_t)di * gx + blockIdx.x] = c2;
+                if (blockIdx.x == 0) {
+                    double fs = 0.0;
+                    for (int w = 0; w < TF_T / 32; w++) fs += s_fn[w];
+                    // fp32 norms: relative error < 1e-6, rounded up below
+                    s_abs[slot] = (fresh ? 0.0 : s_abs[slot]) + fs * (1.0 + 1e-5);
+                }
+                __threadfence();
+                s_last = atomicAdd(&tf_cnt[di], 1) == gx - 1;
+            }
+        }
+        __syncthreads();
+        if (s_last && tid == 0) {  // last slice of this slot: ||C32||^2 in slice order, drift bound
+            __threadfence();
+            float c2 = 0.f;
+            for (int x = 0; x < gx; x++) c2 += __ldcg(&tf_cn2[(int64_t)di * gx + x]);
+            s_cn2[slot] = c2;
+            const double u = 1.1102230246251565e-16, nn = (double)n;
+            const double gam = nn * u / (1.0 - nn * u);
+            const double sa = __ldcg(&s_abs[slot]);
+            s_sdev[slot] = (2.0 * gam * sa / nn + 4.0 * u * sqrt((double)c2) * 1.01) * 1.01 + 1e-300;
+            tf_cnt[di] = 0;
+        }
+        __syncthreads();
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K2c: the reference's float64 running sums, bit for bit (clustering.py:56-59),
+// one batch behind on the engine's second stream: for each slot of the
+// batch's chain descriptor, its members are added in stream order, and an
+// evicted slot's final centroid (S / n, sealed at eviction) is recorded.
+// The resolve of the next batch waits for this only where it reads S (its
+// exact path); the screen and the fast path never do.
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(FOLD_THREADS) k_fold(int D, ChainDesc cd, double *__restrict__ S,
+                                                      double *__restrict__ fcent, int32_t *__restrict__ cl_nfeat,
+                                                      int32_t *__restrict__ cl_size, long long *__restrict__ fprof) {
     constexpr int R = fold_rows<T>();
     extern __shared__ __align__(16) unsigned char fold_raw[];
     T *ring = (T *)fold_raw;                                                // [NS][R][FD]
     __shared__ __align__(8) uint64_t full[FOLD_NS], empty[FOLD_NS];
-    const int nd = (int)ctr[C_NDIRTY];
+    const int nd = (int)*cd.nd;
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     const int k = blockIdx.x * FD + lane;
     // barrier phases run on across the slots this CTA folds: global stage G
@@ -2421,13 +2559,13 @@ __global__ void __launch_bounds__(FOLD_THREADS) k_fold(int D, int64_t c0, const 
     }
     __syncthreads();
     int J0 = 0;
-    // grid row 0 folds only dirty[0] -- the slot with the most pending rows
-    // (the resolve puts it first), so its long chain starts at once; the
+    // grid row 0 folds only the first slot -- the one with the most pending
+    // rows (the resolve puts it first), so its long chain starts at once; the
     // other rows share the remaining slots
     const int dstart = blockIdx.y, dstep = blockIdx.y == 0 ? nd : (int)gridDim.y - 1;
     for (int di = dstart; di < nd; di += dstep) {
-        const int slot = dirty[di];
-        const int p0 = dirty_off[di], p1 = dirty_off[di + 1];
+        const int slot = cd.meta[CD_SLOT * cd.ldm + di];
+        const int p0 = cd.off[di], p1 = cd.off[di + 1];
         const int nst = (p1 - p0 + R - 1) / R;
         if (wid == 0) {
             // consumer: the float64 chain, one dimension per lane.  Every row is
@@ -2435,7 +2573,7 @@ __global__ void __launch_bounds__(FOLD_THREADS) k_fold(int D, int64_t c0, const 
             // seed row then lands exactly: -0 + v = v, like the reference's
             // sum = feature.copy()), skipped rows hold -0.0 (x + -0 = x for
             // every x), so the chain is one dadd per row (~18 cycles on B200).
-            const int fp = s_foldpos[slot], sp = s_seedpos[slot];
+            const int fp = cd.meta[CD_FP * cd.ldm + di], sp = cd.meta[CD_SP * cd.ldm + di];
             double acc = (sp >= 0 && sp >= fp) ? -0.0 : (k < D ? S[(int64_t)slot * D + k] : 0.0);
             const bool prof = fprof && blockIdx.x == 0 && blockIdx.y == 0 && lane == 0;
             long long tw = 0, tc = 0, t0 = prof ? clock64() : 0;
@@ -2462,21 +2600,15 @@ __global__ void __launch_bounds__(FOLD_THREADS) k_fold(int D, int64_t c0, const 
                 atomicAdd((unsigned long long *)&fprof[3], (unsigned long long)(p1 - p0));
                 atomicAdd((unsigned long long *)&fprof[4], 1ull);
             }
-            float c2 = 0.f;
             if (k < D) {
                 S[(int64_t)slot * D + k] = acc;
-                const double cen = ddiv(acc, (double)s_nfeat[slot]);
-                const float c32 = (float)cen;
-                C32[(int64_t)slot * D + k] = c32;
-                c2 = c32 * c32;
-                if (s_evicted[slot]) fcent[(int64_t)s_cid[slot] * D + k] = cen;
-            }
-            c2 = warp_sum(c2);  // ||c||^2 partial of this slice
-            if (lane == 0) {
-                atomicAdd(&s_cn2[slot], c2);
-                if (blockIdx.x == 0 && s_evicted[slot]) {
-                    cl_nfeat[s_cid[slot]] = s_nfeat[slot];
-                    cl_size[s_cid[slot]] = s_size[slot];
+                if (cd.meta[CD_EV * cd.ldm + di]) {  // sealed at eviction: its final centroid
+                    const int cid = cd.meta[CD_CID * cd.ldm + di];
+                    fcent[(int64_t)cid * D + k] = ddiv(acc, (double)cd.meta[CD_NFEAT * cd.ldm + di]);
+                    if (k == 0) {
+                        cl_nfeat[cid] = cd.meta[CD_NFEAT * cd.ldm + di];
+                        cl_size[cid] = cd.meta[CD_SIZE * cd.ldm + di];
+                    }
                 }
             }
         } else {
@@ -2485,14 +2617,11 @@ __global__ void __launch_bounds__(FOLD_THREADS) k_fold(int D, int64_t c0, const 
             // (lane l loads rows l, l+32, ...: coalesced, independent), so a
             // refill costs only the copies once the consumer releases it.
             const int w = wid - 1;
-            const int fp = s_foldpos[slot];
             auto gather = [&](int j, const T **rp) {
                 const int rbase = p0 + j * R, nr = min(R, p1 - rbase);
-                int bq[R / 32];
 #pragma unroll
-                for (int c = 0; c < R / 32; c++) bq[c] = (j < nst && c * 32 + lane < nr) ? pend_list[rbase + c * 32 + lane] : -1;
-#pragma unroll
-                for (int c = 0; c < R / 32; c++) rp[c] = bq[c] >= fp ? (const T *)frow[c0 + bq[c]] : nullptr;
+                for (int c = 0; c < R / 32; c++)
+                    rp[c] = (j < nst && c * 32 + lane < nr) ? (const T *)cd.rows[rbase + c * 32 + lane] : nullptr;
             };
             const T *rp[R / 32];
             int j = (w - J0 % FOLD_NS + FOLD_NS) % FOLD_NS;
@@ -2728,6 +2857,7 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
     const bool rowpass = sizeof(T) == 4 && D % 4 == 0 && D <= 2048 && s->rows_aligned16;
     for (int64_t c0 = c_begin, B = 0; c0 < c_end; c0 += B, bi++) {
         const auto h0 = hclock::now();
+        const int cbuf = (int)(s->batch_no & 1);  // chain descriptor buffer of this batch
         // the drift bound grows like (batch size / objects so far): keep batches
         // at <= 1/4 of the stream's age so young clusters stay decidable by bounds
         const int64_t age = std::max<int64_t>(c0, 0);
@@ -2895,6 +3025,7 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             A.f_gi = s->f_gi.p;
             A.f_gf = s->f_gf.p;
             A.f_gd = s->f_gd.p;
+            A.s_sdev = s->s_sdev.p;
             // fast path first (the common all-certain batch over the whole
             // grid); k_resolve returns at once when it committed
             static const bool nofast = getenv("FOCUS_B200_NOFAST") && atoi(getenv("FOCUS_B200_NOFAST"));
@@ -2914,6 +3045,9 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
                 FX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
                 cur = smem;
             }
+            // its exact path reads the reference's float64 sums: the previous
+            // batch's chain must be done (it ran alongside this batch's screen)
+            if (s->chain_pending[cbuf ^ 1]) FX_CUDA(cudaStreamWaitEvent(st, s->ev_ch[cbuf ^ 1], 0));
             launch_pdl(kern, dim3(1), dim3(RS_THREADS), smem, st, A);
             FX_LAUNCHED();
         }
@@ -2936,6 +3070,7 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             const int64_t need = known + 3 * (int64_t)s->B;
             if (need > s->cl_cap) {
                 FX_CUDA(cudaStreamSynchronize(st));
+                FX_CUDA(cudaStreamSynchronize(s->st2));  // the chain writes fcent / cl_nfeat / cl_size
                 int64_t cap = std::max<int64_t>(need, s->cl_cap * 2);
                 s->fcent.grow((size_t)cap * D, (size_t)s->cl_cap * D, st);
                 s->cl_nfeat.grow(cap, s->cl_cap, st);
@@ -2948,6 +3083,7 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
         s->t_ms[10] += hms(h2, h3);
         if (s->debug_check) {  // FOCUS_B200_CHECK=1: host-side invariants of the resolve output
             FX_CUDA(cudaStreamSynchronize(st));
+            FX_CUDA(cudaStreamSynchronize(s->st2));
             int64_t hc[C_COUNT];
             FX_CUDA(cudaMemcpy(hc, s->ctr.p, sizeof(hc), cudaMemcpyDeviceToHost));
             const int nd = (int)hc[C_NDIRTY];
@@ -2995,27 +3131,41 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
                 std::copy(srow.begin(), srow.end(), chk_expect.begin() + (size_t)i * D);
             }
         }
-        // 5. fold (persistent grid over the batch's dirty slots)
+        // 5. snapshot tree fold (main stream) + the exact chain one batch behind (st2)
         {
             s->tstart(3);
-            // enough CTA rows for the usual dirty count; the kernel loops over the rest
+            const int buf = cbuf;
+            const int64_t gxt = cdiv(D, 32);
+            const int64_t gyt = std::max<int64_t>(8, std::min<int64_t>(2 * (int64_t)B + 1, (148 * 8) / gxt));
+            const int ldm = 2 * s->B + 3;
+            int32_t *meta = s->cd_meta.p + (size_t)buf * CD_NMETA * ldm;
+            int32_t *coff = s->cd_off.p + (size_t)buf * ldm;
+            const char **crows = s->cd_rows.p + (size_t)buf * s->B;
+            launch_pdl(k_tfold<T>, dim3((unsigned)gxt, (unsigned)gyt), dim3(TF_T), 0, st, D, c0, B, s->ctr.p, s->dirty.p,
+                       s->dirty_off.p, s->pend_list.p, s->frow.p, s->fnorm.p, s->s_nfeat.p, s->s_foldpos.p,
+                       s->s_seedpos.p, s->s_evicted.p, s->s_cid.p, s->s_size.p, s->S_tree.p, s->C32.p, s->s_cn2.p,
+                       s->s_abs.p, s->s_sdev.p, s->tf_cn2.p, s->tf_cnt.p, s->cd_nd.p + buf, meta, ldm, coff, crows);
+            FX_LAUNCHED();
+            s->tstop();
+            FX_CUDA(cudaEventRecord(s->ev_tf[buf], st));
+            FX_CUDA(cudaStreamWaitEvent(s->st2, s->ev_tf[buf], 0));
             const int64_t gx = cdiv(D, FD);
             const int64_t gy = std::max<int64_t>(8, std::min<int64_t>(2 * (int64_t)B + 1, (148 * 12) / gx));
-            dim3 grid((unsigned)gx, (unsigned)gy);
             static bool fold_attr[64] = {};
             if (!fold_attr[dev_slot()]) {
                 FX_CUDA(cudaFuncSetAttribute(k_fold<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fold_smem<T>()));
                 fold_attr[dev_slot()] = true;
             }
-            launch_pdl(k_fold<T>, dim3(grid), dim3(FOLD_THREADS), fold_smem<T>(), st, D, c0, s->ctr.p, s->dirty.p, s->dirty_off.p, s->pend_list.p, s->frow.p,
-                                            s->S.p, s->C32.p, s->s_nfeat.p, s->s_foldpos.p, s->s_seedpos.p,
-                                            s->s_evicted.p, s->s_cid.p, s->s_size.p, s->s_cn2.p, s->fcent.p,
-                                            s->cl_nfeat.p, s->cl_size.p, (long long *)(s->prof.p + 16));
+            ChainDesc cd{s->cd_nd.p + buf, meta, ldm, coff, crows};
+            k_fold<T><<<dim3((unsigned)gx, (unsigned)gy), FOLD_THREADS, fold_smem<T>(), s->st2>>>(
+                D, cd, s->S.p, s->fcent.p, s->cl_nfeat.p, s->cl_size.p, (long long *)(s->prof.p + 16));
             FX_LAUNCHED();
-            s->tstop();
+            FX_CUDA(cudaEventRecord(s->ev_ch[buf], s->st2));
+            s->chain_pending[buf] = true;
         }
         if (s->debug_check) {
             FX_CUDA(cudaStreamSynchronize(st));
+            FX_CUDA(cudaStreamSynchronize(s->st2));
             std::vector<double> srow(D);
             int nbad = 0;
             for (size_t i = 0; i < chk_slots.size(); i++) {
