@@ -342,6 +342,22 @@ int fx_session_reset(fx_session *ss);
 int64_t fx_session_gt_total(fx_session *ss);
 
 /* ------------------------------------------------------------------------ */
+/* Tuner grid evaluation: _GridEvaluator._positions (tuner.py:243-256)         */
+/* ------------------------------------------------------------------------ */
+
+/* 0-based position of each queried class in every object's full ranked
+ * output of one profile (classify(...).classes(), classifiers.py:136-149):
+ * rank from the object's SeedSequence/PCG64 draw (seed, oid, 0) and the
+ * profile's rank thresholds (n_thr = output length - 1; ground_truth: rank
+ * 1), then the class's index in the emitted class's confusion order --
+ * inv[e * v1 + c] (classes encoded, OTHER = V; -1 = absent -> position 0).
+ * emitted[n]: the profile's emitted class of each object's true class.
+ * out_pos[n_classes * n], class-major.  Host buffers. */
+int fx_rank_positions(int32_t device, int64_t n, const int64_t *oids, const int32_t *emitted, uint64_t seed,
+                      int32_t ground_truth, int32_t n_thr, const uint64_t *thresholds, const int32_t *inv,
+                      int32_t v1, int32_t n_classes, const int32_t *classes, int32_t *out_pos);
+
+/* ------------------------------------------------------------------------ */
 /* Misc                                                                       */
 /* ------------------------------------------------------------------------ */
 

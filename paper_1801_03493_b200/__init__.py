@@ -15,6 +15,6 @@ from .index import IndexHeader, TopKIndex, build, load, lookup, save
 from .ingest import DEFAULT_PIXEL_EPS, IngestReport, StreamHeader, ingest_arrays, ingest_stream, pixel_diff
 from .query import QueryRequest, QueryResult, QuerySession
 from ._lib import set_device
-from . import streamio
+from . import streamio, tuner
 
 __version__ = "0.1.0"

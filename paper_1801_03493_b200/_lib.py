@@ -120,6 +120,9 @@ _SIGS = {
     "fx_session_needed": (ctypes.c_int, [vp, c_i32p, c_i64p]),
     "fx_session_seen_open": (ctypes.c_int, [vp, c_i32p]),
     "fx_session_seen_close": (ctypes.c_int, [vp, ctypes.c_int32]),
+    "fx_rank_positions": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int64, c_i64p, c_i32p, ctypes.c_uint64, ctypes.c_int32,
+                                         ctypes.c_int32, c_u64p, c_i32p, ctypes.c_int32, ctypes.c_int32, c_i32p,
+                                         c_i32p]),
     "fx_index_reps": (ctypes.c_int, [vp, c_i64p]),
     "fx_session_gt_total": (ctypes.c_int64, [vp]),
 }

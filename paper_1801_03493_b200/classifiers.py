@@ -23,6 +23,7 @@ from functools import lru_cache
 
 import numpy as np
 
+from ._reftypes import shared
 from .core import OTHER_CLASS, DetectedObject, encode_class
 from .errors import DataError, DimensionMismatch, EmptyHistogram, MissingTrueClass, UsageError
 
@@ -95,6 +96,10 @@ class ClassifierProfile:
         if self.class_set is None or class_id in self.class_set:
             return class_id
         return OTHER_CLASS
+
+
+RankModel = shared("classifiers", "RankModel", RankModel)
+ClassifierProfile = shared("classifiers", "ClassifierProfile", ClassifierProfile)
 
 
 def make_default_profiles(vocab: int = 1000) -> dict:

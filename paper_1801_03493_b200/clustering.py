@@ -11,6 +11,8 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
+from ._reftypes import shared
+
 
 @dataclass
 class Cluster:
@@ -29,3 +31,6 @@ class Cluster:
 
     def size(self) -> int:
         return len(self.member_object_ids)
+
+
+Cluster = shared("clustering", "Cluster", Cluster)

@@ -262,7 +262,10 @@ int fx_stream_create(const fx_stream_config *cfg, fx_stream **out) {
                 s->s_abs.reserve(ns);
                 s->s_sdev.reserve(ns);
                 FX_CUDA(cudaMemsetAsync(s->s_sdev.p, 0, sizeof(double) * ns, s->st));
-                const size_t nd = 2 * (size_t)B + 3, gx = (size_t)cdiv(D, 32);
+                const size_t nd = 2 * (size_t)B + 3, gx = (size_t)cdiv(D, 128);
+                s->tf_part.reserve(16 * (size_t)D + 16);
+                s->tf_bcnt.reserve(gx);
+                FX_CUDA(cudaMemsetAsync(s->tf_bcnt.p, 0, sizeof(int32_t) * gx, s->st));
                 s->tf_cn2.reserve(nd * gx);
                 s->tf_cnt.reserve(nd);
                 FX_CUDA(cudaMemsetAsync(s->tf_cnt.p, 0, sizeof(int32_t) * nd, s->st));
@@ -628,11 +631,16 @@ static int ingest_common(fx_stream *s, int64_t n, const int64_t *object_ids, con
         const bool compact = flags & FX_FEATS_COMPACT;
         if (device) {
             ingest_chunk(s, n, object_ids, frame_ids, sigs, (const char *)feats, true_class, topk, compact);
-        } else if (!compact) {
+        } else {
             // host buffers: the copies run on a side stream in chunks of CH
             // objects and the engine consumes chunk k as soon as it has landed,
             // so PCIe transfer of later chunks overlaps the ingest of earlier
-            // ones (pinned host memory makes the copies truly asynchronous)
+            // ones (pinned host memory makes the copies truly asynchronous).
+            // Compact features (FX_FEATS_COMPACT: rows of the classified
+            // objects only, as a cheap CNN emits them after pixel
+            // differencing) need the duplicate flags first to place the
+            // chunk boundaries in the row array: the small per-object arrays
+            // go up first and K0 runs on them.
             const int64_t CH = std::max<int64_t>(4096, ((int64_t)1 << 30) / std::max<int64_t>(1, (int64_t)D * s->esize));
             const int nch = (int)cdiv(n, CH);
             DevBuf<int64_t> o, f;
@@ -643,11 +651,30 @@ static int ingest_common(fx_stream *s, int64_t n, const int64_t *object_ids, con
             g.reserve((size_t)n * std::max(S, 1));
             if (true_class) tc.reserve(n);
             if (topk) tk.reserve((size_t)n * K);
+            std::vector<int64_t> row0(nch + 1, 0);  // first feature row of each chunk
+            if (compact) {
+                h2d(o.p, object_ids, n, st);
+                h2d(f.p, frame_ids, n, st);
+                h2d(g.p, sigs, n * S, st);
+                DevBuf<uint8_t> dup;
+                dup.reserve(n);
+                launch_dup_flags(s, n, f.p, g.p, dup.p);
+                std::vector<uint8_t> hd(n);
+                d2h(hd.data(), dup.p, n, st);
+                FX_CUDA(cudaStreamSynchronize(st));
+                for (int c = 0; c < nch; c++) {
+                    int64_t r = 0;
+                    for (int64_t i = c * CH, e = std::min<int64_t>(n, (c + 1) * CH); i < e; i++) r += hd[i] ? 0 : 1;
+                    row0[c + 1] = row0[c] + r;
+                }
+            } else {
+                for (int c = 0; c < nch; c++) row0[c + 1] = std::min<int64_t>(n, (int64_t)(c + 1) * CH);
+            }
             // feature rows stay resident until finalize (the reference retains
             // member features until seal, clustering.py:71-83)
             auto *fb = new DevBuf<char>();
             s->owned_feats.push_back(fb);
-            fb->reserve((size_t)n * D * s->esize);
+            fb->reserve((size_t)std::max<int64_t>(1, row0[nch]) * D * s->esize);
             cudaStream_t cst = nullptr;
             FX_CUDA(cudaStreamCreateWithFlags(&cst, cudaStreamNonBlocking));
             std::vector<cudaEvent_t> ev(nch + 1, nullptr);
@@ -655,23 +682,28 @@ static int ingest_common(fx_stream *s, int64_t n, const int64_t *object_ids, con
                 FX_CUDA(cudaEventCreateWithFlags(&ev[nch], cudaEventDisableTiming));
                 FX_CUDA(cudaEventRecord(ev[nch], st));  // the allocations above are ordered before the copies
                 FX_CUDA(cudaStreamWaitEvent(cst, ev[nch], 0));
+                const size_t rb = (size_t)D * s->esize;
                 for (int c = 0; c < nch; c++) {
                     const int64_t a = c * CH, m = std::min<int64_t>(CH, n - a);
-                    h2d(o.p + a, object_ids + a, m, cst);
-                    h2d(f.p + a, frame_ids + a, m, cst);
-                    h2d(g.p + a * S, sigs + a * S, m * S, cst);
+                    if (!compact) {
+                        h2d(o.p + a, object_ids + a, m, cst);
+                        h2d(f.p + a, frame_ids + a, m, cst);
+                        h2d(g.p + a * S, sigs + a * S, m * S, cst);
+                    }
                     if (true_class) h2d(tc.p + a, true_class + a, m, cst);
                     if (topk) h2d(tk.p + a * K, topk + a * K, m * K, cst);
-                    FX_CUDA(cudaMemcpyAsync(fb->p + (size_t)a * D * s->esize, (const char *)feats + (size_t)a * D * s->esize,
-                                            (size_t)m * D * s->esize, cudaMemcpyHostToDevice, cst));
+                    const int64_t r0 = row0[c], nr = row0[c + 1] - row0[c];
+                    if (nr > 0)
+                        FX_CUDA(cudaMemcpyAsync(fb->p + (size_t)r0 * rb, (const char *)feats + (size_t)r0 * rb,
+                                                (size_t)nr * rb, cudaMemcpyHostToDevice, cst));
                     FX_CUDA(cudaEventCreateWithFlags(&ev[c], cudaEventDisableTiming));
                     FX_CUDA(cudaEventRecord(ev[c], cst));
                 }
                 for (int c = 0; c < nch; c++) {
                     const int64_t a = c * CH, m = std::min<int64_t>(CH, n - a);
                     FX_CUDA(cudaStreamWaitEvent(st, ev[c], 0));
-                    ingest_chunk(s, m, o.p + a, f.p + a, g.p + a * S, fb->p + (size_t)a * D * s->esize,
-                                 true_class ? tc.p + a : nullptr, topk ? tk.p + a * K : nullptr, 0);
+                    ingest_chunk(s, m, o.p + a, f.p + a, g.p + a * S, fb->p + (size_t)row0[c] * rb,
+                                 true_class ? tc.p + a : nullptr, topk ? tk.p + a * K : nullptr, compact ? 1 : 0);
                 }
                 FX_CUDA(cudaStreamSynchronize(st));
             } catch (...) {
@@ -683,40 +715,6 @@ static int ingest_common(fx_stream *s, int64_t n, const int64_t *object_ids, con
             }
             for (auto e : ev) cudaEventDestroy(e);
             FX_CUDA(cudaStreamDestroy(cst));
-        } else {
-            DevBuf<int64_t> o, f;
-            DevBuf<double> g;
-            DevBuf<int32_t> tc, tk;
-            o.reserve(n);
-            f.reserve(n);
-            g.reserve((size_t)n * std::max(S, 1));
-            h2d(o.p, object_ids, n, st);
-            h2d(f.p, frame_ids, n, st);
-            h2d(g.p, sigs, n * S, st);
-            if (true_class) {
-                tc.reserve(n);
-                h2d(tc.p, true_class, n, st);
-            }
-            if (topk) {
-                tk.reserve((size_t)n * K);
-                h2d(tk.p, topk, n * K, st);
-            }
-            // caller passes only non-dup rows: count them on the device first
-            DevBuf<uint8_t> dup;
-            dup.reserve(n);
-            launch_dup_flags(s, n, f.p, g.p, dup.p);
-            std::vector<uint8_t> hd(n);
-            d2h(hd.data(), dup.p, n, st);
-            FX_CUDA(cudaStreamSynchronize(st));
-            int64_t rows = 0;
-            for (int64_t i = 0; i < n; i++) rows += hd[i] ? 0 : 1;
-            auto *fb = new DevBuf<char>();
-            s->owned_feats.push_back(fb);
-            fb->reserve((size_t)rows * D * s->esize);
-            if (rows > 0)
-                FX_CUDA(cudaMemcpyAsync(fb->p, feats, (size_t)rows * D * s->esize, cudaMemcpyHostToDevice, st));
-            ingest_chunk(s, n, o.p, f.p, g.p, fb->p, true_class ? tc.p : nullptr, topk ? tk.p : nullptr, compact);
-            FX_CUDA(cudaStreamSynchronize(st));
         }
     })
 }

@@ -108,6 +108,8 @@ struct fx_stream {
     fx::DevBuf<double> s_abs, s_sdev;      // [nslots] sum of member norms; bound on |snapshot - exact centroid|
     fx::DevBuf<float> tf_cn2;              // [(2B+2) * gx] per-slice ||c||^2 partials
     fx::DevBuf<int32_t> tf_cnt;            // [2B+2] CTAs done per dirty slot (last-block election)
+    fx::DevBuf<double> tf_part;            // [TF_SPLIT * D + TF_SPLIT] row-chunk partials of the largest slot
+    fx::DevBuf<int32_t> tf_bcnt;           // [gx] row chunks done per column slice
     fx::DevBuf<int32_t> cd_meta, cd_off;   // [2][8][2B+3], [2][2B+3] chain descriptors (double buffered)
     fx::DevBuf<const char *> cd_rows;      // [2][B] member rows of the chain (nullptr: already in S)
     fx::DevBuf<int64_t> cd_nd;             // [2] dirty slots of the chain

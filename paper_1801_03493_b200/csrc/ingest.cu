@@ -439,8 +439,9 @@ __device__ double exact_dist(const ResolveArgs &A, int b, int slot, const int32_
         }
         __syncthreads();
         const int nm = s_nm;
+        const bool fresh = sp >= fp;  // seeded inside [fp, b): the seed row starts the sum
         for (int k = threadIdx.x; k < D; k += blockDim.x) {
-            double s = Sj[k];
+            double s = fresh ? -0.0 : Sj[k];
             for (int i = 0; i < nm; i++) {
                 const int p = mlist[i];
                 double f = to_d(((const T *)A.frow[A.c0 + p])[k]);
@@ -2428,7 +2429,7 @@ struct ChainDesc {
 // others stride over the rest; 8 warps x 4 interleaved accumulators per
 // 32-column slice, combined in a fixed order (deterministic).
 // ---------------------------------------------------------------------------
-constexpr int TF_T = 256;
+constexpr int TF_T = 512, TF_W = TF_T / 32, TF_C = 128, TF_SPLIT = 16;
 
 template <typename T>
 __global__ void __launch_bounds__(TF_T) k_tfold(int D, int64_t c0, int B, const int64_t *__restrict__ ctr,
@@ -2441,32 +2442,40 @@ __global__ void __launch_bounds__(TF_T) k_tfold(int D, int64_t c0, int B, const 
                                                 float *__restrict__ C32, float *__restrict__ s_cn2,
                                                 double *__restrict__ s_abs, double *__restrict__ s_sdev,
                                                 float *__restrict__ tf_cn2, int32_t *__restrict__ tf_cnt,
+                                                double *__restrict__ tf_part, int32_t *__restrict__ tf_bcnt,
                                                 int64_t *__restrict__ cd_nd, int32_t *__restrict__ cd_meta, int ldm,
                                                 int32_t *__restrict__ cd_off, const char **__restrict__ cd_rows) {
     pdl_enter();
-    __shared__ double part[TF_T / 32][32];
-    __shared__ double s_fn[TF_T / 32];
+    __shared__ double part[TF_W][TF_C];
+    __shared__ double s_fn[TF_W];
+    __shared__ float s_c2[TF_W];
     __shared__ int s_last;
     const int nd = (int)ctr[C_NDIRTY];
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const int gx = gridDim.x;
-    const int k = blockIdx.x * 32 + lane;
-    if (blockIdx.x == 0 && blockIdx.y == 0 && tid == 0) {
+    const int gx = gridDim.x, x = blockIdx.x, y = blockIdx.y;
+    if (x == 0 && y == 0 && tid == 0) {
         *cd_nd = nd;
         cd_off[nd] = dirty_off[nd];
     }
-    const int dstart = blockIdx.y, dstep = blockIdx.y == 0 ? nd : (int)gridDim.y - 1;
+    // rows y < TF_SPLIT share dirty[0] (the largest slot: the resolve puts it
+    // first) in row chunks, combined in chunk order; the other rows take the
+    // remaining slots whole
+    const bool split = y < TF_SPLIT;
+    const int dstart = split ? 0 : 1 + (y - TF_SPLIT);
+    const int dstep = split ? nd : (int)gridDim.y - TF_SPLIT;
     for (int di = dstart; di < nd; di += dstep) {
         const int slot = dirty[di];
         const int j0 = dirty_off[di], j1 = dirty_off[di + 1];
+        const int ra = split ? j0 + (int)((int64_t)(j1 - j0) * y / TF_SPLIT) : j0;
+        const int rb = split ? j0 + (int)((int64_t)(j1 - j0) * (y + 1) / TF_SPLIT) : j1;
         const int fp = s_foldpos[slot], sp = s_seedpos[slot], ev = s_evicted[slot];
         const int n = s_nfeat[slot];
-        if (blockIdx.x == 0) {  // the chain's descriptor of this slot
-            for (int j = j0 + tid; j < j1; j += TF_T) {
+        if (x == 0) {  // the chain's descriptor: this CTA's rows, and the slot's meta
+            for (int j = ra + tid; j < rb; j += TF_T) {
                 const int p = pend_list[j];
                 cd_rows[j] = p >= fp ? frow[c0 + p] : nullptr;
             }
-            if (tid == 0) {
+            if (tid == 0 && (!split || y == 0)) {
                 cd_off[di] = j0;
                 cd_meta[CD_SLOT * ldm + di] = slot;
                 cd_meta[CD_NFEAT * ldm + di] = n;
@@ -2479,54 +2488,103 @@ __global__ void __launch_bounds__(TF_T) k_tfold(int D, int64_t c0, int B, const 
         }
         if (ev) continue;  // evicted: no snapshot (its exact centroid comes from the chain)
         const bool fresh = sp >= 0;  // seeded in this batch: S_tree starts empty
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-        double fsum = 0.0;
-        int r = 0;
-        for (int j = j0 + wid; j < j1; j += TF_T / 32, r++) {
-            const int p = pend_list[j];
-            const T *row = (const T *)frow[c0 + p];
-            if (k < D) acc[r & 3] = dadd(acc[r & 3], to_d(row[k]));
-            if (blockIdx.x == 0 && lane == 0) fsum += (double)fnorm[c0 + p];
-        }
-        part[wid][lane] = dadd(dadd(acc[0], acc[1]), dadd(acc[2], acc[3]));
-        if (blockIdx.x == 0 && lane == 0) s_fn[wid] = fsum;
-        __syncthreads();
-        if (wid == 0) {
-            double t = part[0][lane];
+        // warp w sums the 32-row groups w, w + 16, ... of [ra, rb): the group's
+        // row pointers are gathered by its lanes first, so 8 rows' loads are
+        // in flight at once; lane l owns columns x*128 + l + 32 i
+        double acc[4][2];
 #pragma unroll
-            for (int w = 1; w < TF_T / 32; w++) t = dadd(t, part[w][lane]);
+        for (int i = 0; i < 4; i++) acc[i][0] = acc[i][1] = 0.0;
+        double fsum = 0.0;
+        for (int g0 = ra + 32 * wid; g0 < rb; g0 += 32 * TF_W) {
+            const int jl = g0 + lane;
+            const T *ptr = nullptr;
+            if (jl < rb) {
+                const int p = pend_list[jl];
+                ptr = (const T *)frow[c0 + p];
+                if (x == 0) fsum += (double)fnorm[c0 + p];
+            }
+            const int nr = min(32, rb - g0);
+#pragma unroll 8
+            for (int r = 0; r < nr; r++) {
+                const T *row = (const T *)__shfl_sync(0xffffffffu, (unsigned long long)ptr, r);
+#pragma unroll
+                for (int i = 0; i < 4; i++) {
+                    const int col = x * TF_C + lane + 32 * i;
+                    if (col < D) acc[i][r & 1] = dadd(acc[i][r & 1], to_d(row[col]));
+                }
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; i++) part[wid][lane + 32 * i] = dadd(acc[i][0], acc[i][1]);
+        if (x == 0) {
+            fsum = warp_sum(fsum);
+            if (lane == 0) s_fn[wid] = fsum;
+        }
+        __syncthreads();
+        double t = 0.0, fs = 0.0;
+        const int col = x * TF_C + tid;
+        if (tid < TF_C) {
+            t = part[0][tid];
+#pragma unroll
+            for (int w = 1; w < TF_W; w++) t = dadd(t, part[w][tid]);
+        }
+        if (x == 0 && tid == 0)
+            for (int w = 0; w < TF_W; w++) fs += s_fn[w];
+        bool finish = true;
+        if (split) {  // publish this chunk; the slice's last chunk combines them in order
+            if (tid < TF_C && col < D) tf_part[(int64_t)y * D + col] = t;
+            if (x == 0 && tid == 0) tf_part[(int64_t)TF_SPLIT * D + y] = fs;
+            __threadfence();
+            __syncthreads();
+            if (tid == 0) s_last = atomicAdd(&tf_bcnt[x], 1) == TF_SPLIT - 1;
+            __syncthreads();
+            finish = s_last;
+            if (finish) {
+                __threadfence();
+                if (tid < TF_C && col < D) {
+                    t = __ldcg(&tf_part[col]);
+                    for (int q = 1; q < TF_SPLIT; q++) t = dadd(t, __ldcg(&tf_part[(int64_t)q * D + col]));
+                }
+                if (x == 0 && tid == 0) {
+                    fs = 0.0;
+                    for (int q = 0; q < TF_SPLIT; q++) fs += __ldcg(&tf_part[(int64_t)TF_SPLIT * D + q]);
+                }
+                if (tid == 0) tf_bcnt[x] = 0;
+            }
+        }
+        if (finish) {
             float c2 = 0.f;
-            if (k < D) {
-                const double sum = fresh ? t : dadd(S_tree[(int64_t)slot * D + k], t);
-                S_tree[(int64_t)slot * D + k] = sum;
+            if (tid < TF_C && col < D) {
+                const double sum = fresh ? t : dadd(S_tree[(int64_t)slot * D + col], t);
+                S_tree[(int64_t)slot * D + col] = sum;
                 const float c32 = (float)ddiv(sum, (double)n);
-                C32[(int64_t)slot * D + k] = c32;
+                C32[(int64_t)slot * D + col] = c32;
                 c2 = c32 * c32;
             }
             c2 = warp_sum(c2);
-            if (lane == 0) {
-                tf_cn2[(int64_t)di * gx + blockIdx.x] = c2;
-                if (blockIdx.x == 0) {
-                    double fs = 0.0;
-                    for (int w = 0; w < TF_T / 32; w++) fs += s_fn[w];
-                    // fp32 norms: relative error < 1e-6, rounded up below
-                    s_abs[slot] = (fresh ? 0.0 : s_abs[slot]) + fs * (1.0 + 1e-5);
-                }
+            if (lane == 0) s_c2[wid] = c2;
+            __syncthreads();
+            if (tid == 0) {
+                float cs = 0.f;
+                for (int w = 0; w < TF_C / 32; w++) cs += s_c2[w];
+                tf_cn2[(int64_t)di * gx + x] = cs;
+                // fp32 norms: relative error < 1e-6, rounded up
+                if (x == 0) s_abs[slot] = (fresh ? 0.0 : s_abs[slot]) + fs * (1.0 + 1e-5);
                 __threadfence();
                 s_last = atomicAdd(&tf_cnt[di], 1) == gx - 1;
             }
-        }
-        __syncthreads();
-        if (s_last && tid == 0) {  // last slice of this slot: ||C32||^2 in slice order, drift bound
-            __threadfence();
-            float c2 = 0.f;
-            for (int x = 0; x < gx; x++) c2 += __ldcg(&tf_cn2[(int64_t)di * gx + x]);
-            s_cn2[slot] = c2;
-            const double u = 1.1102230246251565e-16, nn = (double)n;
-            const double gam = nn * u / (1.0 - nn * u);
-            const double sa = __ldcg(&s_abs[slot]);
-            s_sdev[slot] = (2.0 * gam * sa / nn + 4.0 * u * sqrt((double)c2) * 1.01) * 1.01 + 1e-300;
-            tf_cnt[di] = 0;
+            __syncthreads();
+            if (s_last && tid == 0) {  // last slice: ||C32||^2 in slice order, the drift bound
+                __threadfence();
+                float cs = 0.f;
+                for (int q = 0; q < gx; q++) cs += __ldcg(&tf_cn2[(int64_t)di * gx + q]);
+                s_cn2[slot] = cs;
+                const double u = 1.1102230246251565e-16, nn = (double)n;
+                const double gam = nn * u / (1.0 - nn * u);
+                const double sa = __ldcg(&s_abs[slot]);
+                s_sdev[slot] = (2.0 * gam * sa / nn + 4.0 * u * sqrt((double)cs) * 1.01) * 1.01 + 1e-300;
+                tf_cnt[di] = 0;
+            }
         }
         __syncthreads();
     }
@@ -3135,8 +3193,8 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
         {
             s->tstart(3);
             const int buf = cbuf;
-            const int64_t gxt = cdiv(D, 32);
-            const int64_t gyt = std::max<int64_t>(8, std::min<int64_t>(2 * (int64_t)B + 1, (148 * 8) / gxt));
+            const int64_t gxt = cdiv(D, TF_C);
+            const int64_t gyt = TF_SPLIT + std::max<int64_t>(4, std::min<int64_t>(2 * (int64_t)B + 1, (148 * 4) / gxt));
             const int ldm = 2 * s->B + 3;
             int32_t *meta = s->cd_meta.p + (size_t)buf * CD_NMETA * ldm;
             int32_t *coff = s->cd_off.p + (size_t)buf * ldm;
@@ -3144,7 +3202,8 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             launch_pdl(k_tfold<T>, dim3((unsigned)gxt, (unsigned)gyt), dim3(TF_T), 0, st, D, c0, B, s->ctr.p, s->dirty.p,
                        s->dirty_off.p, s->pend_list.p, s->frow.p, s->fnorm.p, s->s_nfeat.p, s->s_foldpos.p,
                        s->s_seedpos.p, s->s_evicted.p, s->s_cid.p, s->s_size.p, s->S_tree.p, s->C32.p, s->s_cn2.p,
-                       s->s_abs.p, s->s_sdev.p, s->tf_cn2.p, s->tf_cnt.p, s->cd_nd.p + buf, meta, ldm, coff, crows);
+                       s->s_abs.p, s->s_sdev.p, s->tf_cn2.p, s->tf_cnt.p, s->tf_part.p, s->tf_bcnt.p,
+                       s->cd_nd.p + buf, meta, ldm, coff, crows);
             FX_LAUNCHED();
             s->tstop();
             FX_CUDA(cudaEventRecord(s->ev_tf[buf], st));

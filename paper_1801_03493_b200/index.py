@@ -15,6 +15,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
+from ._reftypes import shared
 from .clustering import Cluster
 import os
 
@@ -33,6 +34,9 @@ class IndexHeader:
     @property
     def k(self) -> int:
         return self.config.k
+
+
+IndexHeader = shared("index", "IndexHeader", IndexHeader)
 
 
 class DeviceIndex:

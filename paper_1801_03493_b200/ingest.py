@@ -21,6 +21,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib, classifiers
+from ._reftypes import shared
 from .core import Config, encode_class, validate_config
 from .errors import DimensionMismatch, SignatureLengthMismatch
 from .index import DeviceIndex, IndexHeader, TopKIndex
@@ -47,6 +48,10 @@ class StreamHeader:
     dim: int
     sig_dim: int
     vocab: int
+
+
+IngestReport = shared("ingest", "IngestReport", IngestReport)
+StreamHeader = shared("streamio", "StreamHeader", StreamHeader)
 
 
 class Stream:

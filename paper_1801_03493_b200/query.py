@@ -15,6 +15,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
+from ._reftypes import shared
 from .classifiers import GROUND_TRUTH, SPECIALIZED
 from .core import OTHER_CLASS, encode_class
 from .errors import KxTooLarge, MissingTrueClass, NonMonotoneSchedule, UnknownClass
@@ -36,6 +37,9 @@ class QueryResult:
     clusters_examined: int
     clusters_matched: int
 
+
+QueryRequest = shared("query", "QueryRequest", QueryRequest)
+QueryResult = shared("query", "QueryResult", QueryResult)
 
 _NO_LABEL, _NO_OBJECT, _NO_REP = -2, -3, -4
 

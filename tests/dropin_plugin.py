@@ -6,7 +6,8 @@ names at import time: ``from focusidx.ingest import ingest_stream``).
     python -m pytest -p dropin_plugin <reference tests>
 
 Replaced: focusidx.ingest.{ingest_stream, pixel_diff},
-focusidx.index.{build, lookup, save, load}, focusidx.query.QuerySession.
+focusidx.index.{build, lookup, save, load}, focusidx.query.QuerySession,
+focusidx.tuner._GridEvaluator (the device grid evaluation).
 Everything else (types, profiles, the rank-model classify, the tuner, the
 simulator) stays the reference's.  This package's error classes are the
 reference's own classes when focusidx is importable (errors.py), so the
@@ -17,6 +18,7 @@ import focusidx  # noqa: F401  (first: errors.py aliases its classes)
 from focusidx import index as _ref_index
 from focusidx import ingest as _ref_ingest
 from focusidx import query as _ref_query
+from focusidx import tuner as _ref_tuner
 
 import paper_1801_03493_b200 as fx
 
@@ -35,6 +37,7 @@ _switch(_ref_index, "lookup", fx.lookup)
 _switch(_ref_index, "save", fx.save)
 _switch(_ref_index, "load", fx.load)
 _switch(_ref_query, "QuerySession", fx.QuerySession)
+_switch(_ref_tuner, "_GridEvaluator", fx.tuner.GridEvaluator)
 assert fx.errors.SHARES_REFERENCE_CLASSES, "the drop-in must raise the reference's error classes"
 
 

@@ -15,7 +15,7 @@ pytestmark = pytest.mark.gpu
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 REF = os.path.join(REPO, "baseline", "_ref")
 SUITE = os.path.join(REF, "focusidx_tests")
-MODULES = ["test_ingest.py", "test_index.py", "test_query.py"]
+MODULES = ["test_ingest.py", "test_index.py", "test_query.py", "test_tuner.py", "test_acceptance.py"]
 
 
 @pytest.mark.timeout(900)

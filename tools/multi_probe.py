@@ -23,6 +23,7 @@ def main():
     ap.add_argument("--streams", default="1,2,4,8")
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--serial", action="store_true", help="one host thread runs the engines one after another")
+    ap.add_argument("--verify", action="store_true", help="compare every run's results with the first (solo) run")
     ap.add_argument("--counters", action="store_true", help="print each engine's resolve/fold counters")
     ap.add_argument("--trace", type=int, default=0, help="CUPTI-trace this many extra runs at the largest N")
     a = ap.parse_args()
@@ -31,6 +32,8 @@ def main():
     datas = [synth.generate(a.objects, seed=1000 + j) for j in range(nmax)]
     torch.cuda.synchronize()
     prof = fx.make_default_profiles(1000)["cheap"]
+
+    solo = {}
 
     def one(j):
         fx.set_device(0)
@@ -44,6 +47,14 @@ def main():
         t2 = time.perf_counter()
         ix, rp = s.finalize()
         t3 = time.perf_counter()
+        if a.verify:
+            import numpy as np
+            cl, _, _ = s.object_results(a.objects, 4)
+            ex = ix.export(centroids=True)
+            h = hash((cl.tobytes(), ex["centroids"].tobytes(), ex["reps"].tobytes()))
+            if j in solo and solo[j] != h:
+                print(f"  MISMATCH engine {j}: concurrent result differs from its solo run", flush=True)
+            solo.setdefault(j, h)
         if a.counters:
             c = s.counters()
             print(f"  engine {j}: " + " ".join(f"{k}={c[k]}" for k in (
@@ -54,7 +65,8 @@ def main():
         return (t1 - t0, t2 - t1, t3 - t2, t4 - t3)
 
     with ThreadPoolExecutor(max_workers=nmax) as pool:
-        list(pool.map(one, range(nmax)))
+        for j in range(nmax):  # solo reference runs (one engine at a time)
+            one(j)
         for n in ns:
             for r in range(a.reps):
                 torch.cuda.synchronize()
