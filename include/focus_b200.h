@@ -127,6 +127,30 @@ int fx_fc_topk_device(int32_t device, void *cuda_stream, int64_t n, int32_t dim,
                       const float *d_feats, const float *d_W, const float *d_bias, int32_t *d_topk, float *d_conf,
                       uint8_t *d_flag);
 
+/* extract_feature (classifiers.py:152-158) on the device, bit for bit:
+ * out[i] = feats[i] + sigma * default_rng([seed, object_ids[i], 1]).standard_normal(dim)
+ * (numpy SeedSequence + PCG64 + ziggurat; float64 arithmetic, as numpy
+ * promotes feature + float64 noise).  sigma == 0 copies the features (the
+ * reference's early return).  feats[n*dim] of feat_type (FX_F32 / FX_F64),
+ * out[n*dim] float64.  *n_flagged (may be NULL): u-layer rejection tests
+ * whose exp() sat within 0.01 ulp of a rounding midpoint (expected 0).
+ * Replaces the per-object numpy call at classifiers.py:156-158. */
+int fx_extract_features(int32_t device, int64_t n, int32_t dim, const int64_t *object_ids, const void *feats,
+                        int32_t feat_type, double sigma, uint64_t seed, double *out, int64_t *n_flagged);
+/* Same with DEVICE pointers and row strides (elements), enqueued on the
+ * caller's CUDA stream (void*, NULL = legacy default stream);
+ * d_flagged: device uint64 counter incremented (may be NULL). */
+int fx_extract_features_device(int32_t device, int64_t n, int32_t dim, const int64_t *d_object_ids,
+                               const void *d_feats, int32_t feat_type, int64_t ld_in, double sigma, uint64_t seed,
+                               double *d_out, int64_t ld_out, uint64_t *d_flagged, void *cuda_stream);
+/* Ingest-time feature noise (the drop-in ingest_stream with the synthetic
+ * classifier profile, classifiers.py:152-158): fx_ingest's feature rows are
+ * the objects' RAW features (of in_type, FX_FEATS_COMPACT rows of the
+ * classified objects) and the engine clusters extract_feature of them,
+ * computed on the device.  The stream's feat_type must be FX_F64 when
+ * sigma > 0 (numpy's result type).  Host-buffer fx_ingest only. */
+int fx_stream_set_feature_noise(fx_stream *s, double sigma, uint64_t seed, int32_t in_type);
+
 /* pixel_diff (ingest.py:37-47) of every object against its predecessor in
  * a sequence, without an engine: out_is_dup[0] = 0, out_is_dup[i] =
  * pixel_diff(obj[i-1], obj[i], eps).  sigs[n * sig_dim] float64. */

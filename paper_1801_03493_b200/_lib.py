@@ -71,6 +71,12 @@ _SIGS = {
                                   vp, c_i32p, vp, c_u8p]),
     "fx_fc_topk_device": (ctypes.c_int, [ctypes.c_int32, vp, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32,
                                          ctypes.c_int32, vp, vp, vp, vp, vp, vp]),
+    "fx_extract_features": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int64, ctypes.c_int32, c_i64p, vp, ctypes.c_int32,
+                                           ctypes.c_double, ctypes.c_uint64, c_f64p, c_i64p]),
+    "fx_extract_features_device": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int64, ctypes.c_int32, vp, vp,
+                                                  ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_uint64,
+                                                  vp, ctypes.c_int64, vp, vp]),
+    "fx_stream_set_feature_noise": (ctypes.c_int, [vp, ctypes.c_double, ctypes.c_uint64, ctypes.c_int32]),
     "fx_dup_flags": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int64, ctypes.c_int32, c_i64p, c_f64p, ctypes.c_double,
                                     c_u8p]),
     "fx_stream_dup_flags": (ctypes.c_int, [vp, ctypes.c_int64, c_i64p, c_f64p, c_u8p]),

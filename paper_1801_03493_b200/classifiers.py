@@ -145,6 +145,29 @@ def extract_feature(profile: ClassifierProfile, obj: DetectedObject, rng_seed: i
     return obj.feature + profile.feature_noise_sigma * g.standard_normal(obj.feature.shape[0])
 
 
+def extract_features(profile: ClassifierProfile, object_ids, feats, rng_seed: int,
+                     device: int | None = None) -> np.ndarray:
+    """extract_feature (classifiers.py:152-158) for a batch of objects on the
+    device (csrc/noise.cu): row i = feats[i] + sigma * default_rng([rng_seed,
+    object_ids[i], 1]).standard_normal(D), float64, bit for bit."""
+    from . import _lib
+    oids = np.ascontiguousarray(object_ids, np.int64)
+    F = np.asarray(feats)
+    if F.dtype != np.float32:
+        F = F.astype(np.float64, copy=False)
+    F = np.ascontiguousarray(F).reshape(oids.size, -1)
+    out = np.empty(F.shape, np.float64)
+    if profile.feature_noise_sigma == 0.0:
+        out[...] = F
+        return out
+    nflag = np.zeros(1, np.int64)
+    _lib.check(_lib.load().fx_extract_features(
+        _lib.device() if device is None else device, oids.size, F.shape[1], _lib.p64(oids), _lib.pv(F),
+        _lib.FX_F32 if F.dtype == np.float32 else _lib.FX_F64, float(profile.feature_noise_sigma),
+        rng_seed & ((1 << 64) - 1), _lib.pf64(out), _lib.p64(nflag)))
+    return out
+
+
 # -- device tables -----------------------------------------------------------
 
 def _rank_of_u53(model: RankModel, out_len: int, u53: int) -> int:

@@ -24,6 +24,9 @@ template <typename T>
 void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end);
 void launch_final_live(fx_stream *s);
 size_t resolve_smem(int Bc, const PwPlan &P);
+void launch_extract(int dev, int64_t n, int D, const int64_t *d_oid, const void *d_in, int in_type, int64_t ld_in,
+                    double sigma, uint64_t seed, double *d_out, int64_t ld_out, unsigned long long *d_flag,
+                    cudaStream_t st);
 void launch_fc_head(int64_t n, int64_t c0, const char *const *frow, const int64_t *cls_obj, const float *fnorm, int D,
                     int V, int K, const float *W, const float *wnorm, const float *bias, int32_t *topk, float *conf,
                     uint8_t *flag, unsigned long long *nflag, cudaStream_t st, const float *Xdense);
@@ -269,6 +272,14 @@ int fx_stream_create(const fx_stream_config *cfg, fx_stream **out) {
                 s->tf_cn2.reserve(nd * gx);
                 s->tf_cnt.reserve(nd);
                 FX_CUDA(cudaMemsetAsync(s->tf_cnt.p, 0, sizeof(int32_t) * nd, s->st));
+                {
+                    const size_t gx2 = (size_t)cdiv(D, 512), nch = (size_t)cdiv(B, 64);
+                    s->tf_ccnt.reserve(nd * gx2);
+                    FX_CUDA(cudaMemsetAsync(s->tf_ccnt.p, 0, sizeof(int32_t) * nd * gx2, s->st));
+                    s->tf_pt0.reserve(nch * D);
+                    s->tf_pt1.reserve(nch * D);
+                    s->tf_pf.reserve(2 * nch);
+                }
                 s->cd_meta.reserve(2 * 8 * nd);
                 s->cd_off.reserve(2 * nd);
                 s->cd_rows.reserve(2 * (size_t)B);
@@ -356,6 +367,23 @@ int fx_stream_set_rank_model(fx_stream *s, const fx_rank_model *rm) {
         h2d(s->rm_fill.p, rm->fillers, (int64_t)(V + 1) * K, s->st);
         FX_CUDA(cudaStreamSynchronize(s->st));
         s->has_rm = true;
+    })
+}
+
+int fx_stream_set_feature_noise(fx_stream *s, double sigma, uint64_t seed, int32_t in_type) {
+    FX_GUARD({
+        if (!s) throw Error{FX_E_USAGE, "null stream"};
+        if (s->n_seen > 0) throw Error{FX_E_USAGE, "feature noise must be set before the first ingest"};
+        if (!(sigma >= 0.0) || (in_type != FX_F32 && in_type != FX_F64))
+            throw Error{FX_E_USAGE, "bad feature-noise arguments"};
+        if (sigma > 0.0 && s->cfg.feat_type != FX_F64)
+            throw Error{FX_E_USAGE, "feature noise needs a float64 engine (numpy's result type)"};
+        if (sigma == 0.0 && in_type != s->cfg.feat_type)
+            throw Error{FX_E_USAGE, "sigma = 0 copies the features: in_type must be the engine's feat_type"};
+        s->has_noise = sigma > 0.0;
+        s->noise_sigma = sigma;
+        s->noise_seed = seed;
+        s->noise_in_type = in_type;
     })
 }
 
@@ -629,6 +657,8 @@ static int ingest_common(fx_stream *s, int64_t n, const int64_t *object_ids, con
         cudaStream_t st = s->st;
         const int D = s->cfg.dim, S = s->cfg.sig_dim, K = s->cfg.k;
         const bool compact = flags & FX_FEATS_COMPACT;
+        if (s->has_noise && (device || !compact))
+            throw Error{FX_E_USAGE, "feature noise: host fx_ingest with FX_FEATS_COMPACT rows only"};
         if (device) {
             ingest_chunk(s, n, object_ids, frame_ids, sigs, (const char *)feats, true_class, topk, compact);
         } else {
@@ -646,6 +676,8 @@ static int ingest_common(fx_stream *s, int64_t n, const int64_t *object_ids, con
             DevBuf<int64_t> o, f;
             DevBuf<double> g;
             DevBuf<int32_t> tc, tk;
+            DevBuf<int64_t> noise_oid;  // feature noise: classified objects' ids
+            DevBuf<char> raw;           // feature noise: one chunk of raw rows
             o.reserve(n);
             f.reserve(n);
             g.reserve((size_t)n * std::max(S, 1));
@@ -666,6 +698,15 @@ static int ingest_common(fx_stream *s, int64_t n, const int64_t *object_ids, con
                     int64_t r = 0;
                     for (int64_t i = c * CH, e = std::min<int64_t>(n, (c + 1) * CH); i < e; i++) r += hd[i] ? 0 : 1;
                     row0[c + 1] = row0[c] + r;
+                }
+                if (s->has_noise) {  // object ids of the classified rows (extract_feature's rng key)
+                    std::vector<int64_t> co;
+                    co.reserve((size_t)row0[nch]);
+                    for (int64_t i = 0; i < n; i++)
+                        if (!hd[i]) co.push_back(object_ids[i]);
+                    noise_oid.reserve(std::max<size_t>(1, co.size()));
+                    h2d(noise_oid.p, co.data(), (int64_t)co.size(), st);
+                    FX_CUDA(cudaStreamSynchronize(st));  // co is pageable and goes out of scope
                 }
             } else {
                 for (int c = 0; c < nch; c++) row0[c + 1] = std::min<int64_t>(n, (int64_t)(c + 1) * CH);
@@ -693,9 +734,22 @@ static int ingest_common(fx_stream *s, int64_t n, const int64_t *object_ids, con
                     if (true_class) h2d(tc.p + a, true_class + a, m, cst);
                     if (topk) h2d(tk.p + a * K, topk + a * K, m * K, cst);
                     const int64_t r0 = row0[c], nr = row0[c + 1] - row0[c];
-                    if (nr > 0)
+                    if (nr > 0 && s->has_noise) {
+                        // raw rows -> staging, extract_feature (classifiers.py:152-158) -> engine rows
+                        const size_t ib = (size_t)D * (s->noise_in_type == FX_F32 ? 4 : 8);
+                        if (raw.n < (size_t)nr * ib) {
+                            StreamGuard sg2_(cst);
+                            raw.reserve((size_t)CH * ib);
+                        }
+                        FX_CUDA(cudaMemcpyAsync(raw.p, (const char *)feats + (size_t)r0 * ib, (size_t)nr * ib,
+                                                cudaMemcpyHostToDevice, cst));
+                        launch_extract(s->dev, nr, D, noise_oid.p + r0, raw.p, s->noise_in_type, D, s->noise_sigma,
+                                       s->noise_seed, (double *)(fb->p + (size_t)r0 * rb), D,
+                                       (unsigned long long *)(s->ctr.p + C_NOISEFLAG), cst);
+                    } else if (nr > 0) {
                         FX_CUDA(cudaMemcpyAsync(fb->p + (size_t)r0 * rb, (const char *)feats + (size_t)r0 * rb,
                                                 (size_t)nr * rb, cudaMemcpyHostToDevice, cst));
+                    }
                     FX_CUDA(cudaEventCreateWithFlags(&ev[c], cudaEventDisableTiming));
                     FX_CUDA(cudaEventRecord(ev[c], cst));
                 }

@@ -28,6 +28,7 @@ enum Ctr {
     C_FASTST,          // resolve fast path of the current batch: 0 not run, 1 committed, 2 fall back
     C_FDONE,           // fast path: CTAs done (last-block election)
     C_FASTB,           // batches committed by the fast path
+    C_NOISEFLAG,       // feature noise: exp() decisions within 0.01 ulp of a midpoint (fx_stream_set_feature_noise)
     C_COUNT
 };
 
@@ -56,6 +57,11 @@ struct fx_stream {
     fx::DevBuf<int32_t> rm_emit, rm_fill;
     // K1b classifier head
     bool has_fc = false;
+    // ingest-time feature noise (fx_stream_set_feature_noise)
+    bool has_noise = false;
+    double noise_sigma = 0.0;
+    uint64_t noise_seed = 0;
+    int noise_in_type = 0;
     int fc_V = 0;
     fx::DevBuf<float> fc_W, fc_wnorm, fc_bias;
 
@@ -110,6 +116,8 @@ struct fx_stream {
     fx::DevBuf<int32_t> tf_cnt;            // [2B+2] CTAs done per dirty slot (last-block election)
     fx::DevBuf<double> tf_part;            // [TF_SPLIT * D + TF_SPLIT] row-chunk partials of the largest slot
     fx::DevBuf<int32_t> tf_bcnt;           // [gx] row chunks done per column slice
+    fx::DevBuf<int32_t> tf_ccnt;           // [(2B+3) * ceil(D/512)] k_tfold2: chunks done per (dirty slot, slice)
+    fx::DevBuf<double> tf_pt0, tf_pt1, tf_pf;  // k_tfold2 chunk partials [ceil(B/64) * D] x 2, norms [2 * ceil(B/64)]
     fx::DevBuf<int32_t> cd_meta, cd_off;   // [2][8][2B+3], [2][2B+3] chain descriptors (double buffered)
     fx::DevBuf<const char *> cd_rows;      // [2][B] member rows of the chain (nullptr: already in S)
     fx::DevBuf<int64_t> cd_nd;             // [2] dirty slots of the chain

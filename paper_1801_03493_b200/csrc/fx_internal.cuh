@@ -307,8 +307,10 @@ __device__ __forceinline__ U128 add128(U128 a, U128 b) {
     return r;
 }
 
-// 53-bit integer of the first random() draw (random() = u53 * 2^-53)
-__device__ __forceinline__ uint64_t first_u53(uint64_t a, uint64_t b, uint64_t c) {
+// PCG64 state after SeedSequence([a, b, c]) seeding (numpy
+// _pcg64.pyx / pcg64.h pcg64_set_seed): the state BEFORE the first
+// next_uint64 step.  Draw p (0-based) uses state_{p+1} = mult * state_p + inc.
+__device__ __forceinline__ void pcg64_seed(uint64_t a, uint64_t b, uint64_t c, U128 &state, U128 &inc) {
     uint32_t ent[6];
     int ne = 0;
     uint64_t ints[3] = {a, b, c};
@@ -347,16 +349,27 @@ __device__ __forceinline__ uint64_t first_u53(uint64_t a, uint64_t b, uint64_t c
     uint64_t w0 = (uint64_t)w[0] | ((uint64_t)w[1] << 32), w1 = (uint64_t)w[2] | ((uint64_t)w[3] << 32);
     uint64_t w2 = (uint64_t)w[4] | ((uint64_t)w[5] << 32), w3 = (uint64_t)w[6] | ((uint64_t)w[7] << 32);
     const U128 mult{0x2360ed051fc65da4ull, 0x4385df649fccf645ull};
-    U128 inc{(w2 << 1) | (w3 >> 63), (w3 << 1) | 1ull};
-    U128 state{0, 0};
+    inc = U128{(w2 << 1) | (w3 >> 63), (w3 << 1) | 1ull};
+    state = U128{0, 0};
     state = add128(mul128(state, mult), inc);
     state = add128(state, U128{w0, w1});
     state = add128(mul128(state, mult), inc);
+}
+
+// PCG64 XSL-RR output of a stepped state
+__device__ __forceinline__ uint64_t pcg64_out(U128 st) {
+    const uint64_t x = st.hi ^ st.lo;
+    const unsigned rot = (unsigned)(st.hi >> 58);
+    return (x >> rot) | (x << ((64 - rot) & 63));
+}
+
+// 53-bit integer of the first random() draw (random() = u53 * 2^-53)
+__device__ __forceinline__ uint64_t first_u53(uint64_t a, uint64_t b, uint64_t c) {
+    U128 state, inc;
+    pcg64_seed(a, b, c, state, inc);
+    const U128 mult{0x2360ed051fc65da4ull, 0x4385df649fccf645ull};
     state = add128(mul128(state, mult), inc);  // next_uint64 steps first
-    uint64_t x = state.hi ^ state.lo;
-    unsigned rot = (unsigned)(state.hi >> 58);
-    uint64_t out = (x >> rot) | (x << ((64 - rot) & 63));
-    return out >> 11;
+    return pcg64_out(state) >> 11;
 }
 
 // ---------------------------------------------------------------------------

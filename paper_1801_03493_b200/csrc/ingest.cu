@@ -2590,6 +2590,218 @@ __global__ void __launch_bounds__(TF_T) k_tfold(int D, int64_t c0, int B, const 
     }
 }
 
+// K2c' (current): the same snapshot tree fold, load-balanced.  The batch's
+// pending rows (pend_list, grouped by dirty slot through dirty_off) are cut
+// into fixed chunks of TF2_R rows; CTA (x, c) sums chunk c's rows over column
+// slice x (512 columns: 128 column threads x 4 columns, 4 row groups).  A slot
+// whose rows lie inside one chunk is finished by that CTA; a slot spanning
+// chunks has each chunk's partial written to scratch (pt0[c] when the slot
+// began before chunk c, pt1[c] when it begins inside c and runs past it) and
+// the last chunk to arrive sums the partials in chunk order.  Every order is
+// fixed (deterministic); the float64 tree-order sum is within the Higham
+// bound of the reference's sequential sum whatever the order.
+// ---------------------------------------------------------------------------
+constexpr int TF2_T = 512, TF2_G = 4, TF2_CT = 128, TF2_COLS = 4 * TF2_CT, TF2_R = 64;
+
+template <typename T, bool VEC>
+__device__ __forceinline__ void tf2_load4(const char *row, int col, int D, double v[4]) {
+    if (VEC && sizeof(T) == 4) {
+        const float4 q = __ldg((const float4 *)((const float *)row + col));
+        v[0] = q.x;
+        v[1] = q.y;
+        v[2] = q.z;
+        v[3] = q.w;
+    } else if (VEC) {
+        const double2 a = __ldg((const double2 *)((const double *)row + col));
+        const double2 b = __ldg((const double2 *)((const double *)row + col) + 1);
+        v[0] = a.x;
+        v[1] = a.y;
+        v[2] = b.x;
+        v[3] = b.y;
+    } else {
+#pragma unroll
+        for (int i = 0; i < 4; i++) v[i] = col + i < D ? to_d(((const T *)row)[col + i]) : 0.0;
+    }
+}
+
+template <typename T, bool VEC>
+__global__ void __launch_bounds__(TF2_T) k_tfold2(
+    int D, int64_t c0, const int64_t *__restrict__ ctr, const int32_t *__restrict__ dirty,
+    const int32_t *__restrict__ dirty_off, const int32_t *__restrict__ pend_list, const char *const *__restrict__ frow,
+    const float *__restrict__ fnorm, const int32_t *__restrict__ s_nfeat, const int32_t *__restrict__ s_foldpos,
+    const int32_t *__restrict__ s_seedpos, const int32_t *__restrict__ s_evicted, const int32_t *__restrict__ s_cid,
+    const int32_t *__restrict__ s_size, double *__restrict__ S_tree, float *__restrict__ C32,
+    float *__restrict__ s_cn2, double *__restrict__ s_abs, double *__restrict__ s_sdev, float *__restrict__ tf_cn2,
+    int32_t *__restrict__ tf_cnt, int32_t *__restrict__ tf_ccnt, double *__restrict__ pt0,
+    double *__restrict__ pt1, double *__restrict__ pf, int64_t *__restrict__ cd_nd, int32_t *__restrict__ cd_meta,
+    int ldm, int32_t *__restrict__ cd_off, const char **__restrict__ cd_rows) {
+    pdl_enter();
+    __shared__ double red[TF2_G][TF2_COLS];
+    __shared__ double s_f[TF2_T / 32];
+    __shared__ float s_c2[TF2_T / 32];
+    __shared__ int s_last;
+    const int nd = (int)ctr[C_NDIRTY];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int g = tid / TF2_CT, ct = tid % TF2_CT;
+    const int gx = gridDim.x, x = blockIdx.x, c = blockIdx.y, nch = gridDim.y;
+    const int Btot = dirty_off[nd];
+    const int cs = c * TF2_R, ce = min(Btot, cs + TF2_R);
+    const bool lastc = c == nch - 1;
+    const int col = x * TF2_COLS + ct * 4;
+    if (x == 0 && c == 0 && tid == 0) {
+        *cd_nd = nd;
+        cd_off[nd] = Btot;
+    }
+    // a non-empty segment [j0, j1) belongs to chunks j0/R .. (j1-1)/R; an empty
+    // one (an evicted slot without rows) to chunk min(j0/R, last)
+    int lo = 0, hi = nd;  // first di with dirty_off[di+1] >= cs
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (dirty_off[mid + 1] >= cs) hi = mid; else lo = mid + 1;
+    }
+    for (int di = lo; di < nd; di++) {
+        const int j0 = dirty_off[di], j1 = dirty_off[di + 1];
+        if (!lastc && j0 >= ce) break;
+        const bool member = j0 < j1 ? (j0 / TF2_R <= c && c <= (j1 - 1) / TF2_R) : min(j0 / TF2_R, nch - 1) == c;
+        if (!member) continue;
+        const int slot = dirty[di];
+        const int fp = s_foldpos[slot], sp = s_seedpos[slot], ev = s_evicted[slot];
+        const int ra = max(j0, cs), rb = min(j1, ce);
+        if (x == 0) {  // chain descriptor: rows of this chunk, the slot's meta from its first chunk
+            for (int j = ra + tid; j < rb; j += TF2_T) {
+                const int p = pend_list[j];
+                cd_rows[j] = p >= fp ? frow[c0 + p] : nullptr;
+            }
+            if (tid == 0 && j0 >= cs) {
+                cd_off[di] = j0;
+                cd_meta[CD_SLOT * ldm + di] = slot;
+                cd_meta[CD_NFEAT * ldm + di] = s_nfeat[slot];
+                cd_meta[CD_FP * ldm + di] = fp;
+                cd_meta[CD_SP * ldm + di] = sp;
+                cd_meta[CD_EV * ldm + di] = ev;
+                cd_meta[CD_CID * ldm + di] = s_cid[slot];
+                cd_meta[CD_SIZE * ldm + di] = s_size[slot];
+            }
+        }
+        if (ev) continue;  // evicted: no snapshot (its exact centroid comes from the chain)
+        // column sums of rows [ra, rb): row group g takes rows ra+g, ra+g+4, ...
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        if (col < D) {
+            int j = ra + g;
+            for (; j + 7 * TF2_G < rb; j += 8 * TF2_G) {
+                double v[8][4];
+#pragma unroll
+                for (int u = 0; u < 8; u++) tf2_load4<T, VEC>(frow[c0 + pend_list[j + u * TF2_G]], col, D, v[u]);
+#pragma unroll
+                for (int u = 0; u < 8; u++)
+#pragma unroll
+                    for (int i = 0; i < 4; i++) acc[i] = dadd(acc[i], v[u][i]);
+            }
+            for (; j < rb; j += TF2_G) {
+                double v[4];
+                tf2_load4<T, VEC>(frow[c0 + pend_list[j]], col, D, v);
+#pragma unroll
+                for (int i = 0; i < 4; i++) acc[i] = dadd(acc[i], v[i]);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 4; i++) red[g][ct * 4 + i] = acc[i];
+        double fs = 0.0;  // sum of the rows' fp32 norms (slice 0)
+        if (x == 0) {
+            for (int j = ra + tid; j < rb; j += TF2_T) fs += (double)fnorm[c0 + pend_list[j]];
+            fs = warp_sum(fs);
+            if (lane == 0) s_f[wid] = fs;
+        }
+        __syncthreads();
+        double t[4];
+        if (g == 0) {
+#pragma unroll
+            for (int i = 0; i < 4; i++)
+                t[i] = dadd(dadd(dadd(red[0][ct * 4 + i], red[1][ct * 4 + i]), red[2][ct * 4 + i]), red[3][ct * 4 + i]);
+        }
+        if (x == 0 && tid == 0) {
+            fs = 0.0;
+            for (int w = 0; w < TF2_T / 32; w++) fs += s_f[w];
+        }
+        const bool whole = j0 >= cs && j1 <= ce;
+        bool finish = true;
+        if (!whole) {  // publish this chunk's partial; the slot's last chunk combines in chunk order
+            double *dst = (j0 < cs ? pt0 : pt1) + (int64_t)c * D;
+            if (g == 0 && col < D) {
+#pragma unroll
+                for (int i = 0; i < 4; i++)
+                    if (col + i < D) dst[col + i] = t[i];
+            }
+            if (x == 0 && tid == 0) pf[2 * c + (j0 < cs ? 0 : 1)] = fs;
+            __threadfence();
+            __syncthreads();
+            const int k0 = j0 / TF2_R, k1 = (j1 - 1) / TF2_R;
+            if (tid == 0) s_last = atomicAdd(&tf_ccnt[di * gx + x], 1) == k1 - k0;
+            __syncthreads();
+            finish = s_last;
+            if (finish) {
+                __threadfence();
+                if (g == 0 && col < D) {
+#pragma unroll
+                    for (int i = 0; i < 4; i++) t[i] = col + i < D ? __ldcg(pt1 + (int64_t)k0 * D + col + i) : 0.0;
+                    for (int k = k0 + 1; k <= k1; k++)
+#pragma unroll
+                        for (int i = 0; i < 4; i++)
+                            if (col + i < D) t[i] = dadd(t[i], __ldcg(pt0 + (int64_t)k * D + col + i));
+                }
+                if (x == 0 && tid == 0) {
+                    fs = __ldcg(pf + 2 * k0 + 1);
+                    for (int k = k0 + 1; k <= k1; k++) fs += __ldcg(pf + 2 * k);
+                }
+                if (tid == 0) tf_ccnt[di * gx + x] = 0;
+            }
+        }
+        if (finish) {
+            const bool fresh = sp >= 0;  // seeded in this batch: S_tree starts empty
+            const int n = s_nfeat[slot];
+            float c2 = 0.f;
+            if (g == 0) {
+#pragma unroll
+                for (int i = 0; i < 4; i++) {
+                    const int cc = col + i;
+                    if (cc < D) {
+                        const double sum = fresh ? t[i] : dadd(S_tree[(int64_t)slot * D + cc], t[i]);
+                        S_tree[(int64_t)slot * D + cc] = sum;
+                        const float c32 = (float)ddiv(sum, (double)n);
+                        C32[(int64_t)slot * D + cc] = c32;
+                        c2 = fmaf(c32, c32, c2);
+                    }
+                }
+            }
+            c2 = warp_sum(c2);
+            if (lane == 0) s_c2[wid] = c2;
+            __syncthreads();
+            if (tid == 0) {
+                float cs2 = 0.f;
+                for (int w = 0; w < TF2_CT / 32; w++) cs2 += s_c2[w];
+                tf_cn2[(int64_t)di * gx + x] = cs2;
+                // fp32 norms: relative error < 1e-6, rounded up
+                if (x == 0) s_abs[slot] = (fresh ? 0.0 : s_abs[slot]) + fs * (1.0 + 1e-5);
+                __threadfence();
+                s_last = atomicAdd(&tf_cnt[di], 1) == gx - 1;
+            }
+            __syncthreads();
+            if (s_last && tid == 0) {  // last slice: ||C32||^2 in slice order, the drift bound
+                __threadfence();
+                float cs2 = 0.f;
+                for (int q = 0; q < gx; q++) cs2 += __ldcg(&tf_cn2[(int64_t)di * gx + q]);
+                s_cn2[slot] = cs2;
+                const double u = 1.1102230246251565e-16, nn = (double)n;
+                const double gam = nn * u / (1.0 - nn * u);
+                const double sa = __ldcg(&s_abs[slot]);
+                s_sdev[slot] = (2.0 * gam * sa / nn + 4.0 * u * sqrt((double)cs2) * 1.01) * 1.01 + 1e-300;
+                tf_cnt[di] = 0;
+            }
+        }
+        __syncthreads();
+    }
+}
+
 // ---------------------------------------------------------------------------
 // K2c: the reference's float64 running sums, bit for bit (clustering.py:56-59),
 // one batch behind on the engine's second stream: for each slot of the
@@ -3199,11 +3411,22 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             int32_t *meta = s->cd_meta.p + (size_t)buf * CD_NMETA * ldm;
             int32_t *coff = s->cd_off.p + (size_t)buf * ldm;
             const char **crows = s->cd_rows.p + (size_t)buf * s->B;
-            launch_pdl(k_tfold<T>, dim3((unsigned)gxt, (unsigned)gyt), dim3(TF_T), 0, st, D, c0, B, s->ctr.p, s->dirty.p,
-                       s->dirty_off.p, s->pend_list.p, s->frow.p, s->fnorm.p, s->s_nfeat.p, s->s_foldpos.p,
-                       s->s_seedpos.p, s->s_evicted.p, s->s_cid.p, s->s_size.p, s->S_tree.p, s->C32.p, s->s_cn2.p,
-                       s->s_abs.p, s->s_sdev.p, s->tf_cn2.p, s->tf_cnt.p, s->tf_part.p, s->tf_bcnt.p,
-                       s->cd_nd.p + buf, meta, ldm, coff, crows);
+            static const bool tf_old = getenv("FOCUS_B200_TFOLD_OLD") && atoi(getenv("FOCUS_B200_TFOLD_OLD"));
+            if (tf_old) {
+                launch_pdl(k_tfold<T>, dim3((unsigned)gxt, (unsigned)gyt), dim3(TF_T), 0, st, D, c0, B, s->ctr.p,
+                           s->dirty.p, s->dirty_off.p, s->pend_list.p, s->frow.p, s->fnorm.p, s->s_nfeat.p,
+                           s->s_foldpos.p, s->s_seedpos.p, s->s_evicted.p, s->s_cid.p, s->s_size.p, s->S_tree.p,
+                           s->C32.p, s->s_cn2.p, s->s_abs.p, s->s_sdev.p, s->tf_cn2.p, s->tf_cnt.p, s->tf_part.p,
+                           s->tf_bcnt.p, s->cd_nd.p + buf, meta, ldm, coff, crows);
+            } else {
+                const dim3 grid((unsigned)cdiv(D, TF2_COLS), (unsigned)cdiv(B, TF2_R));
+                auto kern = (s->rows_aligned16 && D % 4 == 0) ? k_tfold2<T, true> : k_tfold2<T, false>;
+                launch_pdl(kern, grid, dim3(TF2_T), 0, st, D, c0, s->ctr.p, s->dirty.p, s->dirty_off.p,
+                           s->pend_list.p, s->frow.p, s->fnorm.p, s->s_nfeat.p, s->s_foldpos.p, s->s_seedpos.p,
+                           s->s_evicted.p, s->s_cid.p, s->s_size.p, s->S_tree.p, s->C32.p, s->s_cn2.p, s->s_abs.p,
+                           s->s_sdev.p, s->tf_cn2.p, s->tf_cnt.p, s->tf_ccnt.p, s->tf_pt0.p, s->tf_pt1.p,
+                           s->tf_pf.p, s->cd_nd.p + buf, meta, ldm, coff, crows);
+            }
             FX_LAUNCHED();
             s->tstop();
             FX_CUDA(cudaEventRecord(s->ev_tf[buf], st));

@@ -89,6 +89,12 @@ class Stream:
         self._keep += [W, b]
         _lib.check(self.L.fx_stream_set_fc_head(self.handle, W.shape[0], _lib.pv(W), None if b is None else _lib.pv(b)))
 
+    def set_feature_noise(self, sigma: float, seed: int, in_dtype):
+        """The engine clusters extract_feature (classifiers.py:152-158) of the
+        raw feature rows fx_ingest receives, computed on the device."""
+        it = _lib.FX_F32 if np.dtype(in_dtype) == np.float32 else _lib.FX_F64
+        _lib.check(self.L.fx_stream_set_feature_noise(self.handle, float(sigma), seed & ((1 << 64) - 1), it))
+
     def dup_flags(self, fids: np.ndarray, sigs: np.ndarray) -> np.ndarray:
         n = fids.size
         out = np.zeros(n, np.uint8)
@@ -122,7 +128,7 @@ class Stream:
 
     COUNTERS = ("nlive", "next_cid", "dc", "nfree", "nevict_total", "exact", "nsnap", "nres", "ninserted",
                 "nevict_batch", "ndefer", "nod", "last_cid", "ndirty", "err", "fast", "fc_flagged", "ev_cursor",
-                "fast_state", "fast_done", "fast_batches", "cyc_passA", "cyc_passB", "cyc_passCD", "cyc_confirm", "cyc_passE", "cyc_seq", "windows", "seq_steps",
+                "fast_state", "fast_done", "fast_batches", "noise_flagged", "cyc_passA", "cyc_passB", "cyc_passCD", "cyc_confirm", "cyc_passE", "cyc_seq", "windows", "seq_steps",
                 "conf_b0", "conf_b1_7", "conf_b8_15", "conf_b16_31", "conf_b32_63", "conf_b64_127", "conf_b128",
                 "conf_young", "fold_wait_cyc", "fold_chain_cyc", "fold_slot_cyc", "fold_rows", "fold_slots")
     PHASES = ("k0_k1a", "screen", "resolve", "fold", "seal", "index", "batches", "screen_resid",
@@ -178,9 +184,12 @@ def _f32_exact(x: np.ndarray) -> bool:
 
 def ingest_arrays(oids, fids, sigs, feats, cfg: Config, profile, *, vocab: int, seed: int = 0,
                   pixel_eps: float = DEFAULT_PIXEL_EPS, true_class=None, topk=None, compact: bool = False,
-                  stream_id: str = "synthetic", device: int | None = None, batch: int = 0, fc_head=None):
+                  stream_id: str = "synthetic", device: int | None = None, batch: int = 0, fc_head=None,
+                  raw_features: bool = False):
     """Array-level ingest: the C-ABI call with host buffers.  `feats` rows are
-    the extracted features (float32 or float64); `true_class` (int32, -2 =
+    the extracted features (float32 or float64) -- or, with `raw_features`,
+    the objects' raw features (compact rows), extracted on the device with the
+    profile's noise (classifiers.py:152-158); `true_class` (int32, -2 =
     unlabeled) drives the device rank model, or `topk` (n x k encoded, OTHER =
     V) comes from an external classifier.  Returns (TopKIndex, IngestReport,
     Stream)."""
@@ -191,8 +200,15 @@ def ingest_arrays(oids, fids, sigs, feats, cfg: Config, profile, *, vocab: int, 
     sigs = np.ascontiguousarray(sigs, np.float64).reshape(n, S)
     D = feats.shape[1] if feats.ndim == 2 else 0
     feat_type = _lib.FX_F64 if feats.dtype == np.float64 else _lib.FX_F32
+    noise = raw_features and profile.feature_noise_sigma != 0.0
+    if noise:
+        if not compact:
+            raise ValueError("raw_features needs compact feature rows")
+        feat_type = _lib.FX_F64  # feature + float64 noise is float64 (numpy promotion)
     feats = np.ascontiguousarray(feats)
     st = Stream(D, S, vocab, cfg.k, cfg.t, cfg.m, pixel_eps, feat_type, device, batch)
+    if noise:
+        st.set_feature_noise(profile.feature_noise_sigma, seed, feats.dtype)
     if fc_head is not None:
         st.set_fc_head(fc_head)
     elif topk is None:
@@ -238,10 +254,12 @@ def ingest_stream(header, stream, cfg: Config, profiles, pixel_eps: float = DEFA
     dup = dup_flags(fids, sigs, pixel_eps)
     keep = np.flatnonzero(~dup)
     fc_head = classify_fn if isinstance(classify_fn, classifiers.FCHead) else None
+    raw = False
     if fc_head is not None:
         # K1b on the device: the head sees the extracted features and emits top-K
         topk, tcls = None, None
-        rows = [classifiers.extract_feature(profile, objs[i], seed) for i in keep.tolist()]
+        rows = None
+        F = classifiers.extract_features(profile, oids[keep], _raw_rows(objs, keep, D), seed)
     elif classify_fn is not None:
         # -1 = no class at that rank: a classifier may emit fewer than K
         # classes and the reference merges only those (clustering.py:65-69)
@@ -254,19 +272,40 @@ def ingest_stream(header, stream, cfg: Config, profiles, pixel_eps: float = DEFA
             rows.append(np.asarray(rc.feature))
         tcls = None
     else:
+        # the device rank model classifies; extract_feature runs on the device
+        # over the raw rows (the engine's feature-noise stage)
         topk = None
         tcls = np.array([-2 if o.true_class is None else o.true_class for o in objs], np.int32)
-        rows = [classifiers.extract_feature(profile, objs[i], seed) for i in keep.tolist()]
+        rows = None
+        F = _raw_rows(objs, keep, D)
+        raw = profile.feature_noise_sigma != 0.0
+    if rows is not None:  # classify_fn's features
+        for r in rows:
+            if np.shape(r)[0] != D:
+                raise DimensionMismatch(f"feature dim {np.shape(r)[0]} != engine dim {D}")
+        all32 = all(np.asarray(r).dtype == np.float32 for r in rows)
+        F = np.array(rows, dtype=np.float64).reshape(len(rows), D) if rows else np.zeros((0, D))
+        if all32:
+            F = F.astype(np.float32)
+    if fc_head is not None:
+        F = F.astype(np.float32)  # the K1b head consumes float32 rows
+    elif not raw and F.dtype != np.float32 and _f32_exact(F):
+        F = F.astype(np.float32)  # float64 values that are float32-exact: the TC screen path
+    idx, report, _ = ingest_arrays(oids, fids, sigs, F, cfg, profile, vocab=V, seed=seed, pixel_eps=pixel_eps,
+                                   true_class=tcls, topk=topk, compact=True, stream_id=header.stream_id,
+                                   fc_head=fc_head, raw_features=raw)
+    idx.header = IndexHeader(stream_id=header.stream_id, dim=D, vocab=V, n_objects=n, config=cfg)
+    return idx, report
+
+
+def _raw_rows(objs, keep, D) -> np.ndarray:
+    """The retained objects' raw feature rows (float32 if every row is
+    float32, else float64 -- numpy's promotion of the stacked rows)."""
+    rows = [objs[i].feature for i in keep.tolist()]
     for r in rows:
         if np.shape(r)[0] != D:
             raise DimensionMismatch(f"feature dim {np.shape(r)[0]} != engine dim {D}")
-    F = np.array(rows, dtype=np.float64).reshape(len(rows), D) if rows else np.zeros((0, D))
-    if all(np.asarray(r).dtype == np.float32 for r in rows) or _f32_exact(F):
-        F = F.astype(np.float32)
-    if fc_head is not None:
-        F = F.astype(np.float32)
-    idx, report, _ = ingest_arrays(oids, fids, sigs, F, cfg, profile, vocab=V, seed=seed, pixel_eps=pixel_eps,
-                                   true_class=tcls, topk=topk, compact=True, stream_id=header.stream_id,
-                                   fc_head=fc_head)
-    idx.header = IndexHeader(stream_id=header.stream_id, dim=D, vocab=V, n_objects=n, config=cfg)
-    return idx, report
+    if not rows:
+        return np.zeros((0, D), np.float32)
+    dt = np.float32 if all(np.asarray(r).dtype == np.float32 for r in rows) else np.float64
+    return np.ascontiguousarray(np.array(rows, dtype=dt).reshape(len(rows), D))

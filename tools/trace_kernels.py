@@ -62,3 +62,13 @@ tg = sum(v[1] for v in gaps.values())
 print(f"\ndevice span {span / 1e3:.2f} ms, idle gaps {tg / 1e3:.2f} ms")
 for k, v in sorted(gaps.items(), key=lambda x: -x[1][1])[:15]:
     print(f"{k:62s} {v[0]:6d} {v[1] / 1e3:8.3f} ms  avg {v[1] / v[0]:7.2f} us")
+
+# timeline of three steady-state batches (k_snap_pack starts each batch)
+marks = [i for i, e in enumerate(ev) if "k_snap_pack" in e[2]]
+if len(marks) > 160:
+    for bi in (150, 151, 152):
+        i0, i1 = marks[bi], marks[bi + 1]
+        t0 = ev[i0][0]
+        print(f"\nbatch {bi}: {(ev[i1][0] - t0) / 1e3 * 1e3:.1f} us")
+        for a, b, nm in ev[i0:i1]:
+            print(f"   {nm[:44]:44s} start {(a - t0):8.1f} us  end {(b - t0):8.1f} us  dur {(b - a):7.1f} us")
