@@ -228,7 +228,14 @@ int fx_stream_create(const fx_stream_config *cfg, fx_stream **out) {
                 const char *tm = getenv("FOCUS_B200_TIMERS");
                 s->timing = tm && strcmp(tm, "1") == 0;
             }
-            FX_CUDA(cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking));
+            // the batch chain runs at the highest stream priority, the lagged
+            // exact chain (st2) at the lowest: pending CTAs of the critical
+            // path are scheduled ahead of the chain's
+            int prio_lo = 0, prio_hi = 0;
+            FX_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
+            static const bool noprio = getenv("FOCUS_B200_NOPRIO") && atoi(getenv("FOCUS_B200_NOPRIO"));
+            if (noprio) prio_lo = prio_hi = 0;
+            FX_CUDA(cudaStreamCreateWithPriority(&s->st, cudaStreamNonBlocking, prio_hi));
             cur_stream() = s->st;
             const int D = cfg->dim;
             int B = cfg->batch;
@@ -256,7 +263,7 @@ int fx_stream_create(const fx_stream_config *cfg, fx_stream **out) {
             s->s_drift.reserve(ns);
             s->s_cn2.reserve(ns);
             {  // snapshot tree fold + lagged exact chain (k_tfold / k_fold on st2)
-                FX_CUDA(cudaStreamCreateWithFlags(&s->st2, cudaStreamNonBlocking));
+                FX_CUDA(cudaStreamCreateWithPriority(&s->st2, cudaStreamNonBlocking, prio_lo));
                 for (int i = 0; i < 2; i++) {
                     FX_CUDA(cudaEventCreateWithFlags(&s->ev_tf[i], cudaEventDisableTiming));
                     FX_CUDA(cudaEventCreateWithFlags(&s->ev_ch[i], cudaEventDisableTiming));
@@ -272,14 +279,8 @@ int fx_stream_create(const fx_stream_config *cfg, fx_stream **out) {
                 s->tf_cn2.reserve(nd * gx);
                 s->tf_cnt.reserve(nd);
                 FX_CUDA(cudaMemsetAsync(s->tf_cnt.p, 0, sizeof(int32_t) * nd, s->st));
-                {
-                    const size_t gx2 = (size_t)cdiv(D, 512), nch = (size_t)cdiv(B, 64);
-                    s->tf_ccnt.reserve(nd * gx2);
-                    FX_CUDA(cudaMemsetAsync(s->tf_ccnt.p, 0, sizeof(int32_t) * nd * gx2, s->st));
-                    s->tf_pt0.reserve(nch * D);
-                    s->tf_pt1.reserve(nch * D);
-                    s->tf_pf.reserve(2 * nch);
-                }
+                s->tf_P.reserve((size_t)B * D);
+                s->tf_PF.reserve((size_t)B);
                 s->cd_meta.reserve(2 * 8 * nd);
                 s->cd_off.reserve(2 * nd);
                 s->cd_rows.reserve(2 * (size_t)B);

@@ -2128,23 +2128,47 @@ __global__ void __launch_bounds__(RF_T) k_rfast1(ResolveArgs A) {
     int c = 0, d = 0;
     float su = 0.f, mx = 0.f, drift = 0.f;
     const int gg = tid;  // nsnap <= RF_MAXG = RF_T: one group per thread
+    // the group's slot state, fetched before the chunk scan
+    int g_sl = 0, g_nf = 0;
+    float g_cn2 = 0.f;
+    double g_sdev = 0.0;
     if (gg < nsnap) {
-        for (int k = 0; k < nch; k++) {
-            const int idx = k * RF_MAXG + gg;
-            const int ck = __ldcg(A.f_ccnt + idx), dk = __ldcg(A.f_cdup + idx);
-            const float sk = __ldcg(A.f_csum + idx), mk = __ldcg(A.f_cmax + idx);
-            A.f_ccnt[idx] = c;
-            A.f_cdup[idx] = d;
-            A.f_csum[idx] = su;
-            c += ck;
-            d += dk;
-            su = __fadd_ru(su, sk);
-            mx = fmaxf(mx, mk);
+        g_sl = A.snap_slot[gg];
+        g_cn2 = A.s_cn2[g_sl];
+        g_sdev = A.s_sdev[g_sl];
+        g_nf = A.s_nfeat[g_sl];
+    }
+    if (gg < nsnap) {
+        // chunk totals -> exclusive bases; 8 chunks' loads in flight before
+        // the dependent scan (the stores would otherwise serialise them)
+        for (int k0 = 0; k0 < nch; k0 += 8) {
+            int ck[8], dk[8];
+            float sk[8], mk[8];
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                const int idx = (k0 + u) * RF_MAXG + gg;
+                const bool in = k0 + u < nch;
+                ck[u] = in ? __ldcg(A.f_ccnt + idx) : 0;
+                dk[u] = in ? __ldcg(A.f_cdup + idx) : 0;
+                sk[u] = in ? __ldcg(A.f_csum + idx) : 0.f;
+                mk[u] = in ? __ldcg(A.f_cmax + idx) : 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                if (k0 + u >= nch) break;
+                const int idx = (k0 + u) * RF_MAXG + gg;
+                A.f_ccnt[idx] = c;
+                A.f_cdup[idx] = d;
+                A.f_csum[idx] = su;
+                c += ck[u];
+                d += dk[u];
+                su = __fadd_ru(su, sk[u]);
+                mx = fmaxf(mx, mk[u]);
+            }
         }
-        const int sl = A.snap_slot[gg];
-        const float cn = sqrtf(A.s_cn2[sl]) * 1.00001f;
-        const float d0 = __double2float_ru(A.s_sdev[sl]);  // k_resolve's prologue: s_drift = s_sdev
-        drift = c > 0 ? drift_avg(d0, A.s_nfeat[sl], su, c, cn, mx) : d0;
+        const float cn = sqrtf(g_cn2) * 1.00001f;
+        const float d0 = __double2float_ru(g_sdev);  // k_resolve's prologue: s_drift = s_sdev
+        drift = c > 0 ? drift_avg(d0, g_nf, su, c, cn, mx) : d0;
         A.f_gi[gg * 4 + 0] = c;
         A.f_gi[gg * 4 + 1] = d;
         A.f_gf[gg * 4 + 0] = drift;
@@ -2590,215 +2614,181 @@ __global__ void __launch_bounds__(TF_T) k_tfold(int D, int64_t c0, int B, const 
     }
 }
 
-// K2c' (current): the same snapshot tree fold, load-balanced.  The batch's
-// pending rows (pend_list, grouped by dirty slot through dirty_off) are cut
-// into fixed chunks of TF2_R rows; CTA (x, c) sums chunk c's rows over column
-// slice x (512 columns: 128 column threads x 4 columns, 4 row groups).  A slot
-// whose rows lie inside one chunk is finished by that CTA; a slot spanning
-// chunks has each chunk's partial written to scratch (pt0[c] when the slot
-// began before chunk c, pt1[c] when it begins inside c and runs past it) and
-// the last chunk to arrive sums the partials in chunk order.  Every order is
-// fixed (deterministic); the float64 tree-order sum is within the Higham
-// bound of the reference's sequential sum whatever the order.
+// K2c' (current): the snapshot tree fold in two load-balanced passes.
+//   k_tfold_a: CTA (slice x of 512 columns, chunk c of TF3_R pending rows),
+//     one column per thread: the chunk's rows are summed in row order per
+//     "piece" (the part of one dirty slot's row range inside the chunk; a new
+//     piece starts at the chunk start and at every slot boundary) and each
+//     piece's float64 column sums go to P[piece start row] (its fp32-norm sum
+//     to PF).  Row pointers and piece starts are staged in shared memory; 16
+//     row loads per thread are in flight.
+//   k_tfold_b: CTA (slice x, dirty slot di): the slot's pieces (start j0, then
+//     every chunk boundary inside [j0, j1)) are added in row order, then the
+//     slot's S_tree / C32 / norms / drift bound are refreshed as in k_tfold.
+// Every order is fixed (deterministic); whatever the order, the float64 sum
+// is within the Higham bound of the reference's sequential sum (s_sdev).
 // ---------------------------------------------------------------------------
-constexpr int TF2_T = 512, TF2_G = 4, TF2_CT = 128, TF2_COLS = 4 * TF2_CT, TF2_R = 64;
+constexpr int TF3_T = 512, TF3_R = 64;
 
-template <typename T, bool VEC>
-__device__ __forceinline__ void tf2_load4(const char *row, int col, int D, double v[4]) {
-    if (VEC && sizeof(T) == 4) {
-        const float4 q = __ldg((const float4 *)((const float *)row + col));
-        v[0] = q.x;
-        v[1] = q.y;
-        v[2] = q.z;
-        v[3] = q.w;
-    } else if (VEC) {
-        const double2 a = __ldg((const double2 *)((const double *)row + col));
-        const double2 b = __ldg((const double2 *)((const double *)row + col) + 1);
-        v[0] = a.x;
-        v[1] = a.y;
-        v[2] = b.x;
-        v[3] = b.y;
-    } else {
-#pragma unroll
-        for (int i = 0; i < 4; i++) v[i] = col + i < D ? to_d(((const T *)row)[col + i]) : 0.0;
-    }
-}
-
-template <typename T, bool VEC>
-__global__ void __launch_bounds__(TF2_T) k_tfold2(
-    int D, int64_t c0, const int64_t *__restrict__ ctr, const int32_t *__restrict__ dirty,
-    const int32_t *__restrict__ dirty_off, const int32_t *__restrict__ pend_list, const char *const *__restrict__ frow,
-    const float *__restrict__ fnorm, const int32_t *__restrict__ s_nfeat, const int32_t *__restrict__ s_foldpos,
-    const int32_t *__restrict__ s_seedpos, const int32_t *__restrict__ s_evicted, const int32_t *__restrict__ s_cid,
-    const int32_t *__restrict__ s_size, double *__restrict__ S_tree, float *__restrict__ C32,
-    float *__restrict__ s_cn2, double *__restrict__ s_abs, double *__restrict__ s_sdev, float *__restrict__ tf_cn2,
-    int32_t *__restrict__ tf_cnt, int32_t *__restrict__ tf_ccnt, double *__restrict__ pt0,
-    double *__restrict__ pt1, double *__restrict__ pf, int64_t *__restrict__ cd_nd, int32_t *__restrict__ cd_meta,
-    int ldm, int32_t *__restrict__ cd_off, const char **__restrict__ cd_rows) {
+template <typename T>
+__global__ void __launch_bounds__(TF3_T) k_tfold_a(int D, int64_t c0, const int64_t *__restrict__ ctr,
+                                                   const int32_t *__restrict__ dirty,
+                                                   const int32_t *__restrict__ dirty_off,
+                                                   const int32_t *__restrict__ pend_list,
+                                                   const char *const *__restrict__ frow,
+                                                   const float *__restrict__ fnorm,
+                                                   const int32_t *__restrict__ s_foldpos, double *__restrict__ P,
+                                                   double *__restrict__ PF, const char **__restrict__ cd_rows) {
     pdl_enter();
-    __shared__ double red[TF2_G][TF2_COLS];
-    __shared__ double s_f[TF2_T / 32];
-    __shared__ float s_c2[TF2_T / 32];
-    __shared__ int s_last;
+    __shared__ const T *s_row[TF3_R];
+    __shared__ float s_fn[TF3_R];
+    __shared__ int s_start[TF3_R];
     const int nd = (int)ctr[C_NDIRTY];
-    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-    const int g = tid / TF2_CT, ct = tid % TF2_CT;
-    const int gx = gridDim.x, x = blockIdx.x, c = blockIdx.y, nch = gridDim.y;
+    const int tid = threadIdx.x, x = blockIdx.x, c = blockIdx.y;
     const int Btot = dirty_off[nd];
-    const int cs = c * TF2_R, ce = min(Btot, cs + TF2_R);
-    const bool lastc = c == nch - 1;
-    const int col = x * TF2_COLS + ct * 4;
-    if (x == 0 && c == 0 && tid == 0) {
-        *cd_nd = nd;
-        cd_off[nd] = Btot;
+    const int cs = c * TF3_R, nr = min(TF3_R, Btot - cs);
+    if (nr <= 0) return;
+    if (tid < nr) {
+        const int j = cs + tid;
+        int lo = 0, hi = nd - 1;  // the segment holding row j: last di with dirty_off[di] <= j
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (dirty_off[mid] <= j) lo = mid; else hi = mid - 1;
+        }
+        const int p = pend_list[j];
+        const char *r = frow[c0 + p];
+        s_row[tid] = (const T *)r;
+        s_fn[tid] = fnorm[c0 + p];
+        s_start[tid] = (tid == 0 || dirty_off[lo] == j) ? 1 : 0;
+        if (x == 0) cd_rows[j] = p >= s_foldpos[dirty[lo]] ? r : nullptr;
     }
-    // a non-empty segment [j0, j1) belongs to chunks j0/R .. (j1-1)/R; an empty
-    // one (an evicted slot without rows) to chunk min(j0/R, last)
-    int lo = 0, hi = nd;  // first di with dirty_off[di+1] >= cs
-    while (lo < hi) {
-        const int mid = (lo + hi) >> 1;
-        if (dirty_off[mid + 1] >= cs) hi = mid; else lo = mid + 1;
-    }
-    for (int di = lo; di < nd; di++) {
-        const int j0 = dirty_off[di], j1 = dirty_off[di + 1];
-        if (!lastc && j0 >= ce) break;
-        const bool member = j0 < j1 ? (j0 / TF2_R <= c && c <= (j1 - 1) / TF2_R) : min(j0 / TF2_R, nch - 1) == c;
-        if (!member) continue;
-        const int slot = dirty[di];
-        const int fp = s_foldpos[slot], sp = s_seedpos[slot], ev = s_evicted[slot];
-        const int ra = max(j0, cs), rb = min(j1, ce);
-        if (x == 0) {  // chain descriptor: rows of this chunk, the slot's meta from its first chunk
-            for (int j = ra + tid; j < rb; j += TF2_T) {
-                const int p = pend_list[j];
-                cd_rows[j] = p >= fp ? frow[c0 + p] : nullptr;
-            }
-            if (tid == 0 && j0 >= cs) {
-                cd_off[di] = j0;
-                cd_meta[CD_SLOT * ldm + di] = slot;
-                cd_meta[CD_NFEAT * ldm + di] = s_nfeat[slot];
-                cd_meta[CD_FP * ldm + di] = fp;
-                cd_meta[CD_SP * ldm + di] = sp;
-                cd_meta[CD_EV * ldm + di] = ev;
-                cd_meta[CD_CID * ldm + di] = s_cid[slot];
-                cd_meta[CD_SIZE * ldm + di] = s_size[slot];
-            }
-        }
-        if (ev) continue;  // evicted: no snapshot (its exact centroid comes from the chain)
-        // column sums of rows [ra, rb): row group g takes rows ra+g, ra+g+4, ...
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-        if (col < D) {
-            int j = ra + g;
-            for (; j + 7 * TF2_G < rb; j += 8 * TF2_G) {
-                double v[8][4];
+    __syncthreads();
+    const int col = x * TF3_T + tid;
+    if (col < D) {
+        double acc = 0.0;
+        int ps = 0;
+        for (int r0 = 0; r0 < nr; r0 += 16) {
+            double v[16];
 #pragma unroll
-                for (int u = 0; u < 8; u++) tf2_load4<T, VEC>(frow[c0 + pend_list[j + u * TF2_G]], col, D, v[u]);
+            for (int u = 0; u < 16; u++) v[u] = r0 + u < nr ? to_d(__ldg(s_row[r0 + u] + col)) : 0.0;
 #pragma unroll
-                for (int u = 0; u < 8; u++)
-#pragma unroll
-                    for (int i = 0; i < 4; i++) acc[i] = dadd(acc[i], v[u][i]);
-            }
-            for (; j < rb; j += TF2_G) {
-                double v[4];
-                tf2_load4<T, VEC>(frow[c0 + pend_list[j]], col, D, v);
-#pragma unroll
-                for (int i = 0; i < 4; i++) acc[i] = dadd(acc[i], v[i]);
-            }
-        }
-#pragma unroll
-        for (int i = 0; i < 4; i++) red[g][ct * 4 + i] = acc[i];
-        double fs = 0.0;  // sum of the rows' fp32 norms (slice 0)
-        if (x == 0) {
-            for (int j = ra + tid; j < rb; j += TF2_T) fs += (double)fnorm[c0 + pend_list[j]];
-            fs = warp_sum(fs);
-            if (lane == 0) s_f[wid] = fs;
-        }
-        __syncthreads();
-        double t[4];
-        if (g == 0) {
-#pragma unroll
-            for (int i = 0; i < 4; i++)
-                t[i] = dadd(dadd(dadd(red[0][ct * 4 + i], red[1][ct * 4 + i]), red[2][ct * 4 + i]), red[3][ct * 4 + i]);
-        }
-        if (x == 0 && tid == 0) {
-            fs = 0.0;
-            for (int w = 0; w < TF2_T / 32; w++) fs += s_f[w];
-        }
-        const bool whole = j0 >= cs && j1 <= ce;
-        bool finish = true;
-        if (!whole) {  // publish this chunk's partial; the slot's last chunk combines in chunk order
-            double *dst = (j0 < cs ? pt0 : pt1) + (int64_t)c * D;
-            if (g == 0 && col < D) {
-#pragma unroll
-                for (int i = 0; i < 4; i++)
-                    if (col + i < D) dst[col + i] = t[i];
-            }
-            if (x == 0 && tid == 0) pf[2 * c + (j0 < cs ? 0 : 1)] = fs;
-            __threadfence();
-            __syncthreads();
-            const int k0 = j0 / TF2_R, k1 = (j1 - 1) / TF2_R;
-            if (tid == 0) s_last = atomicAdd(&tf_ccnt[di * gx + x], 1) == k1 - k0;
-            __syncthreads();
-            finish = s_last;
-            if (finish) {
-                __threadfence();
-                if (g == 0 && col < D) {
-#pragma unroll
-                    for (int i = 0; i < 4; i++) t[i] = col + i < D ? __ldcg(pt1 + (int64_t)k0 * D + col + i) : 0.0;
-                    for (int k = k0 + 1; k <= k1; k++)
-#pragma unroll
-                        for (int i = 0; i < 4; i++)
-                            if (col + i < D) t[i] = dadd(t[i], __ldcg(pt0 + (int64_t)k * D + col + i));
-                }
-                if (x == 0 && tid == 0) {
-                    fs = __ldcg(pf + 2 * k0 + 1);
-                    for (int k = k0 + 1; k <= k1; k++) fs += __ldcg(pf + 2 * k);
-                }
-                if (tid == 0) tf_ccnt[di * gx + x] = 0;
-            }
-        }
-        if (finish) {
-            const bool fresh = sp >= 0;  // seeded in this batch: S_tree starts empty
-            const int n = s_nfeat[slot];
-            float c2 = 0.f;
-            if (g == 0) {
-#pragma unroll
-                for (int i = 0; i < 4; i++) {
-                    const int cc = col + i;
-                    if (cc < D) {
-                        const double sum = fresh ? t[i] : dadd(S_tree[(int64_t)slot * D + cc], t[i]);
-                        S_tree[(int64_t)slot * D + cc] = sum;
-                        const float c32 = (float)ddiv(sum, (double)n);
-                        C32[(int64_t)slot * D + cc] = c32;
-                        c2 = fmaf(c32, c32, c2);
+            for (int u = 0; u < 16; u++) {
+                const int r = r0 + u;
+                if (r < nr) {
+                    if (s_start[r]) {
+                        if (r > 0) P[(int64_t)(cs + ps) * D + col] = acc;
+                        acc = v[u];
+                        ps = r;
+                    } else {
+                        acc = dadd(acc, v[u]);
                     }
                 }
             }
-            c2 = warp_sum(c2);
-            if (lane == 0) s_c2[wid] = c2;
-            __syncthreads();
-            if (tid == 0) {
-                float cs2 = 0.f;
-                for (int w = 0; w < TF2_CT / 32; w++) cs2 += s_c2[w];
-                tf_cn2[(int64_t)di * gx + x] = cs2;
-                // fp32 norms: relative error < 1e-6, rounded up
-                if (x == 0) s_abs[slot] = (fresh ? 0.0 : s_abs[slot]) + fs * (1.0 + 1e-5);
-                __threadfence();
-                s_last = atomicAdd(&tf_cnt[di], 1) == gx - 1;
-            }
-            __syncthreads();
-            if (s_last && tid == 0) {  // last slice: ||C32||^2 in slice order, the drift bound
-                __threadfence();
-                float cs2 = 0.f;
-                for (int q = 0; q < gx; q++) cs2 += __ldcg(&tf_cn2[(int64_t)di * gx + q]);
-                s_cn2[slot] = cs2;
-                const double u = 1.1102230246251565e-16, nn = (double)n;
-                const double gam = nn * u / (1.0 - nn * u);
-                const double sa = __ldcg(&s_abs[slot]);
-                s_sdev[slot] = (2.0 * gam * sa / nn + 4.0 * u * sqrt((double)cs2) * 1.01) * 1.01 + 1e-300;
-                tf_cnt[di] = 0;
-            }
         }
-        __syncthreads();
+        P[(int64_t)(cs + ps) * D + col] = acc;
+    }
+    if (x == 0 && tid == 0) {  // the pieces' fp32-norm sums
+        double f = 0.0;
+        int ps = 0;
+        for (int r = 0; r < nr; r++) {
+            if (s_start[r] && r > 0) {
+                PF[cs + ps] = f;
+                f = 0.0;
+                ps = r;
+            }
+            f += (double)s_fn[r];
+        }
+        PF[cs + ps] = f;
+    }
+}
+
+__global__ void __launch_bounds__(TF3_T) k_tfold_b(
+    int D, const int64_t *__restrict__ ctr, const int32_t *__restrict__ dirty, const int32_t *__restrict__ dirty_off,
+    const int32_t *__restrict__ s_nfeat, const int32_t *__restrict__ s_foldpos, const int32_t *__restrict__ s_seedpos,
+    const int32_t *__restrict__ s_evicted, const int32_t *__restrict__ s_cid, const int32_t *__restrict__ s_size,
+    const double *__restrict__ P, const double *__restrict__ PF, double *__restrict__ S_tree, float *__restrict__ C32,
+    float *__restrict__ s_cn2, double *__restrict__ s_abs, double *__restrict__ s_sdev, float *__restrict__ tf_cn2,
+    int32_t *__restrict__ tf_cnt, int64_t *__restrict__ cd_nd, int32_t *__restrict__ cd_meta, int ldm,
+    int32_t *__restrict__ cd_off) {
+    pdl_enter();
+    __shared__ float s_c2[TF3_T / 32];
+    __shared__ int s_last;
+    const int nd = (int)ctr[C_NDIRTY];
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    const int x = blockIdx.x, gx = gridDim.x;
+    if (x == 0 && blockIdx.y == 0 && tid == 0) {
+        *cd_nd = nd;
+        cd_off[nd] = dirty_off[nd];
+    }
+    for (int di = blockIdx.y; di < nd; di += gridDim.y) {
+    const int j0 = dirty_off[di], j1 = dirty_off[di + 1];
+    const int slot = dirty[di];
+    const int sp = s_seedpos[slot], ev = s_evicted[slot];
+    if (x == 0 && tid == 0) {  // the lagged chain's descriptor
+        cd_off[di] = j0;
+        cd_meta[CD_SLOT * ldm + di] = slot;
+        cd_meta[CD_NFEAT * ldm + di] = s_nfeat[slot];
+        cd_meta[CD_FP * ldm + di] = s_foldpos[slot];
+        cd_meta[CD_SP * ldm + di] = sp;
+        cd_meta[CD_EV * ldm + di] = ev;
+        cd_meta[CD_CID * ldm + di] = s_cid[slot];
+        cd_meta[CD_SIZE * ldm + di] = s_size[slot];
+    }
+    if (ev) continue;  // evicted: no snapshot (its exact centroid comes from the chain)
+    const int np = j1 > j0 ? (j1 - 1) / TF3_R - j0 / TF3_R + 1 : 0;
+    auto pstart = [&](int k) { return k == 0 ? j0 : (j0 / TF3_R + k) * TF3_R; };
+    const int col = x * TF3_T + tid;
+    double t = 0.0;
+    if (col < D) {
+        for (int k0 = 0; k0 < np; k0 += 16) {
+            double v[16];
+#pragma unroll
+            for (int u = 0; u < 16; u++) v[u] = k0 + u < np ? __ldcg(P + (int64_t)pstart(k0 + u) * D + col) : 0.0;
+#pragma unroll
+            for (int u = 0; u < 16; u++)
+                if (k0 + u < np) t = (k0 + u == 0) ? v[u] : dadd(t, v[u]);
+        }
+    }
+    double fs = 0.0;
+    if (x == 0 && wid == 0) {
+        for (int k = lane; k < np; k += 32) fs += __ldcg(PF + pstart(k));
+        fs = warp_sum(fs);
+    }
+    const bool fresh = sp >= 0;  // seeded in this batch: S_tree starts empty
+    const int n = s_nfeat[slot];
+    float c2 = 0.f;
+    if (col < D) {
+        const double sum = fresh ? t : dadd(S_tree[(int64_t)slot * D + col], t);
+        S_tree[(int64_t)slot * D + col] = sum;
+        const float c32 = (float)ddiv(sum, (double)n);
+        C32[(int64_t)slot * D + col] = c32;
+        c2 = c32 * c32;
+    }
+    c2 = warp_sum(c2);
+    if (lane == 0) s_c2[wid] = c2;
+    __syncthreads();
+    if (tid == 0) {
+        float cs2 = 0.f;
+        for (int w = 0; w < TF3_T / 32; w++) cs2 += s_c2[w];
+        tf_cn2[(int64_t)di * gx + x] = cs2;
+        // fp32 norms: relative error < 1e-6, rounded up
+        if (x == 0) s_abs[slot] = (fresh ? 0.0 : s_abs[slot]) + fs * (1.0 + 1e-5);
+        __threadfence();
+        s_last = atomicAdd(&tf_cnt[di], 1) == gx - 1;
+    }
+    __syncthreads();
+    if (s_last && tid == 0) {  // last slice: ||C32||^2 in slice order, the drift bound
+        __threadfence();
+        float cs2 = 0.f;
+        for (int q = 0; q < gx; q++) cs2 += __ldcg(&tf_cn2[(int64_t)di * gx + q]);
+        s_cn2[slot] = cs2;
+        const double u = 1.1102230246251565e-16, nn = (double)n;
+        const double gam = nn * u / (1.0 - nn * u);
+        const double sa = __ldcg(&s_abs[slot]);
+        s_sdev[slot] = (2.0 * gam * sa / nn + 4.0 * u * sqrt((double)cs2) * 1.01) * 1.01 + 1e-300;
+        tf_cnt[di] = 0;
+    }
+    __syncthreads();
     }
 }
 
@@ -3333,7 +3323,15 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             int64_t known = 0;
             if (s->batch_no >= 2) {
                 const int slot_old = (int)((s->batch_no - 2) % 3);
+                static const double stall_ms = getenv("FOCUS_B200_STALL") ? atof(getenv("FOCUS_B200_STALL")) : 0.0;
+                const auto w0 = hclock::now();
                 FX_CUDA(cudaEventSynchronize(s->ring_ev[slot_old]));
+                if (stall_ms > 0.0) {
+                    const double w = hms(w0, hclock::now()), lb = hms(h0, w0);
+                    if (w > stall_ms || lb > stall_ms)
+                        fprintf(stderr, "STALL engine %p batch %ld: ring sync %.1f ms, launches before it %.1f ms\n",
+                                (void *)s, (long)s->batch_no, w, lb);
+                }
                 known = s->h_ctr_ring[slot_old * C_COUNT + C_NEXT_CID];
             }
             s->batch_no++;
@@ -3419,20 +3417,24 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
                            s->C32.p, s->s_cn2.p, s->s_abs.p, s->s_sdev.p, s->tf_cn2.p, s->tf_cnt.p, s->tf_part.p,
                            s->tf_bcnt.p, s->cd_nd.p + buf, meta, ldm, coff, crows);
             } else {
-                const dim3 grid((unsigned)cdiv(D, TF2_COLS), (unsigned)cdiv(B, TF2_R));
-                auto kern = (s->rows_aligned16 && D % 4 == 0) ? k_tfold2<T, true> : k_tfold2<T, false>;
-                launch_pdl(kern, grid, dim3(TF2_T), 0, st, D, c0, s->ctr.p, s->dirty.p, s->dirty_off.p,
-                           s->pend_list.p, s->frow.p, s->fnorm.p, s->s_nfeat.p, s->s_foldpos.p, s->s_seedpos.p,
-                           s->s_evicted.p, s->s_cid.p, s->s_size.p, s->S_tree.p, s->C32.p, s->s_cn2.p, s->s_abs.p,
-                           s->s_sdev.p, s->tf_cn2.p, s->tf_cnt.p, s->tf_ccnt.p, s->tf_pt0.p, s->tf_pt1.p,
-                           s->tf_pf.p, s->cd_nd.p + buf, meta, ldm, coff, crows);
+                const unsigned gx3 = (unsigned)cdiv(D, TF3_T);
+                launch_pdl(k_tfold_a<T>, dim3(gx3, (unsigned)cdiv(B, TF3_R)), dim3(TF3_T), 0, st, D, c0, s->ctr.p,
+                           s->dirty.p, s->dirty_off.p, s->pend_list.p, s->frow.p, s->fnorm.p, s->s_foldpos.p,
+                           s->tf_P.p, s->tf_PF.p, crows);
+                FX_LAUNCHED();
+                launch_pdl(k_tfold_b, dim3(gx3, (unsigned)std::min<int64_t>(2 * (int64_t)B + 3, std::max<int64_t>(64, 1184 / gx3))), dim3(TF3_T), 0, st, D, s->ctr.p, s->dirty.p,
+                           s->dirty_off.p, s->s_nfeat.p, s->s_foldpos.p, s->s_seedpos.p, s->s_evicted.p, s->s_cid.p,
+                           s->s_size.p, s->tf_P.p, s->tf_PF.p, s->S_tree.p, s->C32.p, s->s_cn2.p, s->s_abs.p,
+                           s->s_sdev.p, s->tf_cn2.p, s->tf_cnt.p, s->cd_nd.p + buf, meta, ldm, coff);
             }
             FX_LAUNCHED();
             s->tstop();
             FX_CUDA(cudaEventRecord(s->ev_tf[buf], st));
             FX_CUDA(cudaStreamWaitEvent(s->st2, s->ev_tf[buf], 0));
             const int64_t gx = cdiv(D, FD);
-            const int64_t gy = std::max<int64_t>(8, std::min<int64_t>(2 * (int64_t)B + 1, (148 * 12) / gx));
+            static const int fold_gy = getenv("FOCUS_B200_FOLD_GY") ? atoi(getenv("FOCUS_B200_FOLD_GY")) : 0;
+            const int64_t gy = fold_gy > 0 ? std::min<int64_t>(fold_gy, 2 * (int64_t)B + 1)
+                                           : std::max<int64_t>(8, std::min<int64_t>(2 * (int64_t)B + 1, (148 * 12) / gx));
             static bool fold_attr[64] = {};
             if (!fold_attr[dev_slot()]) {
                 FX_CUDA(cudaFuncSetAttribute(k_fold<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fold_smem<T>()));

@@ -26,6 +26,9 @@ def main():
     ap.add_argument("--verify", action="store_true", help="compare every run's results with the first (solo) run")
     ap.add_argument("--counters", action="store_true", help="print each engine's resolve/fold counters")
     ap.add_argument("--trace", type=int, default=0, help="CUPTI-trace this many extra runs at the largest N")
+    ap.add_argument("--trace-stall", type=int, default=0,
+                    help="trace up to this many runs at the largest N; report the longest device activities of a "
+                         "run slower than 1 s")
     a = ap.parse_args()
     ns = [int(x) for x in a.streams.split(",")]
     nmax = max(ns)
@@ -81,6 +84,31 @@ def main():
                 print(f"N={n} rep={r} wall={dt*1e3:.1f} ms  {n * a.objects / dt / 1e6:.2f} M obj/s  "
                       f"max create={mx[0]*1e3:.1f} ingest={mx[1]*1e3:.1f} finalize={mx[2]*1e3:.1f} "
                       f"destroy={mx[3]*1e3:.1f} ms", flush=True)
+        for r in range(a.trace_stall):
+            from torch.profiler import ProfilerActivity, profile
+            with profile(activities=[ProfilerActivity.CUDA]) as p:
+                t0 = time.perf_counter()
+                list(pool.map(one, range(nmax)))
+                torch.cuda.synchronize()
+                dt = time.perf_counter() - t0
+            print(f"STALLPROBE run {r}: wall {dt*1e3:.1f} ms", flush=True)
+            if dt < 1.0:
+                continue
+            ev = sorted([(e.time_range.start, e.time_range.end, e.name.split("(")[0].replace("void ", "")[:60])
+                         for e in p.events() if e.device_type == torch.autograd.DeviceType.CUDA], key=lambda x: x[0])
+            t00 = ev[0][0]
+            longest = sorted(ev, key=lambda x: x[0] - x[1])[:12]
+            for s0, s1, nm in longest:
+                print(f"   {nm:60s} start {(s0 - t00)/1e3:10.3f} ms dur {(s1 - s0)/1e3:10.3f} ms", flush=True)
+            # idle stretches of the whole device
+            busy_end, gaps = ev[0][1], []
+            for s0, s1, nm in ev[1:]:
+                if s0 > busy_end:
+                    gaps.append((s0 - busy_end, busy_end - t00, nm))
+                busy_end = max(busy_end, s1)
+            for g, at, nm in sorted(gaps, reverse=True)[:8]:
+                print(f"   device idle {g/1e3:10.3f} ms at {at/1e3:10.3f} ms (then {nm})", flush=True)
+            break
         for r in range(a.trace):
             from torch.profiler import ProfilerActivity, profile
             with profile(activities=[ProfilerActivity.CUDA]) as p:
