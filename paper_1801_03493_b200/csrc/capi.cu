@@ -303,7 +303,7 @@ int fx_stream_create(const fx_stream_config *cfg, fx_stream **out) {
             s->dres.reserve((size_t)B * B);
             s->dod.reserve((size_t)B * B);
             for (auto *b : {&s->res_col, &s->res_pos, &s->slot_of, &s->pend_rank, &s->evict_slot, &s->evict_cid,
-                            &s->pend_list, &s->sum_slot, &s->sum_q})
+                            &s->pend_list, &s->pend_seg, &s->sum_slot, &s->sum_q})
                 b->reserve(B + 1);
             for (auto *b : {&s->sum_d1, &s->sum_e1, &s->sum_lbr}) b->reserve(B + 1);
             for (auto *b : {&s->ev_pos, &s->ev_vic}) b->reserve(B + 1);

@@ -103,7 +103,7 @@ struct fx_stream {
     fx::DevBuf<float> dres;    // [B*B]
     fx::DevBuf<int32_t> res_col, res_pos;
     fx::DevBuf<float> dod;     // [B*B] on-demand columns
-    fx::DevBuf<int32_t> slot_of, pend_rank, evict_slot, evict_cid, dirty, dirty_off, pend_list, sum_slot, sum_q;
+    fx::DevBuf<int32_t> slot_of, pend_rank, evict_slot, evict_cid, dirty, dirty_off, pend_list, pend_seg, sum_slot, sum_q;
     fx::DevBuf<float> sum_d1, sum_e1, sum_lbr;
     // resolve fast path scratch (k_rfast1 / k_rfast3)
     fx::DevBuf<int32_t> f_rank, f_dup, f_ccnt, f_cdup, f_gi;

@@ -340,6 +340,7 @@ struct ResolveArgs {
     int32_t *live, *live_pos, *free_stack, *defer_free, *snap_slot;
     int64_t *ctr;
     int32_t *slot_of, *pend_rank, *evict_slot, *evict_cid, *dirty, *dirty_off, *pend_list;
+    int32_t *pend_seg;  // [B] dirty index of each pend_list entry
     int32_t *cid_slot, *s_fjoin, *ev_pos, *ev_vic;  // eviction FIFO: slot of each cid, first join, plan
     int32_t *cluster_of, *mrank, *frank;
     const PwPlan *plan;
@@ -880,6 +881,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
         if (threadIdx.x == 0) A.ctr[C_FASTST] = 0;
         if (fst == 1) return;
     }
+
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int B = A.B;
     const int BC = A.Bcap;  // layout by capacity (multiple of 64): every array stays aligned
@@ -1976,7 +1978,9 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
         int32_t *__restrict__ pend_list = A.pend_list;
         for (int bb = tid; bb < B; bb += blockDim.x) {
             const int slot = sh_slot_of[bb];
-            pend_list[cnt[s_didx[slot]] + pend_rank[bb]] = bb;
+            const int di = s_didx[slot];
+            pend_list[cnt[di] + pend_rank[bb]] = bb;
+            A.pend_seg[cnt[di] + pend_rank[bb]] = di;
         }
     }
     for (int q = tid; q < s_L; q += blockDim.x) A.snap_slot[q] = A.live[q];
@@ -2280,14 +2284,14 @@ __global__ void __launch_bounds__(RF_T) k_rfast3(ResolveArgs A) {
     __shared__ int s_last, s_fail;
     const int tid = threadIdx.x;
     int64_t *ctr = A.ctr;
-    if (ctr[C_FASTST] == 2) return;  // k_rfast1 declined
+    const bool declined = ctr[C_FASTST] == 2;  // k_rfast1 declined
     const int B = A.B;
     const double md1 = A.f_gd[0], md2 = A.f_gd[1];
     const int md1g = (int)A.f_gd[2];
     if (tid == 0) s_fail = 0;
     __syncthreads();
     const int p = blockIdx.x * RF_T + tid;
-    if (p < B) {
+    if (p < B && !declined) {
         const int g = A.sum_q[p];
         const int idx = blockIdx.x * RF_MAXG + g;
         const int i = A.f_ccnt[idx] + A.f_rank[p];
@@ -2309,6 +2313,7 @@ __global__ void __launch_bounds__(RF_T) k_rfast3(ResolveArgs A) {
             A.pend_rank[p] = i;
             A.slot_of[p] = sl;
             A.pend_list[A.f_gi[g * 4 + 3] + i] = p;
+            A.pend_seg[A.f_gi[g * 4 + 3] + i] = A.f_gi[g * 4 + 2];
         } else {
             s_fail = 1;
         }
@@ -2631,10 +2636,9 @@ __global__ void __launch_bounds__(TF_T) k_tfold(int D, int64_t c0, int B, const 
 constexpr int TF3_T = 512, TF3_R = 64;
 
 template <typename T>
-__global__ void __launch_bounds__(TF3_T) k_tfold_a(int D, int64_t c0, const int64_t *__restrict__ ctr,
-                                                   const int32_t *__restrict__ dirty,
-                                                   const int32_t *__restrict__ dirty_off,
+__global__ void __launch_bounds__(TF3_T) k_tfold_a(int D, int64_t c0, int Btot, const int32_t *__restrict__ dirty,
                                                    const int32_t *__restrict__ pend_list,
+                                                   const int32_t *__restrict__ pend_seg,
                                                    const char *const *__restrict__ frow,
                                                    const float *__restrict__ fnorm,
                                                    const int32_t *__restrict__ s_foldpos, double *__restrict__ P,
@@ -2642,25 +2646,19 @@ __global__ void __launch_bounds__(TF3_T) k_tfold_a(int D, int64_t c0, const int6
     pdl_enter();
     __shared__ const T *s_row[TF3_R];
     __shared__ float s_fn[TF3_R];
-    __shared__ int s_start[TF3_R];
-    const int nd = (int)ctr[C_NDIRTY];
+    __shared__ int s_start[TF3_R], s_p[TF3_R], s_seg[TF3_R];
     const int tid = threadIdx.x, x = blockIdx.x, c = blockIdx.y;
-    const int Btot = dirty_off[nd];
     const int cs = c * TF3_R, nr = min(TF3_R, Btot - cs);
     if (nr <= 0) return;
-    if (tid < nr) {
+    if (tid < nr) {  // two rounds of independent loads per row
         const int j = cs + tid;
-        int lo = 0, hi = nd - 1;  // the segment holding row j: last di with dirty_off[di] <= j
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (dirty_off[mid] <= j) lo = mid; else hi = mid - 1;
-        }
-        const int p = pend_list[j];
-        const char *r = frow[c0 + p];
-        s_row[tid] = (const T *)r;
+        const int p = pend_list[j], sg = pend_seg[j];
+        const int sp = tid > 0 ? pend_seg[j - 1] : -1;
+        s_row[tid] = (const T *)frow[c0 + p];
         s_fn[tid] = fnorm[c0 + p];
-        s_start[tid] = (tid == 0 || dirty_off[lo] == j) ? 1 : 0;
-        if (x == 0) cd_rows[j] = p >= s_foldpos[dirty[lo]] ? r : nullptr;
+        s_start[tid] = (tid == 0 || sp != sg) ? 1 : 0;
+        s_p[tid] = p;
+        s_seg[tid] = sg;
     }
     __syncthreads();
     const int col = x * TF3_T + tid;
@@ -2687,18 +2685,22 @@ __global__ void __launch_bounds__(TF3_T) k_tfold_a(int D, int64_t c0, const int6
         }
         P[(int64_t)(cs + ps) * D + col] = acc;
     }
-    if (x == 0 && tid == 0) {  // the pieces' fp32-norm sums
-        double f = 0.0;
-        int ps = 0;
-        for (int r = 0; r < nr; r++) {
-            if (s_start[r] && r > 0) {
-                PF[cs + ps] = f;
-                f = 0.0;
-                ps = r;
+    if (x == 0) {
+        if (tid == 0) {  // the pieces' fp32-norm sums
+            double f = 0.0;
+            int ps = 0;
+            for (int r = 0; r < nr; r++) {
+                if (s_start[r] && r > 0) {
+                    PF[cs + ps] = f;
+                    f = 0.0;
+                    ps = r;
+                }
+                f += (double)s_fn[r];
             }
-            f += (double)s_fn[r];
+            PF[cs + ps] = f;
         }
-        PF[cs + ps] = f;
+        // the lagged chain's rows (nullptr: already folded by the exact path)
+        if (tid < nr) cd_rows[cs + tid] = s_p[tid] >= s_foldpos[dirty[s_seg[tid]]] ? (const char *)s_row[tid] : nullptr;
     }
 }
 
@@ -3262,6 +3264,7 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             A.dirty = s->dirty.p;
             A.dirty_off = s->dirty_off.p;
             A.pend_list = s->pend_list.p;
+            A.pend_seg = s->pend_seg.p;
             A.cluster_of = s->cluster_of.p;
             A.mrank = s->mrank.p;
             A.frank = s->frank.p;
@@ -3289,13 +3292,6 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             // fast path first (the common all-certain batch over the whole
             // grid); k_resolve returns at once when it committed
             static const bool nofast = getenv("FOCUS_B200_NOFAST") && atoi(getenv("FOCUS_B200_NOFAST"));
-            if (!nofast) {
-                const unsigned nch = (unsigned)cdiv(B, RF_T);
-                launch_pdl(k_rfast1, dim3(nch), dim3(RF_T), 0, st, A);
-                FX_LAUNCHED();
-                launch_pdl(k_rfast3, dim3(nch), dim3(RF_T), 0, st, A);
-                FX_LAUNCHED();
-            }
             const PwPlan &P = *s->plan_host;
             size_t smem = resolve_smem(s->B, P);
             auto kern = k_resolve<T>;
@@ -3304,6 +3300,15 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             if (smem > cur) {
                 FX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
                 cur = smem;
+            }
+            // fast path first (the common all-certain batch over the whole
+            // grid); k_resolve returns at once when it committed
+            if (!nofast) {
+                const unsigned nch = (unsigned)cdiv(B, RF_T);
+                launch_pdl(k_rfast1, dim3(nch), dim3(RF_T), 0, st, A);
+                FX_LAUNCHED();
+                launch_pdl(k_rfast3, dim3(nch), dim3(RF_T), 0, st, A);
+                FX_LAUNCHED();
             }
             // its exact path reads the reference's float64 sums: the previous
             // batch's chain must be done (it ran alongside this batch's screen)
@@ -3418,8 +3423,8 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
                            s->tf_bcnt.p, s->cd_nd.p + buf, meta, ldm, coff, crows);
             } else {
                 const unsigned gx3 = (unsigned)cdiv(D, TF3_T);
-                launch_pdl(k_tfold_a<T>, dim3(gx3, (unsigned)cdiv(B, TF3_R)), dim3(TF3_T), 0, st, D, c0, s->ctr.p,
-                           s->dirty.p, s->dirty_off.p, s->pend_list.p, s->frow.p, s->fnorm.p, s->s_foldpos.p,
+                launch_pdl(k_tfold_a<T>, dim3(gx3, (unsigned)cdiv(B, TF3_R)), dim3(TF3_T), 0, st, D, c0, (int)B,
+                           s->dirty.p, s->pend_list.p, s->pend_seg.p, s->frow.p, s->fnorm.p, s->s_foldpos.p,
                            s->tf_P.p, s->tf_PF.p, crows);
                 FX_LAUNCHED();
                 launch_pdl(k_tfold_b, dim3(gx3, (unsigned)std::min<int64_t>(2 * (int64_t)B + 3, std::max<int64_t>(64, 1184 / gx3))), dim3(TF3_T), 0, st, D, s->ctr.p, s->dirty.p,
