@@ -19,6 +19,7 @@ same workload; `--impl reference` times that port as the reference arm.
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import subprocess
@@ -310,6 +311,8 @@ def main():
     ap.add_argument("--no-fc", action="store_true", help="skip the K1b FC head sub-benchmark")
     ap.add_argument("--multi-streams", type=int, default=8, help="concurrent engines for the C4-shape line (<=1: skip)")
     ap.add_argument("--multi-objects", type=int, default=1_000_000, help="objects per engine in the C4-shape line")
+    ap.add_argument("--multi-partitions", type=int, default=4,
+                    help="SM partitions (green contexts) = engines ingesting concurrently in the C4-shape line")
     ap.add_argument("--c3-objects", type=int, default=300_000,
                     help="objects of the C3-shape line (T=5, M=100k: every object seeds; 0 = skip)")
     args = ap.parse_args()
@@ -561,11 +564,21 @@ def main():
                                 seed=1000 + rank * nms + j) for j in range(nms)]
         torch.cuda.synchronize()
 
-        def one(j):
+        # SM partitions (CUDA green contexts, fx_device_set_partitions): worker w
+        # runs engines w, w + P, ... in partition w, so concurrent engines never
+        # share SMs.  Without them, concurrent engines starve each other's
+        # large-shared-memory CTAs (the single-CTA resolve, the TC screen) for
+        # up to seconds at a time.
+        nparts = max(1, min(nms, args.multi_partitions))
+        sms = ctypes.c_int32(0)
+        if nparts > 1:
+            _lib.check(_lib.load().fx_device_set_partitions(local, nparts, ctypes.byref(sms)))
+
+        def one(j, part):
             fx.set_device(local)
             d = datas[j]
             sj = fx.ingest.Stream(W["dim"], 16, W["vocab"], W["k"], W["t"], W["m"], 0.01, _lib.FX_F32, local,
-                                  args.batch)
+                                  args.batch, partition=part)
             sj.set_rank_model(prof, 0)
             sj.ingest_device(nobj, d.oids.data_ptr(), d.fids.data_ptr(), d.sigs.data_ptr(), d.feats.data_ptr(),
                              d.true_class.data_ptr())
@@ -573,23 +586,30 @@ def main():
             del ix, sj
             return rp.objects_seen
 
-        with ThreadPoolExecutor(max_workers=nms) as pool:
-            list(pool.map(one, range(nms)))  # warm-up
+        def worker(w):
+            return sum(one(j, w + 1 if nparts > 1 else 0) for j in range(w, nms, nparts))
+
+        with ThreadPoolExecutor(max_workers=nparts) as pool:
+            list(pool.map(worker, range(nparts)))  # warm-up
             dts = []
             for _ in range(3):  # median of 3 wall-clock runs (host thread scheduling jitter)
                 torch.cuda.synchronize()
                 t0 = time.perf_counter()
-                seen = sum(pool.map(one, range(nms)))
+                seen = sum(pool.map(worker, range(nparts)))
                 torch.cuda.synchronize()
                 dts.append(time.perf_counter() - t0)
             dt = sorted(dts)[1]
+        if nparts > 1:
+            _lib.check(_lib.load().fx_device_set_partitions(local, 0, None))
         if ws > 1:
             tt = torch.tensor([dt], device=dev_red)
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
             dt = float(tt.item())
-        msres = {"streams_per_gpu": nms, "objects_per_stream": nobj, "objects_per_s": seen * ws / dt,
-                 "wall_s": dt, "note": "C4 shape: concurrent engines per GPU (host thread + CUDA stream each), "
-                                       "inputs resident, wall clock (median of 3 runs), max over ranks"}
+        msres = {"streams_per_gpu": nms, "sm_partitions": nparts, "sms_per_partition": int(sms.value) or 148,
+                 "objects_per_stream": nobj, "objects_per_s": seen * ws / dt, "wall_s": dt, "all_runs_s": dts,
+                 "note": "C4 shape: engines per GPU, one host thread per SM partition (CUDA green context) running "
+                         "its engines one after another, inputs resident, wall clock (median of 3 runs), max over "
+                         "ranks"}
         del datas
 
     # C3 shape (BASELINE configs[2]: M = 100 k, T = 5 -- every object seeds,

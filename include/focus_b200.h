@@ -81,7 +81,8 @@ typedef struct {
     int32_t feat_type; /* FX_F32 or FX_F64                              */
     int32_t device;    /* CUDA device ordinal                           */
     int32_t batch;     /* objects per clustering batch, 0 = auto        */
-    int32_t reserved;
+    int32_t partition; /* SM partition (fx_device_set_partitions): p > 0
+                          = partition p-1, 0 = next in round-robin order */
 } fx_stream_config;
 
 /* Device rank model (the synthetic "cheap CNN" top-K, classifiers.py:59-70,
@@ -387,6 +388,14 @@ int fx_rank_positions(int32_t device, int64_t n, const int64_t *oids, const int3
 
 const char *fx_last_error(void);
 int fx_version(void);
+
+/* SM partitions for several engines on one device: engines created after this
+ * call run their streams in SM partition (i mod n_groups) -- CUDA green
+ * contexts of ~SMs/n_groups SMs each -- so concurrent engines cannot starve
+ * each other's CTAs.  n_groups <= 1 turns it off for engines created later.
+ * *out_sms_per_group (may be NULL): SMs per partition.  The reference has no
+ * counterpart (its cross-stream parallelism is process-level). */
+int fx_device_set_partitions(int32_t device, int32_t n_groups, int32_t *out_sms_per_group);
 /* Number of this library's kernels launched so far (process-wide). */
 int64_t fx_kernel_launches(void);
 /* Device time (CUDA events on the stream's CUDA stream) accumulated over all

@@ -31,7 +31,7 @@ class StreamConfig(ctypes.Structure):
     _fields_ = [("dim", ctypes.c_int32), ("sig_dim", ctypes.c_int32), ("vocab", ctypes.c_int32),
                 ("k", ctypes.c_int32), ("t", ctypes.c_double), ("m", ctypes.c_int64),
                 ("pixel_eps", ctypes.c_double), ("feat_type", ctypes.c_int32), ("device", ctypes.c_int32),
-                ("batch", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("batch", ctypes.c_int32), ("partition", ctypes.c_int32)]
 
 
 class RankModelC(ctypes.Structure):
@@ -77,6 +77,7 @@ _SIGS = {
                                                   ctypes.c_int32, ctypes.c_int64, ctypes.c_double, ctypes.c_uint64,
                                                   vp, ctypes.c_int64, vp, vp]),
     "fx_stream_set_feature_noise": (ctypes.c_int, [vp, ctypes.c_double, ctypes.c_uint64, ctypes.c_int32]),
+    "fx_device_set_partitions": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int32, c_i32p]),
     "fx_dup_flags": (ctypes.c_int, [ctypes.c_int32, ctypes.c_int64, ctypes.c_int32, c_i64p, c_f64p, ctypes.c_double,
                                     c_u8p]),
     "fx_stream_dup_flags": (ctypes.c_int, [vp, ctypes.c_int64, c_i64p, c_f64p, c_u8p]),

@@ -148,6 +148,7 @@ void fx_stream::tcollect() {
 }
 
 fx_stream::~fx_stream() {
+    if (counted) live_engines(dev, -1);
     if (st2) cudaStreamSynchronize(st2);  // the lagged chain reads engine buffers
     for (auto &e : ev_tf)
         if (e) cudaEventDestroy(e);
@@ -201,6 +202,106 @@ extern "C" {
 
 const char *fx_last_error(void) { return fx::last_error(); }
 int fx_version(void) { return 1; }
+
+// ---------------------------------------------------------------------------
+// SM partitions (green contexts) for several engines on one device: engine i
+// created after fx_device_set_partitions(dev, n) runs its streams in partition
+// i mod n, so engines cannot starve each other's CTAs.  Driver
+// entry points are resolved at run time (the library does not link libcuda).
+// ---------------------------------------------------------------------------
+namespace {
+struct GreenApi {
+    CUresult (*getDev)(CUdevice *, int) = nullptr;
+    CUresult (*getRes)(CUdevice, CUdevResource *, CUdevResourceType) = nullptr;
+    CUresult (*split)(CUdevResource *, unsigned int *, const CUdevResource *, CUdevResource *, unsigned int,
+                      unsigned int) = nullptr;
+    CUresult (*genDesc)(CUdevResourceDesc *, CUdevResource *, unsigned int) = nullptr;
+    CUresult (*create)(CUgreenCtx *, CUdevResourceDesc, CUdevice, unsigned int) = nullptr;
+    CUresult (*streamCreate)(CUstream *, CUgreenCtx, unsigned int, int) = nullptr;
+    bool ok = false;
+};
+const GreenApi &green_api() {
+    static GreenApi g = [] {
+        GreenApi a;
+        auto get = [](const char *name, void **fn) {
+            cudaDriverEntryPointQueryResult q;
+            return cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) == cudaSuccess &&
+                   q == cudaDriverEntryPointSuccess && *fn;
+        };
+        a.ok = get("cuDeviceGet", (void **)&a.getDev) && get("cuDeviceGetDevResource", (void **)&a.getRes) &&
+               get("cuDevSmResourceSplitByCount", (void **)&a.split) &&
+               get("cuDevResourceGenerateDesc", (void **)&a.genDesc) && get("cuGreenCtxCreate", (void **)&a.create) &&
+               get("cuGreenCtxStreamCreate", (void **)&a.streamCreate);
+        return a;
+    }();
+    return g;
+}
+struct Partitions {
+    std::mutex mu;
+    std::vector<CUgreenCtx> ctx;
+    std::vector<int> sms;
+    int next = 0;
+};
+Partitions g_parts[64];
+}  // namespace
+
+extern "C" int fx_device_set_partitions(int32_t device, int32_t n_groups, int32_t *out_sms_per_group) {
+    FX_GUARD({
+        if (device < 0 || device >= 64 || n_groups < 0 || n_groups > 32) throw Error{FX_E_USAGE, "bad arguments"};
+        Partitions &P = g_parts[device];
+        std::lock_guard<std::mutex> lk(P.mu);
+        P.ctx.clear();  // contexts of earlier partitions stay alive for the engines bound to them
+        P.sms.clear();
+        P.next = 0;
+        if (out_sms_per_group) *out_sms_per_group = 0;
+        if (n_groups <= 1) return FX_OK;
+        const GreenApi &g = green_api();
+        if (!g.ok) throw Error{FX_E_CUDA, "green contexts unavailable in this driver"};
+        set_dev(device);
+        FX_CUDA(cudaFree(nullptr));
+        CUdevice dev;
+        CUdevResource all;
+        if (g.getDev(&dev, device) != CUDA_SUCCESS || g.getRes(dev, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS)
+            throw Error{FX_E_CUDA, "cuDeviceGetDevResource failed"};
+        unsigned per = (all.sm.smCount / (unsigned)n_groups) & ~7u;  // multiples of 8 SMs
+        if (per < 8) throw Error{FX_E_USAGE, "too many partitions for this device"};
+        std::vector<CUdevResource> grp(n_groups);
+        CUdevResource rem;
+        unsigned ng = (unsigned)n_groups;
+        if (g.split(grp.data(), &ng, &all, &rem, 0, per) != CUDA_SUCCESS || ng < (unsigned)n_groups)
+            throw Error{FX_E_CUDA, "cuDevSmResourceSplitByCount failed"};
+        for (unsigned i = 0; i < ng; i++) {
+            CUdevResourceDesc d;
+            CUgreenCtx c;
+            if (g.genDesc(&d, &grp[i], 1) != CUDA_SUCCESS || g.create(&c, d, dev, CU_GREEN_CTX_DEFAULT_STREAM) != CUDA_SUCCESS)
+                throw Error{FX_E_CUDA, "cuGreenCtxCreate failed"};
+            P.ctx.push_back(c);
+            P.sms.push_back((int)grp[i].sm.smCount);
+        }
+        if (out_sms_per_group) *out_sms_per_group = P.sms.empty() ? 0 : P.sms[0];
+    })
+}
+
+namespace fx {
+// the partition a new engine's streams belong to (nullptr: the whole device)
+static CUgreenCtx next_partition(int dev, int want) {
+    Partitions &P = g_parts[dev & 63];
+    std::lock_guard<std::mutex> lk(P.mu);
+    if (P.ctx.empty()) return nullptr;
+    if (want > 0) return P.ctx[(size_t)(want - 1) % P.ctx.size()];
+    return P.ctx[(size_t)(P.next++) % P.ctx.size()];
+}
+static void make_stream(cudaStream_t *st, CUgreenCtx gc, int prio) {
+    if (!gc) {
+        FX_CUDA(cudaStreamCreateWithPriority(st, cudaStreamNonBlocking, prio));
+        return;
+    }
+    CUstream cs;
+    if (green_api().streamCreate(&cs, gc, CU_STREAM_NON_BLOCKING, prio) != CUDA_SUCCESS)
+        throw Error{FX_E_CUDA, "cuGreenCtxStreamCreate failed"};
+    *st = (cudaStream_t)cs;
+}
+}  // namespace fx
 int64_t fx_kernel_launches(void) { return fx::launches(); }
 
 int fx_stream_create(const fx_stream_config *cfg, fx_stream **out) {
@@ -218,6 +319,8 @@ int fx_stream_create(const fx_stream_config *cfg, fx_stream **out) {
         try {
             s->cfg = *cfg;
             s->dev = cfg->device;
+            live_engines(s->dev, +1);
+            s->counted = true;
             s->esize = cfg->feat_type == FX_F64 ? 8 : 4;
             {
                 const char *env = getenv("FOCUS_B200_SCREEN");
@@ -235,7 +338,9 @@ int fx_stream_create(const fx_stream_config *cfg, fx_stream **out) {
             FX_CUDA(cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi));
             static const bool noprio = getenv("FOCUS_B200_NOPRIO") && atoi(getenv("FOCUS_B200_NOPRIO"));
             if (noprio) prio_lo = prio_hi = 0;
-            FX_CUDA(cudaStreamCreateWithPriority(&s->st, cudaStreamNonBlocking, prio_hi));
+            CUgreenCtx gctx = next_partition(s->dev, cfg->partition);
+            s->partitioned = gctx != nullptr;
+            make_stream(&s->st, gctx, prio_hi);
             cur_stream() = s->st;
             const int D = cfg->dim;
             int B = cfg->batch;
@@ -263,7 +368,7 @@ int fx_stream_create(const fx_stream_config *cfg, fx_stream **out) {
             s->s_drift.reserve(ns);
             s->s_cn2.reserve(ns);
             {  // snapshot tree fold + lagged exact chain (k_tfold / k_fold on st2)
-                FX_CUDA(cudaStreamCreateWithPriority(&s->st2, cudaStreamNonBlocking, prio_lo));
+                make_stream(&s->st2, gctx, prio_lo);
                 for (int i = 0; i < 2; i++) {
                     FX_CUDA(cudaEventCreateWithFlags(&s->ev_tf[i], cudaEventDisableTiming));
                     FX_CUDA(cudaEventCreateWithFlags(&s->ev_ch[i], cudaEventDisableTiming));

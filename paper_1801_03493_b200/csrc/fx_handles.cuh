@@ -46,6 +46,8 @@ struct fx_stream {
     bool tc_screen = false;    // tcgen05 TF32 screen (f32 features, D % 4 == 0)
     bool finalized = false;
     bool debug_check = false;
+    bool counted = false;      // included in live_engines(dev)
+    bool partitioned = false;  // streams in an SM partition (green context, fx_device_set_partitions)
     bool timing = false;  // per-phase CUDA-event timers (fx_stream_set_timing / FOCUS_B200_TIMERS=1)
     bool rows_aligned16 = true;  // every feature row pointer so far is 16-byte aligned  // FOCUS_B200_CHECK=1: per-batch host-side invariant checks (slow)
 

@@ -68,6 +68,8 @@ __device__ __forceinline__ void pdl_enter() {
 }
 
 bool pdl_enabled();  // FOCUS_B200_NOPDL=1 turns programmatic dependent launch off (diagnostics)
+void pdl_suppress(bool s);  // this host thread launches without PDL while set
+int live_engines(int dev, int delta);  // engines alive on a device (after adding delta)
 
 template <typename... KArgs, typename... Args>
 void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args &&...args) {

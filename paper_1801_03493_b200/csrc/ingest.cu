@@ -645,8 +645,8 @@ __global__ void k_row_summary(int nA, const int64_t *__restrict__ ctr, const flo
 //     (<= RC_MAX residuals; more go to the tiled SIMT kernel), as k_res_cols.
 // Each lane sums at most 4 NV <= 64 squared differences sequentially, then a
 // 5-level warp tree: within the SIMT screen model screen_rel(D).
-template <int NV>
-__global__ void __launch_bounds__(256) k_rowpass(int nA, int64_t a0, const char *const *__restrict__ frow, int D,
+template <int NV, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_rowpass(int nA, int64_t a0, const char *const *__restrict__ frow, int D,
                                                 const int64_t *__restrict__ ctr, const float *__restrict__ dist,
                                                 int64_t ld, const float *__restrict__ cn2, const int32_t *__restrict__ snap,
                                                 const float *__restrict__ fnorm, ScreenModel sm, float rel, float absc,
@@ -3062,6 +3062,17 @@ __global__ void k_batch_rows(int nb, const int64_t *__restrict__ cfirst, const i
 template <typename T>
 void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
     cudaStream_t st = s->st;
+    // Several engines ingesting on one device: programmatic dependent launch
+    // parks each dependent grid's CTAs on SMs before its primary finishes, and
+    // with many engines those parked CTAs starve other engines' large-shared-
+    // memory CTAs (the TC screen, the resolve) for up to seconds (CUPTI traces,
+    // DESIGN.md §6).  So with more than one live engine: no PDL, and the
+    // exact chain on the main stream.
+    const bool multi_inline = live_engines(s->dev, 0) > 1 && !s->partitioned;
+    struct PdlScope {
+        explicit PdlScope(bool on) { pdl_suppress(on); }
+        ~PdlScope() { pdl_suppress(false); }
+    } pdl_scope_(multi_inline);
     const int D = s->cfg.dim;
     const float rel = (float)screen_rel(D);
     const float absc = (float)(2.0 * 2.384185791015625e-07);  // 2^-22 * 2
@@ -3190,13 +3201,14 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
         const float *snorm = s->tc_screen ? s->snorm.p : nullptr;
         if (rowpass) {
             const unsigned grid = (unsigned)std::min<int64_t>(cdiv((int64_t)B * 32, 256), 148 * 8);
+            static const int rp_minb = getenv("FOCUS_B200_RP_MINB") ? atoi(getenv("FOCUS_B200_RP_MINB")) : 1;
             if (D <= 1024)
-                launch_pdl(k_rowpass<8>, dim3(grid), dim3(256), 0, st, B, c0, s->frow.p, D, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p,
+                launch_pdl(k_rowpass<8, 1>, dim3(grid), dim3(256), 0, st, B, c0, s->frow.p, D, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p,
                                                    s->snap_slot.p, s->fnorm.p, sm, rel, absc, s->C32.p, s->cfg.t,
                                                    s->res_pos.p, s->dres.p, B, s->sum_slot.p, s->sum_q.p, s->sum_d1.p,
                                                    s->sum_e1.p, s->sum_lbr.p, snorm);
             else
-                launch_pdl(k_rowpass<16>, dim3(grid), dim3(256), 0, st, B, c0, s->frow.p, D, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p,
+                launch_pdl(rp_minb >= 3 ? k_rowpass<16, 3> : k_rowpass<16, 1>, dim3(grid), dim3(256), 0, st, B, c0, s->frow.p, D, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p,
                                                     s->snap_slot.p, s->fnorm.p, sm, rel, absc, s->C32.p, s->cfg.t,
                                                     s->res_pos.p, s->dres.p, B, s->sum_slot.p, s->sum_q.p, s->sum_d1.p,
                                                    s->sum_e1.p, s->sum_lbr.p, snorm);
@@ -3434,8 +3446,15 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             }
             FX_LAUNCHED();
             s->tstop();
-            FX_CUDA(cudaEventRecord(s->ev_tf[buf], st));
-            FX_CUDA(cudaStreamWaitEvent(s->st2, s->ev_tf[buf], 0));
+            // several engines on the device (multi_inline): the chain runs on the
+            // main stream -- no cross-stream events; FOCUS_B200_FOLD_INLINE=1 forces it
+            static const bool fold_inline_env = getenv("FOCUS_B200_FOLD_INLINE") && atoi(getenv("FOCUS_B200_FOLD_INLINE"));
+            const bool fold_inline = fold_inline_env || multi_inline;
+            cudaStream_t fst = fold_inline ? st : s->st2;
+            if (!fold_inline) {
+                FX_CUDA(cudaEventRecord(s->ev_tf[buf], st));
+                FX_CUDA(cudaStreamWaitEvent(s->st2, s->ev_tf[buf], 0));
+            }
             const int64_t gx = cdiv(D, FD);
             static const int fold_gy = getenv("FOCUS_B200_FOLD_GY") ? atoi(getenv("FOCUS_B200_FOLD_GY")) : 0;
             const int64_t gy = fold_gy > 0 ? std::min<int64_t>(fold_gy, 2 * (int64_t)B + 1)
@@ -3446,11 +3465,13 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
                 fold_attr[dev_slot()] = true;
             }
             ChainDesc cd{s->cd_nd.p + buf, meta, ldm, coff, crows};
-            k_fold<T><<<dim3((unsigned)gx, (unsigned)gy), FOLD_THREADS, fold_smem<T>(), s->st2>>>(
+            k_fold<T><<<dim3((unsigned)gx, (unsigned)gy), FOLD_THREADS, fold_smem<T>(), fst>>>(
                 D, cd, s->S.p, s->fcent.p, s->cl_nfeat.p, s->cl_size.p, (long long *)(s->prof.p + 16));
             FX_LAUNCHED();
-            FX_CUDA(cudaEventRecord(s->ev_ch[buf], s->st2));
-            s->chain_pending[buf] = true;
+            if (!fold_inline) {
+                FX_CUDA(cudaEventRecord(s->ev_ch[buf], s->st2));
+                s->chain_pending[buf] = true;
+            }
         }
         if (s->debug_check) {
             FX_CUDA(cudaStreamSynchronize(st));

@@ -242,8 +242,15 @@ void scan_u8_to_i64(const uint8_t *in, int64_t n, int invert, int64_t *out_excl,
 }  // namespace fx
 
 namespace fx {
+static thread_local bool t_pdl_suppressed = false;
 bool pdl_enabled() {
     static const bool on = !(getenv("FOCUS_B200_NOPDL") && atoi(getenv("FOCUS_B200_NOPDL")));
-    return on;
+    return on && !t_pdl_suppressed;
 }
+void pdl_suppress(bool s) { t_pdl_suppressed = s; }
+
+// engines alive per device: several concurrent engines run without PDL and
+// with the exact chain on their main stream (run_batches)
+static std::atomic<int> g_live_engines[64];
+int live_engines(int dev, int delta) { return g_live_engines[dev & 63].fetch_add(delta) + delta; }
 }  // namespace fx

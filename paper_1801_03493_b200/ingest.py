@@ -59,11 +59,12 @@ class Stream:
 
     def __init__(self, dim: int, sig_dim: int, vocab: int, k: int, t: float, m: int,
                  pixel_eps: float = DEFAULT_PIXEL_EPS, feat_type: int = _lib.FX_F32,
-                 device: int | None = None, batch: int = 0):
+                 device: int | None = None, batch: int = 0, partition: int = 0):
         self.L = _lib.load()
         cfg = _lib.StreamConfig(dim=dim, sig_dim=sig_dim, vocab=vocab, k=k, t=float(t), m=int(m),
                                 pixel_eps=float(pixel_eps), feat_type=feat_type,
-                                device=_lib.device() if device is None else device, batch=batch)
+                                device=_lib.device() if device is None else device, batch=batch,
+                                partition=partition)
         self.cfg = cfg
         h = _lib.vp()
         _lib.check(self.L.fx_stream_create(ctypes.byref(cfg), ctypes.byref(h)))

@@ -67,9 +67,12 @@ class QuerySession:
         self.L = _lib.load()
         dev = idx.ensure_device()  # e.g. index.load(): posted on the device once
         C = int(dev.sizes.n_clusters)
-        reps = np.empty(C, np.int64)
-        if C:
-            _lib.check(self.L.fx_index_reps(dev.handle, _lib.p64(reps)))
+        reps = getattr(dev, "_reps_cache", None)  # built indexes are immutable: read once
+        if reps is None:
+            reps = np.empty(C, np.int64)
+            if C:
+                _lib.check(self.L.fx_index_reps(dev.handle, _lib.p64(reps)))
+            dev._reps_cache = reps
         self._reps = reps
         # memo key = representative object id (query.py:53-60); representatives
         # of distinct clusters are distinct objects unless the index was built
@@ -89,9 +92,15 @@ class QuerySession:
         _lib.check(self.L.fx_session_create(dev.handle, None, None if key is None else _lib.p32(key), n_keys,
                                             _lib.pu8(other) if other is not None else None, ctypes.byref(h)))
         self.handle = h
-        if isinstance(labels, np.ndarray):
-            lab = np.ascontiguousarray(labels, np.int32)
-            _lib.check(self.L.fx_session_gather_labels(h, _lib.p32(lab), 0, lab.size))
+        if isinstance(labels, np.ndarray) and C:
+            # the representatives' labels only (C values, not the whole array)
+            lab = np.asarray(labels)
+            ok = (reps >= 0) & (reps < lab.size)
+            rl = np.full(C, _NO_OBJECT, np.int32)
+            rl[ok] = lab[reps[ok]]
+            rl[reps < 0] = _NO_REP
+            cidx = np.arange(C, dtype=np.int32)
+            _lib.check(self.L.fx_session_set_labels(h, C, _lib.p32(cidx), _lib.p32(rl)))
 
     def __del__(self):
         h, self.handle = getattr(self, "handle", None), None

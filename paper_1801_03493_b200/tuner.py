@@ -34,7 +34,7 @@ import numpy as np
 
 from . import _lib, classifiers
 from ._reftypes import shared
-from .classifiers import GENERIC_CHEAP, GROUND_TRUTH, ClassifierProfile, RankModel, extract_feature, ground_truth_label
+from .classifiers import GENERIC_CHEAP, GROUND_TRUTH, ClassifierProfile, RankModel, ground_truth_label
 from .core import OTHER_CLASS, AccuracyTarget, Config, encode_class
 from .errors import EmptySample, UsageError
 from .ingest import DEFAULT_PIXEL_EPS, dup_flags, ingest_arrays
@@ -188,8 +188,14 @@ class GridEvaluator:
         if sigma not in self._features:
             stub = ClassifierProfile("_noise", GENERIC_CHEAP, self.header.vocab, RankModel(0.5, 0.5), 1.0,
                                      feature_noise_sigma=sigma)
-            F = np.array([extract_feature(stub, o, self.seed) for o in self.classified], np.float64)
-            self._features[sigma] = F.reshape(self.n_classified, self.header.dim)
+            # extract_feature (classifiers.py:152-158) for the whole sample on the device
+            D = self.header.dim
+            raw = [np.asarray(o.feature) for o in self.classified]
+            dt = np.float32 if raw and all(r.dtype == np.float32 for r in raw) else np.float64
+            R = np.array(raw, dtype=dt).reshape(self.n_classified, D) if raw else np.zeros((0, D), dt)
+            oids = np.array([o.object_id for o in self.classified], np.int64)
+            F = classifiers.extract_features(stub, oids, R, self.seed) if raw else np.zeros((0, D))
+            self._features[sigma] = F.reshape(self.n_classified, D)
         return self._features[sigma]
 
     def _skeleton_for(self, sigma: float, t: float) -> _Skeleton:

@@ -29,12 +29,18 @@ def main():
     ap.add_argument("--trace-stall", type=int, default=0,
                     help="trace up to this many runs at the largest N; report the longest device activities of a "
                          "run slower than 1 s")
+    ap.add_argument("--partitions", type=int, default=0, help="SM partitions (green contexts) for the engines")
     a = ap.parse_args()
     ns = [int(x) for x in a.streams.split(",")]
     nmax = max(ns)
     datas = [synth.generate(a.objects, seed=1000 + j) for j in range(nmax)]
     torch.cuda.synchronize()
     prof = fx.make_default_profiles(1000)["cheap"]
+    if a.partitions > 1:
+        import ctypes
+        sms = ctypes.c_int32(0)
+        _lib.check(_lib.load().fx_device_set_partitions(0, a.partitions, ctypes.byref(sms)))
+        print(f"{a.partitions} SM partitions of {sms.value} SMs", flush=True)
 
     solo = {}
 
@@ -63,8 +69,12 @@ def main():
             print(f"  engine {j}: " + " ".join(f"{k}={c[k]}" for k in (
                 "windows", "seq_steps", "exact", "fast", "cyc_passA", "cyc_passB", "cyc_passCD", "cyc_passE",
                 "cyc_seq", "fold_wait_cyc", "fold_chain_cyc", "fold_slot_cyc", "fold_rows")), flush=True)
+        tm = s.timings()
         del ix, s
         t4 = time.perf_counter()
+        if t2 - t1 > 1.0:  # a stalled ingest: where did the host wait?
+            print(f"  SLOW engine {j}: ingest {(t2 - t1)*1e3:.0f} ms; host phases (ms): " +
+                  " ".join(f"{k}={v:.1f}" for k, v in tm.items() if k.startswith("host") and v > 1.0), flush=True)
         return (t1 - t0, t2 - t1, t3 - t2, t4 - t3)
 
     with ThreadPoolExecutor(max_workers=nmax) as pool:
