@@ -687,6 +687,45 @@ def main():
                  "frac": tf / tf32_peak, "peak_kind": pk, "flagged": int(fl.sum().item()),
                  "bound": "tensor", "note": "TF32 tcgen05 logits + float64 re-score of the candidates"}
 
+    # feature noise (extract_feature, classifiers.py:152-158) on the device:
+    # 65 k objects x D normals, float32 features in, float64 out; one numpy
+    # object timed beside it (the reference's per-object call)
+    noiseres = None
+    if not args.no_fc:
+        nn_ = min(1 << 16, W["n"])
+        Fn = data.feats[:nn_]
+        On = data.oids[:nn_]
+        outn = torch.empty(nn_, W["dim"], dtype=torch.float64, device="cuda")
+        flg = torch.zeros(1, dtype=torch.int64, device="cuda")
+        csn = torch.cuda.current_stream()
+
+        def noise_call():
+            _lib.check(L.fx_extract_features_device(local, nn_, W["dim"], _lib.vp(On.data_ptr()), _lib.vp(Fn.data_ptr()),
+                                                    _lib.FX_F32, W["dim"], 0.05, 0, _lib.vp(outn.data_ptr()),
+                                                    W["dim"], _lib.vp(flg.data_ptr()), _lib.vp(csn.cuda_stream)))
+        noise_call()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(csn)
+        for _ in range(3):
+            noise_call()
+        e1.record(csn)
+        torch.cuda.synchronize()
+        msn = e0.elapsed_time(e1) / 3
+        fh = Fn[:200].cpu().numpy()
+        oh = On[:200].cpu().numpy()
+        q0 = time.perf_counter()
+        for i in range(200):
+            fh[i].astype(np.float64) + 0.05 * np.random.default_rng([0, int(oh[i]), 1]).standard_normal(W["dim"])
+        cpu_s = (time.perf_counter() - q0) / 200
+        noiseres = {"objects": nn_, "dim": W["dim"], "ms": msn, "objects_per_s": nn_ / (msn / 1e3),
+                    "normals_per_s": nn_ * W["dim"] / (msn / 1e3),
+                    "hbm_gbs": nn_ * W["dim"] * (4 + 8) / (msn / 1e3) / 1e9, "flagged": int(flg.item()),
+                    "cpu_numpy_objects_per_s": 1.0 / cpu_s,
+                    "note": "fx_extract_features_device: SeedSequence + PCG64 + ziggurat (bit-exact numpy), "
+                            "f32 features in, f64 out; cpu = numpy default_rng(...).standard_normal per object, 1 core"}
+        del outn
+
     parity = c5 = h = None
     if rank == 0 and not args.no_check:
         parity, c5, h = parity_and_c5(data, W, local, args)
@@ -716,7 +755,7 @@ def main():
                        "streams_per_gpu": 1, "parallelism": f"stream-sharded x{ws}",
                        "l2": "inputs (8 GB features/stream) exceed L2; no flush", **W},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
-            "query": qres, "c5_query_sweep": c5, "parity": parity, "k1b_fc_head": fcres, "multi_stream": msres,
+            "query": qres, "c5_query_sweep": c5, "parity": parity, "k1b_fc_head": fcres, "feature_noise": noiseres, "multi_stream": msres,
             "c3_shape": c3res,
             "gpu_launches": int(launches),
             "ingest": {"clusters": rep.clusters_emitted, "classified": rep.objects_classified,
