@@ -3201,14 +3201,14 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
         const float *snorm = s->tc_screen ? s->snorm.p : nullptr;
         if (rowpass) {
             const unsigned grid = (unsigned)std::min<int64_t>(cdiv((int64_t)B * 32, 256), 148 * 8);
-            static const int rp_minb = getenv("FOCUS_B200_RP_MINB") ? atoi(getenv("FOCUS_B200_RP_MINB")) : 1;
+            static const int rp_minb = getenv("FOCUS_B200_RP_MINB") ? atoi(getenv("FOCUS_B200_RP_MINB")) : 2;
             if (D <= 1024)
-                launch_pdl(k_rowpass<8, 1>, dim3(grid), dim3(256), 0, st, B, c0, s->frow.p, D, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p,
+                launch_pdl(k_rowpass<8, 2>, dim3(grid), dim3(256), 0, st, B, c0, s->frow.p, D, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p,
                                                    s->snap_slot.p, s->fnorm.p, sm, rel, absc, s->C32.p, s->cfg.t,
                                                    s->res_pos.p, s->dres.p, B, s->sum_slot.p, s->sum_q.p, s->sum_d1.p,
                                                    s->sum_e1.p, s->sum_lbr.p, snorm);
             else
-                launch_pdl(rp_minb >= 3 ? k_rowpass<16, 3> : k_rowpass<16, 1>, dim3(grid), dim3(256), 0, st, B, c0, s->frow.p, D, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p,
+                launch_pdl(rp_minb >= 3 ? k_rowpass<16, 3> : k_rowpass<16, 2>, dim3(grid), dim3(256), 0, st, B, c0, s->frow.p, D, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p,
                                                     s->snap_slot.p, s->fnorm.p, sm, rel, absc, s->C32.p, s->cfg.t,
                                                     s->res_pos.p, s->dres.p, B, s->sum_slot.p, s->sum_q.p, s->sum_d1.p,
                                                    s->sum_e1.p, s->sum_lbr.p, snorm);

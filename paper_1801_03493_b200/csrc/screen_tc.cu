@@ -314,7 +314,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
     cg::cluster_group cluster = cg::this_cluster();
     cluster.sync();
     const int rank = (int)cluster.block_rank();
-    const int rows_per = TC_M / split;
+    const int rows_per = (TC_M + split - 1) / split;
+    const int r_lo = rank * rows_per, r_hi = min(TC_M, r_lo + rows_per);
     const int ncol = min(TC_N, nB - tb);
     const int nc4 = (ncol + 3) >> 2;
     const float *part[8];
@@ -323,8 +324,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
     __shared__ int rowmin[TC_M];  // min screen lower bound per row (non-negative float bits)
     for (int i = tid; i < TC_M; i += TC_THREADS) rowmin[i] = 0x7f800000;  // +inf
     __syncthreads();
-    for (int e = tid; e < rows_per * nc4; e += TC_THREADS) {
-        const int rr = rank * rows_per + e / nc4, c = (e % nc4) * 4;
+    for (int e = tid; e < (r_hi - r_lo) * nc4; e += TC_THREADS) {
+        const int rr = r_lo + e / nc4, c = (e % nc4) * 4;
         const int a = rcls[rr];
         if (a < 0) continue;
         float4 dot = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -364,13 +365,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
     if (rowmin_g) {
         // several column tiles: per-row minimum across CTAs (k_res_from_min flags the residuals)
         __syncthreads();
-        for (int rr = rank * rows_per + tid; rr < (rank + 1) * rows_per; rr += TC_THREADS)
+        for (int rr = r_lo + tid; rr < r_hi; rr += TC_THREADS)
             if (rcls[rr] >= 0) atomicMin(&rowmin_g[rcls[rr]], rowmin[rr]);
     } else if (res_col) {
         // fused residual detection (one column tile = the whole snapshot):
         // objects with no snapshot centroid whose lower bound is <= T
         __syncthreads();
-        for (int rr = rank * rows_per + tid; rr < (rank + 1) * rows_per; rr += TC_THREADS) {
+        for (int rr = r_lo + tid; rr < r_hi; rr += TC_THREADS) {
             const int a = rcls[rr];
             if (a < 0) continue;
             if ((double)__int_as_float(rowmin[rr]) > T) {
@@ -439,12 +440,14 @@ void launch_screen_tc(int nA, int64_t a0, const char *const *frow, const float *
         rmap = nullptr;
     }
     const int64_t tiles = cdiv(nB_max, TC_N) * cdiv(nR, TC_M);
+    // split-K: the largest factor that keeps the grid in one wave (one CTA
+    // per SM) with >= 4 pipeline stages per CTA
     int split = 1;
-    while (tiles * split * 2 <= 148 && D / (split * 2) >= 4 * TC_KT) split *= 2;
+    while (split < 8 && tiles * (split + 1) <= 148 && D / (split + 1) >= 4 * TC_KT) split++;
     if (split_env > 0) split = split_env;
     split = std::min(split, 8);  // split-K CTAs of a tile form one (portable-size) cluster
-    while (TC_M % split) split--;
     const int kchunk = (int)(cdiv(cdiv(D, split), TC_KT) * TC_KT);
+    split = (int)cdiv(D, kchunk);  // no empty K range
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3((unsigned)(cdiv(nB_max, TC_N) * cdiv(nR, TC_M)), 1, (unsigned)split);
     lc.blockDim = dim3(TC_THREADS);
