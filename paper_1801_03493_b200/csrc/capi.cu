@@ -24,6 +24,8 @@ template <typename T>
 void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end);
 void launch_final_live(fx_stream *s);
 size_t resolve_smem(int Bc, const PwPlan &P);
+size_t resolve_obj_bytes(int Bc, const PwPlan &P);
+constexpr int FX_BMAX_DEFAULT = 8192;  // C2: 8192 is +7 %, 16384 -12 % (r02ai)
 void launch_extract(int dev, int64_t n, int D, const int64_t *d_oid, const void *d_in, int in_type, int64_t ld_in,
                     double sigma, uint64_t seed, double *d_out, int64_t ld_out, unsigned long long *d_flag,
                     cudaStream_t st);
@@ -343,16 +345,24 @@ int fx_stream_create(const fx_stream_config *cfg, fx_stream **out) {
             make_stream(&s->st, gctx, prio_hi);
             cur_stream() = s->st;
             const int D = cfg->dim;
+            // batch capacity: up to FX_BMAX classified objects (k_resolve keeps
+            // its per-object state in shared memory up to 4096, in global
+            // memory above that; its windows never exceed 4096 objects)
+            static const int bmax = getenv("FOCUS_B200_BMAX") ? atoi(getenv("FOCUS_B200_BMAX")) : FX_BMAX_DEFAULT;
+            const int bcap = std::max(64, std::min(bmax, 16384));
             int B = cfg->batch;
             if (B <= 0) {
                 int64_t b = ((int64_t)1 << 26) / std::max<int64_t>(cfg->m, 1);
-                B = (int)std::min<int64_t>(4096, std::max<int64_t>(256, b));
+                B = (int)std::min<int64_t>(bcap, std::max<int64_t>(256, b));
             }
-            B = std::max(64, (std::min(B, 4096) / 64) * 64);  // k_resolve windows are <= 4096 objects
+            B = std::max(64, (std::min(B, bcap) / 64) * 64);
             s->plan_host = new PwPlan();
             build_pw_plan(D, s->plan_host);
-            // k_resolve keeps per-object state of the whole batch in shared memory
-            while (B > 64 && resolve_smem(B, *s->plan_host) + 48 * 1024 > 227 * 1024) B -= 64;
+            if (B <= 4096) {  // k_resolve keeps per-object state of the whole batch in shared memory
+                while (B > 64 && resolve_smem(B, *s->plan_host) + 48 * 1024 > 227 * 1024) B -= 64;
+            } else {
+                s->rs_gobj.reserve(resolve_obj_bytes(B, *s->plan_host));
+            }
             s->B = B;
             const int64_t max_slots_mem = (int64_t)(48e9 / (20.0 * D));  // S + S_tree + C32
             int64_t live_cap = std::min<int64_t>(cfg->m, max_slots_mem);

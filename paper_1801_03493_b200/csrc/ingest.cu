@@ -355,6 +355,7 @@ struct ResolveArgs {
     int32_t *f_rank, *f_dup, *f_ccnt, *f_cdup, *f_gi;
     float *f_P, *f_csum, *f_cmax, *f_gf;
     double *f_gd;
+    unsigned char *rs_gobj;  // per-object state in global memory (B > 4096), else nullptr
 };
 
 constexpr int RS_THREADS = 512;
@@ -886,7 +887,9 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
     const int B = A.B;
     const int BC = A.Bcap;  // layout by capacity (multiple of 64): every array stays aligned
     unsigned short *wcnt = (unsigned short *)smem_raw;    // [RS_RANKW][RS_MAXGRP] per-warp group counts
-    int32_t *sh_slot_of = (int32_t *)(smem_raw + RS_WCNT_BYTES);  // [B]
+    // per-object state: shared memory up to 4096 objects, else global (A.rs_gobj)
+    unsigned char *obj_base = A.rs_gobj ? A.rs_gobj : smem_raw + RS_WCNT_BYTES;
+    int32_t *sh_slot_of = (int32_t *)obj_base;             // [B]
     int *mlist = (int *)(sh_slot_of + BC);                 // [B]
     int32_t *seg_key = (int32_t *)(mlist + BC);            // [B] hypothesis slot
     float *seg_ub0 = (float *)(seg_key + BC);              // [B] d1 + e1
@@ -954,7 +957,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
     for (int b = tid; b < B; b += blockDim.x) sh_slot_of[b] = -1;
     __syncthreads();
 
-    int b = 0, win = B;  // first window: the whole batch (failures shrink it)
+    int b = 0, win = min(B, 4096);  // first window: the whole batch up to 4096 (failures shrink it)
     while (b < B) {
         // =================== parallel segment: speculate every object in
         // [b, e_end) joins its nearest candidate, verify with bounds, commit
@@ -1667,7 +1670,7 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
         if (tid == 0) A.prof[4] += clock64() - t4;
         if (f >= e_end) {
             b = e_end;
-            win = min(win * 2, B);
+            win = min(win * 2, min(B, 4096));
             continue;
         }
         long long t5 = clock64();
@@ -3031,8 +3034,11 @@ static double screen_rel(int D) {
 }
 
 // dynamic shared memory of k_resolve for batch capacity Bc (static smem ~39 KB on top)
+size_t resolve_obj_bytes(int Bc, const PwPlan &P) {
+    return (size_t)Bc * (9 * 4 + 2 + 1) + 16 + sizeof(double) * (P.n_chains + P.n_leaves + P.n_ops + 8);
+}
 size_t resolve_smem(int Bc, const PwPlan &P) {
-    return (size_t)RS_WCNT_BYTES + (size_t)Bc * (9 * 4 + 2 + 1) + 16 + sizeof(double) * (P.n_chains + P.n_leaves + P.n_ops + 8);
+    return (size_t)RS_WCNT_BYTES + (Bc > 4096 ? 16 : resolve_obj_bytes(Bc, P));
 }
 
 // FP32 snapshot packed in snapshot order (TMA boxes of the TC screen need
@@ -3301,6 +3307,7 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             A.f_gf = s->f_gf.p;
             A.f_gd = s->f_gd.p;
             A.s_sdev = s->s_sdev.p;
+            A.rs_gobj = s->B > 4096 ? s->rs_gobj.p : nullptr;
             // fast path first (the common all-certain batch over the whole
             // grid); k_resolve returns at once when it committed
             static const bool nofast = getenv("FOCUS_B200_NOFAST") && atoi(getenv("FOCUS_B200_NOFAST"));
