@@ -3004,6 +3004,130 @@ __global__ void __launch_bounds__(256) k_seal_dist(int64_t nfeat_total, int D, c
     if ((threadIdx.x & 31) == 0 && cur >= 0) atomicMin(&best_bits[cur], best);
 }
 
+// Screened seal.  k_seal_c32 rounds the final centroids to fp32 (and their
+// norms); k_seal_screen measures every featured member against its fp32
+// centroid in fp32 (float4 loads, the centroid row L1-resident for a warp's
+// run of members), d32, with |d_exact - d32| <= eps1 d32 + eps2:
+//   eps1 covers the fp32 terms and sum ((D + 3) 2^-24 relative on the squared
+//   sum), eps2 = 2^-24 ||c|| the rounding of the centroid (triangle
+//   inequality).  Per cluster U = min (d32 (1 + eps1) + eps2); k_seal_exact
+// computes the float64 distance in numpy's pairwise order (the reference's
+// np.linalg.norm, clustering.py:77) only for members with
+// d32 (1 - eps1) - eps2 <= U -- the minimum and its near-ties -- and leaves
+// +inf for the rest, so the pick (first minimum) is unchanged.
+__global__ void k_seal_c32(int64_t C, int D, const double *__restrict__ fcent, float *__restrict__ c32,
+                           float *__restrict__ cnorm) {
+    __shared__ double red[32];
+    for (int64_t c = blockIdx.x; c < C; c += gridDim.x) {
+        double acc = 0.0;
+        for (int k = threadIdx.x; k < D; k += blockDim.x) {
+            const double v = fcent[c * D + k];
+            c32[c * D + k] = (float)v;
+            acc += v * v;
+        }
+        acc = warp_sum(acc);
+        if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t = 0.0;
+            for (int w = 0; w < (int)(blockDim.x >> 5); w++) t += red[w];
+            cnorm[c] = (float)(sqrt(t) * (1.0 + 1e-6));
+        }
+        __syncthreads();
+    }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_seal_screen(int64_t nfeat_total, int D, const int32_t *__restrict__ fmem_cls,
+                                                     const int32_t *__restrict__ fmem_cid,
+                                                     const char *const *__restrict__ frow,
+                                                     const float *__restrict__ c32, const float *__restrict__ cnorm,
+                                                     float eps1, float *__restrict__ dlo,
+                                                     unsigned int *__restrict__ ubits) {
+    const int wpb = blockDim.x >> 5, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t nw = (int64_t)gridDim.x * wpb, gw = (int64_t)blockIdx.x * wpb + w;
+    const int64_t chunk = (nfeat_total + nw - 1) / nw;
+    const int64_t m0 = gw * chunk, m1 = min(nfeat_total, m0 + chunk);
+    int cur = -1;
+    unsigned int best = ~0u;
+    for (int64_t m = m0; m < m1; m++) {
+        const int cid = fmem_cid[m];
+        const T *f = (const T *)frow[fmem_cls[m]];
+        const float *c = c32 + (int64_t)cid * D;
+        float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        int k = lane;
+#pragma unroll 2
+        for (; k + 224 < D; k += 256) {
+#pragma unroll
+            for (int u = 0; u < 8; u++) {
+                const float x = __ldg(c + k + 32 * u) - (float)f[k + 32 * u];
+                acc[u] = fmaf(x, x, acc[u]);
+            }
+        }
+        for (; k < D; k += 32) {
+            const float x = __ldg(c + k) - (float)f[k];
+            acc[0] = fmaf(x, x, acc[0]);
+        }
+        float t = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+#pragma unroll
+        for (int o = 16; o; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (lane == 0) {
+            const float d = sqrtf(t);
+            const float e2 = cnorm[cid] * 5.96046448e-08f * 1.01f;
+            dlo[m] = d * (1.f - eps1) - e2;
+            const float up = (d * (1.f + eps1) + e2) * (1.f + 1e-6f);
+            if (cid != cur) {
+                if (cur >= 0) atomicMin(&ubits[cur], best);
+                cur = cid;
+                best = ~0u;
+            }
+            best = min(best, __float_as_uint(up));  // non-negative: bit order = value order
+        }
+    }
+    if (lane == 0 && cur >= 0) atomicMin(&ubits[cur], best);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_seal_exact(int64_t nfeat_total, int D, const int32_t *__restrict__ fmem_cls,
+                                                    const int32_t *__restrict__ fmem_cid,
+                                                    const char *const *__restrict__ frow,
+                                                    const double *__restrict__ fcent, const PwPlan *__restrict__ plan,
+                                                    const float *__restrict__ dlo,
+                                                    const unsigned int *__restrict__ ubits,
+                                                    unsigned long long *__restrict__ best_bits,
+                                                    double *__restrict__ dout) {
+    extern __shared__ double sscratch[];
+    const int wpb = blockDim.x >> 5, w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int per = plan->n_chains + plan->n_leaves + plan->n_ops;
+    double *scr = sscratch + w * per;
+    const int64_t base = ((int64_t)blockIdx.x * wpb + w) * 32;
+    if (base >= nfeat_total) return;
+    const int64_t m = base + lane;
+    bool cand = false;
+    int cid = -1;
+    if (m < nfeat_total) {
+        cid = fmem_cid[m];
+        cand = dlo[m] <= __uint_as_float(ubits[cid]);
+        if (!cand) dout[m] = __longlong_as_double(0x7ff0000000000000ll);  // +inf: never the minimum
+    }
+    for (unsigned b = __ballot_sync(0xffffffffu, cand); b; b &= b - 1) {
+        const int l = __ffs(b) - 1;
+        const int64_t mm = base + l;
+        const int cc = __shfl_sync(0xffffffffu, cid, l);
+        const T *f = (const T *)frow[fmem_cls[mm]];
+        const double *c = fcent + (int64_t)cc * D;
+        const double sx = pw_sum_warp(*plan, [&](int k) {
+            const double x = dsub(c[k], to_d(f[k]));
+            return dmul(x, x);
+        }, scr);
+        if (lane == 0) {
+            const double d = __dsqrt_rn(sx);
+            dout[mm] = d;
+            atomicMin(&best_bits[cc], (unsigned long long)__double_as_longlong(d));
+        }
+    }
+}
+
 __global__ void k_seal_pick(int64_t nfeat_total, const int32_t *__restrict__ fmem_cid, const int64_t *__restrict__ foff,
                             const double *__restrict__ dout, const unsigned long long *__restrict__ best_bits,
                             int *__restrict__ best_pos) {
@@ -3576,7 +3700,39 @@ void launch_seal(fx_stream *s, int64_t nfeat_total, const int32_t *fmem_cls, con
     const int threads = 256;
     size_t smem = sizeof(double) * per * (threads / 32);
     unsigned grid = (unsigned)std::min<int64_t>(cdiv(nfeat_total, threads / 32), 148 * 16);
-    if (s->cfg.feat_type == FX_F64) {
+    static const bool seal_full = getenv("FOCUS_B200_SEAL_FULL") && atoi(getenv("FOCUS_B200_SEAL_FULL"));
+    if (!seal_full) {
+        // screened: an fp32 pass for every member, numpy's float64 pairwise
+        // order only for the candidates of each cluster's minimum
+        const int D = s->cfg.dim;
+        const float eps1 = (float)((double)(D + 3) * 5.960464477539063e-08 * 1.01);
+        const int64_t C = s->h_ctr[C_NEXT_CID];
+        DevBuf<float> c32, cn, dl;
+        DevBuf<unsigned int> ub;
+        c32.reserve((size_t)std::max<int64_t>(C, 1) * D);
+        cn.reserve(C + 1);
+        dl.reserve(nfeat_total + 1);
+        ub.reserve(C + 1);
+        FX_CUDA(cudaMemsetAsync(ub.p, 0xff, sizeof(unsigned int) * (C + 1), s->st));
+        k_seal_c32<<<(unsigned)std::min<int64_t>(std::max<int64_t>(C, 1), 148 * 8), 256, 0, s->st>>>(C, D, s->fcent.p,
+                                                                                                    c32.p, cn.p);
+        const unsigned g1 = (unsigned)std::min<int64_t>(cdiv(nfeat_total, threads / 32), 148 * 16);
+        const unsigned g2 = (unsigned)cdiv(nfeat_total, threads);
+        if (s->cfg.feat_type == FX_F64) {
+            k_seal_screen<double><<<g1, threads, 0, s->st>>>(nfeat_total, D, fmem_cls, fmem_cid, s->frow.p, c32.p, cn.p,
+                                                             eps1, dl.p, ub.p);
+            FX_CUDA(cudaFuncSetAttribute(k_seal_exact<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            k_seal_exact<double><<<g2, threads, smem, s->st>>>(nfeat_total, D, fmem_cls, fmem_cid, s->frow.p, s->fcent.p,
+                                                              s->plan.p, dl.p, ub.p, best_bits, dout);
+        } else {
+            k_seal_screen<float><<<g1, threads, 0, s->st>>>(nfeat_total, D, fmem_cls, fmem_cid, s->frow.p, c32.p, cn.p,
+                                                            eps1, dl.p, ub.p);
+            FX_CUDA(cudaFuncSetAttribute(k_seal_exact<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            k_seal_exact<float><<<g2, threads, smem, s->st>>>(nfeat_total, D, fmem_cls, fmem_cid, s->frow.p, s->fcent.p,
+                                                             s->plan.p, dl.p, ub.p, best_bits, dout);
+        }
+        FX_LAUNCHED();
+    } else if (s->cfg.feat_type == FX_F64) {
         FX_CUDA(cudaFuncSetAttribute(k_seal_dist<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         k_seal_dist<double><<<grid, threads, smem, s->st>>>(nfeat_total, s->cfg.dim, fmem_cls, fmem_cid, s->frow.p,
                                                             s->fcent.p, s->plan.p, best_bits, dout);

@@ -88,19 +88,20 @@ class QuerySession:
             other = np.ones(V, np.uint8)
             cs = np.array([c for c in ingest_profile.class_set if 0 <= c < V], np.int64)
             other[cs] = 0
-        h = _lib.vp()
-        _lib.check(self.L.fx_session_create(dev.handle, None, None if key is None else _lib.p32(key), n_keys,
-                                            _lib.pu8(other) if other is not None else None, ctypes.byref(h)))
-        self.handle = h
+        rl = None
         if isinstance(labels, np.ndarray) and C:
-            # the representatives' labels only (C values, not the whole array)
+            # the representatives' labels only (C values, not the whole array),
+            # handed to the session when it is created
             lab = np.asarray(labels)
             ok = (reps >= 0) & (reps < lab.size)
             rl = np.full(C, _NO_OBJECT, np.int32)
             rl[ok] = lab[reps[ok]]
             rl[reps < 0] = _NO_REP
-            cidx = np.arange(C, dtype=np.int32)
-            _lib.check(self.L.fx_session_set_labels(h, C, _lib.p32(cidx), _lib.p32(rl)))
+        h = _lib.vp()
+        _lib.check(self.L.fx_session_create(dev.handle, None if rl is None else _lib.p32(rl),
+                                            None if key is None else _lib.p32(key), n_keys,
+                                            _lib.pu8(other) if other is not None else None, ctypes.byref(h)))
+        self.handle = h
 
     def __del__(self):
         h, self.handle = getattr(self, "handle", None), None

@@ -1,0 +1,7 @@
+mkdir -p gpurun_out
+timeout 400 python -m pytest tests/test_gpu_parity.py tests/test_gpu_seeds.py tests/test_gpu_scale_parity.py tests/test_gpu_reference_ports.py -x -q > gpurun_out/pytest_r02al.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_r02al.log
+tail -2 gpurun_out/pytest_r02al.log
+Q="--steps 5 --warmup 3 --no-check --no-cpu --queries 0 --no-fc --multi-streams 0 --c3-objects 0 --e2e-steps 1"
+timeout 120 python bench.py $Q > gpurun_out/bench_r02al.log 2>&1
+FOCUS_B200_SEAL_FULL=1 timeout 120 python bench.py $Q > gpurun_out/bench_r02al_full.log 2>&1
+for f in gpurun_out/bench_r02al*.log; do echo $f; grep '^{' $f | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['value'], d['ms_per_step'], d['roofline']['per_kernel']['seal'])"; done
