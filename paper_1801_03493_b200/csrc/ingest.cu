@@ -32,25 +32,55 @@ namespace fx {
 // K0: pixel differencing (ingest.py:37-47)
 // ---------------------------------------------------------------------------
 
-__global__ void k_dup_flags(int64_t n, int S, const int64_t *__restrict__ fid, const double *__restrict__ sig,
-                            int has_prev, int64_t prev_fid, const double *__restrict__ prev_sig, double eps,
-                            uint8_t *__restrict__ is_dup) {
-    int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+// K0: pixel_diff of every object against its predecessor (ingest.py:37-47).
+// A CTA stages its 256 objects' signatures plus the predecessor's in shared
+// memory with coalesced loads (row stride S + 1 doubles: conflict-free
+// column reads), then each thread takes numpy's pairwise mean of |a - b|.
+constexpr int DUP_T = 256, DUP_SMAX = 20;
+__global__ void __launch_bounds__(DUP_T) k_dup_flags(int64_t n, int S, const int64_t *__restrict__ fid,
+                                                     const double *__restrict__ sig, int has_prev, int64_t prev_fid,
+                                                     const double *__restrict__ prev_sig, double eps,
+                                                     uint8_t *__restrict__ is_dup) {
+    __shared__ double ssig[(DUP_T + 1) * (DUP_SMAX + 1)];
+    const int64_t i0 = (int64_t)blockIdx.x * DUP_T;
+    const int tid = threadIdx.x;
+    const int64_t i = i0 + tid;
+    const bool staged = S <= DUP_SMAX;
+    if (staged && eps >= 0.0) {
+        const int64_t rem = n - i0 + 1;
+        const int nrow = (int)(rem < DUP_T + 1 ? rem : DUP_T + 1);  // rows i0-1 .. i0+DUP_T-1
+        for (int e = tid; e < nrow * S; e += DUP_T) {
+            const int r = e / S, k = e % S;
+            const int64_t src = i0 - 1 + r;
+            double v = 0.0;
+            if (src >= 0) v = sig[src * S + k];
+            else if (has_prev) v = prev_sig[k];
+            ssig[r * (S + 1) + k] = v;
+        }
+    }
+    __syncthreads();
     if (i >= n) return;
     uint8_t d = 0;
     if (eps >= 0.0) {
-        const double *a = nullptr;
         int64_t pf = 0;
+        bool have = false;
         if (i > 0) {
-            a = sig + (i - 1) * S;
             pf = fid[i - 1];
+            have = true;
         } else if (has_prev) {
-            a = prev_sig;
             pf = prev_fid;
+            have = true;
         }
-        if (a && fid[i] - pf <= 1) {
-            const double *b = sig + i * S;
-            double sum = pw_sum_seq(S, [&](int k) { return fabs(dsub(a[k], b[k])); });
+        if (have && fid[i] - pf <= 1) {
+            double sum;
+            if (staged) {
+                const double *a = ssig + tid * (S + 1), *b = ssig + (tid + 1) * (S + 1);
+                sum = pw_sum_seq(S, [&](int k) { return fabs(dsub(a[k], b[k])); });
+            } else {
+                const double *a = i > 0 ? sig + (i - 1) * S : prev_sig;
+                const double *b = sig + i * S;
+                sum = pw_sum_seq(S, [&](int k) { return fabs(dsub(a[k], b[k])); });
+            }
             d = ddiv(sum, (double)S) <= eps;
         }
     }
@@ -3629,14 +3659,14 @@ template void run_batches<double>(fx_stream *, int64_t, int64_t);
 
 void launch_dup_flags(fx_stream *s, int64_t n, const int64_t *d_fid, const double *d_sig, uint8_t *d_out) {
     const int S = s->cfg.sig_dim;
-    k_dup_flags<<<(unsigned)cdiv(n, 256), 256, 0, s->st>>>(n, S, d_fid, d_sig, s->has_prev ? 1 : 0, s->prev_fid,
+    k_dup_flags<<<(unsigned)cdiv(n, DUP_T), DUP_T, 0, s->st>>>(n, S, d_fid, d_sig, s->has_prev ? 1 : 0, s->prev_fid,
                                                            s->prev_sig.p, s->cfg.pixel_eps, d_out);
     FX_LAUNCHED();
 }
 
 void launch_dup_flags_raw(int64_t n, int S, const int64_t *d_fid, const double *d_sig, double eps, uint8_t *d_out,
                           cudaStream_t st) {
-    k_dup_flags<<<(unsigned)cdiv(n, 256), 256, 0, st>>>(n, S, d_fid, d_sig, 0, 0, nullptr, eps, d_out);
+    k_dup_flags<<<(unsigned)cdiv(n, DUP_T), DUP_T, 0, st>>>(n, S, d_fid, d_sig, 0, 0, nullptr, eps, d_out);
     FX_LAUNCHED();
 }
 

@@ -65,8 +65,9 @@ for k, v in sorted(gaps.items(), key=lambda x: -x[1][1])[:15]:
 
 # timeline of three steady-state batches (k_snap_pack starts each batch)
 marks = [i for i, e in enumerate(ev) if "k_snap_pack" in e[2]]
-if len(marks) > 160:
-    for bi in (150, 151, 152):
+if len(marks) > 8:
+    b0 = (3 * len(marks)) // 4  # steady state
+    for bi in (b0, b0 + 1, b0 + 2):
         i0, i1 = marks[bi], marks[bi + 1]
         t0 = ev[i0][0]
         print(f"\nbatch {bi}: {(ev[i1][0] - t0) / 1e3 * 1e3:.1f} us")
