@@ -394,6 +394,10 @@ int fx_stream_create(const fx_stream_config *cfg, fx_stream **out) {
                 s->tf_cn2.reserve(nd * gx);
                 s->tf_cnt.reserve(nd);
                 FX_CUDA(cudaMemsetAsync(s->tf_cnt.p, 0, sizeof(int32_t) * nd, s->st));
+                s->chain_epoch.reserve(1);
+                s->fold_done.reserve(1);
+                FX_CUDA(cudaMemsetAsync(s->chain_epoch.p, 0, sizeof(unsigned long long), s->st));
+                FX_CUDA(cudaMemsetAsync(s->fold_done.p, 0, sizeof(unsigned int), s->st));
                 s->tf_P.reserve((size_t)B * D);
                 s->tf_PF.reserve((size_t)B);
                 s->cd_meta.reserve(2 * 8 * nd);

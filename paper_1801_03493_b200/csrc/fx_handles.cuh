@@ -119,6 +119,8 @@ struct fx_stream {
     fx::DevBuf<double> tf_part;            // [TF_SPLIT * D + TF_SPLIT] row-chunk partials of the largest slot
     fx::DevBuf<int32_t> tf_bcnt;           // [gx] row chunks done per column slice
     fx::DevBuf<unsigned char> rs_gobj;     // k_resolve's per-object state when B > 4096 (global instead of smem)
+    fx::DevBuf<unsigned long long> chain_epoch;  // [1] lagged chains completed (k_fold's last CTA)
+    fx::DevBuf<unsigned int> fold_done;          // [1] k_fold CTAs finished (last-CTA election)
     fx::DevBuf<double> tf_P, tf_PF;        // k_tfold_a piece sums [B * D] (by piece start row), norm sums [B]
     fx::DevBuf<int32_t> cd_meta, cd_off;   // [2][8][2B+3], [2][2B+3] chain descriptors (double buffered)
     fx::DevBuf<const char *> cd_rows;      // [2][B] member rows of the chain (nullptr: already in S)

@@ -386,6 +386,7 @@ struct ResolveArgs {
     float *f_P, *f_csum, *f_cmax, *f_gf;
     double *f_gd;
     unsigned char *rs_gobj;  // per-object state in global memory (B > 4096), else nullptr
+    const unsigned long long *chain_epoch;  // lagged exact chains completed (k_fold's last CTA)
 };
 
 constexpr int RS_THREADS = 512;
@@ -776,6 +777,101 @@ __global__ void __launch_bounds__(256, MINB) k_rowpass(int nA, int64_t a0, const
     }
 }
 
+// Lean row pass (D <= 2048, fp32 rows, 16-byte aligned): the same outputs as
+// k_rowpass<16> with the same arithmetic order (each lane's 64 squared
+// differences summed sequentially, then the warp tree), but the row is not
+// held in registers across the distance-row scan: it is streamed in quarters
+// together with the centroid row, so the kernel fits 4 CTAs per SM (one
+// wave for a batch of 8192) instead of 2.
+__global__ void __launch_bounds__(256, 4) k_rowpass_lean(int nA, int64_t a0, const char *const *__restrict__ frow,
+                                                        int D, const int64_t *__restrict__ ctr,
+                                                        const float *__restrict__ dist, int64_t ld,
+                                                        const float *__restrict__ cn2, const int32_t *__restrict__ snap,
+                                                        const float *__restrict__ fnorm, ScreenModel sm, float rel,
+                                                        float absc, const float *__restrict__ C32, double T,
+                                                        const int32_t *__restrict__ res_pos, float *__restrict__ dres,
+                                                        int64_t ldr, int32_t *__restrict__ sum_slot,
+                                                        int32_t *__restrict__ sum_q, float *__restrict__ sum_d1,
+                                                        float *__restrict__ sum_e1, float *__restrict__ sum_lbr,
+                                                        const float *__restrict__ snorm) {
+    pdl_enter();
+    constexpr int NV = 16, QV = 4;  // float4 per lane per row, per quarter
+    __shared__ int s_rpos[RC_MAX];
+    __shared__ int s_pmin;
+    const int nsnap = (int)ctr[C_NSNAP];
+    const int nres_all = (int)ctr[C_NRES];
+    const int nres = nres_all <= RC_MAX ? nres_all : 0;  // more: the tiled kernel writes the columns
+    if (threadIdx.x == 0) s_pmin = INT_MAX;
+    __syncthreads();
+    for (int r = threadIdx.x; r < nres; r += blockDim.x) {
+        s_rpos[r] = res_pos[r];
+        atomicMin(&s_pmin, res_pos[r]);
+    }
+    __syncthreads();
+    const int pmin = s_pmin;
+    const int lane = threadIdx.x & 31;
+    const int nw = blockDim.x >> 5;
+    for (int w = blockIdx.x * nw + (threadIdx.x >> 5); w < nA; w += gridDim.x * nw) {
+        const float fn = fnorm[a0 + w];
+        const float4 *f4 = (const float4 *)frow[a0 + w];
+        float u1, l1, lbr;
+        int q1;
+        row_scan(dist + (int64_t)w * ld, nsnap, cn2, snap, snorm, sm, fn, lane, u1, l1, lbr, q1);
+        float d1 = 0.5f * (l1 + u1), e1 = 0.5f * (u1 - l1);
+        auto dist_to = [&](const float4 *c4) {
+            float acc = 0.f;
+#pragma unroll 1
+            for (int j0 = 0; j0 < NV; j0 += QV) {
+                float4 x[QV], c[QV];
+#pragma unroll
+                for (int j = 0; j < QV; j++) {
+                    const int e = lane + 32 * (j0 + j);
+                    const bool in = 4 * e < D;
+                    x[j] = in ? __ldg(f4 + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    c[j] = in ? __ldg(c4 + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+                for (int j = 0; j < QV; j++) {
+                    if (4 * (lane + 32 * (j0 + j)) < D) {
+                        float d = x[j].x - c[j].x;
+                        acc = fmaf(d, d, acc);
+                        d = x[j].y - c[j].y;
+                        acc = fmaf(d, d, acc);
+                        d = x[j].z - c[j].z;
+                        acc = fmaf(d, d, acc);
+                        d = x[j].w - c[j].w;
+                        acc = fmaf(d, d, acc);
+                    }
+                }
+            }
+            return sqrtf(warp_sum(acc));
+        };
+        if (sm.tc && q1 >= 0) {  // a tight ub0 keeps the resolve's drift bounds small
+            const float dd = dist_to((const float4 *)(C32 + (int64_t)snap[q1] * D));
+            const float ee = rel * dd + absc * (sqrtf(cn2[snap[q1]]) * 1.00001f + fn) + 1e-30f;
+            if (dd + ee < u1) {  // keep whichever interval is tighter (both are valid)
+                d1 = dd;
+                e1 = ee;
+            }
+        }
+        if (nres > 0 && w > pmin) {
+            for (int r = 0; r < nres; r++) {
+                const int rp = s_rpos[r];
+                if (rp >= w) continue;
+                const float v = dist_to((const float4 *)frow[a0 + rp]);
+                if (lane == 0) dres[(int64_t)w * ldr + r] = v;
+            }
+        }
+        if (lane == 0) {
+            sum_slot[w] = q1 >= 0 ? snap[q1] : -1;
+            sum_q[w] = q1;
+            sum_d1[w] = d1;
+            sum_e1[w] = e1;
+            sum_lbr[w] = lbr;
+        }
+    }
+}
+
 constexpr int RS_MAXGRP = 512;
 constexpr int RS_RANKW = 8;
 #ifndef RS_UB_SCAN
@@ -911,6 +1007,18 @@ __global__ void __launch_bounds__(RS_THREADS, 1) k_resolve(ResolveArgs A) {
         __syncthreads();
         if (threadIdx.x == 0) A.ctr[C_FASTST] = 0;
         if (fst == 1) return;
+    }
+    // the exact path reads and writes the reference's float64 sums S: the
+    // previous batch's lagged chain (k_fold, second stream) must be done.
+    // Waiting here instead of on the stream keeps the fast path off the
+    // chain (the chain needs no SM this CTA holds, so it always progresses).
+    if (A.chain_epoch) {
+        if (threadIdx.x == 0) {
+            while (*(volatile const unsigned long long *)A.chain_epoch < (unsigned long long)A.batch_no)
+                __nanosleep(200);
+            __threadfence();
+        }
+        __syncthreads();
     }
 
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -2838,7 +2946,9 @@ __global__ void __launch_bounds__(TF3_T) k_tfold_b(
 template <typename T>
 __global__ void __launch_bounds__(FOLD_THREADS) k_fold(int D, ChainDesc cd, double *__restrict__ S,
                                                       double *__restrict__ fcent, int32_t *__restrict__ cl_nfeat,
-                                                      int32_t *__restrict__ cl_size, long long *__restrict__ fprof) {
+                                                      int32_t *__restrict__ cl_size, long long *__restrict__ fprof,
+                                                      unsigned int *__restrict__ done_ctas,
+                                                      unsigned long long *__restrict__ chain_epoch) {
     constexpr int R = fold_rows<T>();
     extern __shared__ __align__(16) unsigned char fold_raw[];
     T *ring = (T *)fold_raw;                                                // [NS][R][FD]
@@ -2947,6 +3057,17 @@ __global__ void __launch_bounds__(FOLD_THREADS) k_fold(int D, ChainDesc cd, doub
             }
         }
         J0 += nst;
+    }
+    // the last CTA to finish publishes the chain's completion (k_resolve's
+    // exact path waits for it)
+    __syncthreads();
+    if (threadIdx.x == 0 && done_ctas) {
+        __threadfence();
+        if (atomicAdd(done_ctas, 1u) == gridDim.x * gridDim.y - 1) {
+            *done_ctas = 0;
+            __threadfence();
+            atomicAdd(chain_epoch, 1ull);
+        }
     }
 }
 
@@ -3362,7 +3483,13 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
         if (rowpass) {
             const unsigned grid = (unsigned)std::min<int64_t>(cdiv((int64_t)B * 32, 256), 148 * 8);
             static const int rp_minb = getenv("FOCUS_B200_RP_MINB") ? atoi(getenv("FOCUS_B200_RP_MINB")) : 2;
-            if (D <= 1024)
+            static const bool rp_lean = !(getenv("FOCUS_B200_RP_LEAN") && atoi(getenv("FOCUS_B200_RP_LEAN")) == 0);
+            if (rp_lean && D > 1024)
+                launch_pdl(k_rowpass_lean, dim3((unsigned)std::min<int64_t>(cdiv((int64_t)B * 32, 256), 148 * 4)),
+                           dim3(256), 0, st, B, c0, s->frow.p, D, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p,
+                           s->snap_slot.p, s->fnorm.p, sm, rel, absc, s->C32.p, s->cfg.t, s->res_pos.p, s->dres.p, B,
+                           s->sum_slot.p, s->sum_q.p, s->sum_d1.p, s->sum_e1.p, s->sum_lbr.p, snorm);
+            else if (D <= 1024)
                 launch_pdl(k_rowpass<8, 2>, dim3(grid), dim3(256), 0, st, B, c0, s->frow.p, D, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p,
                                                    s->snap_slot.p, s->fnorm.p, sm, rel, absc, s->C32.p, s->cfg.t,
                                                    s->res_pos.p, s->dres.p, B, s->sum_slot.p, s->sum_q.p, s->sum_d1.p,
@@ -3484,8 +3611,15 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
                 FX_LAUNCHED();
             }
             // its exact path reads the reference's float64 sums: the previous
-            // batch's chain must be done (it ran alongside this batch's screen)
-            if (s->chain_pending[cbuf ^ 1]) FX_CUDA(cudaStreamWaitEvent(st, s->ev_ch[cbuf ^ 1], 0));
+            // batch's chain must be done -- the resolve waits for it on the
+            // device, and only when it takes the exact path (inline chains are
+            // stream-ordered already)
+            if (multi_inline || !s->chain_epoch.p) {
+                if (s->chain_pending[cbuf ^ 1]) FX_CUDA(cudaStreamWaitEvent(st, s->ev_ch[cbuf ^ 1], 0));
+                A.chain_epoch = nullptr;
+            } else {
+                A.chain_epoch = s->chain_epoch.p;
+            }
             launch_pdl(kern, dim3(1), dim3(RS_THREADS), smem, st, A);
             FX_LAUNCHED();
         }
@@ -3581,6 +3715,8 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
         {
             s->tstart(3);
             const int buf = cbuf;
+            // the chain of two batches ago read this buffer's descriptor
+            if (s->chain_pending[buf]) FX_CUDA(cudaStreamWaitEvent(st, s->ev_ch[buf], 0));
             const int64_t gxt = cdiv(D, TF_C);
             const int64_t gyt = TF_SPLIT + std::max<int64_t>(4, std::min<int64_t>(2 * (int64_t)B + 1, (148 * 4) / gxt));
             const int ldm = 2 * s->B + 3;
@@ -3627,7 +3763,8 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             }
             ChainDesc cd{s->cd_nd.p + buf, meta, ldm, coff, crows};
             k_fold<T><<<dim3((unsigned)gx, (unsigned)gy), FOLD_THREADS, fold_smem<T>(), fst>>>(
-                D, cd, s->S.p, s->fcent.p, s->cl_nfeat.p, s->cl_size.p, (long long *)(s->prof.p + 16));
+                D, cd, s->S.p, s->fcent.p, s->cl_nfeat.p, s->cl_size.p, (long long *)(s->prof.p + 16),
+                s->fold_done.p, s->chain_epoch.p);  // inline chains count too (the mode can change mid-stream)
             FX_LAUNCHED();
             if (!fold_inline) {
                 FX_CUDA(cudaEventRecord(s->ev_ch[buf], s->st2));
