@@ -541,13 +541,14 @@ __device__ double exact_dist(const ResolveArgs &A, int b, int slot, const int32_
 // two-level gather cn2[snap[q]] when present.
 __device__ __forceinline__ void row_scan(const float *__restrict__ drow, int nsnap, const float *__restrict__ cn2,
                                          const int32_t *__restrict__ snap, const float *__restrict__ snorm,
-                                         ScreenModel sm, float fn, int lane, float &u1, float &l1, float &lbr, int &q1) {
+                                         ScreenModel sm, float fn, int lane, float &u1, float &l1, float &lbr, int &q1,
+                                         int qbeg = 0) {
     constexpr int U = 8;
     u1 = INFINITY;
     l1 = INFINITY;
     lbr = INFINITY;
     q1 = -1;
-    for (int q0 = 0; q0 < nsnap; q0 += 32 * U) {
+    for (int q0 = qbeg; q0 < nsnap; q0 += 32 * U) {
         float dv[U], nv[U];
 #pragma unroll
         for (int u = 0; u < U; u++) {
@@ -869,6 +870,106 @@ __global__ void __launch_bounds__(256, 4) k_rowpass_lean(int nA, int64_t a0, con
             sum_e1[w] = e1;
             sum_lbr[w] = lbr;
         }
+    }
+}
+
+// Wide row pass for large snapshots (C3: 100 k live centroids): one CTA per
+// object, the distance row split over 8 warps (row_scan per segment, merged
+// in warp order with row_scan's tie rule), then warp 0 refines the best
+// candidate exactly as k_rowpass_lean.  Residual columns are left to the
+// tiled kernel (this variant runs only when there are none to do here).
+constexpr int RPW_T = 256, RPW_W = RPW_T / 32;
+__global__ void __launch_bounds__(RPW_T) k_rowpass_wide(int nA, int64_t a0, const char *const *__restrict__ frow,
+                                                       int D, const int64_t *__restrict__ ctr,
+                                                       const float *__restrict__ dist, int64_t ld,
+                                                       const float *__restrict__ cn2, const int32_t *__restrict__ snap,
+                                                       const float *__restrict__ fnorm, ScreenModel sm, float rel,
+                                                       float absc, const float *__restrict__ C32,
+                                                       int32_t *__restrict__ sum_slot, int32_t *__restrict__ sum_q,
+                                                       float *__restrict__ sum_d1, float *__restrict__ sum_e1,
+                                                       float *__restrict__ sum_lbr, const float *__restrict__ snorm) {
+    pdl_enter();
+    __shared__ float s_u[RPW_W], s_l[RPW_W], s_r[RPW_W];
+    __shared__ int s_q[RPW_W];
+    const int nsnap = (int)ctr[C_NSNAP];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int w = blockIdx.x; w < nA; w += gridDim.x) {
+        const float fn = fnorm[a0 + w];
+        const int seg = ((nsnap + RPW_W - 1) / RPW_W + 255) & ~255;  // whole 32 x 8 row_scan steps
+        const int qb = wid * seg, qe = min(nsnap, qb + seg);
+        float u1, l1, lbr;
+        int q1;
+        row_scan(dist + (int64_t)w * ld, qe, cn2, snap, snorm, sm, fn, lane, u1, l1, lbr, q1, qb);
+        if (lane == 0) {
+            s_u[wid] = u1;
+            s_l[wid] = l1;
+            s_r[wid] = lbr;
+            s_q[wid] = q1;
+        }
+        __syncthreads();
+        if (wid == 0) {
+            u1 = s_u[0];
+            l1 = s_l[0];
+            lbr = s_r[0];
+            q1 = s_q[0];
+            for (int v = 1; v < RPW_W; v++) {
+                const float ou = s_u[v], ol = s_l[v], olbr = s_r[v];
+                const int oq = s_q[v];
+                const bool take = oq >= 0 && (q1 < 0 || ou < u1 || (ou == u1 && oq < q1));
+                if (take) {
+                    lbr = fminf(fminf(lbr, olbr), q1 >= 0 ? l1 : INFINITY);
+                    u1 = ou;
+                    l1 = ol;
+                    q1 = oq;
+                } else {
+                    lbr = fminf(fminf(lbr, olbr), oq >= 0 ? ol : INFINITY);
+                }
+            }
+            float d1 = 0.5f * (l1 + u1), e1 = 0.5f * (u1 - l1);
+            if (sm.tc && q1 >= 0) {
+                const float4 *f4 = (const float4 *)frow[a0 + w];
+                const float4 *c4 = (const float4 *)(C32 + (int64_t)snap[q1] * D);
+                float acc = 0.f;
+#pragma unroll 1
+                for (int j0 = 0; j0 < 16; j0 += 4) {
+                    float4 x[4], c[4];
+#pragma unroll
+                    for (int j = 0; j < 4; j++) {
+                        const int e = lane + 32 * (j0 + j);
+                        const bool in = 4 * e < D;
+                        x[j] = in ? __ldg(f4 + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+                        c[j] = in ? __ldg(c4 + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+#pragma unroll
+                    for (int j = 0; j < 4; j++) {
+                        if (4 * (lane + 32 * (j0 + j)) < D) {
+                            float d = x[j].x - c[j].x;
+                            acc = fmaf(d, d, acc);
+                            d = x[j].y - c[j].y;
+                            acc = fmaf(d, d, acc);
+                            d = x[j].z - c[j].z;
+                            acc = fmaf(d, d, acc);
+                            d = x[j].w - c[j].w;
+                            acc = fmaf(d, d, acc);
+                        }
+                    }
+                }
+                const float dd = sqrtf(warp_sum(acc));
+                const float ee = rel * dd + absc * (sqrtf(cn2[snap[q1]]) * 1.00001f + fn) + 1e-30f;
+                if (dd + ee < u1) {
+                    d1 = dd;
+                    e1 = ee;
+                }
+            }
+            if (lane == 0) {
+                sum_slot[w] = q1 >= 0 ? snap[q1] : -1;
+                sum_q[w] = q1;
+                sum_d1[w] = d1;
+                sum_e1[w] = e1;
+                sum_lbr[w] = lbr;
+            }
+        }
+        __syncthreads();
     }
 }
 
@@ -3409,6 +3510,9 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
     std::vector<int32_t> chk_slots;
     // fused row pass: FP32 rows, D % 4 == 0, D <= 2048, 16-byte aligned rows
     const bool rowpass = sizeof(T) == 4 && D % 4 == 0 && D <= 2048 && s->rows_aligned16;
+    // large snapshots (C3): one CTA per object scans its distance row (k_rowpass_wide)
+    static const int wide_min = getenv("FOCUS_B200_RP_WIDE") ? atoi(getenv("FOCUS_B200_RP_WIDE")) : 4096;
+    const bool use_wide = rowpass && wide_min > 0 && s->ld > wide_min && D > 1024;
     for (int64_t c0 = c_begin, B = 0; c0 < c_end; c0 += B, bi++) {
         const auto h0 = hclock::now();
         const int cbuf = (int)(s->batch_no & 1);  // chain descriptor buffer of this batch
@@ -3459,7 +3563,8 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
                     s->res_col.p, s->res_pos.p, s->ctr.p + C_NRES);
                 FX_LAUNCHED();
             }
-            const bool rc_ok = D <= 6144;  // RC_COLS staged rows fit in shared memory
+            const bool rc_ok = D <= 6144 && !use_wide;  // RC_COLS staged rows fit in shared memory; the wide
+                                                        // row pass leaves every residual column to the tiled kernel
             if (rc_ok && !rowpass) {
                 const size_t smem = sizeof(float) * RC_COLS * D;
                 static size_t rc_set[64] = {};
@@ -3484,7 +3589,11 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             const unsigned grid = (unsigned)std::min<int64_t>(cdiv((int64_t)B * 32, 256), 148 * 8);
             static const int rp_minb = getenv("FOCUS_B200_RP_MINB") ? atoi(getenv("FOCUS_B200_RP_MINB")) : 2;
             static const bool rp_lean = !(getenv("FOCUS_B200_RP_LEAN") && atoi(getenv("FOCUS_B200_RP_LEAN")) == 0);
-            if (rp_lean && D > 1024)
+            if (use_wide)
+                launch_pdl(k_rowpass_wide, dim3((unsigned)std::min<int64_t>(B, 148 * 8)), dim3(RPW_T), 0, st, B, c0,
+                           s->frow.p, D, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p, s->snap_slot.p, s->fnorm.p, sm, rel,
+                           absc, s->C32.p, s->sum_slot.p, s->sum_q.p, s->sum_d1.p, s->sum_e1.p, s->sum_lbr.p, snorm);
+            else if (rp_lean && D > 1024)
                 launch_pdl(k_rowpass_lean, dim3((unsigned)std::min<int64_t>(cdiv((int64_t)B * 32, 256), 148 * 4)),
                            dim3(256), 0, st, B, c0, s->frow.p, D, s->ctr.p, s->dist.p, s->ld, s->s_cn2.p,
                            s->snap_slot.p, s->fnorm.p, sm, rel, absc, s->C32.p, s->cfg.t, s->res_pos.p, s->dres.p, B,
