@@ -432,7 +432,7 @@ int fx_stream_create(const fx_stream_config *cfg, fx_stream **out) {
                 s->f_P.reserve(B + 1);
                 for (auto *b : {&s->f_ccnt, &s->f_cdup}) b->reserve(nch * ng);
                 for (auto *b : {&s->f_csum, &s->f_cmax}) b->reserve(nch * ng);
-                s->f_gi.reserve(4 * ng);
+                s->f_gi.reserve(8 * ng);
                 s->f_gf.reserve(4 * ng);
                 s->f_gd.reserve(8);
             }

@@ -2375,7 +2375,7 @@ __global__ void __launch_bounds__(RF_T) k_rfast1(ResolveArgs A) {
     float su = 0.f, mx = 0.f, drift = 0.f;
     const int gg = tid;  // nsnap <= RF_MAXG = RF_T: one group per thread
     // the group's slot state, fetched before the chunk scan
-    int g_sl = 0, g_nf = 0;
+    int g_sl = 0, g_nf = 0, g_cid = 0, g_size = 0;
     float g_cn2 = 0.f;
     double g_sdev = 0.0;
     if (gg < nsnap) {
@@ -2383,6 +2383,8 @@ __global__ void __launch_bounds__(RF_T) k_rfast1(ResolveArgs A) {
         g_cn2 = A.s_cn2[g_sl];
         g_sdev = A.s_sdev[g_sl];
         g_nf = A.s_nfeat[g_sl];
+        g_cid = A.s_cid[g_sl];
+        g_size = A.s_size[g_sl];
     }
     if (gg < nsnap) {
         // chunk totals -> exclusive bases; 8 chunks' loads in flight before
@@ -2415,8 +2417,12 @@ __global__ void __launch_bounds__(RF_T) k_rfast1(ResolveArgs A) {
         const float cn = sqrtf(g_cn2) * 1.00001f;
         const float d0 = __double2float_ru(g_sdev);  // k_resolve's prologue: s_drift = s_sdev
         drift = c > 0 ? drift_avg(d0, g_nf, su, c, cn, mx) : d0;
-        A.f_gi[gg * 4 + 0] = c;
-        A.f_gi[gg * 4 + 1] = d;
+        A.f_gi[gg * 8 + 0] = c;
+        A.f_gi[gg * 8 + 1] = d;
+        A.f_gi[gg * 8 + 4] = g_sl;  // the group's slot state for k_rfast3 (one round of loads)
+        A.f_gi[gg * 8 + 5] = g_nf;
+        A.f_gi[gg * 8 + 6] = g_cid;
+        A.f_gi[gg * 8 + 7] = g_size;
         A.f_gf[gg * 4 + 0] = drift;
         A.f_gf[gg * 4 + 1] = mx;
         A.f_gf[gg * 4 + 2] = cn;
@@ -2508,14 +2514,14 @@ __global__ void __launch_bounds__(RF_T) k_rfast1(ResolveArgs A) {
     if (gg < nsnap) {
         const bool has = bcc > 0;  // the largest group is dirty[0] when any object joined
         if (gg == best && c > 0) {
-            A.f_gi[gg * 4 + 2] = 0;
-            A.f_gi[gg * 4 + 3] = 0;
+            A.f_gi[gg * 8 + 2] = 0;
+            A.f_gi[gg * 8 + 3] = 0;
         } else if (fl) {
-            A.f_gi[gg * 4 + 2] = (has ? 1 : 0) + bf + xf - 1;
-            A.f_gi[gg * 4 + 3] = (has ? bcc : 0) + bcn + xc - cv;
+            A.f_gi[gg * 8 + 2] = (has ? 1 : 0) + bf + xf - 1;
+            A.f_gi[gg * 8 + 3] = (has ? bcc : 0) + bcn + xc - cv;
         } else {
-            A.f_gi[gg * 4 + 2] = -1;
-            A.f_gi[gg * 4 + 3] = 0;
+            A.f_gi[gg * 8 + 2] = -1;
+            A.f_gi[gg * 8 + 3] = 0;
         }
     }
     if (tid == 0) ctr[C_FDONE] = 0;
@@ -2538,8 +2544,8 @@ __global__ void __launch_bounds__(RF_T) k_rfast3(ResolveArgs A) {
         const int idx = blockIdx.x * RF_MAXG + g;
         const int i = A.f_ccnt[idx] + A.f_rank[p];
         const float P = __fadd_ru(A.f_csum[idx], A.f_P[p]);
-        const int sl = A.snap_slot[g];
-        const int nf0 = A.s_nfeat[sl];
+        const int sl = A.f_gi[g * 8 + 4];
+        const int nf0 = A.f_gi[g * 8 + 5];
         const float ub0 = (A.sum_d1[p] + A.sum_e1[p]) * 1.000001f + 1e-30f;
         const double ub =
             (double)ub0 + (double)drift_avg(A.f_gf[g * 4 + 3], nf0, P, i, A.f_gf[g * 4 + 2], A.f_gf[g * 4 + 1]);
@@ -2549,13 +2555,13 @@ __global__ void __launch_bounds__(RF_T) k_rfast3(ResolveArgs A) {
         const double lbo = (double)lbr2 - md * 1.000001;
         if (lbo > ub && ub <= A.T) {
             const int64_t obj = A.cls_obj[A.c0 + p];
-            A.cluster_of[obj] = A.s_cid[sl];
-            A.mrank[obj] = A.s_size[sl] + i + A.f_cdup[idx] + A.f_dup[p];
+            A.cluster_of[obj] = A.f_gi[g * 8 + 6];
+            A.mrank[obj] = A.f_gi[g * 8 + 7] + i + A.f_cdup[idx] + A.f_dup[p];
             A.frank[obj] = nf0 + i;
             A.pend_rank[p] = i;
             A.slot_of[p] = sl;
-            A.pend_list[A.f_gi[g * 4 + 3] + i] = p;
-            A.pend_seg[A.f_gi[g * 4 + 3] + i] = A.f_gi[g * 4 + 2];
+            A.pend_list[A.f_gi[g * 8 + 3] + i] = p;
+            A.pend_seg[A.f_gi[g * 8 + 3] + i] = A.f_gi[g * 8 + 2];
         } else {
             s_fail = 1;
         }
@@ -2576,28 +2582,28 @@ __global__ void __launch_bounds__(RF_T) k_rfast3(ResolveArgs A) {
     const int gg = tid;
     int nd = 0;
     if (gg < nsnap) {
-        const int sl = A.snap_slot[gg];
-        const int c = A.f_gi[gg * 4 + 0];
+        const int sl = A.f_gi[gg * 8 + 4];
+        const int c = A.f_gi[gg * 8 + 0];
         A.s_snapq[sl] = gg;
         A.s_seedpos[sl] = -1;
         A.s_foldpos[sl] = 0;
         A.s_odcol[sl] = -1;
         if (c > 0) {
-            const int di = A.f_gi[gg * 4 + 2];
+            const int di = A.f_gi[gg * 8 + 2];
             A.s_drift[sl] = (double)A.f_gf[gg * 4 + 0];
-            A.s_nfeat[sl] += c;
-            A.s_size[sl] += c + A.f_gi[gg * 4 + 1];
+            A.s_nfeat[sl] = A.f_gi[gg * 8 + 5] + c;
+            A.s_size[sl] = A.f_gi[gg * 8 + 7] + c + A.f_gi[gg * 8 + 1];
             A.s_pend[sl] = c;
             A.s_didx[sl] = di;
             A.dirty[di] = sl;
-            A.dirty_off[di] = A.f_gi[gg * 4 + 3];
+            A.dirty_off[di] = A.f_gi[gg * 8 + 3];
             A.s_cn2[sl] = 0.f;  // the fold re-accumulates ||c||^2
         } else {
             A.s_drift[sl] = A.s_sdev[sl];
             A.s_pend[sl] = 0;
         }
     }
-    const unsigned long long has = __ballot_sync(0xffffffffu, gg < nsnap && A.f_gi[gg * 4 + 0] > 0);
+    const unsigned long long has = __ballot_sync(0xffffffffu, gg < nsnap && A.f_gi[gg * 8 + 0] > 0);
     __shared__ int s_nd;
     if (tid == 0) s_nd = 0;
     __syncthreads();
@@ -2618,7 +2624,7 @@ __global__ void __launch_bounds__(RF_T) k_rfast3(ResolveArgs A) {
         ctr[C_DC] += (int64_t)L * B;
         ctr[C_FAST] += B;
         ctr[C_NINSERTED] += B;
-        ctr[C_LAST_CID] = A.s_cid[A.snap_slot[A.sum_q[B - 1]]];
+        ctr[C_LAST_CID] = A.f_gi[A.sum_q[B - 1] * 8 + 6];  // the fast path creates no cluster
         ctr[C_FASTB] += 1;
         if (A.h_ring) {
             A.h_ring[C_NEXT_CID] = ctr[C_NEXT_CID];
