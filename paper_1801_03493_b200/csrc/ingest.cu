@@ -2952,6 +2952,89 @@ __global__ void __launch_bounds__(TF3_T) k_tfold_a(int D, int64_t c0, int Btot, 
     }
 }
 
+// k_tfold_a for fp32 rows with 16-byte alignment: 128 threads per CTA, 4
+// adjacent columns per thread (float4 loads, 16 rows in flight = 256 B per
+// thread), same pieces, same per-column row order, same P / PF / cd_rows.
+constexpr int TF4_T = 128;
+__global__ void __launch_bounds__(TF4_T, 4) k_tfold_a4(int D, int64_t c0, int Btot, const int32_t *__restrict__ dirty,
+                                                   const int32_t *__restrict__ pend_list,
+                                                   const int32_t *__restrict__ pend_seg,
+                                                   const char *const *__restrict__ frow,
+                                                   const float *__restrict__ fnorm,
+                                                   const int32_t *__restrict__ s_foldpos, double *__restrict__ P,
+                                                   double *__restrict__ PF, const char **__restrict__ cd_rows) {
+    pdl_enter();
+    __shared__ const float *s_row[TF3_R];
+    __shared__ float s_fn[TF3_R];
+    __shared__ int s_start[TF3_R], s_p[TF3_R], s_seg[TF3_R];
+    const int tid = threadIdx.x, x = blockIdx.x, c = blockIdx.y;
+    const int cs = c * TF3_R, nr = min(TF3_R, Btot - cs);
+    if (nr <= 0) return;
+    if (tid < nr) {
+        const int j = cs + tid;
+        const int p = pend_list[j], sg = pend_seg[j];
+        const int sp = tid > 0 ? pend_seg[j - 1] : -1;
+        s_row[tid] = (const float *)frow[c0 + p];
+        s_fn[tid] = fnorm[c0 + p];
+        s_start[tid] = (tid == 0 || sp != sg) ? 1 : 0;
+        s_p[tid] = p;
+        s_seg[tid] = sg;
+    }
+    __syncthreads();
+    const int col = x * (4 * TF4_T) + 4 * tid;
+    if (col < D) {
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        int ps = 0;
+        auto flush = [&](int at) {
+            double2 *dst = (double2 *)(P + (int64_t)(cs + at) * D + col);
+            dst[0] = make_double2(acc[0], acc[1]);
+            dst[1] = make_double2(acc[2], acc[3]);
+        };
+        for (int r0 = 0; r0 < nr; r0 += 16) {
+            float4 v[16];
+#pragma unroll
+            for (int u = 0; u < 16; u++)
+                v[u] = r0 + u < nr ? __ldg((const float4 *)(s_row[r0 + u] + col)) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int u = 0; u < 16; u++) {
+                const int r = r0 + u;
+                if (r < nr) {
+                    if (s_start[r]) {
+                        if (r > 0) flush(ps);
+                        acc[0] = (double)v[u].x;
+                        acc[1] = (double)v[u].y;
+                        acc[2] = (double)v[u].z;
+                        acc[3] = (double)v[u].w;
+                        ps = r;
+                    } else {
+                        acc[0] = dadd(acc[0], (double)v[u].x);
+                        acc[1] = dadd(acc[1], (double)v[u].y);
+                        acc[2] = dadd(acc[2], (double)v[u].z);
+                        acc[3] = dadd(acc[3], (double)v[u].w);
+                    }
+                }
+            }
+        }
+        flush(ps);
+    }
+    if (x == 0) {
+        if (tid == 0) {  // the pieces' fp32-norm sums
+            double f = 0.0;
+            int ps = 0;
+            for (int r = 0; r < nr; r++) {
+                if (s_start[r] && r > 0) {
+                    PF[cs + ps] = f;
+                    f = 0.0;
+                    ps = r;
+                }
+                f += (double)s_fn[r];
+            }
+            PF[cs + ps] = f;
+        }
+        if (tid < nr) cd_rows[cs + tid] = s_p[tid] >= s_foldpos[dirty[s_seg[tid]]] ? (const char *)s_row[tid] : nullptr;
+    }
+}
+
 __global__ void __launch_bounds__(TF3_T) k_tfold_b(
     int D, const int64_t *__restrict__ ctr, const int32_t *__restrict__ dirty, const int32_t *__restrict__ dirty_off,
     const int32_t *__restrict__ s_nfeat, const int32_t *__restrict__ s_foldpos, const int32_t *__restrict__ s_seedpos,
@@ -3847,9 +3930,15 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
                            s->tf_bcnt.p, s->cd_nd.p + buf, meta, ldm, coff, crows);
             } else {
                 const unsigned gx3 = (unsigned)cdiv(D, TF3_T);
-                launch_pdl(k_tfold_a<T>, dim3(gx3, (unsigned)cdiv(B, TF3_R)), dim3(TF3_T), 0, st, D, c0, (int)B,
-                           s->dirty.p, s->pend_list.p, s->pend_seg.p, s->frow.p, s->fnorm.p, s->s_foldpos.p,
-                           s->tf_P.p, s->tf_PF.p, crows);
+                static const bool tf4_off = getenv("FOCUS_B200_TF4") && atoi(getenv("FOCUS_B200_TF4")) == 0;
+                if (sizeof(T) == 4 && s->rows_aligned16 && D % 4 == 0 && !tf4_off)
+                    launch_pdl(k_tfold_a4, dim3(gx3, (unsigned)cdiv(B, TF3_R)), dim3(TF4_T), 0, st, D, c0, (int)B,
+                               s->dirty.p, s->pend_list.p, s->pend_seg.p, s->frow.p, s->fnorm.p, s->s_foldpos.p,
+                               s->tf_P.p, s->tf_PF.p, crows);
+                else
+                    launch_pdl(k_tfold_a<T>, dim3(gx3, (unsigned)cdiv(B, TF3_R)), dim3(TF3_T), 0, st, D, c0, (int)B,
+                               s->dirty.p, s->pend_list.p, s->pend_seg.p, s->frow.p, s->fnorm.p, s->s_foldpos.p,
+                               s->tf_P.p, s->tf_PF.p, crows);
                 FX_LAUNCHED();
                 launch_pdl(k_tfold_b, dim3(gx3, (unsigned)std::min<int64_t>(2 * (int64_t)B + 3, std::max<int64_t>(64, 1184 / gx3))), dim3(TF3_T), 0, st, D, s->ctr.p, s->dirty.p,
                            s->dirty_off.p, s->s_nfeat.p, s->s_foldpos.p, s->s_seedpos.p, s->s_evicted.p, s->s_cid.p,
