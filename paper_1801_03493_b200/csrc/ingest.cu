@@ -3533,6 +3533,8 @@ __global__ void k_batch_rows(int nb, const int64_t *__restrict__ cfirst, const i
 template <typename T>
 void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
     cudaStream_t st = s->st;
+    // batches are capped at 1/age_div of the objects seen so far (young clusters stay decidable)
+    static const int64_t age_div = getenv("FOCUS_B200_AGE_DIV") ? std::max(1, atoi(getenv("FOCUS_B200_AGE_DIV"))) : 4;
     // Several engines ingesting on one device: programmatic dependent launch
     // parks each dependent grid's CTAs on SMs before its primary finishes, and
     // with many engines those parked CTAs starve other engines' large-shared-
@@ -3565,7 +3567,7 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
     std::vector<int64_t> bfirst, blast, brows;
     if (tma) {
         for (int64_t c0 = c_begin, B = 0; c0 < c_end; c0 += B) {
-            const int64_t cap = std::max<int64_t>(64, (std::max<int64_t>(c0, 0) / 4 / 64) * 64);
+            const int64_t cap = std::max<int64_t>(64, (std::max<int64_t>(c0, 0) / age_div / 64) * 64);
             B = std::min<int64_t>(std::min<int64_t>(s->B, cap), c_end - c0);
             bfirst.push_back(c0);
             blast.push_back(c0 + B - 1);
@@ -3608,7 +3610,7 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
         // the drift bound grows like (batch size / objects so far): keep batches
         // at <= 1/4 of the stream's age so young clusters stay decidable by bounds
         const int64_t age = std::max<int64_t>(c0, 0);
-        const int64_t cap = std::max<int64_t>(64, (age / 4 / 64) * 64);
+        const int64_t cap = std::max<int64_t>(64, (age / age_div / 64) * 64);
         B = (int)std::min<int64_t>(std::min<int64_t>(s->B, cap), c_end - c0);
         s->t_ms[6] += 1.0;
         // 1. snapshot screen
@@ -3931,6 +3933,7 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
             } else {
                 const unsigned gx3 = (unsigned)cdiv(D, TF3_T);
                 static const bool tf4_off = getenv("FOCUS_B200_TF4") && atoi(getenv("FOCUS_B200_TF4")) == 0;
+                static const int tfb_gy = getenv("FOCUS_B200_TFB_GY") ? atoi(getenv("FOCUS_B200_TFB_GY")) : 0;
                 if (sizeof(T) == 4 && s->rows_aligned16 && D % 4 == 0 && !tf4_off)
                     launch_pdl(k_tfold_a4, dim3(gx3, (unsigned)cdiv(B, TF3_R)), dim3(TF4_T), 0, st, D, c0, (int)B,
                                s->dirty.p, s->pend_list.p, s->pend_seg.p, s->frow.p, s->fnorm.p, s->s_foldpos.p,
@@ -3940,7 +3943,7 @@ void run_batches(fx_stream *s, int64_t c_begin, int64_t c_end) {
                                s->dirty.p, s->pend_list.p, s->pend_seg.p, s->frow.p, s->fnorm.p, s->s_foldpos.p,
                                s->tf_P.p, s->tf_PF.p, crows);
                 FX_LAUNCHED();
-                launch_pdl(k_tfold_b, dim3(gx3, (unsigned)std::min<int64_t>(2 * (int64_t)B + 3, std::max<int64_t>(64, 1184 / gx3))), dim3(TF3_T), 0, st, D, s->ctr.p, s->dirty.p,
+                launch_pdl(k_tfold_b, dim3(gx3, (unsigned)std::min<int64_t>(2 * (int64_t)B + 3, tfb_gy > 0 ? tfb_gy : std::max<int64_t>(64, 1184 / gx3))), dim3(TF3_T), 0, st, D, s->ctr.p, s->dirty.p,
                            s->dirty_off.p, s->s_nfeat.p, s->s_foldpos.p, s->s_seedpos.p, s->s_evicted.p, s->s_cid.p,
                            s->s_size.p, s->tf_P.p, s->tf_PF.p, s->S_tree.p, s->C32.p, s->s_cn2.p, s->s_abs.p,
                            s->s_sdev.p, s->tf_cn2.p, s->tf_cnt.p, s->cd_nd.p + buf, meta, ldm, coff);
