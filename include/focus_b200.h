@@ -173,6 +173,13 @@ enum { FX_FEATS_COMPACT = 1 };
 int fx_ingest(fx_stream *s, int64_t n, const int64_t *object_ids, const int64_t *frame_ids,
               const double *sigs, const void *feats, const int32_t *true_class,
               const int32_t *topk, int32_t flags);
+/* fx_ingest with FX_FEATS_COMPACT host rows whose count the caller knows
+ * (n_feat_rows = classified objects): the feature rows start crossing PCIe
+ * immediately, in chunks, while pixel differencing places the object chunks
+ * (the e2e path: nothing waits for K0 before the big copy starts).
+ * FX_E_USAGE if n_feat_rows differs from the classified objects K0 finds. */
+int fx_ingest_rows(fx_stream *s, int64_t n, const int64_t *object_ids, const int64_t *frame_ids, const double *sigs,
+                   const void *feats, int64_t n_feat_rows, const int32_t *true_class, const int32_t *topk);
 /* Same with device pointers (inputs already resident in HBM). */
 int fx_ingest_device(fx_stream *s, int64_t n, const int64_t *object_ids, const int64_t *frame_ids,
                      const double *sigs, const void *feats, const int32_t *true_class,

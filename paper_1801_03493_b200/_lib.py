@@ -82,6 +82,7 @@ _SIGS = {
                                     c_u8p]),
     "fx_stream_dup_flags": (ctypes.c_int, [vp, ctypes.c_int64, c_i64p, c_f64p, c_u8p]),
     "fx_ingest": (ctypes.c_int, [vp, ctypes.c_int64, c_i64p, c_i64p, c_f64p, vp, c_i32p, c_i32p, ctypes.c_int32]),
+    "fx_ingest_rows": (ctypes.c_int, [vp, ctypes.c_int64, c_i64p, c_i64p, c_f64p, vp, ctypes.c_int64, c_i32p, c_i32p]),
     "fx_ingest_device": (ctypes.c_int, [vp, ctypes.c_int64, vp, vp, vp, vp, vp, vp, ctypes.c_int32]),
     "fx_finalize": (ctypes.c_int, [vp, ctypes.POINTER(vp), ctypes.POINTER(IngestReportC)]),
     "fx_stream_object_results": (ctypes.c_int, [vp, c_i32p, c_u8p, c_i32p]),

@@ -765,7 +765,7 @@ static void ingest_chunk(fx_stream *s, int64_t n, const int64_t *d_oid, const in
 
 static int ingest_common(fx_stream *s, int64_t n, const int64_t *object_ids, const int64_t *frame_ids,
                          const double *sigs, const void *feats, const int32_t *true_class, const int32_t *topk,
-                         int32_t flags, bool device) {
+                         int32_t flags, bool device, int64_t n_rows = -1) {
     FX_GUARD({
         if (!s) throw Error{FX_E_USAGE, "null stream"};
         if (s->finalized) throw Error{FX_E_USAGE, "stream already finalized"};
@@ -791,7 +791,11 @@ static int ingest_common(fx_stream *s, int64_t n, const int64_t *object_ids, con
             // differencing) need the duplicate flags first to place the
             // chunk boundaries in the row array: the small per-object arrays
             // go up first and K0 runs on them.
-            const int64_t CH = std::max<int64_t>(4096, ((int64_t)1 << 30) / std::max<int64_t>(1, (int64_t)D * s->esize));
+            // chunk of CH objects (~FOCUS_B200_H2D_MB MB of feature rows, default 256):
+            // the GPU is far ahead of PCIe, so what is left after the last
+            // copy lands (that chunk's ingest + finalize) is the e2e tail
+            static const int64_t ch_mb = getenv("FOCUS_B200_H2D_MB") ? std::max(16, atoi(getenv("FOCUS_B200_H2D_MB"))) : 256;
+            const int64_t CH = std::max<int64_t>(4096, (ch_mb << 20) / std::max<int64_t>(1, (int64_t)D * s->esize));
             const int nch = (int)cdiv(n, CH);
             DevBuf<int64_t> o, f;
             DevBuf<double> g;
@@ -804,10 +808,51 @@ static int ingest_common(fx_stream *s, int64_t n, const int64_t *object_ids, con
             if (true_class) tc.reserve(n);
             if (topk) tk.reserve((size_t)n * K);
             std::vector<int64_t> row0(nch + 1, 0);  // first feature row of each chunk
+            // the row count is known (fx_ingest_rows): the feature rows start
+            // crossing PCIe at once, in row chunks, while the per-object arrays
+            // go up and K0 places the object chunks' boundaries
+            const bool early = compact && n_rows >= 0 && !s->has_noise;
+            const size_t rbe = (size_t)D * s->esize;
+            DevBuf<char> *fbe = nullptr;
+            cudaStream_t cste = nullptr;
+            std::vector<cudaEvent_t> evr;
+            const int64_t nrch = early ? cdiv(std::max<int64_t>(n_rows, 1), CH) : 0;
+            struct EarlyGuard {
+                cudaStream_t *cs;
+                std::vector<cudaEvent_t> *ev;
+                ~EarlyGuard() {
+                    if (*cs) cudaStreamSynchronize(*cs);
+                    for (auto e : *ev)
+                        if (e) cudaEventDestroy(e);
+                    if (*cs) cudaStreamDestroy(*cs);
+                }
+            } early_guard_{&cste, &evr};
+            if (early) {
+                fbe = new DevBuf<char>();
+                s->owned_feats.push_back(fbe);
+                fbe->reserve((size_t)std::max<int64_t>(1, n_rows) * rbe);
+                if (true_class) h2d(tc.p, true_class, n, st);
+                if (topk) h2d(tk.p, topk, n * K, st);
+            }
             if (compact) {
                 h2d(o.p, object_ids, n, st);
                 h2d(f.p, frame_ids, n, st);
                 h2d(g.p, sigs, n * S, st);
+                if (early) {  // the feature rows queue behind the small per-object copies
+                    FX_CUDA(cudaStreamCreateWithFlags(&cste, cudaStreamNonBlocking));
+                    evr.assign((size_t)nrch + 1, nullptr);
+                    FX_CUDA(cudaEventCreateWithFlags(&evr[nrch], cudaEventDisableTiming));
+                    FX_CUDA(cudaEventRecord(evr[nrch], st));  // allocation and small copies first
+                    FX_CUDA(cudaStreamWaitEvent(cste, evr[nrch], 0));
+                    for (int64_t j = 0; j < nrch; j++) {
+                        const int64_t r0 = j * CH, nr = std::min<int64_t>(CH, n_rows - r0);
+                        if (nr > 0)
+                            FX_CUDA(cudaMemcpyAsync(fbe->p + (size_t)r0 * rbe, (const char *)feats + (size_t)r0 * rbe,
+                                                    (size_t)nr * rbe, cudaMemcpyHostToDevice, cste));
+                        FX_CUDA(cudaEventCreateWithFlags(&evr[j], cudaEventDisableTiming));
+                        FX_CUDA(cudaEventRecord(evr[j], cste));
+                    }
+                }
                 DevBuf<uint8_t> dup;
                 dup.reserve(n);
                 launch_dup_flags(s, n, f.p, g.p, dup.p);
@@ -830,6 +875,20 @@ static int ingest_common(fx_stream *s, int64_t n, const int64_t *object_ids, con
                 }
             } else {
                 for (int c = 0; c < nch; c++) row0[c + 1] = std::min<int64_t>(n, (int64_t)(c + 1) * CH);
+            }
+            if (early) {
+                if (row0[nch] != n_rows)
+                    throw Error{FX_E_USAGE, "feature rows (" + std::to_string(n_rows) + ") != classified objects (" +
+                                                std::to_string(row0[nch]) + ")"};
+                for (int c = 0; c < nch; c++) {
+                    const int64_t a = c * CH, m = std::min<int64_t>(CH, n - a);
+                    if (row0[c + 1] > row0[c])
+                        FX_CUDA(cudaStreamWaitEvent(st, evr[(size_t)((row0[c + 1] - 1) / CH)], 0));
+                    ingest_chunk(s, m, o.p + a, f.p + a, g.p + a * S, fbe->p + (size_t)row0[c] * rbe,
+                                 true_class ? tc.p + a : nullptr, topk ? tk.p + a * K : nullptr, 1);
+                }
+                FX_CUDA(cudaStreamSynchronize(st));
+                return FX_OK;
             }
             // feature rows stay resident until finalize (the reference retains
             // member features until seal, clustering.py:71-83)
@@ -896,6 +955,16 @@ static int ingest_common(fx_stream *s, int64_t n, const int64_t *object_ids, con
 int fx_ingest(fx_stream *s, int64_t n, const int64_t *object_ids, const int64_t *frame_ids, const double *sigs,
               const void *feats, const int32_t *true_class, const int32_t *topk, int32_t flags) {
     return ingest_common(s, n, object_ids, frame_ids, sigs, feats, true_class, topk, flags, false);
+}
+
+int fx_ingest_rows(fx_stream *s, int64_t n, const int64_t *object_ids, const int64_t *frame_ids, const double *sigs,
+                   const void *feats, int64_t n_feat_rows, const int32_t *true_class, const int32_t *topk) {
+    if (n_feat_rows < 0) {
+        set_error("fx_ingest_rows: negative row count");
+        return FX_E_USAGE;
+    }
+    return ingest_common(s, n, object_ids, frame_ids, sigs, feats, true_class, topk, FX_FEATS_COMPACT, false,
+                         n_feat_rows);
 }
 
 int fx_ingest_device(fx_stream *s, int64_t n, const int64_t *object_ids, const int64_t *frame_ids, const double *sigs,

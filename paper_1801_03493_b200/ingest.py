@@ -95,6 +95,7 @@ class Stream:
         raw feature rows fx_ingest receives, computed on the device."""
         it = _lib.FX_F32 if np.dtype(in_dtype) == np.float32 else _lib.FX_F64
         _lib.check(self.L.fx_stream_set_feature_noise(self.handle, float(sigma), seed & ((1 << 64) - 1), it))
+        self._noise = sigma != 0.0
 
     def dup_flags(self, fids: np.ndarray, sigs: np.ndarray) -> np.ndarray:
         n = fids.size
@@ -105,6 +106,13 @@ class Stream:
 
     def ingest(self, oids, fids, sigs, feats, true_class=None, topk=None, compact=False):
         n = oids.size
+        if compact and not getattr(self, "_noise", False):
+            # the row count is known: the feature upload starts before K0 (fx_ingest_rows)
+            _lib.check(self.L.fx_ingest_rows(self.handle, n, _lib.p64(oids), _lib.p64(fids), _lib.pf64(sigs),
+                                             _lib.pv(feats), int(feats.shape[0]) if feats.ndim == 2 else 0,
+                                             _lib.p32(true_class) if true_class is not None else None,
+                                             _lib.p32(topk) if topk is not None else None))
+            return
         _lib.check(self.L.fx_ingest(self.handle, n, _lib.p64(oids), _lib.p64(fids), _lib.pf64(sigs), _lib.pv(feats),
                                     _lib.p32(true_class) if true_class is not None else None,
                                     _lib.p32(topk) if topk is not None else None,

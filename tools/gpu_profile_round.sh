@@ -7,7 +7,7 @@ B="python bench.py --steps 1 --warmup 0 --objects 200000 --no-cpu --no-check --e
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 4000 --csv \
   --log-file gpurun_out/launches_$T.csv $B --no-fc > gpurun_out/launches_$T.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on \
-  -k 'regex:k_screen_tc|k_rowpass|k_rfast|k_tfold_a|k_tfold_b|k_fold|k_snap_pack' --launch-skip 420 --launch-count 12 \
+  -k 'regex:k_screen_tc|k_rowpass_lean|k_rfast|k_tfold_a4|k_tfold_b|k_fold|k_snap_pack|k_seal' --launch-skip 300 --launch-count 14 \
   -o gpurun_out/full_$T -f $B --no-fc > gpurun_out/full_$T.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k 'regex:k_fc_tc|k_fc_merge|k_extract' --launch-count 3 \
   -o gpurun_out/fc_$T -f $B > gpurun_out/fc_$T.log 2>&1
