@@ -45,7 +45,18 @@ struct FcTile {  // per (object, class tile) result of k_fc_tc
 // box per operand and stage (A: 128 rows of tmA from row arow0 + ta, B: 256
 // class rows of tmW), issued by one producer thread; one MMA thread; per-
 // stage full barriers count bytes, empty barriers take the MMA commit.
-template <bool TMA>
+//
+// CL > 1 (TMA only): the CTAs of a (1, CL) cluster share one class tile and
+// take CL consecutive object tiles; each loads 256/CL rows of the W box and
+// multicasts them to every CTA of the cluster, so a CTA pulls 1 + 2/CL MB
+// from L2 per (128 objects x 256 classes x 2048) tile instead of 3 MB.  A
+// stage is free again when all CL MMAs consumed it (each MMA commit arrives
+// on every CTA's empty barrier, count CL).
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+template <bool TMA, int CL>
 __global__ void __launch_bounds__(FC_THREADS, 1) k_fc_tc(int n, int64_t a0, const char *const *__restrict__ frow,
                                                         const float *__restrict__ fnorm, int D, int V,
                                                         const float *__restrict__ W, const float *__restrict__ wnorm,
@@ -69,11 +80,16 @@ __global__ void __launch_bounds__(FC_THREADS, 1) k_fc_tc(int n, int64_t a0, cons
     }
     if (tid == 0) {
         for (int s = 0; s < FC_STAGES; s++) {
-            mbar_init(&bar_stage[s], 1);
+            mbar_init(&bar_stage[s], CL);
             mbar_init(&bar_full[s], 1);
         }
         mbar_init(&bar_done, 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+    }
+    uint32_t crank = 0;
+    if (CL > 1) {
+        asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(crank));
+        cluster_sync_all();  // peers' barriers initialised before any multicast lands
     }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base)),
@@ -102,11 +118,20 @@ __global__ void __launch_bounds__(FC_THREADS, 1) k_fc_tc(int n, int64_t a0, cons
                     "%3}], [%4];\n" ::"r"(st),
                     "l"(&tmA), "r"(it * TC_KT), "r"(arow0 + ta), "r"(fb)
                     : "memory");
-                asm volatile(
-                    "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
-                    "%3}], [%4];\n" ::"r"(st + FC_A_BYTES),
-                    "l"(&tmW), "r"(it * TC_KT), "r"(tv), "r"(fb)
-                    : "memory");
+                if (CL == 1) {
+                    asm volatile(
+                        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, "
+                        "{%2, %3}], [%4];\n" ::"r"(st + FC_A_BYTES),
+                        "l"(&tmW), "r"(it * TC_KT), "r"(tv), "r"(fb)
+                        : "memory");
+                } else {
+                    constexpr int WR = FC_N / CL;  // W rows this CTA fetches for the whole cluster
+                    asm volatile(
+                        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::"
+                        "cluster [%0], [%1, {%2, %3}], [%4], %5;\n" ::"r"(st + FC_A_BYTES + crank * (WR * TC_KT * 4)),
+                        "l"(&tmW), "r"(it * TC_KT), "r"(tv + (int)crank * WR), "r"(fb), "h"((uint16_t)((1u << CL) - 1u))
+                        : "memory");
+                }
             }
         } else if (warp == 1 && lane == 0) {  // MMA issue
             for (int it = 0; it < nk; it++) {
@@ -124,8 +149,14 @@ __global__ void __launch_bounds__(FC_THREADS, 1) k_fc_tc(int n, int64_t a0, cons
                         "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
                         "l"(da), "l"(db), "r"(idesc), "r"(acc));
                 }
-                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                    smem_u32(&bar_stage[s])));
+                if (CL == 1)
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                        smem_u32(&bar_stage[s])));
+                else
+                    asm volatile(
+                        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], "
+                        "%1;\n" ::"r"(smem_u32(&bar_stage[s])),
+                        "h"((uint16_t)((1u << CL) - 1u)));
             }
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
                 smem_u32(&bar_done)));
@@ -184,6 +215,7 @@ __global__ void __launch_bounds__(FC_THREADS, 1) k_fc_tc(int n, int64_t a0, cons
     // its list to the lower one through shared memory (its class ids are all
     // larger, so inserting after keeps the tie order).  The tail (largest
     // upper bound of a dropped class) uses the tile's largest ||w||.
+    if (!(dbg & 4)) {  // dbg & 4: main loop only (timing experiments)
     const int quad = warp & 3, half = warp >> 2;
     const int a = ta + quad * 32 + lane;
     const float fn = a < n ? fnorm[a0 + a] : 0.f;
@@ -220,41 +252,48 @@ __global__ void __launch_bounds__(FC_THREADS, 1) k_fc_tc(int n, int64_t a0, cons
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
     };
-    auto insert = [&](float x, int xi) {  // strict > keeps the earlier (smaller) id first
-        if (x > kv[FC_KC - 1]) {
-            dropped = fmaxf(dropped, kv[FC_KC - 1]);
+    // Sorted insert without branches (strict >: ties keep the earlier, smaller
+    // id first): slot q takes x if x beats it and not its predecessor, its
+    // predecessor if x beats both, else stays.  All slots update in
+    // parallel, no divergence between the lanes (objects) of a warp.
+    auto insert = [&](float x, int xi) {
+        bool c[FC_KC];
 #pragma unroll
-            for (int q = 0; q < FC_KC; q++) {
-                if (x > kv[q]) {
-                    const float tvv = kv[q];
-                    const int tii = ki[q];
-                    kv[q] = x;
-                    ki[q] = xi;
-                    x = tvv;
-                    xi = tii;
-                }
-            }
-        } else {
-            dropped = fmaxf(dropped, x);
+        for (int q = 0; q < FC_KC; q++) c[q] = x > kv[q];
+        dropped = fmaxf(dropped, c[FC_KC - 1] ? kv[FC_KC - 1] : x);
+#pragma unroll
+        for (int q = FC_KC - 1; q > 0; q--) {
+            const float nv = c[q - 1] ? kv[q - 1] : x;
+            const int ni = c[q - 1] ? ki[q - 1] : xi;
+            kv[q] = c[q] ? nv : kv[q];
+            ki[q] = c[q] ? ni : ki[q];
         }
+        kv[0] = c[0] ? x : kv[0];
+        ki[0] = c[0] ? xi : ki[0];
     };
     constexpr int HC = FC_N / 2;
-    float m = -FLT_MAX, ssum = 0.f;  // online logsumexp partial (one TMEM pass)
+    float m = -FLT_MAX, ssum = 0.f;  // logsumexp partial, updated per 32-class chunk (one TMEM pass)
     for (int c0 = half * HC; c0 < (half + 1) * HC; c0 += 32) {
         uint32_t v[32];
         tmem_row(c0, v);
-#pragma unroll 4
+        float x[32];
+        float cm = -FLT_MAX;
+#pragma unroll
         for (int j = 0; j < 32; j++) {
             const int cls = tv + c0 + j;
-            if (a >= n || cls >= V) break;
-            const float x = __uint_as_float(v[j]) + (bias ? bias[cls] : 0.f);
-            if (x > m) {
-                ssum = ssum * __expf(m - x) + 1.f;
-                m = x;
-            } else {
-                ssum += __expf(x - m);
-            }
-            insert(x, cls);
+            x[j] = (a < n && cls < V) ? __uint_as_float(v[j]) + (bias ? bias[cls] : 0.f) : -FLT_MAX;
+            cm = fmaxf(cm, x[j]);
+        }
+        if (cm != -FLT_MAX) {  // else past the last class (or object); no divergent exit before tcgen05.ld
+            const float nm = fmaxf(m, cm);
+            float cs = 0.f;
+#pragma unroll
+            for (int j = 0; j < 32; j++) cs += x[j] == -FLT_MAX ? 0.f : __expf(x[j] - nm);
+            ssum = ssum * __expf(m - nm) + cs;
+            m = nm;
+#pragma unroll
+            for (int j = 0; j < 32; j++)
+                if (x[j] != -FLT_MAX) insert(x[j], tv + c0 + j);
         }
     }
     // upper half -> lower half (pipeline shared memory is idle now)
@@ -301,8 +340,10 @@ __global__ void __launch_bounds__(FC_THREADS, 1) k_fc_tc(int n, int64_t a0, cons
             o->lse_s = ssum;
         }
     }
+    }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
     __syncthreads();
+    if (CL > 1) cluster_sync_all();  // no peer still multicasts into this CTA's stages or barriers
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(FC_N));
 }
 
@@ -324,15 +365,46 @@ __device__ __forceinline__ double fc_logit64(const float *f, const float *w, int
     return acc + b;
 }
 
+// Same sums as fc_logit64, the feature row held in registers (fr[i] = f4[lane
+// + 32 i], i < nf = D / 128 <= 16): per candidate only the W row is loaded,
+// 8 float4 per lane in flight.
+__device__ __forceinline__ double fc_logit64_reg(const float4 (&fr)[16], int nf, const float *w, double b) {
+    const float4 *w4 = (const float4 *)w;
+    const int lane = threadIdx.x & 31;
+    double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+    for (int h = 0; h < 16; h += 8) {
+        if (h >= nf) break;
+        float4 y[8];
+#pragma unroll
+        for (int i = 0; i < 8; i++)
+            if (h + i < nf) y[i] = __ldg(w4 + lane + 32 * (h + i));
+#pragma unroll
+        for (int i = 0; i < 8; i++)
+            if (h + i < nf) {
+                const float4 x = fr[h + i];
+                a0 = fma((double)x.x, (double)y[i].x, a0);
+                a1 = fma((double)x.y, (double)y[i].y, a1);
+                a0 = fma((double)x.z, (double)y[i].z, a0);
+                a1 = fma((double)x.w, (double)y[i].w, a1);
+            }
+    }
+    double acc = a0 + a1;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    return acc + b;
+}
+
 constexpr int FC_MAXC = 64;  // candidates re-scored per object before the all-class fallback
 
-__global__ void __launch_bounds__(256) k_fc_merge(int n, int64_t a0, const char *const *__restrict__ frow,
+__global__ void __launch_bounds__(256, 2) k_fc_merge(int n, int64_t a0, const char *const *__restrict__ frow,
                                                  const int64_t *__restrict__ cls_obj, const float *__restrict__ fnorm,
                                                  int D, int V, int K, const float *__restrict__ W,
                                                  const float *__restrict__ wnorm, const float *__restrict__ bias,
                                                  float gamma, int ntile, const FcTile *__restrict__ tiles,
                                                  int32_t *__restrict__ topk, float *__restrict__ conf,
-                                                 uint8_t *__restrict__ flag, unsigned long long *__restrict__ nflag) {
+                                                 uint8_t *__restrict__ flag, unsigned long long *__restrict__ nflag,
+                                                 int merge_reg) {
     __shared__ int s_idx[8][FC_MAXC];
     __shared__ float s_lb[8][FC_MAXC], s_ub[8][FC_MAXC];
     __shared__ unsigned char s_need[8][FC_MAXC];
@@ -495,11 +567,20 @@ __global__ void __launch_bounds__(256) k_fc_merge(int n, int64_t a0, const char 
     }
     __syncwarp();
     const int nscore = all ? V : ncand;
+    const bool reg = merge_reg && (D & 127) == 0 && D <= 2048;  // feature row cached in registers
+    const int nf = D >> 7;
+    float4 fr[16];
+    if (reg) {
+#pragma unroll
+        for (int i = 0; i < 16; i++)
+            if (i < nf) fr[i] = __ldg((const float4 *)f + lane + 32 * i);
+    }
     for (int c = 0; c < nscore; c++) {
         const int cls = all ? c : s_idx[wib][c];
         double l;
         if (all || s_need[wib][c])
-            l = fc_logit64(f, W + (int64_t)cls * D, D, bias ? (double)bias[cls] : 0.0);
+            l = reg ? fc_logit64_reg(fr, nf, W + (int64_t)cls * D, bias ? (double)bias[cls] : 0.0)
+                    : fc_logit64(f, W + (int64_t)cls * D, D, bias ? (double)bias[cls] : 0.0);
         else
             l = 0.5 * ((double)s_lb[wib][c] + (double)s_ub[wib][c]);  // disjoint interval: its order is certain
         if (lane == 0) {  // lane 0's value decides (its reduction order is fixed)
@@ -568,14 +649,20 @@ void launch_fc_head(int64_t n, int64_t c0, const char *const *frow, const int64_
     bool &attr = attr_set[dev_slot()];
     const size_t smem = (size_t)FC_STAGES * (FC_A_BYTES + FC_B_BYTES) + 1024;
     if (!attr) {
-        FX_CUDA(cudaFuncSetAttribute(k_fc_tc<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        FX_CUDA(cudaFuncSetAttribute(k_fc_tc<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        for (auto k : {k_fc_tc<false, 1>, k_fc_tc<true, 1>, k_fc_tc<true, 2>, k_fc_tc<true, 4>})
+            FX_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
     static const bool tma_off = getenv("FOCUS_B200_TCLOAD") && std::string(getenv("FOCUS_B200_TCLOAD")) == "cp";
+    // W multicast cluster size (FOCUS_B200_FC_CL: 1, 2 or 4; default 1: 4 measured
+    // 17% slower -- the head is not bound by L2 -> SM operand traffic)
+    static const int cl_env = getenv("FOCUS_B200_FC_CL") ? atoi(getenv("FOCUS_B200_FC_CL")) : 1;
+    // float64 re-score with the feature row in registers (FOCUS_B200_FC_MERGE_REG=0: re-read per candidate)
+    static const int merge_reg = getenv("FOCUS_B200_FC_MERGE_REG") ? atoi(getenv("FOCUS_B200_FC_MERGE_REG")) : 1;
+    const int CL = (cl_env == 2 || cl_env == 4) ? cl_env : 1;
     CUtensorMap tmA = {}, tmW = {};
     const bool tma = Xdense && !tma_off && D % 4 == 0 && make_rows_map(&tmA, Xdense, n, D, (int64_t)D * 4, FC_M) &&
-                     make_rows_map(&tmW, W, V, D, (int64_t)D * 4, FC_N);
+                     make_rows_map(&tmW, W, V, D, (int64_t)D * 4, FC_N / CL);
     const int ntile = (int)cdiv(V, FC_N);
     const float gamma = (float)((1.953125e-03 + (double)D * 2.384185791015625e-07) * 1.01);
     DevBuf<FcTile> tiles;
@@ -583,13 +670,33 @@ void launch_fc_head(int64_t n, int64_t c0, const char *const *frow, const int64_
     tiles.reserve((size_t)std::min<int64_t>(n, CH) * ntile);
     for (int64_t b = 0; b < n; b += CH) {
         const int64_t m = std::min<int64_t>(CH, n - b);
-        dim3 grid((unsigned)ntile, (unsigned)cdiv(m, FC_M));
         static const int dbg = getenv("FOCUS_B200_FCDBG") ? atoi(getenv("FOCUS_B200_FCDBG")) : 0;
-        (tma ? k_fc_tc<true> : k_fc_tc<false>)<<<grid, FC_THREADS, smem, st>>>(
-            (int)m, c0 + b, frow, fnorm, D, V, W, wnorm, bias, gamma, tiles.p, dbg, tmA, tmW, (int)b);
+        if (tma && CL > 1) {
+            // object tiles padded to whole clusters (TMA zero-fills rows past the
+            // features; the padded tiles write nothing)
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3((unsigned)ntile, (unsigned)(cdiv(cdiv(m, FC_M), CL) * CL));
+            cfg.blockDim = dim3(FC_THREADS);
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = st;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = 1;
+            at[0].val.clusterDim.y = (unsigned)CL;
+            at[0].val.clusterDim.z = 1;
+            cfg.attrs = at;
+            cfg.numAttrs = 1;
+            FX_CUDA(cudaLaunchKernelEx(&cfg, CL == 2 ? k_fc_tc<true, 2> : k_fc_tc<true, 4>, (int)m, c0 + b, frow,
+                                       fnorm, D, V, W, wnorm, bias, gamma, tiles.p, dbg, tmA, tmW, (int)b));
+        } else {
+            dim3 grid((unsigned)ntile, (unsigned)cdiv(m, FC_M));
+            (tma ? k_fc_tc<true, 1> : k_fc_tc<false, 1>)<<<grid, FC_THREADS, smem, st>>>(
+                (int)m, c0 + b, frow, fnorm, D, V, W, wnorm, bias, gamma, tiles.p, dbg, tmA, tmW, (int)b);
+        }
         FX_LAUNCHED();
         k_fc_merge<<<(unsigned)cdiv(m, 8), 256, 0, st>>>((int)m, c0 + b, frow, cls_obj, fnorm, D, V, K, W, wnorm, bias,
-                                                        gamma, ntile, tiles.p, topk, conf, flag, nflag);
+                                                        gamma, ntile, tiles.p, topk, conf, flag, nflag,
+                                                        merge_reg);
         FX_LAUNCHED();
     }
 }
