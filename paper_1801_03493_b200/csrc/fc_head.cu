@@ -45,6 +45,140 @@ struct FcTile {  // per (object, class tile) result of k_fc_tc
 // box per operand and stage (A: 128 rows of tmA from row arow0 + ta, B: 256
 // class rows of tmW), issued by one producer thread; one MMA thread; per-
 // stage full barriers count bytes, empty barriers take the MMA commit.
+// Packed (logit, class) keys of the epilogue; see fc_epilogue.
+constexpr float FC_REL = 6.2e-5f;  // relative error of a kept logit: key truncation 2^-15 (x2) + fp32 2^-22
+__device__ __forceinline__ int fc_key(float x, int c) {  // c: class within the 256-class tile
+    const int b = __float_as_int(x);
+    const int o = b < 0 ? b ^ 0x7FFFFFFF : b;  // order-preserving as a signed int
+    return (o & ~255) | (255 - c);
+}
+__device__ __forceinline__ float fc_key_value(int key) {
+    const int o = key & ~255;
+    return __int_as_float(o < 0 ? o ^ 0x7FFFFFFF : o);
+}
+
+// Epilogue of one 128 x 256 accumulator (TMEM columns tmem..tmem+255): 256
+// threads, warps (quad, half): TMEM lanes 32 quad.. (object rows) and one half
+// of the 256 classes each; a thread keeps the FC_KC largest logits of its
+// half (sorted descending, ties -> smaller class id), the largest dropped
+// logit and a logsumexp partial, then the upper half hands its list to the
+// lower one through shared memory (its class ids are all larger, so
+// inserting after keeps the tie order).  The tail (largest upper bound of a
+// dropped class) uses the tile's largest ||w||.  out: this class tile's
+// FcTile of object 0 (stride ntile per object).  tmem_empty: arrived on by
+// every thread once the accumulator is read (persistent kernel).
+template <class Sync>
+__device__ __forceinline__ void fc_epilogue(uint32_t tmem, int quad, int half, int lane, int etid, int ta, int tv,
+                                            int n, int64_t a0, int V, const float *__restrict__ fnorm,
+                                            const float *__restrict__ wnorm, const float *__restrict__ bias,
+                                            float gamma, FcTile *__restrict__ out, int ntile, float *s_wmax, float *s_bias,
+                                            float *hv, int *hi, float *hx, uint64_t *tmem_empty, Sync sync) {
+    const int a = ta + quad * 32 + lane;
+    const float fn = a < n ? fnorm[a0 + a] : 0.f;
+    {
+        float wm = tv + etid < V ? wnorm[tv + etid] : 0.f;  // 256 epilogue threads, 256 classes
+        s_bias[etid] = bias && tv + etid < V ? bias[tv + etid] : 0.f;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) wm = fmaxf(wm, __shfl_xor_sync(0xffffffffu, wm, o));
+        if (lane == 0) s_wmax[etid >> 5] = wm;
+        sync();
+    }
+    float wmax = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; w++) wmax = fmaxf(wmax, s_wmax[w]);
+    // Kept logits as packed keys: the float's order-preserving int with the
+    // low 8 bits replaced by 255 - (class within the tile), so one signed
+    // compare orders by value and then by smaller class id; the dropped bits
+    // cost < 2^-15 |logit| (FC_REL covers it).  A sorted insert is then a
+    // min/max network: slot q = max(slot q, min(slot q-1, key)), every slot
+    // independent, no divergence between the lanes (objects) of a warp.
+    int kv[FC_KC];
+#pragma unroll
+    for (int j = 0; j < FC_KC; j++) kv[j] = INT_MIN;
+    int dropped = INT_MIN;
+    auto tmem_row = [&](int c0, uint32_t *v) {
+        const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)c0;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
+            "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+              "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
+    };
+    auto insert = [&](int key) {
+        dropped = max(dropped, min(kv[FC_KC - 1], key));
+#pragma unroll
+        for (int q = FC_KC - 1; q > 0; q--) kv[q] = max(kv[q], min(kv[q - 1], key));
+        kv[0] = max(kv[0], key);
+    };
+    constexpr int HC = FC_N / 2;
+    float m = -FLT_MAX, ssum = 0.f;  // logsumexp partial, updated per 32-class chunk (one TMEM pass)
+    for (int c0 = half * HC; c0 < (half + 1) * HC; c0 += 32) {
+        uint32_t v[32];
+        tmem_row(c0, v);
+        float x[32];
+        float cm = -FLT_MAX;
+#pragma unroll
+        for (int j = 0; j < 32; j++) {
+            const int cls = tv + c0 + j;
+            x[j] = (a < n && cls < V) ? __uint_as_float(v[j]) + s_bias[c0 + j] : -FLT_MAX;
+            cm = fmaxf(cm, x[j]);
+        }
+        if (cm != -FLT_MAX) {  // else past the last class (or object); no divergent exit before tcgen05.ld
+            const float nm = fmaxf(m, cm);
+            float cs = 0.f;
+#pragma unroll
+            for (int j = 0; j < 32; j++) cs += x[j] == -FLT_MAX ? 0.f : __expf(x[j] - nm);
+            ssum = ssum * __expf(m - nm) + cs;
+            m = nm;
+#pragma unroll
+            for (int j = 0; j < 32; j++)
+                if (x[j] != -FLT_MAX) insert(fc_key(x[j], c0 + j));
+        }
+    }
+    if (tmem_empty) {  // accumulator read: the MMA may overwrite it
+        asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(tmem_empty)) : "memory");
+    }
+    // upper half -> lower half through shared memory
+    const int r = quad * 32 + lane;
+    int *hk = (int *)hv;
+    sync();
+    if (half == 1) {
+#pragma unroll
+        for (int j = 0; j < FC_KC; j++) hk[r * FC_KC + j] = kv[j];
+        hx[r * 3 + 0] = __int_as_float(dropped);
+        hx[r * 3 + 1] = m;
+        hx[r * 3 + 2] = ssum;
+    }
+    sync();
+    if (half == 0) {
+#pragma unroll
+        for (int j = 0; j < FC_KC; j++) insert(hk[r * FC_KC + j]);
+        dropped = max(dropped, __float_as_int(hx[r * 3 + 0]));
+        const float m1 = hx[r * 3 + 1], s1 = hx[r * 3 + 2];
+        const float mm = fmaxf(m, m1);
+        ssum = (ssum > 0.f ? ssum * __expf(m - mm) : 0.f) + (s1 > 0.f ? s1 * __expf(m1 - mm) : 0.f);
+        const float dv = fc_key_value(dropped);
+        const float tail = dropped == INT_MIN ? -FLT_MAX : dv + gamma * fn * wmax + fabsf(dv) * FC_REL;
+        if (a < n) {
+            FcTile *o = out + (int64_t)a * ntile;
+#pragma unroll
+            for (int j = 0; j < FC_KC; j++) {
+                o->val[j] = kv[j] == INT_MIN ? -FLT_MAX : fc_key_value(kv[j]);
+                o->idx[j] = kv[j] == INT_MIN ? -1 : tv + 255 - (kv[j] & 255);
+            }
+            o->tail = tail;
+            o->lse_m = mm;
+            o->lse_s = ssum;
+        }
+    }
+    sync();  // hv / s_wmax free for the next tile
+}
+
 //
 // CL > 1 (TMA only): the CTAs of a (1, CL) cluster share one class tile and
 // take CL consecutive object tiles; each loads 256/CL rows of the W box and
@@ -216,135 +350,139 @@ __global__ void __launch_bounds__(FC_THREADS, 1) k_fc_tc(int n, int64_t a0, cons
     // larger, so inserting after keeps the tie order).  The tail (largest
     // upper bound of a dropped class) uses the tile's largest ||w||.
     if (!(dbg & 4)) {  // dbg & 4: main loop only (timing experiments)
-    const int quad = warp & 3, half = warp >> 2;
-    const int a = ta + quad * 32 + lane;
-    const float fn = a < n ? fnorm[a0 + a] : 0.f;
-    __shared__ float s_wmax[FC_THREADS / 32];
-    {
-        float wm = 0.f;
-        for (int c = tid; c < FC_N; c += FC_THREADS)
-            if (tv + c < V) wm = fmaxf(wm, wnorm[tv + c]);
-#pragma unroll
-        for (int o = 16; o; o >>= 1) wm = fmaxf(wm, __shfl_xor_sync(0xffffffffu, wm, o));
-        if (lane == 0) s_wmax[warp] = wm;
-        __syncthreads();
-    }
-    float wmax = 0.f;
-#pragma unroll
-    for (int w = 0; w < FC_THREADS / 32; w++) wmax = fmaxf(wmax, s_wmax[w]);
-    float kv[FC_KC];
-    int ki[FC_KC];
-#pragma unroll
-    for (int j = 0; j < FC_KC; j++) {
-        kv[j] = -FLT_MAX;
-        ki[j] = -1;
-    }
-    float dropped = -FLT_MAX;
-    auto tmem_row = [&](int c0, uint32_t *v) {
-        const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)c0;
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,"
-            "%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-              "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
-              "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
-              "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-            : "r"(taddr));
-        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
-    };
-    // Sorted insert without branches (strict >: ties keep the earlier, smaller
-    // id first): slot q takes x if x beats it and not its predecessor, its
-    // predecessor if x beats both, else stays.  All slots update in
-    // parallel, no divergence between the lanes (objects) of a warp.
-    auto insert = [&](float x, int xi) {
-        bool c[FC_KC];
-#pragma unroll
-        for (int q = 0; q < FC_KC; q++) c[q] = x > kv[q];
-        dropped = fmaxf(dropped, c[FC_KC - 1] ? kv[FC_KC - 1] : x);
-#pragma unroll
-        for (int q = FC_KC - 1; q > 0; q--) {
-            const float nv = c[q - 1] ? kv[q - 1] : x;
-            const int ni = c[q - 1] ? ki[q - 1] : xi;
-            kv[q] = c[q] ? nv : kv[q];
-            ki[q] = c[q] ? ni : ki[q];
-        }
-        kv[0] = c[0] ? x : kv[0];
-        ki[0] = c[0] ? xi : ki[0];
-    };
-    constexpr int HC = FC_N / 2;
-    float m = -FLT_MAX, ssum = 0.f;  // logsumexp partial, updated per 32-class chunk (one TMEM pass)
-    for (int c0 = half * HC; c0 < (half + 1) * HC; c0 += 32) {
-        uint32_t v[32];
-        tmem_row(c0, v);
-        float x[32];
-        float cm = -FLT_MAX;
-#pragma unroll
-        for (int j = 0; j < 32; j++) {
-            const int cls = tv + c0 + j;
-            x[j] = (a < n && cls < V) ? __uint_as_float(v[j]) + (bias ? bias[cls] : 0.f) : -FLT_MAX;
-            cm = fmaxf(cm, x[j]);
-        }
-        if (cm != -FLT_MAX) {  // else past the last class (or object); no divergent exit before tcgen05.ld
-            const float nm = fmaxf(m, cm);
-            float cs = 0.f;
-#pragma unroll
-            for (int j = 0; j < 32; j++) cs += x[j] == -FLT_MAX ? 0.f : __expf(x[j] - nm);
-            ssum = ssum * __expf(m - nm) + cs;
-            m = nm;
-#pragma unroll
-            for (int j = 0; j < 32; j++)
-                if (x[j] != -FLT_MAX) insert(x[j], tv + c0 + j);
-        }
-    }
-    // upper half -> lower half (pipeline shared memory is idle now)
-    float *hv = (float *)smem;                       // [128][FC_KC]
-    int *hi = (int *)(hv + FC_M * FC_KC);            // [128][FC_KC]
-    float *hx = (float *)(hi + FC_M * FC_KC);        // [128][3]: dropped, m, ssum
-    const int r = quad * 32 + lane;
-    __syncthreads();
-    if (half == 1) {
-#pragma unroll
-        for (int j = 0; j < FC_KC; j++) {
-            hv[r * FC_KC + j] = kv[j];
-            hi[r * FC_KC + j] = ki[j];
-        }
-        hx[r * 3 + 0] = dropped;
-        hx[r * 3 + 1] = m;
-        hx[r * 3 + 2] = ssum;
-    }
-    __syncthreads();
-    if (half == 0) {
-        for (int j = 0; j < FC_KC; j++) {
-            const float x = hv[r * FC_KC + j];
-            if (!(x > kv[FC_KC - 1])) {  // sorted: the rest are no larger
-                dropped = fmaxf(dropped, x);
-                break;
-            }
-            insert(x, hi[r * FC_KC + j]);
-        }
-        dropped = fmaxf(dropped, hx[r * 3 + 0]);
-        const float m1 = hx[r * 3 + 1], s1 = hx[r * 3 + 2];
-        const float mm = fmaxf(m, m1);
-        ssum = (ssum > 0.f ? ssum * __expf(m - mm) : 0.f) + (s1 > 0.f ? s1 * __expf(m1 - mm) : 0.f);
-        m = kv[0];
-        const float tail = dropped == -FLT_MAX ? -FLT_MAX : dropped + gamma * fn * wmax + fabsf(dropped) * 2.4e-7f;
-        if (a < n) {
-            FcTile *o = out + (int64_t)a * gridDim.x + blockIdx.x;
-#pragma unroll
-            for (int j = 0; j < FC_KC; j++) {
-                o->val[j] = kv[j];
-                o->idx[j] = ki[j];
-            }
-            o->tail = tail;
-            o->lse_m = m;
-            o->lse_s = ssum;
-        }
-    }
+        __shared__ float s_wmax[8], s_bias[FC_N];
+        float *hv = (float *)smem;  // the pipeline's shared memory is idle now
+        fc_epilogue(tmem, warp & 3, warp >> 2, lane, tid, ta, tv, n, a0, V, fnorm, wnorm, bias, gamma,
+                    out + blockIdx.x, gridDim.x, s_wmax, s_bias, hv, (int *)(hv + FC_M * FC_KC),
+                    (float *)(hv + 2 * FC_M * FC_KC), nullptr, [] { __syncthreads(); });
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
     __syncthreads();
     if (CL > 1) cluster_sync_all();  // no peer still multicasts into this CTA's stages or barriers
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(FC_N));
+}
+
+// Persistent K1b logits (TMA operands): one CTA per SM walks the (object
+// tile, class tile) pairs t = blockIdx.x + i gridDim.x, class tile fastest
+// (CTAs running at the same time share object rows in L2).  Warp 0 lane 0
+// streams the operands through the FC_STAGES ring, warp 1 lane 0 issues the
+// MMAs into one of two TMEM accumulators (2 x 256 columns), warps 4..11 run
+// fc_epilogue on the other: tile i's epilogue overlaps tile i+1's main loop.
+// Barriers: full/empty per stage (as k_fc_tc), acc_full[b] (MMA commit ->
+// epilogue), acc_empty[b] (256 epilogue arrivals -> MMA).
+constexpr int FCP_THREADS = 384;
+__global__ void __launch_bounds__(FCP_THREADS, 1) k_fc_tcp(int n, int64_t a0, const float *__restrict__ fnorm, int D,
+                                                          int V, const float *__restrict__ wnorm,
+                                                          const float *__restrict__ bias, float gamma,
+                                                          FcTile *__restrict__ out, int ntile, int ntiles,
+                                                          const __grid_constant__ CUtensorMap tmA,
+                                                          const __grid_constant__ CUtensorMap tmW, int arow0,
+                                                          int dbg) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    __shared__ __align__(8) uint64_t bar_empty[FC_STAGES];
+    __shared__ __align__(8) uint64_t bar_full[FC_STAGES];
+    __shared__ __align__(8) uint64_t acc_full[2];
+    __shared__ __align__(8) uint64_t acc_empty[2];
+    __shared__ float s_wmax[8], s_bias[FC_N];
+    __shared__ uint32_t tmem_base;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    constexpr int SB = FC_A_BYTES + FC_B_BYTES;
+    float *hv = (float *)(smem + FC_STAGES * SB);  // [128][FC_KC] vals, [128][FC_KC] ids, [128][3]
+    if (tid == 0) {
+        for (int s = 0; s < FC_STAGES; s++) {
+            mbar_init(&bar_empty[s], 1);
+            mbar_init(&bar_full[s], 1);
+        }
+        for (int b = 0; b < 2; b++) {
+            mbar_init(&acc_full[b], 1);
+            mbar_init(&acc_empty[b], 256);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+    }
+    if (warp == 2) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base)),
+                     "r"(2 * FC_N));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+    const uint32_t tmem = tmem_base;
+    const uint32_t sbase = smem_u32(smem);
+    const int nk = (D + TC_KT - 1) / TC_KT;
+    constexpr uint32_t idesc = idesc_tf32(FC_M, FC_N);
+    if (warp == 0 && lane == 0) {  // producer
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmA) : "memory");
+        asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmW) : "memory");
+        uint32_t g = 0;  // stage uses so far
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            const int tv = (t % ntile) * FC_N, ta = (t / ntile) * FC_M;
+            for (int it = 0; it < nk; it++, g++) {
+                const int s = g % FC_STAGES;
+                mbar_wait(&bar_empty[s], ((g / FC_STAGES) + 1) & 1);
+                const uint32_t st = sbase + s * SB, fb = smem_u32(&bar_full[s]);
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(fb), "r"(SB) : "memory");
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+                    "%3}], [%4];\n" ::"r"(st),
+                    "l"(&tmA), "r"(it * TC_KT), "r"(arow0 + ta), "r"(fb)
+                    : "memory");
+                asm volatile(
+                    "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+                    "%3}], [%4];\n" ::"r"(st + FC_A_BYTES),
+                    "l"(&tmW), "r"(it * TC_KT), "r"(tv), "r"(fb)
+                    : "memory");
+            }
+        }
+    } else if (warp == 1 && lane == 0) {  // MMA issue
+        uint32_t g = 0, i = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, i++) {
+            const uint32_t b = i & 1, acc_t = tmem + b * FC_N;
+            mbar_wait(&acc_empty[b], ((i >> 1) + 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+            for (int it = 0; it < nk; it++, g++) {
+                const int s = g % FC_STAGES;
+                mbar_wait(&bar_full[s], (g / FC_STAGES) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+                const uint32_t st = sbase + s * SB;
+#pragma unroll
+                for (int kk = 0; kk < TC_KT / 8; kk++) {
+                    const uint64_t da = umma_desc_sw128(st + kk * 32);
+                    const uint64_t db = umma_desc_sw128(st + FC_A_BYTES + kk * 32);
+                    const uint32_t acc = (it > 0 || kk > 0) ? 1u : 0u;
+                    asm volatile(
+                        "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(acc_t),
+                        "l"(da), "l"(db), "r"(idesc), "r"(acc));
+                }
+                asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                    smem_u32(&bar_empty[s])));
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                smem_u32(&acc_full[b])));
+        }
+    } else if (warp >= 4) {  // epilogue
+        const int ew = warp - 4, etid = tid - 128;
+        uint32_t i = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, i++) {
+            const int ct = t % ntile, tv = ct * FC_N, ta = (t / ntile) * FC_M;
+            const uint32_t b = i & 1;
+            if (lane == 0) mbar_wait_sleep(&acc_full[b], (i >> 1) & 1);  // one waiter per warp
+            __syncwarp();
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
+            if (dbg & 4) {  // main loop only (timing experiments)
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(&acc_empty[b])) : "memory");
+                continue;
+            }
+            fc_epilogue(tmem + b * FC_N, ew & 3, ew >> 2, lane, etid, ta, tv, n, a0, V, fnorm, wnorm, bias, gamma,
+                        out + ct, ntile, s_wmax, s_bias, hv, (int *)(hv + FC_M * FC_KC), (float *)(hv + 2 * FC_M * FC_KC),
+                        &acc_empty[b], [] { asm volatile("bar.sync 1, 256;\n" ::: "memory"); });
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
+    __syncthreads();
+    if (warp == 2) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(2 * FC_N));
 }
 
 // float64 logit of class v for feature row f (warp-cooperative; result in all lanes)
@@ -436,8 +574,8 @@ __global__ void __launch_bounds__(256, 2) k_fc_merge(int n, int64_t a0, const ch
             ecls[u] = e < nc ? t[e / FC_KC].idx[e % FC_KC] : -1;
             elv[u] = e < nc ? t[e / FC_KC].val[e % FC_KC] : 0.f;
             const float ge = ecls[u] >= 0 ? gamma * fn * wnorm[ecls[u]] : 0.f;
-            const float err = ge + fabsf(elv[u]) * 2.4e-7f;
-            ekb[u] = elv[u] - ge - fabsf(elv[u]) * 2.4e-7f;
+            const float err = ge + fabsf(elv[u]) * FC_REL;
+            ekb[u] = elv[u] - ge - fabsf(elv[u]) * FC_REL;
             elb[u] = elv[u] - err;
             eub[u] = elv[u] + err;
         }
@@ -492,7 +630,7 @@ __global__ void __launch_bounds__(256, 2) k_fc_merge(int n, int64_t a0, const ch
                 bool done = false;
                 for (int q = 0; q < r; q++) done |= (s_idx[wib][q] == e);
                 const float lv = t[ti].val[j];
-                const float lb = lv - gamma * fn * wnorm[cls] - fabsf(lv) * 2.4e-7f;
+                const float lb = lv - gamma * fn * wnorm[cls] - fabsf(lv) * FC_REL;
                 if (!done && lb > best) {
                     best = lb;
                     bslot = e;
@@ -523,7 +661,7 @@ __global__ void __launch_bounds__(256, 2) k_fc_merge(int n, int64_t a0, const ch
                     cls = t[ti].idx[j];
                     if (cls >= 0) {
                         const float lv = t[ti].val[j];
-                        take = lv + gamma * fn * wnorm[cls] + fabsf(lv) * 2.4e-7f >= lbk;
+                        take = lv + gamma * fn * wnorm[cls] + fabsf(lv) * FC_REL >= lbk;
                     }
                 }
                 const unsigned m = __ballot_sync(0xffffffffu, take);
@@ -532,7 +670,7 @@ __global__ void __launch_bounds__(256, 2) k_fc_merge(int n, int64_t a0, const ch
                     if (pos < FC_MAXC) {
                         const int ti = e / FC_KC, j = e % FC_KC;
                         const float lv = t[ti].val[j];
-                        const float err = gamma * fn * wnorm[cls] + fabsf(lv) * 2.4e-7f;
+                        const float err = gamma * fn * wnorm[cls] + fabsf(lv) * FC_REL;
                         s_idx[wib][pos] = cls;
                         s_lb[wib][pos] = lv - err;
                         s_ub[wib][pos] = lv + err;
@@ -637,6 +775,17 @@ __global__ void k_row_norms(int64_t rows, int D, const float *__restrict__ X, fl
 
 bool make_rows_map(CUtensorMap *tm, const void *base, int64_t rows, int D, int64_t row_bytes, int box_rows);
 
+static int num_sms() {
+    static int v[64] = {};
+    int &x = v[dev_slot()];
+    if (!x) {
+        int dev = 0;
+        FX_CUDA(cudaGetDevice(&dev));
+        FX_CUDA(cudaDeviceGetAttribute(&x, cudaDevAttrMultiProcessorCount, dev));
+    }
+    return x;
+}
+
 // K1b over classified objects [c0, c0 + n) of a stream (topk written by object index).
 // Xdense: when the n objects' rows are the consecutive fp32 rows Xdense[0..n)
 // (standalone head, compact ingest), operands are staged by TMA.
@@ -648,9 +797,13 @@ void launch_fc_head(int64_t n, int64_t c0, const char *const *frow, const int64_
     static bool attr_set[64] = {};
     bool &attr = attr_set[dev_slot()];
     const size_t smem = (size_t)FC_STAGES * (FC_A_BYTES + FC_B_BYTES) + 1024;
+    const size_t smem_p = smem + (size_t)FC_M * (2 * FC_KC + 3) * 4;  // + the epilogue's hand-off
+    // persistent kernel (TMA operands): FOCUS_B200_FC_PERSIST=0 -> one CTA per tile
+    static const bool persist = !(getenv("FOCUS_B200_FC_PERSIST") && atoi(getenv("FOCUS_B200_FC_PERSIST")) == 0);
     if (!attr) {
         for (auto k : {k_fc_tc<false, 1>, k_fc_tc<true, 1>, k_fc_tc<true, 2>, k_fc_tc<true, 4>})
             FX_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        FX_CUDA(cudaFuncSetAttribute(k_fc_tcp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_p));
         attr = true;
     }
     static const bool tma_off = getenv("FOCUS_B200_TCLOAD") && std::string(getenv("FOCUS_B200_TCLOAD")) == "cp";
@@ -671,7 +824,12 @@ void launch_fc_head(int64_t n, int64_t c0, const char *const *frow, const int64_
     for (int64_t b = 0; b < n; b += CH) {
         const int64_t m = std::min<int64_t>(CH, n - b);
         static const int dbg = getenv("FOCUS_B200_FCDBG") ? atoi(getenv("FOCUS_B200_FCDBG")) : 0;
-        if (tma && CL > 1) {
+        if (tma && persist && CL == 1) {
+            const int ntiles = ntile * (int)cdiv(m, FC_M);
+            const int grid = std::min(ntiles, num_sms());
+            k_fc_tcp<<<grid, FCP_THREADS, smem_p, st>>>((int)m, c0 + b, fnorm, D, V, wnorm, bias, gamma, tiles.p,
+                                                        ntile, ntiles, tmA, tmW, (int)b, dbg);
+        } else if (tma && CL > 1) {
             // object tiles padded to whole clusters (TMA zero-fills rows past the
             // features; the padded tiles write nothing)
             cudaLaunchConfig_t cfg = {};

@@ -49,6 +49,21 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         "r"(parity));
 }
 
+// As mbar_wait, backing off between polls (waiters that would otherwise
+// compete for issue slots with the threads they wait for).
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
+    uint32_t ok = 0;
+    for (;;) {
+        asm volatile(
+            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(parity)
+            : "memory");
+        if (ok) return;
+        __nanosleep(64);
+    }
+}
+
 // Operand tile: NR rows x TC_KT floats at k0; row r of the tile -> global row
 // pointer rows[r] (nullptr -> zeros).  Canonical no-swizzle K-major layout:
 // ((r/8)*(KT/4) + c)*128 + (r%8)*16 (8-row x 16-byte core matrices).
