@@ -23,6 +23,7 @@
 #include <algorithm>
 #include <cfloat>
 #include <climits>
+#include <cstdio>
 #include <cstdlib>
 #include <string>
 
@@ -489,27 +490,45 @@ __global__ void __launch_bounds__(FCP_THREADS, 1) k_fc_tcp(int n, int64_t a0, co
 // (rows 16-byte aligned, D % 4 == 0: float4 loads, two independent chains per lane)
 __device__ __forceinline__ double fc_logit64(const float *f, const float *w, int D, double b) {
     const float4 *f4 = (const float4 *)f, *w4 = (const float4 *)w;
-    double a0 = 0.0, a1 = 0.0;
-    for (int k = threadIdx.x & 31; k < (D >> 2); k += 32) {
-        const float4 x = __ldg(f4 + k), y = __ldg(w4 + k);
-        a0 = fma((double)x.x, (double)y.x, a0);
-        a1 = fma((double)x.y, (double)y.y, a1);
-        a0 = fma((double)x.z, (double)y.z, a0);
-        a1 = fma((double)x.w, (double)y.w, a1);
-    }
-    double acc = a0 + a1;
+    double acc[8];
 #pragma unroll
-    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    return acc + b;
+    for (int e = 0; e < 8; e++) acc[e] = 0.0;
+    const int n4 = D >> 2;
+    int k = threadIdx.x & 31;
+    for (; k + 32 < n4; k += 64) {  // two float4 of each row per lane in flight
+        const float4 x0 = __ldg(f4 + k), y0 = __ldg(w4 + k), x1 = __ldg(f4 + k + 32), y1 = __ldg(w4 + k + 32);
+        acc[0] = fma((double)x0.x, (double)y0.x, acc[0]);
+        acc[1] = fma((double)x0.y, (double)y0.y, acc[1]);
+        acc[2] = fma((double)x0.z, (double)y0.z, acc[2]);
+        acc[3] = fma((double)x0.w, (double)y0.w, acc[3]);
+        acc[4] = fma((double)x1.x, (double)y1.x, acc[4]);
+        acc[5] = fma((double)x1.y, (double)y1.y, acc[5]);
+        acc[6] = fma((double)x1.z, (double)y1.z, acc[6]);
+        acc[7] = fma((double)x1.w, (double)y1.w, acc[7]);
+    }
+    if (k < n4) {
+        const float4 x = __ldg(f4 + k), y = __ldg(w4 + k);
+        acc[0] = fma((double)x.x, (double)y.x, acc[0]);
+        acc[1] = fma((double)x.y, (double)y.y, acc[1]);
+        acc[2] = fma((double)x.z, (double)y.z, acc[2]);
+        acc[3] = fma((double)x.w, (double)y.w, acc[3]);
+    }
+    double r = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+    return r + b;
 }
 
-// Same sums as fc_logit64, the feature row held in registers (fr[i] = f4[lane
+// The float64 logit as fc_logit64 (eight partial sums per lane), the feature row held in registers (fr[i] = f4[lane
 // + 32 i], i < nf = D / 128 <= 16): per candidate only the W row is loaded,
 // 8 float4 per lane in flight.
-__device__ __forceinline__ double fc_logit64_reg(const float4 (&fr)[16], int nf, const float *w, double b) {
+template <bool REG>
+__device__ __forceinline__ double fc_logit64_reg(const float4 (&fr)[REG ? 16 : 1], int nf, const float *w, double b) {
     const float4 *w4 = (const float4 *)w;
     const int lane = threadIdx.x & 31;
-    double a0 = 0.0, a1 = 0.0;
+    double acc[8];  // eight independent FMA chains (a chain of 64 dependent DFMAs stalls the warp)
+#pragma unroll
+    for (int e = 0; e < 8; e++) acc[e] = 0.0;
 #pragma unroll
     for (int h = 0; h < 16; h += 8) {
         if (h >= nf) break;
@@ -520,29 +539,34 @@ __device__ __forceinline__ double fc_logit64_reg(const float4 (&fr)[16], int nf,
 #pragma unroll
         for (int i = 0; i < 8; i++)
             if (h + i < nf) {
-                const float4 x = fr[h + i];
-                a0 = fma((double)x.x, (double)y[i].x, a0);
-                a1 = fma((double)x.y, (double)y[i].y, a1);
-                a0 = fma((double)x.z, (double)y[i].z, a0);
-                a1 = fma((double)x.w, (double)y[i].w, a1);
+                const float4 x = fr[REG ? h + i : 0];
+                double *a = acc + 4 * (i & 1);
+                a[0] = fma((double)x.x, (double)y[i].x, a[0]);
+                a[1] = fma((double)x.y, (double)y[i].y, a[1]);
+                a[2] = fma((double)x.z, (double)y[i].z, a[2]);
+                a[3] = fma((double)x.w, (double)y[i].w, a[3]);
             }
     }
-    double acc = a0 + a1;
+    double r = ((acc[0] + acc[1]) + (acc[2] + acc[3])) + ((acc[4] + acc[5]) + (acc[6] + acc[7]));
 #pragma unroll
-    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    return acc + b;
+    for (int o = 16; o; o >>= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+    return r + b;
 }
 
 constexpr int FC_MAXC = 64;  // candidates re-scored per object before the all-class fallback
+#ifndef FC_MERGE_MINB
+#define FC_MERGE_MINB 4  // merge CTAs per SM (registers <= 64: the re-score is latency-bound)
+#endif
 
-__global__ void __launch_bounds__(256, 2) k_fc_merge(int n, int64_t a0, const char *const *__restrict__ frow,
+template <bool REG>
+__global__ void __launch_bounds__(256, REG ? 2 : FC_MERGE_MINB) k_fc_merge(int n, int64_t a0, const char *const *__restrict__ frow,
                                                  const int64_t *__restrict__ cls_obj, const float *__restrict__ fnorm,
                                                  int D, int V, int K, const float *__restrict__ W,
                                                  const float *__restrict__ wnorm, const float *__restrict__ bias,
                                                  float gamma, int ntile, const FcTile *__restrict__ tiles,
                                                  int32_t *__restrict__ topk, float *__restrict__ conf,
                                                  uint8_t *__restrict__ flag, unsigned long long *__restrict__ nflag,
-                                                 int merge_reg) {
+                                                 unsigned long long *stats) {
     __shared__ int s_idx[8][FC_MAXC];
     __shared__ float s_lb[8][FC_MAXC], s_ub[8][FC_MAXC];
     __shared__ unsigned char s_need[8][FC_MAXC];
@@ -705,10 +729,10 @@ __global__ void __launch_bounds__(256, 2) k_fc_merge(int n, int64_t a0, const ch
     }
     __syncwarp();
     const int nscore = all ? V : ncand;
-    const bool reg = merge_reg && (D & 127) == 0 && D <= 2048;  // feature row cached in registers
+    const bool reg = REG && (D & 127) == 0 && D <= 2048;  // feature row cached in registers
     const int nf = D >> 7;
-    float4 fr[16];
-    if (reg) {
+    float4 fr[REG ? 16 : 1];
+    if (REG && reg) {
 #pragma unroll
         for (int i = 0; i < 16; i++)
             if (i < nf) fr[i] = __ldg((const float4 *)f + lane + 32 * i);
@@ -717,7 +741,7 @@ __global__ void __launch_bounds__(256, 2) k_fc_merge(int n, int64_t a0, const ch
         const int cls = all ? c : s_idx[wib][c];
         double l;
         if (all || s_need[wib][c])
-            l = reg ? fc_logit64_reg(fr, nf, W + (int64_t)cls * D, bias ? (double)bias[cls] : 0.0)
+            l = reg ? fc_logit64_reg<REG>(fr, nf, W + (int64_t)cls * D, bias ? (double)bias[cls] : 0.0)
                     : fc_logit64(f, W + (int64_t)cls * D, D, bias ? (double)bias[cls] : 0.0);
         else
             l = 0.5 * ((double)s_lb[wib][c] + (double)s_ub[wib][c]);  // disjoint interval: its order is certain
@@ -760,6 +784,13 @@ __global__ void __launch_bounds__(256, 2) k_fc_merge(int n, int64_t a0, const ch
         }
         if (flag) flag[obj] = flagged ? 1 : 0;
         if (flagged && nflag) atomicAdd(nflag, 1ull);
+        if (stats) {  // FOCUS_B200_FC_STATS: objects re-scored over every class / candidates re-scored
+            atomicAdd(stats, all ? 1ull : 0ull);
+            unsigned long long nr = 0;
+            for (int c = 0; c < ncand && !all; c++) nr += s_need[wib][c];
+            atomicAdd(stats + 1, all ? (unsigned long long)V : nr);
+            atomicAdd(stats + 2, all ? 0ull : (unsigned long long)(ncand > 64 ? 64 : ncand));
+        }
     }
 }
 
@@ -810,14 +841,21 @@ void launch_fc_head(int64_t n, int64_t c0, const char *const *frow, const int64_
     // W multicast cluster size (FOCUS_B200_FC_CL: 1, 2 or 4; default 1: 4 measured
     // 17% slower -- the head is not bound by L2 -> SM operand traffic)
     static const int cl_env = getenv("FOCUS_B200_FC_CL") ? atoi(getenv("FOCUS_B200_FC_CL")) : 1;
-    // float64 re-score with the feature row in registers (FOCUS_B200_FC_MERGE_REG=0: re-read per candidate)
-    static const int merge_reg = getenv("FOCUS_B200_FC_MERGE_REG") ? atoi(getenv("FOCUS_B200_FC_MERGE_REG")) : 1;
+    // float64 re-score: the feature row re-read per candidate (L1) at 64 registers, 4 CTAs per SM
+    // (FOCUS_B200_FC_MERGE_REG=1: the row held in registers, 2 CTAs per SM -- measured 818 vs 531 us)
+    static const int merge_reg = getenv("FOCUS_B200_FC_MERGE_REG") ? atoi(getenv("FOCUS_B200_FC_MERGE_REG")) : 0;
     const int CL = (cl_env == 2 || cl_env == 4) ? cl_env : 1;
     CUtensorMap tmA = {}, tmW = {};
     const bool tma = Xdense && !tma_off && D % 4 == 0 && make_rows_map(&tmA, Xdense, n, D, (int64_t)D * 4, FC_M) &&
                      make_rows_map(&tmW, W, V, D, (int64_t)D * 4, FC_N / CL);
     const int ntile = (int)cdiv(V, FC_N);
     const float gamma = (float)((1.953125e-03 + (double)D * 2.384185791015625e-07) * 1.01);
+    static const bool fc_stats = getenv("FOCUS_B200_FC_STATS") != nullptr;
+    DevBuf<unsigned long long> stats;
+    if (fc_stats) {
+        stats.reserve(3);
+        FX_CUDA(cudaMemsetAsync(stats.p, 0, 3 * sizeof(unsigned long long), st));
+    }
     DevBuf<FcTile> tiles;
     const int64_t CH = 1 << 16;  // objects per pass (bounds the tile scratch)
     tiles.reserve((size_t)std::min<int64_t>(n, CH) * ntile);
@@ -852,10 +890,17 @@ void launch_fc_head(int64_t n, int64_t c0, const char *const *frow, const int64_
                 (int)m, c0 + b, frow, fnorm, D, V, W, wnorm, bias, gamma, tiles.p, dbg, tmA, tmW, (int)b);
         }
         FX_LAUNCHED();
-        k_fc_merge<<<(unsigned)cdiv(m, 8), 256, 0, st>>>((int)m, c0 + b, frow, cls_obj, fnorm, D, V, K, W, wnorm, bias,
+        (merge_reg ? k_fc_merge<true> : k_fc_merge<false>)<<<(unsigned)cdiv(m, 8), 256, 0, st>>>((int)m, c0 + b, frow, cls_obj, fnorm, D, V, K, W, wnorm, bias,
                                                         gamma, ntile, tiles.p, topk, conf, flag, nflag,
-                                                        merge_reg);
+                                                        fc_stats ? stats.p : nullptr);
         FX_LAUNCHED();
+    }
+    if (fc_stats) {
+        unsigned long long h[3];
+        FX_CUDA(cudaMemcpyAsync(h, stats.p, sizeof(h), cudaMemcpyDeviceToHost, st));
+        FX_CUDA(cudaStreamSynchronize(st));
+        fprintf(stderr, "fc_stats: objects %lld, all-class %llu, re-scored %llu, candidates %llu\n", (long long)n, h[0],
+                h[1], h[2]);
     }
 }
 
