@@ -682,7 +682,23 @@ def main():
             tf32_peak, pk = bf16 / 2.0, "MEASURED_PEAKS bf16 dense / 2 (TF32 is half the BF16 rate)"
         except Exception:
             tf32_peak, pk = 1125.0, "fallback: nominal 2.25 PF bf16 / 2"
-        fcres = {"objects": nfc, "vocab": W["vocab"], "dim": W["dim"], "k": W["k"], "ms": ms,
+        # per-kernel split of one more call (CUPTI): the logits kernel's own tensor-pipe fraction
+        per_k = {}
+        try:
+            from torch.profiler import ProfilerActivity, profile
+            with profile(activities=[ProfilerActivity.CUDA]) as prof:
+                fc_call()
+                torch.cuda.synchronize()
+            for ev in prof.events():
+                if ev.device_type == torch.autograd.DeviceType.CUDA and "k_fc" in ev.name:
+                    nm = ev.name.split("(")[0].replace("void ", "").replace("fx::", "")
+                    per_k[nm] = per_k.get(nm, 0.0) + ev.device_time_total / 1e3
+        except Exception as e:  # profiler unavailable: the split is optional
+            per_k = {"unavailable": str(e)[:80]}
+        fc_kernels = {k: {"ms": v, "tflops": flops / (v / 1e3) / 1e12 if "tcp" in k or "fc_tc" in k else None,
+                          "frac": (flops / (v / 1e3) / 1e12) / tf32_peak if "tcp" in k or "fc_tc" in k else None}
+                      for k, v in per_k.items() if isinstance(v, float)}
+        fcres = {"objects": nfc, "vocab": W["vocab"], "dim": W["dim"], "k": W["k"], "ms": ms, "kernels": fc_kernels,
                  "objects_per_s": nfc / (ms / 1e3), "achieved_tflops": tf, "peak_tflops": tf32_peak,
                  "frac": tf / tf32_peak, "peak_kind": pk, "flagged": int(fl.sum().item()),
                  "bound": "tensor", "note": "TF32 tcgen05 logits + float64 re-score of the candidates"}
