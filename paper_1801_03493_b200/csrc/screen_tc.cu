@@ -35,7 +35,7 @@ namespace cg = cooperative_groups;
 
 namespace fx {
 
-constexpr int TC_M = 128, TC_N = 128, TC_STAGES = 6, TC_THREADS = 256;  // warps 4-7 only help load
+constexpr int TC_M = 128, TC_N = 128, TC_STAGES = 6, TC_STAGES2 = 3, TC_THREADS = 256;  // warps 4-7 only help load
 constexpr int TC_TILE_BYTES = TC_M * TC_KT * 4;  // 16 KB per operand per stage
 
 // Operand staging by TMA (TMA = true): one 2-D tiled box (32 fp32 x 128 rows,
@@ -50,7 +50,7 @@ constexpr int TC_TILE_BYTES = TC_M * TC_KT * 4;  // 16 KB per operand per stage
 // empty barriers the MMA commit plus the four norm warps.
 
 // out[a][q] = ||A_a||^2 + ||B_q||^2 - 2 A_a.B_q   (float, not clamped)
-template <bool TMA>
+template <bool TMA, int ST>
 __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0, const char *const *__restrict__ frow,
                                                            const float *fnorm, int D,  // aliases fnorm_out
                                                            const int64_t *__restrict__ nB_dev,
@@ -106,8 +106,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
     __shared__ const float *rowsB[TC_N];
     __shared__ int rcls[TC_M];  // batch-local classified index of each tile row, -1: none
     __shared__ float cn2t[TC_N];  // ||c||^2 of the tile's snapshot columns (gathered once)
-    __shared__ __align__(8) uint64_t bar_stage[TC_STAGES];
-    __shared__ __align__(8) uint64_t bar_full[TC_STAGES];
+    __shared__ __align__(8) uint64_t bar_stage[ST];
+    __shared__ __align__(8) uint64_t bar_full[ST];
     __shared__ __align__(8) uint64_t bar_done;
     __shared__ uint32_t tmem_base;
 
@@ -123,7 +123,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
         }
     }
     if (tid == 0) {
-        for (int s = 0; s < TC_STAGES; s++) {
+        for (int s = 0; s < ST; s++) {
             mbar_init(&bar_stage[s], TMA ? 5 : 1);
             mbar_init(&bar_full[s], 1);
         }
@@ -152,8 +152,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
             asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmA) : "memory");
             asm volatile("prefetch.tensormap [%0];\n" ::"l"(&tmB) : "memory");
             for (int it = 0; it < nk; it++) {
-                const int s = it % TC_STAGES;
-                if (it >= TC_STAGES) mbar_wait(&bar_stage[s], (uint32_t)(((it / TC_STAGES) - 1) & 1));
+                const int s = it % ST;
+                if (it >= ST) mbar_wait(&bar_stage[s], (uint32_t)(((it / ST) - 1) & 1));
                 const uint32_t st = sbase + s * 2 * TC_TILE_BYTES;
                 const uint32_t fb = smem_u32(&bar_full[s]);
                 asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(fb), "r"(2 * TC_TILE_BYTES)
@@ -172,8 +172,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
             }
         } else if (warp == 5) {  // MMA issue
             for (int it = 0; it < nk; it++) {
-                const int s = it % TC_STAGES;
-                mbar_wait(&bar_full[s], (uint32_t)((it / TC_STAGES) & 1));
+                const int s = it % ST;
+                mbar_wait(&bar_full[s], (uint32_t)((it / ST) & 1));
                 if (lane == 0) {
                     asm volatile("tcgen05.fence::after_thread_sync;\n" ::);
                     const uint32_t st = sbase + s * 2 * TC_TILE_BYTES;
@@ -197,8 +197,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
                     smem_u32(&bar_done)));
         } else if (warp < 4) {  // row norms: row tid's 8 chunks of 16 B in the swizzled atom
             for (int it = 0; it < nk; it++) {
-                const int s = it % TC_STAGES;
-                mbar_wait(&bar_full[s], (uint32_t)((it / TC_STAGES) & 1));
+                const int s = it % ST;
+                mbar_wait(&bar_full[s], (uint32_t)((it / ST) & 1));
                 const unsigned char *row = smem + s * 2 * TC_TILE_BYTES + (tid >> 3) * 1024 + (tid & 7) * 128;
                 float p = 0.f;
 #pragma unroll
@@ -217,7 +217,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
     } else {
         auto kof = [&](int i) { return kbeg + i * TC_KT; };
         // prologue: stages 0..S-2
-        for (int s = 0; s < TC_STAGES - 1; s++) {
+        for (int s = 0; s < ST - 1; s++) {
             if (s < nk && !(dbg & 1)) {
                 const uint32_t st = sbase + s * 2 * TC_TILE_BYTES;
                 load_tile<TC_M, TC_THREADS>(st, rowsA, kof(s), kend, fnorm);
@@ -226,8 +226,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
             asm volatile("cp.async.commit_group;\n" ::);
         }
         for (int it = 0; it < nk; it++) {
-            const int s = it % TC_STAGES;
-            asm volatile("cp.async.wait_group %0;\n" ::"n"(TC_STAGES - 2));
+            const int s = it % ST;
+            asm volatile("cp.async.wait_group %0;\n" ::"n"(ST - 2));
             asm volatile("fence.proxy.async.shared::cta;\n" ::);
             __syncthreads();
             if (tid < TC_M) {  // the row norm rides along: row tid's 32 values of this stage (stable until its refill)
@@ -260,10 +260,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
                     smem_u32(&bar_stage[s])));
             }
             // refill the stage consumed S-1 iterations from now
-            const int nt = it + TC_STAGES - 1;
+            const int nt = it + ST - 1;
             if (nt < nk) {
-                const int ns = nt % TC_STAGES;
-                if (nt >= TC_STAGES && !(dbg & 2)) mbar_wait(&bar_stage[ns], (uint32_t)(((nt / TC_STAGES) - 1) & 1));
+                const int ns = nt % ST;
+                if (nt >= ST && !(dbg & 2)) mbar_wait(&bar_stage[ns], (uint32_t)(((nt / ST) - 1) & 1));
                 const uint32_t st = sbase + ns * 2 * TC_TILE_BYTES;
                 if (!(dbg & 1)) {
                     load_tile<TC_M, TC_THREADS>(st, rowsA, kof(nt), kend, fnorm);
@@ -388,9 +388,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1) k_screen_tc(int nA, int64_t a0,
     if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(TC_N));
 }
 
-size_t screen_tc_smem() {
+size_t screen_tc_smem(int stages) {
     // pipeline stages; the epilogue's [128][TC_N+4] tile reuses them
-    const size_t pipe = (size_t)TC_STAGES * 2 * TC_TILE_BYTES;
+    const size_t pipe = (size_t)stages * 2 * TC_TILE_BYTES;
     return std::max(pipe, (size_t)TC_M * (TC_N + 4) * 4) + 1024;
 }
 
@@ -426,8 +426,10 @@ void launch_screen_tc(int nA, int64_t a0, const char *const *frow, const float *
     static bool attr_set[64] = {};
     bool &attr = attr_set[dev_slot()];
     if (!attr) {
-        for (auto k : {k_screen_tc<false>, k_screen_tc<true>})
-            FX_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)screen_tc_smem()));
+        for (auto k : {k_screen_tc<false, TC_STAGES>, k_screen_tc<true, TC_STAGES>})
+            FX_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)screen_tc_smem(TC_STAGES)));
+        FX_CUDA(cudaFuncSetAttribute(k_screen_tc<true, TC_STAGES2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)screen_tc_smem(TC_STAGES2)));
         attr = true;
     }
     const bool tma = tmA && tmB;
@@ -444,6 +446,18 @@ void launch_screen_tc(int nA, int64_t a0, const char *const *frow, const float *
     // per SM) with >= 4 pipeline stages per CTA
     int split = 1;
     while (split < 8 && tiles * (split + 1) <= 148 && D / (split + 1) >= 4 * TC_KT) split++;
+    // FOCUS_B200_TC2=1: two CTAs per SM (TC_STAGES2-stage rings, 97 KB each)
+    // when a 2-way split no longer fits one CTA per SM but fits two.  Measured
+    // at C2 (B = 8192, 80 row tiles -> 160 CTAs): screen 42.8 -> 39.3 us per
+    // launch, but the stream is not faster (44.4 vs 44.8 M objects/s, one run
+    // of four stalled at 32.7 M): the half-SM CTAs delay the PDL-launched
+    // kernels behind them.  Off by default.
+    static const bool two_env = getenv("FOCUS_B200_TC2") && atoi(getenv("FOCUS_B200_TC2")) == 1;
+    bool two = false;
+    if (tma && two_env && split == 1 && tiles * 2 > 148 && tiles * 2 <= 2 * 148 && D / 2 >= 4 * TC_KT) {
+        split = 2;
+        two = true;
+    }
     if (split_env > 0) split = split_env;
     split = std::min(split, 8);  // split-K CTAs of a tile form one (portable-size) cluster
     const int kchunk = (int)(cdiv(cdiv(D, split), TC_KT) * TC_KT);
@@ -451,7 +465,7 @@ void launch_screen_tc(int nA, int64_t a0, const char *const *frow, const float *
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3((unsigned)(cdiv(nB_max, TC_N) * cdiv(nR, TC_M)), 1, (unsigned)split);
     lc.blockDim = dim3(TC_THREADS);
-    lc.dynamicSmemBytes = screen_tc_smem();
+    lc.dynamicSmemBytes = screen_tc_smem(two ? TC_STAGES2 : TC_STAGES);
     lc.stream = st;
     cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -462,7 +476,11 @@ void launch_screen_tc(int nA, int64_t a0, const char *const *frow, const float *
     at[1].val.programmaticStreamSerializationAllowed = 1;
     lc.attrs = at;
     lc.numAttrs = pdl_enabled() ? 2 : 1;
-    FX_CUDA(cudaLaunchKernelEx(&lc, tma ? k_screen_tc<true> : k_screen_tc<false>, nA, a0, frow, fnorm, D, nB_dev, C32,
+    FX_CUDA(cudaLaunchKernelEx(&lc,
+                               two   ? k_screen_tc<true, TC_STAGES2>
+                               : tma ? k_screen_tc<true, TC_STAGES>
+                                     : k_screen_tc<false, TC_STAGES>,
+                               nA, a0, frow, fnorm, D, nB_dev, C32,
                                snap, cn2, out, ld, kchunk, dbg, fnorm_out, sm, T, res_col, res_pos, nres, rowmin_g,
                                snorm, tma ? *tmA : zero_map, tma ? *tmB : zero_map, rbase, nR, rmap));
     FX_LAUNCHED();
