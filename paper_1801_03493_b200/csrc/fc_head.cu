@@ -73,7 +73,8 @@ __device__ __forceinline__ void fc_epilogue(uint32_t tmem, int quad, int half, i
                                             int n, int64_t a0, int V, const float *__restrict__ fnorm,
                                             const float *__restrict__ wnorm, const float *__restrict__ bias,
                                             float gamma, FcTile *__restrict__ out, int ntile, float *s_wmax, float *s_bias,
-                                            float *hv, int *hi, float *hx, uint64_t *tmem_empty, Sync sync) {
+                                            float *hv, int *hi, float *hx, uint64_t *tmem_empty, Sync sync,
+                                            int edbg = 0) {
     const int a = ta + quad * 32 + lane;
     const float fn = a < n ? fnorm[a0 + a] : 0.f;
     {
@@ -132,12 +133,12 @@ __device__ __forceinline__ void fc_epilogue(uint32_t tmem, int quad, int half, i
             const float nm = fmaxf(m, cm);
             float cs = 0.f;
 #pragma unroll
-            for (int j = 0; j < 32; j++) cs += x[j] == -FLT_MAX ? 0.f : __expf(x[j] - nm);
+            for (int j = 0; j < 32; j++) cs += (edbg & 32) || x[j] == -FLT_MAX ? 0.f : __expf(x[j] - nm);
             ssum = ssum * __expf(m - nm) + cs;
             m = nm;
 #pragma unroll
             for (int j = 0; j < 32; j++)
-                if (x[j] != -FLT_MAX) insert(fc_key(x[j], c0 + j));
+                if (x[j] != -FLT_MAX && !(edbg & 16)) insert(fc_key(x[j], c0 + j));
         }
     }
     if (tmem_empty) {  // accumulator read: the MMA may overwrite it
@@ -478,7 +479,7 @@ __global__ void __launch_bounds__(FCP_THREADS, 1) k_fc_tcp(int n, int64_t a0, co
             }
             fc_epilogue(tmem + b * FC_N, ew & 3, ew >> 2, lane, etid, ta, tv, n, a0, V, fnorm, wnorm, bias, gamma,
                         out + ct, ntile, s_wmax, s_bias, hv, (int *)(hv + FC_M * FC_KC), (float *)(hv + 2 * FC_M * FC_KC),
-                        &acc_empty[b], [] { asm volatile("bar.sync 1, 256;\n" ::: "memory"); });
+                        &acc_empty[b], [] { asm volatile("bar.sync 1, 256;\n" ::: "memory"); }, dbg);
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::);
