@@ -11,4 +11,6 @@ timeout 900 ncu --set full --clock-control none --import-source on \
   -o gpurun_out/full_$T -f $B --no-fc > gpurun_out/full_$T.log 2>&1
 timeout 600 ncu --set full --clock-control none --import-source on -k 'regex:k_fc_tc|k_fc_merge|k_extract' --launch-count 3 \
   -o gpurun_out/fc_$T -f $B > gpurun_out/fc_$T.log 2>&1
+
+timeout 600 python tools/trace_kernels.py 1000000 > gpurun_out/cupti_c2_$T.txt 2>&1
 echo done
