@@ -456,9 +456,9 @@ def main():
     roofline = {"kernel": "k_screen_tc (K2 TF32 distance screen)", "bound": "hbm", "achieved": scr_ach, "peak": peak,
                 "unit": "GB/s", "frac": scr_ach / peak, "traffic": traffic,
                 "traffic_note": "dram read+write bytes per launch, ncu --set full of a steady-state batch "
-                                "(profiles/r01e_ncu_full_metrics.txt); algorithmic bytes of a B=4096 launch = "
-                                "4*D*4096 + 4*4096*101 = 35.2 MB; the TMA boxes also stage the duplicate objects' "
-                                "rows between the batch's classified rows (~1.22x)", "peak_kind": peak_kind,
+                                "(profiles/r02f_ncu_full_metrics.txt, B = 8192 classified objects: algorithmic "
+                                "4*D*8192 + 4*8192*101 = 70.4 MB, so ~1.26x): the TMA boxes also stage the "
+                                "duplicate objects' rows between the batch's classified rows", "peak_kind": peak_kind,
                 "launches_per_step": int(nb), "bytes_per_launch": kern["screen"][0] / nb,
                 "avg_launch_us": scr_ms * 1e3 / nb,
                 "per_kernel": rl,

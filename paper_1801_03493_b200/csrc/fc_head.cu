@@ -489,6 +489,7 @@ __global__ void __launch_bounds__(FCP_THREADS, 1) k_fc_tcp(int n, int64_t a0, co
 
 // float64 logit of class v for feature row f (warp-cooperative; result in all lanes)
 // (rows 16-byte aligned, D % 4 == 0: float4 loads, two independent chains per lane)
+template <int FC_LD>  // 16-byte chunks of each row per lane in flight
 __device__ __forceinline__ double fc_logit64(const float *f, const float *w, int D, double b) {
     const float4 *f4 = (const float4 *)f, *w4 = (const float4 *)w;
     double acc[8];
@@ -496,18 +497,23 @@ __device__ __forceinline__ double fc_logit64(const float *f, const float *w, int
     for (int e = 0; e < 8; e++) acc[e] = 0.0;
     const int n4 = D >> 2;
     int k = threadIdx.x & 31;
-    for (; k + 32 < n4; k += 64) {  // two float4 of each row per lane in flight
-        const float4 x0 = __ldg(f4 + k), y0 = __ldg(w4 + k), x1 = __ldg(f4 + k + 32), y1 = __ldg(w4 + k + 32);
-        acc[0] = fma((double)x0.x, (double)y0.x, acc[0]);
-        acc[1] = fma((double)x0.y, (double)y0.y, acc[1]);
-        acc[2] = fma((double)x0.z, (double)y0.z, acc[2]);
-        acc[3] = fma((double)x0.w, (double)y0.w, acc[3]);
-        acc[4] = fma((double)x1.x, (double)y1.x, acc[4]);
-        acc[5] = fma((double)x1.y, (double)y1.y, acc[5]);
-        acc[6] = fma((double)x1.z, (double)y1.z, acc[6]);
-        acc[7] = fma((double)x1.w, (double)y1.w, acc[7]);
+    for (; k + 32 * (FC_LD - 1) < n4; k += 32 * FC_LD) {  // FC_LD 16-byte chunks of each row per lane in flight
+        float4 x[FC_LD], y[FC_LD];
+#pragma unroll
+        for (int u = 0; u < FC_LD; u++) {
+            y[u] = __ldg(w4 + k + 32 * u);
+            x[u] = __ldg(f4 + k + 32 * u);
+        }
+#pragma unroll
+        for (int u = 0; u < FC_LD; u++) {
+            double *a = acc + 4 * (u & 1);
+            a[0] = fma((double)x[u].x, (double)y[u].x, a[0]);
+            a[1] = fma((double)x[u].y, (double)y[u].y, a[1]);
+            a[2] = fma((double)x[u].z, (double)y[u].z, a[2]);
+            a[3] = fma((double)x[u].w, (double)y[u].w, a[3]);
+        }
     }
-    if (k < n4) {
+    for (; k < n4; k += 32) {
         const float4 x = __ldg(f4 + k), y = __ldg(w4 + k);
         acc[0] = fma((double)x.x, (double)y.x, acc[0]);
         acc[1] = fma((double)x.y, (double)y.y, acc[1]);
@@ -559,7 +565,7 @@ constexpr int FC_MAXC = 64;  // candidates re-scored per object before the all-c
 #define FC_MERGE_MINB 4  // merge CTAs per SM (registers <= 64: the re-score is latency-bound)
 #endif
 
-template <bool REG>
+template <bool REG, int LD>
 __global__ void __launch_bounds__(256, REG ? 2 : FC_MERGE_MINB) k_fc_merge(int n, int64_t a0, const char *const *__restrict__ frow,
                                                  const int64_t *__restrict__ cls_obj, const float *__restrict__ fnorm,
                                                  int D, int V, int K, const float *__restrict__ W,
@@ -743,7 +749,7 @@ __global__ void __launch_bounds__(256, REG ? 2 : FC_MERGE_MINB) k_fc_merge(int n
         double l;
         if (all || s_need[wib][c])
             l = reg ? fc_logit64_reg<REG>(fr, nf, W + (int64_t)cls * D, bias ? (double)bias[cls] : 0.0)
-                    : fc_logit64(f, W + (int64_t)cls * D, D, bias ? (double)bias[cls] : 0.0);
+                    : fc_logit64<LD>(f, W + (int64_t)cls * D, D, bias ? (double)bias[cls] : 0.0);
         else
             l = 0.5 * ((double)s_lb[wib][c] + (double)s_ub[wib][c]);  // disjoint interval: its order is certain
         if (lane == 0) {  // lane 0's value decides (its reduction order is fixed)
@@ -845,6 +851,8 @@ void launch_fc_head(int64_t n, int64_t c0, const char *const *frow, const int64_
     // float64 re-score: the feature row re-read per candidate (L1) at 64 registers, 4 CTAs per SM
     // (FOCUS_B200_FC_MERGE_REG=1: the row held in registers, 2 CTAs per SM -- measured 818 vs 531 us)
     static const int merge_reg = getenv("FOCUS_B200_FC_MERGE_REG") ? atoi(getenv("FOCUS_B200_FC_MERGE_REG")) : 0;
+    // row chunks in flight per lane in the re-score (FOCUS_B200_FC_LD: 2 or 4)
+    static const int merge_ld = getenv("FOCUS_B200_FC_LD") ? atoi(getenv("FOCUS_B200_FC_LD")) : 4;
     const int CL = (cl_env == 2 || cl_env == 4) ? cl_env : 1;
     CUtensorMap tmA = {}, tmW = {};
     const bool tma = Xdense && !tma_off && D % 4 == 0 && make_rows_map(&tmA, Xdense, n, D, (int64_t)D * 4, FC_M) &&
@@ -891,7 +899,7 @@ void launch_fc_head(int64_t n, int64_t c0, const char *const *frow, const int64_
                 (int)m, c0 + b, frow, fnorm, D, V, W, wnorm, bias, gamma, tiles.p, dbg, tmA, tmW, (int)b);
         }
         FX_LAUNCHED();
-        (merge_reg ? k_fc_merge<true> : k_fc_merge<false>)<<<(unsigned)cdiv(m, 8), 256, 0, st>>>((int)m, c0 + b, frow, cls_obj, fnorm, D, V, K, W, wnorm, bias,
+        (merge_reg ? k_fc_merge<true, 2> : merge_ld == 2 ? k_fc_merge<false, 2> : k_fc_merge<false, 4>)<<<(unsigned)cdiv(m, 8), 256, 0, st>>>((int)m, c0 + b, frow, cls_obj, fnorm, D, V, K, W, wnorm, bias,
                                                         gamma, ntile, tiles.p, topk, conf, flag, nflag,
                                                         fc_stats ? stats.p : nullptr);
         FX_LAUNCHED();
