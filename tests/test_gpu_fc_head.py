@@ -40,6 +40,22 @@ def test_topk_matches_float64_oracle(n, dim, V, k, seed):
     np.testing.assert_allclose(conf[ok], np.take_along_axis(p, ref.astype(np.int64), axis=1)[ok], rtol=1e-2, atol=1e-6)
 
 
+@pytest.mark.parametrize("n,dim,V,k,seed", [(70000, 64, 1000, 4, 5), (40000, 128, 300, 2, 6)])
+def test_persistent_logits_many_tiles_per_cta(n, dim, V, k, seed):
+    # >= 3 (object, class) tiles per CTA of the persistent k_fc_tcp (both TMEM
+    # accumulators reused, phases wrapping), a partial last class tile, and
+    # (n > 65536) two object chunks of the head
+    rng = np.random.default_rng(200 + seed)
+    F = rng.standard_normal((n, dim)).astype(np.float32)
+    W = (rng.standard_normal((V, dim)) / np.sqrt(dim)).astype(np.float32)
+    b = (0.1 * rng.standard_normal(V)).astype(np.float32)
+    tk, conf, flag = fx.FCHead(W, b).topk(F, k)
+    ref, rflag = O.fc_topk(F, W, b, k)
+    ok = ~(flag | rflag)
+    assert ok.mean() > 0.99
+    assert np.array_equal(tk[ok], ref[ok])
+
+
 def test_near_ties_use_the_all_class_rescore_and_stay_exact():
     # duplicated weight rows (+ tiny perturbations) put many classes inside the
     # TF32 error band of the K-th logit: the kernel must fall back to scoring
