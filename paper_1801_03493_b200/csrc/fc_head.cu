@@ -58,6 +58,45 @@ __device__ __forceinline__ float fc_key_value(int key) {
     return __int_as_float(o < 0 ? o ^ 0x7FFFFFFF : o);
 }
 
+// Bitonic sorting network, 16 keys, descending (min/max only).
+__device__ __forceinline__ void fc_sort16_desc(int (&a)[16]) {
+#pragma unroll
+    for (int k = 2; k <= 16; k <<= 1)
+#pragma unroll
+        for (int j = k >> 1; j > 0; j >>= 1)
+#pragma unroll
+            for (int i = 0; i < 16; i++) {
+                const int l = i ^ j;
+                if (l > i) {
+                    const int hi = max(a[i], a[l]), lo = min(a[i], a[l]);
+                    const bool desc = (i & k) == 0 || k == 16;
+                    a[i] = desc ? hi : lo;
+                    a[l] = desc ? lo : hi;
+                }
+            }
+}
+// kv (16 keys, descending) <- the 16 largest of kv and c (descending); the
+// largest key that falls out goes to dropped.
+__device__ __forceinline__ void fc_merge16(int (&kv)[16], const int (&c)[16], int &dropped) {
+    int m[16];
+#pragma unroll
+    for (int i = 0; i < 16; i++) {  // kv descending, c reversed ascending: m is bitonic
+        m[i] = max(kv[i], c[15 - i]);
+        dropped = max(dropped, min(kv[i], c[15 - i]));
+    }
+#pragma unroll
+    for (int j = 8; j > 0; j >>= 1)  // bitonic clean, descending
+#pragma unroll
+        for (int i = 0; i < 16; i++)
+            if ((i & j) == 0) {
+                const int hi = max(m[i], m[i + j]), lo = min(m[i], m[i + j]);
+                m[i] = hi;
+                m[i + j] = lo;
+            }
+#pragma unroll
+    for (int i = 0; i < 16; i++) kv[i] = m[i];
+}
+
 // Epilogue of one 128 x 256 accumulator (TMEM columns tmem..tmem+255): 256
 // threads, warps (quad, half): TMEM lanes 32 quad.. (object rows) and one half
 // of the 256 classes each; a thread keeps the FC_KC largest logits of its
@@ -91,9 +130,11 @@ __device__ __forceinline__ void fc_epilogue(uint32_t tmem, int quad, int half, i
     // Kept logits as packed keys: the float's order-preserving int with the
     // low 8 bits replaced by 255 - (class within the tile), so one signed
     // compare orders by value and then by smaller class id; the dropped bits
-    // cost < 2^-15 |logit| (FC_REL covers it).  A sorted insert is then a
-    // min/max network: slot q = max(slot q, min(slot q-1, key)), every slot
-    // independent, no divergence between the lanes (objects) of a warp.
+    // cost < 2^-15 |logit| (FC_REL covers it).  Keys are unique within the
+    // tile, so the kept set and the largest dropped key do not depend on the
+    // order of insertion: 16 keys at a time are sorted by a bitonic network
+    // and merged into the list (fc_merge16) -- min/max only, no divergence
+    // between the lanes (objects) of a warp.
     int kv[FC_KC];
 #pragma unroll
     for (int j = 0; j < FC_KC; j++) kv[j] = INT_MIN;
@@ -109,12 +150,6 @@ __device__ __forceinline__ void fc_epilogue(uint32_t tmem, int quad, int half, i
               "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
             : "r"(taddr));
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::);
-    };
-    auto insert = [&](int key) {
-        dropped = max(dropped, min(kv[FC_KC - 1], key));
-#pragma unroll
-        for (int q = FC_KC - 1; q > 0; q--) kv[q] = max(kv[q], min(kv[q - 1], key));
-        kv[0] = max(kv[0], key);
     };
     constexpr int HC = FC_N / 2;
     float m = -FLT_MAX, ssum = 0.f;  // logsumexp partial, updated per 32-class chunk (one TMEM pass)
@@ -136,9 +171,16 @@ __device__ __forceinline__ void fc_epilogue(uint32_t tmem, int quad, int half, i
             for (int j = 0; j < 32; j++) cs += (edbg & 32) || x[j] == -FLT_MAX ? 0.f : __expf(x[j] - nm);
             ssum = ssum * __expf(m - nm) + cs;
             m = nm;
+            if (!(edbg & 16)) {
 #pragma unroll
-            for (int j = 0; j < 32; j++)
-                if (x[j] != -FLT_MAX && !(edbg & 16)) insert(fc_key(x[j], c0 + j));
+                for (int h = 0; h < 32; h += 16) {  // 16 keys at a time: sort them, merge into the list
+                    int c[16];
+#pragma unroll
+                    for (int i = 0; i < 16; i++) c[i] = x[h + i] != -FLT_MAX ? fc_key(x[h + i], c0 + h + i) : INT_MIN;
+                    fc_sort16_desc(c);
+                    fc_merge16(kv, c, dropped);
+                }
+            }
         }
     }
     if (tmem_empty) {  // accumulator read: the MMA may overwrite it
@@ -158,8 +200,10 @@ __device__ __forceinline__ void fc_epilogue(uint32_t tmem, int quad, int half, i
     }
     sync();
     if (half == 0) {
+        int c[FC_KC];
 #pragma unroll
-        for (int j = 0; j < FC_KC; j++) insert(hk[r * FC_KC + j]);
+        for (int j = 0; j < FC_KC; j++) c[j] = hk[r * FC_KC + j];  // sorted (descending) already
+        fc_merge16(kv, c, dropped);
         dropped = max(dropped, __float_as_int(hx[r * 3 + 0]));
         const float m1 = hx[r * 3 + 1], s1 = hx[r * 3 + 2];
         const float mm = fmaxf(m, m1);
