@@ -20,6 +20,7 @@ from __future__ import annotations
 
 import argparse
 import ctypes
+import gc
 import json
 import os
 import subprocess
@@ -550,6 +551,13 @@ def main():
                 "merge": f"{args.backend} all_gather x2 over {ws} ranks" if ws > 1 else "single stream",
                 "timing": "host wall clock per query (fresh session, ids copied to host), max over ranks"}
         del sess, tix
+    del last, last_idx  # the last timed step's engine and index
+
+    # Engines still referenced by earlier legs' objects (indexes, sessions in
+    # reference cycles) count as live on the device, and an engine that is not
+    # alone drops programmatic dependent launch (run_batches: multi_inline):
+    # free them before each leg so its number does not depend on GC timing.
+    gc.collect()
 
     # C4 shape on this GPU: several stream engines ingesting concurrently
     # ("the 1/2/4-GPU points of C4 run 8/4/2 engines per GPU"),
@@ -612,6 +620,7 @@ def main():
                          "ranks"}
         del datas
 
+    gc.collect()  # see above: no leftover engine may turn the C3 engine's PDL off
     # C3 shape (BASELINE configs[2]: M = 100 k, T = 5 -- every object seeds,
     # the live set saturates at 100 k and every batch evicts) on a bounded
     # prefix, inputs resident; parity of this path: tests/test_gpu_seeds.py
